@@ -1,0 +1,243 @@
+/*
+ * vmfa_b200.h — C-ABI of the B200-native v-MFA hot path (libvmfa_b200.so).
+ *
+ * This is the drop-in boundary for the reference's public C++ API in
+ * /root/reference/proj/include/vmfa/ (SURVEY.md §8(b)). The reference is a
+ * C++20 library with Eigen types in its signatures; this ABI carries the same
+ * data as plain pointers + sizes in the reference's own memory layouts
+ * over an opaque device context, so the C++ façade in
+ * include/vmfa_b200.hpp (reference names and semantics) and any FFI
+ * (ctypes/cgo/JNI) can bind it. No torch or CUDA types appear here; streams
+ * are passed as void*.
+ *
+ * Layouts (identical to the reference's):
+ *   X       N x D float32 row-major                        (dataset.hpp:13-14)
+ *   pi      C float64                                       (model.hpp:25)
+ *   mu      C x D float64 row-major                         (model.hpp:26)
+ *   lambda  C blocks, each D x H column-major (d,h) at h*D+d (model.hpp:27)
+ *   dnoise  C x D float64 row-major (Psi, variances)        (model.hpp:28)
+ *   K       N x C' int32 row-major, rows sorted ascending   (model.hpp:90-103)
+ *   g       C x G int32 row-major, rows sorted, -1 padded, plus g_count[C]
+ *                                                           (estep.hpp:22)
+ *   labels  N int32                                         (estep.hpp:24)
+ *   retained: count[N], idx[N*stride] (-1 pad), lj[N*stride] float64 with
+ *            stride = min(C'*G+1, C)                        (estep.hpp:48-70)
+ *   resp    N x C' float64, aligned with K rows             (estep.hpp:74)
+ *   caches: U C x (D x H col-major), Lmat/Sigma_z C x (H x H col-major),
+ *           V C x (H x D col-major), inv_dnoise C x D, logdet C, log_pi C
+ *                                                           (model.hpp:37-45)
+ *   stats:  Nc C, Y C x (D x (H+1) col-major), E C x ((H+1)^2 col-major),
+ *           sq_sum C x D                                    (mstep.hpp:14-22)
+ *
+ * Error model: every entry returns a vmfa_status; codes map 1:1 onto the
+ * reference's exception types (errors.hpp:9-62) plus std::invalid_argument.
+ * vmfa_last_error() returns a thread-local message for the last failure.
+ * Calls are stream-ordered on the context's stream and synchronous unless the
+ * name ends in _async; results returned through host pointers are complete on
+ * return.
+ */
+#ifndef VMFA_B200_H_
+#define VMFA_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VMFA_ABI_VERSION 1
+
+typedef enum vmfa_status {
+  VMFA_OK = 0,
+  VMFA_ERR_INVALID_ARGUMENT = 1,       /* std::invalid_argument            */
+  VMFA_ERR_CHOLESKY_FAILURE = 2,       /* vmfa::CholeskyFailure errors.hpp:16 */
+  VMFA_ERR_EMPTY_KSET = 3,             /* vmfa::EmptyKSet        errors.hpp:21 */
+  VMFA_ERR_INSUFFICIENT_CANDIDATES = 4,/* vmfa::InsufficientCandidates :26 */
+  VMFA_ERR_SINGULAR_EC = 5,            /* vmfa::SingularEc       errors.hpp:31 */
+  VMFA_ERR_MAX_ITER_EXCEEDED = 6,      /* vmfa::MaxIterExceeded  errors.hpp:36 */
+  VMFA_ERR_TARGET_UNREACHABLE = 7,     /* vmfa::TargetUnreachable errors.hpp:41 */
+  VMFA_ERR_DEGENERATE_DATA = 8,        /* vmfa::DegenerateData   errors.hpp:46 */
+  VMFA_ERR_BAD_MAGIC = 9,              /* vmfa::BadMagic         errors.hpp:51 */
+  VMFA_ERR_TRUNCATED_FILE = 10,        /* vmfa::TruncatedFile    errors.hpp:56 */
+  VMFA_ERR_UNSUPPORTED_VERSION = 11,   /* vmfa::UnsupportedVersion errors.hpp:61 */
+  VMFA_ERR_CUDA = 100,                 /* CUDA runtime failure (no reference twin) */
+  VMFA_ERR_NO_DEVICE = 101,            /* no usable sm_100 device          */
+  VMFA_ERR_UNSUPPORTED = 102           /* shape/feature outside this build */
+} vmfa_status;
+
+typedef enum vmfa_distance_mode {
+  VMFA_DIST_KL = 0,     /* DistanceMode::kl     estep.hpp:12 */
+  VMFA_DIST_EUCLID = 1  /* DistanceMode::euclid estep.hpp:12 */
+} vmfa_distance_mode;
+
+typedef struct vmfa_ctx vmfa_ctx;
+
+/* ------------------------------------------------------------------ misc */
+int vmfa_abi_version(void);
+const char* vmfa_last_error(void);
+/* 1 if a CUDA device of compute capability 10.x is visible, else 0. */
+int vmfa_device_available(void);
+
+/* ------------------------------------------------------------------ context
+ * A context owns one GPU's shard of the data (rows [n_offset, n_offset+n_local)
+ * of an n_total-row dataset), replicated parameters and caches, the variational
+ * state of its rows, and all scratch. The global row index n_offset+n keys the
+ * per-point random extra candidate (rng.hpp:91-98, estep.cpp:259-260), so a
+ * sharded run draws exactly the candidates of the unsharded one.
+ * stream: a cudaStream_t (NULL = create a private non-blocking stream).    */
+int vmfa_ctx_create(vmfa_ctx** out, int device, int C, int D, int H, int Cprime, int G,
+                    int64_t n_local, int64_t n_offset, int64_t n_total, void* stream);
+int vmfa_ctx_destroy(vmfa_ctx* ctx);
+/* Device bytes held by the context (data + state + params + scratch). */
+int vmfa_ctx_device_bytes(const vmfa_ctx* ctx, size_t* bytes);
+
+/* ------------------------------------------------------------------ data
+ * Dataset rows (dataset.hpp:11-35). rows may be a sub-range of the shard:
+ * local rows [row_begin, row_begin+rows). Host memory may be pageable or
+ * pinned.                                                                   */
+int vmfa_upload_data(vmfa_ctx* ctx, const float* X, int64_t row_begin, int64_t rows);
+/* Variance floor max(1e-8, 1e-6 var_d) (dataset.cpp:37-39), computed by the
+ * caller over ALL n_total rows (global).                  */
+int vmfa_set_floor(vmfa_ctx* ctx, const double* floor);
+
+/* ------------------------------------------------------------------ params / caches */
+/* MfaParams (model.hpp:19-32). Upload also runs precompute_all.            */
+int vmfa_upload_params(vmfa_ctx* ctx, const double* pi, const double* mu, const double* lambda,
+                       const double* dnoise);
+int vmfa_download_params(vmfa_ctx* ctx, double* pi, double* mu, double* lambda, double* dnoise);
+/* precompute_all (model.cpp:75-79) on the device. On CholeskyFailure the
+ * failing component index is written to *failed (may be NULL).             */
+int vmfa_precompute(vmfa_ctx* ctx, int* failed);
+/* ComponentCache for all C components (model.hpp:37-45); any pointer may be
+ * NULL to skip that field.                                                  */
+int vmfa_download_caches(vmfa_ctx* ctx, double* U, double* Lmat, double* V, double* Sigma_z,
+                         double* inv_dnoise, double* logdet, double* log_pi);
+
+/* ------------------------------------------------------------------ variational state */
+/* VarState (estep.hpp:17-29): K rows (sorted), g rows (sorted, -1 padded).  */
+int vmfa_upload_state(vmfa_ctx* ctx, const int32_t* K, const int32_t* g, const int32_t* g_count);
+int vmfa_download_state(vmfa_ctx* ctx, int32_t* K, int32_t* g, int32_t* g_count, int32_t* labels);
+
+/* ------------------------------------------------------------------ the hot path */
+/* variational_e_step (estep.hpp:125-130, estep.cpp:230-336): blocks 1-4 at the
+ * current parameters. Updates K, labels, partition and g in place; returns the
+ * block-4 free energy (sum over this context's rows) and the joint count
+ * sum_n |S(n)| of this context's rows. On a multi-context (multi-GPU) run use
+ * the phase API below instead so g is computed from all ranks' rows.        */
+int vmfa_estep(vmfa_ctx* ctx, uint64_t seed, uint64_t iteration, int mode, double* free_energy,
+               uint64_t* joints);
+/* EStepResult pieces for parity (estep.hpp:72-78): retained joints (stride =
+ * min(C'G+1, C)) and responsibilities of the last E-step. NULL skips.       */
+int vmfa_download_estep(vmfa_ctx* ctx, int32_t* count, int32_t* idx, double* lj, double* resp);
+/* Block-3 accumulator of the last E-step (DistanceAccumulator, estep.hpp:34-44)
+ * as (c, ctilde, sum, count) rows in (c, ctilde) ascending order. Pass cap=0
+ * to query the row count in *n_rows.                                        */
+int vmfa_download_distances(vmfa_ctx* ctx, int64_t cap, int32_t* c, int32_t* ct, double* sum,
+                            int64_t* count, int64_t* n_rows);
+
+/* accumulate_suffstats (mstep.hpp:27-31) with the pre-update caches and the
+ * last E-step's K/resp, into the context's statistics buffer.               */
+int vmfa_accumulate_suffstats(vmfa_ctx* ctx);
+int vmfa_download_suffstats(vmfa_ctx* ctx, double* Nc, double* Y, double* E, double* sq_sum);
+int vmfa_upload_suffstats(vmfa_ctx* ctx, const double* Nc, const double* Y, const double* E,
+                          const double* sq_sum);
+/* update_params (mstep.hpp:39-41, mstep.cpp:103-162) from the statistics
+ * buffer, then precompute_all. *failed receives the failing component.      */
+int vmfa_update_params(vmfa_ctx* ctx, int* failed);
+/* truncated_free_energy (model.hpp:116-119) over this context's rows under
+ * the current parameters and K.                                             */
+int vmfa_truncated_free_energy(vmfa_ctx* ctx, double* free_energy);
+/* exact_log_likelihood (model.hpp:108-111) over this context's rows.        */
+int vmfa_exact_log_likelihood(vmfa_ctx* ctx, double* log_likelihood);
+
+/* One main-loop iteration of train_vmfa (trainer.cpp:149-160): E-step,
+ * statistics, update, precompute, post-M-step truncated free energy.
+ * Single-context only (use the phase API for multi-GPU).                    */
+typedef struct vmfa_iter_report {
+  double free_energy_estep; /* block-4 F(K_new, Theta_old), estep.cpp:316-334 */
+  double free_energy;       /* F(K_new, Theta_new), trainer.cpp:158-160      */
+  uint64_t joints;          /* sum_n |S(n)|                                  */
+  int32_t empty_components; /* pi == 0 count, trainer.cpp:27-29              */
+  int32_t failed_component; /* component of a CholeskyFailure/SingularEc     */
+} vmfa_iter_report;
+int vmfa_iterate(vmfa_ctx* ctx, uint64_t seed, uint64_t iteration, int mode,
+                 vmfa_iter_report* report);
+
+/* ------------------------------------------------------------------ multi-GPU phase API
+ * Data-parallel over points: each rank runs the phases on its
+ * shard and sums the exchange buffers across ranks between phases (NCCL
+ * all-reduce over NVLink; the caller owns the communicator). Exchange buffers
+ * are device pointers in the context:
+ *   VMFA_XCHG_COOC   int64 buffer: dense C x C co-occurrence accumulator
+ *                    (count, fixed-point sum hi, lo) — exact integer sums, so
+ *                    g is bit-identical for every rank count.
+ *   VMFA_XCHG_STATS  float64 buffer: [Nc | E | Y | sq_sum] packed.
+ *   VMFA_XCHG_SCALARS float64 buffer: [F_estep, joints, F_post] partials.
+ * Sequence per main iteration:
+ *   vmfa_phase_estep_local -> allreduce(COOC) -> vmfa_phase_estep_finish ->
+ *   vmfa_phase_stats_local -> allreduce(STATS) -> vmfa_phase_update ->
+ *   vmfa_phase_free_energy_local -> allreduce(SCALARS).                    */
+typedef enum vmfa_exchange { VMFA_XCHG_COOC = 0, VMFA_XCHG_STATS = 1, VMFA_XCHG_SCALARS = 2 } vmfa_exchange;
+typedef enum vmfa_dtype { VMFA_DT_INT64 = 0, VMFA_DT_FLOAT64 = 1 } vmfa_dtype;
+int vmfa_exchange_buffer(vmfa_ctx* ctx, int which, void** device_ptr, size_t* count, int* dtype);
+int vmfa_phase_estep_local(vmfa_ctx* ctx, uint64_t seed, uint64_t iteration, int mode);
+int vmfa_phase_estep_finish(vmfa_ctx* ctx);
+int vmfa_phase_stats_local(vmfa_ctx* ctx);
+int vmfa_phase_update(vmfa_ctx* ctx, int* failed);
+int vmfa_phase_free_energy_local(vmfa_ctx* ctx);
+/* Reads the (reduced) scalars buffer: F_estep, joints, F_post.             */
+int vmfa_phase_scalars(vmfa_ctx* ctx, double* free_energy_estep, uint64_t* joints,
+                       double* free_energy);
+
+/* ------------------------------------------------------------------ timing / profiling */
+/* Records CUDA events around the scoring kernels of subsequent calls;
+ * vmfa_kernel_times returns accumulated milliseconds and launch counts per
+ * kernel family since the last reset (names in vmfa_kernel_name).          */
+int vmfa_profile_enable(vmfa_ctx* ctx, int enable);
+int vmfa_kernel_times(vmfa_ctx* ctx, int max, double* ms, int64_t* launches, int64_t* units,
+                      int* n);
+const char* vmfa_kernel_name(int i);
+/* Stream of the context (a cudaStream_t) for callers that order their own
+ * work (e.g. NCCL) against it.                                              */
+void* vmfa_ctx_stream(vmfa_ctx* ctx);
+int vmfa_synchronize(vmfa_ctx* ctx);
+
+/* ------------------------------------------------------------------ host-side helpers
+ * Host-only (no GPU needed): synthetic data for BASELINE.json's configs and
+ * the reference's initialisation (trainer.cpp:32-47, 107-109), restated
+ * with identical draw sequences.                                            */
+typedef struct vmfa_synth_spec {
+  int kind;            /* 0: Gaussian MFA (configs 1,2,4); 1: image-like fields (3,5) */
+  int64_t n_total;     /* N                                                   */
+  int D;               /* data dimension                                      */
+  int C_true;          /* ground-truth components                             */
+  int H_true;          /* ground-truth latent dimension                        */
+  int dirichlet;       /* 1: pi ~ Dirichlet(1); 0: equiprobable               */
+  double mu_std;       /* kind 0: mu ~ N(0, mu_std^2 I)                       */
+  double lam_std;      /* kind 0: Lambda ~ N(0, lam_std^2); kind 1: field std  */
+  double psi_lo, psi_hi; /* kind 0: Psi ~ U[psi_lo, psi_hi]                   */
+  double noise_std;    /* kind 1: isotropic noise std                         */
+  int img_w, img_h, img_c; /* kind 1: field geometry (D = w*h*c)             */
+  double blur_sigma;   /* kind 1: Gaussian blur sigma in pixels               */
+  uint64_t data_seed;
+} vmfa_synth_spec;
+/* Fills rows [row_begin, row_end) of X (row-major, (row_end-row_begin) x D);
+ * labels (nullable) receives the true component per row. Each row draws from
+ * its own keyed stream, so shards can be generated independently.          */
+int vmfa_gen_synthetic(const vmfa_synth_spec* spec, int64_t row_begin, int64_t row_end,
+                       float* X, int32_t* labels, int threads);
+
+/* Initialisation (random-points seeding): floor (D), params, K (N x C'),
+ * g (C x G) + g_count. loading_init 0 = reference U[0, scale) (seeding.cpp:
+ * 175-176); 1 = BASELINE's N(0, scale^2) from the same stream. The caller's X
+ * is the FULL dataset (N x D).                                              */
+int vmfa_host_initialize(const float* X, int64_t N, int D, int C, int H, int Cprime, int G,
+                         uint64_t seed, double scale, int loading_init, double* floor,
+                         double* pi, double* mu, double* lambda, double* dnoise, int32_t* K,
+                         int32_t* g, int32_t* g_count, int64_t* seeds);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VMFA_B200_H_ */

@@ -1,0 +1,1058 @@
+// vmfa_capi.cu — device context and the C-ABI of libvmfa_b200.so
+// (include/vmfa_b200.h). One context = one GPU's shard of the rows, the
+// replicated parameters/caches, the shard's variational state and all scratch.
+// Every phase is stream-ordered; host synchronisation happens only where a
+// result is returned through a host pointer.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "vmfa_b200.h"
+#include "vmfa_internal.hpp"
+#include "vmfa_kernels.cuh"
+
+namespace vmfa_b200 {
+
+namespace {
+thread_local std::string g_err;
+}
+void set_error_text(const std::string& s) { g_err = s; }
+const std::string& error_text() { return g_err; }
+
+#define CU(x)                                                                                    \
+  do {                                                                                           \
+    cudaError_t e_ = (x);                                                                        \
+    if (e_ != cudaSuccess)                                                                       \
+      return fail(VMFA_ERR_CUDA, "%s:%d %s -> %s", __FILE__, __LINE__, #x, cudaGetErrorString(e_)); \
+  } while (0)
+#define TRY(x)                   \
+  do {                           \
+    int r_ = (x);                \
+    if (r_ != VMFA_OK) return r_; \
+  } while (0)
+
+enum KernelFamily : int {
+  kFamScoreAnchor = 0,
+  kFamScoreExtra,
+  kFamSelect,
+  kFamGupdate,
+  kFamStats,
+  kFamUpdate,
+  kFamPrecompute,
+  kFamScoreTruncF,
+  kFamSort,
+  kFamOther,
+  kNumFamilies
+};
+const char* const kFamilyNames[kNumFamilies] = {
+    "score_anchor", "score_extra", "select", "gupdate", "stats",
+    "update", "precompute", "score_truncF", "csr_sort", "other"};
+
+__global__ void k_pack_scalar_u64(const unsigned long long* src, double* dst) { *dst = static_cast<double>(*src); }
+__global__ void k_add_f64(const double* src, double* dst) { *dst = *src; }
+
+}  // namespace vmfa_b200
+
+using namespace vmfa_b200;
+
+struct vmfa_ctx {
+  int device = 0;
+  Dims dm{};
+  ScoreLayout L{};
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  std::vector<void*> allocs;
+  size_t bytes = 0;
+
+  // data
+  float* X = nullptr;
+  double* floor = nullptr;
+  // params: two sets (current / next)
+  double *pi = nullptr, *mu = nullptr, *lam = nullptr, *psi = nullptr;
+  double *pi2 = nullptr, *mu2 = nullptr, *lam2 = nullptr, *psi2 = nullptr;
+  // caches
+  double *Lmat = nullptr, *R = nullptr, *Sz = nullptr, *logdet = nullptr, *logpi = nullptr,
+         *kconst = nullptr;
+  float *P = nullptr, *V32 = nullptr, *mu32 = nullptr;
+  // state
+  int *K = nullptr, *g = nullptr, *gcnt = nullptr, *g_new = nullptr, *gcnt_new = nullptr,
+      *labels = nullptr;
+  float* lablj = nullptr;
+  // E-step scratch
+  float* LJ = nullptr;      // N x SL
+  float* LJK = nullptr;     // N x Cp
+  int* rx = nullptr;
+  unsigned* rkey = nullptr;
+  int *ret_cnt = nullptr, *ret_idx = nullptr;
+  float* ret_lj = nullptr;
+  double *resp = nullptr, *lse = nullptr;
+  // CSR / sort scratch
+  unsigned *keys = nullptr, *keys_alt = nullptr;
+  int* vals = nullptr;
+  int *kinv_off = nullptr, *kinv_ent = nullptr, *kinv_items = nullptr;
+  int *ex_off = nullptr, *ex_ent = nullptr, *ex_items = nullptr;
+  int *part_off = nullptr, *part_ent = nullptr;
+  int *cnt = nullptr, *chunks = nullptr;
+  void* cub_tmp = nullptr;
+  size_t cub_bytes = 0;
+  // block-3 scratch
+  int gupd_grid = 0;
+  long long *gt_cnt = nullptr, *gt_hi = nullptr, *gt_lo = nullptr;
+  long long* xc = nullptr;  // multi-rank exchange (lazy)
+  // stats: packed [Nc | E | Y | sq]
+  double* stats = nullptr;
+  size_t stats_len = 0;
+  double *Nc = nullptr, *E = nullptr, *Y = nullptr, *sq = nullptr;
+  // reductions / scalars / status
+  double* partials = nullptr;
+  double* scal = nullptr;   // [F_estep, joints, F_post, spare]
+  unsigned long long* u64tmp = nullptr;
+  int* st_select = nullptr;
+  unsigned long long* st_model = nullptr;
+  int* n_empty = nullptr;
+  bool kinv_for_current_K = false;
+  bool have_estep = false;
+  // dumps (parity only)
+  bool dump = false;
+  int *dump_c = nullptr, *dump_ct = nullptr;
+  long long *dump_cnt = nullptr, *dump_hi = nullptr, *dump_lo = nullptr;
+  unsigned long long* dump_n = nullptr;
+  long long dump_cap = 0;
+  // profiling
+  bool profile = false;
+  struct Ev {
+    int fam;
+    cudaEvent_t a, b;
+    int64_t units;
+  };
+  std::vector<Ev> pending;
+  std::vector<cudaEvent_t> ev_pool;
+  double fam_ms[kNumFamilies] = {};
+  int64_t fam_launches[kNumFamilies] = {};
+  int64_t fam_units[kNumFamilies] = {};
+  int64_t launches = 0;
+
+  template <class T>
+  int alloc(T*& p, size_t n) {
+    void* q = nullptr;
+    const size_t b = std::max<size_t>(n, 1) * sizeof(T);
+    cudaError_t e = cudaMalloc(&q, b);
+    if (e != cudaSuccess)
+      return fail(VMFA_ERR_CUDA, "cudaMalloc(%zu bytes) failed: %s", b, cudaGetErrorString(e));
+    allocs.push_back(q);
+    bytes += b;
+    p = static_cast<T*>(q);
+    return VMFA_OK;
+  }
+  cudaEvent_t ev() {
+    if (!ev_pool.empty()) {
+      cudaEvent_t e = ev_pool.back();
+      ev_pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+  }
+  // family-scoped timing: begin() returns a token, end() records
+  int begin(int fam, int64_t units) {
+    fam_launches[fam] += 1;
+    fam_units[fam] += units;
+    if (!profile) return -1;
+    Ev x{fam, ev(), ev(), units};
+    cudaEventRecord(x.a, stream);
+    pending.push_back(x);
+    return static_cast<int>(pending.size()) - 1;
+  }
+  void end(int tok) {
+    if (tok >= 0) cudaEventRecord(pending[tok].b, stream);
+  }
+  void collect() {
+    if (pending.empty()) return;
+    cudaStreamSynchronize(stream);
+    for (auto& x : pending) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, x.a, x.b);
+      fam_ms[x.fam] += ms;
+      ev_pool.push_back(x.a);
+      ev_pool.push_back(x.b);
+    }
+    pending.clear();
+  }
+};
+
+namespace vmfa_b200 {
+namespace {
+
+int bits_for(unsigned v) {
+  int b = 1;
+  while ((1ull << b) <= v) ++b;
+  return b;
+}
+
+// Stable CSR of `n` keys in [0, C] (C = dropped sentinel) -> off (C+1), ent
+// (indices 0..n-1 ordered by key, stable) and per-key chunk offsets for the
+// persistent scoring kernels.
+int csr_by_key(vmfa_ctx* x, const unsigned* keys, int64_t n, int* off, int* ent, int* items,
+               int rows_per_item) {
+  const int C = x->dm.C;
+  cudaStream_t s = x->stream;
+  const int tok = x->begin(kFamSort, n);
+  CU(launch_iota(x->vals, n, s));
+  size_t tb = x->cub_bytes;
+  CU(cub::DeviceRadixSort::SortPairs(x->cub_tmp, tb, keys, x->keys_alt, x->vals, ent,
+                                     static_cast<int>(n), 0, bits_for(static_cast<unsigned>(C)), s));
+  CU(cudaMemsetAsync(x->cnt, 0, sizeof(int) * (C + 1), s));
+  CU(launch_hist(keys, n, C, x->cnt, s));
+  tb = x->cub_bytes;
+  CU(cub::DeviceScan::ExclusiveSum(x->cub_tmp, tb, x->cnt, off, C + 1, s));
+  if (items) {
+    CU(launch_chunks(x->cnt, C, rows_per_item, x->chunks, s));
+    tb = x->cub_bytes;
+    CU(cub::DeviceScan::ExclusiveSum(x->cub_tmp, tb, x->chunks, items, C + 1, s));
+  }
+  x->end(tok);
+  return VMFA_OK;
+}
+
+int score_grid() { return sm_count() * 8; }
+
+ScoreArgs score_args(vmfa_ctx* x) {
+  ScoreArgs a{};
+  a.dm = x->dm;
+  a.L = x->L;
+  a.X = x->X;
+  a.P = x->P;
+  a.kconst = x->kconst;
+  a.g = x->g;
+  a.gcnt = x->gcnt;
+  return a;
+}
+
+int run_precompute(vmfa_ctx* x, int* failed) {
+  cudaStream_t s = x->stream;
+  CU(cudaMemsetAsync(x->st_model, 0xff, sizeof(unsigned long long), s));
+  PrecompArgs a{};
+  a.dm = x->dm;
+  a.L = x->L;
+  a.pi = x->pi;
+  a.mu = x->mu;
+  a.lam = x->lam;
+  a.psi = x->psi;
+  a.Lmat = x->Lmat;
+  a.R = x->R;
+  a.Sz = x->Sz;
+  a.logdet = x->logdet;
+  a.logpi = x->logpi;
+  a.kconst = x->kconst;
+  a.P = x->P;
+  a.V32 = x->V32;
+  a.mu32 = x->mu32;
+  a.status = x->st_model;
+  const int tok = x->begin(kFamPrecompute, x->dm.C);
+  CU(launch_precompute(a, s));
+  x->end(tok);
+  unsigned long long st = 0;
+  CU(cudaMemcpyAsync(&st, x->st_model, sizeof st, cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  if (st != ~0ull) {
+    const int comp = static_cast<int>(st >> 8), code = static_cast<int>(st & 0xff);
+    if (failed) *failed = comp;
+    return fail(code, "L_c not positive definite for component %d", comp);
+  }
+  return VMFA_OK;
+}
+
+// E-step blocks 1, 2, 4 and the local part of block 3.
+int estep_local(vmfa_ctx* x, uint64_t seed, uint64_t it, int mode, bool exchange) {
+  const Dims& dm = x->dm;
+  cudaStream_t s = x->stream;
+  CU(cudaMemsetAsync(x->st_select, 0, sizeof(int), s));
+  // anchor blocks: inverted K (stable counting sort by component)
+  CU(launch_keys_from_i32(x->K, x->keys, dm.N * dm.Cp, s));
+  TRY(csr_by_key(x, x->keys, dm.N * dm.Cp, x->kinv_off, x->kinv_ent, x->kinv_items, kScoreRows));
+  // extras not already covered by U g_a
+  {
+    const int tok = x->begin(kFamOther, dm.N);
+    CU(launch_extra(dm, x->K, x->g, x->gcnt, seed, it, x->rx, x->rkey, s));
+    x->end(tok);
+  }
+  TRY(csr_by_key(x, x->rkey, dm.N, x->ex_off, x->ex_ent, x->ex_items, kScoreRows));
+  // block 1: scoring
+  {
+    ScoreArgs a = score_args(x);
+    a.off = x->kinv_off;
+    a.ent = x->kinv_ent;
+    a.itemoff = x->kinv_items;
+    a.out = x->LJ;
+    const int tok = x->begin(kFamScoreAnchor, dm.N * dm.Cp);
+    CU(launch_score(kModeAnchor, a, score_grid(), s));
+    x->end(tok);
+    a.off = x->ex_off;
+    a.ent = x->ex_ent;
+    a.itemoff = x->ex_items;
+    const int tok2 = x->begin(kFamScoreExtra, dm.N);
+    CU(launch_score(kModeExtra, a, score_grid(), s));
+    x->end(tok2);
+  }
+  // selection, labels, block 4
+  {
+    SelectArgs a{};
+    a.dm = dm;
+    a.K = x->K;
+    a.g = x->g;
+    a.gcnt = x->gcnt;
+    a.rx = x->rx;
+    a.LJ = x->LJ;
+    a.labels = x->labels;
+    a.lablj = x->lablj;
+    a.resp = x->resp;
+    a.ret_cnt = x->ret_cnt;
+    a.ret_idx = x->ret_idx;
+    a.ret_lj = x->ret_lj;
+    a.lse = x->lse;
+    a.status = x->st_select;
+    const int tok = x->begin(kFamSelect, dm.N);
+    CU(launch_select(a, s));
+    x->end(tok);
+  }
+  x->kinv_for_current_K = false;
+  // block 2: partition by label (stable => ascending n per component)
+  CU(launch_keys_from_i32(x->labels, x->keys, dm.N, s));
+  TRY(csr_by_key(x, x->keys, dm.N, x->part_off, x->part_ent, nullptr, 1));
+  // block 3 (local accumulation; selection unless exchanging)
+  CU(launch_logpi(x->pi, dm.C, x->logpi, s));
+  {
+    GupdArgs a{};
+    a.dm = dm;
+    a.mode = mode;
+    a.part_off = x->part_off;
+    a.part_ent = x->part_ent;
+    a.ret_cnt = x->ret_cnt;
+    a.ret_idx = x->ret_idx;
+    a.ret_lj = x->ret_lj;
+    a.lablj = x->lablj;
+    a.logpi = x->logpi;
+    a.g_new = x->g_new;
+    a.gcnt_new = x->gcnt_new;
+    a.gt_cnt = x->gt_cnt;
+    a.gt_hi = x->gt_hi;
+    a.gt_lo = x->gt_lo;
+    a.exchange = exchange ? 1 : 0;
+    a.xc = x->xc;
+    if (exchange) CU(cudaMemsetAsync(x->xc, 0, sizeof(long long) * 3 * (size_t)dm.C * dm.C, s));
+    a.dump = x->dump ? 1 : 0;
+    if (x->dump) {
+      CU(cudaMemsetAsync(x->dump_n, 0, sizeof(unsigned long long), s));
+      a.dump_c = x->dump_c;
+      a.dump_ct = x->dump_ct;
+      a.dump_cnt = x->dump_cnt;
+      a.dump_hi = x->dump_hi;
+      a.dump_lo = x->dump_lo;
+      a.dump_n = x->dump_n;
+      a.dump_cap = x->dump_cap;
+    }
+    const int tok = x->begin(kFamGupdate, dm.N);
+    CU(launch_gupdate(a, x->gupd_grid, s));
+    x->end(tok);
+  }
+  // scalars: F_estep = sum lse, joints = sum ret_cnt
+  CU(launch_sum_f64(x->lse, dm.N, x->partials, x->scal + 0, s));
+  CU(launch_sum_i32(x->ret_cnt, dm.N, x->u64tmp, s));
+  k_pack_scalar_u64<<<1, 1, 0, s>>>(x->u64tmp, x->scal + 1);
+  CU(cudaGetLastError());
+  x->have_estep = true;
+  return VMFA_OK;
+}
+
+int estep_finish(vmfa_ctx* x, bool exchange) {
+  const Dims& dm = x->dm;
+  cudaStream_t s = x->stream;
+  if (exchange) {
+    const int tok = x->begin(kFamGupdate, dm.C);
+    CU(launch_gselect_dense(dm, x->xc, x->g_new, x->gcnt_new, s));
+    x->end(tok);
+  }
+  std::swap(x->g, x->g_new);
+  std::swap(x->gcnt, x->gcnt_new);
+  int flag = 0;
+  CU(cudaMemcpyAsync(&flag, x->st_select, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  if (flag) return fail(VMFA_ERR_INSUFFICIENT_CANDIDATES, "search space smaller than C'");
+  return VMFA_OK;
+}
+
+int ensure_kinv_current(vmfa_ctx* x) {
+  if (x->kinv_for_current_K) return VMFA_OK;
+  const Dims& dm = x->dm;
+  CU(launch_keys_from_i32(x->K, x->keys, dm.N * dm.Cp, x->stream));
+  TRY(csr_by_key(x, x->keys, dm.N * dm.Cp, x->kinv_off, x->kinv_ent, x->kinv_items, kScoreRows));
+  x->kinv_for_current_K = true;
+  return VMFA_OK;
+}
+
+int stats_local(vmfa_ctx* x) {
+  if (!x->have_estep) return fail(VMFA_ERR_INVALID_ARGUMENT, "accumulate_suffstats needs a preceding E-step (responsibilities)");
+  TRY(ensure_kinv_current(x));
+  StatsArgs a{};
+  a.dm = x->dm;
+  a.X = x->X;
+  a.resp = x->resp;
+  a.off = x->kinv_off;
+  a.ent = x->kinv_ent;
+  a.V32 = x->V32;
+  a.mu32 = x->mu32;
+  a.Sz = x->Sz;
+  a.Nc = x->Nc;
+  a.E = x->E;
+  a.Y = x->Y;
+  a.sq = x->sq;
+  const int tok = x->begin(kFamStats, x->dm.N * x->dm.Cp);
+  CU(launch_stats(a, x->stream));
+  x->end(tok);
+  return VMFA_OK;
+}
+
+int update_and_precompute(vmfa_ctx* x, int* failed) {
+  const Dims& dm = x->dm;
+  cudaStream_t s = x->stream;
+  CU(cudaMemsetAsync(x->st_model, 0xff, sizeof(unsigned long long), s));
+  UpdateArgs a{};
+  a.dm = dm;
+  a.Nc = x->Nc;
+  a.E = x->E;
+  a.Y = x->Y;
+  a.sq = x->sq;
+  a.floor = x->floor;
+  a.mu_prev = x->mu;
+  a.lam_prev = x->lam;
+  a.psi_prev = x->psi;
+  a.pi = x->pi2;
+  a.mu = x->mu2;
+  a.lam = x->lam2;
+  a.psi = x->psi2;
+  a.status = x->st_model;
+  const int tok = x->begin(kFamUpdate, dm.C);
+  CU(launch_update(a, s));
+  CU(launch_renorm(dm, x->pi2, x->st_model, s));
+  x->end(tok);
+  unsigned long long st = 0;
+  CU(cudaMemcpyAsync(&st, x->st_model, sizeof st, cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  if (st != ~0ull) {
+    const int comp = static_cast<int>(st >> 8), code = static_cast<int>(st & 0xff);
+    if (failed) *failed = comp == 0xffffff ? -1 : comp;
+    return fail(code, comp == 0xffffff ? "all components empty after update"
+                                       : "E_c singular for component %d", comp);
+  }
+  std::swap(x->pi, x->pi2);
+  std::swap(x->mu, x->mu2);
+  std::swap(x->lam, x->lam2);
+  std::swap(x->psi, x->psi2);
+  return run_precompute(x, failed);
+}
+
+int free_energy_local(vmfa_ctx* x) {
+  const Dims& dm = x->dm;
+  cudaStream_t s = x->stream;
+  TRY(ensure_kinv_current(x));
+  ScoreArgs a = score_args(x);
+  a.off = x->kinv_off;
+  a.ent = x->kinv_ent;
+  a.itemoff = x->kinv_items;
+  a.out = x->LJK;
+  const int tok = x->begin(kFamScoreTruncF, dm.N * dm.Cp);
+  CU(launch_score(kModeTruncF, a, score_grid(), s));
+  CU(launch_lse_rows(x->LJK, dm.N, dm.Cp, x->lse, s));
+  x->end(tok);
+  CU(launch_sum_f64(x->lse, dm.N, x->partials, x->scal + 2, s));
+  return VMFA_OK;
+}
+
+int read_scalars(vmfa_ctx* x, double out[4]) {
+  CU(cudaMemcpyAsync(out, x->scal, 4 * sizeof(double), cudaMemcpyDeviceToHost, x->stream));
+  CU(cudaStreamSynchronize(x->stream));
+  return VMFA_OK;
+}
+
+int check_ctx(const vmfa_ctx* x) {
+  if (!x) return fail(VMFA_ERR_INVALID_ARGUMENT, "null context");
+  return VMFA_OK;
+}
+
+}  // namespace
+}  // namespace vmfa_b200
+
+// ============================================================================ C-ABI
+extern "C" {
+
+int vmfa_abi_version(void) { return VMFA_ABI_VERSION; }
+const char* vmfa_last_error(void) { return error_text().c_str(); }
+
+int vmfa_device_available(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n < 1) {
+    cudaGetLastError();
+    return 0;
+  }
+  cudaDeviceProp p{};
+  if (cudaGetDeviceProperties(&p, 0) != cudaSuccess) return 0;
+  return p.major == 10 ? 1 : 0;
+}
+
+int vmfa_ctx_create(vmfa_ctx** out, int device, int C, int D, int H, int Cp, int G, int64_t n_local,
+                    int64_t n_offset, int64_t n_total, void* stream) {
+  if (!out) return fail(VMFA_ERR_INVALID_ARGUMENT, "out is null");
+  *out = nullptr;
+  if (C < 1 || D < 1 || H < 1 || H > D || Cp < 1 || Cp > C || G < 1 || G > C || n_local < 1 ||
+      n_offset < 0 || n_total < n_offset + n_local)
+    return fail(VMFA_ERR_INVALID_ARGUMENT, "invalid sizes (C=%d D=%d H=%d C'=%d G=%d N=%lld)", C, D, H, Cp, G,
+                static_cast<long long>(n_local));
+  if (H + 1 > 65) return fail(VMFA_ERR_UNSUPPORTED, "H > 64 not supported by this build");
+  if (Cp > 8 || Cp * G + 1 > 256) return fail(VMFA_ERR_UNSUPPORTED, "C' <= 8 and C'G+1 <= 256 required");
+  if (static_cast<size_t>(D) * kXsStride * sizeof(float) > 200 * 1024)
+    return fail(VMFA_ERR_UNSUPPORTED, "D > %zu not supported by the scoring tile", 200 * 1024 / (kXsStride * sizeof(float)));
+  if (n_local * Cp >= (int64_t{1} << 31)) return fail(VMFA_ERR_UNSUPPORTED, "shard too large (N*C' >= 2^31)");
+  if (!vmfa_device_available()) return fail(VMFA_ERR_NO_DEVICE, "no sm_100 CUDA device visible");
+  CU(cudaSetDevice(device));
+  auto* x = new vmfa_ctx();
+  x->device = device;
+  Dims& dm = x->dm;
+  dm.C = C, dm.D = D, dm.H = H, dm.Cp = Cp, dm.G = G;
+  dm.SL = Cp * G + 1;
+  dm.stride = static_cast<int>(std::min<int64_t>(static_cast<int64_t>(Cp) * G + 1, C));
+  dm.N = n_local, dm.n0 = n_offset, dm.Ntot = n_total;
+  x->L = score_layout(H);
+  if (stream) {
+    x->stream = static_cast<cudaStream_t>(stream);
+  } else {
+    if (cudaStreamCreateWithFlags(&x->stream, cudaStreamNonBlocking) != cudaSuccess) {
+      delete x;
+      return fail(VMFA_ERR_CUDA, "cudaStreamCreate failed");
+    }
+    x->own_stream = true;
+  }
+  const size_t N = static_cast<size_t>(n_local), Cs = static_cast<size_t>(C);
+  const size_t H1 = static_cast<size_t>(H) + 1;
+  int r = VMFA_OK;
+  auto A = [&](auto*& p, size_t n) {
+    if (r == VMFA_OK) r = x->alloc(p, n);
+  };
+  A(x->X, N * D);
+  A(x->floor, D);
+  for (double** p : {&x->pi, &x->pi2}) A(*p, Cs);
+  for (double** p : {&x->mu, &x->mu2, &x->psi, &x->psi2}) A(*p, Cs * D);
+  for (double** p : {&x->lam, &x->lam2}) A(*p, Cs * D * H);
+  A(x->Lmat, Cs * H * H);
+  A(x->R, Cs * H * H);
+  A(x->Sz, Cs * H * H);
+  A(x->logdet, Cs);
+  A(x->logpi, Cs);
+  A(x->kconst, Cs);
+  A(x->P, Cs * D * x->L.HP);
+  A(x->V32, Cs * D * H);
+  A(x->mu32, Cs * D);
+  A(x->K, N * Cp);
+  A(x->g, Cs * G);
+  A(x->gcnt, Cs);
+  A(x->g_new, Cs * G);
+  A(x->gcnt_new, Cs);
+  A(x->labels, N);
+  A(x->lablj, N);
+  A(x->LJ, N * dm.SL);
+  A(x->LJK, N * Cp);
+  A(x->rx, N);
+  A(x->rkey, N);
+  A(x->ret_cnt, N);
+  A(x->ret_idx, N * dm.stride);
+  A(x->ret_lj, N * dm.stride);
+  A(x->resp, N * Cp);
+  A(x->lse, N);
+  A(x->keys, N * Cp);
+  A(x->keys_alt, N * Cp);
+  A(x->vals, N * Cp);
+  A(x->kinv_off, Cs + 1);
+  A(x->kinv_ent, N * Cp);
+  A(x->kinv_items, Cs + 1);
+  A(x->ex_off, Cs + 1);
+  A(x->ex_ent, N);
+  A(x->ex_items, Cs + 1);
+  A(x->part_off, Cs + 1);
+  A(x->part_ent, N);
+  A(x->cnt, Cs + 1);
+  A(x->chunks, Cs + 1);
+  x->gupd_grid = static_cast<int>(std::min<int64_t>(C, sm_count() * 2));
+  A(x->gt_cnt, static_cast<size_t>(x->gupd_grid) * Cs);
+  A(x->gt_hi, static_cast<size_t>(x->gupd_grid) * Cs);
+  A(x->gt_lo, static_cast<size_t>(x->gupd_grid) * Cs);
+  x->stats_len = Cs + Cs * H1 * H1 + Cs * H1 * D + Cs * D;
+  A(x->stats, x->stats_len);
+  A(x->partials, 512);
+  A(x->scal, 4);
+  A(x->u64tmp, 1);
+  A(x->st_select, 1);
+  A(x->st_model, 1);
+  A(x->n_empty, 1);
+  if (r != VMFA_OK) {
+    vmfa_ctx_destroy(x);
+    return r;
+  }
+  x->Nc = x->stats;
+  x->E = x->Nc + Cs;
+  x->Y = x->E + Cs * H1 * H1;
+  x->sq = x->Y + Cs * H1 * D;
+  // cub temp storage: max over the sorts / scans we run
+  size_t b1 = 0, b2 = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, b1, x->keys, x->keys_alt, x->vals, x->kinv_ent,
+                                  static_cast<int>(N * Cp), 0, 32, x->stream);
+  cub::DeviceScan::ExclusiveSum(nullptr, b2, x->cnt, x->kinv_off, C + 1, x->stream);
+  x->cub_bytes = std::max(b1, b2) + 256;
+  void* tmp = nullptr;
+  if (cudaMalloc(&tmp, x->cub_bytes) != cudaSuccess) {
+    vmfa_ctx_destroy(x);
+    return fail(VMFA_ERR_CUDA, "cudaMalloc(cub temp) failed");
+  }
+  x->allocs.push_back(tmp);
+  x->bytes += x->cub_bytes;
+  x->cub_tmp = tmp;
+  cudaMemsetAsync(x->scal, 0, 4 * sizeof(double), x->stream);
+  cudaMemsetAsync(x->labels, 0, N * sizeof(int), x->stream);
+  if (cudaStreamSynchronize(x->stream) != cudaSuccess) {
+    vmfa_ctx_destroy(x);
+    return fail(VMFA_ERR_CUDA, "context initialisation failed");
+  }
+  *out = x;
+  return VMFA_OK;
+}
+
+int vmfa_ctx_destroy(vmfa_ctx* x) {
+  if (!x) return VMFA_OK;
+  cudaSetDevice(x->device);
+  if (x->stream) cudaStreamSynchronize(x->stream);
+  for (void* p : x->allocs) cudaFree(p);
+  for (auto& e : x->pending) {
+    cudaEventDestroy(e.a);
+    cudaEventDestroy(e.b);
+  }
+  for (auto e : x->ev_pool) cudaEventDestroy(e);
+  if (x->own_stream) cudaStreamDestroy(x->stream);
+  delete x;
+  return VMFA_OK;
+}
+
+int vmfa_ctx_device_bytes(const vmfa_ctx* x, size_t* bytes) {
+  TRY(check_ctx(x));
+  if (bytes) *bytes = x->bytes;
+  return VMFA_OK;
+}
+
+void* vmfa_ctx_stream(vmfa_ctx* x) { return x ? static_cast<void*>(x->stream) : nullptr; }
+int vmfa_synchronize(vmfa_ctx* x) {
+  TRY(check_ctx(x));
+  CU(cudaStreamSynchronize(x->stream));
+  return VMFA_OK;
+}
+
+int vmfa_upload_data(vmfa_ctx* x, const float* X, int64_t row_begin, int64_t rows) {
+  TRY(check_ctx(x));
+  if (!X || row_begin < 0 || rows < 0 || row_begin + rows > x->dm.N)
+    return fail(VMFA_ERR_INVALID_ARGUMENT, "vmfa_upload_data: row range outside the shard");
+  CU(cudaMemcpyAsync(x->X + row_begin * x->dm.D, X, sizeof(float) * rows * x->dm.D,
+                     cudaMemcpyHostToDevice, x->stream));
+  CU(cudaStreamSynchronize(x->stream));
+  return VMFA_OK;
+}
+
+int vmfa_set_floor(vmfa_ctx* x, const double* floor) {
+  TRY(check_ctx(x));
+  if (!floor) return fail(VMFA_ERR_INVALID_ARGUMENT, "floor is null");
+  CU(cudaMemcpyAsync(x->floor, floor, sizeof(double) * x->dm.D, cudaMemcpyHostToDevice, x->stream));
+  CU(cudaStreamSynchronize(x->stream));
+  return VMFA_OK;
+}
+
+int vmfa_upload_params(vmfa_ctx* x, const double* pi, const double* mu, const double* lambda,
+                       const double* dnoise) {
+  TRY(check_ctx(x));
+  if (!pi || !mu || !lambda || !dnoise) return fail(VMFA_ERR_INVALID_ARGUMENT, "null parameter array");
+  const size_t C = x->dm.C, D = x->dm.D, H = x->dm.H;
+  cudaStream_t s = x->stream;
+  CU(cudaMemcpyAsync(x->pi, pi, sizeof(double) * C, cudaMemcpyHostToDevice, s));
+  CU(cudaMemcpyAsync(x->mu, mu, sizeof(double) * C * D, cudaMemcpyHostToDevice, s));
+  CU(cudaMemcpyAsync(x->lam, lambda, sizeof(double) * C * D * H, cudaMemcpyHostToDevice, s));
+  CU(cudaMemcpyAsync(x->psi, dnoise, sizeof(double) * C * D, cudaMemcpyHostToDevice, s));
+  x->have_estep = false;
+  return run_precompute(x, nullptr);
+}
+
+int vmfa_download_params(vmfa_ctx* x, double* pi, double* mu, double* lambda, double* dnoise) {
+  TRY(check_ctx(x));
+  const size_t C = x->dm.C, D = x->dm.D, H = x->dm.H;
+  cudaStream_t s = x->stream;
+  if (pi) CU(cudaMemcpyAsync(pi, x->pi, sizeof(double) * C, cudaMemcpyDeviceToHost, s));
+  if (mu) CU(cudaMemcpyAsync(mu, x->mu, sizeof(double) * C * D, cudaMemcpyDeviceToHost, s));
+  if (lambda) CU(cudaMemcpyAsync(lambda, x->lam, sizeof(double) * C * D * H, cudaMemcpyDeviceToHost, s));
+  if (dnoise) CU(cudaMemcpyAsync(dnoise, x->psi, sizeof(double) * C * D, cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  return VMFA_OK;
+}
+
+int vmfa_precompute(vmfa_ctx* x, int* failed) {
+  TRY(check_ctx(x));
+  return run_precompute(x, failed);
+}
+
+int vmfa_download_caches(vmfa_ctx* x, double* U, double* Lmat, double* V, double* Sigma_z,
+                         double* inv_dnoise, double* logdet, double* log_pi) {
+  TRY(check_ctx(x));
+  const size_t C = x->dm.C, D = x->dm.D, H = x->dm.H;
+  cudaStream_t s = x->stream;
+  if (U || V || inv_dnoise) {
+    double *dU = nullptr, *dV = nullptr, *dI = nullptr;
+    CU(cudaMallocAsync(&dU, sizeof(double) * C * D * H, s));
+    CU(cudaMallocAsync(&dV, sizeof(double) * C * D * H, s));
+    CU(cudaMallocAsync(&dI, sizeof(double) * C * D, s));
+    CU(launch_caches_full(x->dm, x->lam, x->psi, x->R, dU, dV, dI, s));
+    if (U) CU(cudaMemcpyAsync(U, dU, sizeof(double) * C * D * H, cudaMemcpyDeviceToHost, s));
+    if (V) CU(cudaMemcpyAsync(V, dV, sizeof(double) * C * D * H, cudaMemcpyDeviceToHost, s));
+    if (inv_dnoise) CU(cudaMemcpyAsync(inv_dnoise, dI, sizeof(double) * C * D, cudaMemcpyDeviceToHost, s));
+    CU(cudaFreeAsync(dU, s));
+    CU(cudaFreeAsync(dV, s));
+    CU(cudaFreeAsync(dI, s));
+  }
+  if (Lmat) CU(cudaMemcpyAsync(Lmat, x->Lmat, sizeof(double) * C * H * H, cudaMemcpyDeviceToHost, s));
+  if (Sigma_z) CU(cudaMemcpyAsync(Sigma_z, x->Sz, sizeof(double) * C * H * H, cudaMemcpyDeviceToHost, s));
+  if (logdet) CU(cudaMemcpyAsync(logdet, x->logdet, sizeof(double) * C, cudaMemcpyDeviceToHost, s));
+  if (log_pi) {
+    CU(launch_logpi(x->pi, x->dm.C, x->logpi, s));
+    CU(cudaMemcpyAsync(log_pi, x->logpi, sizeof(double) * C, cudaMemcpyDeviceToHost, s));
+  }
+  CU(cudaStreamSynchronize(s));
+  return VMFA_OK;
+}
+
+int vmfa_upload_state(vmfa_ctx* x, const int32_t* K, const int32_t* g, const int32_t* g_count) {
+  TRY(check_ctx(x));
+  if (!K || !g || !g_count) return fail(VMFA_ERR_INVALID_ARGUMENT, "null state array");
+  const Dims& dm = x->dm;
+  // structural validation (VarState::validate, estep.cpp:15-68) on the host copy
+  for (int c = 0; c < dm.C; ++c) {
+    const int m = g_count[c];
+    if (m < 1 || m > dm.G) return fail(VMFA_ERR_INVALID_ARGUMENT, "g_c size out of range (c=%d)", c);
+    bool has_c = false;
+    for (int i = 0; i < m; ++i) {
+      const int v = g[static_cast<int64_t>(c) * dm.G + i];
+      if (v < 0 || v >= dm.C || (i > 0 && v <= g[static_cast<int64_t>(c) * dm.G + i - 1]))
+        return fail(VMFA_ERR_INVALID_ARGUMENT, "g_c not sorted distinct in-range indices (c=%d)", c);
+      has_c |= (v == c);
+    }
+    if (!has_c) return fail(VMFA_ERR_INVALID_ARGUMENT, "g_c does not contain c (c=%d)", c);
+  }
+  for (int64_t n = 0; n < dm.N; ++n)
+    for (int j = 0; j < dm.Cp; ++j) {
+      const int v = K[n * dm.Cp + j];
+      if (v < 0 || v >= dm.C || (j > 0 && v <= K[n * dm.Cp + j - 1]))
+        return fail(VMFA_ERR_INVALID_ARGUMENT, "K row not sorted distinct in-range indices (n=%lld)", static_cast<long long>(n));
+    }
+  std::vector<int32_t> gp(static_cast<size_t>(dm.C) * dm.G);
+  for (int c = 0; c < dm.C; ++c)
+    for (int i = 0; i < dm.G; ++i) gp[static_cast<size_t>(c) * dm.G + i] = i < g_count[c] ? g[static_cast<int64_t>(c) * dm.G + i] : -1;
+  cudaStream_t s = x->stream;
+  CU(cudaMemcpyAsync(x->K, K, sizeof(int) * dm.N * dm.Cp, cudaMemcpyHostToDevice, s));
+  CU(cudaMemcpyAsync(x->g, gp.data(), sizeof(int) * gp.size(), cudaMemcpyHostToDevice, s));
+  CU(cudaMemcpyAsync(x->gcnt, g_count, sizeof(int) * dm.C, cudaMemcpyHostToDevice, s));
+  CU(cudaStreamSynchronize(s));
+  x->kinv_for_current_K = false;
+  x->have_estep = false;
+  return VMFA_OK;
+}
+
+int vmfa_download_state(vmfa_ctx* x, int32_t* K, int32_t* g, int32_t* g_count, int32_t* labels) {
+  TRY(check_ctx(x));
+  const Dims& dm = x->dm;
+  cudaStream_t s = x->stream;
+  if (K) CU(cudaMemcpyAsync(K, x->K, sizeof(int) * dm.N * dm.Cp, cudaMemcpyDeviceToHost, s));
+  if (g) CU(cudaMemcpyAsync(g, x->g, sizeof(int) * dm.C * dm.G, cudaMemcpyDeviceToHost, s));
+  if (g_count) CU(cudaMemcpyAsync(g_count, x->gcnt, sizeof(int) * dm.C, cudaMemcpyDeviceToHost, s));
+  if (labels) CU(cudaMemcpyAsync(labels, x->labels, sizeof(int) * dm.N, cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  return VMFA_OK;
+}
+
+int vmfa_estep(vmfa_ctx* x, uint64_t seed, uint64_t iteration, int mode, double* F, uint64_t* joints) {
+  TRY(check_ctx(x));
+  if (mode != VMFA_DIST_KL && mode != VMFA_DIST_EUCLID) return fail(VMFA_ERR_INVALID_ARGUMENT, "mode");
+  TRY(estep_local(x, seed, iteration, mode, false));
+  TRY(estep_finish(x, false));
+  double sc[4];
+  TRY(read_scalars(x, sc));
+  if (F) *F = sc[0];
+  if (joints) *joints = static_cast<uint64_t>(sc[1]);
+  return VMFA_OK;
+}
+
+int vmfa_download_estep(vmfa_ctx* x, int32_t* count, int32_t* idx, double* lj, double* resp) {
+  TRY(check_ctx(x));
+  if (!x->have_estep) return fail(VMFA_ERR_INVALID_ARGUMENT, "no E-step has run");
+  const Dims& dm = x->dm;
+  cudaStream_t s = x->stream;
+  const size_t NS = static_cast<size_t>(dm.N) * dm.stride;
+  std::vector<int32_t> cnt(dm.N);
+  CU(cudaMemcpyAsync(cnt.data(), x->ret_cnt, sizeof(int) * dm.N, cudaMemcpyDeviceToHost, s));
+  std::vector<int32_t> id(NS);
+  std::vector<float> l(NS);
+  CU(cudaMemcpyAsync(id.data(), x->ret_idx, sizeof(int) * NS, cudaMemcpyDeviceToHost, s));
+  CU(cudaMemcpyAsync(l.data(), x->ret_lj, sizeof(float) * NS, cudaMemcpyDeviceToHost, s));
+  if (resp) CU(cudaMemcpyAsync(resp, x->resp, sizeof(double) * dm.N * dm.Cp, cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  // reference layout: -1 / 0.0 padding beyond count (RetainedJoints::reset)
+  for (int64_t n = 0; n < dm.N; ++n) {
+    if (count) count[n] = cnt[n];
+    for (int j = 0; j < dm.stride; ++j) {
+      const size_t at = static_cast<size_t>(n) * dm.stride + j;
+      const bool live = j < cnt[n];
+      if (idx) idx[at] = live ? id[at] : -1;
+      if (lj) lj[at] = live ? static_cast<double>(l[at]) : 0.0;
+    }
+  }
+  return VMFA_OK;
+}
+
+int vmfa_download_distances(vmfa_ctx* x, int64_t cap, int32_t* c, int32_t* ct, double* sum,
+                            int64_t* count, int64_t* n_rows) {
+  TRY(check_ctx(x));
+  // Re-run block 3 of the last E-step in dump mode is not possible after g was
+  // replaced, so the dump is armed here and filled by the NEXT E-step when
+  // cap == 0 (query); with cap > 0 the rows of the last armed E-step are read.
+  if (cap == 0) {
+    if (!x->dump) {
+      x->dump = true;
+      x->dump_cap = static_cast<long long>(x->dm.N) * x->dm.stride;
+      int r = VMFA_OK;
+      auto A = [&](auto*& p, size_t n) {
+        if (r == VMFA_OK) r = x->alloc(p, n);
+      };
+      A(x->dump_c, x->dump_cap);
+      A(x->dump_ct, x->dump_cap);
+      A(x->dump_cnt, x->dump_cap);
+      A(x->dump_hi, x->dump_cap);
+      A(x->dump_lo, x->dump_cap);
+      A(x->dump_n, 1);
+      if (r != VMFA_OK) return r;
+      CU(cudaMemsetAsync(x->dump_n, 0, sizeof(unsigned long long), x->stream));
+    }
+    unsigned long long m = 0;
+    CU(cudaMemcpyAsync(&m, x->dump_n, sizeof m, cudaMemcpyDeviceToHost, x->stream));
+    CU(cudaStreamSynchronize(x->stream));
+    if (n_rows) *n_rows = static_cast<int64_t>(m);
+    return VMFA_OK;
+  }
+  if (!x->dump) return fail(VMFA_ERR_INVALID_ARGUMENT, "distance dump not armed (call with cap=0 first)");
+  unsigned long long m = 0;
+  CU(cudaMemcpyAsync(&m, x->dump_n, sizeof m, cudaMemcpyDeviceToHost, x->stream));
+  CU(cudaStreamSynchronize(x->stream));
+  const int64_t rows = std::min<int64_t>(static_cast<int64_t>(m), x->dump_cap);
+  std::vector<int32_t> vc(rows), vct(rows);
+  std::vector<long long> vn(rows), vh(rows), vl(rows);
+  cudaStream_t s = x->stream;
+  CU(cudaMemcpyAsync(vc.data(), x->dump_c, sizeof(int) * rows, cudaMemcpyDeviceToHost, s));
+  CU(cudaMemcpyAsync(vct.data(), x->dump_ct, sizeof(int) * rows, cudaMemcpyDeviceToHost, s));
+  CU(cudaMemcpyAsync(vn.data(), x->dump_cnt, sizeof(long long) * rows, cudaMemcpyDeviceToHost, s));
+  CU(cudaMemcpyAsync(vh.data(), x->dump_hi, sizeof(long long) * rows, cudaMemcpyDeviceToHost, s));
+  CU(cudaMemcpyAsync(vl.data(), x->dump_lo, sizeof(long long) * rows, cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  std::vector<int64_t> order(rows);
+  for (int64_t i = 0; i < rows; ++i) order[i] = i;
+  std::sort(order.begin(), order.end(), [&](int64_t a, int64_t b) {
+    return vc[a] != vc[b] ? vc[a] < vc[b] : vct[a] < vct[b];
+  });
+  const int64_t w = std::min<int64_t>(rows, cap);
+  for (int64_t i = 0; i < w; ++i) {
+    const int64_t k = order[i];
+    if (c) c[i] = vc[k];
+    if (ct) ct[i] = vct[k];
+    if (sum) sum[i] = static_cast<double>(vh[k]) / 1024.0 + static_cast<double>(vl[k]) / 1125899906842624.0;
+    if (count) count[i] = vn[k];
+  }
+  if (n_rows) *n_rows = rows;
+  return VMFA_OK;
+}
+
+int vmfa_accumulate_suffstats(vmfa_ctx* x) {
+  TRY(check_ctx(x));
+  TRY(stats_local(x));
+  CU(cudaStreamSynchronize(x->stream));
+  return VMFA_OK;
+}
+
+int vmfa_download_suffstats(vmfa_ctx* x, double* Nc, double* Y, double* E, double* sq) {
+  TRY(check_ctx(x));
+  const size_t C = x->dm.C, D = x->dm.D, H1 = x->dm.H + 1;
+  cudaStream_t s = x->stream;
+  if (Nc) CU(cudaMemcpyAsync(Nc, x->Nc, sizeof(double) * C, cudaMemcpyDeviceToHost, s));
+  if (Y) CU(cudaMemcpyAsync(Y, x->Y, sizeof(double) * C * H1 * D, cudaMemcpyDeviceToHost, s));
+  if (E) CU(cudaMemcpyAsync(E, x->E, sizeof(double) * C * H1 * H1, cudaMemcpyDeviceToHost, s));
+  if (sq) CU(cudaMemcpyAsync(sq, x->sq, sizeof(double) * C * D, cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  return VMFA_OK;
+}
+
+int vmfa_upload_suffstats(vmfa_ctx* x, const double* Nc, const double* Y, const double* E,
+                          const double* sq) {
+  TRY(check_ctx(x));
+  if (!Nc || !Y || !E || !sq) return fail(VMFA_ERR_INVALID_ARGUMENT, "null statistics array");
+  const size_t C = x->dm.C, D = x->dm.D, H1 = x->dm.H + 1;
+  cudaStream_t s = x->stream;
+  CU(cudaMemcpyAsync(x->Nc, Nc, sizeof(double) * C, cudaMemcpyHostToDevice, s));
+  CU(cudaMemcpyAsync(x->Y, Y, sizeof(double) * C * H1 * D, cudaMemcpyHostToDevice, s));
+  CU(cudaMemcpyAsync(x->E, E, sizeof(double) * C * H1 * H1, cudaMemcpyHostToDevice, s));
+  CU(cudaMemcpyAsync(x->sq, sq, sizeof(double) * C * D, cudaMemcpyHostToDevice, s));
+  CU(cudaStreamSynchronize(s));
+  return VMFA_OK;
+}
+
+int vmfa_update_params(vmfa_ctx* x, int* failed) {
+  TRY(check_ctx(x));
+  return update_and_precompute(x, failed);
+}
+
+int vmfa_truncated_free_energy(vmfa_ctx* x, double* F) {
+  TRY(check_ctx(x));
+  TRY(free_energy_local(x));
+  double sc[4];
+  TRY(read_scalars(x, sc));
+  if (F) *F = sc[2];
+  return VMFA_OK;
+}
+
+int vmfa_exact_log_likelihood(vmfa_ctx* x, double* ll) {
+  TRY(check_ctx(x));
+  (void)ll;
+  return fail(VMFA_ERR_UNSUPPORTED, "exact_log_likelihood is SURVEY §8(f) 'next' item 1 (not in this build)");
+}
+
+int vmfa_iterate(vmfa_ctx* x, uint64_t seed, uint64_t iteration, int mode, vmfa_iter_report* rep) {
+  TRY(check_ctx(x));
+  if (mode != VMFA_DIST_KL && mode != VMFA_DIST_EUCLID) return fail(VMFA_ERR_INVALID_ARGUMENT, "mode");
+  int failed = -1;
+  TRY(estep_local(x, seed, iteration, mode, false));
+  TRY(estep_finish(x, false));
+  TRY(stats_local(x));
+  const int r = update_and_precompute(x, &failed);
+  if (rep) rep->failed_component = failed;
+  if (r != VMFA_OK) return r;
+  TRY(free_energy_local(x));
+  CU(launch_count_empty(x->pi, x->dm.C, x->n_empty, x->stream));
+  double sc[4];
+  int ne = 0;
+  CU(cudaMemcpyAsync(&ne, x->n_empty, sizeof(int), cudaMemcpyDeviceToHost, x->stream));
+  TRY(read_scalars(x, sc));
+  if (rep) {
+    rep->free_energy_estep = sc[0];
+    rep->joints = static_cast<uint64_t>(sc[1]);
+    rep->free_energy = sc[2];
+    rep->empty_components = ne;
+  }
+  return VMFA_OK;
+}
+
+// ---------------------------------------------------------------- phase API (multi-GPU)
+int vmfa_exchange_buffer(vmfa_ctx* x, int which, void** ptr, size_t* count, int* dtype) {
+  TRY(check_ctx(x));
+  if (!ptr || !count || !dtype) return fail(VMFA_ERR_INVALID_ARGUMENT, "null output");
+  if (which == VMFA_XCHG_COOC) {
+    const size_t n = 3 * static_cast<size_t>(x->dm.C) * x->dm.C;
+    if (n * sizeof(long long) > (size_t{8} << 30))
+      return fail(VMFA_ERR_UNSUPPORTED, "dense co-occurrence exchange limited to C <= ~18900 in this build");
+    if (!x->xc) TRY(x->alloc(x->xc, n));
+    *ptr = x->xc;
+    *count = n;
+    *dtype = VMFA_DT_INT64;
+  } else if (which == VMFA_XCHG_STATS) {
+    *ptr = x->stats;
+    *count = x->stats_len;
+    *dtype = VMFA_DT_FLOAT64;
+  } else if (which == VMFA_XCHG_SCALARS) {
+    *ptr = x->scal;
+    *count = 3;
+    *dtype = VMFA_DT_FLOAT64;
+  } else {
+    return fail(VMFA_ERR_INVALID_ARGUMENT, "unknown exchange buffer %d", which);
+  }
+  return VMFA_OK;
+}
+
+int vmfa_phase_estep_local(vmfa_ctx* x, uint64_t seed, uint64_t iteration, int mode) {
+  TRY(check_ctx(x));
+  if (!x->xc) {
+    void* p;
+    size_t n;
+    int dt;
+    TRY(vmfa_exchange_buffer(x, VMFA_XCHG_COOC, &p, &n, &dt));
+  }
+  TRY(estep_local(x, seed, iteration, mode, true));
+  CU(cudaMemsetAsync(x->scal + 2, 0, sizeof(double), x->stream));
+  CU(cudaStreamSynchronize(x->stream));
+  return VMFA_OK;
+}
+int vmfa_phase_estep_finish(vmfa_ctx* x) {
+  TRY(check_ctx(x));
+  return estep_finish(x, true);
+}
+int vmfa_phase_stats_local(vmfa_ctx* x) {
+  TRY(check_ctx(x));
+  TRY(stats_local(x));
+  CU(cudaStreamSynchronize(x->stream));
+  return VMFA_OK;
+}
+int vmfa_phase_update(vmfa_ctx* x, int* failed) {
+  TRY(check_ctx(x));
+  return update_and_precompute(x, failed);
+}
+int vmfa_phase_free_energy_local(vmfa_ctx* x) {
+  TRY(check_ctx(x));
+  TRY(free_energy_local(x));
+  CU(cudaStreamSynchronize(x->stream));
+  return VMFA_OK;
+}
+int vmfa_phase_scalars(vmfa_ctx* x, double* Fe, uint64_t* joints, double* F) {
+  TRY(check_ctx(x));
+  double sc[4];
+  TRY(read_scalars(x, sc));
+  if (Fe) *Fe = sc[0];
+  if (joints) *joints = static_cast<uint64_t>(sc[1]);
+  if (F) *F = sc[2];
+  return VMFA_OK;
+}
+
+// ---------------------------------------------------------------- profiling
+int vmfa_profile_enable(vmfa_ctx* x, int enable) {
+  TRY(check_ctx(x));
+  x->collect();
+  x->profile = enable != 0;
+  for (int i = 0; i < kNumFamilies; ++i) {
+    x->fam_ms[i] = 0.0;
+    x->fam_launches[i] = 0;
+    x->fam_units[i] = 0;
+  }
+  return VMFA_OK;
+}
+int vmfa_kernel_times(vmfa_ctx* x, int max, double* ms, int64_t* launches, int64_t* units, int* n) {
+  TRY(check_ctx(x));
+  x->collect();
+  const int m = std::min<int>(max, kNumFamilies);
+  for (int i = 0; i < m; ++i) {
+    if (ms) ms[i] = x->fam_ms[i];
+    if (launches) launches[i] = x->fam_launches[i];
+    if (units) units[i] = x->fam_units[i];
+  }
+  if (n) *n = kNumFamilies;
+  return VMFA_OK;
+}
+const char* vmfa_kernel_name(int i) { return (i >= 0 && i < kNumFamilies) ? kFamilyNames[i] : ""; }
+
+}  // extern "C"

@@ -1,0 +1,1302 @@
+// vmfa_kernels.cu — sm_100a kernels of one v-MFA EM iteration.
+//
+// Design: the E-step scoring is organised around ANCHOR BLOCKS.
+// For every component a, the points n with a in K(n) (the inverted K map, a
+// stable counting sort) need every component of g_a, because
+// S(n) = U_{a in K(n)} g_a U {r_n} (estep.cpp:83-101). A block (64 gathered
+// rows of a) x (g_a) is therefore dense: the rows are staged once in shared
+// memory and every component of g_a is scored against them, so each gathered
+// row is read from HBM/L2 C' times per iteration instead of |S(n)| times.
+// Duplicates across anchors are scored but dropped by k_select, which also
+// reproduces the reference's insertion order, tie rules and counters exactly.
+#include <cfloat>
+#include <cmath>
+#include <cstdint>
+
+#include "vmfa_kernels.cuh"
+#include "vmfa_rng.hpp"
+
+namespace vmfa_b200 {
+
+namespace {
+
+constexpr double kLog2Pi = 1.8378770664093453;  // numerics.hpp:10
+constexpr unsigned kFull = 0xffffffffu;
+
+__device__ __forceinline__ int find_item(const int* itemoff, int C, int item) {
+  // largest c with itemoff[c] <= item (itemoff is non-decreasing, size C+1)
+  int lo = 0, hi = C;  // invariant itemoff[lo] <= item < itemoff[hi]
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (__ldg(itemoff + mid) <= item) lo = mid;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// ---------------------------------------------------------------- small utilities
+__global__ void k_iota(int* v, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    v[i] = static_cast<int>(i);
+}
+__global__ void k_fill_i32(int* v, int64_t n, int value) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    v[i] = value;
+}
+__global__ void k_keys_from_i32(const int* src, unsigned* keys, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    keys[i] = static_cast<unsigned>(src[i]);
+}
+__global__ void k_hist(const unsigned* keys, int64_t n, int C, int* cnt) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned k = keys[i];
+    if (k < static_cast<unsigned>(C)) atomicAdd(cnt + k, 1);
+  }
+}
+__global__ void k_chunks(const int* cnt, int C, int rows, int* chunks) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c <= C; c += gridDim.x * blockDim.x)
+    chunks[c] = c < C ? (cnt[c] + rows - 1) / rows : 0;
+}
+
+// ---------------------------------------------------------------- K0: extra candidate
+// r_n = uniform_component(seed, iteration, n_global, C) (rng.hpp:91-98,
+// estep.cpp:259-260). rkey = r_n if it is not already in U_{a in K(n)} g_a,
+// else the sentinel C (the reference pushes it and the epoch-stamp drops it).
+__global__ void k_extra(Dims dm, const int* __restrict__ K, const int* __restrict__ g,
+                        const int* __restrict__ gcnt, uint64_t seed, uint64_t it, int* rx,
+                        unsigned* rkey) {
+  for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < dm.N; n += (int64_t)gridDim.x * blockDim.x) {
+    const int r = extra_candidate(seed, it, static_cast<uint64_t>(dm.n0 + n), dm.C);
+    bool dup = false;
+    for (int j = 0; j < dm.Cp && !dup; ++j) {
+      const int a = K[n * dm.Cp + j];
+      const int m = gcnt[a];
+      for (int i = 0; i < m; ++i)
+        if (g[(int64_t)a * dm.G + i] == r) {
+          dup = true;
+          break;
+        }
+    }
+    rx[n] = r;
+    rkey[n] = dup ? static_cast<unsigned>(dm.C) : static_cast<unsigned>(r);
+  }
+}
+
+// ---------------------------------------------------------------- K2: scoring (FFMA)
+// One warp scores one component against the 64 staged rows of the item: lane l
+// owns rows 2l and 2l+1; per dimension it reads the row pair from the
+// transposed smem tile and the component's packed parameter row (broadcast
+// ld.global.nc), computing v = x - mu, diag += v^2/psi and y = W^T v in fp32.
+// l(n,c) = kconst_c - 0.5 (diag - |y|^2), combined in fp64 (model.cpp:87-94).
+template <int HC>
+__device__ __forceinline__ void score_pair_rows(const float* __restrict__ xs, int D, int H,
+                                                int Hc, int HP, const float* __restrict__ Pc,
+                                                int lane, float& diag0, float& diag1,
+                                                float& yy0, float& yy1) {
+  diag0 = diag1 = yy0 = yy1 = 0.f;
+  for (int h0 = 0; h0 < Hc; h0 += HC) {
+    float a0[HC], a1[HC];
+#pragma unroll
+    for (int h = 0; h < HC; ++h) a0[h] = a1[h] = 0.f;
+    const bool first = (h0 == 0);
+#pragma unroll 2
+    for (int d = 0; d < D; ++d) {
+      const float2 xv = *reinterpret_cast<const float2*>(xs + d * kXsStride + 2 * lane);
+      const float* pd = Pc + (int64_t)d * HP;
+      const float2 mp = __ldg(reinterpret_cast<const float2*>(pd + Hc));
+      const float v0 = xv.x - mp.x, v1 = xv.y - mp.x;
+      if (first) {
+        diag0 = fmaf(v0 * mp.y, v0, diag0);
+        diag1 = fmaf(v1 * mp.y, v1, diag1);
+      }
+#pragma unroll
+      for (int h = 0; h < HC; h += 4) {
+        const float4 w = __ldg(reinterpret_cast<const float4*>(pd + h0 + h));
+        a0[h + 0] = fmaf(w.x, v0, a0[h + 0]);
+        a1[h + 0] = fmaf(w.x, v1, a1[h + 0]);
+        a0[h + 1] = fmaf(w.y, v0, a0[h + 1]);
+        a1[h + 1] = fmaf(w.y, v1, a1[h + 1]);
+        a0[h + 2] = fmaf(w.z, v0, a0[h + 2]);
+        a1[h + 2] = fmaf(w.z, v1, a1[h + 2]);
+        a0[h + 3] = fmaf(w.w, v0, a0[h + 3]);
+        a1[h + 3] = fmaf(w.w, v1, a1[h + 3]);
+      }
+    }
+#pragma unroll
+    for (int h = 0; h < HC; ++h) {
+      yy0 = fmaf(a0[h], a0[h], yy0);
+      yy1 = fmaf(a1[h], a1[h], yy1);
+    }
+  }
+  (void)H;
+}
+
+template <int MODE, int HC>
+__global__ void __launch_bounds__(kScoreThreads)
+k_score(ScoreArgs a) {
+  extern __shared__ __align__(16) float xs[];  // [D][kXsStride]
+  __shared__ int s_n[kScoreRows];
+  __shared__ int s_e[kScoreRows];
+  const Dims dm = a.dm;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int total = __ldg(a.itemoff + dm.C);
+  for (int item = blockIdx.x; item < total; item += gridDim.x) {
+    const int c = find_item(a.itemoff, dm.C, item);
+    const int row0 = __ldg(a.off + c) + (item - __ldg(a.itemoff + c)) * kScoreRows;
+    const int nrows = min(kScoreRows, __ldg(a.off + c + 1) - row0);
+    if (tid < kScoreRows) {
+      int e = -1, n = -1;
+      if (tid < nrows) {
+        e = __ldg(a.ent + row0 + tid);
+        n = MODE == kModeExtra ? e : e / dm.Cp;
+      }
+      s_e[tid] = e;
+      s_n[tid] = n;
+    }
+    __syncthreads();
+    // gather rows, transposed into xs[d][r] (coalesced global reads along d)
+    for (int r = warp; r < kScoreRows; r += kScoreThreads / 32) {
+      const int n = s_n[r];
+      const float* xr = a.X + (int64_t)(n < 0 ? 0 : n) * dm.D;
+      for (int d = lane; d < dm.D; d += 32) xs[d * kXsStride + r] = n < 0 ? 0.f : __ldg(xr + d);
+    }
+    __syncthreads();
+    const int ncomp = MODE == kModeAnchor ? __ldg(a.gcnt + c) : 1;
+    for (int ci = warp; ci < ncomp; ci += kScoreThreads / 32) {
+      const int comp = MODE == kModeAnchor ? __ldg(a.g + (int64_t)c * dm.G + ci) : c;
+      const float* Pc = a.P + (int64_t)comp * dm.D * a.L.HP;
+      float d0, d1, y0, y1;
+      score_pair_rows<HC>(xs, dm.D, dm.H, a.L.Hc, a.L.HP, Pc, lane, d0, d1, y0, y1);
+      const double kc = __ldg(a.kconst + comp);
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const int r = 2 * lane + k;
+        if (r >= nrows) continue;
+        const double diag = k == 0 ? d0 : d1, yy = k == 0 ? y0 : y1;
+        const float lj = static_cast<float>(kc - 0.5 * (diag - yy));
+        const int e = s_e[r];
+        if (MODE == kModeAnchor) {
+          const int n = e / dm.Cp, j = e - n * dm.Cp;
+          a.out[(int64_t)n * dm.SL + j * dm.G + ci] = lj;
+        } else if (MODE == kModeExtra) {
+          a.out[(int64_t)e * dm.SL + dm.Cp * dm.G] = lj;
+        } else {
+          a.out[e] = lj;
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------- K3: selection (warp per row)
+// Reconstructs S(n) in the reference's insertion order (slot s = j*G + i for
+// g_{K(n)[j]}[i], then the extra), keeps the first occurrence of each component
+// (epoch-stamp dedup, estep.cpp:83-101), selects the top-C' by (l desc, index
+// asc) (estep.cpp:103-122), labels the row by the first strict maximum over the
+// ascending K row (estep.cpp:157-166) and computes the fp64 responsibilities
+// and LSE of block 4 (estep.cpp:316-335).
+struct Cand {
+  float l;
+  int c;
+  int slot;
+  int valid;
+};
+__device__ __forceinline__ bool better(const Cand& x, const Cand& y) {
+  if (x.valid != y.valid) return x.valid > y.valid;
+  if (x.l != y.l) return x.l > y.l;
+  return x.c < y.c;
+}
+
+template <int NS>
+__global__ void __launch_bounds__(256) k_select(SelectArgs a) {
+  const Dims dm = a.dm;
+  const int lane = threadIdx.x & 31;
+  const int64_t warp0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int CpG = dm.Cp * dm.G;
+  for (int64_t n = warp0; n < dm.N; n += nwarps) {
+    int comp[NS];
+    bool uniq[NS];
+    float lj[NS];
+#pragma unroll
+    for (int k = 0; k < NS; ++k) {
+      const int s = k * 32 + lane;
+      int cmp = -1;
+      if (s < CpG) {
+        const int j = s / dm.G, i = s - j * dm.G;
+        const int an = a.K[n * dm.Cp + j];
+        if (i < a.gcnt[an]) cmp = a.g[(int64_t)an * dm.G + i];
+      } else if (s == CpG) {
+        cmp = a.rx[n];
+      }
+      comp[k] = cmp;
+      uniq[k] = cmp >= 0;
+    }
+    // first-occurrence dedup in slot order
+#pragma unroll
+    for (int k = 0; k < NS; ++k) {
+      for (int src = 0; src < 32; ++src) {
+        const int t = k * 32 + src;
+        if (t >= dm.SL) break;
+        const int ct = __shfl_sync(kFull, comp[k], src);
+        if (ct < 0) continue;
+#pragma unroll
+        for (int kk = 0; kk < NS; ++kk) {
+          const int s = kk * 32 + lane;
+          if (s > t && comp[kk] == ct) uniq[kk] = false;
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < NS; ++k) {
+      float v = 0.f;
+      if (uniq[k]) {
+        v = a.LJ[n * dm.SL + k * 32 + lane];
+        if (v != v) v = -INFINITY;  // NaN ranks last (reference comparator undefined)
+      }
+      lj[k] = v;
+    }
+    // compaction of the retained joints (reference layout, insertion order)
+    int base = 0;
+#pragma unroll
+    for (int k = 0; k < NS; ++k) {
+      const unsigned b = __ballot_sync(kFull, uniq[k]);
+      if (uniq[k]) {
+        const int pos = base + __popc(b & ((1u << lane) - 1u));
+        a.ret_idx[n * dm.stride + pos] = comp[k];
+        a.ret_lj[n * dm.stride + pos] = lj[k];
+      }
+      base += __popc(b);
+    }
+    const int m = base;
+    // top-C' by (l desc, index asc)
+    bool sel[NS];
+#pragma unroll
+    for (int k = 0; k < NS; ++k) sel[k] = false;
+    int kc[8];
+    float kl[8];
+    for (int r = 0; r < dm.Cp; ++r) {
+      Cand best{-INFINITY, 0x7fffffff, -1, 0};
+#pragma unroll
+      for (int k = 0; k < NS; ++k) {
+        if (!uniq[k] || sel[k]) continue;
+        Cand cnd{lj[k], comp[k], k * 32 + lane, 1};
+        if (better(cnd, best)) best = cnd;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        Cand oth;
+        oth.l = __shfl_xor_sync(kFull, best.l, o);
+        oth.c = __shfl_xor_sync(kFull, best.c, o);
+        oth.slot = __shfl_xor_sync(kFull, best.slot, o);
+        oth.valid = __shfl_xor_sync(kFull, best.valid, o);
+        if (better(oth, best)) best = oth;
+      }
+      kc[r] = best.c;
+      kl[r] = best.l;
+      if (best.valid && (best.slot & 31) == lane) {
+#pragma unroll
+        for (int k = 0; k < NS; ++k)
+          if (best.slot == k * 32 + lane) sel[k] = true;
+      }
+      if (!best.valid && lane == 0) atomicOr(a.status, 1);  // InsufficientCandidates
+    }
+    // sort (kc, kl) ascending by component (estep.cpp:121)
+    for (int i = 1; i < dm.Cp; ++i) {
+      const int c0 = kc[i];
+      const float l0 = kl[i];
+      int j = i - 1;
+      while (j >= 0 && kc[j] > c0) {
+        kc[j + 1] = kc[j];
+        kl[j + 1] = kl[j];
+        --j;
+      }
+      kc[j + 1] = c0;
+      kl[j + 1] = l0;
+    }
+    // label: first member, replaced only by a strictly larger l (estep.cpp:157-166)
+    int best_c = kc[0];
+    float best_l = kl[0];
+    for (int j = 1; j < dm.Cp; ++j)
+      if (kl[j] > best_l) {
+        best_l = kl[j];
+        best_c = kc[j];
+      }
+    // block 4: fp64 log-sum-exp and responsibilities (numerics.hpp:15-22)
+    double mx = -INFINITY;
+    for (int j = 0; j < dm.Cp; ++j) mx = fmax(mx, static_cast<double>(kl[j]));
+    double l = mx;
+    if (isfinite(mx)) {
+      double s = 0.0;
+      for (int j = 0; j < dm.Cp; ++j) s += exp(static_cast<double>(kl[j]) - mx);
+      l = mx + log(s);
+    }
+    if (lane < dm.Cp) {
+      int myc = kc[0];
+      float myl = kl[0];
+      for (int j = 1; j < dm.Cp; ++j)
+        if (j == lane) {
+          myc = kc[j];
+          myl = kl[j];
+        }
+      a.K[n * dm.Cp + lane] = myc;
+      a.resp[n * dm.Cp + lane] = exp(static_cast<double>(myl) - l);
+    }
+    if (lane == 0) {
+      a.labels[n] = best_c;
+      a.lablj[n] = best_l;
+      a.lse[n] = l;
+      a.ret_cnt[n] = m;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- K4: g update (CTA per component)
+// Block 3 (estep.cpp:286-312): for n in I_c and each retained ct != c with
+// pi_ct > 0, accumulate value = (l(n,c) - log pi_c) - (l(n,ct) - log pi_ct)
+// [kl] or -l(n,ct) [euclid] into (sum, count) per ct; then update_g
+// (estep.cpp:204-220): g_c = {c} U the G-1 smallest (sum/count, ct), sorted.
+// Sums are exact fixed-point integers (2^-50 resolution, split hi/lo int64),
+// so the accumulation order — and the number of ranks — cannot change them.
+__device__ __forceinline__ void to_fixed(double v, long long& hi, long long& lo) {
+  const double kMax = 2147483648.0;  // |value| saturates at 2^31
+  if (!(v == v)) v = kMax;
+  v = fmin(fmax(v, -kMax), kMax);
+  const double y = v * 1024.0;  // 2^10
+  const double f = floor(y);
+  hi = static_cast<long long>(f);
+  lo = static_cast<long long>((y - f) * 1099511627776.0);  // 2^40
+}
+__device__ __forceinline__ double from_fixed(long long hi, long long lo) {
+  return static_cast<double>(hi) * (1.0 / 1024.0) + static_cast<double>(lo) * (1.0 / 1125899906842624.0);
+}
+__device__ __forceinline__ unsigned hash_key(int k) { return static_cast<unsigned>(k) * 2654435761u; }
+
+struct KeyMin {
+  double v;
+  int c;
+};
+__device__ __forceinline__ bool kless(const KeyMin& x, const KeyMin& y) {
+  if (x.v != y.v) return x.v < y.v;
+  return x.c < y.c;
+}
+
+__global__ void __launch_bounds__(kGupdThreads) k_gupdate(GupdArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  long long* t_hi = reinterpret_cast<long long*>(smem_raw);
+  long long* t_lo = t_hi + kGupdCap;
+  int* t_key = reinterpret_cast<int*>(t_lo + kGupdCap);
+  int* t_cnt = t_key + kGupdCap;
+  __shared__ KeyMin red[kGupdThreads / 32];
+  __shared__ int s_sel[64];
+  __shared__ int s_nsel;
+  const Dims dm = a.dm;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nw = kGupdThreads / 32;
+  long long* g_cnt = a.gt_cnt + (int64_t)blockIdx.x * dm.C;
+  long long* g_hi = a.gt_hi + (int64_t)blockIdx.x * dm.C;
+  long long* g_lo = a.gt_lo + (int64_t)blockIdx.x * dm.C;
+  for (int c = blockIdx.x; c < dm.C; c += gridDim.x) {
+    const int p0 = a.part_off[c], p1 = a.part_off[c + 1];
+    const int npts = p1 - p0;
+    const long long bound = llmin((long long)dm.C - 1, (long long)npts * (dm.stride - 1));
+    int cap = 32;
+    while (cap < 2 * bound && cap < 2 * kGupdCap) cap <<= 1;
+    const bool use_smem = cap <= kGupdCap;
+    if (npts > 0) {
+      if (use_smem) {
+        for (int i = tid; i < cap; i += kGupdThreads) {
+          t_key[i] = -1;
+          t_cnt[i] = 0;
+          t_hi[i] = 0;
+          t_lo[i] = 0;
+        }
+      } else {
+        for (int i = tid; i < dm.C; i += kGupdThreads) {
+          g_cnt[i] = 0;
+          g_hi[i] = 0;
+          g_lo[i] = 0;
+        }
+      }
+      __syncthreads();
+      const double logpi_c = a.logpi[c];
+      for (int p = p0 + warp; p < p1; p += nw) {
+        const int n = a.part_ent[p];
+        const double cond_c = static_cast<double>(a.lablj[n]) - logpi_c;
+        const int m = a.ret_cnt[n];
+        for (int j = lane; j < m; j += 32) {
+          const int ct = a.ret_idx[(int64_t)n * dm.stride + j];
+          if (ct == c) continue;
+          const double lpt = a.logpi[ct];
+          if (lpt == -INFINITY) continue;  // pi_ct <= 0 (estep.cpp:301)
+          const double lt = static_cast<double>(a.ret_lj[(int64_t)n * dm.stride + j]);
+          const double v = a.mode == 0 ? cond_c - (lt - lpt) : -lt;
+          long long hi, lo;
+          to_fixed(v, hi, lo);
+          if (use_smem) {
+            unsigned h = hash_key(ct) & (cap - 1);
+            while (true) {
+              const int prev = atomicCAS(t_key + h, -1, ct);
+              if (prev == -1 || prev == ct) break;
+              h = (h + 1) & (cap - 1);
+            }
+            atomicAdd(t_cnt + h, 1);
+            atomicAdd(reinterpret_cast<unsigned long long*>(t_hi + h), static_cast<unsigned long long>(hi));
+            atomicAdd(reinterpret_cast<unsigned long long*>(t_lo + h), static_cast<unsigned long long>(lo));
+          } else {
+            atomicAdd(reinterpret_cast<unsigned long long*>(g_cnt + ct), 1ULL);
+            atomicAdd(reinterpret_cast<unsigned long long*>(g_hi + ct), static_cast<unsigned long long>(hi));
+            atomicAdd(reinterpret_cast<unsigned long long*>(g_lo + ct), static_cast<unsigned long long>(lo));
+          }
+        }
+      }
+      __syncthreads();
+    }
+    const int tab_n = npts == 0 ? 0 : (use_smem ? cap : dm.C);
+    auto entry = [&](int i, int& ct, long long& cnt, long long& hi, long long& lo) {
+      if (use_smem) {
+        ct = t_key[i];
+        cnt = t_cnt[i];
+        hi = t_hi[i];
+        lo = t_lo[i];
+      } else {
+        ct = i;
+        cnt = g_cnt[i];
+        hi = g_hi[i];
+        lo = g_lo[i];
+      }
+    };
+    if (a.dump && npts > 0) {
+      for (int i = tid; i < tab_n; i += kGupdThreads) {
+        int ct;
+        long long cnt, hi, lo;
+        entry(i, ct, cnt, hi, lo);
+        if (ct < 0 || cnt <= 0) continue;
+        const unsigned long long w = atomicAdd(a.dump_n, 1ULL);
+        if ((long long)w < a.dump_cap) {
+          a.dump_c[w] = c;
+          a.dump_ct[w] = ct;
+          a.dump_cnt[w] = cnt;
+          a.dump_hi[w] = hi;
+          a.dump_lo[w] = lo;
+        }
+      }
+    }
+    if (a.exchange) {
+      const int64_t CC = (int64_t)dm.C * dm.C;
+      for (int i = tid; i < tab_n; i += kGupdThreads) {
+        int ct;
+        long long cnt, hi, lo;
+        entry(i, ct, cnt, hi, lo);
+        if (ct < 0 || cnt <= 0) continue;
+        const int64_t at = (int64_t)c * dm.C + ct;
+        a.xc[at] = cnt;
+        a.xc[CC + at] = hi;
+        a.xc[2 * CC + at] = lo;
+      }
+      __syncthreads();
+      continue;
+    }
+    // update_g: G-1 rounds of a block-wide argmin over (avg, ct)
+    if (tid == 0) s_nsel = 0;
+    __syncthreads();
+    for (int r = 0; r < dm.G - 1 && npts > 0; ++r) {
+      KeyMin best{INFINITY, 0x7fffffff};
+      for (int i = tid; i < tab_n; i += kGupdThreads) {
+        int ct;
+        long long cnt, hi, lo;
+        entry(i, ct, cnt, hi, lo);
+        if (ct < 0 || cnt <= 0) continue;
+        bool taken = false;
+        for (int q = 0; q < s_nsel; ++q) taken |= (s_sel[q] == ct);
+        if (taken) continue;
+        const KeyMin k{from_fixed(hi, lo) / static_cast<double>(cnt), ct};
+        if (kless(k, best)) best = k;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        KeyMin oth{__shfl_xor_sync(kFull, best.v, o), __shfl_xor_sync(kFull, best.c, o)};
+        if (kless(oth, best)) best = oth;
+      }
+      if (lane == 0) red[warp] = best;
+      __syncthreads();
+      if (tid == 0) {
+        KeyMin b = red[0];
+        for (int w = 1; w < nw; ++w)
+          if (kless(red[w], b)) b = red[w];
+        if (b.c != 0x7fffffff) s_sel[s_nsel++] = b.c;
+      }
+      __syncthreads();
+      if (s_nsel <= r) break;  // no more keys
+    }
+    if (tid == 0) {
+      int out[64];
+      int m = 0;
+      out[m++] = c;
+      for (int q = 0; q < s_nsel; ++q) out[m++] = s_sel[q];
+      for (int i = 1; i < m; ++i) {
+        const int v = out[i];
+        int j = i - 1;
+        while (j >= 0 && out[j] > v) {
+          out[j + 1] = out[j];
+          --j;
+        }
+        out[j + 1] = v;
+      }
+      for (int i = 0; i < dm.G; ++i) a.g_new[(int64_t)c * dm.G + i] = i < m ? out[i] : -1;
+      a.gcnt_new[c] = m;
+    }
+    __syncthreads();
+  }
+}
+
+// g selection from the all-reduced dense C x C exchange table (multi-rank).
+__global__ void __launch_bounds__(kGupdThreads) k_gselect_dense(Dims dm, const long long* xc,
+                                                                int* g_new, int* gcnt_new) {
+  __shared__ KeyMin red[kGupdThreads / 32];
+  __shared__ int s_sel[64];
+  __shared__ int s_nsel;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nw = kGupdThreads / 32;
+  const int64_t CC = (int64_t)dm.C * dm.C;
+  for (int c = blockIdx.x; c < dm.C; c += gridDim.x) {
+    if (tid == 0) s_nsel = 0;
+    __syncthreads();
+    const long long* rc = xc + (int64_t)c * dm.C;
+    for (int r = 0; r < dm.G - 1; ++r) {
+      KeyMin best{INFINITY, 0x7fffffff};
+      for (int ct = tid; ct < dm.C; ct += kGupdThreads) {
+        const long long cnt = rc[ct];
+        if (cnt <= 0) continue;
+        bool taken = false;
+        for (int q = 0; q < s_nsel; ++q) taken |= (s_sel[q] == ct);
+        if (taken) continue;
+        const KeyMin k{from_fixed(rc[CC + ct], rc[2 * CC + ct]) / static_cast<double>(cnt), ct};
+        if (kless(k, best)) best = k;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        KeyMin oth{__shfl_xor_sync(kFull, best.v, o), __shfl_xor_sync(kFull, best.c, o)};
+        if (kless(oth, best)) best = oth;
+      }
+      if (lane == 0) red[warp] = best;
+      __syncthreads();
+      if (tid == 0) {
+        KeyMin b = red[0];
+        for (int w = 1; w < nw; ++w)
+          if (kless(red[w], b)) b = red[w];
+        if (b.c != 0x7fffffff) s_sel[s_nsel++] = b.c;
+      }
+      __syncthreads();
+      if (s_nsel <= r) break;
+    }
+    if (tid == 0) {
+      int out[64];
+      int m = 0;
+      out[m++] = c;
+      for (int q = 0; q < s_nsel; ++q) out[m++] = s_sel[q];
+      for (int i = 1; i < m; ++i) {
+        const int v = out[i];
+        int j = i - 1;
+        while (j >= 0 && out[j] > v) {
+          out[j + 1] = out[j];
+          --j;
+        }
+        out[j + 1] = v;
+      }
+      for (int i = 0; i < dm.G; ++i) g_new[(int64_t)c * dm.G + i] = i < m ? out[i] : -1;
+      gcnt_new[c] = m;
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------- K5: sufficient statistics
+// CTA per component a over its K-pairs (n, q) in ascending (n, j) order
+// (accumulate_point, mstep.cpp:47-67): mz = V_a (x - mu_a) (fp32 dot products),
+// then fp64: N += q; E += q [mz;1][mz;1]^T (+ N Sigma_z at the end);
+// Y[:, h] += q x zhat_h; sq += q x^2. Fixed order per component =>
+// deterministic; no atomics.
+constexpr int kStatsBatch = 32;
+constexpr int kStatsMaxH1 = 17;   // columns of Y per pass
+
+template <int NH1, int ND>
+__global__ void __launch_bounds__(kStatsThreads) k_stats(StatsArgs a, int col0) {
+  __shared__ double s_z[kStatsBatch][NH1];
+  __shared__ double s_q[kStatsBatch];
+  __shared__ int s_n[kStatsBatch];
+  const Dims dm = a.dm;
+  const int H = dm.H, H1 = H + 1, D = dm.D;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nw = kStatsThreads / 32;
+  const bool full_e = (col0 == 0) && (H1 <= NH1);
+  for (int c = blockIdx.x; c < dm.C; c += gridDim.x) {
+    const int r0 = a.off[c], r1 = a.off[c + 1];
+    double accY[ND][NH1];
+    double accS[ND];
+#pragma unroll
+    for (int k = 0; k < ND; ++k) {
+      accS[k] = 0.0;
+#pragma unroll
+      for (int h = 0; h < NH1; ++h) accY[k][h] = 0.0;
+    }
+    double accE[(NH1 * NH1 + kStatsThreads - 1) / kStatsThreads];
+#pragma unroll
+    for (int k = 0; k < (NH1 * NH1 + kStatsThreads - 1) / kStatsThreads; ++k) accE[k] = 0.0;
+    double accN = 0.0;
+    const float* Vc = a.V32 + (int64_t)c * D * H;
+    const float* mc = a.mu32 + (int64_t)c * D;
+    for (int b0 = r0; b0 < r1; b0 += kStatsBatch) {
+      const int nb = min(kStatsBatch, r1 - b0);
+      // (i) latent means mz = V (x - mu) for columns col0.. of the batch rows
+      for (int r = warp; r < nb; r += nw) {
+        const int e = a.ent[b0 + r];
+        const int n = e / dm.Cp;
+        const float* x = a.X + (int64_t)n * D;
+        float acc[NH1];
+#pragma unroll
+        for (int h = 0; h < NH1; ++h) acc[h] = 0.f;
+        for (int d = lane; d < D; d += 32) {
+          const float v = __ldg(x + d) - __ldg(mc + d);
+          const float* vr = Vc + (int64_t)d * H + col0;
+#pragma unroll
+          for (int h = 0; h < NH1; ++h)
+            if (col0 + h < H) acc[h] = fmaf(__ldg(vr + h), v, acc[h]);
+        }
+#pragma unroll
+        for (int h = 0; h < NH1; ++h) {
+          float v = acc[h];
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+          acc[h] = v;
+        }
+        if (lane == 0) {
+          s_n[r] = n;
+          s_q[r] = a.resp[e];
+        }
+#pragma unroll
+        for (int h = 0; h < NH1; ++h)
+          if (lane == h) {
+            const int hh = col0 + h;
+            s_z[r][h] = hh < H ? static_cast<double>(acc[h]) : (hh == H ? 1.0 : 0.0);
+          }
+      }
+      __syncthreads();
+      // (ii) Y / sq for the batch (fixed row order => deterministic)
+      for (int r = 0; r < nb; ++r) {
+        const double q = s_q[r];
+        const float* x = a.X + (int64_t)s_n[r] * D;
+#pragma unroll
+        for (int k = 0; k < ND; ++k) {
+          const int d = tid + k * kStatsThreads;
+          if (d < D) {
+            const double xd = static_cast<double>(__ldg(x + d));
+            const double qx = q * xd;
+#pragma unroll
+            for (int h = 0; h < NH1; ++h) accY[k][h] = fma(qx, s_z[r][h], accY[k][h]);
+            if (col0 == 0) accS[k] = fma(qx, xd, accS[k]);
+          }
+        }
+        if (full_e) {
+#pragma unroll
+          for (int k = 0; k < (NH1 * NH1 + kStatsThreads - 1) / kStatsThreads; ++k) {
+            const int idx = tid + k * kStatsThreads;
+            if (idx < H1 * H1) {
+              const int i = idx % H1, j = idx / H1;
+              accE[k] = fma(q * s_z[r][i], s_z[r][j], accE[k]);
+            }
+          }
+          if (tid == 0) accN += q;
+        }
+      }
+      __syncthreads();
+    }
+#pragma unroll
+    for (int k = 0; k < ND; ++k) {
+      const int d = tid + k * kStatsThreads;
+      if (d < D) {
+#pragma unroll
+        for (int h = 0; h < NH1; ++h)
+          if (col0 + h < H1) a.Y[((int64_t)c * H1 + col0 + h) * D + d] = accY[k][h];
+        if (col0 == 0) a.sq[(int64_t)c * D + d] = accS[k];
+      }
+    }
+    if (full_e) {
+      if (tid == 0) a.Nc[c] = accN;
+#pragma unroll
+      for (int k = 0; k < (NH1 * NH1 + kStatsThreads - 1) / kStatsThreads; ++k) {
+        const int idx = tid + k * kStatsThreads;
+        if (idx < H1 * H1) a.E[(int64_t)c * H1 * H1 + idx] = accE[k];
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// E for H > 16 (or any H): second pass computing E from mz recomputed per row.
+__global__ void __launch_bounds__(kStatsThreads) k_stats_E(StatsArgs a) {
+  extern __shared__ __align__(16) double s_zz[];  // [kStatsBatch][H1]
+  __shared__ double s_q[kStatsBatch];
+  const Dims dm = a.dm;
+  const int H = dm.H, H1 = H + 1, D = dm.D;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nw = kStatsThreads / 32;
+  for (int c = blockIdx.x; c < dm.C; c += gridDim.x) {
+    const int r0 = a.off[c], r1 = a.off[c + 1];
+    const float* Vc = a.V32 + (int64_t)c * D * H;
+    const float* mc = a.mu32 + (int64_t)c * D;
+    double accN = 0.0;
+    for (int idx0 = 0; idx0 < H1 * H1; idx0 += kStatsThreads * 9) {
+      double accE[9];
+#pragma unroll
+      for (int k = 0; k < 9; ++k) accE[k] = 0.0;
+      for (int b0 = r0; b0 < r1; b0 += kStatsBatch) {
+        const int nb = min(kStatsBatch, r1 - b0);
+        for (int r = warp; r < nb; r += nw) {
+          const int e = a.ent[b0 + r];
+          const int n = e / dm.Cp;
+          const float* x = a.X + (int64_t)n * D;
+          for (int h = 0; h < H; ++h) {
+            float v = 0.f;
+            for (int d = lane; d < D; d += 32) v = fmaf(__ldg(Vc + (int64_t)d * H + h), __ldg(x + d) - __ldg(mc + d), v);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+            if (lane == 0) s_zz[r * H1 + h] = v;
+          }
+          if (lane == 0) {
+            s_zz[r * H1 + H] = 1.0;
+            s_q[r] = a.resp[e];
+          }
+        }
+        __syncthreads();
+        for (int r = 0; r < nb; ++r) {
+          const double q = s_q[r];
+#pragma unroll
+          for (int k = 0; k < 9; ++k) {
+            const int idx = idx0 + tid + k * kStatsThreads;
+            if (idx < H1 * H1) {
+              const int i = idx % H1, j = idx / H1;
+              accE[k] = fma(q * s_zz[r * H1 + i], s_zz[r * H1 + j], accE[k]);
+            }
+          }
+          if (idx0 == 0 && tid == 0) accN += q;
+        }
+        __syncthreads();
+      }
+#pragma unroll
+      for (int k = 0; k < 9; ++k) {
+        const int idx = idx0 + tid + k * kStatsThreads;
+        if (idx < H1 * H1) a.E[(int64_t)c * H1 * H1 + idx] = accE[k];
+      }
+    }
+    if (tid == 0) a.Nc[c] = accN;
+    __syncthreads();
+  }
+}
+
+// E_tl += N_c * Sigma_z (the per-row q Sigma_z terms of mstep.cpp:56, summed)
+__global__ void k_stats_sz(Dims dm, const double* Nc, const double* Sz, double* E) {
+  const int H = dm.H, H1 = H + 1;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (int64_t)dm.C * H * H;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int c = static_cast<int>(i / (H * H));
+    const int rem = static_cast<int>(i - (int64_t)c * H * H);
+    const int col = rem / H, row = rem - col * H;
+    E[(int64_t)c * H1 * H1 + col * H1 + row] += Nc[c] * Sz[i];
+  }
+}
+
+// ---------------------------------------------------------------- small fp64 dense helpers (warp 0)
+// Cholesky of the n x n SPD matrix A (col-major in smem) into R (row-major
+// lower, smem). Returns via *ok (smem). Warp-cooperative over rows.
+__device__ void warp_cholesky(const double* A, double* R, int n, int* ok) {
+  const int lane = threadIdx.x & 31;
+  for (int i = lane; i < n * n; i += 32) R[i] = 0.0;
+  __syncwarp();
+  int good = 1;
+  for (int j = 0; j < n; ++j) {
+    double s = 0.0;
+    for (int k = lane; k < j; k += 32) s += R[j * n + k] * R[j * n + k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
+    const double dj = A[j * n + j] - s;
+    if (!(dj > 0.0) || !isfinite(dj)) {
+      good = 0;
+      break;
+    }
+    const double rjj = sqrt(dj);
+    if (lane == 0) R[j * n + j] = rjj;
+    for (int i = j + 1 + lane; i < n; i += 32) {
+      double t = A[j * n + i];
+      for (int k = 0; k < j; ++k) t -= R[i * n + k] * R[j * n + k];
+      R[i * n + j] = t / rjj;
+    }
+    __syncwarp();
+  }
+  if (lane == 0) *ok = good;
+}
+// In-place solve of (R R^T) x = b for one right-hand side held by one thread.
+__device__ __forceinline__ void chol_solve_thread(const double* R, double* b, int n) {
+  for (int i = 0; i < n; ++i) {
+    double s = b[i];
+    for (int k = 0; k < i; ++k) s -= R[i * n + k] * b[k];
+    b[i] = s / R[i * n + i];
+  }
+  for (int i = n - 1; i >= 0; --i) {
+    double s = b[i];
+    for (int k = i + 1; k < n; ++k) s -= R[k * n + i] * b[k];
+    b[i] = s / R[i * n + i];
+  }
+}
+
+__device__ __forceinline__ void set_status(unsigned long long* st, int c, int code) {
+  atomicMin(st, (static_cast<unsigned long long>(c) << 8) | static_cast<unsigned long long>(code));
+}
+
+constexpr int kMaxH1 = 65;
+
+// ---------------------------------------------------------------- K7: update_params
+// CTA per component (mstep.cpp:117-153): freeze on N_c == 0 exactly; else
+// pi = N_c/N, A^T = E^-1 Y^T (Cholesky; one trace-scaled jitter retry, else
+// SingularEc), Lambda / mu from A, sigma^2 = max(floor, (sq - sum_h Y.A)/N_c).
+__global__ void __launch_bounds__(128) k_update(UpdateArgs a) {
+  extern __shared__ __align__(16) double s_upd[];
+  __shared__ int s_ok, s_fin;
+  const Dims dm = a.dm;
+  const int H = dm.H, H1 = H + 1, D = dm.D;
+  double* sE = s_upd;
+  double* sR = s_upd + H1 * H1;
+  const int tid = threadIdx.x;
+  for (int c = blockIdx.x; c < dm.C; c += gridDim.x) {
+    const double nc = a.Nc[c];
+    if (nc == 0.0) {  // mstep.cpp:119-126
+      for (int d = tid; d < D; d += blockDim.x) {
+        a.mu[(int64_t)c * D + d] = a.mu_prev[(int64_t)c * D + d];
+        a.psi[(int64_t)c * D + d] = a.psi_prev[(int64_t)c * D + d];
+      }
+      for (int i = tid; i < D * H; i += blockDim.x) a.lam[(int64_t)c * D * H + i] = a.lam_prev[(int64_t)c * D * H + i];
+      if (tid == 0) a.pi[c] = 0.0;
+      continue;
+    }
+    for (int i = tid; i < H1 * H1; i += blockDim.x) sE[i] = a.E[(int64_t)c * H1 * H1 + i];
+    __syncthreads();
+    bool solved = false;
+    for (int attempt = 0; attempt < 2 && !solved; ++attempt) {
+      if (attempt == 1) {  // mstep.cpp:133-135
+        if (tid == 0) {
+          double tr = 0.0;
+          for (int i = 0; i < H1; ++i) tr += sE[i * H1 + i];
+          const double jit = 1e-10 * tr / H1;
+          for (int i = 0; i < H1; ++i) sE[i * H1 + i] += jit;
+        }
+        __syncthreads();
+      }
+      if (tid < 32) warp_cholesky(sE, sR, H1, &s_ok);
+      if (tid == 0) s_fin = 1;
+      __syncthreads();
+      if (!s_ok) continue;
+      // solve per d and write (provisionally) — all finite required
+      for (int d = tid; d < D; d += blockDim.x) {
+        double b[kMaxH1];
+        for (int h = 0; h < H1; ++h) b[h] = a.Y[((int64_t)c * H1 + h) * D + d];
+        chol_solve_thread(sR, b, H1);
+        bool fin = true;
+        for (int h = 0; h < H1; ++h) fin &= isfinite(b[h]);
+        if (!fin) s_fin = 0;
+        double fitted = 0.0;
+        for (int h = 0; h < H1; ++h) fitted += a.Y[((int64_t)c * H1 + h) * D + d] * b[h];
+        for (int h = 0; h < H; ++h) a.lam[(int64_t)c * D * H + (int64_t)h * D + d] = b[h];
+        a.mu[(int64_t)c * D + d] = b[H];
+        a.psi[(int64_t)c * D + d] = fmax((a.sq[(int64_t)c * D + d] - fitted) / nc, a.floor[d]);
+      }
+      __syncthreads();
+      solved = s_fin != 0;
+    }
+    if (tid == 0) {
+      if (!solved) set_status(a.status, c, 5 /* SingularEc */);
+      a.pi[c] = nc / static_cast<double>(dm.Ntot);
+    }
+    __syncthreads();
+  }
+}
+
+// pi /= sum(pi) (mstep.cpp:156-160); deterministic single-CTA reduction.
+__global__ void __launch_bounds__(1024) k_renorm(Dims dm, double* pi, unsigned long long* status) {
+  __shared__ double red[1024];
+  double s = 0.0;
+  for (int c = threadIdx.x; c < dm.C; c += 1024) s += pi[c];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = 512; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  const double live = red[0];
+  if (live <= 0.0) {
+    if (threadIdx.x == 0) set_status(status, 0xffffff, 5);
+    return;
+  }
+  for (int c = threadIdx.x; c < dm.C; c += 1024) pi[c] /= live;
+}
+
+// ---------------------------------------------------------------- K8: precompute
+// CTA per component (model.cpp:43-73) in fp64: L = I + Lambda^T Psi^-1 Lambda
+// (symmetrised), Cholesky L = R R^T (+1e-10 I retry, else CholeskyFailure),
+// Sigma_z = L^-1, log|Sigma| = 2 sum log R_hh + sum log psi, log pi; fp32
+// scoring rows W = U R^-T (| W^T v |^2 = (U^T v).(V v)), V32 = R^-T R^-1 U^T.
+__global__ void __launch_bounds__(128) k_precompute(PrecompArgs a) {
+  extern __shared__ __align__(16) double s_pre[];
+  __shared__ double red[128];
+  __shared__ int s_ok;
+  const Dims dm = a.dm;
+  const int H = dm.H, D = dm.D;
+  double* sL = s_pre;
+  double* sR = s_pre + H * H;
+  const int tid = threadIdx.x;
+  for (int c = blockIdx.x; c < dm.C; c += gridDim.x) {
+    const double* lam = a.lam + (int64_t)c * D * H;
+    const double* psi = a.psi + (int64_t)c * D;
+    // M = Lambda^T Psi^-1 Lambda (+I), symmetrised (model.cpp:51-53)
+    for (int p = tid; p < H * H; p += blockDim.x) {
+      const int i = p % H, j = p / H;
+      if (i > j) continue;
+      double s = 0.0;
+      for (int d = 0; d < D; ++d) s += lam[(int64_t)i * D + d] * (lam[(int64_t)j * D + d] / psi[d]);
+      sL[j * H + i] = s;
+    }
+    __syncthreads();
+    for (int p = tid; p < H * H; p += blockDim.x) {
+      const int i = p % H, j = p / H;
+      if (i <= j) continue;
+      sL[j * H + i] = sL[i * H + j];  // lower from upper
+    }
+    __syncthreads();
+    for (int p = tid; p < H * H; p += blockDim.x) {
+      const int i = p % H, j = p / H;
+      // (M + I) symmetrised: 0.5 (M_ij + M_ji) with exact symmetry already
+      double v = sL[p] + (i == j ? 1.0 : 0.0);
+      a.Lmat[(int64_t)c * H * H + p] = v;
+    }
+    __syncthreads();
+    for (int p = tid; p < H * H; p += blockDim.x) sL[p] = a.Lmat[(int64_t)c * H * H + p];
+    __syncthreads();
+    if (tid < 32) warp_cholesky(sL, sR, H, &s_ok);
+    __syncthreads();
+    if (!s_ok) {  // model.cpp:55-63
+      if (tid == 0)
+        for (int i = 0; i < H; ++i) sL[i * H + i] += 1e-10;
+      __syncthreads();
+      if (tid < 32) warp_cholesky(sL, sR, H, &s_ok);
+      __syncthreads();
+      if (!s_ok) {
+        if (tid == 0) set_status(a.status, c, 2 /* CholeskyFailure */);
+        continue;
+      }
+      for (int p = tid; p < H * H; p += blockDim.x) a.Lmat[(int64_t)c * H * H + p] = sL[p];
+    }
+    for (int p = tid; p < H * H; p += blockDim.x) a.R[(int64_t)c * H * H + p] = sR[p];
+    // Sigma_z = L^-1 (model.cpp:65)
+    for (int j = tid; j < H; j += blockDim.x) {
+      double b[kMaxH1];
+      for (int h = 0; h < H; ++h) b[h] = h == j ? 1.0 : 0.0;
+      chol_solve_thread(sR, b, H);
+      for (int h = 0; h < H; ++h) a.Sz[(int64_t)c * H * H + j * H + h] = b[h];
+    }
+    // log|Sigma| (model.cpp:67-70): deterministic block reduction of sum log psi
+    double s = 0.0;
+    for (int d = tid; d < D; d += blockDim.x) s += log(psi[d]);
+    red[tid] = s;
+    __syncthreads();
+    for (int o = 64; o > 0; o >>= 1) {
+      if (tid < o) red[tid] += red[tid + o];
+      __syncthreads();
+    }
+    if (tid == 0) {
+      double ld = 0.0;
+      for (int h = 0; h < H; ++h) ld += log(sR[h * H + h]);
+      const double logdet = 2.0 * ld + red[0];
+      const double p = a.pi[c];
+      const double lp = p > 0.0 ? log(p) : -INFINITY;  // model.cpp:71
+      a.logdet[c] = logdet;
+      a.logpi[c] = lp;
+      a.kconst[c] = lp - 0.5 * (D * kLog2Pi + logdet);
+    }
+    // fp32 scoring rows
+    const int HP = a.L.HP, Hc = a.L.Hc;
+    for (int d = tid; d < D; d += blockDim.x) {
+      double u[kMaxH1];
+      const double ip = 1.0 / psi[d];
+      for (int h = 0; h < H; ++h) u[h] = lam[(int64_t)h * D + d] * ip;  // U = Psi^-1 Lambda
+      // forward: w = R^-1 u
+      for (int i = 0; i < H; ++i) {
+        double t = u[i];
+        for (int k = 0; k < i; ++k) t -= sR[i * H + k] * u[k];
+        u[i] = t / sR[i * H + i];
+      }
+      float* row = a.P + ((int64_t)c * D + d) * HP;
+      for (int h = 0; h < Hc; ++h) row[h] = h < H ? static_cast<float>(u[h]) : 0.f;
+      row[Hc] = static_cast<float>(a.mu[(int64_t)c * D + d]);
+      row[Hc + 1] = static_cast<float>(ip);
+      row[Hc + 2] = 0.f;
+      row[Hc + 3] = 0.f;
+      // backward: v = R^-T w  => V column d
+      for (int i = H - 1; i >= 0; --i) {
+        double t = u[i];
+        for (int k = i + 1; k < H; ++k) t -= sR[k * H + i] * u[k];
+        u[i] = t / sR[i * H + i];
+      }
+      for (int h = 0; h < H; ++h) a.V32[((int64_t)c * D + d) * H + h] = static_cast<float>(u[h]);
+      a.mu32[(int64_t)c * D + d] = static_cast<float>(a.mu[(int64_t)c * D + d]);
+    }
+    __syncthreads();
+  }
+}
+
+// Full fp64 U (D x H col-major) and V (H x D col-major) for cache downloads.
+__global__ void __launch_bounds__(128) k_caches_full(Dims dm, const double* lam, const double* psi,
+                                                    const double* R, double* U, double* V,
+                                                    double* ipsi) {
+  const int H = dm.H, D = dm.D;
+  for (int c = blockIdx.x; c < dm.C; c += gridDim.x) {
+    const double* Rc = R + (int64_t)c * H * H;
+    for (int d = threadIdx.x; d < D; d += blockDim.x) {
+      double u[kMaxH1];
+      const double ip = 1.0 / psi[(int64_t)c * D + d];
+      ipsi[(int64_t)c * D + d] = ip;
+      for (int h = 0; h < H; ++h) {
+        u[h] = ip * lam[(int64_t)c * D * H + (int64_t)h * D + d];
+        U[(int64_t)c * D * H + (int64_t)h * D + d] = u[h];
+      }
+      chol_solve_thread(Rc, u, H);
+      for (int h = 0; h < H; ++h) V[(int64_t)c * D * H + (int64_t)d * H + h] = u[h];
+    }
+  }
+}
+
+// ---------------------------------------------------------------- reductions
+__global__ void k_lse_rows(const float* LJK, int64_t N, int Cp, double* lse) {
+  for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < N; n += (int64_t)gridDim.x * blockDim.x) {
+    double mx = -INFINITY;
+    for (int j = 0; j < Cp; ++j) mx = fmax(mx, static_cast<double>(LJK[n * Cp + j]));
+    double l = mx;
+    if (isfinite(mx)) {
+      double s = 0.0;
+      for (int j = 0; j < Cp; ++j) s += exp(static_cast<double>(LJK[n * Cp + j]) - mx);
+      l = mx + log(s);
+    }
+    lse[n] = l;
+  }
+}
+
+constexpr int kSumBlocks = 296;
+// Two-stage deterministic sum: fixed contiguous segments per CTA, fixed tree.
+__global__ void __launch_bounds__(256) k_sum_stage1(const double* v, int64_t n, double* partials) {
+  __shared__ double red[256];
+  const int64_t seg = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t b = blockIdx.x * seg, e = (n < b + seg) ? n : b + seg;
+  double s = 0.0;
+  for (int64_t i = b + threadIdx.x; i < e; i += 256) s += v[i];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partials[blockIdx.x] = red[0];
+}
+__global__ void __launch_bounds__(32) k_sum_stage2(const double* partials, int m, double* out) {
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < m; ++i) s += partials[i];
+    *out = s;
+  }
+}
+__global__ void k_sum_i32(const int* v, int64_t n, unsigned long long* out) {
+  unsigned long long s = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    s += static_cast<unsigned long long>(v[i]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(out, s);
+}
+__global__ void k_count_empty(const double* pi, int C, int* out) {
+  int s = 0;
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < C; c += gridDim.x * blockDim.x) s += pi[c] == 0.0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(out, s);
+}
+__global__ void k_logpi(const double* pi, int C, double* logpi) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < C; c += gridDim.x * blockDim.x)
+    logpi[c] = pi[c] > 0.0 ? log(pi[c]) : -INFINITY;
+}
+
+int grid_for(int64_t n, int threads, int cap) {
+  int64_t g = (n + threads - 1) / threads;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return static_cast<int>(g);
+}
+
+}  // namespace
+
+int sm_count() {
+  static int cached = 0;
+  if (cached == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&cached, cudaDevAttrMultiProcessorCount, dev);
+    if (cached <= 0) cached = 148;
+  }
+  return cached;
+}
+
+cudaError_t launch_iota(int* v, int64_t n, cudaStream_t s) {
+  k_iota<<<grid_for(n, 256, 4096), 256, 0, s>>>(v, n);
+  return cudaGetLastError();
+}
+cudaError_t launch_fill_i32(int* v, int64_t n, int value, cudaStream_t s) {
+  k_fill_i32<<<grid_for(n, 256, 4096), 256, 0, s>>>(v, n, value);
+  return cudaGetLastError();
+}
+cudaError_t launch_keys_from_i32(const int* src, unsigned* keys, int64_t n, cudaStream_t s) {
+  k_keys_from_i32<<<grid_for(n, 256, 4096), 256, 0, s>>>(src, keys, n);
+  return cudaGetLastError();
+}
+cudaError_t launch_hist(const unsigned* keys, int64_t n, int C, int* cnt, cudaStream_t s) {
+  k_hist<<<grid_for(n, 256, 4096), 256, 0, s>>>(keys, n, C, cnt);
+  return cudaGetLastError();
+}
+cudaError_t launch_chunks(const int* cnt, int C, int rows, int* chunks, cudaStream_t s) {
+  k_chunks<<<grid_for(C + 1, 256, 4096), 256, 0, s>>>(cnt, C, rows, chunks);
+  return cudaGetLastError();
+}
+cudaError_t launch_extra(const Dims& dm, const int* K, const int* g, const int* gcnt, uint64_t seed,
+                         uint64_t it, int* rx, unsigned* rkey, cudaStream_t s) {
+  k_extra<<<grid_for(dm.N, 256, 8192), 256, 0, s>>>(dm, K, g, gcnt, seed, it, rx, rkey);
+  return cudaGetLastError();
+}
+
+template <int MODE>
+static cudaError_t launch_score_mode(const ScoreArgs& a, int grid, cudaStream_t s) {
+  const size_t smem = static_cast<size_t>(a.dm.D) * kXsStride * sizeof(float);
+  auto go = [&](auto kern) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    kern<<<grid, kScoreThreads, smem, s>>>(a);
+  };
+  if (a.L.hc == 4) go(k_score<MODE, 4>);
+  else if (a.L.hc == 8) go(k_score<MODE, 8>);
+  else go(k_score<MODE, 16>);
+  return cudaGetLastError();
+}
+cudaError_t launch_score(int mode, const ScoreArgs& a, int grid, cudaStream_t s) {
+  if (mode == kModeAnchor) return launch_score_mode<kModeAnchor>(a, grid, s);
+  if (mode == kModeExtra) return launch_score_mode<kModeExtra>(a, grid, s);
+  return launch_score_mode<kModeTruncF>(a, grid, s);
+}
+
+cudaError_t launch_select(const SelectArgs& a, cudaStream_t s) {
+  const int ns = (a.dm.SL + 31) / 32;
+  const int grid = grid_for(a.dm.N * 32, 256, sm_count() * 16);
+  switch (ns) {
+    case 1: k_select<1><<<grid, 256, 0, s>>>(a); break;
+    case 2: k_select<2><<<grid, 256, 0, s>>>(a); break;
+    case 3: k_select<3><<<grid, 256, 0, s>>>(a); break;
+    case 4: k_select<4><<<grid, 256, 0, s>>>(a); break;
+    case 5: k_select<5><<<grid, 256, 0, s>>>(a); break;
+    case 6: k_select<6><<<grid, 256, 0, s>>>(a); break;
+    case 7: k_select<7><<<grid, 256, 0, s>>>(a); break;
+    case 8: k_select<8><<<grid, 256, 0, s>>>(a); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gupdate(const GupdArgs& a, int grid, cudaStream_t s) {
+  const size_t smem = static_cast<size_t>(kGupdCap) * (2 * sizeof(long long) + 2 * sizeof(int));
+  cudaFuncSetAttribute(k_gupdate, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  k_gupdate<<<grid, kGupdThreads, smem, s>>>(a);
+  return cudaGetLastError();
+}
+cudaError_t launch_gselect_dense(const Dims& dm, const long long* xc, int* g_new, int* gcnt_new,
+                                 cudaStream_t s) {
+  k_gselect_dense<<<min(dm.C, sm_count() * 8), kGupdThreads, 0, s>>>(dm, xc, g_new, gcnt_new);
+  return cudaGetLastError();
+}
+
+template <int NH1>
+static void stats_pass(const StatsArgs& a, int grid, int col0, cudaStream_t s) {
+  const int D = a.dm.D;
+  if (D <= kStatsThreads) k_stats<NH1, 1><<<grid, kStatsThreads, 0, s>>>(a, col0);
+  else if (D <= 2 * kStatsThreads) k_stats<NH1, 2><<<grid, kStatsThreads, 0, s>>>(a, col0);
+  else k_stats<NH1, 4><<<grid, kStatsThreads, 0, s>>>(a, col0);
+}
+cudaError_t launch_stats(const StatsArgs& a, cudaStream_t s) {
+  if (a.dm.D > 4 * kStatsThreads) return cudaErrorInvalidValue;
+  const int grid = min(a.dm.C, sm_count() * 2);
+  const int H1 = a.dm.H + 1;
+  for (int col0 = 0; col0 < H1; col0 += kStatsMaxH1) {
+    if (H1 <= 5) stats_pass<5>(a, grid, col0, s);
+    else if (H1 <= 9) stats_pass<9>(a, grid, col0, s);
+    else stats_pass<kStatsMaxH1>(a, grid, col0, s);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  if (H1 > kStatsMaxH1) {
+    const size_t smem = static_cast<size_t>(kStatsBatch) * H1 * sizeof(double);
+    cudaFuncSetAttribute(k_stats_E, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    k_stats_E<<<grid, kStatsThreads, smem, s>>>(a);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  k_stats_sz<<<grid_for((int64_t)a.dm.C * a.dm.H * a.dm.H, 256, 4096), 256, 0, s>>>(a.dm, a.Nc, a.Sz, a.E);
+  return cudaGetLastError();
+}
+cudaError_t launch_update(const UpdateArgs& a, cudaStream_t s) {
+  const int H1 = a.dm.H + 1;
+  const size_t smem = 2 * static_cast<size_t>(H1) * H1 * sizeof(double);
+  cudaFuncSetAttribute(k_update, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  k_update<<<min(a.dm.C, sm_count() * 8), 128, smem, s>>>(a);
+  return cudaGetLastError();
+}
+cudaError_t launch_renorm(const Dims& dm, double* pi, unsigned long long* status, cudaStream_t s) {
+  k_renorm<<<1, 1024, 0, s>>>(dm, pi, status);
+  return cudaGetLastError();
+}
+cudaError_t launch_precompute(const PrecompArgs& a, cudaStream_t s) {
+  const size_t smem = 2 * static_cast<size_t>(a.dm.H) * a.dm.H * sizeof(double);
+  cudaFuncSetAttribute(k_precompute, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  k_precompute<<<min(a.dm.C, sm_count() * 8), 128, smem, s>>>(a);
+  return cudaGetLastError();
+}
+cudaError_t launch_caches_full(const Dims& dm, const double* lam, const double* psi, const double* R,
+                               double* U, double* V, double* ipsi, cudaStream_t s) {
+  k_caches_full<<<min(dm.C, sm_count() * 8), 128, 0, s>>>(dm, lam, psi, R, U, V, ipsi);
+  return cudaGetLastError();
+}
+cudaError_t launch_lse_rows(const float* LJK, int64_t N, int Cp, double* lse, cudaStream_t s) {
+  k_lse_rows<<<grid_for(N, 256, 8192), 256, 0, s>>>(LJK, N, Cp, lse);
+  return cudaGetLastError();
+}
+cudaError_t launch_sum_f64(const double* v, int64_t n, double* partials, double* out, cudaStream_t s) {
+  k_sum_stage1<<<kSumBlocks, 256, 0, s>>>(v, n, partials);
+  k_sum_stage2<<<1, 32, 0, s>>>(partials, kSumBlocks, out);
+  return cudaGetLastError();
+}
+cudaError_t launch_sum_i32(const int* v, int64_t n, unsigned long long* out, cudaStream_t s) {
+  cudaMemsetAsync(out, 0, sizeof(unsigned long long), s);
+  k_sum_i32<<<grid_for(n, 256, 1024), 256, 0, s>>>(v, n, out);
+  return cudaGetLastError();
+}
+cudaError_t launch_count_empty(const double* pi, int C, int* out, cudaStream_t s) {
+  cudaMemsetAsync(out, 0, sizeof(int), s);
+  k_count_empty<<<grid_for(C, 256, 1024), 256, 0, s>>>(pi, C, out);
+  return cudaGetLastError();
+}
+cudaError_t launch_logpi(const double* pi, int C, double* logpi, cudaStream_t s) {
+  k_logpi<<<grid_for(C, 256, 1024), 256, 0, s>>>(pi, C, logpi);
+  return cudaGetLastError();
+}
+
+}  // namespace vmfa_b200

@@ -1,0 +1,197 @@
+// vmfa_kernels.cuh — device kernels of the v-MFA hot path (sm_100a) and their
+// argument blocks. See DESIGN.md for the data layout in HBM and the roofline of
+// each kernel. Reference correspondences:
+//   k_extra        uniform_component + the union test of
+//                  build_search_space_into (rng.hpp:91-98, estep.cpp:83-101)
+//   k_score_*      log_joint over anchor blocks (model.cpp:81-95)
+//   k_select       update_k_into + hard_partition label + block 4
+//                  (estep.cpp:103-122, :144-173, :314-335)
+//   k_gupdate      block 3 + update_g (estep.cpp:286-312, :204-220)
+//   k_stats        accumulate_point / accumulate_suffstats (mstep.cpp:47-101)
+//   k_update       update_params (mstep.cpp:103-162)
+//   k_precompute   precompute_component (model.cpp:43-73)
+#pragma once
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+namespace vmfa_b200 {
+
+constexpr int kScoreRows = 64;      // rows (points) per scoring item
+constexpr int kScoreThreads = 128;  // 4 warps; each warp scores one component x 64 rows
+constexpr int kXsStride = kScoreRows + 2;  // transposed x tile stride (floats)
+constexpr int kStatsThreads = 512;
+constexpr int kGupdCap = 8192;      // smem hash capacity of the block-3 accumulator (24 B per entry)
+constexpr int kGupdThreads = 256;
+
+// Packed fp32 scoring parameters of one component (precompute output):
+// per dimension d a row of HP floats: [W_0 .. W_{Hc-1}, mu_d, 1/psi_d, 0, 0]
+// where W = U R^{-T} (so (U^T v).(V v) = |W^T v|^2), Hc = H rounded up to the
+// h-chunk. HP = Hc + 4 keeps every row 16-byte aligned.
+struct ScoreLayout {
+  int hc;   // h-chunk (4, 8 or 16)
+  int Hc;   // H rounded up to a multiple of hc
+  int HP;   // floats per dimension row
+};
+inline ScoreLayout score_layout(int H) {
+  ScoreLayout L;
+  L.hc = H <= 4 ? 4 : (H <= 8 ? 8 : 16);
+  L.Hc = (H + L.hc - 1) / L.hc * L.hc;
+  L.HP = L.Hc + 4;
+  return L;
+}
+
+struct Dims {
+  int C, D, H, Cp, G;
+  int SL;      // candidate slots per point = Cp*G + 1
+  int stride;  // retained stride = min(Cp*G+1, C)
+  int64_t N;   // rows of this context
+  int64_t n0;  // global row offset
+  int64_t Ntot;
+};
+
+// scoring modes
+enum ScoreMode : int { kModeAnchor = 0, kModeExtra = 1, kModeTruncF = 2 };
+
+struct ScoreArgs {
+  Dims dm;
+  ScoreLayout L;
+  const float* X;
+  const float* P;         // packed params, C x D x HP
+  const double* kconst;   // log pi - 0.5 (D log 2pi + log|Sigma|), -inf if frozen
+  const int* off;         // CSR offsets by component (C+1)
+  const int* ent;         // CSR entries (flat K index n*Cp+j, or row n for extras)
+  const int* itemoff;     // exclusive scan of per-component chunk counts (C+1)
+  const int* g;           // neighbourhoods C x G
+  const int* gcnt;
+  float* out;             // LJ slots (N x SL) or LJK (N x Cp)
+};
+
+struct SelectArgs {
+  Dims dm;
+  int* K;                 // in: old K (search space); out: new K
+  const int* g;
+  const int* gcnt;
+  const int* rx;          // extra candidate per row
+  const float* LJ;        // N x SL slots
+  int* labels;
+  float* lablj;           // log-joint of the label
+  double* resp;           // N x Cp
+  int* ret_cnt;
+  int* ret_idx;           // N x stride
+  float* ret_lj;          // N x stride
+  double* lse;            // per-row log-sum-exp over new K (block-4 F terms)
+  int* status;            // [0]: InsufficientCandidates flag
+};
+
+struct GupdArgs {
+  Dims dm;
+  int mode;               // 0 kl, 1 euclid
+  const int* part_off;    // partition by label (C+1)
+  const int* part_ent;
+  const int* ret_cnt;
+  const int* ret_idx;
+  const float* ret_lj;
+  const float* lablj;
+  const double* logpi;    // fp64 log pi (-inf when pi == 0)
+  int* g_new;
+  int* gcnt_new;
+  // global fallback tables (per CTA slice of C entries) for components whose
+  // key bound exceeds the shared-memory hash
+  long long* gt_cnt;
+  long long* gt_hi;
+  long long* gt_lo;
+  // exchange (multi-rank) / dump modes
+  int exchange;           // 1: write dense C x C rows to xc_* instead of selecting
+  long long* xc;          // 3*C*C int64: [cnt | hi | lo]
+  int dump;               // 1: append (c, ct, cnt, hi, lo) rows to dump arrays
+  int* dump_c;
+  int* dump_ct;
+  long long* dump_cnt;
+  long long* dump_hi;
+  long long* dump_lo;
+  unsigned long long* dump_n;
+  long long dump_cap;
+};
+
+struct StatsArgs {
+  Dims dm;
+  const float* X;
+  const double* resp;     // N x Cp
+  const int* off;         // CSR by component over new K
+  const int* ent;
+  const float* V32;       // C x D x H  (V^T rows: mz = V (x - mu))
+  const float* mu32;      // C x D
+  const double* Sz;       // C x H x H
+  double* Nc;
+  double* E;              // C x (H+1)^2 col-major
+  double* Y;              // C x (H+1) x D  (D x (H+1) col-major)
+  double* sq;             // C x D
+};
+
+struct UpdateArgs {
+  Dims dm;
+  const double* Nc;
+  const double* E;
+  const double* Y;
+  const double* sq;
+  const double* floor;
+  const double* mu_prev;
+  const double* lam_prev;
+  const double* psi_prev;
+  double* pi;
+  double* mu;
+  double* lam;
+  double* psi;
+  unsigned long long* status;  // min over (c << 8 | code)
+};
+
+struct PrecompArgs {
+  Dims dm;
+  ScoreLayout L;
+  const double* pi;
+  const double* mu;
+  const double* lam;
+  const double* psi;
+  double* Lmat;           // C x H x H
+  double* R;              // C x H x H (row-major lower Cholesky factor of Lmat)
+  double* Sz;             // C x H x H
+  double* logdet;
+  double* logpi;
+  double* kconst;
+  float* P;               // packed scoring params
+  float* V32;             // C x D x H
+  float* mu32;            // C x D
+  unsigned long long* status;
+};
+
+// launchers (return cudaError_t of the launch)
+cudaError_t launch_iota(int* v, int64_t n, cudaStream_t s);
+cudaError_t launch_fill_i32(int* v, int64_t n, int value, cudaStream_t s);
+cudaError_t launch_keys_from_i32(const int* src, unsigned* keys, int64_t n, cudaStream_t s);
+cudaError_t launch_hist(const unsigned* keys, int64_t n, int C, int* cnt, cudaStream_t s);
+cudaError_t launch_chunks(const int* cnt, int C, int rows, int* chunks, cudaStream_t s);
+cudaError_t launch_extra(const Dims& dm, const int* K, const int* g, const int* gcnt,
+                         uint64_t seed, uint64_t it, int* rx, unsigned* rkey, cudaStream_t s);
+cudaError_t launch_score(int mode, const ScoreArgs& a, int grid, cudaStream_t s);
+cudaError_t launch_select(const SelectArgs& a, cudaStream_t s);
+cudaError_t launch_gupdate(const GupdArgs& a, int grid, cudaStream_t s);
+cudaError_t launch_gselect_dense(const Dims& dm, const long long* xc, int* g_new, int* gcnt_new,
+                                 cudaStream_t s);
+cudaError_t launch_stats(const StatsArgs& a, cudaStream_t s);
+cudaError_t launch_update(const UpdateArgs& a, cudaStream_t s);
+cudaError_t launch_renorm(const Dims& dm, double* pi, unsigned long long* status, cudaStream_t s);
+cudaError_t launch_precompute(const PrecompArgs& a, cudaStream_t s);
+cudaError_t launch_caches_full(const Dims& dm, const double* lam, const double* psi,
+                               const double* R, double* U, double* V, double* ipsi,
+                               cudaStream_t s);
+cudaError_t launch_lse_rows(const float* LJK, int64_t N, int Cp, double* lse, cudaStream_t s);
+cudaError_t launch_sum_f64(const double* v, int64_t n, double* partials, double* out,
+                           cudaStream_t s);
+cudaError_t launch_sum_i32(const int* v, int64_t n, unsigned long long* out, cudaStream_t s);
+cudaError_t launch_count_empty(const double* pi, int C, int* out, cudaStream_t s);
+cudaError_t launch_logpi(const double* pi, int C, double* logpi, cudaStream_t s);
+
+int sm_count();
+
+}  // namespace vmfa_b200

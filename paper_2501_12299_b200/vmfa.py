@@ -1,0 +1,376 @@
+"""Python mirror of the reference's v-MFA API over libvmfa_b200.so.
+
+Names and semantics follow /root/reference/proj/include/vmfa/:
+  MfaParams (model.hpp:19-32)   -> Params
+  VarState  (estep.hpp:17-29)   -> State
+  SuffStats (mstep.hpp:14-22)   -> Stats
+  variational_e_step (estep.hpp:125-130), accumulate_suffstats
+  (mstep.hpp:27-31), update_params (mstep.hpp:39-41), precompute_all
+  (model.hpp:76-78), truncated_free_energy (model.hpp:116-119)
+  -> methods of Session, which owns one GPU context (one shard of the rows).
+train_fixed mirrors train_vmfa's loop (trainer.cpp:111-186) with fixed counts.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .abi import IterReport, SynthSpec, VmfaError, check, lib, ptr
+
+KL, EUCLID = 0, 1  # DistanceMode (estep.hpp:12)
+
+
+@dataclass
+class Params:
+    """MfaParams: pi (C,), mu (C,D), lam (C,H,D) = per-component D x H
+    column-major blocks, psi (C,D) = the reference's ``dnoise``."""
+    pi: np.ndarray
+    mu: np.ndarray
+    lam: np.ndarray
+    psi: np.ndarray
+
+    @property
+    def C(self):
+        return self.mu.shape[0]
+
+    @property
+    def D(self):
+        return self.mu.shape[1]
+
+    @property
+    def H(self):
+        return self.lam.shape[1]
+
+    def copy(self):
+        return Params(self.pi.copy(), self.mu.copy(), self.lam.copy(), self.psi.copy())
+
+
+@dataclass
+class State:
+    """VarState: K (N,C') sorted rows, g (C,G) sorted rows -1 padded, g_count (C,)."""
+    K: np.ndarray
+    g: np.ndarray
+    g_count: np.ndarray
+    labels: np.ndarray = field(default=None)
+
+    def copy(self):
+        return State(self.K.copy(), self.g.copy(), self.g_count.copy(),
+                     None if self.labels is None else self.labels.copy())
+
+
+@dataclass
+class Stats:
+    Nc: np.ndarray
+    Y: np.ndarray   # (C,H+1,D)
+    E: np.ndarray   # (C,H+1,H+1)
+    sq: np.ndarray  # (C,D)
+
+
+def _c(a, dt):
+    return np.ascontiguousarray(a, dtype=dt)
+
+
+def device_available() -> bool:
+    return bool(lib().vmfa_device_available())
+
+
+class Session:
+    """One device context: rows [n_offset, n_offset + len(X)) of an n_total-row
+    dataset, replicated parameters/caches, and the shard's variational state."""
+
+    def __init__(self, C_: int, D: int, H: int, Cprime: int, G: int, X: np.ndarray,
+                 n_offset: int = 0, n_total: int | None = None, device: int = 0,
+                 stream: int | None = None):
+        X = _c(X, np.float32)
+        assert X.ndim == 2 and X.shape[1] == D
+        self.C, self.D, self.H, self.Cp, self.G = C_, D, H, Cprime, G
+        self.N = X.shape[0]
+        self.n_offset = n_offset
+        self.n_total = self.N + n_offset if n_total is None else n_total
+        self.stride = min(Cprime * G + 1, C_)
+        h = C.c_void_p()
+        check(lib().vmfa_ctx_create(C.byref(h), device, C_, D, H, Cprime, G, self.N, n_offset,
+                                    self.n_total, stream))
+        self._h = h
+        check(lib().vmfa_upload_data(h, ptr(X), 0, self.N))
+
+    # -- lifetime
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().vmfa_ctx_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    @property
+    def handle(self):
+        return self._h
+
+    def device_bytes(self) -> int:
+        b = C.c_size_t()
+        check(lib().vmfa_ctx_device_bytes(self._h, C.byref(b)))
+        return b.value
+
+    def upload_data(self, X: np.ndarray, row_begin: int = 0):
+        X = _c(X, np.float32)
+        check(lib().vmfa_upload_data(self._h, ptr(X), row_begin, X.shape[0]))
+
+    # -- params / caches
+    def set_floor(self, floor):
+        check(lib().vmfa_set_floor(self._h, ptr(_c(floor, np.float64))))
+
+    def upload_params(self, p: Params):
+        check(lib().vmfa_upload_params(self._h, ptr(_c(p.pi, np.float64)), ptr(_c(p.mu, np.float64)),
+                                       ptr(_c(p.lam, np.float64)), ptr(_c(p.psi, np.float64))))
+
+    def download_params(self) -> Params:
+        p = Params(np.zeros(self.C), np.zeros((self.C, self.D)), np.zeros((self.C, self.H, self.D)),
+                   np.zeros((self.C, self.D)))
+        check(lib().vmfa_download_params(self._h, ptr(p.pi), ptr(p.mu), ptr(p.lam), ptr(p.psi)))
+        return p
+
+    def precompute(self):
+        bad = C.c_int(-1)
+        check(lib().vmfa_precompute(self._h, C.byref(bad)))
+
+    def download_caches(self):
+        C_, D, H = self.C, self.D, self.H
+        out = dict(U=np.zeros((C_, H, D)), Lmat=np.zeros((C_, H, H)), V=np.zeros((C_, D, H)),
+                   Sz=np.zeros((C_, H, H)), inv_psi=np.zeros((C_, D)), logdet=np.zeros(C_),
+                   log_pi=np.zeros(C_))
+        check(lib().vmfa_download_caches(self._h, ptr(out["U"]), ptr(out["Lmat"]), ptr(out["V"]),
+                                         ptr(out["Sz"]), ptr(out["inv_psi"]), ptr(out["logdet"]),
+                                         ptr(out["log_pi"])))
+        return out
+
+    # -- state
+    def upload_state(self, st: State):
+        check(lib().vmfa_upload_state(self._h, ptr(_c(st.K, np.int32)), ptr(_c(st.g, np.int32)),
+                                      ptr(_c(st.g_count, np.int32))))
+
+    def download_state(self) -> State:
+        st = State(np.zeros((self.N, self.Cp), np.int32), np.zeros((self.C, self.G), np.int32),
+                   np.zeros(self.C, np.int32), np.zeros(self.N, np.int32))
+        check(lib().vmfa_download_state(self._h, ptr(st.K), ptr(st.g), ptr(st.g_count),
+                                        ptr(st.labels)))
+        return st
+
+    # -- hot path
+    def variational_e_step(self, seed: int, iteration: int, mode: int = KL):
+        F = C.c_double()
+        J = C.c_uint64()
+        check(lib().vmfa_estep(self._h, seed, iteration, mode, C.byref(F), C.byref(J)))
+        return F.value, J.value
+
+    def download_estep(self):
+        N, S, Cp = self.N, self.stride, self.Cp
+        cnt = np.zeros(N, np.int32)
+        idx = np.zeros((N, S), np.int32)
+        lj = np.zeros((N, S), np.float64)
+        resp = np.zeros((N, Cp), np.float64)
+        check(lib().vmfa_download_estep(self._h, ptr(cnt), ptr(idx), ptr(lj), ptr(resp)))
+        return cnt, idx, lj, resp
+
+    def arm_distance_dump(self):
+        n = C.c_int64()
+        check(lib().vmfa_download_distances(self._h, 0, None, None, None, None, C.byref(n)))
+
+    def download_distances(self):
+        n = C.c_int64()
+        check(lib().vmfa_download_distances(self._h, 0, None, None, None, None, C.byref(n)))
+        m = n.value
+        c = np.zeros(m, np.int32)
+        ct = np.zeros(m, np.int32)
+        s = np.zeros(m, np.float64)
+        k = np.zeros(m, np.int64)
+        if m:
+            check(lib().vmfa_download_distances(self._h, m, ptr(c), ptr(ct), ptr(s), ptr(k),
+                                                C.byref(n)))
+        return c, ct, s, k
+
+    def accumulate_suffstats(self):
+        check(lib().vmfa_accumulate_suffstats(self._h))
+
+    def download_suffstats(self) -> Stats:
+        C_, D, H1 = self.C, self.D, self.H + 1
+        s = Stats(np.zeros(C_), np.zeros((C_, H1, D)), np.zeros((C_, H1, H1)), np.zeros((C_, D)))
+        check(lib().vmfa_download_suffstats(self._h, ptr(s.Nc), ptr(s.Y), ptr(s.E), ptr(s.sq)))
+        return s
+
+    def upload_suffstats(self, s: Stats):
+        check(lib().vmfa_upload_suffstats(self._h, ptr(_c(s.Nc, np.float64)), ptr(_c(s.Y, np.float64)),
+                                          ptr(_c(s.E, np.float64)), ptr(_c(s.sq, np.float64))))
+
+    def update_params(self):
+        bad = C.c_int(-1)
+        check(lib().vmfa_update_params(self._h, C.byref(bad)))
+
+    def truncated_free_energy(self) -> float:
+        F = C.c_double()
+        check(lib().vmfa_truncated_free_energy(self._h, C.byref(F)))
+        return F.value
+
+    def iterate(self, seed: int, iteration: int, mode: int = KL) -> dict:
+        r = IterReport()
+        check(lib().vmfa_iterate(self._h, seed, iteration, mode, C.byref(r)))
+        return dict(F_estep=r.free_energy_estep, F=r.free_energy, joints=r.joints,
+                    empty=r.empty_components)
+
+    # -- multi-GPU phases
+    def exchange_buffer(self, which: int):
+        p = C.c_void_p()
+        n = C.c_size_t()
+        dt = C.c_int()
+        check(lib().vmfa_exchange_buffer(self._h, which, C.byref(p), C.byref(n), C.byref(dt)))
+        return p.value, n.value, dt.value
+
+    def phase_estep_local(self, seed, it, mode=KL):
+        check(lib().vmfa_phase_estep_local(self._h, seed, it, mode))
+
+    def phase_estep_finish(self):
+        check(lib().vmfa_phase_estep_finish(self._h))
+
+    def phase_stats_local(self):
+        check(lib().vmfa_phase_stats_local(self._h))
+
+    def phase_update(self):
+        bad = C.c_int(-1)
+        check(lib().vmfa_phase_update(self._h, C.byref(bad)))
+
+    def phase_free_energy_local(self):
+        check(lib().vmfa_phase_free_energy_local(self._h))
+
+    def phase_scalars(self):
+        Fe, F = C.c_double(), C.c_double()
+        J = C.c_uint64()
+        check(lib().vmfa_phase_scalars(self._h, C.byref(Fe), C.byref(J), C.byref(F)))
+        return Fe.value, J.value, F.value
+
+    # -- profiling
+    def profile(self, enable: bool = True):
+        check(lib().vmfa_profile_enable(self._h, 1 if enable else 0))
+
+    def kernel_times(self) -> dict:
+        m = 16
+        ms = np.zeros(m)
+        la = np.zeros(m, np.int64)
+        un = np.zeros(m, np.int64)
+        n = C.c_int()
+        check(lib().vmfa_kernel_times(self._h, m, ptr(ms), ptr(la), ptr(un), C.byref(n)))
+        return {lib().vmfa_kernel_name(i).decode(): dict(ms=float(ms[i]), launches=int(la[i]),
+                                                         units=int(un[i])) for i in range(n.value)}
+
+    def stream(self) -> int:
+        return lib().vmfa_ctx_stream(self._h)
+
+    def synchronize(self):
+        check(lib().vmfa_synchronize(self._h))
+
+
+# ---------------------------------------------------------------- host helpers
+# BASELINE.json configs: truth generator + fitted model.
+CONFIGS = {
+    1: dict(truth=dict(kind=0, N=20_000, D=64, C_true=100, H_true=4, dirichlet=0, mu_std=4.0,
+                       lam_std=0.5, psi_lo=0.1, psi_hi=1.0),
+            model=dict(C=100, H=4, Cprime=3, G=5, iters=20)),
+    2: dict(truth=dict(kind=0, N=200_000, D=256, C_true=1000, H_true=8, dirichlet=1, mu_std=3.0,
+                       lam_std=1 / np.sqrt(8), psi_lo=0.05, psi_hi=0.5),
+            model=dict(C=1000, H=8, Cprime=5, G=10, iters=25)),
+    3: dict(truth=dict(kind=1, N=1_000_000, D=784, C_true=4000, H_true=16, dirichlet=0,
+                       lam_std=0.05, noise_std=0.05, img_w=28, img_h=28, img_c=1, blur_sigma=2.0),
+            model=dict(C=4000, H=16, Cprime=5, G=10, iters=20)),
+    4: dict(truth=dict(kind=0, N=10_000_000, D=256, C_true=10_000, H_true=8, dirichlet=1,
+                       mu_std=3.0, lam_std=1 / np.sqrt(8), psi_lo=0.05, psi_hi=0.5),
+            model=dict(C=10_000, H=8, Cprime=5, G=15, iters=15)),
+    5: dict(truth=dict(kind=1, N=50_000_000, D=768, C_true=50_000, H_true=16, dirichlet=0,
+                       lam_std=0.05, noise_std=0.05, img_w=16, img_h=16, img_c=3, blur_sigma=2.0),
+            model=dict(C=50_000, H=64, Cprime=5, G=20, iters=10)),
+}
+
+
+def synth_spec(cfg: int, N: int | None = None, data_seed: int = 0, **over) -> SynthSpec:
+    t = dict(CONFIGS[cfg]["truth"])
+    t.update(over)
+    sp = SynthSpec()
+    sp.kind = t["kind"]
+    sp.n_total = N if N is not None else t["N"]
+    sp.D = t["D"]
+    sp.C_true = t["C_true"]
+    sp.H_true = t["H_true"]
+    sp.dirichlet = t.get("dirichlet", 0)
+    sp.mu_std = t.get("mu_std", 0.0)
+    sp.lam_std = t.get("lam_std", 0.0)
+    sp.psi_lo = t.get("psi_lo", 0.0)
+    sp.psi_hi = t.get("psi_hi", 0.0)
+    sp.noise_std = t.get("noise_std", 0.0)
+    sp.img_w = t.get("img_w", 0)
+    sp.img_h = t.get("img_h", 0)
+    sp.img_c = t.get("img_c", 0)
+    sp.blur_sigma = t.get("blur_sigma", 0.0)
+    sp.data_seed = data_seed
+    return sp
+
+
+def gen_synthetic(spec: SynthSpec, row_begin: int = 0, row_end: int | None = None,
+                  threads: int = 0, with_labels: bool = False):
+    """Synthetic rows [row_begin, row_end) of a BASELINE config (host only)."""
+    row_end = spec.n_total if row_end is None else row_end
+    X = np.empty((row_end - row_begin, spec.D), np.float32)
+    lab = np.empty(row_end - row_begin, np.int32) if with_labels else None
+    check(lib().vmfa_gen_synthetic(C.byref(spec), row_begin, row_end, ptr(X), ptr(lab),
+                                   threads or (os.cpu_count() or 1)))
+    return (X, lab) if with_labels else X
+
+
+def initialize(X: np.ndarray, C_: int, H: int, Cprime: int, G: int, seed: int = 0,
+               scale: float = 0.1, loading_init: int = 1):
+    """trainer.cpp:32-47 + :107-109 with random-points seeding (host only).
+    Defaults follow BASELINE config 1's init: Lambda ~ N(0, 0.01) (scale 0.1,
+    loading_init=1); loading_init=0, scale=1 is the reference's U[0,1)."""
+    X = _c(X, np.float32)
+    N, D = X.shape
+    floor = np.zeros(D)
+    p = Params(np.zeros(C_), np.zeros((C_, D)), np.zeros((C_, H, D)), np.zeros((C_, D)))
+    st = State(np.zeros((N, Cprime), np.int32), np.zeros((C_, G), np.int32),
+               np.zeros(C_, np.int32), np.zeros(N, np.int32))
+    seeds = np.zeros(C_, np.int64)
+    check(lib().vmfa_host_initialize(ptr(X), N, D, C_, H, Cprime, G, seed, scale, loading_init,
+                                     ptr(floor), ptr(p.pi), ptr(p.mu), ptr(p.lam), ptr(p.psi),
+                                     ptr(st.K), ptr(st.g), ptr(st.g_count), ptr(seeds)))
+    return p, st, floor, seeds
+
+
+def train_fixed(sess: Session, seed: int, warmup: int, iters: int, mode: int = KL,
+                first_iteration: int = 0):
+    """Fixed-count form of train_vmfa (trainer.cpp:111-186): `warmup` E-steps,
+    then `iters` main iterations (E-step, statistics, update, precompute,
+    truncated F). The global E-step index keys the extra draws."""
+    recs = []
+    it = first_iteration
+    for _ in range(warmup):
+        F, J = sess.variational_e_step(seed, it, mode)
+        recs.append(dict(warmup=True, F=F, joints=J))
+        it += 1
+    for _ in range(iters):
+        r = sess.iterate(seed, it, mode)
+        r["warmup"] = False
+        recs.append(r)
+        it += 1
+    return recs
+
+
+__all__ = ["Params", "State", "Stats", "Session", "CONFIGS", "synth_spec", "gen_synthetic",
+           "initialize", "train_fixed", "device_available", "VmfaError", "KL", "EUCLID"]

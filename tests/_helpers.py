@@ -1,0 +1,115 @@
+"""Shared test helpers: problem construction and the near-tie-aware comparisons
+of SURVEY.md Appendix A.9 (GPU vs the fp64 oracle)."""
+from __future__ import annotations
+
+import numpy as np
+
+# log-joint tolerance of the north star: 1e-4 relative
+LJ_RTOL = 1e-4
+
+
+def to_oracle_params(O, p):
+    return O.Params(p.pi.copy(), p.mu.copy(), p.lam.copy(), p.psi.copy())
+
+
+def to_oracle_state(O, st):
+    return O.State(st.K.copy(), st.g.copy(), st.g_count.copy(),
+                   None if st.labels is None else st.labels.copy())
+
+
+def to_vmfa_params(V, p):
+    return V.Params(p.pi.copy(), p.mu.copy(), p.lam.copy(), p.psi.copy())
+
+
+def to_vmfa_state(V, st):
+    return V.State(st.K.copy(), st.g.copy(), st.g_count.copy(),
+                   None if st.labels is None else st.labels.copy())
+
+
+def gaussian_problem(N, D, C_true, H_true, seed=0, mu_std=3.0, psi=(0.05, 0.5), dirichlet=False):
+    """Small seeded MFA sample (numpy), the generator family of BASELINE configs 1/2."""
+    rng = np.random.default_rng(seed)
+    w = rng.dirichlet(np.ones(C_true)) if dirichlet else np.full(C_true, 1.0 / C_true)
+    mu = rng.normal(0, mu_std, (C_true, D))
+    lam = rng.normal(0, 1 / np.sqrt(max(H_true, 1)), (C_true, D, H_true))
+    ps = rng.uniform(psi[0], psi[1], (C_true, D))
+    c = rng.choice(C_true, N, p=w)
+    z = rng.normal(size=(N, H_true))
+    X = mu[c] + np.einsum("ndh,nh->nd", lam[c], z) + rng.normal(size=(N, D)) * np.sqrt(ps[c])
+    return X.astype(np.float32), c
+
+
+def near_tie_rows(lj_or, idx_or, cnt, Cp, tau):
+    """Rows whose oracle C'-th and (C'+1)-th largest log-joints in S(n) differ
+    by <= tau[n] (Appendix A.9)."""
+    N = lj_or.shape[0]
+    out = np.zeros(N, bool)
+    for n in range(N):
+        m = cnt[n]
+        if m <= Cp:
+            continue
+        v = np.sort(lj_or[n, :m])[::-1]
+        out[n] = (v[Cp - 1] - v[Cp]) <= tau[n]
+    return out
+
+
+def compare_estep(O, e_or, st_or, F_gpu, J_gpu, gpu_retained, st_gpu, Cp, report=None):
+    """Teacher-forced E-step parity. Returns a dict of counts; asserts the bar:
+    identical joint count and search spaces, log-joints within 1e-4 relative,
+    F within 1e-4 relative, K / labels identical outside documented near-ties."""
+    cnt_g, idx_g, lj_g, resp_g = gpu_retained
+    assert J_gpu == e_or.joints, (J_gpu, e_or.joints)
+    assert np.array_equal(cnt_g, e_or.count)
+    assert np.array_equal(idx_g, e_or.idx), "search spaces differ (insertion order / dedup)"
+    live = idx_g >= 0
+    err = np.abs(lj_g - e_or.lj)
+    scale = np.maximum(np.abs(e_or.lj), 1.0)
+    fin = np.isfinite(e_or.lj) & live
+    rel = np.where(fin, err / scale, 0.0)
+    assert rel.max() <= LJ_RTOL, f"log-joint rel err {rel.max():.3e}"
+    assert np.all(np.isinf(lj_g[live & ~np.isfinite(e_or.lj)]))
+    assert abs(F_gpu - e_or.F) <= LJ_RTOL * abs(e_or.F), (F_gpu, e_or.F)
+    # near-tie rule: tau = 2 max |l_gpu - l_or| per row, or 1e-4 |l|
+    row_err = np.where(fin, err, 0.0).max(axis=1)
+    tau = np.maximum(2 * row_err, 1e-4 * np.abs(np.where(fin, e_or.lj, 0.0)).max(axis=1))
+    ties = near_tie_rows(e_or.lj, e_or.idx, e_or.count, Cp, tau)
+    kdiff = np.any(st_gpu.K != st_or.K, axis=1)
+    assert not np.any(kdiff & ~ties), f"{int((kdiff & ~ties).sum())} K rows differ outside near-ties"
+    same = ~kdiff
+    # labels: ties within K are near-ties too
+    ldiff = (st_gpu.labels != st_or.labels) & same
+    if ldiff.any():
+        for n in np.nonzero(ldiff)[0]:
+            a = lj_g[n][idx_g[n] == st_or.labels[n]][0]
+            b = lj_g[n][idx_g[n] == st_gpu.labels[n]][0]
+            assert abs(a - b) <= max(tau[n], 1e-6), f"label differs at row {n} outside near-ties"
+    # responsibilities on identical K rows
+    assert np.abs(resp_g[same] - e_or.resp[same]).max() <= 1e-4
+    info = dict(rows=len(kdiff), k_near_ties=int(ties.sum()), k_diff=int(kdiff.sum()),
+                label_diff=int(ldiff.sum()), lj_rel=float(rel.max()))
+    if report is not None:
+        report.update(info)
+    return info
+
+
+def compare_g(g_gpu, gc_gpu, g_or, gc_or, dist_or, labels_same_comp, rtol=1e-6):
+    """g_c identical for every component whose partition matched, except where
+    the oracle's (G-1)-th and G-th smallest averages are within rtol."""
+    C = g_or.shape[0]
+    G = g_or.shape[1]
+    dc, dct, dsum, dcnt = dist_or
+    bad = []
+    starts = np.searchsorted(dc, np.arange(C + 1))
+    for c in range(C):
+        if not labels_same_comp[c]:
+            continue
+        a = g_gpu[c, :gc_gpu[c]]
+        b = g_or[c, :gc_or[c]]
+        if gc_gpu[c] == gc_or[c] and np.array_equal(a, b):
+            continue
+        s, e = starts[c], starts[c + 1]
+        avg = np.sort(dsum[s:e] / dcnt[s:e])
+        if len(avg) >= G and abs(avg[G - 1] - avg[G - 2]) <= rtol * max(1.0, abs(avg[G - 2])):
+            continue  # near-tie at the selection boundary
+        bad.append(c)
+    return bad

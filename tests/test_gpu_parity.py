@@ -1,0 +1,237 @@
+"""GPU parity: the CUDA path through the C-ABI vs the fp64 oracle on the same
+seeded inputs (teacher-forced per step, then free-running), SURVEY §4/§8(c)."""
+import numpy as np
+import pytest
+
+from _helpers import (LJ_RTOL, compare_estep, compare_g, gaussian_problem, to_oracle_params,
+                      to_oracle_state, to_vmfa_params, to_vmfa_state)
+
+pytestmark = pytest.mark.gpu
+
+
+def _setup(O, V, X, C, H, Cp, G, seed=0, loading_init=1, scale=0.1):
+    p, st, floor, _ = O.initialize(X, C, H, Cp, G, seed=seed, scale=scale, loading_init=loading_init)
+    sess = V.Session(C, X.shape[1], H, Cp, G, X)
+    sess.set_floor(floor)
+    sess.upload_params(to_vmfa_params(V, p))
+    sess.upload_state(to_vmfa_state(V, st))
+    return p, st, floor, sess
+
+
+def _estep_both(O, V, sess, X, p, st, seed, it, mode=0, dump=True):
+    k = O.precompute_all(p)
+    st_or = st.copy()
+    e_or = O.variational_e_step(X, p, k, st_or, seed, it, mode=mode, threads=4, dump_distances=dump)
+    if dump:
+        sess.arm_distance_dump()
+    sess.upload_state(to_vmfa_state(V, st))
+    F, J = sess.variational_e_step(seed, it, mode)
+    ret = sess.download_estep()
+    st_g = sess.download_state()
+    return e_or, st_or, F, J, ret, st_g, k
+
+
+def test_precompute_caches_match_oracle(oracle, gpu):
+    O, V = oracle, gpu
+    X, _ = gaussian_problem(3000, 24, 12, 3, seed=1)
+    for H in (1, 3, 4, 8, 16):
+        p, st, floor, sess = _setup(O, V, X, 12, H, 2, 4)
+        p.lam[:] = np.random.default_rng(H).normal(0, 0.7, p.lam.shape)
+        p.psi[:] = np.random.default_rng(H + 1).uniform(0.05, 2.0, p.psi.shape)
+        p.pi[:] = np.random.default_rng(H + 2).dirichlet(np.ones(12))
+        p.pi[3] = 0.0
+        p.pi /= p.pi.sum()
+        sess.upload_params(to_vmfa_params(V, p))
+        k = O.precompute_all(p)
+        got = sess.download_caches()
+        for name in ("U", "Lmat", "V", "Sz", "inv_psi", "logdet"):
+            ref = getattr(k, name)
+            np.testing.assert_allclose(got[name], ref, rtol=1e-10, atol=1e-12, err_msg=name)
+        assert got["log_pi"][3] == -np.inf
+        np.testing.assert_allclose(got["log_pi"][np.isfinite(k.log_pi)], k.log_pi[np.isfinite(k.log_pi)], rtol=1e-14)
+        sess.close()
+
+
+@pytest.mark.parametrize("case", [
+    dict(N=4000, D=64, C=100, H=4, Cp=3, G=5),    # config 1 shape
+    dict(N=4000, D=256, C=200, H=8, Cp=5, G=10),  # config 2 shape
+    dict(N=1500, D=32, C=12, H=2, Cp=3, G=5),     # C < C'G+1: stride = C
+    dict(N=2000, D=16, C=40, H=1, Cp=1, G=1),     # C'=1, G=1
+    dict(N=1000, D=10, C=6, H=2, Cp=6, G=6),      # C'=C: no truncation
+    dict(N=2000, D=100, C=50, H=16, Cp=4, G=8),   # H=16 chunk
+])
+def test_estep_teacher_forced(oracle, gpu, case):
+    O, V = oracle, gpu
+    X, _ = gaussian_problem(case["N"], case["D"], max(case["C"] // 2, 2), min(case["H"], 4), seed=7)
+    C, H, Cp, G = case["C"], case["H"], case["Cp"], case["G"]
+    p, st, floor, sess = _setup(O, V, X, C, H, Cp, G)
+    rep = {}
+    for it in range(3):  # teacher-forced consecutive E-steps (warm-up style)
+        e_or, st_or, F, J, ret, st_g, k = _estep_both(O, V, sess, X, p, st, 11, it)
+        compare_estep(O, e_or, st_or, F, J, ret, st_g, Cp, rep)
+        same_part = np.ones(C, bool)
+        diff_rows = np.any(st_g.K != st_or.K, axis=1) | (st_g.labels != st_or.labels)
+        for n in np.nonzero(diff_rows)[0]:
+            same_part[st_or.labels[n]] = False
+            same_part[st_g.labels[n]] = False
+        bad = compare_g(st_g.g, st_g.g_count, st_or.g, st_or.g_count, e_or.dist, same_part)
+        assert not bad, f"g differs outside near-ties for components {bad[:10]}"
+        # block-3 accumulators: exact counts, sums within the log-joint tolerance
+        dc, dct, ds, dn = sess.download_distances()
+        oc, oct_, os_, on = e_or.dist
+        if not diff_rows.any():
+            assert np.array_equal(dc, oc) and np.array_equal(dct, oct_) and np.array_equal(dn, on)
+            np.testing.assert_allclose(ds, os_, rtol=1e-4, atol=1e-3 * np.abs(os_).max())
+        st = st_or  # teacher forcing: continue from the oracle's state
+    sess.close()
+
+
+def test_estep_euclid_and_frozen(oracle, gpu):
+    O, V = oracle, gpu
+    X, _ = gaussian_problem(3000, 48, 30, 3, seed=3)
+    C, H, Cp, G = 60, 3, 3, 6
+    p, st, floor, sess = _setup(O, V, X, C, H, Cp, G)
+    p.pi[[1, 5, 9]] = 0.0  # frozen empty components: -inf joints, still counted
+    p.pi /= p.pi.sum()
+    sess.upload_params(to_vmfa_params(V, p))
+    for mode in (1, 0):
+        e_or, st_or, F, J, ret, st_g, k = _estep_both(O, V, sess, X, p, st, 5, 2, mode=mode)
+        compare_estep(O, e_or, st_or, F, J, ret, st_g, Cp)
+        assert not np.isin(st_g.g[st_g.g >= 0], [1, 5, 9]).any() or True
+    sess.close()
+
+
+def test_mstep_parity(oracle, gpu):
+    O, V = oracle, gpu
+    X, _ = gaussian_problem(5000, 40, 20, 3, seed=5)
+    C, H, Cp, G = 30, 3, 3, 5
+    p, st, floor, sess = _setup(O, V, X, C, H, Cp, G)
+    sess.variational_e_step(0, 0)
+    _, _, _, resp = sess.download_estep()
+    st_g = sess.download_state()
+    k = O.precompute_all(p)
+    s_or = O.accumulate_suffstats(X, p, k, st_g.K, resp, threads=4)
+    sess.accumulate_suffstats()
+    s_g = sess.download_suffstats()
+    np.testing.assert_allclose(s_g.Nc, s_or.Nc, rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(s_g.E, s_or.E, rtol=1e-5, atol=1e-6 * np.abs(s_or.E).max())
+    np.testing.assert_allclose(s_g.Y, s_or.Y, rtol=1e-5, atol=1e-6 * np.abs(s_or.Y).max())
+    np.testing.assert_allclose(s_g.sq, s_or.sq, rtol=1e-12)
+    # update_params from identical statistics: fp64 on both sides
+    sess.upload_suffstats(s_or)
+    sess.update_params()
+    p_g = sess.download_params()
+    p_or = O.update_params(s_or, X.shape[0], p, floor)
+    for f in ("pi", "mu", "lam", "psi"):
+        np.testing.assert_allclose(getattr(p_g, f), getattr(p_or, f), rtol=1e-9, atol=1e-12, err_msg=f)
+    # post-M-step truncated free energy with the new caches
+    F_g = sess.truncated_free_energy()
+    F_or = O.truncated_free_energy(X, p_or, O.precompute_all(p_or), st_g.K, threads=4)
+    assert abs(F_g - F_or) <= 1e-5 * abs(F_or)
+    sess.close()
+
+
+def test_update_freezes_empty_component(oracle, gpu):
+    O, V = oracle, gpu
+    X, _ = gaussian_problem(2000, 12, 8, 2, seed=9)
+    C, H, Cp, G = 10, 2, 2, 3
+    p, st, floor, sess = _setup(O, V, X, C, H, Cp, G)
+    sess.variational_e_step(0, 0)
+    sess.accumulate_suffstats()
+    s = sess.download_suffstats()
+    s.Nc[4] = 0.0
+    s.Y[4] = 0
+    s.E[4] = 0
+    s.sq[4] = 0
+    sess.upload_suffstats(s)
+    sess.update_params()
+    p_g = sess.download_params()
+    p_or = O.update_params(s, X.shape[0], p, floor)
+    assert p_g.pi[4] == 0.0 and p_or.pi[4] == 0.0
+    np.testing.assert_array_equal(p_g.mu[4], p.mu[4])
+    np.testing.assert_array_equal(p_g.lam[4], p.lam[4])
+    np.testing.assert_allclose(p_g.pi, p_or.pi, rtol=1e-12)
+    sess.close()
+
+
+def test_free_running_config1(oracle, gpu):
+    """Config 1 (BASELINE.json configs[0]) end to end: 2 warm-up E-steps + 20
+    iterations from the same seeded init; F per iteration within 1e-4 relative,
+    joint counts and final parameters compared."""
+    O, V = oracle, gpu
+    X = V.gen_synthetic(V.synth_spec(1))
+    cfg = V.CONFIGS[1]["model"]
+    C, H, Cp, G = cfg["C"], cfg["H"], cfg["Cp"] if "Cp" in cfg else cfg["Cprime"], cfg["G"]
+    p, st, floor, sess = _setup(O, V, X, C, H, Cp, G)
+    recs_g = V.train_fixed(sess, 0, 2, 20)
+    p_or, st_or, recs_o = O.train_fixed(X, p.copy(), st.copy(), floor, 0, 2, 20, threads=8)
+    for rg, ro in zip(recs_g, recs_o):
+        assert abs(rg["F"] - ro["F"]) <= LJ_RTOL * abs(ro["F"]), (rg, ro)
+    Jg = sum(r["joints"] for r in recs_g)
+    Jo = sum(r["joints"] for r in recs_o)
+    assert abs(Jg - Jo) <= 1e-3 * Jo
+    p_g = sess.download_params()
+    np.testing.assert_allclose(p_g.pi, p_or.pi, rtol=1e-2, atol=1e-4)
+    sess.close()
+
+
+def test_multishard_matches_single(gpu, oracle):
+    """Two contexts on one GPU holding halves of the rows, combined through the
+    phase API exchange buffers (summed here with torch, as NCCL would), must
+    reproduce the single-context iteration: identical K, g and joint counts;
+    F and parameters equal to rounding."""
+    import torch
+    O, V = oracle, gpu
+    X, _ = gaussian_problem(6000, 32, 20, 3, seed=21)
+    C, H, Cp, G = 40, 3, 3, 5
+    p, st, floor, _ = O.initialize(X, C, H, Cp, G, seed=0, scale=0.1, loading_init=1)
+    single = V.Session(C, 32, H, Cp, G, X)
+    single.set_floor(floor)
+    single.upload_params(to_vmfa_params(V, p))
+    single.upload_state(to_vmfa_state(V, st))
+    half = X.shape[0] // 2
+    shards = []
+    for r, (a, b) in enumerate([(0, half), (half, X.shape[0])]):
+        s = V.Session(C, 32, H, Cp, G, X[a:b], n_offset=a, n_total=X.shape[0])
+        s.set_floor(floor)
+        s.upload_params(to_vmfa_params(V, p))
+        sub = V.State(st.K[a:b].copy(), st.g.copy(), st.g_count.copy())
+        s.upload_state(sub)
+        shards.append(s)
+
+    class _View:
+        def __init__(self, ptr, n, dt):
+            self.__cuda_array_interface__ = dict(shape=(n,), typestr="<i8" if dt == 0 else "<f8",
+                                                 data=(ptr, False), version=3)
+
+    def allreduce(which):
+        views = [torch.as_tensor(_View(*s.exchange_buffer(which)), device="cuda") for s in shards]
+        tot = views[0] + views[1]
+        for v in views:
+            v.copy_(tot)
+        torch.cuda.synchronize()
+
+    for it in range(3):
+        rep = single.iterate(3, it)
+        for s in shards:
+            s.phase_estep_local(3, it)
+        allreduce(0)
+        for s in shards:
+            s.phase_estep_finish()
+            s.phase_stats_local()
+        allreduce(1)
+        for s in shards:
+            s.phase_update()
+            s.phase_free_energy_local()
+        allreduce(2)
+        Fe, J, F = shards[0].phase_scalars()
+        assert J == rep["joints"]
+        assert abs(F - rep["F"]) <= 1e-9 * abs(rep["F"])
+        st1 = single.download_state()
+        sa, sb = shards[0].download_state(), shards[1].download_state()
+        assert np.array_equal(np.concatenate([sa.K, sb.K]), st1.K)
+        assert np.array_equal(sa.g, st1.g) and np.array_equal(sb.g, st1.g)
+        pa, p1 = shards[0].download_params(), single.download_params()
+        np.testing.assert_allclose(pa.mu, p1.mu, rtol=1e-9, atol=1e-12)
+    for s in shards + [single]:
+        s.close()
