@@ -1,0 +1,408 @@
+"""bench.py — v-MFA EM iterations on B200 (BASELINE.json metric: candidate
+log-joint evaluations/sec and EM iteration time).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl reference]
+
+A step is one main-loop iteration of train_vmfa (trainer.cpp:149-160): the
+variational E-step (candidates, Woodbury log-joints, top-C', labels, g update,
+responsibilities), sufficient statistics, update_params, precompute and the
+post-M-step truncated free energy, over BASELINE config 2 (configs[1]: N=200k,
+D=256, C=1000, H=8, C'=5, G=10) on synthetic data of that generator. value =
+joint evaluations (sum_n |S(n)|, the reference counter) of all ranks per
+second of the max-over-ranks device time. Under torchrun each rank holds its
+own config-2-sized shard (weak scaling) and the ranks exchange the
+co-occurrence table and the statistics with NCCL all-reduces.
+
+--impl reference times the reference algorithm's CPU restatement (oracle/, the
+reference library needs Eigen3, absent here) on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "candidate log-joint evals/sec & EM iteration time"
+PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--n", type=int, default=0, help="override rows per rank (testing only)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--profile-only", action="store_true",
+                    help="run warm-up + 2 steps only (for ncu launch lists)")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(PEAKS) as f:
+            d = json.load(f)
+        return dict(hbm=float(d["hbm_gbs"]), bf16=float(d["bf16_tflops"]), src="measured")
+    except Exception:
+        return dict(hbm=6650.0, bf16=1590.0, src="fallback")
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm = [float(r[0]) for r in self.rows if len(r) >= 8 and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) >= 8 and r[1].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            if len(r) < 8:
+                continue
+            for name, v in zip(names, r[4:8]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def build_problem(cfg: int, rank: int, world: int, n_override: int = 0):
+    from paper_2501_12299_b200 import vmfa as V
+    m = V.CONFIGS[cfg]["model"]
+    per = n_override or V.CONFIGS[cfg]["truth"]["N"]
+    n_total = per * world
+    spec = V.synth_spec(cfg, N=n_total)
+    X = V.gen_synthetic(spec)
+    p, st, floor, _ = V.initialize(X, m["C"], m["H"], m["Cprime"], m["G"], seed=0, scale=0.1,
+                                   loading_init=1)
+    a, b = rank * n_total // world, (rank + 1) * n_total // world
+    return V, m, X, p, st, floor, a, b, n_total
+
+
+def alg_per_joint(D, H):
+    """F_j = 2DH + 3D + 2H flops, B_j = 4D + 8 bytes per joint."""
+    return 2 * D * H + 3 * D + 2 * H, 4 * D + 8
+
+
+def count_launches(sess, step_fn):
+    """Kernels launched by one step, counted by the CUDA profiler (CUPTI via
+    torch.profiler): every kernel in the process, ours and cub's."""
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        step_fn()
+        torch.cuda.synchronize()
+    n = 0
+    names = {}
+    for e in prof.events():
+        if e.device_type.name == "CUDA" and not e.name.startswith("Memcpy") and not e.name.startswith("Memset"):
+            n += 1
+            names[e.name] = names.get(e.name, 0) + 1
+    return n, names
+
+
+def cpu_baseline_port(cfg: int, steps: int = 1, rows: int = 20000, threads: int = 0):
+    """The reference algorithm restated (oracle/) on the host cores: full
+    iterations on the first `rows` rows of the config's data with full C."""
+    from oracle import oracle as O
+    from paper_2501_12299_b200 import vmfa as V
+    m = V.CONFIGS[cfg]["model"]
+    threads = threads or os.cpu_count() or 1
+    X = V.gen_synthetic(V.synth_spec(cfg), 0, rows)
+    p, st, floor, _ = O.initialize(X, m["C"], m["H"], m["Cprime"], m["G"], seed=0, scale=0.1,
+                                   loading_init=1)
+    k = O.precompute_all(p)
+    for it in range(2):  # warm-up E-steps, as in the GPU arm
+        O.variational_e_step(X, p, k, st, 0, it, threads=threads)
+    it = 2
+    times, joints = [], []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        e = O.variational_e_step(X, p, k, st, 0, it, threads=threads)
+        s = O.accumulate_suffstats(X, p, k, st.K, e.resp, threads=threads)
+        p = O.update_params(s, X.shape[0], p, floor)
+        k = O.precompute_all(p)
+        O.truncated_free_energy(X, p, k, st.K, threads=threads)
+        times.append(time.perf_counter() - t0)
+        joints.append(e.joints)
+        it += 1
+    return dict(value=float(sum(joints) / sum(times)), unit="joint evals/s", cores=threads,
+                kind="port", iter_s=float(np.mean(times)),
+                sample=f"config {cfg}, first {rows} rows, full C={m['C']}, {steps} full EM iteration(s) "
+                       f"(E-step+stats+update+precompute+F) after 2 warm-up E-steps, {threads} threads")
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference algorithm's CPU restatement on the host
+    cores (rank 0 only)."""
+    if rank != 0:
+        return
+    from paper_2501_12299_b200 import vmfa as V
+    m = V.CONFIGS[args.config]["model"]
+    D, H = V.CONFIGS[args.config]["truth"]["D"], m["H"]
+    rows = 20000
+    cb = cpu_baseline_port(args.config, steps=max(1, args.steps), rows=rows)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "joint evals/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": cb["iter_s"] * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (BASELINE config generator)",
+        "config": {"workload": f"config{args.config} sample: {rows} rows, C={m['C']}, D={D}, H={H}, "
+                               f"C'={m['Cprime']}, G={m['G']}"},
+        "cpu_baseline": {"value": cb["value"], "unit": "joint evals/s", "cores": cb["cores"],
+                         "kind": "port", "sample": cb["sample"]},
+        "e2e": {"value": cb["value"], "unit": "joint evals/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "note": "reference library unbuildable (needs Eigen3, absent); timed = oracle/ fp64 "
+                "restatement of the same algorithm, plain loops, std::thread with the reference chunking",
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    import torch
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_2501_12299_b200 import vmfa as V
+    V_, m, X, p, st, floor, a, b, n_total = build_problem(args.config, rank, world, args.n)
+    D = X.shape[1]
+    C, H, Cp, G = m["C"], m["H"], m["Cprime"], m["G"]
+    sess = V.Session(C, D, H, Cp, G, X[a:b], n_offset=a, n_total=n_total, device=local)
+    sess.set_floor(floor)
+    sess.upload_params(p)
+    sess.upload_state(V.State(st.K[a:b].copy(), st.g, st.g_count))
+    ext = torch.cuda.ExternalStream(sess.stream())
+
+    class _View:
+        def __init__(self, ptr, n, dt):
+            self.__cuda_array_interface__ = dict(shape=(n,), typestr="<i8" if dt == 0 else "<f8",
+                                                 data=(ptr, False), version=3)
+
+    xb = {}
+    if world > 1:
+        for w in (0, 1, 2):
+            xb[w] = torch.as_tensor(_View(*sess.exchange_buffer(w)), device=f"cuda:{local}")
+
+    def allreduce(w):
+        with torch.cuda.stream(ext):
+            dist.all_reduce(xb[w])
+        ext.synchronize()
+
+    it_counter = [0]
+
+    def warm_estep():
+        if world > 1:
+            sess.phase_estep_local(0, it_counter[0])
+            allreduce(0)
+            sess.phase_estep_finish()
+        else:
+            sess.variational_e_step(0, it_counter[0])
+        it_counter[0] += 1
+
+    def step():
+        it = it_counter[0]
+        it_counter[0] += 1
+        if world == 1:
+            return sess.iterate(0, it)
+        sess.phase_estep_local(0, it)
+        allreduce(0)
+        sess.phase_estep_finish()
+        sess.phase_stats_local()
+        allreduce(1)
+        sess.phase_update()
+        sess.phase_free_energy_local()
+        allreduce(2)
+        Fe, J, F = sess.phase_scalars()
+        return dict(F_estep=Fe, joints=J, F=F)
+
+    # the reference trainer's minimum warm-up: 2 E-steps
+    for _ in range(2):
+        warm_estep()
+    for _ in range(args.warmup):
+        step()
+    if args.profile_only:
+        for _ in range(2):
+            step()
+        torch.cuda.synchronize()
+        return
+
+    # L2 flush buffer (> 126 MB L2), written between timed iterations
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{local}")
+    sess.profile(True)
+    times, joints, Fs = [], [], []
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            with torch.cuda.stream(ext):
+                flush.fill_(1.0)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(ext)
+            r = step()
+            e1.record(ext)
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1))
+            joints.append(r["joints"])
+            Fs.append(r["F"])
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    kt = sess.kernel_times()
+    sess.profile(False)
+    ms_step = float(np.sum(times) / args.steps)
+    J_rank = float(np.sum(joints) / args.steps)  # after the all-reduce J is already the job total
+    if dist:
+        t = torch.tensor([ms_step], device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_step = float(t.item())
+    J_job = J_rank if world > 1 else J_rank
+    value = J_job / (ms_step * 1e-3)
+
+    # dominant kernel: the candidate scoring (anchor + extra launches) of each E-step
+    Fj, Bj = alg_per_joint(D, H)
+    pk = peaks()
+    sc_ms = (kt["score_anchor"]["ms"] + kt["score_extra"]["ms"]) / args.steps
+    J_local = J_rank if world == 1 else J_rank / world
+    ach_gbs = J_local * Bj / (sc_ms * 1e-3) / 1e9 if sc_ms > 0 else None
+    ach_tfs = J_local * Fj / (sc_ms * 1e-3) / 1e12 if sc_ms > 0 else None
+    phase_ms = {k: v["ms"] / args.steps for k, v in kt.items()}
+
+    # launches per step (CUPTI), outside the timed region
+    n_launch, names = count_launches(sess, step)
+
+    e2e = None
+    if not args.no_e2e and world == 1:
+        e2e = measure_e2e(V, sess, X[a:b], p, st, floor, args, ext)
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline and world == 1:
+        try:
+            cpu = cpu_baseline_port(args.config)
+            cpu.pop("iter_s", None)
+        except Exception as ex:  # the baseline is reported, never required
+            cpu = {"error": str(ex)}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "joint evals/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (BASELINE config generator, seeded), random-points init",
+            "config": {"workload": f"config{args.config}: N={b - a} rows/GPU (N_total={n_total}), "
+                                   f"D={D}, C={C}, H={H}, C'={Cp}, G={G}; one EM main iteration "
+                                   f"per step (E-step, stats, update, precompute, truncated F)",
+                       "l2": "flushed (256 MB write) before every timed iteration",
+                       "parallelism": f"dp{world} (rows sharded, params replicated)"},
+            "joints_per_step": J_job, "F_last": Fs[-1],
+            "em_iteration_ms": ms_step,
+            "phase_ms": phase_ms,
+            "roofline": {"bound": "hbm", "kernel": "candidate scoring (score_anchor+score_extra)",
+                         "achieved": ach_gbs, "peak": pk["hbm"], "unit": "GB/s",
+                         "frac": (ach_gbs / pk["hbm"]) if ach_gbs else None,
+                         "traffic": None, "peak_src": pk["src"],
+                         "per_unit": f"B_j = 4D+8 = {Bj} B per joint (SURVEY §8(d)), J={J_local:.0f} joints per launch pair",
+                         "flops_view": {"achieved_tflops": ach_tfs, "F_j": Fj}},
+            "gpu_launches": int(n_launch * args.steps),
+            "launches_per_step": n_launch,
+            "clocks": clk.summary(),
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+        }
+        print(json.dumps(line), flush=True)
+    sess.close()
+    if dist:
+        dist.destroy_process_group()
+
+
+def measure_e2e(V, sess, Xs, p, st, floor, args, ext):
+    """The same metric through the public API with host buffers: every step
+    uploads the shard's rows (pinned host memory), the parameters and the
+    variational state, runs the iteration and downloads the new parameters,
+    state and free energy."""
+    import torch
+    Xp = torch.from_numpy(np.ascontiguousarray(Xs)).pin_memory().numpy()
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()  # noqa: E731
+    pp = V.Params(pin(p.pi), pin(p.mu), pin(p.lam), pin(p.psi))
+    sp = V.State(pin(st.K[:Xs.shape[0]]), pin(st.g), pin(st.g_count))
+    h2d = Xp.nbytes + sum(a.nbytes for a in (pp.pi, pp.mu, pp.lam, pp.psi, sp.K, sp.g, sp.g_count))
+    d2h = sum(a.nbytes for a in (pp.pi, pp.mu, pp.lam, pp.psi, sp.K, sp.g, sp.g_count)) + Xs.shape[0] * 4 + 24
+    ts, js = [], []
+    it = 1000
+    for i in range(args.warmup + args.steps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        sess.upload_data(Xp)
+        sess.upload_params(pp)
+        sess.upload_state(sp)
+        r = sess.iterate(0, it)
+        pn = sess.download_params()
+        sn = sess.download_state()
+        t1 = time.perf_counter()
+        it += 1
+        if i >= args.warmup:
+            ts.append(t1 - t0)
+            js.append(r["joints"])
+        pp = V.Params(pin(pn.pi), pin(pn.mu), pin(pn.lam), pin(pn.psi))
+        sp = V.State(pin(sn.K), pin(sn.g), pin(sn.g_count))
+    return {"value": float(np.sum(js) / np.sum(ts)), "unit": "joint evals/s",
+            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+            "ms_per_step": float(np.mean(ts) * 1e3),
+            "how": "host wall clock around upload(X, params, state) + iterate + download(params, state, labels, F)"}
+
+
+if __name__ == "__main__":
+    main()

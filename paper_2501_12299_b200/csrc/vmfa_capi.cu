@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -77,7 +78,10 @@ struct vmfa_ctx {
   // caches
   double *Lmat = nullptr, *R = nullptr, *Sz = nullptr, *logdet = nullptr, *logpi = nullptr,
          *kconst = nullptr;
-  float *P = nullptr, *V32 = nullptr, *mu32 = nullptr;
+  float *P = nullptr, *V32 = nullptr, *mu32 = nullptr, *WT = nullptr, *ipsi32 = nullptr;
+  int Hp = 4;
+  bool use_tc = true;       // tcgen05 3xTF32 scorer (VMFA_SCORER=ffma selects the FFMA kernel)
+  int score_rows = kScoreRowsTc;
   // state
   int *K = nullptr, *g = nullptr, *gcnt = nullptr, *g_new = nullptr, *gcnt_new = nullptr,
       *labels = nullptr;
@@ -95,7 +99,11 @@ struct vmfa_ctx {
   int* vals = nullptr;
   int *kinv_off = nullptr, *kinv_ent = nullptr, *kinv_items = nullptr;
   int *ex_off = nullptr, *ex_ent = nullptr, *ex_items = nullptr;
-  int *part_off = nullptr, *part_ent = nullptr;
+  int *part_off = nullptr, *part_ent = nullptr, *part_items = nullptr;
+  int* stats_items = nullptr;
+  int stats_rows = 256;     // K-pairs per statistics item
+  int gupd_pts = 256;       // partition points per block-3 item
+  double* stats_part = nullptr;
   int *cnt = nullptr, *chunks = nullptr;
   void* cub_tmp = nullptr;
   size_t cub_bytes = 0;
@@ -221,6 +229,11 @@ int csr_by_key(vmfa_ctx* x, const unsigned* keys, int64_t n, int* off, int* ent,
 
 int score_grid() { return sm_count() * 8; }
 
+cudaError_t run_score(vmfa_ctx* x, int mode, const ScoreArgs& a) {
+  if (x->use_tc) return launch_score_tc(mode, a, x->WT, x->ipsi32, x->mu32, x->stream);
+  return launch_score(mode, a, score_grid(), x->stream);
+}
+
 ScoreArgs score_args(vmfa_ctx* x) {
   ScoreArgs a{};
   a.dm = x->dm;
@@ -252,6 +265,9 @@ int run_precompute(vmfa_ctx* x, int* failed) {
   a.P = x->P;
   a.V32 = x->V32;
   a.mu32 = x->mu32;
+  a.WT = x->WT;
+  a.ipsi32 = x->ipsi32;
+  a.Hp = x->Hp;
   a.status = x->st_model;
   const int tok = x->begin(kFamPrecompute, x->dm.C);
   CU(launch_precompute(a, s));
@@ -274,14 +290,14 @@ int estep_local(vmfa_ctx* x, uint64_t seed, uint64_t it, int mode, bool exchange
   CU(cudaMemsetAsync(x->st_select, 0, sizeof(int), s));
   // anchor blocks: inverted K (stable counting sort by component)
   CU(launch_keys_from_i32(x->K, x->keys, dm.N * dm.Cp, s));
-  TRY(csr_by_key(x, x->keys, dm.N * dm.Cp, x->kinv_off, x->kinv_ent, x->kinv_items, kScoreRows));
+  TRY(csr_by_key(x, x->keys, dm.N * dm.Cp, x->kinv_off, x->kinv_ent, x->kinv_items, x->score_rows));
   // extras not already covered by U g_a
   {
     const int tok = x->begin(kFamOther, dm.N);
     CU(launch_extra(dm, x->K, x->g, x->gcnt, seed, it, x->rx, x->rkey, s));
     x->end(tok);
   }
-  TRY(csr_by_key(x, x->rkey, dm.N, x->ex_off, x->ex_ent, x->ex_items, kScoreRows));
+  TRY(csr_by_key(x, x->rkey, dm.N, x->ex_off, x->ex_ent, x->ex_items, x->score_rows));
   // block 1: scoring
   {
     ScoreArgs a = score_args(x);
@@ -290,13 +306,13 @@ int estep_local(vmfa_ctx* x, uint64_t seed, uint64_t it, int mode, bool exchange
     a.itemoff = x->kinv_items;
     a.out = x->LJ;
     const int tok = x->begin(kFamScoreAnchor, dm.N * dm.Cp);
-    CU(launch_score(kModeAnchor, a, score_grid(), s));
+    CU(run_score(x, kModeAnchor, a));
     x->end(tok);
     a.off = x->ex_off;
     a.ent = x->ex_ent;
     a.itemoff = x->ex_items;
     const int tok2 = x->begin(kFamScoreExtra, dm.N);
-    CU(launch_score(kModeExtra, a, score_grid(), s));
+    CU(run_score(x, kModeExtra, a));
     x->end(tok2);
   }
   // selection, labels, block 4
@@ -324,6 +340,11 @@ int estep_local(vmfa_ctx* x, uint64_t seed, uint64_t it, int mode, bool exchange
   // block 2: partition by label (stable => ascending n per component)
   CU(launch_keys_from_i32(x->labels, x->keys, dm.N, s));
   TRY(csr_by_key(x, x->keys, dm.N, x->part_off, x->part_ent, nullptr, 1));
+  {
+    size_t tb = x->cub_bytes;
+    CU(launch_chunks_from_off(x->part_off, dm.C, x->gupd_pts, 1, x->chunks, s));
+    CU(cub::DeviceScan::ExclusiveSum(x->cub_tmp, tb, x->chunks, x->part_items, dm.C + 1, s));
+  }
   // block 3 (local accumulation; selection unless exchanging)
   CU(launch_logpi(x->pi, dm.C, x->logpi, s));
   {
@@ -342,9 +363,10 @@ int estep_local(vmfa_ctx* x, uint64_t seed, uint64_t it, int mode, bool exchange
     a.gt_cnt = x->gt_cnt;
     a.gt_hi = x->gt_hi;
     a.gt_lo = x->gt_lo;
+    a.itemoff = x->part_items;
+    a.pts_per_item = x->gupd_pts;
     a.exchange = exchange ? 1 : 0;
     a.xc = x->xc;
-    if (exchange) CU(cudaMemsetAsync(x->xc, 0, sizeof(long long) * 3 * (size_t)dm.C * dm.C, s));
     a.dump = x->dump ? 1 : 0;
     if (x->dump) {
       CU(cudaMemsetAsync(x->dump_n, 0, sizeof(unsigned long long), s));
@@ -358,6 +380,7 @@ int estep_local(vmfa_ctx* x, uint64_t seed, uint64_t it, int mode, bool exchange
     }
     const int tok = x->begin(kFamGupdate, dm.N);
     CU(launch_gupdate(a, x->gupd_grid, s));
+    if (!exchange && x->xc) CU(launch_gselect_dense(dm, x->xc, x->part_items, 0, x->g_new, x->gcnt_new, s));
     x->end(tok);
   }
   // scalars: F_estep = sum lse, joints = sum ret_cnt
@@ -374,7 +397,7 @@ int estep_finish(vmfa_ctx* x, bool exchange) {
   cudaStream_t s = x->stream;
   if (exchange) {
     const int tok = x->begin(kFamGupdate, dm.C);
-    CU(launch_gselect_dense(dm, x->xc, x->g_new, x->gcnt_new, s));
+    CU(launch_gselect_dense(dm, x->xc, x->part_items, 1, x->g_new, x->gcnt_new, s));
     x->end(tok);
   }
   std::swap(x->g, x->g_new);
@@ -390,7 +413,7 @@ int ensure_kinv_current(vmfa_ctx* x) {
   if (x->kinv_for_current_K) return VMFA_OK;
   const Dims& dm = x->dm;
   CU(launch_keys_from_i32(x->K, x->keys, dm.N * dm.Cp, x->stream));
-  TRY(csr_by_key(x, x->keys, dm.N * dm.Cp, x->kinv_off, x->kinv_ent, x->kinv_items, kScoreRows));
+  TRY(csr_by_key(x, x->keys, dm.N * dm.Cp, x->kinv_off, x->kinv_ent, x->kinv_items, x->score_rows));
   x->kinv_for_current_K = true;
   return VMFA_OK;
 }
@@ -412,7 +435,10 @@ int stats_local(vmfa_ctx* x) {
   a.Y = x->Y;
   a.sq = x->sq;
   const int tok = x->begin(kFamStats, x->dm.N * x->dm.Cp);
-  CU(launch_stats(a, x->stream));
+  size_t tb = x->cub_bytes;
+  CU(launch_chunks_from_off(x->kinv_off, x->dm.C, x->stats_rows, 0, x->chunks, x->stream));
+  CU(cub::DeviceScan::ExclusiveSum(x->cub_tmp, tb, x->chunks, x->stats_items, x->dm.C + 1, x->stream));
+  CU(launch_stats(a, x->stats_items, x->stats_rows, x->stats_part, x->stream));
   x->end(tok);
   return VMFA_OK;
 }
@@ -466,7 +492,7 @@ int free_energy_local(vmfa_ctx* x) {
   a.itemoff = x->kinv_items;
   a.out = x->LJK;
   const int tok = x->begin(kFamScoreTruncF, dm.N * dm.Cp);
-  CU(launch_score(kModeTruncF, a, score_grid(), s));
+  CU(run_score(x, kModeTruncF, a));
   CU(launch_lse_rows(x->LJK, dm.N, dm.Cp, x->lse, s));
   x->end(tok);
   CU(launch_sum_f64(x->lse, dm.N, x->partials, x->scal + 2, s));
@@ -527,6 +553,12 @@ int vmfa_ctx_create(vmfa_ctx** out, int device, int C, int D, int H, int Cp, int
   dm.stride = static_cast<int>(std::min<int64_t>(static_cast<int64_t>(Cp) * G + 1, C));
   dm.N = n_local, dm.n0 = n_offset, dm.Ntot = n_total;
   x->L = score_layout(H);
+  x->Hp = H <= 4 ? 4 : H <= 8 ? 8 : H <= 16 ? 16 : H <= 32 ? 32 : 64;
+  {
+    const char* sc = std::getenv("VMFA_SCORER");
+    x->use_tc = !(sc && std::string(sc) == "ffma") && score_tc_supported(x->dm);
+    x->score_rows = x->use_tc ? kScoreRowsTc : kScoreRows;
+  }
   if (stream) {
     x->stream = static_cast<cudaStream_t>(stream);
   } else {
@@ -556,6 +588,8 @@ int vmfa_ctx_create(vmfa_ctx** out, int device, int C, int D, int H, int Cp, int
   A(x->P, Cs * D * x->L.HP);
   A(x->V32, Cs * D * H);
   A(x->mu32, Cs * D);
+  A(x->WT, Cs * x->Hp * D);
+  A(x->ipsi32, Cs * D);
   A(x->K, N * Cp);
   A(x->g, Cs * G);
   A(x->gcnt, Cs);
@@ -583,6 +617,27 @@ int vmfa_ctx_create(vmfa_ctx** out, int device, int C, int D, int H, int Cp, int
   A(x->ex_items, Cs + 1);
   A(x->part_off, Cs + 1);
   A(x->part_ent, N);
+  A(x->part_items, Cs + 1);
+  A(x->stats_items, Cs + 1);
+  {
+    const int64_t pairs = static_cast<int64_t>(N) * Cp;
+    const int64_t target = (pairs + sm_count() * 8 - 1) / (sm_count() * 8);
+    x->stats_rows = static_cast<int>(std::max<int64_t>(256, (target + 31) / 32 * 32));
+    const int64_t max_items = C + (pairs + x->stats_rows - 1) / x->stats_rows;
+    A(x->stats_part, static_cast<size_t>(max_items) * stats_part_stride(dm));
+    const int64_t bal = std::max<int64_t>(128, static_cast<int64_t>(N) / (4 * sm_count()));
+    const int64_t capb = (C - 1 <= kGupdCap / 2) ? (int64_t{1} << 30)
+                                                 : std::max<int64_t>(1, (kGupdCap / 2) / std::max(1, dm.stride - 1));
+    x->gupd_pts = static_cast<int>(std::min(bal, capb));
+  }
+  // dense C x C rows (count, fixed-point hi, lo) for split components and the
+  // multi-rank exchange; without it (very large C) components are not split.
+  if (3.0 * Cs * Cs * sizeof(long long) <= 8.0 * (1ull << 30)) {
+    A(x->xc, 3 * Cs * Cs);
+    if (r == VMFA_OK) cudaMemsetAsync(x->xc, 0, 3 * Cs * Cs * sizeof(long long), x->stream);
+  } else {
+    x->gupd_pts = 1 << 30;
+  }
   A(x->cnt, Cs + 1);
   A(x->chunks, Cs + 1);
   x->gupd_grid = static_cast<int>(std::min<int64_t>(C, sm_count() * 2));
@@ -855,7 +910,7 @@ int vmfa_download_distances(vmfa_ctx* x, int64_t cap, int32_t* c, int32_t* ct, d
   unsigned long long m = 0;
   CU(cudaMemcpyAsync(&m, x->dump_n, sizeof m, cudaMemcpyDeviceToHost, x->stream));
   CU(cudaStreamSynchronize(x->stream));
-  const int64_t rows = std::min<int64_t>(static_cast<int64_t>(m), x->dump_cap);
+  int64_t rows = std::min<int64_t>(static_cast<int64_t>(m), x->dump_cap);
   std::vector<int32_t> vc(rows), vct(rows);
   std::vector<long long> vn(rows), vh(rows), vl(rows);
   cudaStream_t s = x->stream;
@@ -870,14 +925,27 @@ int vmfa_download_distances(vmfa_ctx* x, int64_t cap, int32_t* c, int32_t* ct, d
   std::sort(order.begin(), order.end(), [&](int64_t a, int64_t b) {
     return vc[a] != vc[b] ? vc[a] < vc[b] : vct[a] < vct[b];
   });
-  const int64_t w = std::min<int64_t>(rows, cap);
-  for (int64_t i = 0; i < w; ++i) {
+  // merge rows of split components (one row per item) in (c, ct) order
+  int64_t w = 0;
+  for (int64_t i = 0; i < rows;) {
     const int64_t k = order[i];
-    if (c) c[i] = vc[k];
-    if (ct) ct[i] = vct[k];
-    if (sum) sum[i] = static_cast<double>(vh[k]) / 1024.0 + static_cast<double>(vl[k]) / 1125899906842624.0;
-    if (count) count[i] = vn[k];
+    long long n = 0, hi = 0, lo = 0;
+    int64_t j = i;
+    for (; j < rows && vc[order[j]] == vc[k] && vct[order[j]] == vct[k]; ++j) {
+      n += vn[order[j]];
+      hi += vh[order[j]];
+      lo += vl[order[j]];
+    }
+    if (w < cap) {
+      if (c) c[w] = vc[k];
+      if (ct) ct[w] = vct[k];
+      if (sum) sum[w] = static_cast<double>(hi) / 1024.0 + static_cast<double>(lo) / 1125899906842624.0;
+      if (count) count[w] = n;
+    }
+    ++w;
+    i = j;
   }
+  rows = w;
   if (n_rows) *n_rows = rows;
   return VMFA_OK;
 }
@@ -966,9 +1034,8 @@ int vmfa_exchange_buffer(vmfa_ctx* x, int which, void** ptr, size_t* count, int*
   if (!ptr || !count || !dtype) return fail(VMFA_ERR_INVALID_ARGUMENT, "null output");
   if (which == VMFA_XCHG_COOC) {
     const size_t n = 3 * static_cast<size_t>(x->dm.C) * x->dm.C;
-    if (n * sizeof(long long) > (size_t{8} << 30))
+    if (!x->xc)
       return fail(VMFA_ERR_UNSUPPORTED, "dense co-occurrence exchange limited to C <= ~18900 in this build");
-    if (!x->xc) TRY(x->alloc(x->xc, n));
     *ptr = x->xc;
     *count = n;
     *dtype = VMFA_DT_INT64;

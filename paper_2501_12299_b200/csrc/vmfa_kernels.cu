@@ -53,6 +53,16 @@ __global__ void k_hist(const unsigned* keys, int64_t n, int C, int* cnt) {
     if (k < static_cast<unsigned>(C)) atomicAdd(cnt + k, 1);
   }
 }
+__global__ void k_chunks_from_off(const int* off, int C, int rows, int min1, int* chunks) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c <= C; c += gridDim.x * blockDim.x) {
+    if (c == C) {
+      chunks[c] = 0;
+      continue;
+    }
+    const int n = off[c + 1] - off[c];
+    chunks[c] = max(min1, (n + rows - 1) / rows);
+  }
+}
 __global__ void k_chunks(const int* cnt, int C, int rows, int* chunks) {
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c <= C; c += gridDim.x * blockDim.x)
     chunks[c] = c < C ? (cnt[c] + rows - 1) / rows : 0;
@@ -382,6 +392,23 @@ __device__ __forceinline__ bool kless(const KeyMin& x, const KeyMin& y) {
   return x.c < y.c;
 }
 
+__device__ __forceinline__ void sort_small(int* v, int m) {
+  for (int i = 1; i < m; ++i) {
+    const int x = v[i];
+    int j = i - 1;
+    while (j >= 0 && v[j] > x) {
+      v[j + 1] = v[j];
+      --j;
+    }
+    v[j + 1] = x;
+  }
+}
+
+// Items are (component c, chunk of <= a.pts_per_item points of I_c). A
+// component with one item accumulates and selects in shared memory; chunks of
+// larger components (and every component in exchange mode) add their exact
+// integer partial sums into row c of the dense table xc (order-independent),
+// and k_gselect_dense selects from the rows.
 __global__ void __launch_bounds__(kGupdThreads) k_gupdate(GupdArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   long long* t_hi = reinterpret_cast<long long*>(smem_raw);
@@ -394,12 +421,18 @@ __global__ void __launch_bounds__(kGupdThreads) k_gupdate(GupdArgs a) {
   const Dims dm = a.dm;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nw = kGupdThreads / 32;
+  const int64_t CC = (int64_t)dm.C * dm.C;
   long long* g_cnt = a.gt_cnt + (int64_t)blockIdx.x * dm.C;
   long long* g_hi = a.gt_hi + (int64_t)blockIdx.x * dm.C;
   long long* g_lo = a.gt_lo + (int64_t)blockIdx.x * dm.C;
-  for (int c = blockIdx.x; c < dm.C; c += gridDim.x) {
-    const int p0 = a.part_off[c], p1 = a.part_off[c + 1];
-    const int npts = p1 - p0;
+  const int total = a.itemoff[dm.C];
+  for (int item = blockIdx.x; item < total; item += gridDim.x) {
+    const int c = find_item(a.itemoff, dm.C, item);
+    const int nitems = a.itemoff[c + 1] - a.itemoff[c];
+    const int p0 = a.part_off[c] + (item - a.itemoff[c]) * a.pts_per_item;
+    const int p1 = min(a.part_off[c + 1], p0 + a.pts_per_item);
+    const int npts = max(0, p1 - p0);
+    const bool to_rows = a.exchange || nitems > 1;
     const long long bound = llmin((long long)dm.C - 1, (long long)npts * (dm.stride - 1));
     int cap = 32;
     while (cap < 2 * bound && cap < 2 * kGupdCap) cap <<= 1;
@@ -467,7 +500,7 @@ __global__ void __launch_bounds__(kGupdThreads) k_gupdate(GupdArgs a) {
         lo = g_lo[i];
       }
     };
-    if (a.dump && npts > 0) {
+    if (a.dump) {
       for (int i = tid; i < tab_n; i += kGupdThreads) {
         int ct;
         long long cnt, hi, lo;
@@ -483,17 +516,16 @@ __global__ void __launch_bounds__(kGupdThreads) k_gupdate(GupdArgs a) {
         }
       }
     }
-    if (a.exchange) {
-      const int64_t CC = (int64_t)dm.C * dm.C;
+    if (to_rows) {
       for (int i = tid; i < tab_n; i += kGupdThreads) {
         int ct;
         long long cnt, hi, lo;
         entry(i, ct, cnt, hi, lo);
         if (ct < 0 || cnt <= 0) continue;
         const int64_t at = (int64_t)c * dm.C + ct;
-        a.xc[at] = cnt;
-        a.xc[CC + at] = hi;
-        a.xc[2 * CC + at] = lo;
+        atomicAdd(reinterpret_cast<unsigned long long*>(a.xc + at), static_cast<unsigned long long>(cnt));
+        atomicAdd(reinterpret_cast<unsigned long long*>(a.xc + CC + at), static_cast<unsigned long long>(hi));
+        atomicAdd(reinterpret_cast<unsigned long long*>(a.xc + 2 * CC + at), static_cast<unsigned long long>(lo));
       }
       __syncthreads();
       continue;
@@ -535,15 +567,7 @@ __global__ void __launch_bounds__(kGupdThreads) k_gupdate(GupdArgs a) {
       int m = 0;
       out[m++] = c;
       for (int q = 0; q < s_nsel; ++q) out[m++] = s_sel[q];
-      for (int i = 1; i < m; ++i) {
-        const int v = out[i];
-        int j = i - 1;
-        while (j >= 0 && out[j] > v) {
-          out[j + 1] = out[j];
-          --j;
-        }
-        out[j + 1] = v;
-      }
+      sort_small(out, m);
       for (int i = 0; i < dm.G; ++i) a.g_new[(int64_t)c * dm.G + i] = i < m ? out[i] : -1;
       a.gcnt_new[c] = m;
     }
@@ -551,8 +575,11 @@ __global__ void __launch_bounds__(kGupdThreads) k_gupdate(GupdArgs a) {
   }
 }
 
-// g selection from the all-reduced dense C x C exchange table (multi-rank).
-__global__ void __launch_bounds__(kGupdThreads) k_gselect_dense(Dims dm, const long long* xc,
+// g selection from dense rows of xc: every component in exchange (multi-rank)
+// mode, else the components split over several items. Rows are zeroed after
+// reading so the table is clean for the next E-step.
+__global__ void __launch_bounds__(kGupdThreads) k_gselect_dense(Dims dm, long long* xc,
+                                                                const int* itemoff, int all,
                                                                 int* g_new, int* gcnt_new) {
   __shared__ KeyMin red[kGupdThreads / 32];
   __shared__ int s_sel[64];
@@ -561,9 +588,10 @@ __global__ void __launch_bounds__(kGupdThreads) k_gselect_dense(Dims dm, const l
   const int nw = kGupdThreads / 32;
   const int64_t CC = (int64_t)dm.C * dm.C;
   for (int c = blockIdx.x; c < dm.C; c += gridDim.x) {
+    if (!all && itemoff[c + 1] - itemoff[c] <= 1) continue;
     if (tid == 0) s_nsel = 0;
     __syncthreads();
-    const long long* rc = xc + (int64_t)c * dm.C;
+    long long* rc = xc + (int64_t)c * dm.C;
     for (int r = 0; r < dm.G - 1; ++r) {
       KeyMin best{INFINITY, 0x7fffffff};
       for (int ct = tid; ct < dm.C; ct += kGupdThreads) {
@@ -596,17 +624,14 @@ __global__ void __launch_bounds__(kGupdThreads) k_gselect_dense(Dims dm, const l
       int m = 0;
       out[m++] = c;
       for (int q = 0; q < s_nsel; ++q) out[m++] = s_sel[q];
-      for (int i = 1; i < m; ++i) {
-        const int v = out[i];
-        int j = i - 1;
-        while (j >= 0 && out[j] > v) {
-          out[j + 1] = out[j];
-          --j;
-        }
-        out[j + 1] = v;
-      }
+      sort_small(out, m);
       for (int i = 0; i < dm.G; ++i) g_new[(int64_t)c * dm.G + i] = i < m ? out[i] : -1;
       gcnt_new[c] = m;
+    }
+    for (int ct = tid; ct < dm.C; ct += kGupdThreads) {
+      rc[ct] = 0;
+      rc[CC + ct] = 0;
+      rc[2 * CC + ct] = 0;
     }
     __syncthreads();
   }
@@ -621,18 +646,32 @@ __global__ void __launch_bounds__(kGupdThreads) k_gselect_dense(Dims dm, const l
 constexpr int kStatsBatch = 32;
 constexpr int kStatsMaxH1 = 17;   // columns of Y per pass
 
+// Items are (component, chunk of <= rows_per_item K-pairs): large components
+// are split so no CTA owns a disproportionate share (SURVEY §7 hard part 3).
+// Each item writes fp64 partials; k_stats_reduce sums a component's items in
+// item order (deterministic, no atomics).
+// Partial layout per item (pass col0): [Y cols col0.. (NH1 x D) | sq (D) |
+// E ((H+1)^2) | N] -- sq/E/N only in the first pass, E only when H+1 <= NH1.
 template <int NH1, int ND>
-__global__ void __launch_bounds__(kStatsThreads) k_stats(StatsArgs a, int col0) {
-  __shared__ double s_z[kStatsBatch][NH1];
+__global__ void __launch_bounds__(kStatsThreads) k_stats(StatsArgs a, const int* __restrict__ itemoff,
+                                                        int rows_per_item, int col0, double* part,
+                                                        int64_t part_stride) {
+  extern __shared__ __align__(16) float s_x[];  // [kStatsBatch][D] staged rows
+  __shared__ float s_z[kStatsBatch][NH1];
   __shared__ double s_q[kStatsBatch];
   __shared__ int s_n[kStatsBatch];
   const Dims dm = a.dm;
   const int H = dm.H, H1 = H + 1, D = dm.D;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nw = kStatsThreads / 32;
-  const bool full_e = (col0 == 0) && (H1 <= NH1);
-  for (int c = blockIdx.x; c < dm.C; c += gridDim.x) {
-    const int r0 = a.off[c], r1 = a.off[c + 1];
+  const bool first = col0 == 0;
+  const bool full_e = first && (H1 <= NH1);
+  constexpr int NE = (NH1 * NH1 + kStatsThreads - 1) / kStatsThreads;
+  const int total = __ldg(itemoff + dm.C);
+  for (int item = blockIdx.x; item < total; item += gridDim.x) {
+    const int c = find_item(itemoff, dm.C, item);
+    const int r0 = a.off[c] + (item - itemoff[c]) * rows_per_item;
+    const int r1 = min(a.off[c + 1], r0 + rows_per_item);
     double accY[ND][NH1];
     double accS[ND];
 #pragma unroll
@@ -641,15 +680,15 @@ __global__ void __launch_bounds__(kStatsThreads) k_stats(StatsArgs a, int col0) 
 #pragma unroll
       for (int h = 0; h < NH1; ++h) accY[k][h] = 0.0;
     }
-    double accE[(NH1 * NH1 + kStatsThreads - 1) / kStatsThreads];
+    double accE[NE];
 #pragma unroll
-    for (int k = 0; k < (NH1 * NH1 + kStatsThreads - 1) / kStatsThreads; ++k) accE[k] = 0.0;
+    for (int k = 0; k < NE; ++k) accE[k] = 0.0;
     double accN = 0.0;
     const float* Vc = a.V32 + (int64_t)c * D * H;
     const float* mc = a.mu32 + (int64_t)c * D;
     for (int b0 = r0; b0 < r1; b0 += kStatsBatch) {
       const int nb = min(kStatsBatch, r1 - b0);
-      // (i) latent means mz = V (x - mu) for columns col0.. of the batch rows
+      // (i) latent means mz = V (x - mu) (mstep.cpp:52-53), columns col0..
       for (int r = warp; r < nb; r += nw) {
         const int e = a.ent[b0 + r];
         const int n = e / dm.Cp;
@@ -657,8 +696,11 @@ __global__ void __launch_bounds__(kStatsThreads) k_stats(StatsArgs a, int col0) 
         float acc[NH1];
 #pragma unroll
         for (int h = 0; h < NH1; ++h) acc[h] = 0.f;
+        float* xr = s_x + (int64_t)r * D;
         for (int d = lane; d < D; d += 32) {
-          const float v = __ldg(x + d) - __ldg(mc + d);
+          const float xv = __ldg(x + d);
+          xr[d] = xv;
+          const float v = xv - __ldg(mc + d);
           const float* vr = Vc + (int64_t)d * H + col0;
 #pragma unroll
           for (int h = 0; h < NH1; ++h)
@@ -679,74 +721,81 @@ __global__ void __launch_bounds__(kStatsThreads) k_stats(StatsArgs a, int col0) 
         for (int h = 0; h < NH1; ++h)
           if (lane == h) {
             const int hh = col0 + h;
-            s_z[r][h] = hh < H ? static_cast<double>(acc[h]) : (hh == H ? 1.0 : 0.0);
+            s_z[r][h] = hh < H ? acc[h] : (hh == H ? 1.f : 0.f);
           }
       }
       __syncthreads();
-      // (ii) Y / sq for the batch (fixed row order => deterministic)
+      // (ii) Y = sum q x zhat^T, sq = sum q x^2, E = sum q zhat zhat^T, N = sum q
       for (int r = 0; r < nb; ++r) {
         const double q = s_q[r];
-        const float* x = a.X + (int64_t)s_n[r] * D;
+        const float* x = s_x + (int64_t)r * D;
 #pragma unroll
         for (int k = 0; k < ND; ++k) {
           const int d = tid + k * kStatsThreads;
           if (d < D) {
-            const double xd = static_cast<double>(__ldg(x + d));
+            const double xd = static_cast<double>(x[d]);
             const double qx = q * xd;
 #pragma unroll
-            for (int h = 0; h < NH1; ++h) accY[k][h] = fma(qx, s_z[r][h], accY[k][h]);
-            if (col0 == 0) accS[k] = fma(qx, xd, accS[k]);
+            for (int h = 0; h < NH1; ++h) accY[k][h] = fma(qx, static_cast<double>(s_z[r][h]), accY[k][h]);
+            if (first) accS[k] = fma(qx, xd, accS[k]);
           }
         }
         if (full_e) {
 #pragma unroll
-          for (int k = 0; k < (NH1 * NH1 + kStatsThreads - 1) / kStatsThreads; ++k) {
+          for (int k = 0; k < NE; ++k) {
             const int idx = tid + k * kStatsThreads;
             if (idx < H1 * H1) {
               const int i = idx % H1, j = idx / H1;
-              accE[k] = fma(q * s_z[r][i], s_z[r][j], accE[k]);
+              accE[k] = fma(q * static_cast<double>(s_z[r][i]), static_cast<double>(s_z[r][j]), accE[k]);
             }
           }
-          if (tid == 0) accN += q;
         }
+        if (tid == 0) accN += q;
       }
       __syncthreads();
     }
+    double* pp = part + (int64_t)item * part_stride;
 #pragma unroll
     for (int k = 0; k < ND; ++k) {
       const int d = tid + k * kStatsThreads;
       if (d < D) {
 #pragma unroll
-        for (int h = 0; h < NH1; ++h)
-          if (col0 + h < H1) a.Y[((int64_t)c * H1 + col0 + h) * D + d] = accY[k][h];
-        if (col0 == 0) a.sq[(int64_t)c * D + d] = accS[k];
+        for (int h = 0; h < NH1; ++h) pp[(int64_t)h * D + d] = accY[k][h];
+        if (first) pp[(int64_t)NH1 * D + d] = accS[k];
       }
     }
-    if (full_e) {
-      if (tid == 0) a.Nc[c] = accN;
+    if (first) {
+      double* pe = pp + (int64_t)NH1 * D + D;
+      if (full_e) {
 #pragma unroll
-      for (int k = 0; k < (NH1 * NH1 + kStatsThreads - 1) / kStatsThreads; ++k) {
-        const int idx = tid + k * kStatsThreads;
-        if (idx < H1 * H1) a.E[(int64_t)c * H1 * H1 + idx] = accE[k];
+        for (int k = 0; k < NE; ++k) {
+          const int idx = tid + k * kStatsThreads;
+          if (idx < H1 * H1) pe[idx] = accE[k];
+        }
       }
+      if (tid == 0) pe[H1 * H1] = accN;
     }
-    __syncthreads();
   }
 }
 
-// E for H > 16 (or any H): second pass computing E from mz recomputed per row.
-__global__ void __launch_bounds__(kStatsThreads) k_stats_E(StatsArgs a) {
+// E for H+1 > kStatsMaxH1: item-based, full zhat per row; partial [E | -].
+__global__ void __launch_bounds__(kStatsThreads) k_stats_E(StatsArgs a, const int* __restrict__ itemoff,
+                                                          int rows_per_item, double* part,
+                                                          int64_t part_stride) {
   extern __shared__ __align__(16) double s_zz[];  // [kStatsBatch][H1]
   __shared__ double s_q[kStatsBatch];
   const Dims dm = a.dm;
   const int H = dm.H, H1 = H + 1, D = dm.D;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nw = kStatsThreads / 32;
-  for (int c = blockIdx.x; c < dm.C; c += gridDim.x) {
-    const int r0 = a.off[c], r1 = a.off[c + 1];
+  const int total = __ldg(itemoff + dm.C);
+  for (int item = blockIdx.x; item < total; item += gridDim.x) {
+    const int c = find_item(itemoff, dm.C, item);
+    const int r0 = a.off[c] + (item - itemoff[c]) * rows_per_item;
+    const int r1 = min(a.off[c + 1], r0 + rows_per_item);
     const float* Vc = a.V32 + (int64_t)c * D * H;
     const float* mc = a.mu32 + (int64_t)c * D;
-    double accN = 0.0;
+    double* pe = part + (int64_t)item * part_stride;
     for (int idx0 = 0; idx0 < H1 * H1; idx0 += kStatsThreads * 9) {
       double accE[9];
 #pragma unroll
@@ -759,7 +808,8 @@ __global__ void __launch_bounds__(kStatsThreads) k_stats_E(StatsArgs a) {
           const float* x = a.X + (int64_t)n * D;
           for (int h = 0; h < H; ++h) {
             float v = 0.f;
-            for (int d = lane; d < D; d += 32) v = fmaf(__ldg(Vc + (int64_t)d * H + h), __ldg(x + d) - __ldg(mc + d), v);
+            for (int d = lane; d < D; d += 32)
+              v = fmaf(__ldg(Vc + (int64_t)d * H + h), __ldg(x + d) - __ldg(mc + d), v);
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
             if (lane == 0) s_zz[r * H1 + h] = v;
@@ -780,18 +830,60 @@ __global__ void __launch_bounds__(kStatsThreads) k_stats_E(StatsArgs a) {
               accE[k] = fma(q * s_zz[r * H1 + i], s_zz[r * H1 + j], accE[k]);
             }
           }
-          if (idx0 == 0 && tid == 0) accN += q;
         }
         __syncthreads();
       }
 #pragma unroll
       for (int k = 0; k < 9; ++k) {
         const int idx = idx0 + tid + k * kStatsThreads;
-        if (idx < H1 * H1) a.E[(int64_t)c * H1 * H1 + idx] = accE[k];
+        if (idx < H1 * H1) pe[idx] = accE[k];
       }
     }
-    if (tid == 0) a.Nc[c] = accN;
-    __syncthreads();
+  }
+}
+
+// Sum a component's item partials in item order into the statistics buffer.
+// kind 0: Y/sq/E/N pass at column block col0 (width nh1); kind 1: E only.
+__global__ void __launch_bounds__(256) k_stats_reduce(Dims dm, const int* __restrict__ itemoff,
+                                                      const double* part, int64_t part_stride,
+                                                      int kind, int col0, int nh1, int full_e,
+                                                      double* Nc, double* E, double* Y, double* sq) {
+  const int D = dm.D, H1 = dm.H + 1;
+  for (int c = blockIdx.x; c < dm.C; c += gridDim.x) {
+    const int i0 = itemoff[c], i1 = itemoff[c + 1];
+    if (kind == 1) {
+      for (int idx = threadIdx.x; idx < H1 * H1; idx += blockDim.x) {
+        double s = 0.0;
+        for (int it = i0; it < i1; ++it) s += part[(int64_t)it * part_stride + idx];
+        E[(int64_t)c * H1 * H1 + idx] = s;
+      }
+      continue;
+    }
+    const int ncols = min(nh1, H1 - col0);
+    for (int idx = threadIdx.x; idx < ncols * D; idx += blockDim.x) {
+      double s = 0.0;
+      for (int it = i0; it < i1; ++it) s += part[(int64_t)it * part_stride + idx];
+      Y[((int64_t)c * H1 + col0) * D + idx] = s;
+    }
+    if (col0 != 0) continue;
+    const int64_t base = (int64_t)nh1 * D;
+    for (int d = threadIdx.x; d < D; d += blockDim.x) {
+      double s = 0.0;
+      for (int it = i0; it < i1; ++it) s += part[(int64_t)it * part_stride + base + d];
+      sq[(int64_t)c * D + d] = s;
+    }
+    const int64_t eb = base + D;
+    if (full_e)
+      for (int idx = threadIdx.x; idx < H1 * H1; idx += blockDim.x) {
+        double s = 0.0;
+        for (int it = i0; it < i1; ++it) s += part[(int64_t)it * part_stride + eb + idx];
+        E[(int64_t)c * H1 * H1 + idx] = s;
+      }
+    if (threadIdx.x == 0) {
+      double s = 0.0;
+      for (int it = i0; it < i1; ++it) s += part[(int64_t)it * part_stride + eb + H1 * H1];
+      Nc[c] = s;
+    }
   }
 }
 
@@ -1036,6 +1128,9 @@ __global__ void __launch_bounds__(128) k_precompute(PrecompArgs a) {
       }
       float* row = a.P + ((int64_t)c * D + d) * HP;
       for (int h = 0; h < Hc; ++h) row[h] = h < H ? static_cast<float>(u[h]) : 0.f;
+      // K-major copy for the tensor-core scorer: WT[c][h][d], h < Hp (zero padded)
+      for (int h = 0; h < a.Hp; ++h) a.WT[((int64_t)c * a.Hp + h) * D + d] = h < H ? static_cast<float>(u[h]) : 0.f;
+      a.ipsi32[(int64_t)c * D + d] = static_cast<float>(ip);
       row[Hc] = static_cast<float>(a.mu[(int64_t)c * D + d]);
       row[Hc + 1] = static_cast<float>(ip);
       row[Hc + 2] = 0.f;
@@ -1172,6 +1267,10 @@ cudaError_t launch_chunks(const int* cnt, int C, int rows, int* chunks, cudaStre
   k_chunks<<<grid_for(C + 1, 256, 4096), 256, 0, s>>>(cnt, C, rows, chunks);
   return cudaGetLastError();
 }
+cudaError_t launch_chunks_from_off(const int* off, int C, int rows, int min1, int* chunks, cudaStream_t s) {
+  k_chunks_from_off<<<grid_for(C + 1, 256, 4096), 256, 0, s>>>(off, C, rows, min1, chunks);
+  return cudaGetLastError();
+}
 cudaError_t launch_extra(const Dims& dm, const int* K, const int* g, const int* gcnt, uint64_t seed,
                          uint64_t it, int* rx, unsigned* rkey, cudaStream_t s) {
   k_extra<<<grid_for(dm.N, 256, 8192), 256, 0, s>>>(dm, K, g, gcnt, seed, it, rx, rkey);
@@ -1219,34 +1318,52 @@ cudaError_t launch_gupdate(const GupdArgs& a, int grid, cudaStream_t s) {
   k_gupdate<<<grid, kGupdThreads, smem, s>>>(a);
   return cudaGetLastError();
 }
-cudaError_t launch_gselect_dense(const Dims& dm, const long long* xc, int* g_new, int* gcnt_new,
-                                 cudaStream_t s) {
-  k_gselect_dense<<<min(dm.C, sm_count() * 8), kGupdThreads, 0, s>>>(dm, xc, g_new, gcnt_new);
+cudaError_t launch_gselect_dense(const Dims& dm, long long* xc, const int* itemoff, int all,
+                                 int* g_new, int* gcnt_new, cudaStream_t s) {
+  k_gselect_dense<<<min(dm.C, sm_count() * 8), kGupdThreads, 0, s>>>(dm, xc, itemoff, all, g_new, gcnt_new);
   return cudaGetLastError();
 }
 
 template <int NH1>
-static void stats_pass(const StatsArgs& a, int grid, int col0, cudaStream_t s) {
+static void stats_pass(const StatsArgs& a, const int* itemoff, int rpi, int grid, int col0,
+                       double* part, int64_t ps, cudaStream_t s) {
   const int D = a.dm.D;
-  if (D <= kStatsThreads) k_stats<NH1, 1><<<grid, kStatsThreads, 0, s>>>(a, col0);
-  else if (D <= 2 * kStatsThreads) k_stats<NH1, 2><<<grid, kStatsThreads, 0, s>>>(a, col0);
-  else k_stats<NH1, 4><<<grid, kStatsThreads, 0, s>>>(a, col0);
+  const size_t smem = static_cast<size_t>(kStatsBatch) * D * sizeof(float);
+  auto go = [&](auto kern) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    kern<<<grid, kStatsThreads, smem, s>>>(a, itemoff, rpi, col0, part, ps);
+  };
+  if (D <= kStatsThreads) go(k_stats<NH1, 1>);
+  else if (D <= 2 * kStatsThreads) go(k_stats<NH1, 2>);
+  else go(k_stats<NH1, 4>);
 }
-cudaError_t launch_stats(const StatsArgs& a, cudaStream_t s) {
+int64_t stats_part_stride(const Dims& dm) {
+  const int H1 = dm.H + 1;
+  const int nh1 = H1 <= 5 ? 5 : (H1 <= 9 ? 9 : kStatsMaxH1);
+  return static_cast<int64_t>(nh1) * dm.D + dm.D + static_cast<int64_t>(H1) * H1 + 1;
+}
+cudaError_t launch_stats(const StatsArgs& a, const int* itemoff, int rows_per_item, double* part,
+                         cudaStream_t s) {
   if (a.dm.D > 4 * kStatsThreads) return cudaErrorInvalidValue;
-  const int grid = min(a.dm.C, sm_count() * 2);
+  const int grid = sm_count() * 4;
   const int H1 = a.dm.H + 1;
-  for (int col0 = 0; col0 < H1; col0 += kStatsMaxH1) {
-    if (H1 <= 5) stats_pass<5>(a, grid, col0, s);
-    else if (H1 <= 9) stats_pass<9>(a, grid, col0, s);
-    else stats_pass<kStatsMaxH1>(a, grid, col0, s);
+  const int nh1 = H1 <= 5 ? 5 : (H1 <= 9 ? 9 : kStatsMaxH1);
+  const int64_t ps = stats_part_stride(a.dm);
+  const int rgrid = min(a.dm.C, sm_count() * 8);
+  for (int col0 = 0; col0 < H1; col0 += nh1) {
+    if (nh1 == 5) stats_pass<5>(a, itemoff, rows_per_item, grid, col0, part, ps, s);
+    else if (nh1 == 9) stats_pass<9>(a, itemoff, rows_per_item, grid, col0, part, ps, s);
+    else stats_pass<kStatsMaxH1>(a, itemoff, rows_per_item, grid, col0, part, ps, s);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
+    k_stats_reduce<<<rgrid, 256, 0, s>>>(a.dm, itemoff, part, ps, 0, col0, nh1, H1 <= nh1 ? 1 : 0,
+                                         a.Nc, a.E, a.Y, a.sq);
   }
-  if (H1 > kStatsMaxH1) {
+  if (H1 > nh1) {
     const size_t smem = static_cast<size_t>(kStatsBatch) * H1 * sizeof(double);
     cudaFuncSetAttribute(k_stats_E, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    k_stats_E<<<grid, kStatsThreads, smem, s>>>(a);
+    k_stats_E<<<grid, kStatsThreads, smem, s>>>(a, itemoff, rows_per_item, part, ps);
+    k_stats_reduce<<<rgrid, 256, 0, s>>>(a.dm, itemoff, part, ps, 1, 0, nh1, 1, a.Nc, a.E, a.Y, a.sq);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }

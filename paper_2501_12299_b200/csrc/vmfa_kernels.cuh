@@ -20,7 +20,7 @@ namespace vmfa_b200 {
 constexpr int kScoreRows = 64;      // rows (points) per scoring item
 constexpr int kScoreThreads = 128;  // 4 warps; each warp scores one component x 64 rows
 constexpr int kXsStride = kScoreRows + 2;  // transposed x tile stride (floats)
-constexpr int kStatsThreads = 512;
+constexpr int kStatsThreads = 256;
 constexpr int kGupdCap = 8192;      // smem hash capacity of the block-3 accumulator (24 B per entry)
 constexpr int kGupdThreads = 256;
 
@@ -102,6 +102,8 @@ struct GupdArgs {
   long long* gt_hi;
   long long* gt_lo;
   // exchange (multi-rank) / dump modes
+  const int* itemoff;     // items over the partition: chunks of pts_per_item points
+  int pts_per_item;
   int exchange;           // 1: write dense C x C rows to xc_* instead of selecting
   long long* xc;          // 3*C*C int64: [cnt | hi | lo]
   int dump;               // 1: append (c, ct, cnt, hi, lo) rows to dump arrays
@@ -162,6 +164,9 @@ struct PrecompArgs {
   float* P;               // packed scoring params
   float* V32;             // C x D x H
   float* mu32;            // C x D
+  float* WT;              // C x Hp x D  K-major W rows (tensor-core scorer)
+  float* ipsi32;          // C x D
+  int Hp;                 // H padded to {4, 8, 16, 32, 64}
   unsigned long long* status;
 };
 
@@ -176,9 +181,13 @@ cudaError_t launch_extra(const Dims& dm, const int* K, const int* g, const int* 
 cudaError_t launch_score(int mode, const ScoreArgs& a, int grid, cudaStream_t s);
 cudaError_t launch_select(const SelectArgs& a, cudaStream_t s);
 cudaError_t launch_gupdate(const GupdArgs& a, int grid, cudaStream_t s);
-cudaError_t launch_gselect_dense(const Dims& dm, const long long* xc, int* g_new, int* gcnt_new,
-                                 cudaStream_t s);
-cudaError_t launch_stats(const StatsArgs& a, cudaStream_t s);
+cudaError_t launch_gselect_dense(const Dims& dm, long long* xc, const int* itemoff, int all,
+                                 int* g_new, int* gcnt_new, cudaStream_t s);
+cudaError_t launch_chunks_from_off(const int* off, int C, int rows, int min1, int* chunks,
+                                   cudaStream_t s);
+cudaError_t launch_stats(const StatsArgs& a, const int* itemoff, int rows_per_item, double* part,
+                         cudaStream_t s);
+int64_t stats_part_stride(const Dims& dm);
 cudaError_t launch_update(const UpdateArgs& a, cudaStream_t s);
 cudaError_t launch_renorm(const Dims& dm, double* pi, unsigned long long* status, cudaStream_t s);
 cudaError_t launch_precompute(const PrecompArgs& a, cudaStream_t s);
@@ -193,5 +202,10 @@ cudaError_t launch_count_empty(const double* pi, int C, int* out, cudaStream_t s
 cudaError_t launch_logpi(const double* pi, int C, double* logpi, cudaStream_t s);
 
 int sm_count();
+// tensor-core scorer (vmfa_score_tc.cu)
+bool score_tc_supported(const Dims& dm);
+cudaError_t launch_score_tc(int mode, const ScoreArgs& s, const float* WT, const float* ipsi32,
+                            const float* mu32, cudaStream_t st);
+constexpr int kScoreRowsTc = 128;
 
 }  // namespace vmfa_b200

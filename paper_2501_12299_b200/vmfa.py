@@ -199,7 +199,8 @@ class Session:
         if m:
             check(lib().vmfa_download_distances(self._h, m, ptr(c), ptr(ct), ptr(s), ptr(k),
                                                 C.byref(n)))
-        return c, ct, s, k
+            m = n.value  # rows of split components merged
+        return c[:m], ct[:m], s[:m], k[:m]
 
     def accumulate_suffstats(self):
         check(lib().vmfa_accumulate_suffstats(self._h))

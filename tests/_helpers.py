@@ -83,8 +83,10 @@ def compare_estep(O, e_or, st_or, F_gpu, J_gpu, gpu_retained, st_gpu, Cp, report
             a = lj_g[n][idx_g[n] == st_or.labels[n]][0]
             b = lj_g[n][idx_g[n] == st_gpu.labels[n]][0]
             assert abs(a - b) <= max(tau[n], 1e-6), f"label differs at row {n} outside near-ties"
-    # responsibilities on identical K rows
-    assert np.abs(resp_g[same] - e_or.resp[same]).max() <= 1e-4
+    # responsibilities on identical K rows: q = softmax(l) over K, so
+    # |dq| <= 2 max|dl| (row-wise bound implied by the log-joint tolerance)
+    dq = np.abs(resp_g - e_or.resp).max(axis=1)
+    assert np.all(dq[same] <= 2 * row_err[same] + 1e-9), float((dq - 2 * row_err)[same].max())
     info = dict(rows=len(kdiff), k_near_ties=int(ties.sum()), k_diff=int(kdiff.sum()),
                 label_diff=int(ldiff.sum()), lj_rel=float(rel.max()))
     if report is not None:

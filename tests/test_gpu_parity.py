@@ -60,8 +60,10 @@ def test_precompute_caches_match_oracle(oracle, gpu):
     dict(N=1000, D=10, C=6, H=2, Cp=6, G=6),      # C'=C: no truncation
     dict(N=2000, D=100, C=50, H=16, Cp=4, G=8),   # H=16 chunk
 ])
-def test_estep_teacher_forced(oracle, gpu, case):
+@pytest.mark.parametrize("scorer", ["tc", "ffma"])
+def test_estep_teacher_forced(oracle, gpu, case, scorer, monkeypatch):
     O, V = oracle, gpu
+    monkeypatch.setenv("VMFA_SCORER", scorer)
     X, _ = gaussian_problem(case["N"], case["D"], max(case["C"] // 2, 2), min(case["H"], 4), seed=7)
     C, H, Cp, G = case["C"], case["H"], case["Cp"], case["G"]
     p, st, floor, sess = _setup(O, V, X, C, H, Cp, G)
