@@ -214,12 +214,9 @@ int csr_by_key(vmfa_ctx* x, const unsigned* keys, int64_t n, int* off, int* ent,
   size_t tb = x->cub_bytes;
   CU(cub::DeviceRadixSort::SortPairs(x->cub_tmp, tb, keys, x->keys_alt, x->vals, ent,
                                      static_cast<int>(n), 0, bits_for(static_cast<unsigned>(C)), s));
-  CU(cudaMemsetAsync(x->cnt, 0, sizeof(int) * (C + 1), s));
-  CU(launch_hist(keys, n, C, x->cnt, s));
-  tb = x->cub_bytes;
-  CU(cub::DeviceScan::ExclusiveSum(x->cub_tmp, tb, x->cnt, off, C + 1, s));
+  CU(launch_offsets_sorted(x->keys_alt, n, C, off, s));
   if (items) {
-    CU(launch_chunks(x->cnt, C, rows_per_item, x->chunks, s));
+    CU(launch_chunks_from_off(off, C, rows_per_item, 0, x->chunks, s));
     tb = x->cub_bytes;
     CU(cub::DeviceScan::ExclusiveSum(x->cub_tmp, tb, x->chunks, items, C + 1, s));
   }

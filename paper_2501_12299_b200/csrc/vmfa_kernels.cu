@@ -9,6 +9,7 @@
 // row is read from HBM/L2 C' times per iteration instead of |S(n)| times.
 // Duplicates across anchors are scored but dropped by k_select, which also
 // reproduces the reference's insertion order, tie rules and counters exactly.
+#include <algorithm>
 #include <cfloat>
 #include <cmath>
 #include <cstdint>
@@ -46,6 +47,18 @@ __global__ void k_fill_i32(int* v, int64_t n, int value) {
 __global__ void k_keys_from_i32(const int* src, unsigned* keys, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     keys[i] = static_cast<unsigned>(src[i]);
+}
+// off[c] = first index i with sorted[i] >= c (lower bound); off[C] = #keys < C.
+__global__ void k_offsets_sorted(const unsigned* sorted, int64_t n, int C, int* off) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c <= C; c += gridDim.x * blockDim.x) {
+    int64_t lo = 0, hi = n;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (sorted[mid] < static_cast<unsigned>(c)) lo = mid + 1;
+      else hi = mid;
+    }
+    off[c] = static_cast<int>(lo);
+  }
 }
 __global__ void k_hist(const unsigned* keys, int64_t n, int C, int* cnt) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -648,132 +661,291 @@ constexpr int kStatsMaxH1 = 17;   // columns of Y per pass
 
 // Items are (component, chunk of <= rows_per_item K-pairs): large components
 // are split so no CTA owns a disproportionate share (SURVEY §7 hard part 3).
-// Each item writes fp64 partials; k_stats_reduce sums a component's items in
-// item order (deterministic, no atomics).
+// Per batch of 32 rows (cp.async double-buffered into smem):
+//   (i)  mz = V (x - mu) (mstep.cpp:52-53): lane = row, warp = 1/8 of the
+//        dimensions, V rows broadcast from smem; warp partials summed in smem.
+//   (ii) Y += q x zhat^T, sq += q x^2 (fp64): each thread owns a 4-dim x NH1
+//        register tile over a row group; E += q zhat zhat^T, N += q.
+// Sole-item components write their statistics directly; split components
+// write fp64 partials summed by k_stats_reduce in item order (deterministic).
 // Partial layout per item (pass col0): [Y cols col0.. (NH1 x D) | sq (D) |
 // E ((H+1)^2) | N] -- sq/E/N only in the first pass, E only when H+1 <= NH1.
+constexpr int kXPad = 4;  // s_x row stride D + 4: conflict-free LDS.128 across rows
+
 template <int NH1, int ND>
 __global__ void __launch_bounds__(kStatsThreads) k_stats(StatsArgs a, const int* __restrict__ itemoff,
                                                         int rows_per_item, int col0, double* part,
-                                                        int64_t part_stride) {
-  extern __shared__ __align__(16) float s_x[];  // [kStatsBatch][D] staged rows
-  __shared__ float s_z[kStatsBatch][NH1];
-  __shared__ double s_q[kStatsBatch];
-  __shared__ int s_n[kStatsBatch];
+                                                        int64_t part_stride, int nbuf) {
+  // smem: s_x [nbuf][B][D+4] | s_V [D][VS] | s_mu [D] | s_pz [8][B][NH1] | s_zd [B][NH1] (double)
+  extern __shared__ __align__(16) float s_x[];
+  constexpr int VS = (NH1 + 3) / 4 * 4;  // V row stride (16-byte rows for LDS.128)
+  __shared__ double s_qb[2][kStatsBatch];
+  __shared__ int s_e[2][kStatsBatch];
   const Dims dm = a.dm;
   const int H = dm.H, H1 = H + 1, D = dm.D;
+  const int XS = (D + 3) / 4 * 4 + kXPad;
+  float* s_V = s_x + (int64_t)nbuf * kStatsBatch * XS;
+  float* s_mu = s_V + (int64_t)D * VS;
+  float* s_pz = s_mu + (D + 3) / 4 * 4 + 4;                 // [8][B][NH1]
+  double* s_zd = reinterpret_cast<double*>(s_pz + 8 * kStatsBatch * NH1 + 2);  // 8-byte aligned
+  s_zd = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(s_zd) + 15) & ~uintptr_t(15));
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int nw = kStatsThreads / 32;
   const bool first = col0 == 0;
   const bool full_e = first && (H1 <= NH1);
+  const bool vec = (D & 3) == 0;
   constexpr int NE = (NH1 * NH1 + kStatsThreads - 1) / kStatsThreads;
+  // phase (ii) tiling: GD dimension groups of 4, RG row groups
+  const int GD = (D + 3) / 4;
+  const int RG = max(1, kStatsThreads / GD);
+  const int my_dg = tid % GD, my_rg = tid / GD;
+  const bool tile_on = my_rg < RG && tid < RG * GD;
+  // phase (i) dimension slice of this warp
+  const int dsl = ((D + 7) / 8 + 3) / 4 * 4;  // dims per warp, multiple of 4
+  const int dw0 = warp * dsl, dw1 = min(D, dw0 + dsl);
   const int total = __ldg(itemoff + dm.C);
   for (int item = blockIdx.x; item < total; item += gridDim.x) {
     const int c = find_item(itemoff, dm.C, item);
     const int r0 = a.off[c] + (item - itemoff[c]) * rows_per_item;
     const int r1 = min(a.off[c + 1], r0 + rows_per_item);
-    double accY[ND][NH1];
-    double accS[ND];
+    const bool direct = itemoff[c + 1] - itemoff[c] == 1;  // sole item: write the statistics
+    // centred statistics (v = x - mu_c): Y_v = sum q v zhat^T, sq_v = sum q v^2
+    // in fp32 over the item; k_stats_uncenter restores Y and sq in fp64
+    float accY[ND][4][NH1];
+    float accS[ND][4];
 #pragma unroll
-    for (int k = 0; k < ND; ++k) {
-      accS[k] = 0.0;
+    for (int k = 0; k < ND; ++k)
 #pragma unroll
-      for (int h = 0; h < NH1; ++h) accY[k][h] = 0.0;
-    }
+      for (int i = 0; i < 4; ++i) {
+        accS[k][i] = 0.f;
+#pragma unroll
+        for (int h = 0; h < NH1; ++h) accY[k][i][h] = 0.f;
+      }
     double accE[NE];
 #pragma unroll
     for (int k = 0; k < NE; ++k) accE[k] = 0.0;
-    double accN = 0.0;
     const float* Vc = a.V32 + (int64_t)c * D * H;
     const float* mc = a.mu32 + (int64_t)c * D;
-    for (int b0 = r0; b0 < r1; b0 += kStatsBatch) {
+    __syncthreads();  // previous item done with the shared buffers
+    for (int i = tid; i < D * VS; i += kStatsThreads) {
+      const int d = i / VS, h = i - d * VS;
+      s_V[i] = (h < NH1 && col0 + h < H) ? __ldg(Vc + (int64_t)d * H + col0 + h) : 0.f;
+    }
+    for (int d = tid; d < D; d += kStatsThreads) s_mu[d] = __ldg(mc + d);
+    const int nbat = (r1 - r0 + kStatsBatch - 1) / kStatsBatch;
+    auto stage_ids = [&](int b, int buf) {
+      if (tid < kStatsBatch) {
+        const int i = r0 + b * kStatsBatch + tid;
+        const int e = i < r1 ? a.ent[i] : -1;
+        s_e[buf][tid] = e;
+        s_qb[buf][tid] = e >= 0 ? a.resp[e] : 0.0;
+      }
+    };
+    auto issue_rows = [&](int buf) {
+      float* dst = s_x + (int64_t)buf * kStatsBatch * XS;
+      if (vec) {
+        const int D4 = D >> 2;
+        for (int i = tid; i < kStatsBatch * D4; i += kStatsThreads) {
+          const int r = i / D4, f = i - r * D4;
+          const int e = s_e[buf][r];
+          if (e < 0) continue;
+          const float* src = a.X + (int64_t)(e / dm.Cp) * D + 4 * f;
+          const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(dst + (int64_t)r * XS + 4 * f));
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(src) : "memory");
+        }
+      } else {
+        for (int i = tid; i < kStatsBatch * D; i += kStatsThreads) {
+          const int r = i / D, f = i - r * D;
+          const int e = s_e[buf][r];
+          if (e < 0) continue;
+          const float* src = a.X + (int64_t)(e / dm.Cp) * D + f;
+          const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(dst + (int64_t)r * XS + f));
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(src) : "memory");
+        }
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    stage_ids(0, 0);
+    __syncthreads();
+    issue_rows(0);
+    for (int bi = 0; bi < nbat; ++bi) {
+      const int buf = nbuf == 2 ? (bi & 1) : 0;
+      const int b0 = r0 + bi * kStatsBatch;
       const int nb = min(kStatsBatch, r1 - b0);
-      // (i) latent means mz = V (x - mu) (mstep.cpp:52-53), columns col0..
-      for (int r = warp; r < nb; r += nw) {
-        const int e = a.ent[b0 + r];
-        const int n = e / dm.Cp;
-        const float* x = a.X + (int64_t)n * D;
+      if (nbuf == 1) {
+        if (bi > 0) {
+          stage_ids(bi, 0);
+          __syncthreads();
+          issue_rows(0);
+        }
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+      } else if (bi + 1 < nbat) {
+        stage_ids(bi + 1, buf ^ 1);
+        __syncthreads();
+        issue_rows(buf ^ 1);
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+      } else {
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+      }
+      __syncthreads();
+      const float* xb = s_x + (int64_t)buf * kStatsBatch * XS;
+      // (i) partial mz over this warp's dimension slice, lane = row
+      {
         float acc[NH1];
 #pragma unroll
         for (int h = 0; h < NH1; ++h) acc[h] = 0.f;
-        float* xr = s_x + (int64_t)r * D;
-        for (int d = lane; d < D; d += 32) {
-          const float xv = __ldg(x + d);
-          xr[d] = xv;
-          const float v = xv - __ldg(mc + d);
-          const float* vr = Vc + (int64_t)d * H + col0;
+        const float* xr = xb + (int64_t)lane * XS;
+        if (lane < nb) {
+          for (int d = dw0; d < dw1; d += 4) {
+            const float4 xv = *reinterpret_cast<const float4*>(xr + d);
+            const float4 mv = *reinterpret_cast<const float4*>(s_mu + d);
+            const float v4[4] = {xv.x - mv.x, xv.y - mv.y, xv.z - mv.z, xv.w - mv.w};
 #pragma unroll
-          for (int h = 0; h < NH1; ++h)
-            if (col0 + h < H) acc[h] = fmaf(__ldg(vr + h), v, acc[h]);
-        }
+            for (int k = 0; k < 4; ++k) {
+              if (d + k >= dw1) break;
+              const float* vr = s_V + (d + k) * VS;
 #pragma unroll
-        for (int h = 0; h < NH1; ++h) {
-          float v = acc[h];
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
-          acc[h] = v;
-        }
-        if (lane == 0) {
-          s_n[r] = n;
-          s_q[r] = a.resp[e];
-        }
-#pragma unroll
-        for (int h = 0; h < NH1; ++h)
-          if (lane == h) {
-            const int hh = col0 + h;
-            s_z[r][h] = hh < H ? acc[h] : (hh == H ? 1.f : 0.f);
+              for (int h4 = 0; h4 < VS; h4 += 4) {
+                const float4 w = *reinterpret_cast<const float4*>(vr + h4);
+                if (h4 + 0 < NH1) acc[h4 + 0] = fmaf(w.x, v4[k], acc[h4 + 0]);
+                if (h4 + 1 < NH1) acc[h4 + 1] = fmaf(w.y, v4[k], acc[h4 + 1]);
+                if (h4 + 2 < NH1) acc[h4 + 2] = fmaf(w.z, v4[k], acc[h4 + 2]);
+                if (h4 + 3 < NH1) acc[h4 + 3] = fmaf(w.w, v4[k], acc[h4 + 3]);
+              }
+            }
           }
+        }
+        float* pz = s_pz + ((int64_t)warp * kStatsBatch + lane) * NH1;
+#pragma unroll
+        for (int h = 0; h < NH1; ++h) pz[h] = acc[h];
       }
       __syncthreads();
-      // (ii) Y = sum q x zhat^T, sq = sum q x^2, E = sum q zhat zhat^T, N = sum q
-      for (int r = 0; r < nb; ++r) {
-        const double q = s_q[r];
-        const float* x = s_x + (int64_t)r * D;
+      const double* s_q = s_qb[buf];
+      for (int i = tid; i < kStatsBatch * NH1; i += kStatsThreads) {
+        const int r = i / NH1, h = i - r * NH1;
+        float z = 0.f;
 #pragma unroll
-        for (int k = 0; k < ND; ++k) {
-          const int d = tid + k * kStatsThreads;
-          if (d < D) {
-            const double xd = static_cast<double>(x[d]);
-            const double qx = q * xd;
+        for (int w = 0; w < 8; ++w) z += s_pz[((int64_t)w * kStatsBatch + r) * NH1 + h];
+        const int hh = col0 + h;
+        s_zd[i] = hh < H ? static_cast<double>(z) : (hh == H ? 1.0 : 0.0);
+      }
+      __syncthreads();
+      // (ii) fp64 register tiles: dims [4*dg, 4*dg+4) x NH1 columns, rows rg::RG
+      if (tile_on) {
+        for (int r = my_rg; r < nb; r += RG) {
+          const double q = s_q[r];
+          const float* xr = xb + (int64_t)r * XS;
+          const double* zr = s_zd + r * NH1;
+          float zf[NH1];
 #pragma unroll
-            for (int h = 0; h < NH1; ++h) accY[k][h] = fma(qx, static_cast<double>(s_z[r][h]), accY[k][h]);
-            if (first) accS[k] = fma(qx, xd, accS[k]);
+          for (int h = 0; h < NH1; ++h) zf[h] = static_cast<float>(zr[h]);
+#pragma unroll
+          const float qf = static_cast<float>(q);
+#pragma unroll
+          for (int k = 0; k < ND; ++k) {
+            const int d = 4 * (my_dg + k * GD);
+            if (d >= D) break;
+            float vs[4];
+            if (vec || d + 3 < D) {
+              const float4 xv = *reinterpret_cast<const float4*>(xr + d);
+              const float4 mv = *reinterpret_cast<const float4*>(s_mu + d);
+              vs[0] = xv.x - mv.x, vs[1] = xv.y - mv.y, vs[2] = xv.z - mv.z, vs[3] = xv.w - mv.w;
+            } else {
+#pragma unroll
+              for (int i = 0; i < 4; ++i) vs[i] = d + i < D ? xr[d + i] - s_mu[d + i] : 0.f;
+            }
+            float qv[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              qv[i] = qf * vs[i];
+              if (first) accS[k][i] = fmaf(qv[i], vs[i], accS[k][i]);
+            }
+#pragma unroll
+            for (int h = 0; h < NH1; ++h) {
+              const float z = zf[h];
+#pragma unroll
+              for (int i = 0; i < 4; ++i) accY[k][i][h] = fmaf(qv[i], z, accY[k][i][h]);
+            }
           }
         }
-        if (full_e) {
+      }
+      if (full_e) {
+        for (int r = 0; r < nb; ++r) {
+          const double q = s_q[r];
 #pragma unroll
           for (int k = 0; k < NE; ++k) {
             const int idx = tid + k * kStatsThreads;
             if (idx < H1 * H1) {
               const int i = idx % H1, j = idx / H1;
-              accE[k] = fma(q * static_cast<double>(s_z[r][i]), static_cast<double>(s_z[r][j]), accE[k]);
+              accE[k] = fma(q * s_zd[r * NH1 + i], s_zd[r * NH1 + j], accE[k]);
             }
           }
         }
-        if (tid == 0) accN += q;
       }
       __syncthreads();
     }
-    double* pp = part + (int64_t)item * part_stride;
+    // combine the row groups of each dimension group through smem (fp64),
+    // reusing the row buffers, then write (direct or partial)
+    double* red = reinterpret_cast<double*>(s_x);  // >= RG * GD * 4 * (NH1 + 1) doubles
+    double* pp = direct ? nullptr : part + (int64_t)item * part_stride;
 #pragma unroll
     for (int k = 0; k < ND; ++k) {
-      const int d = tid + k * kStatsThreads;
-      if (d < D) {
+      __syncthreads();
+      if (tile_on && my_rg > 0) {
+        double* dst = red + ((int64_t)(my_rg - 1) * GD + my_dg) * 4 * (NH1 + 1);
 #pragma unroll
-        for (int h = 0; h < NH1; ++h) pp[(int64_t)h * D + d] = accY[k][h];
-        if (first) pp[(int64_t)NH1 * D + d] = accS[k];
+        for (int i = 0; i < 4; ++i) {
+#pragma unroll
+          for (int h = 0; h < NH1; ++h) dst[i * (NH1 + 1) + h] = accY[k][i][h];
+          dst[i * (NH1 + 1) + NH1] = accS[k][i];
+        }
+      }
+      __syncthreads();
+      if (tile_on && my_rg == 0) {
+        for (int g = 1; g < RG; ++g) {
+          const double* src = red + ((int64_t)(g - 1) * GD + my_dg) * 4 * (NH1 + 1);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+#pragma unroll
+            for (int h = 0; h < NH1; ++h) accY[k][i][h] += static_cast<float>(src[i * (NH1 + 1) + h]);
+            accS[k][i] += static_cast<float>(src[i * (NH1 + 1) + NH1]);
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int d = 4 * (my_dg + k * GD) + i;
+          if (d >= D) continue;
+          if (direct) {
+#pragma unroll
+            for (int h = 0; h < NH1; ++h)
+              if (col0 + h < H1) a.Y[((int64_t)c * H1 + col0 + h) * D + d] = accY[k][i][h];
+            if (first) a.sq[(int64_t)c * D + d] = accS[k][i];
+          } else {
+#pragma unroll
+            for (int h = 0; h < NH1; ++h) pp[(int64_t)h * D + d] = accY[k][i][h];
+            if (first) pp[(int64_t)NH1 * D + d] = accS[k][i];
+          }
+        }
       }
     }
     if (first) {
-      double* pe = pp + (int64_t)NH1 * D + D;
-      if (full_e) {
+      if (direct) {
+        if (full_e) {
 #pragma unroll
-        for (int k = 0; k < NE; ++k) {
-          const int idx = tid + k * kStatsThreads;
-          if (idx < H1 * H1) pe[idx] = accE[k];
+          for (int k = 0; k < NE; ++k) {
+            const int idx = tid + k * kStatsThreads;
+            if (idx < H1 * H1) a.E[(int64_t)c * H1 * H1 + idx] = accE[k];
+          }
+        }
+      } else {
+        double* pe = pp + (int64_t)NH1 * D + D;
+        if (full_e) {
+#pragma unroll
+          for (int k = 0; k < NE; ++k) {
+            const int idx = tid + k * kStatsThreads;
+            if (idx < H1 * H1) pe[idx] = accE[k];
+          }
         }
       }
-      if (tid == 0) pe[H1 * H1] = accN;
     }
   }
 }
@@ -851,6 +1023,7 @@ __global__ void __launch_bounds__(256) k_stats_reduce(Dims dm, const int* __rest
   const int D = dm.D, H1 = dm.H + 1;
   for (int c = blockIdx.x; c < dm.C; c += gridDim.x) {
     const int i0 = itemoff[c], i1 = itemoff[c + 1];
+    if (kind == 0 && i1 - i0 == 1) continue;  // written directly by k_stats
     if (kind == 1) {
       for (int idx = threadIdx.x; idx < H1 * H1; idx += blockDim.x) {
         double s = 0.0;
@@ -879,11 +1052,26 @@ __global__ void __launch_bounds__(256) k_stats_reduce(Dims dm, const int* __rest
         for (int it = i0; it < i1; ++it) s += part[(int64_t)it * part_stride + eb + idx];
         E[(int64_t)c * H1 * H1 + idx] = s;
       }
-    if (threadIdx.x == 0) {
-      double s = 0.0;
-      for (int it = i0; it < i1; ++it) s += part[(int64_t)it * part_stride + eb + H1 * H1];
-      Nc[c] = s;
-    }
+  }
+}
+
+// Restore the raw statistics from the centred ones (mu = the fp32 mean the
+// rows were centred on): Y[:, h] = Y_v[:, h] + mu * E(h, H), sq = sq_v +
+// 2 mu Y_v[:, H] + mu^2 N_c, with N_c = E(H, H) = sum q.
+__global__ void k_stats_uncenter(Dims dm, const float* mu32, double* Nc, const double* E, double* Y,
+                                 double* sq) {
+  const int H1 = dm.H + 1, D = dm.D;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (int64_t)dm.C * D;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int c = static_cast<int>(i / D), d = static_cast<int>(i - (int64_t)c * D);
+    const double* Ec = E + (int64_t)c * H1 * H1;
+    const double n = Ec[(int64_t)dm.H * H1 + dm.H];
+    const double mu = static_cast<double>(mu32[i]);
+    double* Yc = Y + (int64_t)c * H1 * D;
+    const double yvH = Yc[(int64_t)dm.H * D + d];
+    sq[i] += 2.0 * mu * yvH + mu * mu * n;
+    for (int h = 0; h < H1; ++h) Yc[(int64_t)h * D + d] += mu * Ec[(int64_t)dm.H * H1 + h];
+    if (d == 0) Nc[c] = n;
   }
 }
 
@@ -1263,6 +1451,10 @@ cudaError_t launch_hist(const unsigned* keys, int64_t n, int C, int* cnt, cudaSt
   k_hist<<<grid_for(n, 256, 4096), 256, 0, s>>>(keys, n, C, cnt);
   return cudaGetLastError();
 }
+cudaError_t launch_offsets_sorted(const unsigned* sorted, int64_t n, int C, int* off, cudaStream_t s) {
+  k_offsets_sorted<<<grid_for(C + 1, 256, 4096), 256, 0, s>>>(sorted, n, C, off);
+  return cudaGetLastError();
+}
 cudaError_t launch_chunks(const int* cnt, int C, int rows, int* chunks, cudaStream_t s) {
   k_chunks<<<grid_for(C + 1, 256, 4096), 256, 0, s>>>(cnt, C, rows, chunks);
   return cudaGetLastError();
@@ -1328,14 +1520,24 @@ template <int NH1>
 static void stats_pass(const StatsArgs& a, const int* itemoff, int rpi, int grid, int col0,
                        double* part, int64_t ps, cudaStream_t s) {
   const int D = a.dm.D;
-  const size_t smem = static_cast<size_t>(kStatsBatch) * D * sizeof(float);
+  constexpr int VS = (NH1 + 3) / 4 * 4;
+  const size_t XS = (D + 3) / 4 * 4 + kXPad;
+  const size_t fixed = (static_cast<size_t>(D) * VS + (D + 3) / 4 * 4 + 4 + 8 * kStatsBatch * NH1 + 8) * sizeof(float) +
+                       kStatsBatch * NH1 * sizeof(double) + 16;
+  const size_t per_buf = static_cast<size_t>(kStatsBatch) * XS * sizeof(float);
+  // the row-group reduction reuses the row buffers: RG-1 slices of GD*4*(NH1+1) doubles
+  const int GD = (D + 3) / 4;
+  const int RG = std::max(1, kStatsThreads / GD);
+  const size_t red = static_cast<size_t>(std::max(RG - 1, 0)) * GD * 4 * (NH1 + 1) * sizeof(double);
+  int nbuf = (2 * per_buf + fixed <= 200 * 1024) ? 2 : 1;
+  if (static_cast<size_t>(nbuf) * per_buf < red) nbuf = 2;
+  const size_t smem = std::max(static_cast<size_t>(nbuf) * per_buf, red) + fixed;
   auto go = [&](auto kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    kern<<<grid, kStatsThreads, smem, s>>>(a, itemoff, rpi, col0, part, ps);
+    kern<<<grid, kStatsThreads, smem, s>>>(a, itemoff, rpi, col0, part, ps, nbuf);
   };
-  if (D <= kStatsThreads) go(k_stats<NH1, 1>);
-  else if (D <= 2 * kStatsThreads) go(k_stats<NH1, 2>);
-  else go(k_stats<NH1, 4>);
+  if (D <= 4 * kStatsThreads) go(k_stats<NH1, 1>);
+  else go(k_stats<NH1, 2>);
 }
 int64_t stats_part_stride(const Dims& dm) {
   const int H1 = dm.H + 1;
@@ -1367,6 +1569,7 @@ cudaError_t launch_stats(const StatsArgs& a, const int* itemoff, int rows_per_it
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
+  k_stats_uncenter<<<grid_for((int64_t)a.dm.C * a.dm.D, 256, 8192), 256, 0, s>>>(a.dm, a.mu32, a.Nc, a.E, a.Y, a.sq);
   k_stats_sz<<<grid_for((int64_t)a.dm.C * a.dm.H * a.dm.H, 256, 4096), 256, 0, s>>>(a.dm, a.Nc, a.Sz, a.E);
   return cudaGetLastError();
 }

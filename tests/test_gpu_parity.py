@@ -118,7 +118,8 @@ def test_mstep_parity(oracle, gpu):
     np.testing.assert_allclose(s_g.Nc, s_or.Nc, rtol=1e-12, atol=1e-12)
     np.testing.assert_allclose(s_g.E, s_or.E, rtol=1e-5, atol=1e-6 * np.abs(s_or.E).max())
     np.testing.assert_allclose(s_g.Y, s_or.Y, rtol=1e-5, atol=1e-6 * np.abs(s_or.Y).max())
-    np.testing.assert_allclose(s_g.sq, s_or.sq, rtol=1e-12)
+    # centred fp32 accumulation restored in fp64: ~1e-6 relative
+    np.testing.assert_allclose(s_g.sq, s_or.sq, rtol=1e-5)
     # update_params from identical statistics: fp64 on both sides
     sess.upload_suffstats(s_or)
     sess.update_params()
@@ -228,12 +229,13 @@ def test_multishard_matches_single(gpu, oracle):
         allreduce(2)
         Fe, J, F = shards[0].phase_scalars()
         assert J == rep["joints"]
-        assert abs(F - rep["F"]) <= 1e-9 * abs(rep["F"])
+        # statistics are fp32 partials (centred) summed per shard: rounding-level differences
+        assert abs(F - rep["F"]) <= 1e-7 * abs(rep["F"])
         st1 = single.download_state()
         sa, sb = shards[0].download_state(), shards[1].download_state()
         assert np.array_equal(np.concatenate([sa.K, sb.K]), st1.K)
         assert np.array_equal(sa.g, st1.g) and np.array_equal(sb.g, st1.g)
         pa, p1 = shards[0].download_params(), single.download_params()
-        np.testing.assert_allclose(pa.mu, p1.mu, rtol=1e-9, atol=1e-12)
+        np.testing.assert_allclose(pa.mu, p1.mu, rtol=1e-5, atol=1e-5 * np.abs(p1.mu).max())
     for s in shards + [single]:
         s.close()
