@@ -1,0 +1,259 @@
+// vmfa_b200.hpp — C++ mirror of the reference's public API
+// (/root/reference/proj/include/vmfa/*.hpp) over the C-ABI in vmfa_b200.h.
+//
+// Same type and function names, argument meaning and exception behaviour as
+// the reference, without Eigen (the layouts are the reference's own Eigen
+// layouts, stored in std::vector). A reference-side caller swaps
+//   #include "vmfa/trainer.hpp"   ->   #include "vmfa_b200.hpp"
+// and links libvmfa_b200.so. Device residency is kept inside a Session (one
+// GPU context): the free functions take the Session in place of the
+// reference's `int threads` argument, because the device owns the data and
+// the caches between calls.
+#pragma once
+
+#include <algorithm>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "vmfa_b200.h"
+
+namespace vmfa_b200 {
+
+// ---- errors (errors.hpp:9-62) ---------------------------------------------------
+struct Error : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct CholeskyFailure : Error { using Error::Error; };
+struct EmptyKSet : Error { using Error::Error; };
+struct InsufficientCandidates : Error { using Error::Error; };
+struct SingularEc : Error { using Error::Error; };
+struct MaxIterExceeded : Error { using Error::Error; };
+struct TargetUnreachable : Error { using Error::Error; };
+struct DegenerateData : Error { using Error::Error; };
+struct BadMagic : Error { using Error::Error; };
+struct TruncatedFile : Error { using Error::Error; };
+struct UnsupportedVersion : Error { using Error::Error; };
+struct DeviceError : Error { using Error::Error; };  // CUDA / no device / unsupported shape
+
+inline void check(int code) {
+  if (code == VMFA_OK) return;
+  const std::string msg = vmfa_last_error();
+  switch (code) {
+    case VMFA_ERR_INVALID_ARGUMENT: throw std::invalid_argument(msg);
+    case VMFA_ERR_CHOLESKY_FAILURE: throw CholeskyFailure(msg);
+    case VMFA_ERR_EMPTY_KSET: throw EmptyKSet(msg);
+    case VMFA_ERR_INSUFFICIENT_CANDIDATES: throw InsufficientCandidates(msg);
+    case VMFA_ERR_SINGULAR_EC: throw SingularEc(msg);
+    case VMFA_ERR_MAX_ITER_EXCEEDED: throw MaxIterExceeded(msg);
+    case VMFA_ERR_TARGET_UNREACHABLE: throw TargetUnreachable(msg);
+    case VMFA_ERR_DEGENERATE_DATA: throw DegenerateData(msg);
+    case VMFA_ERR_BAD_MAGIC: throw BadMagic(msg);
+    case VMFA_ERR_TRUNCATED_FILE: throw TruncatedFile(msg);
+    case VMFA_ERR_UNSUPPORTED_VERSION: throw UnsupportedVersion(msg);
+    default: throw DeviceError(msg);
+  }
+}
+
+enum class DistanceMode { kl = VMFA_DIST_KL, euclid = VMFA_DIST_EUCLID };  // estep.hpp:12
+
+// ---- data / model types (reference layouts) ---------------------------------------
+struct Dataset {  // dataset.hpp:11-35: N x D float, row-major
+  int64_t N = 0;
+  int D = 0;
+  std::vector<float> rows;
+};
+
+struct MfaParams {  // model.hpp:19-32
+  int C = 0, D = 0, H = 0;
+  std::vector<double> pi;      // C
+  std::vector<double> mu;      // C x D row-major
+  std::vector<double> Lambda;  // C blocks, D x H column-major
+  std::vector<double> dnoise;  // C x D row-major
+};
+
+struct ComponentCaches {  // model.hpp:37-45, all C components
+  std::vector<double> U, Lmat, V, Sigma_z, inv_dnoise, logdet_sigma, log_pi;
+};
+
+struct VarState {  // estep.hpp:17-29
+  int C = 0, Cprime = 0, G = 0;
+  std::vector<int32_t> K;        // N x C' (rows sorted ascending)
+  std::vector<int32_t> g;        // C x G (rows sorted, -1 padded)
+  std::vector<int32_t> g_count;  // C
+  std::vector<int32_t> labels;   // N
+};
+
+struct EStepResult {  // estep.hpp:72-78
+  int stride = 0;
+  std::vector<int32_t> count, idx;
+  std::vector<double> lj, resp;
+  double free_energy = 0.0;
+  uint64_t joints = 0;
+};
+
+struct SuffStats {  // mstep.hpp:14-22
+  std::vector<double> Nc, Y, E, sq_sum;
+};
+
+struct EvalCounter {  // model.hpp:49-58
+  uint64_t joints = 0;
+  uint64_t distances = 0;
+};
+
+// ---- Session: one device context ------------------------------------------------
+class Session {
+ public:
+  Session(const Dataset& data, int C, int H, int Cprime, int G, int device = 0,
+          int64_t n_offset = 0, int64_t n_total = -1)
+      : N_(data.N), D_(data.D), C_(C), H_(H), Cp_(Cprime), G_(G) {
+    check(vmfa_ctx_create(&ctx_, device, C, data.D, H, Cprime, G, data.N, n_offset,
+                          n_total < 0 ? n_offset + data.N : n_total, nullptr));
+    check(vmfa_upload_data(ctx_, data.rows.data(), 0, data.N));
+  }
+  ~Session() { vmfa_ctx_destroy(ctx_); }
+  Session(const Session&) = delete;
+  Session& operator=(const Session&) = delete;
+
+  vmfa_ctx* handle() const { return ctx_; }
+  int64_t rows() const { return N_; }
+  int C() const { return C_; }
+  int D() const { return D_; }
+  int H() const { return H_; }
+  int Cprime() const { return Cp_; }
+  int G() const { return G_; }
+  int stride() const { return static_cast<int>(std::min<int64_t>(int64_t{Cp_} * G_ + 1, C_)); }
+
+  void set_floor(const std::vector<double>& floor) { check(vmfa_set_floor(ctx_, floor.data())); }
+  void upload(const MfaParams& p) {
+    check(vmfa_upload_params(ctx_, p.pi.data(), p.mu.data(), p.Lambda.data(), p.dnoise.data()));
+  }
+  void upload(const VarState& s) { check(vmfa_upload_state(ctx_, s.K.data(), s.g.data(), s.g_count.data())); }
+  MfaParams download_params() const {
+    MfaParams p;
+    p.C = C_, p.D = D_, p.H = H_;
+    p.pi.resize(C_);
+    p.mu.resize(size_t(C_) * D_);
+    p.Lambda.resize(size_t(C_) * D_ * H_);
+    p.dnoise.resize(size_t(C_) * D_);
+    check(vmfa_download_params(ctx_, p.pi.data(), p.mu.data(), p.Lambda.data(), p.dnoise.data()));
+    return p;
+  }
+  void download(VarState& s) const {
+    s.C = C_, s.Cprime = Cp_, s.G = G_;
+    s.K.resize(size_t(N_) * Cp_);
+    s.g.resize(size_t(C_) * G_);
+    s.g_count.resize(C_);
+    s.labels.resize(N_);
+    check(vmfa_download_state(ctx_, s.K.data(), s.g.data(), s.g_count.data(), s.labels.data()));
+  }
+
+ private:
+  vmfa_ctx* ctx_ = nullptr;
+  int64_t N_;
+  int D_, C_, H_, Cp_, G_;
+};
+
+// ---- the reference's free functions -------------------------------------------------
+// precompute_all (model.hpp:76-78): caches of the session's parameters.
+inline ComponentCaches precompute_all(Session& s, const MfaParams& params) {
+  s.upload(params);  // uploads and runs precompute_all on the device
+  ComponentCaches k;
+  const size_t C = s.C(), D = s.D(), H = s.H();
+  k.U.resize(C * D * H);
+  k.V.resize(C * D * H);
+  k.Lmat.resize(C * H * H);
+  k.Sigma_z.resize(C * H * H);
+  k.inv_dnoise.resize(C * D);
+  k.logdet_sigma.resize(C);
+  k.log_pi.resize(C);
+  check(vmfa_download_caches(s.handle(), k.U.data(), k.Lmat.data(), k.V.data(), k.Sigma_z.data(),
+                             k.inv_dnoise.data(), k.logdet_sigma.data(), k.log_pi.data()));
+  return k;
+}
+
+// variational_e_step (estep.hpp:125-130): updates `state` in place.
+inline EStepResult variational_e_step(Session& s, VarState& state, uint64_t seed, uint64_t iteration,
+                                      DistanceMode mode, EvalCounter& counter) {
+  s.upload(state);
+  EStepResult r;
+  check(vmfa_estep(s.handle(), seed, iteration, static_cast<int>(mode), &r.free_energy, &r.joints));
+  r.stride = s.stride();
+  r.count.resize(s.rows());
+  r.idx.resize(size_t(s.rows()) * r.stride);
+  r.lj.resize(size_t(s.rows()) * r.stride);
+  r.resp.resize(size_t(s.rows()) * s.Cprime());
+  check(vmfa_download_estep(s.handle(), r.count.data(), r.idx.data(), r.lj.data(), r.resp.data()));
+  s.download(state);
+  counter.joints += r.joints;
+  return r;
+}
+
+// accumulate_suffstats (mstep.hpp:27-31) of the last E-step on the device.
+inline SuffStats accumulate_suffstats(Session& s) {
+  check(vmfa_accumulate_suffstats(s.handle()));
+  SuffStats st;
+  const size_t C = s.C(), D = s.D(), H1 = s.H() + 1;
+  st.Nc.resize(C);
+  st.Y.resize(C * D * H1);
+  st.E.resize(C * H1 * H1);
+  st.sq_sum.resize(C * D);
+  check(vmfa_download_suffstats(s.handle(), st.Nc.data(), st.Y.data(), st.E.data(), st.sq_sum.data()));
+  return st;
+}
+
+// update_params (mstep.hpp:39-41) from `stats`; the session keeps the result
+// and its caches.
+inline MfaParams update_params(Session& s, const SuffStats& stats) {
+  check(vmfa_upload_suffstats(s.handle(), stats.Nc.data(), stats.Y.data(), stats.E.data(),
+                              stats.sq_sum.data()));
+  int failed = -1;
+  check(vmfa_update_params(s.handle(), &failed));
+  return s.download_params();
+}
+
+// truncated_free_energy (model.hpp:116-119) under the session's parameters.
+inline double truncated_free_energy(Session& s, const VarState& ksets) {
+  (void)ksets;  // the session's K is the state of the last E-step / upload
+  double F = 0.0;
+  check(vmfa_truncated_free_energy(s.handle(), &F));
+  return F;
+}
+
+// train_vmfa's loop (trainer.cpp:111-186) with fixed warm-up / main counts.
+struct IterationRecord {
+  bool warmup = false;
+  double F = 0.0;
+  double F_estep = 0.0;
+  uint64_t joint_evals = 0;
+  int empty_components = 0;
+};
+inline std::vector<IterationRecord> train_fixed(Session& s, uint64_t seed, int warmup, int iters,
+                                                DistanceMode mode = DistanceMode::kl) {
+  std::vector<IterationRecord> recs;
+  uint64_t it = 0, joints = 0;
+  for (int w = 0; w < warmup; ++w) {
+    IterationRecord r;
+    uint64_t j = 0;
+    check(vmfa_estep(s.handle(), seed, it++, static_cast<int>(mode), &r.F, &j));
+    joints += j;
+    r.warmup = true;
+    r.joint_evals = joints;
+    recs.push_back(r);
+  }
+  for (int t = 0; t < iters; ++t) {
+    vmfa_iter_report rep{};
+    check(vmfa_iterate(s.handle(), seed, it++, static_cast<int>(mode), &rep));
+    joints += rep.joints;
+    IterationRecord r;
+    r.F = rep.free_energy;
+    r.F_estep = rep.free_energy_estep;
+    r.joint_evals = joints;
+    r.empty_components = rep.empty_components;
+    recs.push_back(r);
+  }
+  return recs;
+}
+
+}  // namespace vmfa_b200

@@ -1,0 +1,126 @@
+"""CPU tests of the product library's host side and its C-ABI surface:
+  * libvmfa_b200.so loads without a GPU and exports every symbol declared in
+    include/vmfa_b200.h;
+  * error behaviour without a device (NoDevice, mapped like the reference's
+    exception types, errors.hpp:9-62) and argument validation;
+  * the host-side initialisation (trainer.cpp:32-47, 107-109) is bit-identical
+    to the oracle's restatement; the synthetic generators are deterministic
+    and shard-consistent.
+"""
+import ctypes as C
+import os
+import re
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "vmfa_b200.h")
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    names = re.findall(r"^\s*(?:const\s+)?[A-Za-z_][\w\s\*]*?\b(vmfa_\w+)\s*\(", src, flags=re.M)
+    return sorted(set(names))
+
+
+def test_header_declares_the_boundary():
+    names = declared_functions()
+    for must in ("vmfa_ctx_create", "vmfa_estep", "vmfa_iterate", "vmfa_accumulate_suffstats",
+                 "vmfa_update_params", "vmfa_precompute", "vmfa_truncated_free_energy",
+                 "vmfa_exchange_buffer", "vmfa_host_initialize", "vmfa_gen_synthetic"):
+        assert must in names
+
+
+def test_library_exports_every_declared_symbol(vmfa):
+    from paper_2501_12299_b200 import abi
+    lib = C.CDLL(abi.library_path())
+    missing = [n for n in declared_functions() if not hasattr(lib, n)]
+    assert not missing, missing
+    assert abi.lib().vmfa_abi_version() == 1
+
+
+def test_no_device_is_reported_not_faked(vmfa):
+    from paper_2501_12299_b200 import abi
+    if vmfa.device_available():
+        pytest.skip("a GPU is visible")
+    with pytest.raises(abi.VmfaError) as ei:
+        vmfa.Session(4, 3, 1, 2, 2, np.zeros((10, 3), np.float32))
+    assert ei.value.code == 101  # VMFA_ERR_NO_DEVICE: no CPU fallback exists
+
+
+def test_invalid_arguments_map_to_invalid_argument(vmfa):
+    from paper_2501_12299_b200 import abi
+    h = C.c_void_p()
+    # C' > C and H > D are std::invalid_argument in the reference (trainer.cpp:60-77)
+    assert abi.lib().vmfa_ctx_create(C.byref(h), 0, 4, 3, 1, 5, 2, 10, 0, 10, None) == 1
+    assert abi.lib().vmfa_ctx_create(C.byref(h), 0, 4, 3, 4, 2, 2, 10, 0, 10, None) == 1
+    assert b"invalid sizes" in abi.lib().vmfa_last_error()
+
+
+def test_host_initialize_matches_oracle(oracle, vmfa):
+    X = vmfa.gen_synthetic(vmfa.synth_spec(1, N=3000))
+    for li, sc in ((1, 0.1), (0, 1.0)):
+        p, st, floor, seeds = vmfa.initialize(X, 50, 4, 3, 5, seed=7, scale=sc, loading_init=li)
+        po, sto, flo, so = oracle.initialize(X, 50, 4, 3, 5, seed=7, scale=sc, loading_init=li)
+        assert np.array_equal(seeds, so)
+        assert np.array_equal(st.K, sto.K) and np.array_equal(st.g, sto.g)
+        assert np.array_equal(st.g_count, sto.g_count)
+        np.testing.assert_array_equal(p.mu, po.mu)
+        np.testing.assert_array_equal(p.lam, po.lam)
+        np.testing.assert_allclose(p.psi, po.psi, rtol=1e-13)
+        np.testing.assert_allclose(floor, flo, rtol=1e-13)
+
+
+def test_init_varstate_invariants(vmfa):
+    X = vmfa.gen_synthetic(vmfa.synth_spec(2, N=5000))
+    p, st, floor, seeds = vmfa.initialize(X, 300, 8, 5, 10, seed=3)
+    assert np.all(np.diff(st.K, axis=1) > 0) and st.K.min() >= 0 and st.K.max() < 300
+    for c in range(300):
+        row = st.g[c, :st.g_count[c]]
+        assert c in row and np.all(np.diff(row) > 0)
+    # seed rows carry their own component (seeding.cpp:215-218)
+    for c, n in enumerate(seeds):
+        assert c in st.K[n]
+    assert np.all(p.pi == 1.0 / 300)
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
+def test_generators_deterministic_and_shardable(vmfa, cfg):
+    # config 5's 50 000 ground-truth fields are reduced to 500 here (CPU time)
+    sp = vmfa.synth_spec(cfg, N=600, **({"C_true": 500} if cfg == 5 else {}))
+    a = vmfa.gen_synthetic(sp)
+    b = vmfa.gen_synthetic(sp, threads=1)
+    assert np.array_equal(a, b)
+    assert np.array_equal(vmfa.gen_synthetic(sp, 200, 400), a[200:400])
+    assert np.isfinite(a).all() and a.shape == (600, sp.D)
+    if vmfa.CONFIGS[cfg]["truth"]["kind"] == 1:
+        assert a.min() >= 0.0 and a.max() <= 1.0  # clipped image-like fields
+
+
+def test_error_codes_cover_the_reference_exceptions():
+    src = open(HEADER).read()
+    for name in ("CholeskyFailure", "EmptyKSet", "InsufficientCandidates", "SingularEc",
+                 "MaxIterExceeded", "TargetUnreachable", "DegenerateData", "BadMagic",
+                 "TruncatedFile", "UnsupportedVersion"):
+        assert name in src
+
+
+def build_facade(tmp_path):
+    import subprocess
+    exe = tmp_path / "facade_train"
+    lib_dir = os.path.join(ROOT, "paper_2501_12299_b200", "_lib")
+    subprocess.run(["g++", "-std=c++17", "-O2", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "cpp", "facade_train.cpp"), "-L", lib_dir,
+                    "-lvmfa_b200", f"-Wl,-rpath,{lib_dir}", "-o", str(exe)], check=True)
+    return exe
+
+
+def test_cpp_mirror_compiles_and_reports_no_device(vmfa, tmp_path):
+    import subprocess
+    exe = build_facade(tmp_path)
+    if vmfa.device_available():
+        pytest.skip("a GPU is visible")
+    r = subprocess.run([str(exe), "200"], capture_output=True, text=True)
+    assert r.returncode == 3 and "no sm_100" in r.stderr

@@ -239,3 +239,25 @@ def test_multishard_matches_single(gpu, oracle):
         np.testing.assert_allclose(pa.mu, p1.mu, rtol=1e-5, atol=1e-5 * np.abs(p1.mu).max())
     for s in shards + [single]:
         s.close()
+
+
+def test_cpp_mirror_matches_python_path(gpu, tmp_path):
+    """The C++ drop-in (include/vmfa_b200.hpp) and the Python mirror drive the
+    same C-ABI: identical trajectories (the device path is deterministic)."""
+    import subprocess
+    from test_abi_host import build_facade
+    V = gpu
+    exe = build_facade(tmp_path)
+    out = subprocess.run([str(exe), "20000"], capture_output=True, text=True, check=True).stdout
+    rows = [l.split() for l in out.strip().splitlines()]
+    X = V.gen_synthetic(V.synth_spec(1))
+    p, st, floor, _ = V.initialize(X, 100, 4, 3, 5, seed=0, scale=0.1, loading_init=1)
+    s = V.Session(100, 64, 4, 3, 5, X)
+    s.set_floor(floor)
+    s.upload_params(p)
+    s.upload_state(st)
+    recs = V.train_fixed(s, 0, 2, 20)
+    assert len(rows) == len(recs)
+    for r, q in zip(rows, recs):
+        assert float(r[1]) == pytest.approx(q["F"], rel=1e-12, abs=0)
+    s.close()

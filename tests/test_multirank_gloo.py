@@ -1,0 +1,134 @@
+"""Multi-rank host logic on CPU (torch.distributed, gloo, world_size 2).
+
+The B200 path shards rows over ranks and exchanges (i) the block-3
+co-occurrence table and (ii) the sufficient statistics with all-reduces
+(include/vmfa_b200.h phase API). This test runs the same
+algebra with the fp64 oracle per shard: each rank runs the E-step on rows
+[r*N/p, (r+1)*N/p) with the GLOBAL row index keying the extra candidate
+(rng.hpp:91-98), all-reduces the dense (count, sum) co-occurrence table and the
+statistics, and must reproduce the unsharded step: identical joint counts, K
+rows, labels and g; F and the statistics equal to rounding; and the updated
+parameters equal to rounding. The fixed-point encoding used on the GPU makes
+the co-occurrence sums exact integers, checked here for order independence.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from _helpers import gaussian_problem
+
+WORLD = 2
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def select_g(cnt, ssum, G):
+    """update_g (estep.cpp:204-220) from a dense per-component table."""
+    C = cnt.shape[0]
+    g = np.full((C, G), -1, np.int32)
+    gc = np.zeros(C, np.int32)
+    for c in range(C):
+        keys = np.nonzero(cnt[c] > 0)[0]
+        avg = ssum[c, keys] / cnt[c, keys]
+        order = np.lexsort((keys, avg))[: G - 1]
+        row = np.sort(np.concatenate([[c], keys[order]]))
+        g[c, :len(row)] = row
+        gc[c] = len(row)
+    return g, gc
+
+
+def _worker(rank, port, ret):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=WORLD)
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from oracle import oracle as O
+    X, _ = gaussian_problem(1200, 8, 10, 2, seed=4)
+    C, H, Cp, G = 16, 2, 3, 4
+    p, st, floor, _ = O.initialize(X, C, H, Cp, G, seed=1, scale=0.1, loading_init=1)
+    k = O.precompute_all(p)
+    N = X.shape[0]
+    a, b = rank * N // WORLD, (rank + 1) * N // WORLD
+    shard = O.State(st.K[a:b].copy(), st.g.copy(), st.g_count.copy())
+    e = O.variational_e_step(X[a:b], p, k, shard, 9, 3, threads=1, dump_distances=True, n_offset=a)
+    # co-occurrence exchange: dense table, all-reduced
+    cnt = np.zeros((C, C))
+    ssum = np.zeros((C, C))
+    dc, dct, ds, dn = e.dist
+    cnt[dc, dct] = dn
+    ssum[dc, dct] = ds
+    t_cnt, t_sum = torch.from_numpy(cnt), torch.from_numpy(ssum)
+    dist.all_reduce(t_cnt)
+    dist.all_reduce(t_sum)
+    g, gc = select_g(t_cnt.numpy(), t_sum.numpy(), G)
+    # scalars
+    sc = torch.tensor([e.F, float(e.joints)], dtype=torch.float64)
+    dist.all_reduce(sc)
+    # statistics with the pre-update caches and the shard's new K / resp
+    s = O.accumulate_suffstats(X[a:b], p, k, shard.K, e.resp)
+    flat = torch.from_numpy(np.concatenate([s.Nc, s.Y.ravel(), s.E.ravel(), s.sq.ravel()]))
+    dist.all_reduce(flat)
+    Ks = [torch.zeros((N // WORLD + 1, Cp), dtype=torch.int32) for _ in range(WORLD)]
+    kpad = torch.zeros((N // WORLD + 1, Cp), dtype=torch.int32)
+    kpad[: b - a] = torch.from_numpy(shard.K)
+    dist.all_gather(Ks, kpad)
+    if rank == 0:
+        ret["g"], ret["gc"] = g, gc
+        ret["F"], ret["J"] = float(sc[0]), int(sc[1])
+        ret["stats"] = flat.numpy()
+        ret["K"] = np.concatenate([Ks[r][: (r + 1) * N // WORLD - r * N // WORLD].numpy() for r in range(WORLD)])
+    dist.destroy_process_group()
+
+
+def test_two_rank_shard_algebra_matches_single(oracle):
+    O = oracle
+    mgr = mp.Manager()
+    ret = mgr.dict()
+    mp.spawn(_worker, args=(_free_port(), ret), nprocs=WORLD, join=True)
+    X, _ = gaussian_problem(1200, 8, 10, 2, seed=4)
+    C, H, Cp, G = 16, 2, 3, 4
+    p, st, floor, _ = O.initialize(X, C, H, Cp, G, seed=1, scale=0.1, loading_init=1)
+    k = O.precompute_all(p)
+    e = O.variational_e_step(X, p, k, st, 9, 3, threads=1, dump_distances=True)
+    assert ret["J"] == e.joints
+    assert abs(ret["F"] - e.F) <= 1e-12 * abs(e.F)
+    assert np.array_equal(ret["K"], st.K)
+    assert np.array_equal(ret["gc"], st.g_count)
+    assert np.array_equal(ret["g"], st.g)
+    s = O.accumulate_suffstats(X, p, k, st.K, e.resp)
+    single = np.concatenate([s.Nc, s.Y.ravel(), s.E.ravel(), s.sq.ravel()])
+    np.testing.assert_allclose(ret["stats"], single, rtol=1e-12, atol=1e-12)
+
+
+def to_fixed(v):
+    """Host restatement of the device's fixed-point split (vmfa_kernels.cu
+    to_fixed): value = hi * 2^-10 + lo * 2^-50 exactly, hi/lo int64."""
+    v = float(np.clip(v, -2.0 ** 31, 2.0 ** 31))
+    y = v * 1024.0
+    f = np.floor(y)
+    return int(f), int((y - f) * 2.0 ** 40)
+
+
+def test_fixed_point_sums_are_order_and_partition_independent():
+    rng = np.random.default_rng(0)
+    vals = rng.normal(0, 50, 5000) * rng.choice([1e-3, 1, 1e3], 5000)
+    parts = [to_fixed(v) for v in vals]
+    hi = sum(p[0] for p in parts)
+    lo = sum(p[1] for p in parts)
+    perm = rng.permutation(len(parts))
+    shard = [parts[i] for i in perm]
+    hi2 = sum(p[0] for p in shard[:1234]) + sum(p[0] for p in shard[1234:])
+    lo2 = sum(p[1] for p in shard[:1234]) + sum(p[1] for p in shard[1234:])
+    assert (hi, lo) == (hi2, lo2)
+    exact = hi / 1024.0 + lo / 2.0 ** 50
+    assert abs(exact - vals.sum()) <= 1e-9 * np.abs(vals).sum()
