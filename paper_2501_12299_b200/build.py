@@ -20,7 +20,7 @@ OBJ_DIR = os.path.join(ROOT, "build", "obj")
 LIB = os.path.join(OUT_DIR, "libvmfa_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-CU_SOURCES = ["vmfa_kernels.cu", "vmfa_score_tc.cu", "vmfa_capi.cu"]
+CU_SOURCES = ["vmfa_kernels.cu", "vmfa_score_tc.cu", "vmfa_score_ws.cu", "vmfa_capi.cu"]
 CXX_SOURCES = ["host/vmfa_host.cpp"]
 DEPS_H = ["vmfa_kernels.cuh", "vmfa_internal.hpp", "vmfa_rng.hpp"]
 

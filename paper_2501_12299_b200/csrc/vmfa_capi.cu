@@ -79,8 +79,10 @@ struct vmfa_ctx {
   double *Lmat = nullptr, *R = nullptr, *Sz = nullptr, *logdet = nullptr, *logpi = nullptr,
          *kconst = nullptr;
   float *P = nullptr, *V32 = nullptr, *mu32 = nullptr, *WT = nullptr, *ipsi32 = nullptr;
-  int Hp = 4;
-  bool use_tc = true;       // tcgen05 3xTF32 scorer (VMFA_SCORER=ffma selects the FFMA kernel)
+  int Hp = 8;
+  float *WTS = nullptr, *acst = nullptr;
+  int scorer = 2;           // 2: warp-specialised tcgen05 (default), 1: single-role tcgen05, 0: FFMA
+  bool use_tc = true;
   int score_rows = kScoreRowsTc;
   // state
   int *K = nullptr, *g = nullptr, *gcnt = nullptr, *g_new = nullptr, *gcnt_new = nullptr,
@@ -227,7 +229,8 @@ int csr_by_key(vmfa_ctx* x, const unsigned* keys, int64_t n, int* off, int* ent,
 int score_grid() { return sm_count() * 8; }
 
 cudaError_t run_score(vmfa_ctx* x, int mode, const ScoreArgs& a) {
-  if (x->use_tc) return launch_score_tc(mode, a, x->WT, x->ipsi32, x->mu32, x->stream);
+  if (x->scorer == 2) return launch_score_ws(mode, a, x->WTS, x->mu32, x->ipsi32, x->acst, x->stream);
+  if (x->scorer == 1) return launch_score_tc(mode, a, x->WT, x->ipsi32, x->mu32, x->stream);
   return launch_score(mode, a, score_grid(), x->stream);
 }
 
@@ -268,6 +271,7 @@ int run_precompute(vmfa_ctx* x, int* failed) {
   a.status = x->st_model;
   const int tok = x->begin(kFamPrecompute, x->dm.C);
   CU(launch_precompute(a, s));
+  if (x->scorer == 2) CU(launch_ws_prep(x->dm, x->WT, x->WTS, s));
   x->end(tok);
   unsigned long long st = 0;
   CU(cudaMemcpyAsync(&st, x->st_model, sizeof st, cudaMemcpyDeviceToHost, s));
@@ -296,6 +300,11 @@ int estep_local(vmfa_ctx* x, uint64_t seed, uint64_t it, int mode, bool exchange
   }
   TRY(csr_by_key(x, x->rkey, dm.N, x->ex_off, x->ex_ent, x->ex_items, x->score_rows));
   // block 1: scoring
+  if (x->scorer == 2) {
+    const int tok = x->begin(kFamOther, dm.C);
+    CU(launch_anchor_consts(dm, x->WT, x->mu32, x->ipsi32, x->g, x->gcnt, x->acst, s));
+    x->end(tok);
+  }
   {
     ScoreArgs a = score_args(x);
     a.off = x->kinv_off;
@@ -550,10 +559,14 @@ int vmfa_ctx_create(vmfa_ctx** out, int device, int C, int D, int H, int Cp, int
   dm.stride = static_cast<int>(std::min<int64_t>(static_cast<int64_t>(Cp) * G + 1, C));
   dm.N = n_local, dm.n0 = n_offset, dm.Ntot = n_total;
   x->L = score_layout(H);
-  x->Hp = H <= 4 ? 4 : H <= 8 ? 8 : H <= 16 ? 16 : H <= 32 ? 32 : 64;
+  x->Hp = ws_hp(H);
   {
     const char* sc = std::getenv("VMFA_SCORER");
-    x->use_tc = !(sc && std::string(sc) == "ffma") && score_tc_supported(x->dm);
+    const std::string v = sc ? sc : "ws";
+    x->scorer = v == "ffma" ? 0 : (v == "tc" ? 1 : 2);
+    if (x->scorer == 2 && !score_ws_supported(x->dm)) x->scorer = 1;
+    if (x->scorer == 1 && !score_tc_supported(x->dm)) x->scorer = 0;
+    x->use_tc = x->scorer != 0;
     x->score_rows = x->use_tc ? kScoreRowsTc : kScoreRows;
   }
   if (stream) {
@@ -586,6 +599,8 @@ int vmfa_ctx_create(vmfa_ctx** out, int device, int C, int D, int H, int Cp, int
   A(x->V32, Cs * D * H);
   A(x->mu32, Cs * D);
   A(x->WT, Cs * x->Hp * D);
+  A(x->WTS, Cs * ((D + 31) / 32) * 2 * x->Hp * 32);
+  A(x->acst, Cs * G * (x->Hp + 1));
   A(x->ipsi32, Cs * D);
   A(x->K, N * Cp);
   A(x->g, Cs * G);

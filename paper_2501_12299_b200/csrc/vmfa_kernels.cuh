@@ -208,5 +208,13 @@ bool score_tc_supported(const Dims& dm);
 cudaError_t launch_score_tc(int mode, const ScoreArgs& s, const float* WT, const float* ipsi32,
                             const float* mu32, cudaStream_t st);
 constexpr int kScoreRowsTc = 128;
+// warp-specialised tensor-core scorer (vmfa_score_ws.cu)
+int ws_hp(int H);  // W rows per component in WT / WTS (H padded to 8, 16, 32, 64)
+bool score_ws_supported(const Dims& dm);
+cudaError_t launch_ws_prep(const Dims& dm, const float* WT, float* WTS, cudaStream_t s);
+cudaError_t launch_anchor_consts(const Dims& dm, const float* WT, const float* mu32, const float* ipsi32,
+                                 const int* g, const int* gcnt, float* acst, cudaStream_t s);
+cudaError_t launch_score_ws(int mode, const ScoreArgs& s, const float* WTS, const float* mu32,
+                            const float* ipsi32, const float* acst, cudaStream_t st);
 
 }  // namespace vmfa_b200

@@ -508,7 +508,7 @@ cudaError_t launch_score_tc(int mode, const ScoreArgs& s, const float* WT, const
   a.dm = s.dm;
   a.mode = mode;
   const int H = s.dm.H;
-  a.Hp = H <= 4 ? 4 : H <= 8 ? 8 : H <= 16 ? 16 : H <= 32 ? 32 : 64;
+  a.Hp = ws_hp(H);  // WT rows per component (shared with the warp-specialised scorer)
   const int ncomp_max = mode == kModeAnchor ? s.dm.G : 1;
   // group size: GEMM1 width <= 256 and N1 + 2 NL <= 512 TMEM columns; NL == 16
   int qg = std::min(ncomp_max, std::min(16, 256 / a.Hp));
@@ -538,7 +538,6 @@ cudaError_t launch_score_tc(int mode, const ScoreArgs& s, const float* WT, const
     kern<<<grid, kTcThreads, dyn, st>>>(a);
   };
   switch (a.Hp) {
-    case 4: go(k_score_tc<4>); break;
     case 8: go(k_score_tc<8>); break;
     case 16: go(k_score_tc<16>); break;
     case 32: go(k_score_tc<32>); break;

@@ -60,7 +60,7 @@ def test_precompute_caches_match_oracle(oracle, gpu):
     dict(N=1000, D=10, C=6, H=2, Cp=6, G=6),      # C'=C: no truncation
     dict(N=2000, D=100, C=50, H=16, Cp=4, G=8),   # H=16 chunk
 ])
-@pytest.mark.parametrize("scorer", ["tc", "ffma"])
+@pytest.mark.parametrize("scorer", ["ws", "tc", "ffma"])
 def test_estep_teacher_forced(oracle, gpu, case, scorer, monkeypatch):
     O, V = oracle, gpu
     monkeypatch.setenv("VMFA_SCORER", scorer)
