@@ -80,7 +80,7 @@ struct vmfa_ctx {
          *kconst = nullptr;
   float *P = nullptr, *V32 = nullptr, *mu32 = nullptr, *WT = nullptr, *ipsi32 = nullptr;
   int Hp = 8;
-  float *WTS = nullptr, *acst = nullptr;
+  float *WTS = nullptr, *acst = nullptr, *lblk = nullptr, *cblk = nullptr;
   int scorer = 2;           // 2: warp-specialised tcgen05 (default), 1: single-role tcgen05, 0: FFMA
   bool use_tc = true;
   int score_rows = kScoreRowsTc;
@@ -229,7 +229,8 @@ int csr_by_key(vmfa_ctx* x, const unsigned* keys, int64_t n, int* off, int* ent,
 int score_grid() { return sm_count() * 8; }
 
 cudaError_t run_score(vmfa_ctx* x, int mode, const ScoreArgs& a) {
-  if (x->scorer == 2) return launch_score_ws(mode, a, x->WTS, x->mu32, x->ipsi32, x->acst, x->stream);
+  if (x->scorer == 2)
+    return launch_score_ws(mode, a, x->WTS, x->mu32, x->ipsi32, x->acst, x->lblk, x->cblk, x->stream);
   if (x->scorer == 1) return launch_score_tc(mode, a, x->WT, x->ipsi32, x->mu32, x->stream);
   return launch_score(mode, a, score_grid(), x->stream);
 }
@@ -271,7 +272,10 @@ int run_precompute(vmfa_ctx* x, int* failed) {
   a.status = x->st_model;
   const int tok = x->begin(kFamPrecompute, x->dm.C);
   CU(launch_precompute(a, s));
-  if (x->scorer == 2) CU(launch_ws_prep(x->dm, x->WT, x->WTS, s));
+  if (x->scorer == 2) {
+    CU(launch_ws_prep(x->dm, x->WT, x->WTS, s));
+    CU(launch_ws_blocks(x->dm, 1, x->mu32, x->ipsi32, x->g, x->gcnt, x->cblk, s));
+  }
   x->end(tok);
   unsigned long long st = 0;
   CU(cudaMemcpyAsync(&st, x->st_model, sizeof st, cudaMemcpyDeviceToHost, s));
@@ -303,6 +307,7 @@ int estep_local(vmfa_ctx* x, uint64_t seed, uint64_t it, int mode, bool exchange
   if (x->scorer == 2) {
     const int tok = x->begin(kFamOther, dm.C);
     CU(launch_anchor_consts(dm, x->WT, x->mu32, x->ipsi32, x->g, x->gcnt, x->acst, s));
+    CU(launch_ws_blocks(dm, 0, x->mu32, x->ipsi32, x->g, x->gcnt, x->lblk, s));
     x->end(tok);
   }
   {
@@ -601,6 +606,11 @@ int vmfa_ctx_create(vmfa_ctx** out, int device, int C, int D, int H, int Cp, int
   A(x->WT, Cs * x->Hp * D);
   A(x->WTS, Cs * ((D + 31) / 32) * 2 * x->Hp * 32);
   A(x->acst, Cs * G * (x->Hp + 1));
+  if (x->scorer == 2) {
+    const size_t nch = (D + 31) / 32;
+    A(x->lblk, Cs * ws_groups(dm) * nch * 4 * 16 * 32);
+    A(x->cblk, Cs * nch * 4 * 16 * 32);
+  }
   A(x->ipsi32, Cs * D);
   A(x->K, N * Cp);
   A(x->g, Cs * G);

@@ -215,6 +215,10 @@ cudaError_t launch_ws_prep(const Dims& dm, const float* WT, float* WTS, cudaStre
 cudaError_t launch_anchor_consts(const Dims& dm, const float* WT, const float* mu32, const float* ipsi32,
                                  const int* g, const int* gcnt, float* acst, cudaStream_t s);
 cudaError_t launch_score_ws(int mode, const ScoreArgs& s, const float* WTS, const float* mu32,
-                            const float* ipsi32, const float* acst, cudaStream_t st);
+                            const float* ipsi32, const float* acst, const float* lblk, const float* cblk,
+                            cudaStream_t st);
+int ws_groups(const Dims& dm);
+cudaError_t launch_ws_blocks(const Dims& dm, int single, const float* mu32, const float* ipsi32,
+                             const int* g, const int* gcnt, float* blk, cudaStream_t s);
 
 }  // namespace vmfa_b200

@@ -18,6 +18,7 @@
 //              tcgen05.commit to the stage's empty barrier;
 //   warps 9-12 epilogue: tcgen05.ld of a finished accumulator (TMEM double
 //              buffered), log-joint assembly, scatter to the candidate slots.
+#include <algorithm>
 #include <cstdint>
 
 #include "vmfa_kernels.cuh"
@@ -51,6 +52,9 @@ struct WsArgs {
   const float* ipsi32;
   const double* kconst;
   const float* acst; // [C][G][Hp + 1] : b (Hp) then m, anchor mode only
+  const float* lblk; // anchor mode: [C][ngroups][nchunk][4][16][32] lin hi|lo, psi hi|lo tiles
+  const float* cblk; // single mode: [C][nchunk][4][16][32] (lin = 0, psi row 0)
+  int ngroups;
   const int* off;
   const int* ent;
   const int* itemoff;
@@ -277,16 +281,23 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_ws(WsArgs a) {
           if (use >= 1) mbar_wait(&s_empty[s], (use - 1) & 1u);
           const uint32_t st = sbase + s * a.stage_bytes;
           const int d0 = ch * kKC;
-          // W blocks: bulk copies (hi, lo) for each component of the job
+          // B operands: bulk copies of the pre-split, pre-swizzled blocks
           if (tid == 0) {
             const uint32_t blk = HP * 128;
-            mbar_expect_tx(&s_full[s], 2 * nq * blk);
+            mbar_expect_tx(&s_full[s], 2 * nq * blk + 4 * kNL * 128);
             for (int qi = 0; qi < nq; ++qi) {
               const float* src = a.WTS + ((int64_t)M.comp[qi] * nchunk + ch) * 2 * HP * 32;
               const uint32_t row = kNL + qi * HP;
               bulk_copy(st + offB1 + row * 128, src, blk, &s_full[s]);
               bulk_copy(st + offB1 + a.N1max * 128 + row * 128, src + HP * 32, blk, &s_full[s]);
             }
+            const float* lb = a.mode == kModeAnchor
+                                  ? a.lblk + (((int64_t)J.c * a.ngroups + g0 / a.qg) * nchunk + ch) * 4 * kNL * 32
+                                  : a.cblk + ((int64_t)J.c * nchunk + ch) * 4 * kNL * 32;
+            bulk_copy(st + offB1, lb, kNL * 128, &s_full[s]);                               // lin hi
+            bulk_copy(st + offB1 + a.N1max * 128, lb + kNL * 32, kNL * 128, &s_full[s]);    // lin lo
+            bulk_copy(st + offB2, lb + 2 * kNL * 32, kNL * 128, &s_full[s]);                // psi hi
+            bulk_copy(st + offB2 + kNL * 128, lb + 3 * kNL * 32, kNL * 128, &s_full[s]);    // psi lo
           }
           // A: v = x - mu_a and v^2, split hi/lo
 #pragma unroll
@@ -307,44 +318,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_ws(WsArgs a) {
             st4(st + kTileA + o, vl[0], vl[1], vl[2], vl[3]);
             st4(st + 2 * kTileA + o, qh[0], qh[1], qh[2], qh[3]);
             st4(st + 3 * kTileA + o, ql[0], ql[1], ql[2], ql[3]);
-          }
-          // lin rows (B1 rows 0..nq) and psi^-1 rows (B2 rows 0..nq): units (row, chunk j)
-          {
-            const int u = tid;  // 2 * 16 rows x 8 chunks = 256 units
-            const int kind = u >> 7, qi = (u >> 3) & 15, j = u & 7;
-            if (qi < nq) {
-              const int q = M.comp[qi];
-              const int d = d0 + 4 * j;
-              float val[4] = {0.f, 0.f, 0.f, 0.f};
-              if (d < dm.D) {
-                const float* ipq = a.ipsi32 + (int64_t)q * dm.D + d;
-                float ip[4], mq[4];
-                if (vec) {
-                  const float4 t = __ldg(reinterpret_cast<const float4*>(ipq));
-                  ip[0] = t.x, ip[1] = t.y, ip[2] = t.z, ip[3] = t.w;
-                  if (kind == 0) {
-                    const float4 w = __ldg(reinterpret_cast<const float4*>(a.mu32 + (int64_t)q * dm.D + d));
-                    mq[0] = w.x, mq[1] = w.y, mq[2] = w.z, mq[3] = w.w;
-                  }
-                } else {
-                  for (int k = 0; k < 4; ++k) {
-                    ip[k] = d + k < dm.D ? __ldg(ipq + k) : 0.f;
-                    mq[k] = d + k < dm.D ? __ldg(a.mu32 + (int64_t)q * dm.D + d + k) : 0.f;
-                  }
-                }
-#pragma unroll
-                for (int k = 0; k < 4; ++k)
-                  val[k] = kind == 0 ? -2.f * ip[k] * (mq[k] - s_mu[d + k]) : ip[k];
-              }
-              uint32_t bh[4], bl[4];
-#pragma unroll
-              for (int k = 0; k < 4; ++k) split(val[k], bh[k], bl[k]);
-              const uint32_t base = kind == 0 ? st + offB1 : st + offB2;
-              const uint32_t lo_off = kind == 0 ? a.N1max * 128 : kNL * 128;
-              const uint32_t o = swz(qi, j);
-              st4(base + o, bh[0], bh[1], bh[2], bh[3]);
-              st4(base + lo_off + o, bl[0], bl[1], bl[2], bl[3]);
-            }
           }
           fence_async_smem();
           __syncwarp();
@@ -531,7 +504,66 @@ __global__ void k_build_wts(Dims dm, int Hp, const float* WT, float* WTS) {
   }
 }
 
+// Anchor-dependent B blocks, once per E-step (g and the parameters are fixed
+// during the E-step): for anchor a, component group grp, K chunk ch, the 16-row
+// tiles [lin hi | lin lo | psi hi | psi lo] with lin_q = -2 psi_q^-1 (mu_q - mu_a),
+// pre-split and pre-swizzled exactly as the smem B tiles. single != 0 builds
+// the one-component blocks (q = a, lin = 0) of the extra / truncated-F passes.
+__global__ void k_build_blocks(Dims dm, int qg, int ngroups, int single, const float* mu32,
+                               const float* ipsi32, const int* g, const int* gcnt, float* blk) {
+  const int nchunk = (dm.D + kKC - 1) / kKC;
+  const int ng = single ? 1 : ngroups;
+  const int64_t total = (int64_t)dm.C * ng * nchunk * kNL * kKC;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int e = static_cast<int>(i % kKC);
+    int64_t t = i / kKC;
+    const int qi = static_cast<int>(t % kNL);
+    t /= kNL;
+    const int ch = static_cast<int>(t % nchunk);
+    t /= nchunk;
+    const int grp = static_cast<int>(t % ng);
+    const int a = static_cast<int>(t / ng);
+    const int d = ch * kKC + e;
+    int q = -1;
+    if (single) {
+      if (qi == 0) q = a;
+    } else {
+      const int slot = grp * qg + qi;
+      if (qi < qg && slot < gcnt[a]) q = g[(int64_t)a * dm.G + slot];
+    }
+    float lin = 0.f, ip = 0.f;
+    if (q >= 0 && d < dm.D) {
+      ip = ipsi32[(int64_t)q * dm.D + d];
+      lin = single ? 0.f : -2.f * ip * (mu32[(int64_t)q * dm.D + d] - mu32[(int64_t)a * dm.D + d]);
+    }
+    uint32_t lh, ll, ph, pl;
+    split(lin, lh, ll);
+    split(ip, ph, pl);
+    const int j = e >> 2;
+    const int pos = qi * 32 + (((j ^ (qi & 7)) & 7) << 2) + (e & 3);
+    float* b = blk + (((int64_t)a * ng + grp) * nchunk + ch) * 4 * kNL * 32;
+    b[pos] = __uint_as_float(lh);
+    b[kNL * 32 + pos] = __uint_as_float(ll);
+    b[2 * kNL * 32 + pos] = __uint_as_float(ph);
+    b[3 * kNL * 32 + pos] = __uint_as_float(pl);
+  }
+}
+
 }  // namespace
+
+int ws_groups(const Dims& dm) {
+  const int Hp = ws_hp(dm.H);
+  const int qg = std::max(1, std::min(std::min(dm.G, kNL), (256 - kNL) / Hp));
+  return (dm.G + qg - 1) / qg;
+}
+
+cudaError_t launch_ws_blocks(const Dims& dm, int single, const float* mu32, const float* ipsi32,
+                             const int* g, const int* gcnt, float* blk, cudaStream_t s) {
+  const int Hp = ws_hp(dm.H);
+  const int qg = std::max(1, std::min(std::min(dm.G, kNL), (256 - kNL) / Hp));
+  k_build_blocks<<<sm_count() * 8, 256, 0, s>>>(dm, qg, ws_groups(dm), single, mu32, ipsi32, g, gcnt, blk);
+  return cudaGetLastError();
+}
 
 bool score_ws_supported(const Dims& dm) { return dm.D <= kMaxD && dm.H <= 64 && dm.G <= 64; }
 
@@ -551,7 +583,8 @@ cudaError_t launch_anchor_consts(const Dims& dm, const float* WT, const float* m
 }
 
 cudaError_t launch_score_ws(int mode, const ScoreArgs& s, const float* WTS, const float* mu32,
-                            const float* ipsi32, const float* acst, cudaStream_t st) {
+                            const float* ipsi32, const float* acst, const float* lblk, const float* cblk,
+                            cudaStream_t st) {
   WsArgs a{};
   a.dm = s.dm;
   a.mode = mode;
@@ -571,6 +604,9 @@ cudaError_t launch_score_ws(int mode, const ScoreArgs& s, const float* WTS, cons
   a.ipsi32 = ipsi32;
   a.kconst = s.kconst;
   a.acst = acst;
+  a.lblk = lblk;
+  a.cblk = cblk;
+  a.ngroups = ws_groups(s.dm);
   a.off = s.off;
   a.ent = s.ent;
   a.itemoff = s.itemoff;
