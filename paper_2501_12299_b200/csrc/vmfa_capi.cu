@@ -589,6 +589,7 @@ int vmfa_ctx_create(vmfa_ctx** out, int device, int C, int D, int H, int Cp, int
   auto A = [&](auto*& p, size_t n) {
     if (r == VMFA_OK) r = x->alloc(p, n);
   };
+  const bool dense_rows = 3.0 * Cs * Cs * sizeof(long long) <= 8.0 * (1ull << 30);
   A(x->X, N * D);
   A(x->floor, D);
   for (double** p : {&x->pi, &x->pi2}) A(*p, Cs);
@@ -654,7 +655,7 @@ int vmfa_ctx_create(vmfa_ctx** out, int device, int C, int D, int H, int Cp, int
   }
   // dense C x C rows (count, fixed-point hi, lo) for split components and the
   // multi-rank exchange; without it (very large C) components are not split.
-  if (3.0 * Cs * Cs * sizeof(long long) <= 8.0 * (1ull << 30)) {
+  if (dense_rows) {
     A(x->xc, 3 * Cs * Cs);
     if (r == VMFA_OK) cudaMemsetAsync(x->xc, 0, 3 * Cs * Cs * sizeof(long long), x->stream);
   } else {
@@ -662,10 +663,12 @@ int vmfa_ctx_create(vmfa_ctx** out, int device, int C, int D, int H, int Cp, int
   }
   A(x->cnt, Cs + 1);
   A(x->chunks, Cs + 1);
-  x->gupd_grid = static_cast<int>(std::min<int64_t>(C, sm_count() * 2));
-  A(x->gt_cnt, static_cast<size_t>(x->gupd_grid) * Cs);
-  A(x->gt_hi, static_cast<size_t>(x->gupd_grid) * Cs);
-  A(x->gt_lo, static_cast<size_t>(x->gupd_grid) * Cs);
+  x->gupd_grid = sm_count() * 4;
+  // per-CTA dense fallback tables: only needed without the dense C x C rows
+  const size_t gt_n = dense_rows ? 1 : static_cast<size_t>(x->gupd_grid) * Cs;
+  A(x->gt_cnt, gt_n);
+  A(x->gt_hi, gt_n);
+  A(x->gt_lo, gt_n);
   x->stats_len = Cs + Cs * H1 * H1 + Cs * H1 * D + Cs * D;
   A(x->stats, x->stats_len);
   A(x->partials, 512);

@@ -231,6 +231,13 @@ __device__ __forceinline__ bool better(const Cand& x, const Cand& y) {
   return x.c < y.c;
 }
 
+// Order-preserving 64-bit key: larger key = larger l, ties -> smaller index.
+__device__ __forceinline__ unsigned long long sel_key(float l, int c) {
+  unsigned u = __float_as_uint(l);
+  u = (u & 0x80000000u) ? ~u : (u | 0x80000000u);  // monotone float -> uint
+  return (static_cast<unsigned long long>(u) << 32) | static_cast<unsigned>(0x7fffffff - c);
+}
+
 template <int NS>
 __global__ void __launch_bounds__(256) k_select(SelectArgs a) {
   const Dims dm = a.dm;
@@ -238,6 +245,7 @@ __global__ void __launch_bounds__(256) k_select(SelectArgs a) {
   const int64_t warp0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int CpG = dm.Cp * dm.G;
+  const unsigned lt_mask = (1u << lane) - 1u;
   for (int64_t n = warp0; n < dm.N; n += nwarps) {
     int comp[NS];
     bool uniq[NS];
@@ -254,20 +262,21 @@ __global__ void __launch_bounds__(256) k_select(SelectArgs a) {
         cmp = a.rx[n];
       }
       comp[k] = cmp;
-      uniq[k] = cmp >= 0;
     }
-    // first-occurrence dedup in slot order
+    // first-occurrence dedup in slot order (s = k*32 + lane): within a round by
+    // __match_any_sync (keep the lowest lane), across rounds by broadcast compares
 #pragma unroll
     for (int k = 0; k < NS; ++k) {
-      for (int src = 0; src < 32; ++src) {
-        const int t = k * 32 + src;
-        if (t >= dm.SL) break;
-        const int ct = __shfl_sync(kFull, comp[k], src);
-        if (ct < 0) continue;
+      const unsigned m = __match_any_sync(kFull, comp[k]);
+      uniq[k] = comp[k] >= 0 && (m & lt_mask) == 0u;
+    }
 #pragma unroll
-        for (int kk = 0; kk < NS; ++kk) {
-          const int s = kk * 32 + lane;
-          if (s > t && comp[kk] == ct) uniq[kk] = false;
+    for (int k = 1; k < NS; ++k) {
+#pragma unroll
+      for (int k0 = 0; k0 < k; ++k0) {
+        for (int src = 0; src < 32; ++src) {
+          const int ct = __shfl_sync(kFull, comp[k0], src);
+          if (ct >= 0 && ct == comp[k]) uniq[k] = false;
         }
       }
     }
@@ -286,44 +295,42 @@ __global__ void __launch_bounds__(256) k_select(SelectArgs a) {
     for (int k = 0; k < NS; ++k) {
       const unsigned b = __ballot_sync(kFull, uniq[k]);
       if (uniq[k]) {
-        const int pos = base + __popc(b & ((1u << lane) - 1u));
+        const int pos = base + __popc(b & lt_mask);
         a.ret_idx[n * dm.stride + pos] = comp[k];
         a.ret_lj[n * dm.stride + pos] = lj[k];
       }
       base += __popc(b);
     }
     const int m = base;
-    // top-C' by (l desc, index asc)
-    bool sel[NS];
+    // top-C' by (l desc, index asc) on packed keys; 0 = no candidate
+    unsigned long long key[NS];
 #pragma unroll
-    for (int k = 0; k < NS; ++k) sel[k] = false;
+    for (int k = 0; k < NS; ++k) key[k] = uniq[k] ? sel_key(lj[k], comp[k]) : 0ull;
     int kc[8];
     float kl[8];
     for (int r = 0; r < dm.Cp; ++r) {
-      Cand best{-INFINITY, 0x7fffffff, -1, 0};
+      unsigned long long best = 0ull;
 #pragma unroll
-      for (int k = 0; k < NS; ++k) {
-        if (!uniq[k] || sel[k]) continue;
-        Cand cnd{lj[k], comp[k], k * 32 + lane, 1};
-        if (better(cnd, best)) best = cnd;
-      }
+      for (int k = 0; k < NS; ++k) best = key[k] > best ? key[k] : best;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
-        Cand oth;
-        oth.l = __shfl_xor_sync(kFull, best.l, o);
-        oth.c = __shfl_xor_sync(kFull, best.c, o);
-        oth.slot = __shfl_xor_sync(kFull, best.slot, o);
-        oth.valid = __shfl_xor_sync(kFull, best.valid, o);
-        if (better(oth, best)) best = oth;
+        const unsigned long long oth = __shfl_xor_sync(kFull, best, o);
+        best = oth > best ? oth : best;
       }
-      kc[r] = best.c;
-      kl[r] = best.l;
-      if (best.valid && (best.slot & 31) == lane) {
+      if (best == 0ull) {
+        if (lane == 0) atomicOr(a.status, 1);  // InsufficientCandidates
+        kc[r] = 0;
+        kl[r] = -INFINITY;
+        continue;
+      }
+      const int c = 0x7fffffff - static_cast<int>(best & 0xffffffffu);
+      unsigned u = static_cast<unsigned>(best >> 32);
+      u = (u & 0x80000000u) ? (u & 0x7fffffffu) : ~u;
+      kc[r] = c;
+      kl[r] = __uint_as_float(u);
 #pragma unroll
-        for (int k = 0; k < NS; ++k)
-          if (best.slot == k * 32 + lane) sel[k] = true;
-      }
-      if (!best.valid && lane == 0) atomicOr(a.status, 1);  // InsufficientCandidates
+      for (int k = 0; k < NS; ++k)
+        if (key[k] == best) key[k] = 0ull;  // unique keys: only the owner matches
     }
     // sort (kc, kl) ascending by component (estep.cpp:121)
     for (int i = 1; i < dm.Cp; ++i) {
@@ -351,9 +358,9 @@ __global__ void __launch_bounds__(256) k_select(SelectArgs a) {
     for (int j = 0; j < dm.Cp; ++j) mx = fmax(mx, static_cast<double>(kl[j]));
     double l = mx;
     if (isfinite(mx)) {
-      double s = 0.0;
-      for (int j = 0; j < dm.Cp; ++j) s += exp(static_cast<double>(kl[j]) - mx);
-      l = mx + log(s);
+      double s2 = 0.0;
+      for (int j = 0; j < dm.Cp; ++j) s2 += exp(static_cast<double>(kl[j]) - mx);
+      l = mx + log(s2);
     }
     if (lane < dm.Cp) {
       int myc = kc[0];
@@ -422,12 +429,12 @@ __device__ __forceinline__ void sort_small(int* v, int m) {
 // larger components (and every component in exchange mode) add their exact
 // integer partial sums into row c of the dense table xc (order-independent),
 // and k_gselect_dense selects from the rows.
-__global__ void __launch_bounds__(kGupdThreads) k_gupdate(GupdArgs a) {
+__global__ void __launch_bounds__(kGupdThreads) k_gupdate(GupdArgs a, int capmax) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   long long* t_hi = reinterpret_cast<long long*>(smem_raw);
-  long long* t_lo = t_hi + kGupdCap;
-  int* t_key = reinterpret_cast<int*>(t_lo + kGupdCap);
-  int* t_cnt = t_key + kGupdCap;
+  long long* t_lo = t_hi + capmax;
+  int* t_key = reinterpret_cast<int*>(t_lo + capmax);
+  int* t_cnt = t_key + capmax;
   __shared__ KeyMin red[kGupdThreads / 32];
   __shared__ int s_sel[64];
   __shared__ int s_nsel;
@@ -448,8 +455,8 @@ __global__ void __launch_bounds__(kGupdThreads) k_gupdate(GupdArgs a) {
     const bool to_rows = a.exchange || nitems > 1;
     const long long bound = llmin((long long)dm.C - 1, (long long)npts * (dm.stride - 1));
     int cap = 32;
-    while (cap < 2 * bound && cap < 2 * kGupdCap) cap <<= 1;
-    const bool use_smem = cap <= kGupdCap;
+    while (cap < 2 * bound && cap < 2 * capmax) cap <<= 1;
+    const bool use_smem = cap <= capmax;
     if (npts > 0) {
       if (use_smem) {
         for (int i = tid; i < cap; i += kGupdThreads) {
@@ -1504,10 +1511,17 @@ cudaError_t launch_select(const SelectArgs& a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+int gupd_capmax(const Dims& dm, int pts_per_item) {
+  const long long bound = std::min<long long>((long long)dm.C - 1, (long long)pts_per_item * (dm.stride - 1));
+  int cap = 32;
+  while (cap < 2 * bound && cap < kGupdCap) cap <<= 1;
+  return cap;
+}
 cudaError_t launch_gupdate(const GupdArgs& a, int grid, cudaStream_t s) {
-  const size_t smem = static_cast<size_t>(kGupdCap) * (2 * sizeof(long long) + 2 * sizeof(int));
+  const int capmax = gupd_capmax(a.dm, a.pts_per_item);
+  const size_t smem = static_cast<size_t>(capmax) * (2 * sizeof(long long) + 2 * sizeof(int));
   cudaFuncSetAttribute(k_gupdate, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-  k_gupdate<<<grid, kGupdThreads, smem, s>>>(a);
+  k_gupdate<<<grid, kGupdThreads, smem, s>>>(a, capmax);
   return cudaGetLastError();
 }
 cudaError_t launch_gselect_dense(const Dims& dm, long long* xc, const int* itemoff, int all,
