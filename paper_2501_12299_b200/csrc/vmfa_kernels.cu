@@ -680,34 +680,36 @@ constexpr int kStatsMaxH1 = 17;   // columns of Y per pass
 constexpr int kXPad = 4;  // s_x row stride D + 4: conflict-free LDS.128 across rows
 
 template <int NH1, int ND>
-__global__ void __launch_bounds__(kStatsThreads) k_stats(StatsArgs a, const int* __restrict__ itemoff,
+__global__ void __launch_bounds__(kStatsThreads, 2) k_stats(StatsArgs a, const int* __restrict__ itemoff,
                                                         int rows_per_item, int col0, double* part,
                                                         int64_t part_stride, int nbuf) {
-  // smem: s_x [nbuf][B][D+4] | s_V [D][VS] | s_mu [D] | s_pz [8][B][NH1] | s_zd [B][NH1] (double)
+  // smem: s_x [nbuf][B][XS] | s_V [D][VS] | s_mu [D+pad] | s_pz [8][B][NH1] | s_zf [B][ZS] (float)
   extern __shared__ __align__(16) float s_x[];
   constexpr int VS = (NH1 + 3) / 4 * 4;  // V row stride (16-byte rows for LDS.128)
+  constexpr int ZS = VS;                 // zhat row stride in s_zf
   __shared__ double s_qb[2][kStatsBatch];
   __shared__ int s_e[2][kStatsBatch];
+  __shared__ double s_red[kStatsThreads / 32];
   const Dims dm = a.dm;
   const int H = dm.H, H1 = H + 1, D = dm.D;
   const int XS = (D + 3) / 4 * 4 + kXPad;
   float* s_V = s_x + (int64_t)nbuf * kStatsBatch * XS;
   float* s_mu = s_V + (int64_t)D * VS;
-  float* s_pz = s_mu + (D + 3) / 4 * 4 + 4;                 // [8][B][NH1]
-  double* s_zd = reinterpret_cast<double*>(s_pz + 8 * kStatsBatch * NH1 + 2);  // 8-byte aligned
-  s_zd = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(s_zd) + 15) & ~uintptr_t(15));
+  float* s_pz = s_mu + (D + 3) / 4 * 4 + 4;  // [8][B][NH1]
+  float* s_zf = s_pz + 8 * kStatsBatch * NH1;  // [B][ZS]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const bool first = col0 == 0;
   const bool full_e = first && (H1 <= NH1);
   const bool vec = (D & 3) == 0;
-  constexpr int NE = (NH1 * NH1 + kStatsThreads - 1) / kStatsThreads;
-  // phase (ii) tiling: GD dimension groups of 4, RG row groups
-  const int GD = (D + 3) / 4;
+  // register tiles over "dimensions" [0, D) of the centred row and, when E is
+  // produced here, [Dp, Dp + H1) of zhat itself (E = sum q zhat zhat^T)
+  const int Dp = (D + 3) / 4 * 4;
+  const int GX = Dp / 4;
+  const int GD = GX + (full_e ? (H1 + 3) / 4 : 0);
   const int RG = max(1, kStatsThreads / GD);
   const int my_dg = tid % GD, my_rg = tid / GD;
   const bool tile_on = my_rg < RG && tid < RG * GD;
-  // phase (i) dimension slice of this warp
-  const int dsl = ((D + 7) / 8 + 3) / 4 * 4;  // dims per warp, multiple of 4
+  const int dsl = ((D + 7) / 8 + 3) / 4 * 4;  // phase (i) dims per warp, multiple of 4
   const int dw0 = warp * dsl, dw1 = min(D, dw0 + dsl);
   const int total = __ldg(itemoff + dm.C);
   for (int item = blockIdx.x; item < total; item += gridDim.x) {
@@ -715,8 +717,24 @@ __global__ void __launch_bounds__(kStatsThreads) k_stats(StatsArgs a, const int*
     const int r0 = a.off[c] + (item - itemoff[c]) * rows_per_item;
     const int r1 = min(a.off[c + 1], r0 + rows_per_item);
     const bool direct = itemoff[c + 1] - itemoff[c] == 1;  // sole item: write the statistics
-    // centred statistics (v = x - mu_c): Y_v = sum q v zhat^T, sq_v = sum q v^2
-    // in fp32 over the item; k_stats_uncenter restores Y and sq in fp64
+    // responsibilities are scaled by the item's largest q before the fp32
+    // accumulation (no underflow; N_c == 0 exactly iff every q == 0)
+    double qmax = 0.0;
+    for (int i = r0 + tid; i < r1; i += kStatsThreads) qmax = fmax(qmax, a.resp[a.ent[i]]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) qmax = fmax(qmax, __shfl_xor_sync(kFull, qmax, o));
+    __syncthreads();  // previous item done with the shared buffers
+    if (lane == 0) s_red[warp] = qmax;
+    for (int i = tid; i < D * VS; i += kStatsThreads) {
+      const int d = i / VS, h = i - d * VS;
+      s_V[i] = (h < NH1 && col0 + h < H) ? __ldg(a.V32 + (int64_t)c * D * H + (int64_t)d * H + col0 + h) : 0.f;
+    }
+    for (int d = tid; d < Dp + 4; d += kStatsThreads) s_mu[d] = d < D ? __ldg(a.mu32 + (int64_t)c * D + d) : 0.f;
+    __syncthreads();
+    qmax = 0.0;
+#pragma unroll
+    for (int w = 0; w < kStatsThreads / 32; ++w) qmax = fmax(qmax, s_red[w]);
+    const double qinv = qmax > 0.0 ? 1.0 / qmax : 0.0;
     float accY[ND][4][NH1];
     float accS[ND][4];
 #pragma unroll
@@ -727,24 +745,13 @@ __global__ void __launch_bounds__(kStatsThreads) k_stats(StatsArgs a, const int*
 #pragma unroll
         for (int h = 0; h < NH1; ++h) accY[k][i][h] = 0.f;
       }
-    double accE[NE];
-#pragma unroll
-    for (int k = 0; k < NE; ++k) accE[k] = 0.0;
-    const float* Vc = a.V32 + (int64_t)c * D * H;
-    const float* mc = a.mu32 + (int64_t)c * D;
-    __syncthreads();  // previous item done with the shared buffers
-    for (int i = tid; i < D * VS; i += kStatsThreads) {
-      const int d = i / VS, h = i - d * VS;
-      s_V[i] = (h < NH1 && col0 + h < H) ? __ldg(Vc + (int64_t)d * H + col0 + h) : 0.f;
-    }
-    for (int d = tid; d < D; d += kStatsThreads) s_mu[d] = __ldg(mc + d);
     const int nbat = (r1 - r0 + kStatsBatch - 1) / kStatsBatch;
     auto stage_ids = [&](int b, int buf) {
       if (tid < kStatsBatch) {
         const int i = r0 + b * kStatsBatch + tid;
         const int e = i < r1 ? a.ent[i] : -1;
         s_e[buf][tid] = e;
-        s_qb[buf][tid] = e >= 0 ? a.resp[e] : 0.0;
+        s_qb[buf][tid] = e >= 0 ? a.resp[e] * qinv : 0.0;
       }
     };
     auto issue_rows = [&](int buf) {
@@ -826,39 +833,47 @@ __global__ void __launch_bounds__(kStatsThreads) k_stats(StatsArgs a, const int*
         for (int h = 0; h < NH1; ++h) pz[h] = acc[h];
       }
       __syncthreads();
-      const double* s_q = s_qb[buf];
-      for (int i = tid; i < kStatsBatch * NH1; i += kStatsThreads) {
-        const int r = i / NH1, h = i - r * NH1;
+      for (int i = tid; i < kStatsBatch * ZS; i += kStatsThreads) {
+        const int r = i / ZS, h = i - r * ZS;
         float z = 0.f;
+        if (h < NH1) {
 #pragma unroll
-        for (int w = 0; w < 8; ++w) z += s_pz[((int64_t)w * kStatsBatch + r) * NH1 + h];
-        const int hh = col0 + h;
-        s_zd[i] = hh < H ? static_cast<double>(z) : (hh == H ? 1.0 : 0.0);
+          for (int w = 0; w < 8; ++w) z += s_pz[((int64_t)w * kStatsBatch + r) * NH1 + h];
+          const int hh = col0 + h;
+          z = hh < H ? z : (hh == H ? 1.f : 0.f);
+        }
+        s_zf[i] = z;
       }
       __syncthreads();
-      // (ii) fp64 register tiles: dims [4*dg, 4*dg+4) x NH1 columns, rows rg::RG
+      // (ii) register tiles: 4 "dimensions" x NH1 columns, rows my_rg::RG
       if (tile_on) {
+        const double* s_q = s_qb[buf];
         for (int r = my_rg; r < nb; r += RG) {
-          const double q = s_q[r];
+          const float qf = static_cast<float>(s_q[r]);
           const float* xr = xb + (int64_t)r * XS;
-          const double* zr = s_zd + r * NH1;
+          const float* zr = s_zf + r * ZS;
           float zf[NH1];
 #pragma unroll
-          for (int h = 0; h < NH1; ++h) zf[h] = static_cast<float>(zr[h]);
-#pragma unroll
-          const float qf = static_cast<float>(q);
+          for (int h = 0; h < NH1; ++h) zf[h] = zr[h];
 #pragma unroll
           for (int k = 0; k < ND; ++k) {
-            const int d = 4 * (my_dg + k * GD);
-            if (d >= D) break;
+            const int g = my_dg + k * GD;
+            if (k > 0 && g >= GD) break;
             float vs[4];
-            if (vec || d + 3 < D) {
-              const float4 xv = *reinterpret_cast<const float4*>(xr + d);
-              const float4 mv = *reinterpret_cast<const float4*>(s_mu + d);
-              vs[0] = xv.x - mv.x, vs[1] = xv.y - mv.y, vs[2] = xv.z - mv.z, vs[3] = xv.w - mv.w;
-            } else {
+            if (g < GX) {
+              const int d = 4 * g;
+              if (vec || d + 3 < D) {
+                const float4 xv = *reinterpret_cast<const float4*>(xr + d);
+                const float4 mv = *reinterpret_cast<const float4*>(s_mu + d);
+                vs[0] = xv.x - mv.x, vs[1] = xv.y - mv.y, vs[2] = xv.z - mv.z, vs[3] = xv.w - mv.w;
+              } else {
 #pragma unroll
-              for (int i = 0; i < 4; ++i) vs[i] = d + i < D ? xr[d + i] - s_mu[d + i] : 0.f;
+                for (int i = 0; i < 4; ++i) vs[i] = d + i < D ? xr[d + i] - s_mu[d + i] : 0.f;
+              }
+            } else {
+              const int z0 = 4 * (g - GX);
+#pragma unroll
+              for (int i = 0; i < 4; ++i) vs[i] = z0 + i < ZS ? zr[z0 + i] : 0.f;
             }
             float qv[4];
 #pragma unroll
@@ -868,22 +883,8 @@ __global__ void __launch_bounds__(kStatsThreads) k_stats(StatsArgs a, const int*
             }
 #pragma unroll
             for (int h = 0; h < NH1; ++h) {
-              const float z = zf[h];
 #pragma unroll
-              for (int i = 0; i < 4; ++i) accY[k][i][h] = fmaf(qv[i], z, accY[k][i][h]);
-            }
-          }
-        }
-      }
-      if (full_e) {
-        for (int r = 0; r < nb; ++r) {
-          const double q = s_q[r];
-#pragma unroll
-          for (int k = 0; k < NE; ++k) {
-            const int idx = tid + k * kStatsThreads;
-            if (idx < H1 * H1) {
-              const int i = idx % H1, j = idx / H1;
-              accE[k] = fma(q * s_zd[r * NH1 + i], s_zd[r * NH1 + j], accE[k]);
+              for (int i = 0; i < 4; ++i) accY[k][i][h] = fmaf(qv[i], zf[h], accY[k][i][h]);
             }
           }
         }
@@ -891,9 +892,10 @@ __global__ void __launch_bounds__(kStatsThreads) k_stats(StatsArgs a, const int*
       __syncthreads();
     }
     // combine the row groups of each dimension group through smem (fp64),
-    // reusing the row buffers, then write (direct or partial)
+    // reusing the row buffers, then write (direct or partial) scaled by qmax
     double* red = reinterpret_cast<double*>(s_x);  // >= RG * GD * 4 * (NH1 + 1) doubles
     double* pp = direct ? nullptr : part + (int64_t)item * part_stride;
+    double* pe = direct ? a.E + (int64_t)c * H1 * H1 : pp + (int64_t)NH1 * D + D;
 #pragma unroll
     for (int k = 0; k < ND; ++k) {
       __syncthreads();
@@ -908,48 +910,46 @@ __global__ void __launch_bounds__(kStatsThreads) k_stats(StatsArgs a, const int*
       }
       __syncthreads();
       if (tile_on && my_rg == 0) {
-        for (int g = 1; g < RG; ++g) {
-          const double* src = red + ((int64_t)(g - 1) * GD + my_dg) * 4 * (NH1 + 1);
+        double ty[4][NH1], ts[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          ts[i] = accS[k][i];
+#pragma unroll
+          for (int h = 0; h < NH1; ++h) ty[i][h] = accY[k][i][h];
+        }
+        for (int gg = 1; gg < RG; ++gg) {
+          const double* src = red + ((int64_t)(gg - 1) * GD + my_dg) * 4 * (NH1 + 1);
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
 #pragma unroll
-            for (int h = 0; h < NH1; ++h) accY[k][i][h] += static_cast<float>(src[i * (NH1 + 1) + h]);
-            accS[k][i] += static_cast<float>(src[i * (NH1 + 1) + NH1]);
+            for (int h = 0; h < NH1; ++h) ty[i][h] += src[i * (NH1 + 1) + h];
+            ts[i] += src[i * (NH1 + 1) + NH1];
           }
         }
+        const int g = my_dg + k * GD;
+        if (k == 0 || g < GD) {
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int d = 4 * (my_dg + k * GD) + i;
-          if (d >= D) continue;
-          if (direct) {
+          for (int i = 0; i < 4; ++i) {
+            if (g < GX) {
+              const int d = 4 * g + i;
+              if (d >= D) continue;
+              if (direct) {
 #pragma unroll
-            for (int h = 0; h < NH1; ++h)
-              if (col0 + h < H1) a.Y[((int64_t)c * H1 + col0 + h) * D + d] = accY[k][i][h];
-            if (first) a.sq[(int64_t)c * D + d] = accS[k][i];
-          } else {
+                for (int h = 0; h < NH1; ++h)
+                  if (col0 + h < H1) a.Y[((int64_t)c * H1 + col0 + h) * D + d] = ty[i][h] * qmax;
+                if (first) a.sq[(int64_t)c * D + d] = ts[i] * qmax;
+              } else {
 #pragma unroll
-            for (int h = 0; h < NH1; ++h) pp[(int64_t)h * D + d] = accY[k][i][h];
-            if (first) pp[(int64_t)NH1 * D + d] = accS[k][i];
-          }
-        }
-      }
-    }
-    if (first) {
-      if (direct) {
-        if (full_e) {
+                for (int h = 0; h < NH1; ++h) pp[(int64_t)h * D + d] = ty[i][h] * qmax;
+                if (first) pp[(int64_t)NH1 * D + d] = ts[i] * qmax;
+              }
+            } else {
+              const int zi = 4 * (g - GX) + i;  // E row
+              if (zi >= H1) continue;
 #pragma unroll
-          for (int k = 0; k < NE; ++k) {
-            const int idx = tid + k * kStatsThreads;
-            if (idx < H1 * H1) a.E[(int64_t)c * H1 * H1 + idx] = accE[k];
-          }
-        }
-      } else {
-        double* pe = pp + (int64_t)NH1 * D + D;
-        if (full_e) {
-#pragma unroll
-          for (int k = 0; k < NE; ++k) {
-            const int idx = tid + k * kStatsThreads;
-            if (idx < H1 * H1) pe[idx] = accE[k];
+              for (int h = 0; h < NH1; ++h)
+                if (h < H1) pe[h * H1 + zi] = ty[i][h] * qmax;  // E(zi, h), col-major
+            }
           }
         }
       }
@@ -1536,11 +1536,11 @@ static void stats_pass(const StatsArgs& a, const int* itemoff, int rpi, int grid
   const int D = a.dm.D;
   constexpr int VS = (NH1 + 3) / 4 * 4;
   const size_t XS = (D + 3) / 4 * 4 + kXPad;
-  const size_t fixed = (static_cast<size_t>(D) * VS + (D + 3) / 4 * 4 + 4 + 8 * kStatsBatch * NH1 + 8) * sizeof(float) +
-                       kStatsBatch * NH1 * sizeof(double) + 16;
+  const size_t fixed = (static_cast<size_t>(D) * VS + (D + 3) / 4 * 4 + 4 + 8 * kStatsBatch * NH1 +
+                        kStatsBatch * VS + 8) * sizeof(float);
   const size_t per_buf = static_cast<size_t>(kStatsBatch) * XS * sizeof(float);
   // the row-group reduction reuses the row buffers: RG-1 slices of GD*4*(NH1+1) doubles
-  const int GD = (D + 3) / 4;
+  const int GD = (D + 3) / 4 + (NH1 >= a.dm.H + 1 ? (a.dm.H + 1 + 3) / 4 : 0);
   const int RG = std::max(1, kStatsThreads / GD);
   const size_t red = static_cast<size_t>(std::max(RG - 1, 0)) * GD * 4 * (NH1 + 1) * sizeof(double);
   int nbuf = (2 * per_buf + fixed <= 200 * 1024) ? 2 : 1;
@@ -1550,7 +1550,7 @@ static void stats_pass(const StatsArgs& a, const int* itemoff, int rpi, int grid
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     kern<<<grid, kStatsThreads, smem, s>>>(a, itemoff, rpi, col0, part, ps, nbuf);
   };
-  if (D <= 4 * kStatsThreads) go(k_stats<NH1, 1>);
+  if (GD <= kStatsThreads) go(k_stats<NH1, 1>);
   else go(k_stats<NH1, 2>);
 }
 int64_t stats_part_stride(const Dims& dm) {
