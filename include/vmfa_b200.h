@@ -198,6 +198,13 @@ int vmfa_profile_enable(vmfa_ctx* ctx, int enable);
 int vmfa_kernel_times(vmfa_ctx* ctx, int max, double* ms, int64_t* launches, int64_t* units,
                       int* n);
 const char* vmfa_kernel_name(int i);
+/* Diagnostics: per-role cycle counters of the warp-specialised scorer summed
+ * over CTAs since the last read (producer: wait-accumulator, job sync, wait
+ * stage, build; MMA: wait-accumulator, wait stage, issue; epilogue: wait,
+ * work). enable=1 arms (or keeps) the counters; out (n entries) reads and
+ * clears them; enable=0 disarms.                                            */
+int vmfa_diag_scorer_cycles(int enable, unsigned long long* out, int n);
+
 /* Stream of the context (a cudaStream_t) for callers that order their own
  * work (e.g. NCCL) against it.                                              */
 void* vmfa_ctx_stream(vmfa_ctx* ctx);

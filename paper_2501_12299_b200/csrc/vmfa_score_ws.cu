@@ -21,6 +21,7 @@
 #include <algorithm>
 #include <cstdint>
 
+#include "vmfa_b200.h"
 #include "vmfa_kernels.cuh"
 
 namespace vmfa_b200 {
@@ -44,6 +45,8 @@ struct WsArgs {
   int qg;            // components per job (group)
   int N1max;         // 16 + round16(qg * Hp)
   int nstage;
+  int nacc;          // accumulator buffers in TMEM (2 when they fit beside the A stages)
+  uint32_t tmem_cols;
   uint32_t TB;       // TMEM columns per accumulator buffer
   uint32_t stage_bytes;
   const float* X;
@@ -61,6 +64,20 @@ struct WsArgs {
   const int* g;
   const int* gcnt;
   float* out;
+  unsigned long long* prof;  // optional per-role cycle counters (nullptr: off)
+};
+
+// per-role cycle accounting (debug builds of the pipeline; prof == nullptr in production)
+enum ProfSite { kPWaitTE, kPSync, kPWaitEmpty, kPBuild, kMWaitTE, kMWaitFull, kMIssue, kEWait, kEWork, kNumSites };
+struct Prof {
+  unsigned long long acc[kNumSites];
+  unsigned long long t;
+  __device__ void start() { t = clock64(); }
+  __device__ void lap(int site) {
+    const unsigned long long now = clock64();
+    acc[site] += now - t;
+    t = now;
+  }
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -100,6 +117,23 @@ __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
       "l"(a), "l"(b), "r"(id), "r"(accum));
+}
+// A operand from TMEM (lane = row, one tf32 per 32-bit column), B from smem
+__device__ __forceinline__ void mma_tf32_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t id,
+                                            uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(b), "r"(id), "r"(accum));
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
+      "%12, %13, %14, %15, %16};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
+      "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+      : "memory");
 }
 __device__ __forceinline__ void commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
@@ -209,7 +243,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_ws(WsArgs a) {
   }
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&s_tmem)),
-                 "r"(2 * a.TB));
+                 "r"(a.tmem_cols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   for (uint32_t i = tid * 16; i < a.stage_bytes * a.nstage; i += kThreads * 16) st4(sbase + i, 0, 0, 0, 0);
@@ -218,21 +252,28 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_ws(WsArgs a) {
   __syncthreads();
   fence_after();
   const uint32_t tmem = s_tmem;
-  // stage map (offsets from a 1024-aligned stage base)
-  const uint32_t offB1 = 4 * kTileA;                        // B1 hi, then B1 lo (N1max rows each)
+  // smem stage map (offsets from a 1024-aligned stage base): B operands only
+  const uint32_t offB1 = 0;                                 // B1 hi, then B1 lo (N1max rows each)
   const uint32_t offB2 = offB1 + 2 * a.N1max * 128;         // B2 hi, then B2 lo (16 rows each)
+  // TMEM map: accumulators [0, nacc*TB), A stages of 4 x 32 columns after them
+  const uint32_t colA = a.nacc * a.TB;
 
   if (warp < kProdWarps) {
     // ================================================================ producers
-    const int ar = tid & (kRows - 1), ah = tid >> 7;  // A: row, half of the 8 16-byte chunks
+    // A ownership: TMEM lane quadrant of this warp, one row per lane, K half ah
+    const int ar = 32 * (warp & 3) + lane, ah = warp >> 2;
     uint32_t sc = 0;
     int jb = 0;
+    Prof pf{};
+    pf.start();
     for (int item = blockIdx.x; item < total; item += gridDim.x) {
       const Job J = decode(a, item);
       for (int g0 = 0; g0 < J.ncomp; g0 += a.qg, ++jb) {
-        const int b = jb & 1;
+        const int b = a.nacc == 2 ? (jb & 1) : 0;
+        const int use_b = a.nacc == 2 ? (jb >> 1) : jb;
         const int nq = min(a.qg, J.ncomp - g0);
-        if (jb >= 2) mbar_wait(&s_tempty[b], ((jb >> 1) & 1) ^ 1);
+        if (use_b >= 1) mbar_wait(&s_tempty[b], (use_b - 1) & 1);
+        pf.lap(kPWaitTE);
         prod_sync();  // all producers done with the previous job's s_mu / meta reads
         Meta& M = s_meta[b];
         if (tid < kRows) {
@@ -251,6 +292,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_ws(WsArgs a) {
         for (int d = tid; d < nchunk * kKC; d += kProd) s_mu[d] = d < dm.D ? __ldg(mu_a + d) : 0.f;
         prod_sync();
         if (lane == 0) mbar_arrive(&s_mready[b]);  // meta[b] published to the epilogue
+        pf.lap(kPSync);
         const int e = M.e[ar];
         const int n = e < 0 ? -1 : (a.mode == kModeExtra ? e : e / dm.Cp);
         const float* xrow = a.X + (int64_t)(n < 0 ? 0 : n) * dm.D;
@@ -258,7 +300,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_ws(WsArgs a) {
         auto load_x = [&](int ch, float4* xv) {
 #pragma unroll
           for (int jj = 0; jj < 4; ++jj) {
-            const int d = ch * kKC + 4 * (4 * ah + jj);
+            const int d = ch * kKC + 16 * ah + 4 * jj;
             float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
             if (n >= 0 && d < dm.D) {
               if (vec) {
@@ -272,13 +314,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_ws(WsArgs a) {
             xv[jj] = t;
           }
         };
-        float4 xcur[4], xnext[4];
+        // register prefetch ring: rows of chunks ch+1 and ch+2 in flight while ch is built
+        float4 xcur[4], xn1[4], xn2[4];
         load_x(0, xcur);
+        if (nchunk > 1) load_x(1, xn1);
         for (int ch = 0; ch < nchunk; ++ch, ++sc) {
-          if (ch + 1 < nchunk) load_x(ch + 1, xnext);
+          if (ch + 2 < nchunk) load_x(ch + 2, xn2);
           const int s = a.nstage == 2 ? static_cast<int>(sc & 1u) : 0;
           const uint32_t use = a.nstage == 2 ? (sc >> 1) : sc;
+          pf.lap(kPBuild);
           if (use >= 1) mbar_wait(&s_empty[s], (use - 1) & 1u);
+          pf.lap(kPWaitEmpty);
           const uint32_t st = sbase + s * a.stage_bytes;
           const int d0 = ch * kKC;
           // B operands: bulk copies of the pre-split, pre-swizzled blocks
@@ -299,57 +345,72 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_ws(WsArgs a) {
             bulk_copy(st + offB2, lb + 2 * kNL * 32, kNL * 128, &s_full[s]);                // psi hi
             bulk_copy(st + offB2 + kNL * 128, lb + 3 * kNL * 32, kNL * 128, &s_full[s]);    // psi lo
           }
-          // A: v = x - mu_a and v^2, split hi/lo
+          // A: v = x - mu_a and v^2, split hi/lo, stored into TMEM (lane = row)
+          {
+            uint32_t vh[16], vl[16], qh[16], ql[16];
 #pragma unroll
-          for (int jj = 0; jj < 4; ++jj) {
-            const int j = 4 * ah + jj;
-            const float4 mv = *reinterpret_cast<const float4*>(s_mu + d0 + 4 * j);
-            const float4 xv = xcur[jj];
-            float v[4] = {xv.x - mv.x, xv.y - mv.y, xv.z - mv.z, xv.w - mv.w};
-            if (n < 0) v[0] = v[1] = v[2] = v[3] = 0.f;
-            uint32_t vh[4], vl[4], qh[4], ql[4];
+            for (int jj = 0; jj < 4; ++jj) {
+              const float4 mv = *reinterpret_cast<const float4*>(s_mu + d0 + 16 * ah + 4 * jj);
+              const float4 xv = xcur[jj];
+              float v[4] = {xv.x - mv.x, xv.y - mv.y, xv.z - mv.z, xv.w - mv.w};
+              if (n < 0) v[0] = v[1] = v[2] = v[3] = 0.f;
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              split(v[k], vh[k], vl[k]);
-              split(v[k] * v[k], qh[k], ql[k]);
+              for (int k = 0; k < 4; ++k) {
+                split(v[k], vh[4 * jj + k], vl[4 * jj + k]);
+                split(v[k] * v[k], qh[4 * jj + k], ql[4 * jj + k]);
+              }
             }
-            const uint32_t o = swz(ar, j);
-            st4(st + o, vh[0], vh[1], vh[2], vh[3]);
-            st4(st + kTileA + o, vl[0], vl[1], vl[2], vl[3]);
-            st4(st + 2 * kTileA + o, qh[0], qh[1], qh[2], qh[3]);
-            st4(st + 3 * kTileA + o, ql[0], ql[1], ql[2], ql[3]);
+            const uint32_t ta = tmem + (static_cast<uint32_t>(32 * (warp & 3)) << 16) + colA + s * 128 + 16 * ah;
+            tmem_st16(ta, vh);
+            tmem_st16(ta + 32, vl);
+            tmem_st16(ta + 64, qh);
+            tmem_st16(ta + 96, ql);
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
           }
+          fence_before();
           fence_async_smem();
           __syncwarp();
           if (lane == 0) mbar_arrive(&s_full[s]);
 #pragma unroll
-          for (int jj = 0; jj < 4; ++jj) xcur[jj] = xnext[jj];
+          for (int jj = 0; jj < 4; ++jj) {
+            xcur[jj] = xn1[jj];
+            xn1[jj] = xn2[jj];
+          }
         }
       }
     }
+    pf.lap(kPBuild);
+    if (a.prof && lane == 0)
+      for (int i = 0; i < 4; ++i) atomicAdd(a.prof + i, pf.acc[i]);
   } else if (warp == kMmaWarp) {
     // ================================================================ MMA issuer
     uint32_t sc = 0;
     int jb = 0;
+    Prof pf{};
+    pf.start();
     for (int item = blockIdx.x; item < total; item += gridDim.x) {
       const Job J = decode(a, item);
       for (int g0 = 0; g0 < J.ncomp; g0 += a.qg, ++jb) {
-        const int b = jb & 1;
+        const int b = a.nacc == 2 ? (jb & 1) : 0;
+        const int use_b = a.nacc == 2 ? (jb >> 1) : jb;
         const int nq = min(a.qg, J.ncomp - g0);
         const int N1 = kNL + ((nq * HP + 15) / 16) * 16;
         const uint32_t acc1 = tmem + b * a.TB, acc2 = acc1 + N1;
-        if (jb >= 2) mbar_wait(&s_tempty[b], ((jb >> 1) & 1) ^ 1);
+        if (use_b >= 1) mbar_wait(&s_tempty[b], (use_b - 1) & 1);
         fence_after();
+        pf.lap(kMWaitTE);
         for (int ch = 0; ch < nchunk; ++ch, ++sc) {
           const int s = a.nstage == 2 ? static_cast<int>(sc & 1u) : 0;
           const uint32_t use = a.nstage == 2 ? (sc >> 1) : sc;
           mbar_wait(&s_full[s], use & 1u);
           fence_after();
+          pf.lap(kMWaitFull);
           if (lane == 0) {
             const uint32_t st = sbase + s * a.stage_bytes;
             const uint32_t id1 = idesc(N1), id2 = idesc(kNL);
-            const uint32_t Av[3] = {st, st, st + kTileA};
-            const uint32_t Aq[3] = {st + 2 * kTileA, st + 2 * kTileA, st + 3 * kTileA};
+            const uint32_t tA = tmem + colA + s * 128;  // v hi | v lo | v^2 hi | v^2 lo
+            const uint32_t Av[3] = {tA, tA, tA + 32};
+            const uint32_t Aq[3] = {tA + 64, tA + 64, tA + 96};
             const uint32_t B1[3] = {st + offB1, st + offB1 + a.N1max * 128, st + offB1};
             const uint32_t B2[3] = {st + offB2, st + offB2 + kNL * 128, st + offB2};
 #pragma unroll
@@ -357,30 +418,36 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_ws(WsArgs a) {
 #pragma unroll
               for (int k = 0; k < kKC / 8; ++k) {
                 const uint32_t acc = (ch > 0 || p > 0 || k > 0) ? 1u : 0u;
-                const uint32_t ko = k * 32;
-                mma_tf32(acc1, sdesc(Av[p] + ko), sdesc(B1[p] + ko), id1, acc);
-                mma_tf32(acc2, sdesc(Aq[p] + ko), sdesc(B2[p] + ko), id2, acc);
+                mma_tf32_ts(acc1, Av[p] + k * 8, sdesc(B1[p] + k * 32), id1, acc);
+                mma_tf32_ts(acc2, Aq[p] + k * 8, sdesc(B2[p] + k * 32), id2, acc);
               }
             }
             commit(&s_empty[s]);
             if (ch == nchunk - 1) commit(&s_tfull[b]);
           }
           __syncwarp();
+          pf.lap(kMIssue);
         }
       }
     }
+    if (a.prof && lane == 0)
+      for (int i = kMWaitTE; i <= kMIssue; ++i) atomicAdd(a.prof + i, pf.acc[i]);
   } else if (warp >= kEpiWarp0) {
     // ================================================================ epilogue
     const int quad = warp & 3;
     const int r = quad * 32 + lane;
     int jb = 0;
+    Prof pf{};
+    pf.start();
     for (int item = blockIdx.x; item < total; item += gridDim.x) {
       const Job J = decode(a, item);
       for (int g0 = 0; g0 < J.ncomp; g0 += a.qg, ++jb) {
-        const int b = jb & 1;
-        mbar_wait(&s_mready[b], (jb >> 1) & 1);
-        mbar_wait(&s_tfull[b], (jb >> 1) & 1);
+        const int b = a.nacc == 2 ? (jb & 1) : 0;
+        const int use_b = a.nacc == 2 ? (jb >> 1) : jb;
+        mbar_wait(&s_mready[b], use_b & 1);
+        mbar_wait(&s_tfull[b], use_b & 1);
         fence_after();
+        pf.lap(kEWait);
         const Meta& M = s_meta[b];
         const int nq = M.nq;
         const int N1 = kNL + ((nq * HP + 15) / 16) * 16;
@@ -434,13 +501,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_ws(WsArgs a) {
         fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&s_tempty[b]);
+        pf.lap(kEWork);
       }
     }
+    if (a.prof && lane == 0)
+      for (int i = kEWait; i <= kEWork; ++i) atomicAdd(a.prof + i, pf.acc[i]);
   }
   fence_before();
   __syncthreads();
   fence_after();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * a.TB));
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(a.tmem_cols));
 }
 
 // Per-(anchor, slot) constants: b = W_q^T (mu_q - mu_a), m = sum psi_q^-1 (mu_q - mu_a)^2
@@ -582,6 +652,8 @@ cudaError_t launch_anchor_consts(const Dims& dm, const float* WT, const float* m
   return cudaGetLastError();
 }
 
+unsigned long long* g_ws_prof = nullptr;  // set by vmfa_diag_scorer_cycles
+
 cudaError_t launch_score_ws(int mode, const ScoreArgs& s, const float* WTS, const float* mu32,
                             const float* ipsi32, const float* acst, const float* lblk, const float* cblk,
                             cudaStream_t st) {
@@ -594,9 +666,13 @@ cudaError_t launch_score_ws(int mode, const ScoreArgs& s, const float* WTS, cons
   a.N1max = kNL + ((a.qg * a.Hp + 15) / 16) * 16;
   const int cols = a.N1max + kNL;
   a.TB = cols <= 32 ? 32 : cols <= 64 ? 64 : cols <= 128 ? 128 : 256;
-  a.stage_bytes = static_cast<uint32_t>(4 * kTileA + 2 * 128 * (a.N1max + kNL));
+  a.nacc = (2 * a.TB + 2 * 128 <= 512) ? 2 : 1;  // A stages use 2 x 128 TMEM columns
+  const uint32_t need = a.nacc * a.TB + 2 * 128;
+  a.tmem_cols = need <= 256 ? 256 : 512;
+  a.stage_bytes = static_cast<uint32_t>(2 * 128 * (a.N1max + kNL));
   const size_t static_smem = 8 * 1024;
-  a.nstage = (2 * a.stage_bytes + 1024 + static_smem <= 227 * 1024) ? 2 : 1;
+  a.nstage = 2;  // A stages live in TMEM; smem holds the B stages only
+  (void)static_smem;
   const size_t dyn = static_cast<size_t>(a.nstage) * a.stage_bytes + 1024;
   a.X = s.X;
   a.WTS = WTS;
@@ -613,6 +689,7 @@ cudaError_t launch_score_ws(int mode, const ScoreArgs& s, const float* WTS, cons
   a.g = s.g;
   a.gcnt = s.gcnt;
   a.out = s.out;
+  a.prof = g_ws_prof;
   auto go = [&](auto kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn));
     kern<<<sm_count(), kThreads, dyn, st>>>(a);
@@ -627,3 +704,22 @@ cudaError_t launch_score_ws(int mode, const ScoreArgs& s, const float* WTS, cons
 }
 
 }  // namespace vmfa_b200
+
+// Diagnostics: per-role cycle counters of the warp-specialised scorer.
+extern "C" int vmfa_diag_scorer_cycles(int enable, unsigned long long* out, int n) {
+  using namespace vmfa_b200;
+  if (enable && !g_ws_prof) {
+    if (cudaMalloc(&g_ws_prof, sizeof(unsigned long long) * 16) != cudaSuccess) return VMFA_ERR_CUDA;
+    cudaMemset(g_ws_prof, 0, sizeof(unsigned long long) * 16);
+  }
+  if (out && g_ws_prof) {
+    cudaDeviceSynchronize();
+    cudaMemcpy(out, g_ws_prof, sizeof(unsigned long long) * (n < 16 ? n : 16), cudaMemcpyDeviceToHost);
+    cudaMemset(g_ws_prof, 0, sizeof(unsigned long long) * 16);
+  }
+  if (!enable && g_ws_prof) {
+    cudaFree(g_ws_prof);
+    g_ws_prof = nullptr;
+  }
+  return VMFA_OK;
+}

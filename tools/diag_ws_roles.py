@@ -1,0 +1,36 @@
+"""Per-role cycle breakdown of the warp-specialised scorer on BASELINE config 2
+(diagnostics; uses vmfa_diag_scorer_cycles)."""
+import ctypes as C
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.join(os.path.dirname(__file__), ".."))
+from paper_2501_12299_b200 import vmfa as V  # noqa: E402
+from paper_2501_12299_b200.abi import lib  # noqa: E402
+
+X = V.gen_synthetic(V.synth_spec(2))
+m = V.CONFIGS[2]["model"]
+p, st, floor, _ = V.initialize(X, m["C"], m["H"], m["Cprime"], m["G"], seed=0)
+s = V.Session(m["C"], X.shape[1], m["H"], m["Cprime"], m["G"], X)
+s.set_floor(floor)
+s.upload_params(p)
+s.upload_state(st)
+for it in range(4):
+    s.iterate(0, it)
+names = ["P wait acc", "P job sync", "P wait stage", "P build", "M wait acc", "M wait full", "M issue",
+         "E wait", "E work"]
+lib().vmfa_diag_scorer_cycles(1, None, 0)
+out = np.zeros(16, np.uint64)
+s.profile(True)
+s.variational_e_step(0, 10)
+kt = s.kernel_times()
+lib().vmfa_diag_scorer_cycles(1, out.ctypes.data_as(C.c_void_p), 16)
+lib().vmfa_diag_scorer_cycles(0, None, 0)
+print({k: round(v["ms"], 3) for k, v in kt.items() if v["ms"] > 0})
+tot_p = out[0:4].sum()
+print("cycles per CTA-role (summed over CTAs; producer counters summed over 8 warps):")
+for i, nme in enumerate(names):
+    share = out[i] / (tot_p if i < 4 else (out[4:7].sum() if i < 7 else out[7:9].sum()))
+    print(f"  {nme:14s} {int(out[i]):>16d}  share-in-role {share:6.3f}")
