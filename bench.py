@@ -60,53 +60,80 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clocks and throttle reasons sampled by NVML every 5 ms during the
+    timed region (nvidia-smi's loop mode is too coarse for a ~100 ms region);
+    falls back to one nvidia-smi sample per boundary when NVML is missing."""
 
-    def __init__(self, index: int):
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"),
+               ("hw_power_brake", "nvmlClocksEventReasonHwPowerBrakeSlowdown"))
+
+    def __init__(self, index: int, period_s: float = 0.005):
         self.index = index
-        self.rows = []
-        self.proc = None
+        self.period = period_s
+        self.sm, self.mx, self.reasons = [], [], set()
+        self.stop = threading.Event()
+        self.t = None
+
+    def _sample_nvml(self, nv, h):
+        self.sm.append(float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)))
+        self.mx.append(float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)))
+        r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+        for name, const in self.REASONS:
+            if r & getattr(nv, const, 0):
+                self.reasons.add(name)
+
+    def _run(self):
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self.index)
+        except Exception:
+            return self._smi()
+        while True:
+            try:
+                self._sample_nvml(nv, h)
+            except Exception:
+                break
+            if self.stop.wait(self.period):
+                break
+
+    def _smi(self):
+        q = "clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown," \
+            "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown," \
+            "clocks_event_reasons.sw_power_cap"
+        while True:
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=10).stdout
+                r = [x.strip() for x in out.split(",")]
+                self.sm.append(float(r[0]))
+                self.mx.append(float(r[1]))
+                for (name, _), v in zip(self.REASONS, r[2:6]):
+                    if v.lower() == "active":
+                        self.reasons.add(name)
+            except Exception:
+                return
+            if self.stop.wait(0.05):
+                return
 
     def __enter__(self):
-        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
-        try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
-        except Exception:
-            self.proc = None
+        self.t = threading.Thread(target=self._run, daemon=True)
+        self.t.start()
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
-
     def __exit__(self, *exc):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except Exception:
-                self.proc.kill()
+        self.stop.set()
+        if self.t:
+            self.t.join(timeout=15)
 
     def summary(self):
-        sm = [float(r[0]) for r in self.rows if len(r) >= 8 and r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if len(r) >= 8 and r[1].replace(".", "").isdigit()]
-        reasons = set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for r in self.rows:
-            if len(r) < 8:
-                continue
-            for name, v in zip(names, r[4:8]):
-                if v.lower() == "active":
-                    reasons.add(name)
-        return {"sm_mhz": float(np.median(sm)) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        return {"sm_mhz": float(np.median(self.sm)) if self.sm else None,
+                "sm_max_mhz": max(self.mx) if self.mx else None, "reasons": sorted(self.reasons),
+                "samples": len(self.sm)}
 
 
 def build_problem(cfg: int, rank: int, world: int, n_override: int = 0):
@@ -336,6 +363,12 @@ def main():
         except Exception as ex:  # the baseline is reported, never required
             cpu = {"error": str(ex)}
 
+    traffic = {}
+    try:
+        with open(os.path.join(ROOT, "profiles", "scorer_traffic.json")) as f:
+            traffic = json.load(f) if args.config == 2 else {}
+    except Exception:
+        pass
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "joint evals/s", "n_gpus": world,
@@ -353,7 +386,8 @@ def main():
             "roofline": {"bound": "hbm", "kernel": "candidate scoring (score_anchor+score_extra)",
                          "achieved": ach_gbs, "peak": pk["hbm"], "unit": "GB/s",
                          "frac": (ach_gbs / pk["hbm"]) if ach_gbs else None,
-                         "traffic": None, "peak_src": pk["src"],
+                         "traffic": traffic.get("bytes_per_launch_pair"),
+                         "traffic_src": traffic.get("source"), "peak_src": pk["src"],
                          "per_unit": f"B_j = 4D+8 = {Bj} B per joint (SURVEY §8(d)), J={J_local:.0f} joints per launch pair",
                          "flops_view": {"achieved_tflops": ach_tfs, "F_j": Fj}},
             "gpu_launches": int(n_launch * args.steps),

@@ -734,7 +734,7 @@ __global__ void __launch_bounds__(kStatsThreads, 2) k_stats(StatsArgs a, const i
     qmax = 0.0;
 #pragma unroll
     for (int w = 0; w < kStatsThreads / 32; ++w) qmax = fmax(qmax, s_red[w]);
-    const double qinv = qmax > 0.0 ? 1.0 / qmax : 0.0;
+    const double qdiv = qmax > 0.0 ? qmax : 1.0;  // divide (1/qmax overflows for denormal qmax)
     float accY[ND][4][NH1];
     float accS[ND][4];
 #pragma unroll
@@ -751,7 +751,7 @@ __global__ void __launch_bounds__(kStatsThreads, 2) k_stats(StatsArgs a, const i
         const int i = r0 + b * kStatsBatch + tid;
         const int e = i < r1 ? a.ent[i] : -1;
         s_e[buf][tid] = e;
-        s_qb[buf][tid] = e >= 0 ? a.resp[e] * qinv : 0.0;
+        s_qb[buf][tid] = e >= 0 ? a.resp[e] / qdiv : 0.0;
       }
     };
     auto issue_rows = [&](int buf) {
@@ -1166,7 +1166,9 @@ __global__ void __launch_bounds__(128) k_update(UpdateArgs a) {
       if (tid == 0) a.pi[c] = 0.0;
       continue;
     }
-    for (int i = tid; i < H1 * H1; i += blockDim.x) sE[i] = a.E[(int64_t)c * H1 * H1 + i];
+    // A^T = E^-1 Y^T is invariant under a common scale of E and Y: solve the
+    // system normalised by N_c so denormal-scale components keep usable pivots
+    for (int i = tid; i < H1 * H1; i += blockDim.x) sE[i] = a.E[(int64_t)c * H1 * H1 + i] / nc;
     __syncthreads();
     bool solved = false;
     for (int attempt = 0; attempt < 2 && !solved; ++attempt) {
@@ -1186,7 +1188,7 @@ __global__ void __launch_bounds__(128) k_update(UpdateArgs a) {
       // solve per d and write (provisionally) — all finite required
       for (int d = tid; d < D; d += blockDim.x) {
         double b[kMaxH1];
-        for (int h = 0; h < H1; ++h) b[h] = a.Y[((int64_t)c * H1 + h) * D + d];
+        for (int h = 0; h < H1; ++h) b[h] = a.Y[((int64_t)c * H1 + h) * D + d] / nc;
         chol_solve_thread(sR, b, H1);
         bool fin = true;
         for (int h = 0; h < H1; ++h) fin &= isfinite(b[h]);
