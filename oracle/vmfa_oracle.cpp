@@ -195,6 +195,67 @@ inline void chol_solve(const double* R, double* b, int n) {
   }
 }
 
+// LDL^T with diagonal pivoting as Eigen::LDLT<MatrixXd> (Lower) computes it --
+// the factorisation update_params uses (mstep.cpp:129-130). Eigen is a
+// third-party dependency (CMakeLists.txt:12, Eigen3 >= 3.3, not vendored);
+// restated from its published ldlt_inplace<Lower>::unblocked / _solve_impl:
+// left-looking, step k pivots on the largest |diagonal| of rows k.. (the
+// trailing diagonal is the permuted original one), info fails only when a zero
+// pivot is followed by a non-zero one or a zero pivot has a non-zero column;
+// an all-zero diagonal gives D = 0. A (n x n, column-major, symmetric) is
+// overwritten by L (strictly lower) and D (diagonal).
+inline bool ldlt(double* A, int* perm, int n) {
+  auto M = [&](int r, int c) -> double& { return A[c * n + r]; };
+  std::vector<double> temp(n);
+  bool ret = true, found_zero = false;
+  for (int k = 0; k < n; ++k) {
+    int p = k;
+    double best = std::fabs(M(k, k));
+    for (int j = k + 1; j < n; ++j)
+      if (std::fabs(M(j, j)) > best) best = std::fabs(M(j, j)), p = j;
+    perm[k] = p;
+    if (p != k) {
+      for (int c = 0; c < n; ++c) std::swap(M(k, c), M(p, c));
+      for (int r = 0; r < n; ++r) std::swap(M(r, k), M(r, p));
+    }
+    for (int j = 0; j < k; ++j) temp[j] = M(j, j) * M(k, j);
+    double s = 0.0;
+    for (int j = 0; j < k; ++j) s += M(k, j) * temp[j];
+    const double akk = M(k, k) - s;
+    const bool valid = std::fabs(akk) > 0.0;
+    if (k == 0 && !valid) {
+      for (int j = 0; j < n; ++j) perm[j] = j;
+      break;
+    }
+    bool col_zero = true;
+    for (int i = k + 1; i < n; ++i) {
+      double t = M(i, k);
+      for (int j = 0; j < k; ++j) t -= M(i, j) * temp[j];
+      if (valid) t /= akk;
+      else col_zero = col_zero && t == 0.0;
+      M(i, k) = t;
+    }
+    M(k, k) = akk;
+    if (!valid && k + 1 < n) ret = ret && col_zero;
+    if (found_zero && valid) ret = false;
+    else if (!valid) found_zero = true;
+  }
+  return ret;
+}
+// x = P^T L^-T D^+ L^-1 P b, D^+_i = 1/d_i if |d_i| > DBL_MIN else 0.
+inline void ldlt_solve(const double* A, const int* perm, double* b, int n) {
+  for (int k = 0; k < n; ++k) std::swap(b[k], b[perm[k]]);
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < i; ++j) b[i] -= A[j * n + i] * b[j];
+  for (int i = 0; i < n; ++i) {
+    const double d = A[i * n + i];
+    b[i] = std::fabs(d) > std::numeric_limits<double>::min() ? b[i] / d : 0.0;
+  }
+  for (int i = n - 1; i >= 0; --i)
+    for (int j = i + 1; j < n; ++j) b[i] -= A[i * n + j] * b[j];
+  for (int k = n - 1; k >= 0; --k) std::swap(b[k], b[perm[k]]);
+}
+
 // ---------------------------------------------------------------- model
 struct Caches {
   int C, D, H;
@@ -644,9 +705,9 @@ int orc_suffstats(i64 N, int D, int H, int C, int Cp, const float* X, const doub
 }
 
 // ---- update_params, mstep.cpp:103-162 -----------------------------------------------
-// The reference factorises E_c by Eigen LDLT; E_c is SPD whenever N_c > 0
-// (SURVEY App. E.2), so a Cholesky solve is the same linear solve. The jitter
-// rule (1e-10 tr/(H+1) once, else SingularEc) is reproduced.
+// E_c A^T = Y_c^T by the LDLT restatement above (mstep.cpp:129-130); the
+// jitter rule (1e-10 tr/(H+1) once on info != Success or a non-finite
+// solution, else SingularEc, :131-140) is reproduced.
 int orc_update_params(int C, int D, int H, i64 N, const double* Nc, const double* Y,
                       const double* E, const double* sq, const double* floor,
                       const double* pi_prev, const double* mu_prev, const double* lam_prev,
@@ -656,6 +717,7 @@ int orc_update_params(int C, int D, int H, i64 N, const double* Nc, const double
   (void)pi_prev;
   const int H1 = H + 1;
   std::vector<double> Ec(H1 * H1), R(H1 * H1), At((size_t)H1 * D), b(H1);
+  std::vector<int> perm(H1);
   for (int c = 0; c < C; ++c) {
     const double nc = Nc[c];
     if (nc == 0.0) {  // :119-126 freeze
@@ -669,10 +731,11 @@ int orc_update_params(int C, int D, int H, i64 N, const double* Nc, const double
     std::copy(E + (size_t)c * H1 * H1, E + (size_t)(c + 1) * H1 * H1, Ec.begin());
     const double* Yc = Y + (size_t)c * D * H1;
     auto solve_all = [&]() -> bool {
-      if (!chol(Ec.data(), R.data(), H1)) return false;
+      R = Ec;
+      if (!ldlt(R.data(), perm.data(), H1)) return false;
       for (int d = 0; d < D; ++d) {
         for (int h = 0; h < H1; ++h) b[h] = Yc[h * D + d];
-        chol_solve(R.data(), b.data(), H1);
+        ldlt_solve(R.data(), perm.data(), b.data(), H1);
         for (int h = 0; h < H1; ++h) {
           if (!std::isfinite(b[h])) return false;
           At[(size_t)d * H1 + h] = b[h];  // At (H+1) x D stored per d

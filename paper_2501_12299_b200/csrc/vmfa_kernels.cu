@@ -671,8 +671,10 @@ constexpr int kStatsMaxH1 = 17;   // columns of Y per pass
 // Per batch of 32 rows (cp.async double-buffered into smem):
 //   (i)  mz = V (x - mu) (mstep.cpp:52-53): lane = row, warp = 1/8 of the
 //        dimensions, V rows broadcast from smem; warp partials summed in smem.
-//   (ii) Y += q x zhat^T, sq += q x^2 (fp64): each thread owns a 4-dim x NH1
-//        register tile over a row group; E += q zhat zhat^T, N += q.
+//   (ii) Y_v += q v zhat^T, sq_v += q v^2 (v = x - mu, fp32 register tiles of
+//        4 dims x NH1 columns per thread over a row group, scaled by the
+//        item's largest q); E += q [zhat;1][zhat;1]^T in fp64, one thread per
+//        upper-triangle entry (N = E(H,H)).
 // Sole-item components write their statistics directly; split components
 // write fp64 partials summed by k_stats_reduce in item order (deterministic).
 // Partial layout per item (pass col0): [Y cols col0.. (NH1 x D) | sq (D) |
@@ -690,6 +692,7 @@ __global__ void __launch_bounds__(kStatsThreads, 2) k_stats(StatsArgs a, const i
   __shared__ double s_qb[2][kStatsBatch];
   __shared__ int s_e[2][kStatsBatch];
   __shared__ double s_red[kStatsThreads / 32];
+  __shared__ double s_accE[kStatsThreads];  // E entry of thread tid (fp64)
   const Dims dm = a.dm;
   const int H = dm.H, H1 = H + 1, D = dm.D;
   const int XS = (D + 3) / 4 * 4 + kXPad;
@@ -701,11 +704,21 @@ __global__ void __launch_bounds__(kStatsThreads, 2) k_stats(StatsArgs a, const i
   const bool first = col0 == 0;
   const bool full_e = first && (H1 <= NH1);
   const bool vec = (D & 3) == 0;
-  // register tiles over "dimensions" [0, D) of the centred row and, when E is
-  // produced here, [Dp, Dp + H1) of zhat itself (E = sum q zhat zhat^T)
+  // register tiles over the "dimensions" [0, D) of the centred row; E = sum q
+  // [zhat;1][zhat;1]^T is accumulated separately in fp64 (one thread per
+  // upper-triangle entry): its conditioning follows N_c Sigma_z, which fp32
+  // sums cannot resolve for collapsed components
   const int Dp = (D + 3) / 4 * 4;
   const int GX = Dp / 4;
-  const int GD = GX + (full_e ? (H1 + 3) / 4 : 0);
+  const int GD = GX;
+  int ei = -1, ej = -1;  // this thread's E entry (i <= j)
+  if (full_e) {
+    int t = tid;
+    for (int i = 0; i < H1 && ei < 0; ++i) {
+      if (t < H1 - i) ei = i, ej = i + t;
+      else t -= H1 - i;
+    }
+  }
   const int RG = max(1, kStatsThreads / GD);
   const int my_dg = tid % GD, my_rg = tid / GD;
   const bool tile_on = my_rg < RG && tid < RG * GD;
@@ -737,6 +750,7 @@ __global__ void __launch_bounds__(kStatsThreads, 2) k_stats(StatsArgs a, const i
     const double qdiv = qmax > 0.0 ? qmax : 1.0;  // divide (1/qmax overflows for denormal qmax)
     float accY[ND][4][NH1];
     float accS[ND][4];
+    if (ei >= 0) s_accE[tid] = 0.0;
 #pragma unroll
     for (int k = 0; k < ND; ++k)
 #pragma unroll
@@ -845,6 +859,13 @@ __global__ void __launch_bounds__(kStatsThreads, 2) k_stats(StatsArgs a, const i
         s_zf[i] = z;
       }
       __syncthreads();
+      if (ei >= 0) {  // E(ei, ej) += q z_i z_j: fp32 z products are exact in fp64
+        const double* s_q = s_qb[buf];
+        double acc = s_accE[tid];
+        for (int r = 0; r < nb; ++r)
+          acc = fma(s_q[r], static_cast<double>(s_zf[r * ZS + ei]) * static_cast<double>(s_zf[r * ZS + ej]), acc);
+        s_accE[tid] = acc;
+      }
       // (ii) register tiles: 4 "dimensions" x NH1 columns, rows my_rg::RG
       if (tile_on) {
         const double* s_q = s_qb[buf];
@@ -860,20 +881,14 @@ __global__ void __launch_bounds__(kStatsThreads, 2) k_stats(StatsArgs a, const i
             const int g = my_dg + k * GD;
             if (k > 0 && g >= GD) break;
             float vs[4];
-            if (g < GX) {
-              const int d = 4 * g;
-              if (vec || d + 3 < D) {
-                const float4 xv = *reinterpret_cast<const float4*>(xr + d);
-                const float4 mv = *reinterpret_cast<const float4*>(s_mu + d);
-                vs[0] = xv.x - mv.x, vs[1] = xv.y - mv.y, vs[2] = xv.z - mv.z, vs[3] = xv.w - mv.w;
-              } else {
-#pragma unroll
-                for (int i = 0; i < 4; ++i) vs[i] = d + i < D ? xr[d + i] - s_mu[d + i] : 0.f;
-              }
+            const int d = 4 * g;
+            if (vec || d + 3 < D) {
+              const float4 xv = *reinterpret_cast<const float4*>(xr + d);
+              const float4 mv = *reinterpret_cast<const float4*>(s_mu + d);
+              vs[0] = xv.x - mv.x, vs[1] = xv.y - mv.y, vs[2] = xv.z - mv.z, vs[3] = xv.w - mv.w;
             } else {
-              const int z0 = 4 * (g - GX);
 #pragma unroll
-              for (int i = 0; i < 4; ++i) vs[i] = z0 + i < ZS ? zr[z0 + i] : 0.f;
+              for (int i = 0; i < 4; ++i) vs[i] = d + i < D ? xr[d + i] - s_mu[d + i] : 0.f;
             }
             float qv[4];
 #pragma unroll
@@ -896,6 +911,10 @@ __global__ void __launch_bounds__(kStatsThreads, 2) k_stats(StatsArgs a, const i
     double* red = reinterpret_cast<double*>(s_x);  // >= RG * GD * 4 * (NH1 + 1) doubles
     double* pp = direct ? nullptr : part + (int64_t)item * part_stride;
     double* pe = direct ? a.E + (int64_t)c * H1 * H1 : pp + (int64_t)NH1 * D + D;
+    if (ei >= 0) {
+      pe[ej * H1 + ei] = s_accE[tid] * qmax;
+      pe[ei * H1 + ej] = s_accE[tid] * qmax;
+    }
 #pragma unroll
     for (int k = 0; k < ND; ++k) {
       __syncthreads();
@@ -930,25 +949,17 @@ __global__ void __launch_bounds__(kStatsThreads, 2) k_stats(StatsArgs a, const i
         if (k == 0 || g < GD) {
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
-            if (g < GX) {
-              const int d = 4 * g + i;
-              if (d >= D) continue;
-              if (direct) {
-#pragma unroll
-                for (int h = 0; h < NH1; ++h)
-                  if (col0 + h < H1) a.Y[((int64_t)c * H1 + col0 + h) * D + d] = ty[i][h] * qmax;
-                if (first) a.sq[(int64_t)c * D + d] = ts[i] * qmax;
-              } else {
-#pragma unroll
-                for (int h = 0; h < NH1; ++h) pp[(int64_t)h * D + d] = ty[i][h] * qmax;
-                if (first) pp[(int64_t)NH1 * D + d] = ts[i] * qmax;
-              }
-            } else {
-              const int zi = 4 * (g - GX) + i;  // E row
-              if (zi >= H1) continue;
+            const int d = 4 * g + i;
+            if (d >= D) continue;
+            if (direct) {
 #pragma unroll
               for (int h = 0; h < NH1; ++h)
-                if (h < H1) pe[h * H1 + zi] = ty[i][h] * qmax;  // E(zi, h), col-major
+                if (col0 + h < H1) a.Y[((int64_t)c * H1 + col0 + h) * D + d] = ty[i][h] * qmax;
+              if (first) a.sq[(int64_t)c * D + d] = ts[i] * qmax;
+            } else {
+#pragma unroll
+              for (int h = 0; h < NH1; ++h) pp[(int64_t)h * D + d] = ty[i][h] * qmax;
+              if (first) pp[(int64_t)NH1 * D + d] = ts[i] * qmax;
             }
           }
         }
@@ -1144,16 +1155,130 @@ __device__ __forceinline__ void set_status(unsigned long long* st, int c, int co
 constexpr int kMaxH1 = 65;
 
 // ---------------------------------------------------------------- K7: update_params
+// The reference solves E_c A^T = Y_c^T with Eigen's LDLT (mstep.cpp:129-130):
+// a left-looking LDL^T with diagonal pivoting. Restated semantics (Eigen >= 3.3,
+// LDLT.h, ldlt_inplace<Lower>::unblocked and LDLT::_solve_impl):
+//   * step k pivots on the largest |diagonal| among rows k.. (first index on a
+//     tie) -- the trailing diagonal is the permuted ORIGINAL one, the Schur
+//     update of entry (k,k) happens only at step k;
+//   * d_k = A_kk - sum_j L_kj d_j L_kj; L_ik = (A_ik - sum_j L_ij d_j L_kj)/d_k
+//     when d_k != 0, else the column must already be zero;
+//   * the factorisation fails (info != Success) when a zero pivot is followed
+//     by a non-zero one, or a zero pivot has a non-zero column; a matrix with
+//     an all-zero diagonal "succeeds" with D = 0;
+//   * solve: x = P^T L^-T D^+ L^-1 P b with D^+_i = 1/d_i if |d_i| > DBL_MIN
+//     else 0 (pseudo-inverse of D).
+// A: n x n column-major, full symmetric on entry; overwritten by L (strictly
+// lower) and D (diagonal). perm: transpositions. Warp-cooperative.
+__device__ void warp_ldlt(double* A, double* temp, int* perm, int n, int* ok) {
+  const int lane = threadIdx.x & 31;
+  auto M = [&](int r, int c) -> double& { return A[c * n + r]; };
+  bool ret = true, found_zero = false;
+  for (int k = 0; k < n; ++k) {
+    // (1) largest |diagonal| among k.. (first index on a tie)
+    double best = -1.0;
+    int bi = n;
+    for (int j = k + lane; j < n; j += 32) {
+      const double v = fabs(M(j, j));
+      if (v > best) best = v, bi = j;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(kFull, best, o);
+      const int oi = __shfl_xor_sync(kFull, bi, o);
+      if (ov > best || (ov == best && oi < bi)) best = ov, bi = oi;
+    }
+    const int p = bi < n ? bi : k;
+    if (lane == 0) perm[k] = p;
+    if (p != k) {  // symmetric transposition of rows / columns k and p
+      for (int c = lane; c < n; c += 32) {
+        const double t = M(k, c);
+        M(k, c) = M(p, c);
+        M(p, c) = t;
+      }
+      __syncwarp();
+      for (int r = lane; r < n; r += 32) {
+        const double t = M(r, k);
+        M(r, k) = M(r, p);
+        M(r, p) = t;
+      }
+      __syncwarp();
+    }
+    // (2) left-looking update of column k
+    for (int j = lane; j < k; j += 32) temp[j] = M(j, j) * M(k, j);
+    __syncwarp();
+    double s = 0.0;
+    for (int j = lane; j < k; j += 32) s += M(k, j) * temp[j];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
+    const double akk = M(k, k) - s;
+    const bool valid = fabs(akk) > 0.0;
+    if (k == 0 && !valid) {  // all-zero diagonal: D = 0, identity transpositions
+      for (int j = lane; j < n; j += 32) perm[j] = j;
+      __syncwarp();
+      break;
+    }
+    int col_zero = 1;
+    for (int i = k + 1 + lane; i < n; i += 32) {
+      double t = M(i, k);
+      for (int j = 0; j < k; ++j) t -= M(i, j) * temp[j];
+      if (valid) t /= akk;
+      else col_zero &= (t == 0.0);
+      M(i, k) = t;
+    }
+    col_zero = __all_sync(kFull, col_zero);
+    __syncwarp();
+    if (lane == 0) M(k, k) = akk;
+    if (!valid && k + 1 < n) ret = ret && col_zero;
+    if (found_zero && valid) ret = false;
+    else if (!valid) found_zero = true;
+    __syncwarp();
+  }
+  if (lane == 0) *ok = ret ? 1 : 0;
+}
+// x = P^T L^-T D^+ L^-1 P b for one right-hand side held by one thread.
+__device__ __forceinline__ void ldlt_solve_thread(const double* A, const int* perm, double* b, int n) {
+  for (int k = 0; k < n; ++k) {
+    const int p = perm[k];
+    const double t = b[k];
+    b[k] = b[p];
+    b[p] = t;
+  }
+  for (int i = 0; i < n; ++i) {
+    double s = b[i];
+    for (int j = 0; j < i; ++j) s -= A[j * n + i] * b[j];
+    b[i] = s;
+  }
+  for (int i = 0; i < n; ++i) {
+    const double d = A[i * n + i];
+    b[i] = fabs(d) > DBL_MIN ? b[i] / d : 0.0;
+  }
+  for (int i = n - 1; i >= 0; --i) {
+    double s = b[i];
+    for (int j = i + 1; j < n; ++j) s -= A[i * n + j] * b[j];
+    b[i] = s;
+  }
+  for (int k = n - 1; k >= 0; --k) {
+    const int p = perm[k];
+    const double t = b[k];
+    b[k] = b[p];
+    b[p] = t;
+  }
+}
+
 // CTA per component (mstep.cpp:117-153): freeze on N_c == 0 exactly; else
-// pi = N_c/N, A^T = E^-1 Y^T (Cholesky; one trace-scaled jitter retry, else
-// SingularEc), Lambda / mu from A, sigma^2 = max(floor, (sq - sum_h Y.A)/N_c).
+// pi = N_c/N, A^T = E^-1 Y^T by LDLT (one trace-scaled jitter retry on
+// failure or a non-finite solution, else SingularEc), Lambda / mu from A,
+// sigma^2 = max(floor, (sq - sum_h Y.A)/N_c).
 __global__ void __launch_bounds__(128) k_update(UpdateArgs a) {
   extern __shared__ __align__(16) double s_upd[];
   __shared__ int s_ok, s_fin;
+  __shared__ int s_perm[kMaxH1];
+  __shared__ double s_tmp[kMaxH1];
   const Dims dm = a.dm;
   const int H = dm.H, H1 = H + 1, D = dm.D;
-  double* sE = s_upd;
-  double* sR = s_upd + H1 * H1;
+  double* sE = s_upd;              // E_c (+ jitter)
+  double* sF = s_upd + H1 * H1;    // LDLT factors
   const int tid = threadIdx.x;
   for (int c = blockIdx.x; c < dm.C; c += gridDim.x) {
     const double nc = a.Nc[c];
@@ -1166,13 +1291,11 @@ __global__ void __launch_bounds__(128) k_update(UpdateArgs a) {
       if (tid == 0) a.pi[c] = 0.0;
       continue;
     }
-    // A^T = E^-1 Y^T is invariant under a common scale of E and Y: solve the
-    // system normalised by N_c so denormal-scale components keep usable pivots
-    for (int i = tid; i < H1 * H1; i += blockDim.x) sE[i] = a.E[(int64_t)c * H1 * H1 + i] / nc;
+    for (int i = tid; i < H1 * H1; i += blockDim.x) sE[i] = a.E[(int64_t)c * H1 * H1 + i];
     __syncthreads();
     bool solved = false;
     for (int attempt = 0; attempt < 2 && !solved; ++attempt) {
-      if (attempt == 1) {  // mstep.cpp:133-135
+      if (attempt == 1) {  // mstep.cpp:133-135: E_c += 1e-10 tr(E_c)/(H+1) I
         if (tid == 0) {
           double tr = 0.0;
           for (int i = 0; i < H1; ++i) tr += sE[i * H1 + i];
@@ -1181,15 +1304,17 @@ __global__ void __launch_bounds__(128) k_update(UpdateArgs a) {
         }
         __syncthreads();
       }
-      if (tid < 32) warp_cholesky(sE, sR, H1, &s_ok);
+      for (int i = tid; i < H1 * H1; i += blockDim.x) sF[i] = sE[i];
+      __syncthreads();
+      if (tid < 32) warp_ldlt(sF, s_tmp, s_perm, H1, &s_ok);
       if (tid == 0) s_fin = 1;
       __syncthreads();
       if (!s_ok) continue;
-      // solve per d and write (provisionally) — all finite required
+      // solve per d and write (provisionally) -- all finite required
       for (int d = tid; d < D; d += blockDim.x) {
         double b[kMaxH1];
-        for (int h = 0; h < H1; ++h) b[h] = a.Y[((int64_t)c * H1 + h) * D + d] / nc;
-        chol_solve_thread(sR, b, H1);
+        for (int h = 0; h < H1; ++h) b[h] = a.Y[((int64_t)c * H1 + h) * D + d];
+        ldlt_solve_thread(sF, s_perm, b, H1);
         bool fin = true;
         for (int h = 0; h < H1; ++h) fin &= isfinite(b[h]);
         if (!fin) s_fin = 0;
@@ -1542,7 +1667,7 @@ static void stats_pass(const StatsArgs& a, const int* itemoff, int rpi, int grid
                         kStatsBatch * VS + 8) * sizeof(float);
   const size_t per_buf = static_cast<size_t>(kStatsBatch) * XS * sizeof(float);
   // the row-group reduction reuses the row buffers: RG-1 slices of GD*4*(NH1+1) doubles
-  const int GD = (D + 3) / 4 + (NH1 >= a.dm.H + 1 ? (a.dm.H + 1 + 3) / 4 : 0);
+  const int GD = (D + 3) / 4;
   const int RG = std::max(1, kStatsThreads / GD);
   const size_t red = static_cast<size_t>(std::max(RG - 1, 0)) * GD * 4 * (NH1 + 1) * sizeof(double);
   int nbuf = (2 * per_buf + fixed <= 200 * 1024) ? 2 : 1;

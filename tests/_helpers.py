@@ -115,3 +115,34 @@ def compare_g(g_gpu, gc_gpu, g_or, gc_or, dist_or, labels_same_comp, rtol=1e-6):
             continue  # near-tie at the selection boundary
         bad.append(c)
     return bad
+
+
+def ldlt_cases(O):
+    """Statistics exercising update_params' LDLT semantics (mstep.cpp:129-140,
+    Eigen LDLT): c0 SPD; c1 PSD-singular diag(2,0,3) (zero pivot last -> the
+    pseudo-inverse of D zeroes that coordinate); c2 a zero pivot followed by
+    a non-zero one (info != Success -> trace-scaled jitter retry); c3 an
+    indefinite E (LDLT succeeds where a Cholesky would fail). C=4, D=5, H=2.
+    Returns (stats, prev params, floor, expected A^T per component)."""
+    rng = np.random.default_rng(11)
+    C_, D, H = 4, 5, 2
+    H1 = H + 1
+    E = np.zeros((C_, H1, H1))
+    B = rng.normal(size=(H1, H1))
+    E[0] = B @ B.T + 0.5 * np.eye(H1)
+    E[1] = np.diag([2.0, 0.0, 3.0])
+    E[2] = np.array([[1.0, 1.0, 0.0], [1.0, 1.0, 0.0], [0.0, 0.0, 0.5]])
+    E[3] = np.array([[1.0, 2.0, 0.1], [2.0, 1.0, 0.2], [0.1, 0.2, 4.0]])
+    Y = rng.normal(size=(C_, H1, D))
+    Nc = E[:, H, H].copy()
+    sq = np.full((C_, D), 50.0)
+    want = np.zeros((C_, H1, D))
+    want[0] = np.linalg.solve(E[0], Y[0])
+    want[1] = np.stack([Y[1, 0] / 2.0, np.zeros(D), Y[1, 2] / 3.0])
+    E2 = E[2] + 1e-10 * np.trace(E[2]) / H1 * np.eye(H1)
+    want[2] = np.linalg.solve(E2, Y[2])
+    want[3] = np.linalg.solve(E[3], Y[3])
+    s = O.Stats(Nc, Y, E, sq)
+    prev = O.Params(np.full(C_, 1.0 / C_), rng.normal(size=(C_, D)), rng.normal(size=(C_, H, D)),
+                    np.ones((C_, D)))
+    return s, prev, np.full(D, 1e-6), want

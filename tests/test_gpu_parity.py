@@ -159,6 +159,33 @@ def test_update_freezes_empty_component(oracle, gpu):
     sess.close()
 
 
+def test_update_ldlt_semantics_match_oracle(oracle, gpu):
+    # singular / indefinite / jitter-path E_c (mstep.cpp:129-140): the device
+    # LDLT restatement and the oracle's agree; an overflowing solve -> SingularEc
+    from _helpers import ldlt_cases
+    O, V = oracle, gpu
+    s, prev, floor, want = ldlt_cases(O)
+    X = np.random.default_rng(2).normal(size=(10, 5)).astype(np.float32)
+    sess = V.Session(4, 5, 2, 2, 2, X)
+    sess.set_floor(floor)
+    sess.upload_params(to_vmfa_params(V, prev))
+    sess.upload_suffstats(s)
+    sess.update_params()
+    p_g = sess.download_params()
+    p_or = O.update_params(s, 10, prev, floor)
+    for f in ("pi", "mu", "lam", "psi"):
+        np.testing.assert_allclose(getattr(p_g, f), getattr(p_or, f), rtol=1e-12, atol=1e-14, err_msg=f)
+    np.testing.assert_allclose(p_g.lam[1], want[1, :2], rtol=1e-12, atol=1e-14)
+    s.E[3] = np.diag([1e-300, 1e-300, 1e-300])
+    s.Nc[3] = 1e-300
+    s.Y[3] = 1e10
+    sess.upload_params(to_vmfa_params(V, prev))
+    sess.upload_suffstats(s)
+    with pytest.raises(V.VmfaError, match="SingularEc"):
+        sess.update_params()
+    sess.close()
+
+
 def test_free_running_config1(oracle, gpu):
     """Config 1 (BASELINE.json configs[0]) end to end: 2 warm-up E-steps + 20
     iterations from the same seeded init; F per iteration within 1e-4 relative,

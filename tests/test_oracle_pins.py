@@ -313,3 +313,22 @@ def test_sharded_extra_draws_use_global_index(oracle):
     e2 = oracle.variational_e_step(X[300:], p, k, part, 9, 4, n_offset=300)
     assert np.array_equal(e2.idx, e.idx[300:])
     assert np.array_equal(part.K, full.K[300:])
+
+
+def test_update_params_ldlt_semantics(oracle):
+    # mstep.cpp:129-140 factorises E_c with Eigen LDLT: singular/indefinite E_c
+    # solve through the pivoted LDL^T and D's pseudo-inverse; a zero pivot
+    # followed by a non-zero one takes the jitter retry
+    from _helpers import ldlt_cases
+    s, prev, floor, want = ldlt_cases(oracle)
+    p = oracle.update_params(s, 10, prev, floor)
+    H = prev.H
+    for c in range(4):
+        np.testing.assert_allclose(p.lam[c], want[c, :H], rtol=1e-9, atol=1e-12, err_msg=str(c))
+        np.testing.assert_allclose(p.mu[c], want[c, H], rtol=1e-9, atol=1e-12, err_msg=str(c))
+    # a solution that overflows with and without the jitter -> SingularEc
+    s.E[3] = np.diag([1e-300, 1e-300, 1e-300])
+    s.Nc[3] = 1e-300
+    s.Y[3] = 1e10
+    with pytest.raises(oracle.OracleError, match="component 3"):
+        oracle.update_params(s, 10, prev, floor)
