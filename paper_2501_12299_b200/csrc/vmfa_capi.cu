@@ -81,6 +81,8 @@ struct vmfa_ctx {
   float *P = nullptr, *V32 = nullptr, *mu32 = nullptr, *WT = nullptr, *ipsi32 = nullptr;
   int Hp = 8;
   float *WTS = nullptr, *acst = nullptr, *lblk = nullptr, *cblk = nullptr;
+  int4* jobs = nullptr;  // scorer job table (one int4 per 128-row work item)
+  float *bimg = nullptr, *simg = nullptr;  // scorer B stage images (anchor / single)
   int scorer = 2;           // 2: warp-specialised tcgen05 (default), 1: single-role tcgen05, 0: FFMA
   bool use_tc = true;
   int score_rows = kScoreRowsTc;
@@ -227,10 +229,12 @@ int csr_by_key(vmfa_ctx* x, const unsigned* keys, int64_t n, int* off, int* ent,
 }
 
 int score_grid() { return sm_count() * 8; }
+constexpr size_t kImageBudget = size_t(16) << 30;  // scorer B stage images (bytes)
 
 cudaError_t run_score(vmfa_ctx* x, int mode, const ScoreArgs& a) {
   if (x->scorer == 2)
-    return launch_score_ws(mode, a, x->WTS, x->mu32, x->ipsi32, x->acst, x->lblk, x->cblk, x->stream);
+    return launch_score_ws(mode, a, x->WTS, x->mu32, x->ipsi32, x->acst, x->lblk, x->cblk,
+                           mode == kModeAnchor ? x->bimg : x->simg, x->jobs, x->stream);
   if (x->scorer == 1) return launch_score_tc(mode, a, x->WT, x->ipsi32, x->mu32, x->stream);
   return launch_score(mode, a, score_grid(), x->stream);
 }
@@ -273,8 +277,12 @@ int run_precompute(vmfa_ctx* x, int* failed) {
   const int tok = x->begin(kFamPrecompute, x->dm.C);
   CU(launch_precompute(a, s));
   if (x->scorer == 2) {
-    CU(launch_ws_prep(x->dm, x->WT, x->WTS, s));
-    CU(launch_ws_blocks(x->dm, 1, x->mu32, x->ipsi32, x->g, x->gcnt, x->cblk, s));
+    if (x->simg) {
+      CU(launch_ws_images(x->dm, 1, x->WT, x->mu32, x->ipsi32, x->g, x->gcnt, x->simg, s));
+    } else {
+      CU(launch_ws_prep(x->dm, x->WT, x->WTS, s));
+      CU(launch_ws_blocks(x->dm, 1, x->mu32, x->ipsi32, x->g, x->gcnt, x->cblk, s));
+    }
   }
   x->end(tok);
   unsigned long long st = 0;
@@ -307,7 +315,8 @@ int estep_local(vmfa_ctx* x, uint64_t seed, uint64_t it, int mode, bool exchange
   if (x->scorer == 2) {
     const int tok = x->begin(kFamOther, dm.C);
     CU(launch_anchor_consts(dm, x->WT, x->mu32, x->ipsi32, x->g, x->gcnt, x->acst, s));
-    CU(launch_ws_blocks(dm, 0, x->mu32, x->ipsi32, x->g, x->gcnt, x->lblk, s));
+    if (x->bimg) CU(launch_ws_images(dm, 0, x->WT, x->mu32, x->ipsi32, x->g, x->gcnt, x->bimg, s));
+    else CU(launch_ws_blocks(dm, 0, x->mu32, x->ipsi32, x->g, x->gcnt, x->lblk, s));
     x->end(tok);
   }
   {
@@ -608,9 +617,17 @@ int vmfa_ctx_create(vmfa_ctx** out, int device, int C, int D, int H, int Cp, int
   A(x->WTS, Cs * ((D + 31) / 32) * 2 * x->Hp * 32);
   A(x->acst, Cs * G * (x->Hp + 1));
   if (x->scorer == 2) {
-    const size_t nch = (D + 31) / 32;
-    A(x->lblk, Cs * ws_groups(dm) * nch * 4 * 16 * 32);
-    A(x->cblk, Cs * nch * 4 * 16 * 32);
+    A(x->jobs, N * Cp / 128 + Cs + 2);  // items <= sum_c ceil(rows_c / 128)
+    // B stage images when they fit the budget, else per-block operand tiles
+    const size_t img_bytes = (ws_image_floats(dm, 0) + ws_image_floats(dm, 1)) * sizeof(float);
+    if (img_bytes <= kImageBudget) {
+      A(x->bimg, ws_image_floats(dm, 0));
+      A(x->simg, ws_image_floats(dm, 1));
+    } else {
+      const size_t nch = (D + 31) / 32;
+      A(x->lblk, Cs * ws_groups(dm) * nch * 4 * 16 * 32);
+      A(x->cblk, Cs * nch * 4 * 16 * 32);
+    }
   }
   A(x->ipsi32, Cs * D);
   A(x->K, N * Cp);

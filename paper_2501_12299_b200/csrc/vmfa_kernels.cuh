@@ -216,7 +216,11 @@ cudaError_t launch_anchor_consts(const Dims& dm, const float* WT, const float* m
                                  const int* g, const int* gcnt, float* acst, cudaStream_t s);
 cudaError_t launch_score_ws(int mode, const ScoreArgs& s, const float* WTS, const float* mu32,
                             const float* ipsi32, const float* acst, const float* lblk, const float* cblk,
-                            cudaStream_t st);
+                            const float* img, int4* jobs, cudaStream_t st);
+// B stage images of the warp-specialised scorer (single != 0: one component per job)
+int64_t ws_image_floats(const Dims& dm, int single);
+cudaError_t launch_ws_images(const Dims& dm, int single, const float* WT, const float* mu32, const float* ipsi32,
+                             const int* g, const int* gcnt, float* img, cudaStream_t s);
 int ws_groups(const Dims& dm);
 cudaError_t launch_ws_blocks(const Dims& dm, int single, const float* mu32, const float* ipsi32,
                              const int* g, const int* gcnt, float* blk, cudaStream_t s);

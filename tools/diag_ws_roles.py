@@ -19,8 +19,8 @@ s.upload_params(p)
 s.upload_state(st)
 for it in range(4):
     s.iterate(0, it)
-names = ["P wait acc", "P job sync", "P wait stage", "P build", "M wait acc", "M wait full", "M issue",
-         "E wait", "E work"]
+names = ["P wait acc", "P job sync", "P wait stage", "P build(rest)", "M wait acc", "M wait full", "M issue",
+         "E wait", "E work", "P split(+ld)", "P tmem st"]
 lib().vmfa_diag_scorer_cycles(1, None, 0)
 out = np.zeros(16, np.uint64)
 s.profile(True)
@@ -32,5 +32,25 @@ print({k: round(v["ms"], 3) for k, v in kt.items() if v["ms"] > 0})
 tot_p = out[0:4].sum()
 print("cycles per CTA-role (summed over CTAs; producer counters summed over 8 warps):")
 for i, nme in enumerate(names):
-    share = out[i] / (tot_p if i < 4 else (out[4:7].sum() if i < 7 else out[7:9].sum()))
+    tot_p = out[0:4].sum() + out[9:11].sum()
+    share = out[i] / (tot_p if (i < 4 or i >= 9) else (out[4:7].sum() if i < 7 else out[7:9].sum()))
     print(f"  {nme:14s} {int(out[i]):>16d}  share-in-role {share:6.3f}")
+
+# timeline of CTA 0 (anchor launch): per chunk (producer got stage, producer
+# arrived full, MMA saw full, MMA issued), cycles relative to the first event
+DBG = int(os.environ.get("WS_DBG", "0"))
+lib().vmfa_diag_scorer_cycles(1 | (DBG << 1), None, 0)
+big = np.zeros(16 + 8 * 512, np.uint64)
+s.variational_e_step(0, 11)
+lib().vmfa_diag_scorer_cycles(1 | (DBG << 1), big.ctypes.data_as(C.c_void_p), big.size)
+kt2 = s.kernel_times()
+print("WS_DBG", DBG, {k: round(v["ms"], 3) for k, v in kt2.items() if v["ms"] > 0})
+lib().vmfa_diag_scorer_cycles(0, None, 0)
+tr = big[16:].reshape(-1, 8).astype(np.int64)
+n = int((tr[:, 3] > 0).sum())
+t0 = tr[0, 0] if tr[0, 0] > 0 else tr[0, 1]
+print("chunk  got_stage  arrived  mma_sawA mma_sawB  mma_issued  ldr_start ldr_issued ldr_done  (period)")
+for i in range(min(n, 48)):
+    r = tr[i] - t0
+    per = tr[i, 1] - tr[i - 1, 1] if i else 0
+    print(f"{i:5d} {r[0]:10d} {r[1]:8d} {r[4]:8d} {r[2]:8d} {r[3]:10d} {r[5]:9d} {r[7]:9d} {r[6]:8d}  {per:6d}")
