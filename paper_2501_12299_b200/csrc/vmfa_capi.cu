@@ -80,9 +80,11 @@ struct vmfa_ctx {
          *kconst = nullptr;
   float *P = nullptr, *V32 = nullptr, *mu32 = nullptr, *WT = nullptr, *ipsi32 = nullptr;
   int Hp = 8;
-  float *WTS = nullptr, *acst = nullptr, *lblk = nullptr, *cblk = nullptr;
-  int4* jobs = nullptr;  // scorer job table (one int4 per 128-row work item)
-  float *bimg = nullptr, *simg = nullptr;  // scorer B stage images (anchor / single)
+  float *brec = nullptr, *srec = nullptr;  // scorer epilogue records (anchor slots / components)
+  int4* jobs = nullptr;                    // scorer job table (one int4 per 128-row work item)
+  uint16_t *bimg = nullptr, *simg = nullptr;  // scorer B stage images (fp16; anchor / single)
+  float *bscl = nullptr, *sscl = nullptr;     // their row scales
+  float *xmax = nullptr, *mumax = nullptr;    // A-row scale bounds
   int scorer = 2;           // 2: warp-specialised tcgen05 (default), 1: single-role tcgen05, 0: FFMA
   bool use_tc = true;
   int score_rows = kScoreRowsTc;
@@ -233,8 +235,8 @@ constexpr size_t kImageBudget = size_t(16) << 30;  // scorer B stage images (byt
 
 cudaError_t run_score(vmfa_ctx* x, int mode, const ScoreArgs& a) {
   if (x->scorer == 2)
-    return launch_score_ws(mode, a, x->WTS, x->mu32, x->ipsi32, x->acst, x->lblk, x->cblk,
-                           mode == kModeAnchor ? x->bimg : x->simg, x->jobs, x->stream);
+    return launch_score_ws(mode, a, WsOperands{x->xmax, x->mumax, x->mu32, x->brec, x->srec, x->bimg, x->bscl, x->simg, x->sscl},
+                           x->jobs, x->stream);
   if (x->scorer == 1) return launch_score_tc(mode, a, x->WT, x->ipsi32, x->mu32, x->stream);
   return launch_score(mode, a, score_grid(), x->stream);
 }
@@ -277,12 +279,9 @@ int run_precompute(vmfa_ctx* x, int* failed) {
   const int tok = x->begin(kFamPrecompute, x->dm.C);
   CU(launch_precompute(a, s));
   if (x->scorer == 2) {
-    if (x->simg) {
-      CU(launch_ws_images(x->dm, 1, x->WT, x->mu32, x->ipsi32, x->g, x->gcnt, x->simg, s));
-    } else {
-      CU(launch_ws_prep(x->dm, x->WT, x->WTS, s));
-      CU(launch_ws_blocks(x->dm, 1, x->mu32, x->ipsi32, x->g, x->gcnt, x->cblk, s));
-    }
+    CU(launch_ws_images(x->dm, 1, x->WT, x->mu32, x->ipsi32, x->g, x->gcnt, x->simg, x->sscl, s));
+    CU(launch_ws_records(x->dm, 1, x->WT, x->mu32, x->ipsi32, x->kconst, x->g, x->gcnt, x->sscl, x->srec, s));
+    CU(launch_rowmax(x->dm.C, x->dm.D, x->mu32, x->mumax, s));
   }
   x->end(tok);
   unsigned long long st = 0;
@@ -314,9 +313,8 @@ int estep_local(vmfa_ctx* x, uint64_t seed, uint64_t it, int mode, bool exchange
   // block 1: scoring
   if (x->scorer == 2) {
     const int tok = x->begin(kFamOther, dm.C);
-    CU(launch_anchor_consts(dm, x->WT, x->mu32, x->ipsi32, x->g, x->gcnt, x->acst, s));
-    if (x->bimg) CU(launch_ws_images(dm, 0, x->WT, x->mu32, x->ipsi32, x->g, x->gcnt, x->bimg, s));
-    else CU(launch_ws_blocks(dm, 0, x->mu32, x->ipsi32, x->g, x->gcnt, x->lblk, s));
+    CU(launch_ws_images(dm, 0, x->WT, x->mu32, x->ipsi32, x->g, x->gcnt, x->bimg, x->bscl, s));
+    CU(launch_ws_records(dm, 0, x->WT, x->mu32, x->ipsi32, x->kconst, x->g, x->gcnt, x->bscl, x->brec, s));
     x->end(tok);
   }
   {
@@ -579,6 +577,11 @@ int vmfa_ctx_create(vmfa_ctx** out, int device, int C, int D, int H, int Cp, int
     const std::string v = sc ? sc : "ws";
     x->scorer = v == "ffma" ? 0 : (v == "tc" ? 1 : 2);
     if (x->scorer == 2 && !score_ws_supported(x->dm)) x->scorer = 1;
+    // the warp-specialised scorer streams prebuilt B stage images: fall back
+    // to the single-role tensor scorer when they exceed the memory budget
+    if (x->scorer == 2 &&
+        static_cast<size_t>(ws_image_halves(x->dm, 0) + ws_image_halves(x->dm, 1)) * 2 > kImageBudget)
+      x->scorer = 1;
     if (x->scorer == 1 && !score_tc_supported(x->dm)) x->scorer = 0;
     x->use_tc = x->scorer != 0;
     x->score_rows = x->use_tc ? kScoreRowsTc : kScoreRows;
@@ -614,20 +617,16 @@ int vmfa_ctx_create(vmfa_ctx** out, int device, int C, int D, int H, int Cp, int
   A(x->V32, Cs * D * H);
   A(x->mu32, Cs * D);
   A(x->WT, Cs * x->Hp * D);
-  A(x->WTS, Cs * ((D + 31) / 32) * 2 * x->Hp * 32);
-  A(x->acst, Cs * G * (x->Hp + 1));
   if (x->scorer == 2) {
     A(x->jobs, N * Cp / 128 + Cs + 2);  // items <= sum_c ceil(rows_c / 128)
-    // B stage images when they fit the budget, else per-block operand tiles
-    const size_t img_bytes = (ws_image_floats(dm, 0) + ws_image_floats(dm, 1)) * sizeof(float);
-    if (img_bytes <= kImageBudget) {
-      A(x->bimg, ws_image_floats(dm, 0));
-      A(x->simg, ws_image_floats(dm, 1));
-    } else {
-      const size_t nch = (D + 31) / 32;
-      A(x->lblk, Cs * ws_groups(dm) * nch * 4 * 16 * 32);
-      A(x->cblk, Cs * nch * 4 * 16 * 32);
-    }
+    A(x->bimg, ws_image_halves(dm, 0));
+    A(x->simg, ws_image_halves(dm, 1));
+    A(x->bscl, ws_scale_floats(dm, 0));
+    A(x->brec, ws_record_floats(dm, 0));
+    A(x->srec, ws_record_floats(dm, 1));
+    A(x->sscl, ws_scale_floats(dm, 1));
+    A(x->xmax, N);
+    A(x->mumax, Cs);
   }
   A(x->ipsi32, Cs * D);
   A(x->K, N * Cp);
@@ -760,6 +759,7 @@ int vmfa_upload_data(vmfa_ctx* x, const float* X, int64_t row_begin, int64_t row
     return fail(VMFA_ERR_INVALID_ARGUMENT, "vmfa_upload_data: row range outside the shard");
   CU(cudaMemcpyAsync(x->X + row_begin * x->dm.D, X, sizeof(float) * rows * x->dm.D,
                      cudaMemcpyHostToDevice, x->stream));
+  if (x->xmax) CU(launch_rowmax(rows, x->dm.D, x->X + row_begin * x->dm.D, x->xmax + row_begin, x->stream));
   CU(cudaStreamSynchronize(x->stream));
   return VMFA_OK;
 }

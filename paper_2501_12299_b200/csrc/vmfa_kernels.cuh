@@ -209,20 +209,32 @@ cudaError_t launch_score_tc(int mode, const ScoreArgs& s, const float* WT, const
                             const float* mu32, cudaStream_t st);
 constexpr int kScoreRowsTc = 128;
 // warp-specialised tensor-core scorer (vmfa_score_ws.cu)
-int ws_hp(int H);  // W rows per component in WT / WTS (H padded to 8, 16, 32, 64)
+int ws_hp(int H);  // W rows per component in WT (H padded to 8, 16, 32, 64)
 bool score_ws_supported(const Dims& dm);
-cudaError_t launch_ws_prep(const Dims& dm, const float* WT, float* WTS, cudaStream_t s);
-cudaError_t launch_anchor_consts(const Dims& dm, const float* WT, const float* mu32, const float* ipsi32,
-                                 const int* g, const int* gcnt, float* acst, cudaStream_t s);
-cudaError_t launch_score_ws(int mode, const ScoreArgs& s, const float* WTS, const float* mu32,
-                            const float* ipsi32, const float* acst, const float* lblk, const float* cblk,
-                            const float* img, int4* jobs, cudaStream_t st);
-// B stage images of the warp-specialised scorer (single != 0: one component per job)
-int64_t ws_image_floats(const Dims& dm, int single);
-cudaError_t launch_ws_images(const Dims& dm, int single, const float* WT, const float* mu32, const float* ipsi32,
-                             const int* g, const int* gcnt, float* img, cudaStream_t s);
 int ws_groups(const Dims& dm);
-cudaError_t launch_ws_blocks(const Dims& dm, int single, const float* mu32, const float* ipsi32,
-                             const int* g, const int* gcnt, float* blk, cudaStream_t s);
+// operands of the scorer beyond ScoreArgs
+struct WsOperands {
+  const float* xmax;   // per row max |x| (N)
+  const float* mumax;  // per component max |mu32| (C)
+  const float* mu32;
+  const float* brec;   // per (anchor, slot) epilogue records (per E-step)
+  const float* srec;   // per component records (per precompute)
+  const void* bimg;    // anchor-job B stage images (fp16 hi/lo), rebuilt per E-step
+  const float* bscl;   // their row scales
+  const void* simg;    // one-component B stage images (extra / truncated F), per precompute
+  const float* sscl;
+};
+cudaError_t launch_score_ws(int mode, const ScoreArgs& s, const WsOperands& op, int4* jobs, cudaStream_t st);
+int64_t ws_record_floats(const Dims& dm, int single);
+cudaError_t launch_ws_records(const Dims& dm, int single, const float* WT, const float* mu32, const float* ipsi32,
+                              const double* kconst, const int* g, const int* gcnt, const float* scl, float* rec,
+                              cudaStream_t s);
+// B stage images (single != 0: one component per job), sizes in halves / floats
+int64_t ws_image_halves(const Dims& dm, int single);
+int64_t ws_scale_floats(const Dims& dm, int single);
+cudaError_t launch_ws_images(const Dims& dm, int single, const float* WT, const float* mu32, const float* ipsi32,
+                             const int* g, const int* gcnt, void* img, float* bscl, cudaStream_t s);
+// per-row max |value| of an N x D fp32 matrix (A-row scale bounds)
+cudaError_t launch_rowmax(int64_t N, int D, const float* X, float* xmax, cudaStream_t s);
 
 }  // namespace vmfa_b200

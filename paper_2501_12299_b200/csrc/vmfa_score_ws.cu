@@ -1,25 +1,40 @@
 // vmfa_score_ws.cu — warp-specialised tcgen05 scorer of the candidate
 // log-joints (log_joint, model.cpp:81-95) over anchor blocks.
 //
-// Same mathematics as vmfa_score_tc.cu (rows centred on the anchor mean,
-// 3xTF32 split products, fp32 accumulation in TMEM):
+// For anchor a, the rows n with a in K(n) need every component q in g_a, so a
+// job is a dense block: 128 rows x the components of g_a. Rows are centred on
+// the anchor mean (v = x - mu_a) and three products share the A operands:
 //   GEMM1  [v]   (128 x D) x [ -2 psi_q^-1 delta_q (16 rows) | W_q (Hp rows per q) ]
 //   GEMM2  [v^2] (128 x D) x [ psi_q^-1 (16 rows) ]
 // with delta_q = mu_q - mu_a, and per-(anchor, q) constants b = W_q^T delta_q,
-// m = sum psi_q^-1 delta_q^2 precomputed once per E-step (k_anchor_consts):
+// m = sum psi_q^-1 delta_q^2 precomputed once per E-step (k_build_records):
 //   y_q = acc_W - b,   diag_q = acc_psi + acc_lin + m,
 //   l = kconst_q - 0.5 (diag_q - |y_q|^2).
-// Roles (13 warps):
-//   warps 0-7  producers: gather + centre + split the 128 rows of each K
-//              chunk (A tiles), build the lin / psi^-1 B rows, and bulk-copy
-//              the per-component pre-split, pre-swizzled W blocks
-//              (cp.async.bulk, mbarrier transaction count);
-//   warp  8    MMA issuer: tcgen05.mma.kind::tf32 from smem descriptors,
-//              tcgen05.commit to the stage's empty barrier;
-//   warps 9-12 epilogue: tcgen05.ld of a finished accumulator (TMEM double
-//              buffered), log-joint assembly, scatter to the candidate slots.
+//
+// Arithmetic: 3xFP16 on tcgen05.mma.kind::f16 with fp32 accumulation in TMEM.
+// Every operand row is scaled by a power of two so its largest element is
+// ~2^14 (A rows by a bound on |x_n - mu_a|, B rows by their max over D; the
+// scales are undone exactly in the epilogue), then split x = hi + lo into two
+// fp16 values (22 significant bits, the same as 3xTF32); hi*hi + hi*lo + lo*hi
+// drops only lo*lo. K = 16 per instruction (twice tf32's K = 8) halves the
+// instruction count, and fp16 operands halve the B bytes.
+//
+// Roles (14 warps, one CTA per SM, persistent over the job table):
+//   warps 0-7  A producers: each thread streams its own pieces of a row into
+//              a private cp.async ring kAhead chunks ahead, centres / scales /
+//              splits them and stores the A operands into TMEM (tcgen05.st);
+//   warp  8    MMA issuer (one thread): TS-form tcgen05.mma, A from TMEM, B
+//              from shared memory, commits to the stage / accumulator barriers;
+//   warps 9-12 epilogue: stage the job's per-slot records in shared memory,
+//              tcgen05.ld a finished accumulator (double buffered), assemble
+//              the log-joints, scatter them to the candidate slots;
+//   warp 13    loader (one thread): per job the anchor mean into s_mu, per
+//              chunk one bulk copy of the prebuilt B stage image into an
+//              NB-deep ring (few large copies keep many bytes in flight).
 #include <algorithm>
 #include <cstdint>
+
+#include <cuda_fp16.h>
 
 #include "vmfa_b200.h"
 #include "vmfa_kernels.cuh"
@@ -28,19 +43,23 @@ namespace vmfa_b200 {
 namespace {
 
 constexpr int kRows = 128;
-constexpr int kKC = 32;               // K chunk: 32 tf32 = one 128-byte swizzle row
-constexpr int kTileA = kRows * 128;   // 16 KB
+constexpr int kKC = 64;               // K chunk: 64 fp16 = one 128-byte swizzle row
 constexpr int kProdWarps = 8;
+constexpr int kProdThreads = kProdWarps * 32;
 constexpr int kMmaWarp = 8;
 constexpr int kEpiWarp0 = 9;
-constexpr int kLoadWarp = 13;         // B-loader warp
+constexpr int kLoadWarp = 13;
 constexpr int kThreads = (kLoadWarp + 1) * 32;
 constexpr int kMaxNB = 8;             // B ring stages (smem)
-constexpr int kAhead = 5;             // producer row prefetch depth (chunks, cp.async ring)
-constexpr int kProdThreads = kProdWarps * 32;
-constexpr uint32_t kXRingBytes = (kAhead + 1) * 4 * kProdThreads * 16;
+constexpr int kAhead = 2;             // producer prefetch depth (chunks) in the cp.async ring
+constexpr int kXSeg = kKC / 2 / 4;    // 16-byte pieces per thread per chunk (32 floats)
+constexpr uint32_t kXSlotBytes = kXSeg * kProdThreads * 16;
+constexpr uint32_t kXRingBytes = (kAhead + 1) * kXSlotBytes;
 constexpr int kMaxD = 1024;
 constexpr int kNL = 16;               // lin rows / psi rows per group (qg <= 16)
+constexpr int kTargetExp = 14;        // operands scaled to |value| <= 2^14
+__host__ __device__ constexpr int rec_stride(int Hp) { return 8 + 2 * Hp; }  // floats per epilogue record
+__host__ __device__ constexpr int qg_max(int Hp) { return (256 - kNL) / Hp < kNL ? (256 - kNL) / Hp : kNL; }
 
 struct WsArgs {
   Dims dm;
@@ -48,32 +67,29 @@ struct WsArgs {
   int Hp;            // W rows per component (>= 8)
   int qg;            // components per job (group)
   int N1max;         // 16 + round16(qg * Hp)
-  int nbstage;        // B ring depth
+  int nbstage;       // B ring depth
   int nacc;          // accumulator buffers in TMEM (2 when they fit beside the A stages)
   uint32_t tmem_cols;
   uint32_t TB;       // TMEM columns per accumulator buffer
   uint32_t stage_bytes;
   const float* X;
-  const float* WTS;  // [C][nchunk][2][Hp][32] pre-split, pre-swizzled W blocks
+  const float* xmax;   // per row max |x| (A-row scale bound)
+  const float* mumax;  // per component max |mu32|
   const float* mu32;
-  const float* ipsi32;
-  const double* kconst;
-  const float* acst; // [C][G][Hp + 1] : b (Hp) then m, anchor mode only
-  const float* img;  // B stage images [C][groups][nchunk][stage] (nullptr: per-block copies)
-  const float* lblk; // anchor mode: [C][ngroups][nchunk][4][16][32] lin hi|lo, psi hi|lo tiles
-  const float* cblk; // single mode: [C][nchunk][4][16][32] (lin = 0, psi row 0)
+  const float* rec;    // epilogue records [C][G or 1][rec_stride(Hp)]
+  const __half* img;   // B stage images [C][groups][nchunk][stage]
   int ngroups;
-  const int4* jobs;  // per item {component, first CSR row, rows, components}
+  const int4* jobs;    // per item {component, first CSR row, rows, components}
   const int* itemoff;
   const int* ent;
   const int* g;
   const int* gcnt;
   float* out;
   unsigned long long* prof;  // optional per-role cycle counters (nullptr: off)
-  int dbg;                   // diagnostics only: bit0 skip x loads, bit1 skip B copies
+  int dbg;                   // diagnostics only: bit0 skip x loads, bit2 skip MMAs
 };
 
-// per-role cycle accounting (debug builds of the pipeline; prof == nullptr in production)
+// per-role cycle accounting (diagnostic instantiation only)
 enum ProfSite { kPWaitTE, kPSync, kPWaitEmpty, kPBuild, kMWaitTE, kMWaitFull, kMIssue, kEWait, kEWork, kPSplit, kPStore, kNumSites };
 struct Prof {
   unsigned long long acc[kNumSites];
@@ -86,7 +102,7 @@ struct Prof {
   }
 };
 
-// timeline trace of CTA 0 (diagnostics): slot = 16 + 4 * event_index + kind
+// timeline trace of CTA 0 (diagnostics): slot = 16 + 8 * event_index + kind
 constexpr int kTraceEvents = 512;
 __device__ __forceinline__ void trace(unsigned long long* prof, int idx, int kind) {
   if (prof && blockIdx.x == 0 && idx < kTraceEvents) prof[16 + 8 * idx + kind] = clock64();
@@ -95,29 +111,29 @@ __device__ __forceinline__ void trace(unsigned long long* prof, int idx, int kin
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
-__device__ __forceinline__ uint32_t to_tf32(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return r;
+// Power-of-two exponent k with |value| * 2^k <= 2^14 for |value| <= bound.
+__device__ __forceinline__ int scale_exp(float bound) {
+  if (!(bound > 0.f)) return 0;
+  const uint32_t b = __float_as_uint(bound);
+  int e = static_cast<int>((b >> 23) & 0xffu) - 127;  // bound in [2^e, 2^(e+1))
+  if ((b & 0x7fffffu) != 0u) e += 1;                  // bound <= 2^e
+  if (((b >> 23) & 0xffu) == 0u) e = -126;            // denormal bound
+  return max(-100, min(100, kTargetExp - e));
 }
-__device__ __forceinline__ void split(float x, uint32_t& hi, uint32_t& lo) {
-  hi = to_tf32(x);
-  lo = to_tf32(x - __uint_as_float(hi));
-}
-// hi = x rounded to tf32 (nearest, ties away: +half an ulp of tf32 on the
-// magnitude bits, then truncate), lo = x - hi exactly (the tensor core reads
-// its top 19 bits); two integer ops instead of the emulated cvt.rna.tf32.
-__device__ __forceinline__ void split_fast(float x, uint32_t& hi, uint32_t& lo) {
-  hi = (__float_as_uint(x) + 0x1000u) & 0xffffe000u;
-  lo = __float_as_uint(x - __uint_as_float(hi));
+__device__ __forceinline__ float exp2i(int k) { return __uint_as_float(static_cast<uint32_t>(k + 127) << 23); }
+// hi = fp16(x), lo = fp16(x - hi) for two values, packed (element 0 in the low half)
+__device__ __forceinline__ void split2(float x0, float x1, uint32_t& hi, uint32_t& lo) {
+  const __half2 h = __floats2half2_rn(x0, x1);
+  const float2 hf = __half22float2(h);
+  const __half2 l = __floats2half2_rn(x0 - hf.x, x1 - hf.y);
+  hi = *reinterpret_cast<const uint32_t*>(&h);
+  lo = *reinterpret_cast<const uint32_t*>(&l);
 }
 __device__ __forceinline__ void st4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d)
                : "memory");
 }
-__device__ __forceinline__ uint32_t swz(int r, int j) {
-  return static_cast<uint32_t>(((r >> 3) << 10) + ((r & 7) << 7) + (((j ^ (r & 7)) & 7) << 4));
-}
+// K-major, 128-byte-swizzled smem operand descriptor (8-row groups 1 KB apart)
 __device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
   uint64_t d = static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
   d |= static_cast<uint64_t>(1) << 16;
@@ -126,24 +142,17 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
   d |= static_cast<uint64_t>(2) << 61;
   return d;
 }
+// kind::f16 instruction descriptor: fp32 accumulate, fp16 A and B, K-major, M = 128
 __device__ __forceinline__ uint32_t idesc(int N) {
-  return (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(N >> 3) << 17) |
-         (static_cast<uint32_t>(kRows >> 4) << 24);
+  return (1u << 4) | (static_cast<uint32_t>(N >> 3) << 17) | (static_cast<uint32_t>(kRows >> 4) << 24);
 }
-__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t id, uint32_t accum) {
+// A operand from TMEM (lane = row, two fp16 per 32-bit column), B from smem
+__device__ __forceinline__ void mma_f16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t id,
+                                           uint32_t accum) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
-      "l"(a), "l"(b), "r"(id), "r"(accum));
-}
-// A operand from TMEM (lane = row, one tf32 per 32-bit column), B from smem
-__device__ __forceinline__ void mma_tf32_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t id,
-                                            uint32_t accum) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(tmem_d),
       "r"(tmem_a), "l"(b), "r"(id), "r"(accum));
 }
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* v) {
@@ -163,9 +172,6 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
 // Waits for the phase with the given parity; a wait longer than ~10 s of SM
 // clocks traps (a pipeline bug then fails the launch instead of hanging the GPU).
@@ -199,30 +205,6 @@ __device__ __forceinline__ void bulk_copy(uint32_t dst, const void* src, uint32_
 }
 __device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-
-template <int W>
-__device__ __forceinline__ void tmem_ld(uint32_t taddr, float* v) {
-  static_assert(W == 8 || W == 16, "width");
-  uint32_t r[16];
-  if constexpr (W == 8) {
-    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
-                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-                   "=r"(r[7])
-                 : "r"(taddr));
-  } else {
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
-        "%12, %13, %14, %15}, [%16];"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
-          "=r"(r[14]), "=r"(r[15])
-        : "r"(taddr));
-  }
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-  for (int i = 0; i < W; ++i) v[i] = __uint_as_float(r[i]);
-}
 
 template <int W>
 __device__ __forceinline__ void tmem_ld_nowait(uint32_t taddr, float* v) {
@@ -255,13 +237,11 @@ __device__ __forceinline__ void pin_regs(float* v) {
 // Job table: one int4 {component, first CSR row, rows, components to score}
 // per work item (built per launch by k_build_jobs), so every role decodes a
 // job with one 16-byte load instead of a binary search over the item offsets.
-__global__ void k_build_jobs(int C, int mode, int G, const int* off, const int* itemoff, const int* gcnt,
-                             int4* jobs) {
+__global__ void k_build_jobs(int C, int mode, const int* off, const int* itemoff, const int* gcnt, int4* jobs) {
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < C; c += gridDim.x * blockDim.x) {
     const int i0 = itemoff[c], i1 = itemoff[c + 1];
     const int r0 = off[c], r1 = off[c + 1];
     const int nc = mode == kModeAnchor ? gcnt[c] : 1;
-    (void)G;
     for (int it = i0; it < i1; ++it) {
       const int row0 = r0 + (it - i0) * kRows;
       jobs[it] = make_int4(c, row0, min(kRows, r1 - row0), nc);
@@ -291,11 +271,15 @@ __device__ __forceinline__ Walk walk_begin(const int4* jobs, int total) {
   return w;
 }
 
-// x-row index of the producer's row `ar` in job J (-1: padding row)
-__device__ __forceinline__ int job_row(const WsArgs& a, const int4& J, int ar) {
-  if (ar >= J.z) return -1;
-  const int e = __ldg(a.ent + J.y + ar);
+// x-row index of row `r` of job J (-1: padding row)
+__device__ __forceinline__ int job_row(const WsArgs& a, const int4& J, int r) {
+  if (r >= J.z) return -1;
+  const int e = __ldg(a.ent + J.y + r);
   return a.mode == kModeExtra ? e : e / a.dm.Cp;
+}
+// A-row scale exponent of row n centred on component c (same in producer and epilogue)
+__device__ __forceinline__ int row_exp(const WsArgs& a, int n, int c) {
+  return n < 0 ? 0 : scale_exp(__ldg(a.xmax + n) + __ldg(a.mumax + c));
 }
 
 template <int HP, bool PROF>
@@ -306,6 +290,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_ws(WsArgs a) {
   __shared__ uint64_t s_mufull[2], s_muempty[2];
   __shared__ __align__(16) float s_mu[2][kMaxD + 8];
   __shared__ int s_muoff[2];
+  __shared__ __align__(16) float s_rec[4 * qg_max(HP) * rec_stride(HP)];  // epilogue records, per warp
   __shared__ uint32_t s_tmem;
   const Dims dm = a.dm;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -321,8 +306,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_ws(WsArgs a) {
       mbar_init(&s_aempty[i], 1);
       mbar_init(&s_tfull[i], 1);
       mbar_init(&s_tempty[i], 4);
-    }
-    for (int i = 0; i < 2; ++i) {
       mbar_init(&s_mufull[i], 1);
       mbar_init(&s_muempty[i], kProdWarps);
     }
@@ -337,28 +320,26 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_ws(WsArgs a) {
                  "r"(a.tmem_cols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  for (uint32_t i = tid * 16; i < a.stage_bytes * NB; i += kThreads * 16) st4(sbase + i, 0, 0, 0, 0);
-  fence_async_smem();
   fence_before();
   __syncthreads();
   fence_after();
   const uint32_t tmem = s_tmem;
-  // B stage map (offsets from a 1024-aligned stage base)
-  const uint32_t offB1 = 0;                          // B1 hi, then B1 lo (N1max rows each)
-  const uint32_t offB2 = offB1 + 2 * a.N1max * 128;  // B2 hi, then B2 lo (16 rows each)
+  // B stage map (offsets from a 1024-aligned stage base): B1 hi | B1 lo (N1max
+  // rows each) | B2 hi | B2 lo (16 rows each), 128-byte rows
+  const uint32_t offB1 = 0;
+  const uint32_t offB2 = offB1 + 2 * a.N1max * 128;
   // TMEM map: accumulators [0, nacc*TB), then the two A stages of 128 columns
   const uint32_t colA = a.nacc * a.TB;
 
   if (warp < kProdWarps) {
     // ============================================================ A producers
-    // thread = (row ar of the 128-row block, K half ah of each 32-wide chunk).
-    // Each thread streams its own 64-byte row pieces into a private shared-
-    // memory ring with cp.async, `ahead` chunks in advance and across job
-    // borders (no registers held, no cross-thread sync: cp.async groups are
-    // per thread); the anchor mean arrives in shared memory from the loader.
+    // thread = (row ar of the 128-row block, K half ah of each 64-wide chunk):
+    // 32 consecutive x values per chunk through a private cp.async ring
+    // (per-thread commit groups, no cross-thread sync), then
+    // v = (x - mu_a) 2^k and q = v^2 2^-14 split into fp16 hi / lo pairs.
     const int ar = 32 * (warp & 3) + lane, ah = warp >> 2;
     const int ahead = min(kAhead, nchunk);  // prefetch stays within the next job
-    const uint32_t xbase = sbase + NB * a.stage_bytes;  // X ring: (kAhead+1) x [4][256] x 16 B
+    const uint32_t xbase = sbase + NB * a.stage_bytes;
     Prof pf{};
     if (PROF) pf.start();
     Walk w = walk_begin(a.jobs, total);
@@ -368,10 +349,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_ws(WsArgs a) {
     int n_nxt = wn.valid(total) ? job_row(a, wn.J, ar) : -1;
     const bool vec = (dm.D & 3) == 0;
     auto issue_x = [&](int n, int ch, uint32_t unit) {
-      const uint32_t slot = xbase + (unit % (kAhead + 1)) * (4 * kProdThreads * 16);
+      const uint32_t slot = xbase + (unit % (kAhead + 1)) * kXSlotBytes;
 #pragma unroll
-      for (int jj = 0; jj < 4; ++jj) {
-        const int d = ch * kKC + 16 * ah + 4 * jj;
+      for (int jj = 0; jj < kXSeg; ++jj) {
+        const int d = ch * kKC + 32 * ah + 4 * jj;
         const uint32_t dst = slot + (jj * kProdThreads + tid) * 16;
         const float* src = a.X + (int64_t)(n < 0 ? 0 : n) * dm.D + d;
         if (n < 0 || d >= dm.D || (PROF && (a.dbg & 1))) {
@@ -380,8 +361,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_ws(WsArgs a) {
           asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
         } else {
           for (int k = 0; k < 4; ++k) {
-            if (d + k < dm.D) asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst + 4 * k), "l"(src + k) : "memory");
-            else asm volatile("st.shared.b32 [%0], %1;" ::"r"(dst + 4 * k), "r"(0u) : "memory");
+            if (d + k < dm.D)
+              asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst + 4 * k), "l"(src + k) : "memory");
+            else
+              asm volatile("st.shared.b32 [%0], %1;" ::"r"(dst + 4 * k), "r"(0u) : "memory");
           }
         }
       }
@@ -390,55 +373,64 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_ws(WsArgs a) {
     auto wait_x = [&]() {  // all but the newest `ahead` groups landed
       switch (ahead) {
         case 1: asm volatile("cp.async.wait_group 1;" ::: "memory"); break;
-        case 2: asm volatile("cp.async.wait_group 2;" ::: "memory"); break;
-        case 3: asm volatile("cp.async.wait_group 3;" ::: "memory"); break;
-        case 4: asm volatile("cp.async.wait_group 4;" ::: "memory"); break;
-        default: asm volatile("cp.async.wait_group 5;" ::: "memory"); break;
+        default: asm volatile("cp.async.wait_group 2;" ::: "memory"); break;
       }
     };
-    uint32_t sc = 0;  // flat chunk (unit) counter
+    static_assert(kAhead <= 2, "wait_x covers ahead <= 2");
+    uint32_t sc = 0;  // flat chunk counter
     if (w.valid(total))
       for (int k = 0; k < ahead; ++k) issue_x(n_cur, k, static_cast<uint32_t>(k));
     int jb = 0;
     while (w.valid(total)) {
       const int mslot = jb & 1;
+      const float sA = exp2i(row_exp(a, n_cur, w.J.x));
       mbar_wait(&s_mufull[mslot], (jb >> 1) & 1);
       const float* mu_s = s_mu[mslot] + s_muoff[mslot];
       for (int ch = 0; ch < nchunk; ++ch, ++sc) {
-        {  // prefetch unit sc + ahead (this job or the next)
+        {  // prefetch chunk sc + ahead (this job or the next)
           const int c2 = ch + ahead;
           if (c2 < nchunk) issue_x(n_cur, c2, sc + ahead);
           else issue_x(wn.valid(total) ? n_nxt : -1, c2 - nchunk, sc + ahead);
         }
         wait_x();
+        if (PROF) pf.lap(kPBuild);  // (waiting for the row pieces)
         const int s = static_cast<int>(sc & 1u);
         const uint32_t use = sc >> 1;
-        const int d0 = ch * kKC;
-        const uint32_t slot = xbase + (sc % (kAhead + 1)) * (4 * kProdThreads * 16);
-        // v = x - mu_a and v^2, split hi (round to tf32) / lo (exact residual)
+        const int d0 = ch * kKC + 32 * ah;
+        const uint32_t slot = xbase + (sc % (kAhead + 1)) * kXSlotBytes;
         uint32_t vh[16], vl[16], qh[16], ql[16];
 #pragma unroll
-        for (int jj = 0; jj < 4; ++jj) {
-          const int d = d0 + 16 * ah + 4 * jj;
+        for (int jj = 0; jj < kXSeg; ++jj) {
+          const int d = d0 + 4 * jj;
           float xv[4];
           asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
                        : "=f"(xv[0]), "=f"(xv[1]), "=f"(xv[2]), "=f"(xv[3])
                        : "r"(slot + (jj * kProdThreads + tid) * 16)
                        : "memory");
-          float v[4];
+          float mv[4];
+          if (vec) {  // (D % 4 == 0: the mean window starts 16-byte aligned)
+            const float4 m4 = *reinterpret_cast<const float4*>(mu_s + d);
+            mv[0] = m4.x, mv[1] = m4.y, mv[2] = m4.z, mv[3] = m4.w;
+          } else {
 #pragma unroll
-          for (int k = 0; k < 4; ++k) v[k] = d + k < dm.D ? xv[k] - mu_s[d + k] : 0.f;
-          if (n_cur < 0) v[0] = v[1] = v[2] = v[3] = 0.f;
+            for (int k = 0; k < 4; ++k) mv[k] = mu_s[d + k];
+          }
+          float v[4], q[4];
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
-            split_fast(v[k], vh[4 * jj + k], vl[4 * jj + k]);
-            split_fast(v[k] * v[k], qh[4 * jj + k], ql[4 * jj + k]);
+            v[k] = (d + k < dm.D && n_cur >= 0) ? (xv[k] - mv[k]) * sA : 0.f;
+            q[k] = (v[k] * v[k]) * exp2i(-kTargetExp);
           }
+          split2(v[0], v[1], vh[2 * jj], vl[2 * jj]);
+          split2(v[2], v[3], vh[2 * jj + 1], vl[2 * jj + 1]);
+          split2(q[0], q[1], qh[2 * jj], ql[2 * jj]);
+          split2(q[2], q[3], qh[2 * jj + 1], ql[2 * jj + 1]);
         }
         if (PROF) pf.lap(kPSplit);
         if (use >= 1) mbar_wait(&s_aempty[s], (use - 1) & 1u);
         if (PROF) pf.lap(kPWaitEmpty);
         if (tid == 32) trace(tp, static_cast<int>(sc), 0);
+        // operand columns: v hi | v lo | q hi | q lo (32 each); this thread's K half
         const uint32_t ta = tmem + (static_cast<uint32_t>(32 * (warp & 3)) << 16) + colA + s * 128 + 16 * ah;
         tmem_st16(ta, vh);
         tmem_st16(ta + 32, vl);
@@ -454,7 +446,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_ws(WsArgs a) {
       __syncwarp();
       if (lane == 0) mbar_arrive(&s_muempty[mslot]);  // done with this job's mean
       ++jb;
-      // next job
       w = wn;
       if (!w.valid(total)) break;
       wn.advance(a.jobs, a.qg, total);
@@ -465,23 +456,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_ws(WsArgs a) {
     asm volatile("cp.async.wait_all;" ::: "memory");
     if (PROF && a.prof && lane == 0) {
       atomicAdd(a.prof + kPSync, pf.acc[kPSync]);
+      atomicAdd(a.prof + kPBuild, pf.acc[kPBuild]);
       atomicAdd(a.prof + kPWaitEmpty, pf.acc[kPWaitEmpty]);
       atomicAdd(a.prof + kPSplit, pf.acc[kPSplit]);
       atomicAdd(a.prof + kPStore, pf.acc[kPStore]);
     }
   } else if (warp == kLoadWarp) {
-    // ============================================================ B loader
-    // one thread fills an NB-deep shared-memory ring with the B operands,
-    // running ahead of the MMA across job borders: one bulk copy of the
-    // prebuilt stage image per chunk (few large copies keep many bytes in
-    // flight; small copies are serialised by the copy engine), else per-block
-    // copies of the pre-split W blocks and lin/psi tiles
+    // ============================================================ loader
     if (lane == 0) {
       uint32_t bc = 0;
       int jb = 0;
       for (Walk w = walk_begin(a.jobs, total); w.valid(total); w.advance(a.jobs, a.qg, total), ++jb) {
         const int c = w.J.x;
-        const int nq = min(a.qg, w.J.w - w.g0);
         const int grp = w.g0 / a.qg;
         {  // the job's centring mean mu_a -> s_mu[jb & 1] (16-byte aligned window)
           const int m = jb & 1;
@@ -492,39 +478,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_ws(WsArgs a) {
           mbar_arrive_expect_tx(&s_mufull[m], bytes);
           bulk_copy(smem_u32(s_mu[m]), a.mu32 + fa, bytes, &s_mufull[m]);
         }
-        int comp[kNL];
-        if (!a.img)
-          for (int qi = 0; qi < nq; ++qi)
-            comp[qi] = a.mode == kModeAnchor ? __ldg(a.g + (int64_t)c * dm.G + w.g0 + qi) : c;
+        const int ng = a.mode == kModeAnchor ? a.ngroups : 1;
+        const __half* src0 = a.img + ((int64_t)c * ng + grp) * nchunk * (a.stage_bytes / 2);
         for (int ch = 0; ch < nchunk; ++ch, ++bc) {
           const int s = static_cast<int>(bc % NB);
           const uint32_t use = bc / NB;
           if (use >= 1) mbar_wait(&s_bempty[s], (use - 1) & 1u);
           trace(tp, static_cast<int>(bc), 5);
-          const uint32_t st = sbase + s * a.stage_bytes;
-          if (a.img) {
-            const int ng = a.mode == kModeAnchor ? a.ngroups : 1;
-            const float* src = a.img + (((int64_t)c * ng + grp) * nchunk + ch) * (a.stage_bytes / 4);
-            mbar_arrive_expect_tx(&s_bfull[s], a.stage_bytes);
-            bulk_copy(st, src, a.stage_bytes, &s_bfull[s]);
-          } else {
-            const uint32_t blk = HP * 128;
-            mbar_arrive_expect_tx(&s_bfull[s], 2 * nq * blk + 4 * kNL * 128);
-            for (int qi = 0; qi < nq; ++qi) {
-              const float* src = a.WTS + ((int64_t)comp[qi] * nchunk + ch) * 2 * HP * 32;
-              const uint32_t row = kNL + qi * HP;
-              bulk_copy(st + offB1 + row * 128, src, blk, &s_bfull[s]);
-              bulk_copy(st + offB1 + a.N1max * 128 + row * 128, src + HP * 32, blk, &s_bfull[s]);
-            }
-            const float* lb = (a.mode == kModeAnchor
-                                   ? a.lblk + ((int64_t)c * a.ngroups + grp) * nchunk * 4 * kNL * 32
-                                   : a.cblk + (int64_t)c * nchunk * 4 * kNL * 32) +
-                              (int64_t)ch * 4 * kNL * 32;
-            bulk_copy(st + offB1, lb, kNL * 128, &s_bfull[s]);                             // lin hi
-            bulk_copy(st + offB1 + a.N1max * 128, lb + kNL * 32, kNL * 128, &s_bfull[s]);  // lin lo
-            bulk_copy(st + offB2, lb + 2 * kNL * 32, kNL * 128, &s_bfull[s]);              // psi hi
-            bulk_copy(st + offB2 + kNL * 128, lb + 3 * kNL * 32, kNL * 128, &s_bfull[s]);  // psi lo
-          }
+          mbar_arrive_expect_tx(&s_bfull[s], a.stage_bytes);
+          bulk_copy(sbase + s * a.stage_bytes, src0 + (int64_t)ch * (a.stage_bytes / 2), a.stage_bytes,
+                    &s_bfull[s]);
           trace(tp, static_cast<int>(bc), 6);
         }
       }
@@ -556,7 +519,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_ws(WsArgs a) {
         if (lane == 0) {
           const uint32_t st = sbase + sb * a.stage_bytes;
           const uint32_t id1 = idesc(N1), id2 = idesc(kNL);
-          const uint32_t tA = tmem + colA + s * 128;  // v hi | v lo | v^2 hi | v^2 lo
+          const uint32_t tA = tmem + colA + s * 128;  // v hi | v lo | q hi | q lo
           const uint32_t Av[3] = {tA, tA, tA + 32};
           const uint32_t Aq[3] = {tA + 64, tA + 64, tA + 96};
           const uint32_t B1[3] = {st + offB1, st + offB1 + a.N1max * 128, st + offB1};
@@ -564,10 +527,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_ws(WsArgs a) {
 #pragma unroll
           for (int p = 0; p < ((PROF && (a.dbg & 4)) ? 0 : 3); ++p) {
 #pragma unroll
-            for (int k = 0; k < kKC / 8; ++k) {
+            for (int k = 0; k < kKC / 16; ++k) {
               const uint32_t acc = (ch > 0 || p > 0 || k > 0) ? 1u : 0u;
-              mma_tf32_ts(acc1, Av[p] + k * 8, sdesc(B1[p] + k * 32), id1, acc);
-              mma_tf32_ts(acc2, Aq[p] + k * 8, sdesc(B2[p] + k * 32), id2, acc);
+              mma_f16_ts(acc1, Av[p] + k * 8, sdesc(B1[p] + k * 32), id1, acc);
+              mma_f16_ts(acc2, Aq[p] + k * 8, sdesc(B2[p] + k * 32), id2, acc);
             }
           }
           commit(&s_aempty[s]);
@@ -583,9 +546,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_ws(WsArgs a) {
       for (int i = kMWaitTE; i <= kMIssue; ++i) atomicAdd(a.prof + i, pf.acc[i]);
   } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + 4) {
     // ============================================================ epilogue
+    // Each warp stages the job's per-slot records in its own shared-memory
+    // block (vector loads, before waiting for the accumulator), then reads
+    // them as broadcasts while assembling its 32 rows.
     constexpr int kEpiBatch = HP >= 32 ? 1 : 32 / HP;  // components per tcgen05.ld batch
+    constexpr int R = rec_stride(HP);
     const int quad = warp & 3;
     const int r = quad * 32 + lane;
+    float* srec = s_rec + quad * (qg_max(HP) * R);
     int jb = 0;
     Prof pf{};
     if (PROF) pf.start();
@@ -595,6 +563,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_ws(WsArgs a) {
       const int c = w.J.x;
       const int nq = min(a.qg, w.J.w - w.g0);
       const int e = r < w.J.z ? __ldg(a.ent + w.J.y + r) : -1;
+      const int n = e < 0 ? -1 : (a.mode == kModeExtra ? e : e / dm.Cp);
+      {
+        const float4* src = reinterpret_cast<const float4*>(
+            a.rec + ((int64_t)c * (a.mode == kModeAnchor ? dm.G : 1) + w.g0) * R);
+        __syncwarp();
+        for (int i = lane; i < nq * R / 4; i += 32) reinterpret_cast<float4*>(srec)[i] = __ldg(src + i);
+        __syncwarp();
+      }
+      const int kA = row_exp(a, n, c);
+      const float invA = exp2i(-kA), invQ = exp2i(kTargetExp - 2 * kA);
       mbar_wait(&s_tfull[b], use_b & 1);
       fence_after();
       if (PROF) pf.lap(kEWait);
@@ -606,6 +584,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_ws(WsArgs a) {
       tmem_wait_ld();
       pin_regs<16>(lin);
       pin_regs<16>(d2);
+      int64_t obase = 0;
+      if (e >= 0) {
+        if (a.mode == kModeAnchor) {
+          const int nn = e / dm.Cp, j = e - nn * dm.Cp;
+          obase = (int64_t)nn * dm.SL + j * dm.G + w.g0;
+        } else if (a.mode == kModeExtra) {
+          obase = (int64_t)e * dm.SL + dm.Cp * dm.G;
+        } else {
+          obase = e;
+        }
+      }
       for (int q0 = 0; q0 < nq; q0 += kEpiBatch) {
         const int nb = min(kEpiBatch, nq - q0);
         float y[kEpiBatch][HP];
@@ -624,21 +613,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_ws(WsArgs a) {
 #pragma unroll
         for (int qi = 0; qi < kEpiBatch; ++qi) {
           if (qi >= nb) break;
-          const int slot = w.g0 + q0 + qi;
-          const int q = a.mode == kModeAnchor ? __ldg(a.g + (int64_t)c * dm.G + slot) : c;
-          float m = 0.f;
+          const float* rc = srec + (q0 + qi) * R;
           float yy = 0.f;
-          if (a.mode == kModeAnchor) {
-            const float* cst = a.acst + ((int64_t)c * dm.G + slot) * (HP + 1);
 #pragma unroll
-            for (int h = 0; h < HP; ++h) {
-              const float t = y[qi][h] - __ldg(cst + h);
-              yy = fmaf(t, t, yy);
-            }
-            m = __ldg(cst + HP);
-          } else {
-#pragma unroll
-            for (int h = 0; h < HP; ++h) yy = fmaf(y[qi][h], y[qi][h], yy);
+          for (int h = 0; h < HP; ++h) {
+            const float t = y[qi][h] * (invA * rc[8 + HP + h]) - rc[8 + h];
+            yy = fmaf(t, t, yy);
           }
           float linq = 0.f, d2q = 0.f;
 #pragma unroll
@@ -647,18 +627,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_ws(WsArgs a) {
               linq = lin[i];
               d2q = d2[i];
             }
-          const double diag = static_cast<double>(d2q) + static_cast<double>(linq) + static_cast<double>(m);
-          const float lj = static_cast<float>(__ldg(a.kconst + q) - 0.5 * (diag - static_cast<double>(yy)));
-          if (e >= 0) {
-            if (a.mode == kModeAnchor) {
-              const int n = e / dm.Cp, j = e - n * dm.Cp;
-              a.out[(int64_t)n * dm.SL + j * dm.G + slot] = lj;
-            } else if (a.mode == kModeExtra) {
-              a.out[(int64_t)e * dm.SL + dm.Cp * dm.G] = lj;
-            } else {
-              a.out[e] = lj;
-            }
-          }
+          linq *= invA * rc[3];
+          d2q *= invQ * rc[4];
+          const double kc = static_cast<double>(rc[1]) + static_cast<double>(rc[5]);
+          const double diag = static_cast<double>(d2q) + static_cast<double>(linq) + static_cast<double>(rc[2]);
+          const float lj = static_cast<float>(kc - 0.5 * (diag - static_cast<double>(yy)));
+          if (e >= 0) a.out[obase + (a.mode == kModeAnchor ? q0 + qi : 0)] = lj;
         }
       }
       fence_before();
@@ -675,220 +649,198 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_ws(WsArgs a) {
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(a.tmem_cols));
 }
 
-// Per-(anchor, slot) constants: b = W_q^T (mu_q - mu_a), m = sum psi_q^-1 (mu_q - mu_a)^2
-// (fp32 operands of the scorer, fp64 accumulation). One warp per (anchor, slot).
-__global__ void __launch_bounds__(256) k_anchor_consts(Dims dm, int Hp, const float* WT, const float* mu32,
-                                                      const float* ipsi32, const int* g, const int* gcnt,
-                                                      float* acst) {
+// Per-slot epilogue records, one warp per (anchor, slot) -- or per component
+// when single != 0 -- after the stage images (which supply the row scales):
+//   [0] q (int bits)  [1] kconst_q hi  [2] m  [3] lin row scale  [4] psi row scale
+//   [5] kconst_q lo   [8, 8+Hp) b_h     [8+Hp, 8+2Hp) W row scales
+// with b = W_q^T (mu_q - mu_a), m = sum psi_q^-1 (mu_q - mu_a)^2 (fp32 operands,
+// fp64 accumulation; 0 for single), kconst = hi + lo exactly to ~48 bits.
+__global__ void __launch_bounds__(256) k_build_records(Dims dm, int Hp, int qg, int ngroups, int N1max, int single,
+                                                       const float* WT, const float* mu32, const float* ipsi32,
+                                                       const double* kconst, const int* g, const int* gcnt,
+                                                       const float* scl, float* rec) {
   const int lane = threadIdx.x & 31;
+  const int R = rec_stride(Hp);
+  const int nslot = single ? 1 : dm.G;
+  const int ng = single ? 1 : ngroups;
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t w = gw; w < (int64_t)dm.C * dm.G; w += nw) {
-    const int c = static_cast<int>(w / dm.G), i = static_cast<int>(w - (int64_t)c * dm.G);
-    float* out = acst + w * (Hp + 1);
-    if (i >= gcnt[c]) continue;
-    const int q = g[(int64_t)c * dm.G + i];
-    const float* mq = mu32 + (int64_t)q * dm.D;
-    const float* ma = mu32 + (int64_t)c * dm.D;
-    const float* ip = ipsi32 + (int64_t)q * dm.D;
+  for (int64_t w = gw; w < (int64_t)dm.C * nslot; w += nw) {
+    const int c = static_cast<int>(w / nslot), i = static_cast<int>(w - (int64_t)c * nslot);
+    float* out = rec + w * R;
+    if (!single && i >= gcnt[c]) continue;
+    const int q = single ? c : g[(int64_t)c * dm.G + i];
+    const int grp = single ? 0 : i / qg, qi = single ? 0 : i - grp * qg;
+    const float* sr = scl + ((int64_t)c * ng + grp) * (N1max + kNL);
     double m = 0.0;
-    for (int d = lane; d < dm.D; d += 32) {
-      const double dl = static_cast<double>(mq[d]) - static_cast<double>(ma[d]);
-      const float dlf = mq[d] - ma[d];  // same fp32 rounding as the scorer's operands
-      m += static_cast<double>(ip[d]) * static_cast<double>(dlf) * static_cast<double>(dlf);
-      (void)dl;
-    }
+    if (!single) {
+      const float* mq = mu32 + (int64_t)q * dm.D;
+      const float* ma = mu32 + (int64_t)c * dm.D;
+      const float* ip = ipsi32 + (int64_t)q * dm.D;
+      for (int d = lane; d < dm.D; d += 32) {
+        const float dlf = mq[d] - ma[d];  // same fp32 rounding as the scorer's operands
+        m += static_cast<double>(ip[d]) * static_cast<double>(dlf) * static_cast<double>(dlf);
+      }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) m += __shfl_xor_sync(0xffffffffu, m, o);
-    for (int h = 0; h < Hp; ++h) {
-      const float* wr = WT + ((int64_t)q * Hp + h) * dm.D;
-      double s = 0.0;
-      for (int d = lane; d < dm.D; d += 32) s += static_cast<double>(wr[d]) * static_cast<double>(mq[d] - ma[d]);
+      for (int o = 16; o > 0; o >>= 1) m += __shfl_xor_sync(0xffffffffu, m, o);
+      for (int h = 0; h < Hp; ++h) {
+        const float* wr = WT + ((int64_t)q * Hp + h) * dm.D;
+        double sb = 0.0;
+        for (int d = lane; d < dm.D; d += 32) sb += static_cast<double>(wr[d]) * static_cast<double>(mq[d] - ma[d]);
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      if (lane == 0) out[h] = static_cast<float>(s);
-    }
-    if (lane == 0) out[Hp] = static_cast<float>(m);
-  }
-}
-
-// Pre-split, pre-swizzled W blocks: WTS[q][chunk][hi|lo][Hp rows][32] so that a
-// block lands verbatim in a 128B-swizzled K-major tile at any 8-row boundary.
-__global__ void k_build_wts(Dims dm, int Hp, const float* WT, float* WTS) {
-  const int nchunk = (dm.D + kKC - 1) / kKC;
-  const int64_t total = (int64_t)dm.C * nchunk * Hp * kKC;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int e = static_cast<int>(i % kKC);
-    int64_t t = i / kKC;
-    const int h = static_cast<int>(t % Hp);
-    t /= Hp;
-    const int ch = static_cast<int>(t % nchunk);
-    const int q = static_cast<int>(t / nchunk);
-    const int d = ch * kKC + e;
-    const float w = d < dm.D ? WT[((int64_t)q * Hp + h) * dm.D + d] : 0.f;
-    uint32_t hi, lo;
-    split(w, hi, lo);
-    const int j = e >> 2;
-    const int pos = h * 32 + (((j ^ (h & 7)) & 7) << 2) + (e & 3);
-    float* blk = WTS + ((int64_t)q * nchunk + ch) * 2 * Hp * 32;
-    blk[pos] = __uint_as_float(hi);
-    blk[Hp * 32 + pos] = __uint_as_float(lo);
-  }
-}
-
-// Anchor-dependent B blocks, once per E-step (g and the parameters are fixed
-// during the E-step): for anchor a, component group grp, K chunk ch, the 16-row
-// tiles [lin hi | lin lo | psi hi | psi lo] with lin_q = -2 psi_q^-1 (mu_q - mu_a),
-// pre-split and pre-swizzled exactly as the smem B tiles. single != 0 builds
-// the one-component blocks (q = a, lin = 0) of the extra / truncated-F passes.
-__global__ void k_build_blocks(Dims dm, int qg, int ngroups, int single, const float* mu32,
-                               const float* ipsi32, const int* g, const int* gcnt, float* blk) {
-  const int nchunk = (dm.D + kKC - 1) / kKC;
-  const int ng = single ? 1 : ngroups;
-  const int64_t total = (int64_t)dm.C * ng * nchunk * kNL * kKC;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int e = static_cast<int>(i % kKC);
-    int64_t t = i / kKC;
-    const int qi = static_cast<int>(t % kNL);
-    t /= kNL;
-    const int ch = static_cast<int>(t % nchunk);
-    t /= nchunk;
-    const int grp = static_cast<int>(t % ng);
-    const int a = static_cast<int>(t / ng);
-    const int d = ch * kKC + e;
-    int q = -1;
-    if (single) {
-      if (qi == 0) q = a;
+        for (int o = 16; o > 0; o >>= 1) sb += __shfl_xor_sync(0xffffffffu, sb, o);
+        if (lane == 0) out[8 + h] = static_cast<float>(sb);
+      }
     } else {
-      const int slot = grp * qg + qi;
-      if (qi < qg && slot < gcnt[a]) q = g[(int64_t)a * dm.G + slot];
+      for (int h = lane; h < Hp; h += 32) out[8 + h] = 0.f;
     }
-    float lin = 0.f, ip = 0.f;
-    if (q >= 0 && d < dm.D) {
-      ip = ipsi32[(int64_t)q * dm.D + d];
-      lin = single ? 0.f : -2.f * ip * (mu32[(int64_t)q * dm.D + d] - mu32[(int64_t)a * dm.D + d]);
+    for (int h = lane; h < Hp; h += 32) out[8 + Hp + h] = sr[kNL + qi * Hp + h];
+    if (lane == 0) {
+      const double kc = kconst[q];
+      const float hi = static_cast<float>(kc);
+      out[0] = __int_as_float(q);
+      out[1] = hi;
+      out[2] = static_cast<float>(m);
+      out[3] = sr[qi];
+      out[4] = sr[N1max + qi];
+      out[5] = isfinite(kc) ? static_cast<float>(kc - static_cast<double>(hi)) : 0.f;
+      out[6] = 0.f;
+      out[7] = 0.f;
     }
-    uint32_t lh, ll, ph, pl;
-    split(lin, lh, ll);
-    split(ip, ph, pl);
-    const int j = e >> 2;
-    const int pos = qi * 32 + (((j ^ (qi & 7)) & 7) << 2) + (e & 3);
-    float* b = blk + (((int64_t)a * ng + grp) * nchunk + ch) * 4 * kNL * 32;
-    b[pos] = __uint_as_float(lh);
-    b[kNL * 32 + pos] = __uint_as_float(ll);
-    b[2 * kNL * 32 + pos] = __uint_as_float(ph);
-    b[3 * kNL * 32 + pos] = __uint_as_float(pl);
   }
 }
 
 // B stage images: for anchor a, component group grp and K chunk ch, the exact
 // shared-memory stage the MMA reads -- [B1 hi | B1 lo] (N1max rows: 16 lin
 // rows, then Hp W rows per component of the group) and [B2 hi | B2 lo] (16
-// psi^-1 rows) -- pre-split into tf32 hi/lo and 128B-swizzled, so the loader
-// moves a whole stage with one bulk copy. single != 0: one component (q = a),
-// lin = 0 (extra candidates, truncated F).
+// psi^-1 rows) -- each row scaled by 2^k (max over D ~ 2^14), split into fp16
+// hi/lo and 128B-swizzled, so the loader moves a stage with one bulk copy;
+// bscl receives 2^-k per row. One warp per B row (all chunks). single != 0:
+// one component (q = a), lin = 0 (extra candidates, truncated F).
 __global__ void __launch_bounds__(256) k_build_images(Dims dm, int Hp, int qg, int ngroups, int N1max, int single,
                                                       const float* WT, const float* mu32, const float* ipsi32,
-                                                      const int* g, const int* gcnt, float* img) {
-  // one CTA per stage image (a, grp, ch); 32-bit index math inside a stage
+                                                      const int* g, const int* gcnt, __half* img, float* bscl) {
+  const int lane = threadIdx.x & 31;
   const int nchunk = (dm.D + kKC - 1) / kKC;
   const int ng = single ? 1 : ngroups;
-  const int sf = 2 * 32 * (N1max + kNL);  // floats per stage
-  const int nstages = dm.C * ng * nchunk;
-  __shared__ int s_q[kNL];
-  __shared__ int s_nq;
-  for (int sid = blockIdx.x; sid < nstages; sid += gridDim.x) {
-    const int ch = sid % nchunk;
-    const int grp = (sid / nchunk) % ng;
-    const int a = sid / (nchunk * ng);
-    __syncthreads();
-    if (threadIdx.x == 0) s_nq = single ? 1 : min(qg, gcnt[a] - grp * qg);
-    if (threadIdx.x < kNL)
-      s_q[threadIdx.x] = single ? a : (threadIdx.x < min(qg, gcnt[a] - grp * qg) ? g[(int64_t)a * dm.G + grp * qg + threadIdx.x] : 0);
-    __syncthreads();
-    const int nq = s_nq;
-    float* out = img + (int64_t)sid * sf;
-    for (int f = threadIdx.x; f < sf; f += blockDim.x) {
-      // region: 0 B1 hi, 1 B1 lo (N1max rows each), 2 B2 hi, 3 B2 lo (16 rows each)
-      int reg, loc;
-      if (f < 2 * N1max * 32) reg = f / (N1max * 32), loc = f - reg * N1max * 32;
-      else reg = 2 + (f - 2 * N1max * 32) / (kNL * 32), loc = (f - 2 * N1max * 32) - (reg - 2) * kNL * 32;
-      const int r = loc >> 5, pos = loc & 31;
-      const int e = ((((pos >> 2) ^ (r & 7)) & 7) << 2) | (pos & 3);  // un-swizzled column
-      const int d = ch * kKC + e;
-      float v = 0.f;
-      if (d < dm.D) {
-        if (reg < 2) {
-          if (r < kNL) {
-            if (!single && r < nq) {
-              const int q = s_q[r];
-              v = -2.f * __ldg(ipsi32 + (int64_t)q * dm.D + d) *
-                  (__ldg(mu32 + (int64_t)q * dm.D + d) - __ldg(mu32 + (int64_t)a * dm.D + d));
-            }
-          } else {
-            const int qi = (r - kNL) / Hp, h = (r - kNL) - qi * Hp;
-            if (qi < nq) v = __ldg(WT + ((int64_t)s_q[qi] * Hp + h) * dm.D + d);
-          }
-        } else if (r < nq) {
-          v = __ldg(ipsi32 + (int64_t)s_q[r] * dm.D + d);
-        }
+  const int nrow = N1max + kNL;
+  const int64_t stage_h = 2 * 64 * (int64_t)nrow;  // halves per stage
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t wi = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; wi < (int64_t)dm.C * ng * nrow;
+       wi += nw) {
+    const int row = static_cast<int>(wi % nrow);
+    const int grp = static_cast<int>((wi / nrow) % ng);
+    const int a = static_cast<int>(wi / ((int64_t)nrow * ng));
+    const int slot0 = grp * qg;
+    const int nq = single ? 1 : min(qg, gcnt[a] - slot0);
+    // source of this row: kind 0 zero, 1 lin (q), 2 W (q, h), 3 psi (q)
+    int kind = 0, q = 0, h = 0;
+    if (row < N1max) {
+      if (row < kNL) {
+        if (!single && row < nq) kind = 1, q = g[(int64_t)a * dm.G + slot0 + row];
+      } else {
+        const int qi = (row - kNL) / Hp;
+        h = (row - kNL) - qi * Hp;
+        if (qi < nq) kind = 2, q = single ? a : g[(int64_t)a * dm.G + slot0 + qi];
       }
-      uint32_t hi, lo;
-      split(v, hi, lo);
-      out[f] = __uint_as_float((reg & 1) ? lo : hi);
+    } else if (row - N1max < nq) {
+      kind = 3, q = single ? a : g[(int64_t)a * dm.G + slot0 + (row - N1max)];
+    }
+    auto value = [&](int d) -> float {
+      if (kind == 1)
+        return -2.f * ipsi32[(int64_t)q * dm.D + d] * (mu32[(int64_t)q * dm.D + d] - mu32[(int64_t)a * dm.D + d]);
+      if (kind == 2) return WT[((int64_t)q * Hp + h) * dm.D + d];
+      if (kind == 3) return ipsi32[(int64_t)q * dm.D + d];
+      return 0.f;
+    };
+    float mx = 0.f;
+    if (kind != 0)
+      for (int d = lane; d < dm.D; d += 32) mx = fmaxf(mx, fabsf(value(d)));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    const int k = scale_exp(mx);
+    const float sc = exp2i(k);
+    if (lane == 0) bscl[((int64_t)a * ng + grp) * nrow + row] = exp2i(-k);
+    // matrix offsets (halves) within a stage: B1 hi 0, B1 lo N1max*64, B2 hi 2*N1max*64, B2 lo +16*64
+    const int rr = row < N1max ? row : row - N1max;
+    const int64_t off_hi = row < N1max ? 0 : 2 * (int64_t)N1max * 64;
+    const int64_t off_lo = row < N1max ? (int64_t)N1max * 64 : 2 * (int64_t)N1max * 64 + kNL * 64;
+    __half* base = img + ((int64_t)a * ng + grp) * nchunk * stage_h;
+    for (int d = lane; d < nchunk * kKC; d += 32) {
+      const int ch = d / kKC, e = d - ch * kKC;
+      const float v = (kind != 0 && d < dm.D) ? value(d) * sc : 0.f;
+      const __half hi = __float2half_rn(v);
+      const __half lo = __float2half_rn(v - __half2float(hi));
+      const int pos = rr * 64 + ((((e >> 3) ^ (rr & 7)) & 7) << 3) + (e & 7);  // 128B swizzle, 8 halves per 16 B
+      __half* st = base + ch * stage_h;
+      st[off_hi + pos] = hi;
+      st[off_lo + pos] = lo;
     }
   }
 }
 
+// per-row max |x| (A-row scale bounds), one warp per row
+__global__ void k_rowmax(int64_t N, int D, const float* X, float* xmax) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t n = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; n < N; n += nw) {
+    float m = 0.f;
+    for (int d = lane; d < D; d += 32) m = fmaxf(m, fabsf(X[n * D + d]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0) xmax[n] = m;
+  }
+}
+
+int ws_qg(const Dims& dm, int single) {
+  const int Hp = ws_hp(dm.H);
+  return single ? 1 : std::max(1, std::min(std::min(dm.G, kNL), (256 - kNL) / Hp));
+}
+int ws_n1max(const Dims& dm, int single) { return kNL + ((ws_qg(dm, single) * ws_hp(dm.H) + 15) / 16) * 16; }
+
 }  // namespace
 
-int64_t ws_image_floats(const Dims& dm, int single) {
-  const int Hp = ws_hp(dm.H);
-  const int qg = single ? 1 : std::max(1, std::min(std::min(dm.G, kNL), (256 - kNL) / Hp));
-  const int N1max = kNL + ((qg * Hp + 15) / 16) * 16;
-  const int nchunk = (dm.D + kKC - 1) / kKC;
-  const int ng = single ? 1 : ws_groups(dm);
-  return (int64_t)dm.C * ng * nchunk * 2 * 32 * (N1max + kNL);
-}
-
-cudaError_t launch_ws_images(const Dims& dm, int single, const float* WT, const float* mu32, const float* ipsi32,
-                             const int* g, const int* gcnt, float* img, cudaStream_t s) {
-  const int Hp = ws_hp(dm.H);
-  const int qg = single ? 1 : std::max(1, std::min(std::min(dm.G, kNL), (256 - kNL) / Hp));
-  const int N1max = kNL + ((qg * Hp + 15) / 16) * 16;
-  k_build_images<<<sm_count() * 8, 256, 0, s>>>(dm, Hp, qg, ws_groups(dm), N1max, single, WT, mu32, ipsi32, g,
-                                                 gcnt, img);
-  return cudaGetLastError();
-}
+int ws_hp(int H) { return H <= 8 ? 8 : H <= 16 ? 16 : H <= 32 ? 32 : 64; }
 
 int ws_groups(const Dims& dm) {
-  const int Hp = ws_hp(dm.H);
-  const int qg = std::max(1, std::min(std::min(dm.G, kNL), (256 - kNL) / Hp));
+  const int qg = ws_qg(dm, 0);
   return (dm.G + qg - 1) / qg;
-}
-
-cudaError_t launch_ws_blocks(const Dims& dm, int single, const float* mu32, const float* ipsi32,
-                             const int* g, const int* gcnt, float* blk, cudaStream_t s) {
-  const int Hp = ws_hp(dm.H);
-  const int qg = std::max(1, std::min(std::min(dm.G, kNL), (256 - kNL) / Hp));
-  k_build_blocks<<<sm_count() * 8, 256, 0, s>>>(dm, qg, ws_groups(dm), single, mu32, ipsi32, g, gcnt, blk);
-  return cudaGetLastError();
 }
 
 bool score_ws_supported(const Dims& dm) { return dm.D <= kMaxD && dm.H <= 64 && dm.G <= 64; }
 
-int ws_hp(int H) { return H <= 8 ? 8 : H <= 16 ? 16 : H <= 32 ? 32 : 64; }
+int64_t ws_image_halves(const Dims& dm, int single) {
+  const int nchunk = (dm.D + kKC - 1) / kKC;
+  const int ng = single ? 1 : ws_groups(dm);
+  return (int64_t)dm.C * ng * nchunk * 2 * 64 * (ws_n1max(dm, single) + kNL);
+}
+int64_t ws_scale_floats(const Dims& dm, int single) {
+  const int ng = single ? 1 : ws_groups(dm);
+  return (int64_t)dm.C * ng * (ws_n1max(dm, single) + kNL);
+}
+int64_t ws_record_floats(const Dims& dm, int single) {
+  return (int64_t)dm.C * (single ? 1 : dm.G) * rec_stride(ws_hp(dm.H));
+}
 
-cudaError_t launch_ws_prep(const Dims& dm, const float* WT, float* WTS, cudaStream_t s) {
-  const int Hp = ws_hp(dm.H);
-  k_build_wts<<<sm_count() * 8, 256, 0, s>>>(dm, Hp, WT, WTS);
+cudaError_t launch_ws_images(const Dims& dm, int single, const float* WT, const float* mu32, const float* ipsi32,
+                             const int* g, const int* gcnt, void* img, float* bscl, cudaStream_t s) {
+  k_build_images<<<sm_count() * 8, 256, 0, s>>>(dm, ws_hp(dm.H), ws_qg(dm, single), ws_groups(dm),
+                                                ws_n1max(dm, single), single, WT, mu32, ipsi32, g, gcnt,
+                                                static_cast<__half*>(img), bscl);
   return cudaGetLastError();
 }
 
-cudaError_t launch_anchor_consts(const Dims& dm, const float* WT, const float* mu32, const float* ipsi32,
-                                 const int* g, const int* gcnt, float* acst, cudaStream_t s) {
-  const int Hp = ws_hp(dm.H);
-  k_anchor_consts<<<sm_count() * 8, 256, 0, s>>>(dm, Hp, WT, mu32, ipsi32, g, gcnt, acst);
+cudaError_t launch_ws_records(const Dims& dm, int single, const float* WT, const float* mu32, const float* ipsi32,
+                              const double* kconst, const int* g, const int* gcnt, const float* scl, float* rec,
+                              cudaStream_t s) {
+  k_build_records<<<sm_count() * 8, 256, 0, s>>>(dm, ws_hp(dm.H), ws_qg(dm, single), ws_groups(dm),
+                                                 ws_n1max(dm, single), single, WT, mu32, ipsi32, kconst, g, gcnt,
+                                                 scl, rec);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rowmax(int64_t N, int D, const float* X, float* xmax, cudaStream_t s) {
+  k_rowmax<<<sm_count() * 8, 256, 0, s>>>(N, D, X, xmax);
   return cudaGetLastError();
 }
 
@@ -896,35 +848,29 @@ unsigned long long* g_ws_prof = nullptr;  // set by vmfa_diag_scorer_cycles
 int g_ws_dbg = 0;                          // diagnostics flags (enable >> 1)
 constexpr int kProfWords = 16 + 8 * kTraceEvents;
 
-cudaError_t launch_score_ws(int mode, const ScoreArgs& s, const float* WTS, const float* mu32,
-                            const float* ipsi32, const float* acst, const float* lblk, const float* cblk,
-                            const float* img, int4* jobs, cudaStream_t st) {
+cudaError_t launch_score_ws(int mode, const ScoreArgs& s, const WsOperands& op, int4* jobs, cudaStream_t st) {
   WsArgs a{};
   a.dm = s.dm;
   a.mode = mode;
   a.Hp = ws_hp(s.dm.H);
-  const int ncomp_max = mode == kModeAnchor ? s.dm.G : 1;
-  a.qg = std::max(1, std::min(std::min(ncomp_max, kNL), (256 - kNL) / a.Hp));
-  a.N1max = kNL + ((a.qg * a.Hp + 15) / 16) * 16;
+  const int single = mode == kModeAnchor ? 0 : 1;
+  a.qg = ws_qg(s.dm, single);
+  a.N1max = ws_n1max(s.dm, single);
   const int cols = a.N1max + kNL;
   a.TB = cols <= 32 ? 32 : cols <= 64 ? 64 : cols <= 128 ? 128 : 256;
   a.nacc = (2 * a.TB + 2 * 128 <= 512) ? 2 : 1;  // A stages use 2 x 128 TMEM columns
   const uint32_t need = a.nacc * a.TB + 2 * 128;
   a.tmem_cols = need <= 256 ? 256 : 512;
   a.stage_bytes = static_cast<uint32_t>(2 * 128 * (a.N1max + kNL));
-  // B ring: as deep as ~200 KB of shared memory allows
   // shared memory: B ring (as deep as fits, >= 2) + the producers' X ring
   a.nbstage = std::max(2, std::min(kMaxNB, static_cast<int>((200u * 1024u - kXRingBytes) / a.stage_bytes)));
   const size_t dyn = static_cast<size_t>(a.nbstage) * a.stage_bytes + kXRingBytes + 1024;
   a.X = s.X;
-  a.WTS = WTS;
-  a.mu32 = mu32;
-  a.ipsi32 = ipsi32;
-  a.kconst = s.kconst;
-  a.acst = acst;
-  a.lblk = lblk;
-  a.cblk = cblk;
-  a.img = img;
+  a.xmax = op.xmax;
+  a.mumax = op.mumax;
+  a.mu32 = op.mu32;
+  a.rec = single ? op.srec : op.brec;
+  a.img = static_cast<const __half*>(single ? op.simg : op.bimg);
   a.ngroups = ws_groups(s.dm);
   a.jobs = jobs;
   a.itemoff = s.itemoff;
@@ -934,7 +880,7 @@ cudaError_t launch_score_ws(int mode, const ScoreArgs& s, const float* WTS, cons
   a.out = s.out;
   a.prof = g_ws_prof;
   a.dbg = g_ws_prof ? g_ws_dbg : 0;
-  k_build_jobs<<<(s.dm.C + 255) / 256, 256, 0, st>>>(s.dm.C, mode, s.dm.G, s.off, s.itemoff, s.gcnt, jobs);
+  k_build_jobs<<<(s.dm.C + 255) / 256, 256, 0, st>>>(s.dm.C, mode, s.off, s.itemoff, s.gcnt, jobs);
   auto go = [&](auto kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn));
     kern<<<sm_count(), kThreads, dyn, st>>>(a);
@@ -951,7 +897,8 @@ cudaError_t launch_score_ws(int mode, const ScoreArgs& s, const float* WTS, cons
 
 }  // namespace vmfa_b200
 
-// Diagnostics: per-role cycle counters of the warp-specialised scorer.
+// Diagnostics: per-role cycle counters and a CTA-0 timeline of the
+// warp-specialised scorer (enable bit 0; bits 1.. select debug variants).
 extern "C" int vmfa_diag_scorer_cycles(int enable, unsigned long long* out, int n) {
   using namespace vmfa_b200;
   g_ws_dbg = enable >> 1;

@@ -19,8 +19,8 @@ s.upload_params(p)
 s.upload_state(st)
 for it in range(4):
     s.iterate(0, it)
-names = ["P wait acc", "P job sync", "P wait stage", "P build(rest)", "M wait acc", "M wait full", "M issue",
-         "E wait", "E work", "P split(+ld)", "P tmem st"]
+names = ["P wait acc", "P job sync", "P wait stage", "P wait rows", "M wait acc", "M wait full", "M issue",
+         "E wait", "E work", "P split", "P tmem st"]
 lib().vmfa_diag_scorer_cycles(1, None, 0)
 out = np.zeros(16, np.uint64)
 s.profile(True)
