@@ -129,6 +129,11 @@ struct vmfa_ctx {
   unsigned long long* st_model = nullptr;
   int* n_empty = nullptr;
   bool kinv_for_current_K = false;
+  // the anchor pass of the next E-step already ran (under the current K, g
+  // and parameters) while computing the truncated free energy: LJ's anchor
+  // slots are valid and the next estep_local skips block 1's anchor scoring
+  bool prescored = false;
+  bool lookahead = true;  // VMFA_LOOKAHEAD=0 scores the truncated F with its own pass
   bool have_estep = false;
   // dumps (parity only)
   bool dump = false;
@@ -295,14 +300,47 @@ int run_precompute(vmfa_ctx* x, int* failed) {
   return VMFA_OK;
 }
 
+int ensure_kinv_current(vmfa_ctx* x) {
+  if (x->kinv_for_current_K) return VMFA_OK;
+  const Dims& dm = x->dm;
+  CU(launch_keys_from_i32(x->K, x->keys, dm.N * dm.Cp, x->stream));
+  TRY(csr_by_key(x, x->keys, dm.N * dm.Cp, x->kinv_off, x->kinv_ent, x->kinv_items, x->score_rows));
+  x->kinv_for_current_K = true;
+  return VMFA_OK;
+}
+
+// Block 1's anchor pass: log-joints of every (n, c in U_{a in K(n)} g_a) into
+// the LJ slots, under the current K, g and parameters.
+int score_anchors(vmfa_ctx* x) {
+  const Dims& dm = x->dm;
+  cudaStream_t s = x->stream;
+  TRY(ensure_kinv_current(x));
+  if (x->scorer == 2) {
+    const int tok = x->begin(kFamOther, dm.C);
+    CU(launch_ws_images(dm, 0, x->WT, x->mu32, x->ipsi32, x->g, x->gcnt, x->bimg, x->bscl, s));
+    CU(launch_ws_records(dm, 0, x->WT, x->mu32, x->ipsi32, x->kconst, x->g, x->gcnt, x->bscl, x->brec, s));
+    x->end(tok);
+  }
+  ScoreArgs a = score_args(x);
+  a.off = x->kinv_off;
+  a.ent = x->kinv_ent;
+  a.itemoff = x->kinv_items;
+  a.out = x->LJ;
+  const int tok = x->begin(kFamScoreAnchor, dm.N * dm.Cp);
+  CU(run_score(x, kModeAnchor, a));
+  x->end(tok);
+  return VMFA_OK;
+}
+
 // E-step blocks 1, 2, 4 and the local part of block 3.
 int estep_local(vmfa_ctx* x, uint64_t seed, uint64_t it, int mode, bool exchange) {
   const Dims& dm = x->dm;
   cudaStream_t s = x->stream;
   CU(cudaMemsetAsync(x->st_select, 0, sizeof(int), s));
+  const bool prescored = x->prescored;
+  x->prescored = false;
   // anchor blocks: inverted K (stable counting sort by component)
-  CU(launch_keys_from_i32(x->K, x->keys, dm.N * dm.Cp, s));
-  TRY(csr_by_key(x, x->keys, dm.N * dm.Cp, x->kinv_off, x->kinv_ent, x->kinv_items, x->score_rows));
+  if (!prescored) TRY(ensure_kinv_current(x));
   // extras not already covered by U g_a
   {
     const int tok = x->begin(kFamOther, dm.N);
@@ -310,22 +348,11 @@ int estep_local(vmfa_ctx* x, uint64_t seed, uint64_t it, int mode, bool exchange
     x->end(tok);
   }
   TRY(csr_by_key(x, x->rkey, dm.N, x->ex_off, x->ex_ent, x->ex_items, x->score_rows));
-  // block 1: scoring
-  if (x->scorer == 2) {
-    const int tok = x->begin(kFamOther, dm.C);
-    CU(launch_ws_images(dm, 0, x->WT, x->mu32, x->ipsi32, x->g, x->gcnt, x->bimg, x->bscl, s));
-    CU(launch_ws_records(dm, 0, x->WT, x->mu32, x->ipsi32, x->kconst, x->g, x->gcnt, x->bscl, x->brec, s));
-    x->end(tok);
-  }
+  // block 1: scoring (the anchor pass unless it ran ahead with the last F)
+  if (!prescored) TRY(score_anchors(x));
   {
     ScoreArgs a = score_args(x);
-    a.off = x->kinv_off;
-    a.ent = x->kinv_ent;
-    a.itemoff = x->kinv_items;
     a.out = x->LJ;
-    const int tok = x->begin(kFamScoreAnchor, dm.N * dm.Cp);
-    CU(run_score(x, kModeAnchor, a));
-    x->end(tok);
     a.off = x->ex_off;
     a.ent = x->ex_ent;
     a.itemoff = x->ex_items;
@@ -427,15 +454,6 @@ int estep_finish(vmfa_ctx* x, bool exchange) {
   return VMFA_OK;
 }
 
-int ensure_kinv_current(vmfa_ctx* x) {
-  if (x->kinv_for_current_K) return VMFA_OK;
-  const Dims& dm = x->dm;
-  CU(launch_keys_from_i32(x->K, x->keys, dm.N * dm.Cp, x->stream));
-  TRY(csr_by_key(x, x->keys, dm.N * dm.Cp, x->kinv_off, x->kinv_ent, x->kinv_items, x->score_rows));
-  x->kinv_for_current_K = true;
-  return VMFA_OK;
-}
-
 int stats_local(vmfa_ctx* x) {
   if (!x->have_estep) return fail(VMFA_ERR_INVALID_ARGUMENT, "accumulate_suffstats needs a preceding E-step (responsibilities)");
   TRY(ensure_kinv_current(x));
@@ -462,6 +480,7 @@ int stats_local(vmfa_ctx* x) {
 }
 
 int update_and_precompute(vmfa_ctx* x, int* failed) {
+  x->prescored = false;  // parameters change
   const Dims& dm = x->dm;
   cudaStream_t s = x->stream;
   CU(cudaMemsetAsync(x->st_model, 0xff, sizeof(unsigned long long), s));
@@ -500,19 +519,33 @@ int update_and_precompute(vmfa_ctx* x, int* failed) {
   return run_precompute(x, failed);
 }
 
-int free_energy_local(vmfa_ctx* x) {
+// truncated_free_energy (model.cpp:150-159) under the current parameters.
+// lookahead: run the next E-step's anchor pass now (it needs exactly these K,
+// g and parameters, and scores every (n, c in K(n)) -- anchor c scores itself
+// with the one-component arithmetic) and read F from its self slots; the next
+// estep_local then skips that pass. Otherwise one-component jobs over K.
+int free_energy_local(vmfa_ctx* x, bool lookahead) {
   const Dims& dm = x->dm;
   cudaStream_t s = x->stream;
-  TRY(ensure_kinv_current(x));
-  ScoreArgs a = score_args(x);
-  a.off = x->kinv_off;
-  a.ent = x->kinv_ent;
-  a.itemoff = x->kinv_items;
-  a.out = x->LJK;
-  const int tok = x->begin(kFamScoreTruncF, dm.N * dm.Cp);
-  CU(run_score(x, kModeTruncF, a));
-  CU(launch_lse_rows(x->LJK, dm.N, dm.Cp, x->lse, s));
-  x->end(tok);
+  if (lookahead) {
+    TRY(score_anchors(x));
+    const int tok = x->begin(kFamScoreTruncF, dm.N * dm.Cp);
+    CU(launch_self_slots(dm, x->K, x->g, x->gcnt, x->LJ, x->LJK, s));
+    CU(launch_lse_rows(x->LJK, dm.N, dm.Cp, x->lse, s));
+    x->end(tok);
+    x->prescored = true;
+  } else {
+    TRY(ensure_kinv_current(x));
+    ScoreArgs a = score_args(x);
+    a.off = x->kinv_off;
+    a.ent = x->kinv_ent;
+    a.itemoff = x->kinv_items;
+    a.out = x->LJK;
+    const int tok = x->begin(kFamScoreTruncF, dm.N * dm.Cp);
+    CU(run_score(x, kModeTruncF, a));
+    CU(launch_lse_rows(x->LJK, dm.N, dm.Cp, x->lse, s));
+    x->end(tok);
+  }
   CU(launch_sum_f64(x->lse, dm.N, x->partials, x->scal + 2, s));
   return VMFA_OK;
 }
@@ -573,6 +606,8 @@ int vmfa_ctx_create(vmfa_ctx** out, int device, int C, int D, int H, int Cp, int
   x->L = score_layout(H);
   x->Hp = ws_hp(H);
   {
+    const char* la = std::getenv("VMFA_LOOKAHEAD");
+    x->lookahead = !(la && la[0] == '0');
     const char* sc = std::getenv("VMFA_SCORER");
     const std::string v = sc ? sc : "ws";
     x->scorer = v == "ffma" ? 0 : (v == "tc" ? 1 : 2);
@@ -755,6 +790,7 @@ int vmfa_synchronize(vmfa_ctx* x) {
 
 int vmfa_upload_data(vmfa_ctx* x, const float* X, int64_t row_begin, int64_t rows) {
   TRY(check_ctx(x));
+  x->prescored = false;
   if (!X || row_begin < 0 || rows < 0 || row_begin + rows > x->dm.N)
     return fail(VMFA_ERR_INVALID_ARGUMENT, "vmfa_upload_data: row range outside the shard");
   CU(cudaMemcpyAsync(x->X + row_begin * x->dm.D, X, sizeof(float) * rows * x->dm.D,
@@ -766,6 +802,7 @@ int vmfa_upload_data(vmfa_ctx* x, const float* X, int64_t row_begin, int64_t row
 
 int vmfa_set_floor(vmfa_ctx* x, const double* floor) {
   TRY(check_ctx(x));
+  x->prescored = false;
   if (!floor) return fail(VMFA_ERR_INVALID_ARGUMENT, "floor is null");
   CU(cudaMemcpyAsync(x->floor, floor, sizeof(double) * x->dm.D, cudaMemcpyHostToDevice, x->stream));
   CU(cudaStreamSynchronize(x->stream));
@@ -775,6 +812,7 @@ int vmfa_set_floor(vmfa_ctx* x, const double* floor) {
 int vmfa_upload_params(vmfa_ctx* x, const double* pi, const double* mu, const double* lambda,
                        const double* dnoise) {
   TRY(check_ctx(x));
+  x->prescored = false;
   if (!pi || !mu || !lambda || !dnoise) return fail(VMFA_ERR_INVALID_ARGUMENT, "null parameter array");
   const size_t C = x->dm.C, D = x->dm.D, H = x->dm.H;
   cudaStream_t s = x->stream;
@@ -800,6 +838,7 @@ int vmfa_download_params(vmfa_ctx* x, double* pi, double* mu, double* lambda, do
 
 int vmfa_precompute(vmfa_ctx* x, int* failed) {
   TRY(check_ctx(x));
+  x->prescored = false;
   return run_precompute(x, failed);
 }
 
@@ -834,6 +873,7 @@ int vmfa_download_caches(vmfa_ctx* x, double* U, double* Lmat, double* V, double
 
 int vmfa_upload_state(vmfa_ctx* x, const int32_t* K, const int32_t* g, const int32_t* g_count) {
   TRY(check_ctx(x));
+  x->prescored = false;
   if (!K || !g || !g_count) return fail(VMFA_ERR_INVALID_ARGUMENT, "null state array");
   const Dims& dm = x->dm;
   // structural validation (VarState::validate, estep.cpp:15-68) on the host copy
@@ -1032,7 +1072,7 @@ int vmfa_update_params(vmfa_ctx* x, int* failed) {
 
 int vmfa_truncated_free_energy(vmfa_ctx* x, double* F) {
   TRY(check_ctx(x));
-  TRY(free_energy_local(x));
+  TRY(free_energy_local(x, false));
   double sc[4];
   TRY(read_scalars(x, sc));
   if (F) *F = sc[2];
@@ -1055,7 +1095,7 @@ int vmfa_iterate(vmfa_ctx* x, uint64_t seed, uint64_t iteration, int mode, vmfa_
   const int r = update_and_precompute(x, &failed);
   if (rep) rep->failed_component = failed;
   if (r != VMFA_OK) return r;
-  TRY(free_energy_local(x));
+  TRY(free_energy_local(x, x->lookahead));
   CU(launch_count_empty(x->pi, x->dm.C, x->n_empty, x->stream));
   double sc[4];
   int ne = 0;
@@ -1124,7 +1164,7 @@ int vmfa_phase_update(vmfa_ctx* x, int* failed) {
 }
 int vmfa_phase_free_energy_local(vmfa_ctx* x) {
   TRY(check_ctx(x));
-  TRY(free_energy_local(x));
+  TRY(free_energy_local(x, x->lookahead));
   CU(cudaStreamSynchronize(x->stream));
   return VMFA_OK;
 }

@@ -1506,6 +1506,23 @@ __global__ void k_lse_rows(const float* LJK, int64_t N, int Cp, double* lse) {
   }
 }
 
+// LJK[n][j] = the anchor-pass log-joint of (n, K(n)[j]) under the current
+// parameters: anchor c = K(n)[j] scores itself in slot j*G + pos(c in g_c)
+// (mu_c centring, delta = 0 -- the same arithmetic as a one-component pass).
+__global__ void k_self_slots(Dims dm, const int* K, const int* g, const int* gcnt, const float* LJ, float* LJK) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < dm.N * dm.Cp;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t n = i / dm.Cp;
+    const int j = static_cast<int>(i - n * dm.Cp);
+    const int c = K[i];
+    const int* gc = g + (int64_t)c * dm.G;
+    int pos = 0;
+    for (int t = 0; t < gcnt[c]; ++t)
+      if (gc[t] == c) pos = t;
+    LJK[i] = LJ[n * dm.SL + j * dm.G + pos];
+  }
+}
+
 constexpr int kSumBlocks = 296;
 // Two-stage deterministic sum: fixed contiguous segments per CTA, fixed tree.
 __global__ void __launch_bounds__(256) k_sum_stage1(const double* v, int64_t n, double* partials) {
@@ -1734,6 +1751,11 @@ cudaError_t launch_precompute(const PrecompArgs& a, cudaStream_t s) {
 cudaError_t launch_caches_full(const Dims& dm, const double* lam, const double* psi, const double* R,
                                double* U, double* V, double* ipsi, cudaStream_t s) {
   k_caches_full<<<min(dm.C, sm_count() * 8), 128, 0, s>>>(dm, lam, psi, R, U, V, ipsi);
+  return cudaGetLastError();
+}
+cudaError_t launch_self_slots(const Dims& dm, const int* K, const int* g, const int* gcnt, const float* LJ,
+                              float* LJK, cudaStream_t s) {
+  k_self_slots<<<grid_for(dm.N * dm.Cp, 256, 8192), 256, 0, s>>>(dm, K, g, gcnt, LJ, LJK);
   return cudaGetLastError();
 }
 cudaError_t launch_lse_rows(const float* LJK, int64_t N, int Cp, double* lse, cudaStream_t s) {

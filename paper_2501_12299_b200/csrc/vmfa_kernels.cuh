@@ -196,6 +196,8 @@ cudaError_t launch_caches_full(const Dims& dm, const double* lam, const double* 
                                const double* R, double* U, double* V, double* ipsi,
                                cudaStream_t s);
 cudaError_t launch_lse_rows(const float* LJK, int64_t N, int Cp, double* lse, cudaStream_t s);
+cudaError_t launch_self_slots(const Dims& dm, const int* K, const int* g, const int* gcnt, const float* LJ,
+                              float* LJK, cudaStream_t s);
 cudaError_t launch_sum_f64(const double* v, int64_t n, double* partials, double* out,
                            cudaStream_t s);
 cudaError_t launch_sum_i32(const int* v, int64_t n, unsigned long long* out, cudaStream_t s);

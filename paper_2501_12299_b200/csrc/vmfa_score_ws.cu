@@ -51,7 +51,7 @@ constexpr int kEpiWarp0 = 9;
 constexpr int kLoadWarp = 13;
 constexpr int kThreads = (kLoadWarp + 1) * 32;
 constexpr int kMaxNB = 8;             // B ring stages (smem)
-constexpr int kAhead = 2;             // producer prefetch depth (chunks) in the cp.async ring
+constexpr int kAhead = 3;             // producer prefetch depth (chunks) in the cp.async ring
 constexpr int kXSeg = kKC / 2 / 4;    // 16-byte pieces per thread per chunk (32 floats)
 constexpr uint32_t kXSlotBytes = kXSeg * kProdThreads * 16;
 constexpr uint32_t kXRingBytes = (kAhead + 1) * kXSlotBytes;
@@ -373,10 +373,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_ws(WsArgs a) {
     auto wait_x = [&]() {  // all but the newest `ahead` groups landed
       switch (ahead) {
         case 1: asm volatile("cp.async.wait_group 1;" ::: "memory"); break;
-        default: asm volatile("cp.async.wait_group 2;" ::: "memory"); break;
+        case 2: asm volatile("cp.async.wait_group 2;" ::: "memory"); break;
+        default: asm volatile("cp.async.wait_group 3;" ::: "memory"); break;
       }
     };
-    static_assert(kAhead <= 2, "wait_x covers ahead <= 2");
+    static_assert(kAhead <= 3, "wait_x covers ahead <= 3");
     uint32_t sc = 0;  // flat chunk counter
     if (w.valid(total))
       for (int k = 0; k < ahead; ++k) issue_x(n_cur, k, static_cast<uint32_t>(k));
@@ -863,7 +864,7 @@ cudaError_t launch_score_ws(int mode, const ScoreArgs& s, const WsOperands& op, 
   a.tmem_cols = need <= 256 ? 256 : 512;
   a.stage_bytes = static_cast<uint32_t>(2 * 128 * (a.N1max + kNL));
   // shared memory: B ring (as deep as fits, >= 2) + the producers' X ring
-  a.nbstage = std::max(2, std::min(kMaxNB, static_cast<int>((200u * 1024u - kXRingBytes) / a.stage_bytes)));
+  a.nbstage = std::max(2, std::min(kMaxNB, static_cast<int>((208u * 1024u - kXRingBytes) / a.stage_bytes)));
   const size_t dyn = static_cast<size_t>(a.nbstage) * a.stage_bytes + kXRingBytes + 1024;
   a.X = s.X;
   a.xmax = op.xmax;

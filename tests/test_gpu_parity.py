@@ -290,3 +290,31 @@ def test_cpp_mirror_matches_python_path(gpu, tmp_path):
     for r, q in zip(rows, recs):
         assert float(r[1]) == pytest.approx(q["F"], rel=1e-12, abs=0)
     s.close()
+
+
+@pytest.mark.parametrize("scorer", ["ws", "tc"])
+def test_lookahead_free_energy_is_exact(oracle, gpu, scorer, monkeypatch):
+    # the truncated F read from the next E-step's anchor pass (self slots)
+    # equals the one-component pass bit for bit, and the trajectory is unchanged
+    O, V = oracle, gpu
+    monkeypatch.setenv("VMFA_SCORER", scorer)
+    X, _ = gaussian_problem(6000, 48, 24, 3, seed=21)
+    C, H, Cp, G = 40, 3, 3, 6
+    runs = {}
+    for la in ("1", "0"):
+        monkeypatch.setenv("VMFA_LOOKAHEAD", la)
+        p, st, floor, sess = _setup(O, V, X, C, H, Cp, G)
+        sess.variational_e_step(0, 0)
+        F = []
+        for it in range(1, 5):
+            r = sess.iterate(0, it)
+            F.append((r["F"], r["F_estep"], r["joints"]))
+            if it == 2:  # an explicit truncated_free_energy call (own pass) agrees too
+                assert sess.truncated_free_energy() == r["F"]
+        runs[la] = (F, sess.download_state(), sess.download_params())
+        sess.close()
+    (F1, s1, p1), (F0, s0, p0) = runs["1"], runs["0"]
+    assert F1 == F0
+    assert np.array_equal(s1.K, s0.K) and np.array_equal(s1.g, s0.g)
+    for f in ("pi", "mu", "lam", "psi"):
+        assert np.array_equal(getattr(p1, f), getattr(p0, f)), f
