@@ -19,16 +19,16 @@
 // drops only lo*lo. K = 16 per instruction (twice tf32's K = 8) halves the
 // instruction count, and fp16 operands halve the B bytes.
 //
-// Roles (14 warps, one CTA per SM, persistent over the job table):
-//   warps 0-7  A producers: each thread streams its own pieces of a row into
+// Roles (22 warps, one CTA per SM, persistent over the job table):
+//   warps 0-15 A producers: each thread streams its own pieces of a row into
 //              a private cp.async ring kAhead chunks ahead, centres / scales /
 //              splits them and stores the A operands into TMEM (tcgen05.st);
-//   warp  8    MMA issuer (one thread): TS-form tcgen05.mma, A from TMEM, B
+//   warp 16    MMA issuer (one thread): TS-form tcgen05.mma, A from TMEM, B
 //              from shared memory, commits to the stage / accumulator barriers;
-//   warps 9-12 epilogue: stage the job's per-slot records in shared memory,
+//   warps 17-20 epilogue: stage the job's per-slot records in shared memory,
 //              tcgen05.ld a finished accumulator (double buffered), assemble
 //              the log-joints, scatter them to the candidate slots;
-//   warp 13    loader (one thread): per job the anchor mean into s_mu, per
+//   warp 21    loader (one thread): per job the anchor mean into s_mu, per
 //              chunk one bulk copy of the prebuilt B stage image into an
 //              NB-deep ring (few large copies keep many bytes in flight).
 #include <algorithm>
@@ -44,15 +44,17 @@ namespace {
 
 constexpr int kRows = 128;
 constexpr int kKC = 64;               // K chunk: 64 fp16 = one 128-byte swizzle row
-constexpr int kProdWarps = 8;
+constexpr int kProdWarps = 16;        // 4 per TMEM lane quadrant (row gathers scale with issuing warps)
 constexpr int kProdThreads = kProdWarps * 32;
-constexpr int kMmaWarp = 8;
-constexpr int kEpiWarp0 = 9;
-constexpr int kLoadWarp = 13;
+constexpr int kKSplit = kProdWarps / 4;       // K slices of a chunk per row
+constexpr int kElem = 64 / kKSplit;           // x values per producer thread per chunk
+constexpr int kMmaWarp = kProdWarps;
+constexpr int kEpiWarp0 = kProdWarps + 1;
+constexpr int kLoadWarp = kProdWarps + 5;
 constexpr int kThreads = (kLoadWarp + 1) * 32;
 constexpr int kMaxNB = 8;             // B ring stages (smem)
 constexpr int kAhead = 3;             // producer prefetch depth (chunks) in the cp.async ring
-constexpr int kXSeg = kKC / 2 / 4;    // 16-byte pieces per thread per chunk (32 floats)
+constexpr int kXSeg = kElem / 4;      // 16-byte pieces per thread per chunk
 constexpr uint32_t kXSlotBytes = kXSeg * kProdThreads * 16;
 constexpr uint32_t kXRingBytes = (kAhead + 1) * kXSlotBytes;
 constexpr int kMaxD = 1024;
@@ -155,13 +157,21 @@ __device__ __forceinline__ void mma_f16_ts(uint32_t tmem_d, uint32_t tmem_a, uin
       "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(tmem_d),
       "r"(tmem_a), "l"(b), "r"(id), "r"(accum));
 }
-__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* v) {
-  asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
-      "%12, %13, %14, %15, %16};" ::"r"(taddr),
-      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
-      "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
-      : "memory");
+template <int W>
+__device__ __forceinline__ void tmem_st(uint32_t taddr, const uint32_t* v) {
+  static_assert(W == 8 || W == 16, "width");
+  if constexpr (W == 16) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
+        "%12, %13, %14, %15, %16};" ::"r"(taddr),
+        "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
+        "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+        : "memory");
+  } else {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(taddr),
+                 "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+                 : "memory");
+  }
 }
 __device__ __forceinline__ void commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
@@ -337,7 +347,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_ws(WsArgs a) {
     // 32 consecutive x values per chunk through a private cp.async ring
     // (per-thread commit groups, no cross-thread sync), then
     // v = (x - mu_a) 2^k and q = v^2 2^-14 split into fp16 hi / lo pairs.
-    const int ar = 32 * (warp & 3) + lane, ah = warp >> 2;
+    const int ar = 32 * (warp & 3) + lane, ah = warp >> 2;  // row, K slice
     const int ahead = min(kAhead, nchunk);  // prefetch stays within the next job
     const uint32_t xbase = sbase + NB * a.stage_bytes;
     Prof pf{};
@@ -352,7 +362,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_ws(WsArgs a) {
       const uint32_t slot = xbase + (unit % (kAhead + 1)) * kXSlotBytes;
 #pragma unroll
       for (int jj = 0; jj < kXSeg; ++jj) {
-        const int d = ch * kKC + 32 * ah + 4 * jj;
+        const int d = ch * kKC + kElem * ah + 4 * jj;
         const uint32_t dst = slot + (jj * kProdThreads + tid) * 16;
         const float* src = a.X + (int64_t)(n < 0 ? 0 : n) * dm.D + d;
         if (n < 0 || d >= dm.D || (PROF && (a.dbg & 1))) {
@@ -397,9 +407,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_ws(WsArgs a) {
         if (PROF) pf.lap(kPBuild);  // (waiting for the row pieces)
         const int s = static_cast<int>(sc & 1u);
         const uint32_t use = sc >> 1;
-        const int d0 = ch * kKC + 32 * ah;
+        const int d0 = ch * kKC + kElem * ah;
         const uint32_t slot = xbase + (sc % (kAhead + 1)) * kXSlotBytes;
-        uint32_t vh[16], vl[16], qh[16], ql[16];
+        uint32_t vh[kElem / 2], vl[kElem / 2], qh[kElem / 2], ql[kElem / 2];
 #pragma unroll
         for (int jj = 0; jj < kXSeg; ++jj) {
           const int d = d0 + 4 * jj;
@@ -432,11 +442,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_ws(WsArgs a) {
         if (PROF) pf.lap(kPWaitEmpty);
         if (tid == 32) trace(tp, static_cast<int>(sc), 0);
         // operand columns: v hi | v lo | q hi | q lo (32 each); this thread's K half
-        const uint32_t ta = tmem + (static_cast<uint32_t>(32 * (warp & 3)) << 16) + colA + s * 128 + 16 * ah;
-        tmem_st16(ta, vh);
-        tmem_st16(ta + 32, vl);
-        tmem_st16(ta + 64, qh);
-        tmem_st16(ta + 96, ql);
+        const uint32_t ta =
+            tmem + (static_cast<uint32_t>(32 * (warp & 3)) << 16) + colA + s * 128 + (kElem / 2) * ah;
+        tmem_st<kElem / 2>(ta, vh);
+        tmem_st<kElem / 2>(ta + 32, vl);
+        tmem_st<kElem / 2>(ta + 64, qh);
+        tmem_st<kElem / 2>(ta + 96, ql);
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         fence_before();
         __syncwarp();
@@ -550,7 +561,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_ws(WsArgs a) {
     // Each warp stages the job's per-slot records in its own shared-memory
     // block (vector loads, before waiting for the accumulator), then reads
     // them as broadcasts while assembling its 32 rows.
-    constexpr int kEpiBatch = HP >= 32 ? 1 : 32 / HP;  // components per tcgen05.ld batch
+    constexpr int kEpiBatch = HP >= 16 ? 1 : 16 / HP;  // components per tcgen05.ld batch
     constexpr int R = rec_stride(HP);
     const int quad = warp & 3;
     const int r = quad * 32 + lane;
@@ -596,44 +607,61 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_ws(WsArgs a) {
           obase = e;
         }
       }
-      for (int q0 = 0; q0 < nq; q0 += kEpiBatch) {
-        const int nb = min(kEpiBatch, nq - q0);
-        float y[kEpiBatch][HP];
+      // one component's log-joint from |y|^2 (yy), its lin / psi accumulators and record
+      auto finish = [&](int qi, float yy) {
+        const float* rc = srec + qi * R;
+        float linq = 0.f, d2q = 0.f;
 #pragma unroll
-        for (int qi = 0; qi < kEpiBatch; ++qi) {
-          if (qi < nb) {
+        for (int i = 0; i < 16; ++i)
+          if (i == qi) {
+            linq = lin[i];
+            d2q = d2[i];
+          }
+        linq *= invA * rc[3];
+        d2q *= invQ * rc[4];
+        const double kc = static_cast<double>(rc[1]) + static_cast<double>(rc[5]);
+        const double diag = static_cast<double>(d2q) + static_cast<double>(linq) + static_cast<double>(rc[2]);
+        const float lj = static_cast<float>(kc - 0.5 * (diag - static_cast<double>(yy)));
+        if (e >= 0) a.out[obase + (a.mode == kModeAnchor ? qi : 0)] = lj;
+      };
+      if constexpr (HP <= 16) {
+        for (int q0 = 0; q0 < nq; q0 += kEpiBatch) {
+          const int nb = min(kEpiBatch, nq - q0);
+          float y[kEpiBatch][HP];
 #pragma unroll
-            for (int h0 = 0; h0 < HP; h0 += 16) {
-              if constexpr (HP >= 16) tmem_ld_nowait<16>(trow + kNL + (q0 + qi) * HP + h0, y[qi] + h0);
-              else tmem_ld_nowait<8>(trow + kNL + (q0 + qi) * HP + h0, y[qi] + h0);
+          for (int qi = 0; qi < kEpiBatch; ++qi)
+            if (qi < nb) tmem_ld_nowait<HP>(trow + kNL + (q0 + qi) * HP, y[qi]);
+          tmem_wait_ld();
+          pin_regs<kEpiBatch * HP>(&y[0][0]);
+#pragma unroll
+          for (int qi = 0; qi < kEpiBatch; ++qi) {
+            if (qi >= nb) break;
+            const float* rc = srec + (q0 + qi) * R;
+            float yy = 0.f;
+#pragma unroll
+            for (int h = 0; h < HP; ++h) {
+              const float t = y[qi][h] * (invA * rc[8 + HP + h]) - rc[8 + h];
+              yy = fmaf(t, t, yy);
             }
+            finish(q0 + qi, yy);
           }
         }
-        tmem_wait_ld();
-        pin_regs<kEpiBatch * HP>(&y[0][0]);
-#pragma unroll
-        for (int qi = 0; qi < kEpiBatch; ++qi) {
-          if (qi >= nb) break;
-          const float* rc = srec + (q0 + qi) * R;
+      } else {  // wide factors: 16 columns at a time
+        for (int qi = 0; qi < nq; ++qi) {
+          const float* rc = srec + qi * R;
           float yy = 0.f;
+          for (int h0 = 0; h0 < HP; h0 += 16) {
+            float y[16];
+            tmem_ld_nowait<16>(trow + kNL + qi * HP + h0, y);
+            tmem_wait_ld();
+            pin_regs<16>(y);
 #pragma unroll
-          for (int h = 0; h < HP; ++h) {
-            const float t = y[qi][h] * (invA * rc[8 + HP + h]) - rc[8 + h];
-            yy = fmaf(t, t, yy);
-          }
-          float linq = 0.f, d2q = 0.f;
-#pragma unroll
-          for (int i = 0; i < 16; ++i)
-            if (i == q0 + qi) {
-              linq = lin[i];
-              d2q = d2[i];
+            for (int h = 0; h < 16; ++h) {
+              const float t = y[h] * (invA * rc[8 + HP + h0 + h]) - rc[8 + h0 + h];
+              yy = fmaf(t, t, yy);
             }
-          linq *= invA * rc[3];
-          d2q *= invQ * rc[4];
-          const double kc = static_cast<double>(rc[1]) + static_cast<double>(rc[5]);
-          const double diag = static_cast<double>(d2q) + static_cast<double>(linq) + static_cast<double>(rc[2]);
-          const float lj = static_cast<float>(kc - 0.5 * (diag - static_cast<double>(yy)));
-          if (e >= 0) a.out[obase + (a.mode == kModeAnchor ? q0 + qi : 0)] = lj;
+          }
+          finish(qi, yy);
         }
       }
       fence_before();
