@@ -657,6 +657,33 @@ __global__ void __launch_bounds__(kGupdThreads) k_gselect_dense(Dims dm, long lo
   }
 }
 
+// ---------------------------------------------------------------- mbarrier / bulk-copy helpers
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void xbar_init(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(bar)) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void xbar_expect(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void xbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}\n"
+        : "=r"(ok)
+        : "r"(smem_addr(bar)), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+__device__ __forceinline__ void bulk_row(uint32_t dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(smem_addr(bar))
+               : "memory");
+}
+
 // ---------------------------------------------------------------- K5: sufficient statistics
 // CTA per component a over its K-pairs (n, q) in ascending (n, j) order
 // (accumulate_point, mstep.cpp:47-67): mz = V_a (x - mu_a) (fp32 dot products),
@@ -693,6 +720,7 @@ __global__ void __launch_bounds__(kStatsThreads, 2) k_stats(StatsArgs a, const i
   __shared__ int s_e[2][kStatsBatch];
   __shared__ double s_red[kStatsThreads / 32];
   __shared__ double s_accE[kStatsThreads];  // E entry of thread tid (fp64)
+  __shared__ uint64_t s_xbar[2];             // row-batch arrival (bulk copies, D % 4 == 0)
   const Dims dm = a.dm;
   const int H = dm.H, H1 = H + 1, D = dm.D;
   const int XS = (D + 3) / 4 * 4 + kXPad;
@@ -725,6 +753,12 @@ __global__ void __launch_bounds__(kStatsThreads, 2) k_stats(StatsArgs a, const i
   const int dsl = ((D + 7) / 8 + 3) / 4 * 4;  // phase (i) dims per warp, multiple of 4
   const int dw0 = warp * dsl, dw1 = min(D, dw0 + dsl);
   const int total = __ldg(itemoff + dm.C);
+  if (tid == 0) {
+    xbar_init(&s_xbar[0]);
+    xbar_init(&s_xbar[1]);
+  }
+  __syncthreads();
+  uint32_t xuse[2] = {0u, 0u};  // completed phases per row buffer (same in every thread)
   for (int item = blockIdx.x; item < total; item += gridDim.x) {
     const int c = find_item(itemoff, dm.C, item);
     const int r0 = a.off[c] + (item - itemoff[c]) * rows_per_item;
@@ -771,14 +805,15 @@ __global__ void __launch_bounds__(kStatsThreads, 2) k_stats(StatsArgs a, const i
     auto issue_rows = [&](int buf) {
       float* dst = s_x + (int64_t)buf * kStatsBatch * XS;
       if (vec) {
-        const int D4 = D >> 2;
-        for (int i = tid; i < kStatsBatch * D4; i += kStatsThreads) {
-          const int r = i / D4, f = i - r * D4;
-          const int e = s_e[buf][r];
-          if (e < 0) continue;
-          const float* src = a.X + (int64_t)(e / dm.Cp) * D + 4 * f;
-          const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(dst + (int64_t)r * XS + 4 * f));
-          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(src) : "memory");
+        // one bulk copy per row, issued by the 32 lanes of warp 0 in parallel
+        // (many copies in flight: far above what 16-byte cp.async sustains)
+        if (warp == 0) {
+          const int e = s_e[buf][lane];
+          const unsigned valid = __ballot_sync(kFull, e >= 0);
+          if (lane == 0) xbar_expect(&s_xbar[buf], static_cast<uint32_t>(__popc(valid)) * D * 4u);
+          __syncwarp();
+          if (e >= 0)
+            bulk_row(smem_addr(dst + (int64_t)lane * XS), a.X + (int64_t)(e / dm.Cp) * D, D * 4u, &s_xbar[buf]);
         }
       } else {
         for (int i = tid; i < kStatsBatch * D; i += kStatsThreads) {
@@ -805,15 +840,16 @@ __global__ void __launch_bounds__(kStatsThreads, 2) k_stats(StatsArgs a, const i
           __syncthreads();
           issue_rows(0);
         }
-        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        if (!vec) asm volatile("cp.async.wait_group 0;" ::: "memory");
       } else if (bi + 1 < nbat) {
         stage_ids(bi + 1, buf ^ 1);
         __syncthreads();
         issue_rows(buf ^ 1);
-        asm volatile("cp.async.wait_group 1;" ::: "memory");
+        if (!vec) asm volatile("cp.async.wait_group 1;" ::: "memory");
       } else {
-        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        if (!vec) asm volatile("cp.async.wait_group 0;" ::: "memory");
       }
+      if (vec) xbar_wait(&s_xbar[buf], xuse[buf]++ & 1u);
       __syncthreads();
       const float* xb = s_x + (int64_t)buf * kStatsBatch * XS;
       // (i) partial mz over this warp's dimension slice, lane = row

@@ -60,6 +60,41 @@ __global__ void k(const float4* X, int64_t nrows, int rowb, int rows_per_warp, f
         }
       }
     }
+  } else if (MODE == 3) {
+    // every lane issues one row's bulk copy: a batch of 32 rows per warp, U batches in flight
+    const uint32_t base = smem_u32(sm) + warp * U * 32 * rowb;
+    if (lane == 0)
+      for (int u = 0; u < U; ++u) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar[warp][u])));
+    __syncwarp();
+    const int nb = rows_per_warp / 32;
+    for (int r = 0; r < nb + U; ++r) {
+      if (r >= U) {
+        const int u = r % U;
+        const uint32_t ph = ((r - U) / U) & 1;
+        uint32_t ok = 0;
+        do {
+          asm volatile("{.reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p;}"
+                       : "=r"(ok) : "r"(smem_u32(&bar[warp][u])), "r"(ph));
+        } while (!ok);
+        const uint32_t src = base + u * 32 * rowb + lane * rowb;
+        for (int o = 0; o < f4; o += 8) {
+          float a, b, c, d;
+          asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(a), "=f"(b), "=f"(c), "=f"(d) : "r"(src + o * 16));
+          acc += a + b + c + d;
+        }
+        __syncwarp();
+      }
+      if (r < nb) {
+        const int u = r % U;
+        if (lane == 0)
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar[warp][u])), "r"(32 * rowb) : "memory");
+        __syncwarp();
+        const int64_t row = hash(gw * 1000003 + r * 32 + lane) % nrows;
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(base + u * 32 * rowb + lane * rowb),
+                     "l"(X + row * f4), "r"(rowb), "r"(smem_u32(&bar[warp][u])) : "memory");
+      }
+      __syncwarp();
+    }
   } else {
     const uint32_t base = smem_u32(sm) + warp * U * rowb;
     if (lane == 0)
@@ -128,6 +163,10 @@ int main() {
   run(k<1, 8>, 1, 8, 256, 8 * 8 * 1024);
   run(k<1, 8>, 1, 8, 512, 16 * 8 * 1024);
   run(k<1, 4>, 1, 4, 1024, 32 * 4 * 1024);
+  run(k<3, 2>, 3, 2, 64, 2 * 2 * 32 * 1024);
+  run(k<3, 2>, 3, 2, 96, 3 * 2 * 32 * 1024);
+  run(k<3, 3>, 3, 3, 64, 2 * 3 * 32 * 1024);
+  run(k<3, 1>, 3, 1, 192, 6 * 1 * 32 * 1024);
   run(k<2, 4>, 2, 4, 256, 8 * 4 * 1024);
   run(k<2, 8>, 2, 8, 256, 8 * 8 * 1024);
   run(k<2, 12>, 2, 12, 512, 16 * 12 * 1024);
