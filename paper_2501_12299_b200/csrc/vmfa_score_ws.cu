@@ -21,7 +21,7 @@
 //
 // Roles (22 warps, one CTA per SM, persistent over the job table):
 //   warps 0-15 A producers: each thread streams its own pieces of a row into
-//              a private cp.async ring kAhead chunks ahead, centres / scales /
+//              a shared ring of row chunks (bulk copies) ahead, centres / scales /
 //              splits them and stores the A operands into TMEM (tcgen05.st);
 //   warp 16    MMA issuer (one thread): TS-form tcgen05.mma, A from TMEM, B
 //              from shared memory, commits to the stage / accumulator barriers;
@@ -53,10 +53,10 @@ constexpr int kEpiWarp0 = kProdWarps + 1;
 constexpr int kLoadWarp = kProdWarps + 5;
 constexpr int kThreads = (kLoadWarp + 1) * 32;
 constexpr int kMaxNB = 8;             // B ring stages (smem)
-constexpr int kAhead = 3;             // producer prefetch depth (chunks) in the cp.async ring
+constexpr int kMaxXSlots = 4;         // X ring slots (row chunks); prefetch depth = slots - 1
 constexpr int kXSeg = kElem / 4;      // 16-byte pieces per thread per chunk
-constexpr uint32_t kXSlotBytes = kXSeg * kProdThreads * 16;
-constexpr uint32_t kXRingBytes = (kAhead + 1) * kXSlotBytes;
+constexpr int kXRow = kKC + 4;        // floats per row chunk in the X ring (padded: conflict-free LDS.128)
+constexpr uint32_t kXSlotBytes = kRows * kXRow * 4;
 constexpr int kMaxD = 1024;
 constexpr int kNL = 16;               // lin rows / psi rows per group (qg <= 16)
 constexpr int kTargetExp = 14;        // operands scaled to |value| <= 2^14
@@ -70,6 +70,7 @@ struct WsArgs {
   int qg;            // components per job (group)
   int N1max;         // 16 + round16(qg * Hp)
   int nbstage;       // B ring depth
+  int xslots;        // X ring slots (2..kMaxXSlots)
   int nacc;          // accumulator buffers in TMEM (2 when they fit beside the A stages)
   uint32_t tmem_cols;
   uint32_t TB;       // TMEM columns per accumulator buffer
@@ -298,6 +299,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_ws(WsArgs a) {
   __shared__ uint64_t s_afull[2], s_aempty[2], s_tfull[2], s_tempty[2];
   __shared__ uint64_t s_bfull[kMaxNB], s_bempty[kMaxNB];
   __shared__ uint64_t s_mufull[2], s_muempty[2];
+  __shared__ uint64_t s_xfull[kMaxXSlots][4], s_xempty[kMaxXSlots][4];  // X ring, per lane quadrant
   __shared__ __align__(16) float s_mu[2][kMaxD + 8];
   __shared__ int s_muoff[2];
   __shared__ __align__(16) float s_rec[4 * qg_max(HP) * rec_stride(HP)];  // epilogue records, per warp
@@ -323,6 +325,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_ws(WsArgs a) {
       mbar_init(&s_bfull[i], 1);
       mbar_init(&s_bempty[i], 1);
     }
+    for (int i = 0; i < kMaxXSlots; ++i)
+      for (int q = 0; q < 4; ++q) {
+        mbar_init(&s_xfull[i][q], 1);
+        mbar_init(&s_xempty[i][q], kKSplit);
+      }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
@@ -343,12 +350,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_ws(WsArgs a) {
 
   if (warp < kProdWarps) {
     // ============================================================ A producers
-    // thread = (row ar of the 128-row block, K half ah of each 64-wide chunk):
-    // 32 consecutive x values per chunk through a private cp.async ring
-    // (per-thread commit groups, no cross-thread sync), then
-    // v = (x - mu_a) 2^k and q = v^2 2^-14 split into fp16 hi / lo pairs.
+    // thread = (row ar of the 128-row block, K slice ah of each 64-wide chunk).
+    // Rows arrive in a shared-memory ring of row chunks (64 floats per row,
+    // padded rows) slots - 1 chunks ahead and across job borders: in each TMEM
+    // lane quadrant the slice-0 warp issues one bulk copy per row (32 lanes in
+    // parallel keep many copies in flight), and the quadrant's four warps
+    // release the slot after reading it. Then v = (x - mu_a) 2^k and
+    // q = v^2 2^-14 are split into fp16 hi / lo pairs and stored to TMEM.
     const int ar = 32 * (warp & 3) + lane, ah = warp >> 2;  // row, K slice
-    const int ahead = min(kAhead, nchunk);  // prefetch stays within the next job
+    const int quad = warp & 3;
+    const int XS = a.xslots;
+    const int ahead = min(XS - 1, nchunk);
     const uint32_t xbase = sbase + NB * a.stage_bytes;
     Prof pf{};
     if (PROF) pf.start();
@@ -357,39 +369,23 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_ws(WsArgs a) {
     wn.advance(a.jobs, a.qg, total);
     int n_cur = w.valid(total) ? job_row(a, w.J, ar) : -1;
     int n_nxt = wn.valid(total) ? job_row(a, wn.J, ar) : -1;
-    const bool vec = (dm.D & 3) == 0;
+    // issue unit `unit` (chunk ch of row n) of this quadrant (slice-0 warps only)
     auto issue_x = [&](int n, int ch, uint32_t unit) {
-      const uint32_t slot = xbase + (unit % (kAhead + 1)) * kXSlotBytes;
-#pragma unroll
-      for (int jj = 0; jj < kXSeg; ++jj) {
-        const int d = ch * kKC + kElem * ah + 4 * jj;
-        const uint32_t dst = slot + (jj * kProdThreads + tid) * 16;
-        const float* src = a.X + (int64_t)(n < 0 ? 0 : n) * dm.D + d;
-        if (n < 0 || d >= dm.D || (PROF && (a.dbg & 1))) {
-          st4(dst, 0, 0, 0, 0);
-        } else if (vec) {
-          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
-        } else {
-          for (int k = 0; k < 4; ++k) {
-            if (d + k < dm.D)
-              asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst + 4 * k), "l"(src + k) : "memory");
-            else
-              asm volatile("st.shared.b32 [%0], %1;" ::"r"(dst + 4 * k), "r"(0u) : "memory");
-          }
-        }
-      }
-      asm volatile("cp.async.commit_group;" ::: "memory");
+      const int sl = static_cast<int>(unit % XS);
+      const uint32_t use = unit / XS;
+      if (use >= 1) mbar_wait(&s_xempty[sl][quad], (use - 1) & 1u);
+      const int d0 = ch * kKC;
+      const uint32_t bytes = static_cast<uint32_t>(min(kKC, dm.D - d0)) * 4u;
+      const bool valid = n >= 0 && d0 < dm.D && !(PROF && (a.dbg & 1));
+      const unsigned vm = __ballot_sync(0xffffffffu, valid);
+      if (lane == 0) mbar_arrive_expect_tx(&s_xfull[sl][quad], static_cast<uint32_t>(__popc(vm)) * bytes);
+      __syncwarp();
+      if (valid)
+        bulk_copy(xbase + sl * kXSlotBytes + ar * (kXRow * 4), a.X + (int64_t)n * dm.D + d0, bytes,
+                  &s_xfull[sl][quad]);
     };
-    auto wait_x = [&]() {  // all but the newest `ahead` groups landed
-      switch (ahead) {
-        case 1: asm volatile("cp.async.wait_group 1;" ::: "memory"); break;
-        case 2: asm volatile("cp.async.wait_group 2;" ::: "memory"); break;
-        default: asm volatile("cp.async.wait_group 3;" ::: "memory"); break;
-      }
-    };
-    static_assert(kAhead <= 3, "wait_x covers ahead <= 3");
     uint32_t sc = 0;  // flat chunk counter
-    if (w.valid(total))
+    if (w.valid(total) && ah == 0)
       for (int k = 0; k < ahead; ++k) issue_x(n_cur, k, static_cast<uint32_t>(k));
     int jb = 0;
     while (w.valid(total)) {
@@ -398,17 +394,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_ws(WsArgs a) {
       mbar_wait(&s_mufull[mslot], (jb >> 1) & 1);
       const float* mu_s = s_mu[mslot] + s_muoff[mslot];
       for (int ch = 0; ch < nchunk; ++ch, ++sc) {
-        {  // prefetch chunk sc + ahead (this job or the next)
+        if (ah == 0) {  // prefetch chunk sc + ahead (this job or the next)
           const int c2 = ch + ahead;
           if (c2 < nchunk) issue_x(n_cur, c2, sc + ahead);
           else issue_x(wn.valid(total) ? n_nxt : -1, c2 - nchunk, sc + ahead);
         }
-        wait_x();
+        const int xs = static_cast<int>(sc % XS);
+        mbar_wait(&s_xfull[xs][quad], (sc / XS) & 1u);
         if (PROF) pf.lap(kPBuild);  // (waiting for the row pieces)
         const int s = static_cast<int>(sc & 1u);
         const uint32_t use = sc >> 1;
         const int d0 = ch * kKC + kElem * ah;
-        const uint32_t slot = xbase + (sc % (kAhead + 1)) * kXSlotBytes;
+        const uint32_t xrow = xbase + xs * kXSlotBytes + ar * (kXRow * 4) + kElem * ah * 4;
         uint32_t vh[kElem / 2], vl[kElem / 2], qh[kElem / 2], ql[kElem / 2];
 #pragma unroll
         for (int jj = 0; jj < kXSeg; ++jj) {
@@ -416,16 +413,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_ws(WsArgs a) {
           float xv[4];
           asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
                        : "=f"(xv[0]), "=f"(xv[1]), "=f"(xv[2]), "=f"(xv[3])
-                       : "r"(slot + (jj * kProdThreads + tid) * 16)
+                       : "r"(xrow + jj * 16)
                        : "memory");
-          float mv[4];
-          if (vec) {  // (D % 4 == 0: the mean window starts 16-byte aligned)
-            const float4 m4 = *reinterpret_cast<const float4*>(mu_s + d);
-            mv[0] = m4.x, mv[1] = m4.y, mv[2] = m4.z, mv[3] = m4.w;
-          } else {
-#pragma unroll
-            for (int k = 0; k < 4; ++k) mv[k] = mu_s[d + k];
-          }
+          const float4 m4 = *reinterpret_cast<const float4*>(mu_s + d);  // (D % 4 == 0: aligned window)
+          const float mv[4] = {m4.x, m4.y, m4.z, m4.w};
           float v[4], q[4];
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
@@ -437,11 +428,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_ws(WsArgs a) {
           split2(q[0], q[1], qh[2 * jj], ql[2 * jj]);
           split2(q[2], q[3], qh[2 * jj + 1], ql[2 * jj + 1]);
         }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&s_xempty[xs][quad]);  // this warp is done with the row slot
         if (PROF) pf.lap(kPSplit);
         if (use >= 1) mbar_wait(&s_aempty[s], (use - 1) & 1u);
         if (PROF) pf.lap(kPWaitEmpty);
         if (tid == 32) trace(tp, static_cast<int>(sc), 0);
-        // operand columns: v hi | v lo | q hi | q lo (32 each); this thread's K half
+        // operand columns: v hi | v lo | q hi | q lo (32 each); this thread's K slice
         const uint32_t ta =
             tmem + (static_cast<uint32_t>(32 * (warp & 3)) << 16) + colA + s * 128 + (kElem / 2) * ah;
         tmem_st<kElem / 2>(ta, vh);
@@ -465,7 +458,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_ws(WsArgs a) {
       n_nxt = wn.valid(total) ? job_row(a, wn.J, ar) : -1;
       if (PROF) pf.lap(kPSync);
     }
-    asm volatile("cp.async.wait_all;" ::: "memory");
+    // drain: the slots issued beyond the last chunk (nothing is read from them)
+    if (ah == 0 && sc > 0)
+      for (uint32_t u = sc; u < sc + static_cast<uint32_t>(ahead); ++u)
+        mbar_wait(&s_xfull[u % XS][quad], (u / XS) & 1u);
     if (PROF && a.prof && lane == 0) {
       atomicAdd(a.prof + kPSync, pf.acc[kPSync]);
       atomicAdd(a.prof + kPBuild, pf.acc[kPBuild]);
@@ -836,7 +832,17 @@ int ws_groups(const Dims& dm) {
   return (dm.G + qg - 1) / qg;
 }
 
-bool score_ws_supported(const Dims& dm) { return dm.D <= kMaxD && dm.H <= 64 && dm.G <= 64; }
+bool ws_smem_plan(int Hp, uint32_t stage_bytes, int* xslots, int* nb, size_t* dyn);
+
+bool score_ws_supported(const Dims& dm) {
+  if (dm.D > kMaxD || dm.D % 4 != 0 || dm.H > 64 || dm.G > 64) return false;
+  int xs, nb;
+  size_t dyn;
+  for (int single = 0; single < 2; ++single)
+    if (!ws_smem_plan(ws_hp(dm.H), static_cast<uint32_t>(2 * 128 * (ws_n1max(dm, single) + kNL)), &xs, &nb, &dyn))
+      return false;
+  return true;
+}
 
 int64_t ws_image_halves(const Dims& dm, int single) {
   const int nchunk = (dm.D + kKC - 1) / kKC;
@@ -877,6 +883,24 @@ unsigned long long* g_ws_prof = nullptr;  // set by vmfa_diag_scorer_cycles
 int g_ws_dbg = 0;                          // diagnostics flags (enable >> 1)
 constexpr int kProfWords = 16 + 8 * kTraceEvents;
 
+// Shared-memory plan: X ring slots and B ring stages within the opt-in limit
+// (227 KB minus the kernel's static shared memory). false: does not fit.
+bool ws_smem_plan(int Hp, uint32_t stage_bytes, int* xslots, int* nb, size_t* dyn) {
+  const size_t limit = 227 * 1024;
+  const size_t stat = 2 * (kMaxD + 8) * 4 + 4 * qg_max(Hp) * rec_stride(Hp) * 4 + 1024;  // s_mu, s_rec, barriers
+  const size_t avail = limit - stat - 1024;  // 1024: stage alignment slack
+  for (int xs = kMaxXSlots; xs >= 2; --xs) {
+    const size_t xb = static_cast<size_t>(xs) * kXSlotBytes;
+    if (xb + 2 * stage_bytes > avail) continue;
+    *xslots = xs;
+    *nb = std::min(kMaxNB, static_cast<int>((avail - xb) / stage_bytes));
+    if (*nb > 4 && xs < kMaxXSlots) *nb = 4;
+    *dyn = static_cast<size_t>(*nb) * stage_bytes + xb + 1024;
+    return true;
+  }
+  return false;
+}
+
 cudaError_t launch_score_ws(int mode, const ScoreArgs& s, const WsOperands& op, int4* jobs, cudaStream_t st) {
   WsArgs a{};
   a.dm = s.dm;
@@ -891,9 +915,9 @@ cudaError_t launch_score_ws(int mode, const ScoreArgs& s, const WsOperands& op, 
   const uint32_t need = a.nacc * a.TB + 2 * 128;
   a.tmem_cols = need <= 256 ? 256 : 512;
   a.stage_bytes = static_cast<uint32_t>(2 * 128 * (a.N1max + kNL));
-  // shared memory: B ring (as deep as fits, >= 2) + the producers' X ring
-  a.nbstage = std::max(2, std::min(kMaxNB, static_cast<int>((208u * 1024u - kXRingBytes) / a.stage_bytes)));
-  const size_t dyn = static_cast<size_t>(a.nbstage) * a.stage_bytes + kXRingBytes + 1024;
+  // shared memory: the producers' X ring + the B ring (>= 2 stages each)
+  size_t dyn = 0;
+  if (!ws_smem_plan(a.Hp, a.stage_bytes, &a.xslots, &a.nbstage, &dyn)) return cudaErrorInvalidValue;
   a.X = s.X;
   a.xmax = op.xmax;
   a.mumax = op.mumax;
