@@ -82,6 +82,7 @@ struct vmfa_ctx {
   int Hp = 8;
   float *brec = nullptr, *srec = nullptr;  // scorer epilogue records (anchor slots / components)
   int4* jobs = nullptr;                    // scorer job table (one int4 per 128-row work item)
+  int* qctr = nullptr;                     // statistics work-queue counter
   uint16_t *bimg = nullptr, *simg = nullptr;  // scorer B stage images (fp16; anchor / single)
   float *bscl = nullptr, *sscl = nullptr;     // their row scales
   float *xmax = nullptr, *mumax = nullptr;    // A-row scale bounds
@@ -470,6 +471,7 @@ int stats_local(vmfa_ctx* x) {
   a.E = x->E;
   a.Y = x->Y;
   a.sq = x->sq;
+  a.qctr = x->qctr;
   const int tok = x->begin(kFamStats, x->dm.N * x->dm.Cp);
   size_t tb = x->cub_bytes;
   CU(launch_chunks_from_off(x->kinv_off, x->dm.C, x->stats_rows, 0, x->chunks, x->stream));
@@ -693,6 +695,7 @@ int vmfa_ctx_create(vmfa_ctx** out, int device, int C, int D, int H, int Cp, int
   A(x->part_ent, N);
   A(x->part_items, Cs + 1);
   A(x->stats_items, Cs + 1);
+  A(x->qctr, 1);
   {
     const int64_t pairs = static_cast<int64_t>(N) * Cp;
     const int64_t target = (pairs + sm_count() * 8 - 1) / (sm_count() * 8);

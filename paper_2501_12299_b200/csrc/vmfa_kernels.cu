@@ -759,7 +759,16 @@ __global__ void __launch_bounds__(kStatsThreads, 2) k_stats(StatsArgs a, const i
   }
   __syncthreads();
   uint32_t xuse[2] = {0u, 0u};  // completed phases per row buffer (same in every thread)
-  for (int item = blockIdx.x; item < total; item += gridDim.x) {
+  __shared__ int s_item;
+  // items from a global work queue (dynamic balance; results depend only on the item)
+  auto next_item = [&](int cur) -> int {
+    if (!a.qctr) return cur < 0 ? static_cast<int>(blockIdx.x) : cur + static_cast<int>(gridDim.x);
+    __syncthreads();
+    if (tid == 0) s_item = atomicAdd(a.qctr, 1);
+    __syncthreads();
+    return s_item;
+  };
+  for (int item = next_item(-1); item < total; item = next_item(item)) {
     const int c = find_item(itemoff, dm.C, item);
     const int r0 = a.off[c] + (item - itemoff[c]) * rows_per_item;
     const int r1 = min(a.off[c + 1], r0 + rows_per_item);
@@ -1747,6 +1756,10 @@ cudaError_t launch_stats(const StatsArgs& a, const int* itemoff, int rows_per_it
   const int64_t ps = stats_part_stride(a.dm);
   const int rgrid = min(a.dm.C, sm_count() * 8);
   for (int col0 = 0; col0 < H1; col0 += nh1) {
+    if (a.qctr) {
+      cudaError_t e = cudaMemsetAsync(a.qctr, 0, sizeof(int), s);
+      if (e != cudaSuccess) return e;
+    }
     if (nh1 == 5) stats_pass<5>(a, itemoff, rows_per_item, grid, col0, part, ps, s);
     else if (nh1 == 9) stats_pass<9>(a, itemoff, rows_per_item, grid, col0, part, ps, s);
     else stats_pass<kStatsMaxH1>(a, itemoff, rows_per_item, grid, col0, part, ps, s);

@@ -129,6 +129,7 @@ struct StatsArgs {
   double* E;              // C x (H+1)^2 col-major
   double* Y;              // C x (H+1) x D  (D x (H+1) col-major)
   double* sq;             // C x D
+  int* qctr;              // work-queue counter (zeroed per pass; nullptr: static item order)
 };
 
 struct UpdateArgs {
