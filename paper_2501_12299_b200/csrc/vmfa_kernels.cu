@@ -1083,38 +1083,36 @@ __global__ void __launch_bounds__(256) k_stats_reduce(Dims dm, const int* __rest
                                                       const double* part, int64_t part_stride,
                                                       int kind, int col0, int nh1, int full_e,
                                                       double* Nc, double* E, double* Y, double* sq) {
+  // one thread per output element of every component (coalesced over the
+  // partial rows); items summed in item order (deterministic)
   const int D = dm.D, H1 = dm.H + 1;
-  for (int c = blockIdx.x; c < dm.C; c += gridDim.x) {
-    const int i0 = itemoff[c], i1 = itemoff[c + 1];
+  const int ncols = min(nh1, H1 - col0);
+  const int64_t ny = kind == 1 ? 0 : (int64_t)ncols * D;
+  const int64_t nsq = (kind == 0 && col0 == 0) ? D : 0;
+  const int64_t ne = (kind == 1 || (col0 == 0 && full_e)) ? (int64_t)H1 * H1 : 0;
+  const int64_t per = ny + nsq + ne;
+  (void)Nc;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (int64_t)dm.C * per;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int c = static_cast<int>(t / per);
+    const int64_t k = t - (int64_t)c * per;
+    const int i0 = __ldg(itemoff + c), i1 = __ldg(itemoff + c + 1);
     if (kind == 0 && i1 - i0 == 1) continue;  // written directly by k_stats
-    if (kind == 1) {
-      for (int idx = threadIdx.x; idx < H1 * H1; idx += blockDim.x) {
-        double s = 0.0;
-        for (int it = i0; it < i1; ++it) s += part[(int64_t)it * part_stride + idx];
-        E[(int64_t)c * H1 * H1 + idx] = s;
-      }
-      continue;
+    int64_t src;
+    double* dst;
+    if (k < ny) {
+      src = k;
+      dst = Y + ((int64_t)c * H1 + col0) * D + k;
+    } else if (k < ny + nsq) {
+      src = (int64_t)nh1 * D + (k - ny);
+      dst = sq + (int64_t)c * D + (k - ny);
+    } else {
+      src = kind == 1 ? (k - ny - nsq) : (int64_t)nh1 * D + D + (k - ny - nsq);
+      dst = E + (int64_t)c * H1 * H1 + (k - ny - nsq);
     }
-    const int ncols = min(nh1, H1 - col0);
-    for (int idx = threadIdx.x; idx < ncols * D; idx += blockDim.x) {
-      double s = 0.0;
-      for (int it = i0; it < i1; ++it) s += part[(int64_t)it * part_stride + idx];
-      Y[((int64_t)c * H1 + col0) * D + idx] = s;
-    }
-    if (col0 != 0) continue;
-    const int64_t base = (int64_t)nh1 * D;
-    for (int d = threadIdx.x; d < D; d += blockDim.x) {
-      double s = 0.0;
-      for (int it = i0; it < i1; ++it) s += part[(int64_t)it * part_stride + base + d];
-      sq[(int64_t)c * D + d] = s;
-    }
-    const int64_t eb = base + D;
-    if (full_e)
-      for (int idx = threadIdx.x; idx < H1 * H1; idx += blockDim.x) {
-        double s = 0.0;
-        for (int it = i0; it < i1; ++it) s += part[(int64_t)it * part_stride + eb + idx];
-        E[(int64_t)c * H1 * H1 + idx] = s;
-      }
+    double s = 0.0;
+    for (int it = i0; it < i1; ++it) s += part[(int64_t)it * part_stride + src];
+    *dst = s;
   }
 }
 
@@ -1754,7 +1752,6 @@ cudaError_t launch_stats(const StatsArgs& a, const int* itemoff, int rows_per_it
   const int H1 = a.dm.H + 1;
   const int nh1 = H1 <= 5 ? 5 : (H1 <= 9 ? 9 : kStatsMaxH1);
   const int64_t ps = stats_part_stride(a.dm);
-  const int rgrid = min(a.dm.C, sm_count() * 8);
   for (int col0 = 0; col0 < H1; col0 += nh1) {
     if (a.qctr) {
       cudaError_t e = cudaMemsetAsync(a.qctr, 0, sizeof(int), s);
@@ -1765,14 +1762,14 @@ cudaError_t launch_stats(const StatsArgs& a, const int* itemoff, int rows_per_it
     else stats_pass<kStatsMaxH1>(a, itemoff, rows_per_item, grid, col0, part, ps, s);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    k_stats_reduce<<<rgrid, 256, 0, s>>>(a.dm, itemoff, part, ps, 0, col0, nh1, H1 <= nh1 ? 1 : 0,
-                                         a.Nc, a.E, a.Y, a.sq);
+    k_stats_reduce<<<sm_count() * 8, 256, 0, s>>>(a.dm, itemoff, part, ps, 0, col0, nh1, H1 <= nh1 ? 1 : 0,
+                                                  a.Nc, a.E, a.Y, a.sq);
   }
   if (H1 > nh1) {
     const size_t smem = static_cast<size_t>(kStatsBatch) * H1 * sizeof(double);
     cudaFuncSetAttribute(k_stats_E, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     k_stats_E<<<grid, kStatsThreads, smem, s>>>(a, itemoff, rows_per_item, part, ps);
-    k_stats_reduce<<<rgrid, 256, 0, s>>>(a.dm, itemoff, part, ps, 1, 0, nh1, 1, a.Nc, a.E, a.Y, a.sq);
+    k_stats_reduce<<<sm_count() * 8, 256, 0, s>>>(a.dm, itemoff, part, ps, 1, 0, nh1, 1, a.Nc, a.E, a.Y, a.sq);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }

@@ -791,15 +791,20 @@ __global__ void __launch_bounds__(256) k_build_images(Dims dm, int Hp, int qg, i
     const int64_t off_hi = row < N1max ? 0 : 2 * (int64_t)N1max * 64;
     const int64_t off_lo = row < N1max ? (int64_t)N1max * 64 : 2 * (int64_t)N1max * 64 + kNL * 64;
     __half* base = img + ((int64_t)a * ng + grp) * nchunk * stage_h;
-    for (int d = lane; d < nchunk * kKC; d += 32) {
-      const int ch = d / kKC, e = d - ch * kKC;
-      const float v = (kind != 0 && d < dm.D) ? value(d) * sc : 0.f;
-      const __half hi = __float2half_rn(v);
-      const __half lo = __float2half_rn(v - __half2float(hi));
-      const int pos = rr * 64 + ((((e >> 3) ^ (rr & 7)) & 7) << 3) + (e & 7);  // 128B swizzle, 8 halves per 16 B
+    for (int u = lane; u < nchunk * (kKC / 8); u += 32) {  // one 16-byte unit (8 halves) per lane
+      const int ch = u / (kKC / 8), j = u - ch * (kKC / 8);
+      uint32_t hw[4], lw[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int d0 = ch * kKC + 8 * j + 2 * i;
+        const float v0 = (kind != 0 && d0 < dm.D) ? value(d0) * sc : 0.f;
+        const float v1 = (kind != 0 && d0 + 1 < dm.D) ? value(d0 + 1) * sc : 0.f;
+        split2(v0, v1, hw[i], lw[i]);
+      }
+      const int pos = rr * 64 + (((j ^ (rr & 7)) & 7) << 3);  // 128B swizzle: 16-byte unit j of row rr
       __half* st = base + ch * stage_h;
-      st[off_hi + pos] = hi;
-      st[off_lo + pos] = lo;
+      *reinterpret_cast<uint4*>(st + off_hi + pos) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+      *reinterpret_cast<uint4*>(st + off_lo + pos) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
     }
   }
 }
