@@ -353,23 +353,25 @@ __global__ void __launch_bounds__(256) k_select(SelectArgs a) {
         best_l = kl[j];
         best_c = kc[j];
       }
-    // block 4: fp64 log-sum-exp and responsibilities (numerics.hpp:15-22)
+    // block 4: fp64 log-sum-exp and responsibilities (numerics.hpp:15-22); lane j
+    // evaluates member j's exponentials, the terms are summed in member order
     double mx = -INFINITY;
     for (int j = 0; j < dm.Cp; ++j) mx = fmax(mx, static_cast<double>(kl[j]));
+    int myc = kc[0];
+    float myl = kl[0];
+    for (int j = 1; j < dm.Cp; ++j)
+      if (j == lane) {
+        myc = kc[j];
+        myl = kl[j];
+      }
+    const double term = (lane < dm.Cp && isfinite(mx)) ? exp(static_cast<double>(myl) - mx) : 0.0;
     double l = mx;
     if (isfinite(mx)) {
       double s2 = 0.0;
-      for (int j = 0; j < dm.Cp; ++j) s2 += exp(static_cast<double>(kl[j]) - mx);
+      for (int j = 0; j < dm.Cp; ++j) s2 += __shfl_sync(kFull, term, j);
       l = mx + log(s2);
     }
     if (lane < dm.Cp) {
-      int myc = kc[0];
-      float myl = kl[0];
-      for (int j = 1; j < dm.Cp; ++j)
-        if (j == lane) {
-          myc = kc[j];
-          myl = kl[j];
-        }
       a.K[n * dm.Cp + lane] = myc;
       a.resp[n * dm.Cp + lane] = exp(static_cast<double>(myl) - l);
     }
@@ -401,6 +403,7 @@ __device__ __forceinline__ void to_fixed(double v, long long& hi, long long& lo)
 __device__ __forceinline__ double from_fixed(long long hi, long long lo) {
   return static_cast<double>(hi) * (1.0 / 1024.0) + static_cast<double>(lo) * (1.0 / 1125899906842624.0);
 }
+constexpr int kGupdBatch = 4;  // points in flight per warp in k_gupdate
 __device__ __forceinline__ unsigned hash_key(int k) { return static_cast<unsigned>(k) * 2654435761u; }
 
 struct KeyMin {
@@ -474,16 +477,43 @@ __global__ void __launch_bounds__(kGupdThreads) k_gupdate(GupdArgs a, int capmax
       }
       __syncthreads();
       const double logpi_c = a.logpi[c];
-      for (int p = p0 + warp; p < p1; p += nw) {
-        const int n = a.part_ent[p];
-        const double cond_c = static_cast<double>(a.lablj[n]) - logpi_c;
-        const int m = a.ret_cnt[n];
-        for (int j = lane; j < m; j += 32) {
-          const int ct = a.ret_idx[(int64_t)n * dm.stride + j];
-          if (ct == c) continue;
-          const double lpt = a.logpi[ct];
-          if (lpt == -INFINITY) continue;  // pi_ct <= 0 (estep.cpp:301)
-          const double lt = static_cast<double>(a.ret_lj[(int64_t)n * dm.stride + j]);
+      // kGupdBatch points per warp step: every load of the batch is issued
+      // before any is consumed (the per-point chains are latency-bound)
+      for (int pb = p0 + warp; pb < p1; pb += nw * kGupdBatch) {
+        int nn[kGupdBatch], mm[kGupdBatch];
+        float lb[kGupdBatch];
+#pragma unroll
+        for (int u = 0; u < kGupdBatch; ++u) {
+          const int p = pb + u * nw;
+          nn[u] = p < p1 ? a.part_ent[p] : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < kGupdBatch; ++u) {
+          mm[u] = nn[u] >= 0 ? a.ret_cnt[nn[u]] : 0;
+          lb[u] = nn[u] >= 0 ? a.lablj[nn[u]] : 0.f;
+        }
+        int mmax = 0;
+#pragma unroll
+        for (int u = 0; u < kGupdBatch; ++u) mmax = max(mmax, mm[u]);
+        for (int jb = 0; jb < mmax; jb += 32) {
+          const int j = jb + lane;
+          int cts[kGupdBatch];
+          float lts[kGupdBatch];
+#pragma unroll
+          for (int u = 0; u < kGupdBatch; ++u) {
+            cts[u] = j < mm[u] ? a.ret_idx[(int64_t)nn[u] * dm.stride + j] : -1;
+            lts[u] = j < mm[u] ? a.ret_lj[(int64_t)nn[u] * dm.stride + j] : 0.f;
+          }
+          double lps[kGupdBatch];
+#pragma unroll
+          for (int u = 0; u < kGupdBatch; ++u) lps[u] = (cts[u] >= 0 && cts[u] != c) ? a.logpi[cts[u]] : -INFINITY;
+#pragma unroll
+          for (int u = 0; u < kGupdBatch; ++u) {
+          const int ct = cts[u];
+          const double lpt = lps[u];
+          if (ct < 0 || ct == c || lpt == -INFINITY) continue;  // pi_ct <= 0 (estep.cpp:301)
+          const double cond_c = static_cast<double>(lb[u]) - logpi_c;
+          const double lt = static_cast<double>(lts[u]);
           const double v = a.mode == 0 ? cond_c - (lt - lpt) : -lt;
           long long hi, lo;
           to_fixed(v, hi, lo);
@@ -501,6 +531,7 @@ __global__ void __launch_bounds__(kGupdThreads) k_gupdate(GupdArgs a, int capmax
             atomicAdd(reinterpret_cast<unsigned long long*>(g_cnt + ct), 1ULL);
             atomicAdd(reinterpret_cast<unsigned long long*>(g_hi + ct), static_cast<unsigned long long>(hi));
             atomicAdd(reinterpret_cast<unsigned long long*>(g_lo + ct), static_cast<unsigned long long>(lo));
+          }
           }
         }
       }
