@@ -715,6 +715,18 @@ __device__ __forceinline__ void bulk_row(uint32_t dst, const void* src, uint32_t
                : "memory");
 }
 
+// phase timing of k_stats (diagnostics): CTA 0, thread 0, cycles between marks
+__device__ unsigned long long g_stats_prof[16];
+__device__ int g_stats_prof_on;
+#define SPROF(k)                                                                         \
+  do {                                                                                   \
+    if (g_stats_prof_on && blockIdx.x == 0 && threadIdx.x == 0) {                        \
+      const unsigned long long now_ = clock64();                                         \
+      if ((k) > 0) g_stats_prof[(k)] += now_ - sprof_t;                                  \
+      sprof_t = now_;                                                                    \
+    }                                                                                    \
+  } while (0)
+
 // ---------------------------------------------------------------- K5: sufficient statistics
 // CTA per component a over its K-pairs (n, q) in ascending (n, j) order
 // (accumulate_point, mstep.cpp:47-67): mz = V_a (x - mu_a) (fp32 dot products),
@@ -722,6 +734,7 @@ __device__ __forceinline__ void bulk_row(uint32_t dst, const void* src, uint32_t
 // Y[:, h] += q x zhat_h; sq += q x^2. Fixed order per component =>
 // deterministic; no atomics.
 constexpr int kStatsBatch = 32;
+constexpr int kStatsMaxRows = 1024;  // K-pairs per statistics item (upper bound)
 constexpr int kStatsMaxH1 = 17;   // columns of Y per pass
 
 // Items are (component, chunk of <= rows_per_item K-pairs): large components
@@ -752,6 +765,8 @@ __global__ void __launch_bounds__(kStatsThreads, 2) k_stats(StatsArgs a, const i
   __shared__ double s_red[kStatsThreads / 32];
   __shared__ double s_accE[kStatsThreads];  // E entry of thread tid (fp64)
   __shared__ uint64_t s_xbar[2];             // row-batch arrival (bulk copies, D % 4 == 0)
+  __shared__ int s_eall[kStatsMaxRows];      // the item's entries / responsibilities
+  __shared__ double s_qall[kStatsMaxRows];
   const Dims dm = a.dm;
   const int H = dm.H, H1 = H + 1, D = dm.D;
   const int XS = (D + 3) / 4 * 4 + kXPad;
@@ -770,9 +785,13 @@ __global__ void __launch_bounds__(kStatsThreads, 2) k_stats(StatsArgs a, const i
   const int Dp = (D + 3) / 4 * 4;
   const int GX = Dp / 4;
   const int GD = GX;
+  // E: thread = (upper-triangle entry, row group); row groups summed in order at the item end
+  const int NE = H1 * (H1 + 1) / 2;
+  const int EG = max(1, kStatsThreads / NE);
+  const int eg = tid / NE;
   int ei = -1, ej = -1;  // this thread's E entry (i <= j)
-  if (full_e) {
-    int t = tid;
+  if (full_e && eg < EG) {
+    int t = tid - eg * NE;
     for (int i = 0; i < H1 && ei < 0; ++i) {
       if (t < H1 - i) ei = i, ej = i + t;
       else t -= H1 - i;
@@ -790,6 +809,7 @@ __global__ void __launch_bounds__(kStatsThreads, 2) k_stats(StatsArgs a, const i
   }
   __syncthreads();
   uint32_t xuse[2] = {0u, 0u};  // completed phases per row buffer (same in every thread)
+  unsigned long long sprof_t = 0;
   __shared__ int s_item;
   // items from a global work queue (dynamic balance; results depend only on the item)
   auto next_item = [&](int cur) -> int {
@@ -807,10 +827,17 @@ __global__ void __launch_bounds__(kStatsThreads, 2) k_stats(StatsArgs a, const i
     // responsibilities are scaled by the item's largest q before the fp32
     // accumulation (no underflow; N_c == 0 exactly iff every q == 0)
     double qmax = 0.0;
-    for (int i = r0 + tid; i < r1; i += kStatsThreads) qmax = fmax(qmax, a.resp[a.ent[i]]);
+    __syncthreads();  // previous item done with the shared buffers
+    // the item's entries and responsibilities, staged once (one latency per item)
+    for (int i = r0 + tid; i < r1; i += kStatsThreads) {
+      const int e = a.ent[i];
+      const double q = a.resp[e];
+      s_eall[i - r0] = e;
+      s_qall[i - r0] = q;
+      qmax = fmax(qmax, q);
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) qmax = fmax(qmax, __shfl_xor_sync(kFull, qmax, o));
-    __syncthreads();  // previous item done with the shared buffers
     if (lane == 0) s_red[warp] = qmax;
     for (int i = tid; i < D * VS; i += kStatsThreads) {
       const int d = i / VS, h = i - d * VS;
@@ -836,24 +863,29 @@ __global__ void __launch_bounds__(kStatsThreads, 2) k_stats(StatsArgs a, const i
     const int nbat = (r1 - r0 + kStatsBatch - 1) / kStatsBatch;
     auto stage_ids = [&](int b, int buf) {
       if (tid < kStatsBatch) {
-        const int i = r0 + b * kStatsBatch + tid;
-        const int e = i < r1 ? a.ent[i] : -1;
-        s_e[buf][tid] = e;
-        s_qb[buf][tid] = e >= 0 ? a.resp[e] / qdiv : 0.0;
+        const int i = b * kStatsBatch + tid;
+        const bool in = r0 + i < r1;
+        s_e[buf][tid] = in ? s_eall[i] : -1;
+        s_qb[buf][tid] = in ? s_qall[i] / qdiv : 0.0;
       }
     };
     auto issue_rows = [&](int buf) {
       float* dst = s_x + (int64_t)buf * kStatsBatch * XS;
       if (vec) {
-        // one bulk copy per row, issued by the 32 lanes of warp 0 in parallel
-        // (many copies in flight: far above what 16-byte cp.async sustains)
-        if (warp == 0) {
-          const int e = s_e[buf][lane];
-          const unsigned valid = __ballot_sync(kFull, e >= 0);
-          if (lane == 0) xbar_expect(&s_xbar[buf], static_cast<uint32_t>(__popc(valid)) * D * 4u);
-          __syncwarp();
+        // one bulk copy per row, issued by four lanes of every warp (the
+        // copies of a warp are issued one after another, so the batch is
+        // spread over the warps); thread 0 arms the barrier with the total
+        // (a copy may complete before the arm: the transaction count is signed)
+        if (tid == 0) {
+          int nv = 0;
+          for (int r = 0; r < kStatsBatch; ++r) nv += s_e[buf][r] >= 0;
+          xbar_expect(&s_xbar[buf], static_cast<uint32_t>(nv) * D * 4u);
+        }
+        if (lane < kStatsBatch / (kStatsThreads / 32)) {
+          const int r = warp * (kStatsBatch / (kStatsThreads / 32)) + lane;
+          const int e = s_e[buf][r];
           if (e >= 0)
-            bulk_row(smem_addr(dst + (int64_t)lane * XS), a.X + (int64_t)(e / dm.Cp) * D, D * 4u, &s_xbar[buf]);
+            bulk_row(smem_addr(dst + (int64_t)r * XS), a.X + (int64_t)(e / dm.Cp) * D, D * 4u, &s_xbar[buf]);
         }
       } else {
         for (int i = tid; i < kStatsBatch * D; i += kStatsThreads) {
@@ -874,6 +906,7 @@ __global__ void __launch_bounds__(kStatsThreads, 2) k_stats(StatsArgs a, const i
       const int buf = nbuf == 2 ? (bi & 1) : 0;
       const int b0 = r0 + bi * kStatsBatch;
       const int nb = min(kStatsBatch, r1 - b0);
+      SPROF(0);
       if (nbuf == 1) {
         if (bi > 0) {
           stage_ids(bi, 0);
@@ -889,8 +922,11 @@ __global__ void __launch_bounds__(kStatsThreads, 2) k_stats(StatsArgs a, const i
       } else {
         if (!vec) asm volatile("cp.async.wait_group 0;" ::: "memory");
       }
+      SPROF(1);
       if (vec) xbar_wait(&s_xbar[buf], xuse[buf]++ & 1u);
+      SPROF(2);
       __syncthreads();
+      SPROF(3);
       const float* xb = s_x + (int64_t)buf * kStatsBatch * XS;
       // (i) partial mz over this warp's dimension slice, lane = row
       {
@@ -922,7 +958,9 @@ __global__ void __launch_bounds__(kStatsThreads, 2) k_stats(StatsArgs a, const i
 #pragma unroll
         for (int h = 0; h < NH1; ++h) pz[h] = acc[h];
       }
+      SPROF(4);
       __syncthreads();
+      SPROF(5);
       for (int i = tid; i < kStatsBatch * ZS; i += kStatsThreads) {
         const int r = i / ZS, h = i - r * ZS;
         float z = 0.f;
@@ -934,11 +972,13 @@ __global__ void __launch_bounds__(kStatsThreads, 2) k_stats(StatsArgs a, const i
         }
         s_zf[i] = z;
       }
+      SPROF(6);
       __syncthreads();
+      SPROF(7);
       if (ei >= 0) {  // E(ei, ej) += q z_i z_j: fp32 z products are exact in fp64
         const double* s_q = s_qb[buf];
         double acc = s_accE[tid];
-        for (int r = 0; r < nb; ++r)
+        for (int r = eg; r < nb; r += EG)
           acc = fma(s_q[r], static_cast<double>(s_zf[r * ZS + ei]) * static_cast<double>(s_zf[r * ZS + ej]), acc);
         s_accE[tid] = acc;
       }
@@ -980,16 +1020,20 @@ __global__ void __launch_bounds__(kStatsThreads, 2) k_stats(StatsArgs a, const i
           }
         }
       }
+      SPROF(8);
       __syncthreads();
+      SPROF(9);
     }
     // combine the row groups of each dimension group through smem (fp64),
     // reusing the row buffers, then write (direct or partial) scaled by qmax
     double* red = reinterpret_cast<double*>(s_x);  // >= RG * GD * 4 * (NH1 + 1) doubles
     double* pp = direct ? nullptr : part + (int64_t)item * part_stride;
     double* pe = direct ? a.E + (int64_t)c * H1 * H1 : pp + (int64_t)NH1 * D + D;
-    if (ei >= 0) {
-      pe[ej * H1 + ei] = s_accE[tid] * qmax;
-      pe[ei * H1 + ej] = s_accE[tid] * qmax;
+    if (ei >= 0 && eg == 0) {
+      double e = 0.0;
+      for (int g = 0; g < EG; ++g) e += s_accE[tid + g * NE];
+      pe[ej * H1 + ei] = e * qmax;
+      pe[ei * H1 + ej] = e * qmax;
     }
 #pragma unroll
     for (int k = 0; k < ND; ++k) {
@@ -1808,6 +1852,19 @@ cudaError_t launch_stats(const StatsArgs& a, const int* itemoff, int rows_per_it
   k_stats_sz<<<grid_for((int64_t)a.dm.C * a.dm.H * a.dm.H, 256, 4096), 256, 0, s>>>(a.dm, a.Nc, a.Sz, a.E);
   return cudaGetLastError();
 }
+}  // namespace
+extern "C" int vmfa_diag_stats_cycles(int enable, unsigned long long* out) {
+  using namespace vmfa_b200;
+  cudaMemcpyToSymbol(g_stats_prof_on, &enable, sizeof(int));
+  if (out) {
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(out, g_stats_prof, sizeof(unsigned long long) * 16);
+  }
+  unsigned long long z[16] = {};
+  if (out || !enable) cudaMemcpyToSymbol(g_stats_prof, z, sizeof(z));
+  return 0;
+}
+namespace vmfa_b200 {
 cudaError_t launch_update(const UpdateArgs& a, cudaStream_t s) {
   const int H1 = a.dm.H + 1;
   const size_t smem = 2 * static_cast<size_t>(H1) * H1 * sizeof(double);
