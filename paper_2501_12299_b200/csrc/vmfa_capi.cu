@@ -60,6 +60,14 @@ __global__ void k_add_f64(const double* src, double* dst) { *dst = *src; }
 
 using namespace vmfa_b200;
 
+struct IterStatus {
+  int sel;
+  int empty;
+  unsigned long long upd;
+  unsigned long long model;
+  double scal[4];
+};
+
 struct vmfa_ctx {
   int device = 0;
   Dims dm{};
@@ -128,6 +136,8 @@ struct vmfa_ctx {
   unsigned long long* u64tmp = nullptr;
   int* st_select = nullptr;
   unsigned long long* st_model = nullptr;
+  unsigned long long* st_update = nullptr;
+  IterStatus* hstat = nullptr;  // pinned host readback of one iteration's statuses and scalars
   int* n_empty = nullptr;
   bool kinv_for_current_K = false;
   // the anchor pass of the next E-step already ran (under the current K, g
@@ -259,7 +269,7 @@ ScoreArgs score_args(vmfa_ctx* x) {
   return a;
 }
 
-int run_precompute(vmfa_ctx* x, int* failed) {
+int run_precompute(vmfa_ctx* x, int* failed, bool sync = true) {
   cudaStream_t s = x->stream;
   CU(cudaMemsetAsync(x->st_model, 0xff, sizeof(unsigned long long), s));
   PrecompArgs a{};
@@ -290,6 +300,7 @@ int run_precompute(vmfa_ctx* x, int* failed) {
     CU(launch_rowmax(x->dm.C, x->dm.D, x->mu32, x->mumax, s));
   }
   x->end(tok);
+  if (!sync) return VMFA_OK;  // the caller checks st_model later
   unsigned long long st = 0;
   CU(cudaMemcpyAsync(&st, x->st_model, sizeof st, cudaMemcpyDeviceToHost, s));
   CU(cudaStreamSynchronize(s));
@@ -438,7 +449,7 @@ int estep_local(vmfa_ctx* x, uint64_t seed, uint64_t it, int mode, bool exchange
   return VMFA_OK;
 }
 
-int estep_finish(vmfa_ctx* x, bool exchange) {
+int estep_finish(vmfa_ctx* x, bool exchange, bool sync = true) {
   const Dims& dm = x->dm;
   cudaStream_t s = x->stream;
   if (exchange) {
@@ -448,6 +459,7 @@ int estep_finish(vmfa_ctx* x, bool exchange) {
   }
   std::swap(x->g, x->g_new);
   std::swap(x->gcnt, x->gcnt_new);
+  if (!sync) return VMFA_OK;  // the caller checks st_select later
   int flag = 0;
   CU(cudaMemcpyAsync(&flag, x->st_select, sizeof(int), cudaMemcpyDeviceToHost, s));
   CU(cudaStreamSynchronize(s));
@@ -479,6 +491,45 @@ int stats_local(vmfa_ctx* x) {
   CU(launch_stats(a, x->stats_items, x->stats_rows, x->stats_part, x->stream));
   x->end(tok);
   return VMFA_OK;
+}
+
+// update_params into the "next" buffers; status in st_update (~0 = success)
+int launch_update_params(vmfa_ctx* x) {
+  x->prescored = false;  // parameters change
+  const Dims& dm = x->dm;
+  cudaStream_t s = x->stream;
+  CU(cudaMemsetAsync(x->st_update, 0xff, sizeof(unsigned long long), s));
+  UpdateArgs a{};
+  a.dm = dm;
+  a.Nc = x->Nc;
+  a.E = x->E;
+  a.Y = x->Y;
+  a.sq = x->sq;
+  a.floor = x->floor;
+  a.mu_prev = x->mu;
+  a.lam_prev = x->lam;
+  a.psi_prev = x->psi;
+  a.pi = x->pi2;
+  a.mu = x->mu2;
+  a.lam = x->lam2;
+  a.psi = x->psi2;
+  a.status = x->st_update;
+  const int tok = x->begin(kFamUpdate, dm.C);
+  CU(launch_update(a, s));
+  CU(launch_renorm(dm, x->pi2, x->st_update, s));
+  x->end(tok);
+  return VMFA_OK;
+}
+void swap_params(vmfa_ctx* x) {
+  std::swap(x->pi, x->pi2);
+  std::swap(x->mu, x->mu2);
+  std::swap(x->lam, x->lam2);
+  std::swap(x->psi, x->psi2);
+}
+int update_status(unsigned long long st, int* failed) {
+  const int comp = static_cast<int>(st >> 8), code = static_cast<int>(st & 0xff);
+  if (failed) *failed = comp == 0xffffff ? -1 : comp;
+  return fail(code, comp == 0xffffff ? "all components empty after update" : "E_c singular for component %d", comp);
 }
 
 int update_and_precompute(vmfa_ctx* x, int* failed) {
@@ -730,7 +781,10 @@ int vmfa_ctx_create(vmfa_ctx** out, int device, int C, int D, int H, int Cp, int
   A(x->u64tmp, 1);
   A(x->st_select, 1);
   A(x->st_model, 1);
+  A(x->st_update, 1);
   A(x->n_empty, 1);
+  if (r == VMFA_OK && cudaMallocHost(&x->hstat, sizeof(IterStatus)) != cudaSuccess)
+    r = fail(VMFA_ERR_CUDA, "cudaMallocHost failed");
   if (r != VMFA_OK) {
     vmfa_ctx_destroy(x);
     return r;
@@ -768,6 +822,7 @@ int vmfa_ctx_destroy(vmfa_ctx* x) {
   cudaSetDevice(x->device);
   if (x->stream) cudaStreamSynchronize(x->stream);
   for (void* p : x->allocs) cudaFree(p);
+  if (x->hstat) cudaFreeHost(x->hstat);
   for (auto& e : x->pending) {
     cudaEventDestroy(e.a);
     cudaEventDestroy(e.b);
@@ -1092,23 +1147,48 @@ int vmfa_iterate(vmfa_ctx* x, uint64_t seed, uint64_t iteration, int mode, vmfa_
   TRY(check_ctx(x));
   if (mode != VMFA_DIST_KL && mode != VMFA_DIST_EUCLID) return fail(VMFA_ERR_INVALID_ARGUMENT, "mode");
   int failed = -1;
+  cudaStream_t s = x->stream;
+  // the whole iteration is enqueued without a host synchronisation; the
+  // statuses of selection, update and precompute are read back once at the end
   TRY(estep_local(x, seed, iteration, mode, false));
-  TRY(estep_finish(x, false));
+  TRY(estep_finish(x, false, false));
   TRY(stats_local(x));
-  const int r = update_and_precompute(x, &failed);
-  if (rep) rep->failed_component = failed;
-  if (r != VMFA_OK) return r;
+  TRY(launch_update_params(x));
+  swap_params(x);
+  TRY(run_precompute(x, &failed, false));
   TRY(free_energy_local(x, x->lookahead));
-  CU(launch_count_empty(x->pi, x->dm.C, x->n_empty, x->stream));
-  double sc[4];
-  int ne = 0;
-  CU(cudaMemcpyAsync(&ne, x->n_empty, sizeof(int), cudaMemcpyDeviceToHost, x->stream));
-  TRY(read_scalars(x, sc));
+  CU(launch_count_empty(x->pi, x->dm.C, x->n_empty, s));
+  IterStatus* h = x->hstat;
+  CU(cudaMemcpyAsync(&h->sel, x->st_select, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CU(cudaMemcpyAsync(&h->upd, x->st_update, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+  CU(cudaMemcpyAsync(&h->model, x->st_model, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+  CU(cudaMemcpyAsync(&h->empty, x->n_empty, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CU(cudaMemcpyAsync(h->scal, x->scal, 4 * sizeof(double), cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  if (h->sel) {
+    x->prescored = false;
+    return fail(VMFA_ERR_INSUFFICIENT_CANDIDATES, "search space smaller than C'");
+  }
+  if (h->upd != ~0ull) {  // leave the pre-update parameters (and their caches) in place
+    swap_params(x);
+    TRY(run_precompute(x, nullptr));
+    x->prescored = false;
+    const int r = update_status(h->upd, &failed);
+    if (rep) rep->failed_component = failed;
+    return r;
+  }
+  if (h->model != ~0ull) {
+    x->prescored = false;
+    failed = static_cast<int>(h->model >> 8);
+    if (rep) rep->failed_component = failed;
+    return fail(static_cast<int>(h->model & 0xff), "L_c not positive definite for component %d", failed);
+  }
   if (rep) {
-    rep->free_energy_estep = sc[0];
-    rep->joints = static_cast<uint64_t>(sc[1]);
-    rep->free_energy = sc[2];
-    rep->empty_components = ne;
+    rep->failed_component = -1;
+    rep->free_energy_estep = h->scal[0];
+    rep->joints = static_cast<uint64_t>(h->scal[1]);
+    rep->free_energy = h->scal[2];
+    rep->empty_components = h->empty;
   }
   return VMFA_OK;
 }
