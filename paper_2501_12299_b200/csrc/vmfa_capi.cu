@@ -947,12 +947,6 @@ int vmfa_upload_state(vmfa_ctx* x, const int32_t* K, const int32_t* g, const int
     }
     if (!has_c) return fail(VMFA_ERR_INVALID_ARGUMENT, "g_c does not contain c (c=%d)", c);
   }
-  for (int64_t n = 0; n < dm.N; ++n)
-    for (int j = 0; j < dm.Cp; ++j) {
-      const int v = K[n * dm.Cp + j];
-      if (v < 0 || v >= dm.C || (j > 0 && v <= K[n * dm.Cp + j - 1]))
-        return fail(VMFA_ERR_INVALID_ARGUMENT, "K row not sorted distinct in-range indices (n=%lld)", static_cast<long long>(n));
-    }
   std::vector<int32_t> gp(static_cast<size_t>(dm.C) * dm.G);
   for (int c = 0; c < dm.C; ++c)
     for (int i = 0; i < dm.G; ++i) gp[static_cast<size_t>(c) * dm.G + i] = i < g_count[c] ? g[static_cast<int64_t>(c) * dm.G + i] : -1;
@@ -960,9 +954,17 @@ int vmfa_upload_state(vmfa_ctx* x, const int32_t* K, const int32_t* g, const int
   CU(cudaMemcpyAsync(x->K, K, sizeof(int) * dm.N * dm.Cp, cudaMemcpyHostToDevice, s));
   CU(cudaMemcpyAsync(x->g, gp.data(), sizeof(int) * gp.size(), cudaMemcpyHostToDevice, s));
   CU(cudaMemcpyAsync(x->gcnt, g_count, sizeof(int) * dm.C, cudaMemcpyHostToDevice, s));
+  // K rows are validated on the device (one pass over N x C')
+  const long long none = 0x7fffffffffffffffLL;
+  long long* bad = reinterpret_cast<long long*>(x->u64tmp);
+  CU(cudaMemcpyAsync(bad, &none, sizeof none, cudaMemcpyHostToDevice, s));
+  CU(launch_validate_K(x->K, dm.N, dm.Cp, dm.C, bad, s));
+  long long first = none;
+  CU(cudaMemcpyAsync(&first, bad, sizeof first, cudaMemcpyDeviceToHost, s));
   CU(cudaStreamSynchronize(s));
   x->kinv_for_current_K = false;
   x->have_estep = false;
+  if (first != none) return fail(VMFA_ERR_INVALID_ARGUMENT, "K row not sorted distinct in-range indices (n=%lld)", first);
   return VMFA_OK;
 }
 

@@ -1672,6 +1672,19 @@ __global__ void k_sum_i32(const int* v, int64_t n, unsigned long long* out) {
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
   if ((threadIdx.x & 31) == 0) atomicAdd(out, s);
 }
+// VarState::validate for K (estep.cpp:15-68): rows sorted, distinct, in range;
+// the first offending row (smallest n) is reported through *bad (init INT_MAX)
+__global__ void k_validate_K(const int* K, int64_t N, int Cp, int C, long long* bad) {
+  for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < N; n += (int64_t)gridDim.x * blockDim.x) {
+    bool ok = true;
+    for (int j = 0; j < Cp; ++j) {
+      const int v = K[n * Cp + j];
+      ok &= v >= 0 && v < C && (j == 0 || v > K[n * Cp + j - 1]);
+    }
+    if (!ok) atomicMin(bad, static_cast<long long>(n));
+  }
+}
+
 __global__ void k_count_empty(const double* pi, int C, int* out) {
   int s = 0;
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < C; c += gridDim.x * blockDim.x) s += pi[c] == 0.0;
@@ -1904,6 +1917,10 @@ cudaError_t launch_sum_f64(const double* v, int64_t n, double* partials, double*
 cudaError_t launch_sum_i32(const int* v, int64_t n, unsigned long long* out, cudaStream_t s) {
   cudaMemsetAsync(out, 0, sizeof(unsigned long long), s);
   k_sum_i32<<<grid_for(n, 256, 1024), 256, 0, s>>>(v, n, out);
+  return cudaGetLastError();
+}
+cudaError_t launch_validate_K(const int* K, int64_t N, int Cp, int C, long long* bad, cudaStream_t s) {
+  k_validate_K<<<grid_for(N, 256, 4096), 256, 0, s>>>(K, N, Cp, C, bad);
   return cudaGetLastError();
 }
 cudaError_t launch_count_empty(const double* pi, int C, int* out, cudaStream_t s) {

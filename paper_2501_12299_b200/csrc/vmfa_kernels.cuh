@@ -203,6 +203,7 @@ cudaError_t launch_sum_f64(const double* v, int64_t n, double* partials, double*
                            cudaStream_t s);
 cudaError_t launch_sum_i32(const int* v, int64_t n, unsigned long long* out, cudaStream_t s);
 cudaError_t launch_count_empty(const double* pi, int C, int* out, cudaStream_t s);
+cudaError_t launch_validate_K(const int* K, int64_t N, int Cp, int C, long long* bad, cudaStream_t s);
 cudaError_t launch_logpi(const double* pi, int C, double* logpi, cudaStream_t s);
 
 int sm_count();

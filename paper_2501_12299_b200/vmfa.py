@@ -136,9 +136,10 @@ class Session:
         check(lib().vmfa_upload_params(self._h, ptr(_c(p.pi, np.float64)), ptr(_c(p.mu, np.float64)),
                                        ptr(_c(p.lam, np.float64)), ptr(_c(p.psi, np.float64))))
 
-    def download_params(self) -> Params:
-        p = Params(np.zeros(self.C), np.zeros((self.C, self.D)), np.zeros((self.C, self.H, self.D)),
-                   np.zeros((self.C, self.D)))
+    def download_params(self, out: Params | None = None) -> Params:
+        """Parameters into new arrays, or into `out` (e.g. pinned buffers reused per step)."""
+        p = out if out is not None else Params(np.zeros(self.C), np.zeros((self.C, self.D)),
+                                               np.zeros((self.C, self.H, self.D)), np.zeros((self.C, self.D)))
         check(lib().vmfa_download_params(self._h, ptr(p.pi), ptr(p.mu), ptr(p.lam), ptr(p.psi)))
         return p
 
@@ -161,9 +162,11 @@ class Session:
         check(lib().vmfa_upload_state(self._h, ptr(_c(st.K, np.int32)), ptr(_c(st.g, np.int32)),
                                       ptr(_c(st.g_count, np.int32))))
 
-    def download_state(self) -> State:
-        st = State(np.zeros((self.N, self.Cp), np.int32), np.zeros((self.C, self.G), np.int32),
-                   np.zeros(self.C, np.int32), np.zeros(self.N, np.int32))
+    def download_state(self, out: State | None = None) -> State:
+        """State into new arrays, or into `out` (labels included)."""
+        st = out if out is not None else State(np.zeros((self.N, self.Cp), np.int32),
+                                               np.zeros((self.C, self.G), np.int32),
+                                               np.zeros(self.C, np.int32), np.zeros(self.N, np.int32))
         check(lib().vmfa_download_state(self._h, ptr(st.K), ptr(st.g), ptr(st.g_count),
                                         ptr(st.labels)))
         return st
