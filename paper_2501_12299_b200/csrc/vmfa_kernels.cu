@@ -312,11 +312,11 @@ __global__ void __launch_bounds__(256) k_select(SelectArgs a) {
       unsigned long long best = 0ull;
 #pragma unroll
       for (int k = 0; k < NS; ++k) best = key[k] > best ? key[k] : best;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const unsigned long long oth = __shfl_xor_sync(kFull, best, o);
-        best = oth > best ? oth : best;
-      }
+      // warp max of the 64-bit keys: high words by a redux, low words among the ties
+      const unsigned hi = __reduce_max_sync(kFull, static_cast<unsigned>(best >> 32));
+      const unsigned lo = __reduce_max_sync(
+          kFull, static_cast<unsigned>(best >> 32) == hi ? static_cast<unsigned>(best) : 0u);
+      best = (static_cast<unsigned long long>(hi) << 32) | lo;
       if (best == 0ull) {
         if (lane == 0) atomicOr(a.status, 1);  // InsufficientCandidates
         kc[r] = 0;
