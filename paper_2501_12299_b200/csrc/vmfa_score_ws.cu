@@ -61,7 +61,9 @@ constexpr int kMaxD = 1024;
 constexpr int kNL = 16;               // lin rows / psi rows per group (qg <= 16)
 constexpr int kTargetExp = 14;        // operands scaled to |value| <= 2^14
 __host__ __device__ constexpr int rec_stride(int Hp) { return 8 + 2 * Hp; }  // floats per epilogue record
-__host__ __device__ constexpr int qg_max(int Hp) { return (256 - kNL) / Hp < kNL ? (256 - kNL) / Hp : kNL; }
+// components per anchor job: the accumulator [16 lin | qg*Hp W | 16 psi] must
+// fit one 256-column TMEM buffer
+__host__ __device__ constexpr int qg_max(int Hp) { return (256 - 2 * kNL) / Hp < kNL ? (256 - 2 * kNL) / Hp : kNL; }
 
 struct WsArgs {
   Dims dm;
@@ -824,7 +826,7 @@ __global__ void k_rowmax(int64_t N, int D, const float* X, float* xmax) {
 
 int ws_qg(const Dims& dm, int single) {
   const int Hp = ws_hp(dm.H);
-  return single ? 1 : std::max(1, std::min(std::min(dm.G, kNL), (256 - kNL) / Hp));
+  return single ? 1 : std::max(1, std::min(dm.G, qg_max(Hp)));
 }
 int ws_n1max(const Dims& dm, int single) { return kNL + ((ws_qg(dm, single) * ws_hp(dm.H) + 15) / 16) * 16; }
 

@@ -59,6 +59,7 @@ def test_precompute_caches_match_oracle(oracle, gpu):
     dict(N=2000, D=16, C=40, H=1, Cp=1, G=1),     # C'=1, G=1
     dict(N=1000, D=10, C=6, H=2, Cp=6, G=6),      # C'=C: no truncation
     dict(N=2000, D=100, C=50, H=16, Cp=4, G=8),   # H=16 chunk
+    dict(N=1500, D=64, C=60, H=12, Cp=3, G=18),   # two component groups per anchor job (G > 15)
 ])
 @pytest.mark.parametrize("scorer", ["ws", "tc", "ffma"])
 def test_estep_teacher_forced(oracle, gpu, case, scorer, monkeypatch):
@@ -318,3 +319,23 @@ def test_lookahead_free_energy_is_exact(oracle, gpu, scorer, monkeypatch):
     assert np.array_equal(s1.K, s0.K) and np.array_equal(s1.g, s0.g)
     for f in ("pi", "mu", "lam", "psi"):
         assert np.array_equal(getattr(p1, f), getattr(p0, f)), f
+
+
+def test_upload_state_validates_K_on_device(gpu):
+    # VarState::validate (estep.cpp:15-68): K rows sorted, distinct, in range
+    V = gpu
+    X, _ = gaussian_problem(500, 16, 6, 2, seed=3)
+    p, st, floor, _ = V.initialize(X, 10, 2, 3, 4, seed=1)
+    sess = V.Session(10, 16, 2, 3, 4, X)
+    sess.set_floor(floor)
+    sess.upload_params(p)
+    sess.upload_state(st)  # valid
+    bad = st.K.copy()
+    bad[137] = bad[137][::-1]  # unsorted row
+    with pytest.raises(V.VmfaError, match=r"InvalidArgument.*n=137"):
+        sess.upload_state(V.State(bad, st.g, st.g_count))
+    bad = st.K.copy()
+    bad[42, 0] = 10  # out of range
+    with pytest.raises(V.VmfaError, match=r"n=42"):
+        sess.upload_state(V.State(bad, st.g, st.g_count))
+    sess.close()
