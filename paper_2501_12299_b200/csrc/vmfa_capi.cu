@@ -644,8 +644,6 @@ int vmfa_ctx_create(vmfa_ctx** out, int device, int C, int D, int H, int Cp, int
                 static_cast<long long>(n_local));
   if (H + 1 > 65) return fail(VMFA_ERR_UNSUPPORTED, "H > 64 not supported by this build");
   if (Cp > 8 || Cp * G + 1 > 256) return fail(VMFA_ERR_UNSUPPORTED, "C' <= 8 and C'G+1 <= 256 required");
-  if (static_cast<size_t>(D) * kXsStride * sizeof(float) > 200 * 1024)
-    return fail(VMFA_ERR_UNSUPPORTED, "D > %zu not supported by the scoring tile", 200 * 1024 / (kXsStride * sizeof(float)));
   if (n_local * Cp >= (int64_t{1} << 31)) return fail(VMFA_ERR_UNSUPPORTED, "shard too large (N*C' >= 2^31)");
   if (!vmfa_device_available()) return fail(VMFA_ERR_NO_DEVICE, "no sm_100 CUDA device visible");
   CU(cudaSetDevice(device));
@@ -671,6 +669,11 @@ int vmfa_ctx_create(vmfa_ctx** out, int device, int C, int D, int H, int Cp, int
         static_cast<size_t>(ws_image_halves(x->dm, 0) + ws_image_halves(x->dm, 1)) * 2 > kImageBudget)
       x->scorer = 1;
     if (x->scorer == 1 && !score_tc_supported(x->dm)) x->scorer = 0;
+    if (x->scorer == 0 && static_cast<size_t>(D) * kXsStride * sizeof(float) > 200 * 1024) {
+      const size_t dmax = 200 * 1024 / (kXsStride * sizeof(float));
+      delete x;
+      return fail(VMFA_ERR_UNSUPPORTED, "D > %zu not supported by the FFMA scoring tile", dmax);
+    }
     x->use_tc = x->scorer != 0;
     x->score_rows = x->use_tc ? kScoreRowsTc : kScoreRows;
   }
