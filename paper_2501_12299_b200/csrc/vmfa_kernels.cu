@@ -753,7 +753,7 @@ constexpr int kStatsMaxH1 = 17;   // columns of Y per pass
 constexpr int kXPad = 4;  // s_x row stride D + 4: conflict-free LDS.128 across rows
 
 template <int NH1, int ND>
-__global__ void __launch_bounds__(kStatsThreads, 2) k_stats(StatsArgs a, const int* __restrict__ itemoff,
+__global__ void __launch_bounds__(kStatsThreads, NH1 > 9 ? 1 : 2) k_stats(StatsArgs a, const int* __restrict__ itemoff,
                                                         int rows_per_item, int col0, double* part,
                                                         int64_t part_stride, int nbuf) {
   // smem: s_x [nbuf][B][XS] | s_V [D][VS] | s_mu [D+pad] | s_pz [8][B][NH1] | s_zf [B][ZS] (float)
