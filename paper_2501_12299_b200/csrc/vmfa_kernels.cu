@@ -13,6 +13,7 @@
 #include <cfloat>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 
 #include "vmfa_kernels.cuh"
 #include "vmfa_rng.hpp"
@@ -735,6 +736,7 @@ __device__ int g_stats_prof_on;
 // deterministic; no atomics.
 constexpr int kStatsBatch = 32;
 constexpr int kStatsMaxRows = 1024;  // K-pairs per statistics item (upper bound)
+constexpr int kStatsMaxBuf = 4;      // row-batch ring depth (bulk-copy path)
 constexpr int kStatsMaxH1 = 17;   // columns of Y per pass
 
 // Items are (component, chunk of <= rows_per_item K-pairs): large components
@@ -760,11 +762,11 @@ __global__ void __launch_bounds__(kStatsThreads, NH1 > 9 ? 1 : 2) k_stats(StatsA
   extern __shared__ __align__(16) float s_x[];
   constexpr int VS = (NH1 + 3) / 4 * 4;  // V row stride (16-byte rows for LDS.128)
   constexpr int ZS = VS;                 // zhat row stride in s_zf
-  __shared__ double s_qb[2][kStatsBatch];
-  __shared__ int s_e[2][kStatsBatch];
+  __shared__ double s_qb[kStatsMaxBuf][kStatsBatch];
+  __shared__ int s_e[kStatsMaxBuf][kStatsBatch];
   __shared__ double s_red[kStatsThreads / 32];
   __shared__ double s_accE[kStatsThreads];  // E entry of thread tid (fp64)
-  __shared__ uint64_t s_xbar[2];             // row-batch arrival (bulk copies, D % 4 == 0)
+  __shared__ uint64_t s_xbar[kStatsMaxBuf];  // row-batch arrival (bulk copies, D % 4 == 0)
   __shared__ int s_eall[kStatsMaxRows];      // the item's entries / responsibilities
   __shared__ double s_qall[kStatsMaxRows];
   const Dims dm = a.dm;
@@ -803,12 +805,10 @@ __global__ void __launch_bounds__(kStatsThreads, NH1 > 9 ? 1 : 2) k_stats(StatsA
   const int dsl = ((D + 7) / 8 + 3) / 4 * 4;  // phase (i) dims per warp, multiple of 4
   const int dw0 = warp * dsl, dw1 = min(D, dw0 + dsl);
   const int total = __ldg(itemoff + dm.C);
-  if (tid == 0) {
-    xbar_init(&s_xbar[0]);
-    xbar_init(&s_xbar[1]);
-  }
+  if (tid == 0)
+    for (int i = 0; i < kStatsMaxBuf; ++i) xbar_init(&s_xbar[i]);
   __syncthreads();
-  uint32_t xuse[2] = {0u, 0u};  // completed phases per row buffer (same in every thread)
+  uint32_t xuse[kStatsMaxBuf] = {0u, 0u, 0u, 0u};  // completed phases per row buffer (same in every thread)
   unsigned long long sprof_t = 0;
   __shared__ int s_item;
   // items from a global work queue (dynamic balance; results depend only on the item)
@@ -899,15 +899,26 @@ __global__ void __launch_bounds__(kStatsThreads, NH1 > 9 ? 1 : 2) k_stats(StatsA
       }
       asm volatile("cp.async.commit_group;" ::: "memory");
     };
-    stage_ids(0, 0);
-    __syncthreads();
-    issue_rows(0);
+    // ring of nbuf row buffers: batches are issued nbuf - 1 ahead (bulk path);
+    // the cp.async path keeps one batch ahead with nbuf <= 2
+    const int ahead = vec ? nbuf - 1 : 1;
+    for (int b = 0; b < (vec ? min(ahead, nbat) : 1); ++b) {
+      stage_ids(b, b % nbuf);
+      __syncthreads();
+      issue_rows(b % nbuf);
+    }
     for (int bi = 0; bi < nbat; ++bi) {
-      const int buf = nbuf == 2 ? (bi & 1) : 0;
+      const int buf = bi % nbuf;
       const int b0 = r0 + bi * kStatsBatch;
       const int nb = min(kStatsBatch, r1 - b0);
       SPROF(0);
-      if (nbuf == 1) {
+      if (vec) {
+        if (bi + ahead < nbat) {
+          stage_ids(bi + ahead, (bi + ahead) % nbuf);
+          __syncthreads();
+          issue_rows((bi + ahead) % nbuf);
+        }
+      } else if (nbuf == 1) {
         if (bi > 0) {
           stage_ids(bi, 0);
           __syncthreads();
@@ -918,9 +929,9 @@ __global__ void __launch_bounds__(kStatsThreads, NH1 > 9 ? 1 : 2) k_stats(StatsA
         stage_ids(bi + 1, buf ^ 1);
         __syncthreads();
         issue_rows(buf ^ 1);
-        if (!vec) asm volatile("cp.async.wait_group 1;" ::: "memory");
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
       } else {
-        if (!vec) asm volatile("cp.async.wait_group 0;" ::: "memory");
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
       }
       SPROF(1);
       if (vec) xbar_wait(&s_xbar[buf], xuse[buf]++ & 1u);
@@ -1818,8 +1829,18 @@ static void stats_pass(const StatsArgs& a, const int* itemoff, int rpi, int grid
   const int GD = (D + 3) / 4;
   const int RG = std::max(1, kStatsThreads / GD);
   const size_t red = static_cast<size_t>(std::max(RG - 1, 0)) * GD * 4 * (NH1 + 1) * sizeof(double);
+  static const int want = [] {
+    const char* v = std::getenv("VMFA_STATS_NBUF");
+    return v ? std::atoi(v) : 0;
+  }();
   int nbuf = (2 * per_buf + fixed <= 200 * 1024) ? 2 : 1;
   if (static_cast<size_t>(nbuf) * per_buf < red) nbuf = 2;
+  if (a.dm.D % 4 == 0)  // bulk-copy path: deeper ring when it fits
+    for (int nb = std::min(kStatsMaxBuf, want > 0 ? want : 2); nb > nbuf; --nb)
+      if (nb * per_buf + fixed <= 200 * 1024) {
+        nbuf = nb;
+        break;
+      }
   const size_t smem = std::max(static_cast<size_t>(nbuf) * per_buf, red) + fixed;
   auto go = [&](auto kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
