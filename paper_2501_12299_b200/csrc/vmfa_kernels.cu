@@ -1488,9 +1488,12 @@ __global__ void __launch_bounds__(1024) k_renorm(Dims dm, double* pi, unsigned l
 // (symmetrised), Cholesky L = R R^T (+1e-10 I retry, else CholeskyFailure),
 // Sigma_z = L^-1, log|Sigma| = 2 sum log R_hh + sum log psi, log pi; fp32
 // scoring rows W = U R^-T (| W^T v |^2 = (U^T v).(V v)), V32 = R^-T R^-1 U^T.
+constexpr int kPreFastH = 8;  // precompute's register-blocked M for H <= 8
+
 __global__ void __launch_bounds__(128) k_precompute(PrecompArgs a) {
   extern __shared__ __align__(16) double s_pre[];
   __shared__ double red[128];
+  __shared__ double s_mpart[4][kPreFastH * (kPreFastH + 1) / 2];
   __shared__ int s_ok;
   const Dims dm = a.dm;
   const int H = dm.H, D = dm.D;
@@ -1500,13 +1503,54 @@ __global__ void __launch_bounds__(128) k_precompute(PrecompArgs a) {
   for (int c = blockIdx.x; c < dm.C; c += gridDim.x) {
     const double* lam = a.lam + (int64_t)c * D * H;
     const double* psi = a.psi + (int64_t)c * D;
-    // M = Lambda^T Psi^-1 Lambda (+I), symmetrised (model.cpp:51-53)
-    for (int p = tid; p < H * H; p += blockDim.x) {
-      const int i = p % H, j = p / H;
-      if (i > j) continue;
-      double s = 0.0;
-      for (int d = 0; d < D; ++d) s += lam[(int64_t)i * D + d] * (lam[(int64_t)j * D + d] / psi[d]);
-      sL[j * H + i] = s;
+    // M = Lambda^T Psi^-1 Lambda (+I), symmetrised (model.cpp:51-53): every
+    // thread sums its dimensions for all upper entries (H <= kPreFastH), then
+    // a warp-shuffle + fixed-order cross-warp reduction; else one entry per thread
+    if (H <= kPreFastH) {
+      const int np = H * (H + 1) / 2;
+      double acc[kPreFastH * (kPreFastH + 1) / 2];
+#pragma unroll
+      for (int p = 0; p < kPreFastH * (kPreFastH + 1) / 2; ++p) acc[p] = 0.0;
+      for (int d = tid; d < D; d += blockDim.x) {
+        const double w = 1.0 / psi[d];
+        double u[kPreFastH];
+#pragma unroll
+        for (int i = 0; i < kPreFastH; ++i) u[i] = i < H ? lam[(int64_t)i * D + d] : 0.0;
+        int p = 0;
+#pragma unroll
+        for (int j = 0; j < kPreFastH; ++j)
+#pragma unroll
+          for (int i = 0; i <= j; ++i, ++p) acc[p] += u[i] * (u[j] * w);
+      }
+      const int lane = tid & 31, warp = tid >> 5;
+      int p = 0;
+#pragma unroll
+      for (int j = 0; j < kPreFastH; ++j)
+#pragma unroll
+        for (int i = 0; i <= j; ++i, ++p) {
+          double v = acc[p];
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+          if (lane == 0 && j < H) s_mpart[warp][p] = v;
+        }
+      __syncthreads();
+      for (int q = tid; q < np; q += blockDim.x) {
+        // q -> (i, j) with the same packing as above
+        int jj = 0, off = 0;
+        while (off + jj + 1 <= q) off += ++jj;
+        const int ii = q - off;
+        double v = 0.0;
+        for (int w2 = 0; w2 < static_cast<int>(blockDim.x >> 5); ++w2) v += s_mpart[w2][q];
+        sL[jj * H + ii] = v;
+      }
+    } else {
+      for (int p = tid; p < H * H; p += blockDim.x) {
+        const int i = p % H, j = p / H;
+        if (i > j) continue;
+        double s = 0.0;
+        for (int d = 0; d < D; ++d) s += lam[(int64_t)i * D + d] * (lam[(int64_t)j * D + d] / psi[d]);
+        sL[j * H + i] = s;
+      }
     }
     __syncthreads();
     for (int p = tid; p < H * H; p += blockDim.x) {

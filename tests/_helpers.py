@@ -134,6 +134,7 @@ def ldlt_cases(O):
     E[2] = np.array([[1.0, 1.0, 0.0], [1.0, 1.0, 0.0], [0.0, 0.0, 0.5]])
     E[3] = np.array([[1.0, 2.0, 0.1], [2.0, 1.0, 0.2], [0.1, 0.2, 4.0]])
     Y = rng.normal(size=(C_, H1, D))
+    Y[2, 1] = Y[2, 0]  # consistent with E[2]'s null direction: the jittered solution stays bounded
     Nc = E[:, H, H].copy()
     sq = np.full((C_, D), 50.0)
     want = np.zeros((C_, H1, D))

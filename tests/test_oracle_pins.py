@@ -324,8 +324,10 @@ def test_update_params_ldlt_semantics(oracle):
     p = oracle.update_params(s, 10, prev, floor)
     H = prev.H
     for c in range(4):
-        np.testing.assert_allclose(p.lam[c], want[c, :H], rtol=1e-9, atol=1e-12, err_msg=str(c))
-        np.testing.assert_allclose(p.mu[c], want[c, H], rtol=1e-9, atol=1e-12, err_msg=str(c))
+        # c2's jittered E has condition ~1.5e10: fp64 solves agree to ~cond*eps
+        tol = dict(rtol=0, atol=2e-5) if c == 2 else dict(rtol=1e-9, atol=1e-12)
+        np.testing.assert_allclose(p.lam[c], want[c, :H], err_msg=str(c), **tol)
+        np.testing.assert_allclose(p.mu[c], want[c, H], err_msg=str(c), **tol)
     # a solution that overflows with and without the jitter -> SingularEc
     s.E[3] = np.diag([1e-300, 1e-300, 1e-300])
     s.Nc[3] = 1e-300
