@@ -20,6 +20,8 @@ OBJ_DIR = os.path.join(ROOT, "build", "obj")
 LIB = os.path.join(OUT_DIR, "libvmfa_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+# extra nvcc flags for diagnostic builds (e.g. -DVMFA_STATS_PROF; rebuild with force=True)
+EXTRA = os.environ.get("VMFA_NVCC_EXTRA", "").split()
 CU_SOURCES = ["vmfa_kernels.cu", "vmfa_score_tc.cu", "vmfa_score_ws.cu", "vmfa_capi.cu"]
 CXX_SOURCES = ["host/vmfa_host.cpp"]
 DEPS_H = ["vmfa_kernels.cuh", "vmfa_internal.hpp", "vmfa_rng.hpp"]
@@ -46,7 +48,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
             continue
         if src.endswith(".cu"):
             cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
-                   "-Xptxas", "-warn-spills", *inc, "-c", path, "-o", obj]
+                   "-Xptxas", "-warn-spills", *EXTRA, *inc, "-c", path, "-o", obj]
         else:
             cmd = ["g++", "-O3", "-std=c++17", "-fPIC", "-pthread", "-Wall", "-Wextra",
                    "-I", "/usr/local/cuda/include", *inc, "-c", path, "-o", obj]

@@ -716,17 +716,24 @@ __device__ __forceinline__ void bulk_row(uint32_t dst, const void* src, uint32_t
                : "memory");
 }
 
-// phase timing of k_stats (diagnostics): CTA 0, thread 0, cycles between marks
+// phase timing of k_stats (diagnostics, built with -DVMFA_STATS_PROF): CTA 0,
+// thread 0, cycles between marks
 __device__ unsigned long long g_stats_prof[16];
 __device__ int g_stats_prof_on;
+#ifdef VMFA_STATS_PROF
 #define SPROF(k)                                                                         \
   do {                                                                                   \
-    if (g_stats_prof_on && blockIdx.x == 0 && threadIdx.x == 0) {                        \
+    if (sprof_on) {                                                                      \
       const unsigned long long now_ = clock64();                                         \
       if ((k) > 0) g_stats_prof[(k)] += now_ - sprof_t;                                  \
       sprof_t = now_;                                                                    \
     }                                                                                    \
   } while (0)
+#else
+#define SPROF(k) \
+  do {           \
+  } while (0)
+#endif
 
 // ---------------------------------------------------------------- K5: sufficient statistics
 // CTA per component a over its K-pairs (n, q) in ascending (n, j) order
@@ -752,30 +759,33 @@ constexpr int kStatsMaxH1 = 17;   // columns of Y per pass
 // write fp64 partials summed by k_stats_reduce in item order (deterministic).
 // Partial layout per item (pass col0): [Y cols col0.. (NH1 x D) | sq (D) |
 // E ((H+1)^2) | N] -- sq/E/N only in the first pass, E only when H+1 <= NH1.
+constexpr int kStatsXChunk = 4;  // phase (i): float4s of the row loaded ahead
 constexpr int kXPad = 4;  // s_x row stride D + 4: conflict-free LDS.128 across rows
 
 template <int NH1, int ND>
 __global__ void __launch_bounds__(kStatsThreads, NH1 > 9 ? 1 : 2) k_stats(StatsArgs a, const int* __restrict__ itemoff,
                                                         int rows_per_item, int col0, double* part,
                                                         int64_t part_stride, int nbuf) {
-  // smem: s_x [nbuf][B][XS] | s_V [D][VS] | s_mu [D+pad] | s_pz [8][B][NH1] | s_zf [B][ZS] (float)
+  // smem: s_x [nbuf][B][XS] | s_V [D][VS] | s_mu [D+pad] | s_pz [8][B][NZ] | s_zf [B][ZS] (float)
   extern __shared__ __align__(16) float s_x[];
-  constexpr int VS = (NH1 + 3) / 4 * 4;  // V row stride (16-byte rows for LDS.128)
-  constexpr int ZS = VS;                 // zhat row stride in s_zf
-  __shared__ double s_qb[kStatsMaxBuf][kStatsBatch];
-  __shared__ int s_e[kStatsMaxBuf][kStatsBatch];
+  // phase (i) computes the NZ latent columns of this pass; the constant column
+  // of [zhat; 1] is implicit (NH1 = 5, 9 passes hold all of H + 1 <= NH1)
+  constexpr int NZ = NH1 == kStatsMaxH1 ? NH1 : NH1 - 1;
+  constexpr int VS = (NZ + 3) / 4 * 4;   // V row stride (16-byte rows for LDS.128)
+  constexpr int ZS = (NH1 + 3) / 4 * 4;  // [zhat;1] row stride in s_zf
   __shared__ double s_red[kStatsThreads / 32];
   __shared__ double s_accE[kStatsThreads];  // E entry of thread tid (fp64)
   __shared__ uint64_t s_xbar[kStatsMaxBuf];  // row-batch arrival (bulk copies, D % 4 == 0)
-  __shared__ int s_eall[kStatsMaxRows];      // the item's entries / responsibilities
-  __shared__ double s_qall[kStatsMaxRows];
+  __shared__ int s_eall[kStatsMaxRows];      // the item's entries
+  __shared__ double s_qall[kStatsMaxRows];   // ... and responsibilities / qmax
+  __shared__ float s_qfall[kStatsMaxRows];   // the same in fp32 (phase ii)
   const Dims dm = a.dm;
   const int H = dm.H, H1 = H + 1, D = dm.D;
   const int XS = (D + 3) / 4 * 4 + kXPad;
   float* s_V = s_x + (int64_t)nbuf * kStatsBatch * XS;
   float* s_mu = s_V + (int64_t)D * VS;
-  float* s_pz = s_mu + (D + 3) / 4 * 4 + 4;  // [8][B][NH1]
-  float* s_zf = s_pz + 8 * kStatsBatch * NH1;  // [B][ZS]
+  float* s_pz = s_mu + (D + 3) / 4 * 4 + 4;  // [8][B][NZ]
+  float* s_zf = s_pz + 8 * kStatsBatch * NZ;  // [B][ZS]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const bool first = col0 == 0;
   const bool full_e = first && (H1 <= NH1);
@@ -785,8 +795,7 @@ __global__ void __launch_bounds__(kStatsThreads, NH1 > 9 ? 1 : 2) k_stats(StatsA
   // upper-triangle entry): its conditioning follows N_c Sigma_z, which fp32
   // sums cannot resolve for collapsed components
   const int Dp = (D + 3) / 4 * 4;
-  const int GX = Dp / 4;
-  const int GD = GX;
+  const int GD = Dp / 4;
   // E: thread = (upper-triangle entry, row group); row groups summed in order at the item end
   const int NE = H1 * (H1 + 1) / 2;
   const int EG = max(1, kStatsThreads / NE);
@@ -808,8 +817,11 @@ __global__ void __launch_bounds__(kStatsThreads, NH1 > 9 ? 1 : 2) k_stats(StatsA
   if (tid == 0)
     for (int i = 0; i < kStatsMaxBuf; ++i) xbar_init(&s_xbar[i]);
   __syncthreads();
-  uint32_t xuse[kStatsMaxBuf] = {0u, 0u, 0u, 0u};  // completed phases per row buffer (same in every thread)
+  uint32_t xpar = 0u;  // bit b: phase parity of row buffer b's barrier (same in every thread)
+#ifdef VMFA_STATS_PROF
   unsigned long long sprof_t = 0;
+  const bool sprof_on = blockIdx.x == 0 && threadIdx.x == 0 && g_stats_prof_on;
+#endif
   __shared__ int s_item;
   // items from a global work queue (dynamic balance; results depend only on the item)
   auto next_item = [&](int cur) -> int {
@@ -823,17 +835,18 @@ __global__ void __launch_bounds__(kStatsThreads, NH1 > 9 ? 1 : 2) k_stats(StatsA
     const int c = find_item(itemoff, dm.C, item);
     const int r0 = a.off[c] + (item - itemoff[c]) * rows_per_item;
     const int r1 = min(a.off[c + 1], r0 + rows_per_item);
+    const int nr = r1 - r0;
     const bool direct = itemoff[c + 1] - itemoff[c] == 1;  // sole item: write the statistics
     // responsibilities are scaled by the item's largest q before the fp32
     // accumulation (no underflow; N_c == 0 exactly iff every q == 0)
     double qmax = 0.0;
     __syncthreads();  // previous item done with the shared buffers
     // the item's entries and responsibilities, staged once (one latency per item)
-    for (int i = r0 + tid; i < r1; i += kStatsThreads) {
-      const int e = a.ent[i];
+    for (int i = tid; i < nr; i += kStatsThreads) {
+      const int e = a.ent[r0 + i];
       const double q = a.resp[e];
-      s_eall[i - r0] = e;
-      s_qall[i - r0] = q;
+      s_eall[i] = e;
+      s_qall[i] = q;
       qmax = fmax(qmax, q);
     }
 #pragma unroll
@@ -841,7 +854,7 @@ __global__ void __launch_bounds__(kStatsThreads, NH1 > 9 ? 1 : 2) k_stats(StatsA
     if (lane == 0) s_red[warp] = qmax;
     for (int i = tid; i < D * VS; i += kStatsThreads) {
       const int d = i / VS, h = i - d * VS;
-      s_V[i] = (h < NH1 && col0 + h < H) ? __ldg(a.V32 + (int64_t)c * D * H + (int64_t)d * H + col0 + h) : 0.f;
+      s_V[i] = (h < NZ && col0 + h < H) ? __ldg(a.V32 + (int64_t)c * D * H + (int64_t)d * H + col0 + h) : 0.f;
     }
     for (int d = tid; d < Dp + 4; d += kStatsThreads) s_mu[d] = d < D ? __ldg(a.mu32 + (int64_t)c * D + d) : 0.f;
     __syncthreads();
@@ -849,103 +862,103 @@ __global__ void __launch_bounds__(kStatsThreads, NH1 > 9 ? 1 : 2) k_stats(StatsA
 #pragma unroll
     for (int w = 0; w < kStatsThreads / 32; ++w) qmax = fmax(qmax, s_red[w]);
     const double qdiv = qmax > 0.0 ? qmax : 1.0;  // divide (1/qmax overflows for denormal qmax)
+    // every thread rescales the entries it staged (read after the first batch's barriers)
+    for (int i = tid; i < nr; i += kStatsThreads) {
+      const double q = s_qall[i] / qdiv;
+      s_qall[i] = q;
+      s_qfall[i] = static_cast<float>(q);
+    }
     float accY[ND][4][NH1];
     float accS[ND][4];
+    float mreg[ND][4];  // this thread's mean entries (phase ii)
     if (ei >= 0) s_accE[tid] = 0.0;
 #pragma unroll
     for (int k = 0; k < ND; ++k)
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         accS[k][i] = 0.f;
+        mreg[k][i] = s_mu[min(4 * (my_dg + k * GD) + i, Dp + 3)];
 #pragma unroll
         for (int h = 0; h < NH1; ++h) accY[k][i][h] = 0.f;
       }
-    const int nbat = (r1 - r0 + kStatsBatch - 1) / kStatsBatch;
-    auto stage_ids = [&](int b, int buf) {
-      if (tid < kStatsBatch) {
-        const int i = b * kStatsBatch + tid;
-        const bool in = r0 + i < r1;
-        s_e[buf][tid] = in ? s_eall[i] : -1;
-        s_qb[buf][tid] = in ? s_qall[i] / qdiv : 0.0;
-      }
-    };
-    auto issue_rows = [&](int buf) {
+    const int nbat = (nr + kStatsBatch - 1) / kStatsBatch;
+    auto issue_rows = [&](int b, int buf) {
       float* dst = s_x + (int64_t)buf * kStatsBatch * XS;
+      const int nb = min(kStatsBatch, nr - b * kStatsBatch);
+      const int* eb = s_eall + b * kStatsBatch;
       if (vec) {
         // one bulk copy per row, issued by four lanes of every warp (the
         // copies of a warp are issued one after another, so the batch is
         // spread over the warps); thread 0 arms the barrier with the total
         // (a copy may complete before the arm: the transaction count is signed)
-        if (tid == 0) {
-          int nv = 0;
-          for (int r = 0; r < kStatsBatch; ++r) nv += s_e[buf][r] >= 0;
-          xbar_expect(&s_xbar[buf], static_cast<uint32_t>(nv) * D * 4u);
-        }
+        if (tid == 0) xbar_expect(&s_xbar[buf], static_cast<uint32_t>(nb) * D * 4u);
         if (lane < kStatsBatch / (kStatsThreads / 32)) {
           const int r = warp * (kStatsBatch / (kStatsThreads / 32)) + lane;
-          const int e = s_e[buf][r];
-          if (e >= 0)
-            bulk_row(smem_addr(dst + (int64_t)r * XS), a.X + (int64_t)(e / dm.Cp) * D, D * 4u, &s_xbar[buf]);
+          if (r < nb) bulk_row(smem_addr(dst + (int64_t)r * XS), a.X + (int64_t)(eb[r] / dm.Cp) * D, D * 4u, &s_xbar[buf]);
         }
       } else {
-        for (int i = tid; i < kStatsBatch * D; i += kStatsThreads) {
+        for (int i = tid; i < nb * D; i += kStatsThreads) {
           const int r = i / D, f = i - r * D;
-          const int e = s_e[buf][r];
-          if (e < 0) continue;
-          const float* src = a.X + (int64_t)(e / dm.Cp) * D + f;
+          const float* src = a.X + (int64_t)(eb[r] / dm.Cp) * D + f;
           const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(dst + (int64_t)r * XS + f));
           asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(src) : "memory");
         }
+        asm volatile("cp.async.commit_group;" ::: "memory");
       }
-      asm volatile("cp.async.commit_group;" ::: "memory");
     };
-    // ring of nbuf row buffers: batches are issued nbuf - 1 ahead (bulk path);
-    // the cp.async path keeps one batch ahead with nbuf <= 2
-    const int ahead = vec ? nbuf - 1 : 1;
-    for (int b = 0; b < (vec ? min(ahead, nbat) : 1); ++b) {
-      stage_ids(b, b % nbuf);
-      __syncthreads();
-      issue_rows(b % nbuf);
-    }
+    // ring of nbuf row buffers: batch bi + nbuf - 1 is issued once every
+    // thread has passed batch bi's first barrier (its buffer's last readers,
+    // batch bi - 1, are done); two barriers per batch
+    for (int b = 0; b < min(nbuf - 1, nbat); ++b) issue_rows(b, b);
     for (int bi = 0; bi < nbat; ++bi) {
       const int buf = bi % nbuf;
-      const int b0 = r0 + bi * kStatsBatch;
-      const int nb = min(kStatsBatch, r1 - b0);
+      const int nb = min(kStatsBatch, nr - bi * kStatsBatch);
       SPROF(0);
+      if (nbuf == 1) issue_rows(bi, 0);
       if (vec) {
-        if (bi + ahead < nbat) {
-          stage_ids(bi + ahead, (bi + ahead) % nbuf);
-          __syncthreads();
-          issue_rows((bi + ahead) % nbuf);
-        }
-      } else if (nbuf == 1) {
-        if (bi > 0) {
-          stage_ids(bi, 0);
-          __syncthreads();
-          issue_rows(0);
-        }
-        if (!vec) asm volatile("cp.async.wait_group 0;" ::: "memory");
-      } else if (bi + 1 < nbat) {
-        stage_ids(bi + 1, buf ^ 1);
-        __syncthreads();
-        issue_rows(buf ^ 1);
-        asm volatile("cp.async.wait_group 1;" ::: "memory");
+        xbar_wait(&s_xbar[buf], (xpar >> buf) & 1u);
+        xpar ^= 1u << buf;
       } else {
-        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        asm volatile("cp.async.wait_group 0;" ::: "memory");  // batch bi is the only group in flight
+        __syncthreads();
       }
-      SPROF(1);
-      if (vec) xbar_wait(&s_xbar[buf], xuse[buf]++ & 1u);
       SPROF(2);
-      __syncthreads();
-      SPROF(3);
       const float* xb = s_x + (int64_t)buf * kStatsBatch * XS;
       // (i) partial mz over this warp's dimension slice, lane = row
       {
-        float acc[NH1];
+        float acc[NZ];
 #pragma unroll
-        for (int h = 0; h < NH1; ++h) acc[h] = 0.f;
+        for (int h = 0; h < NZ; ++h) acc[h] = 0.f;
         const float* xr = xb + (int64_t)lane * XS;
-        if (lane < nb) {
+        if (lane < nb && vec) {
+          // chunks of 4 * kStatsXChunk dimensions: the row's chunk is loaded first (ILP), then
+          // the broadcast V rows stream through the FMAs
+          for (int d0 = dw0; d0 < dw1; d0 += 4 * kStatsXChunk) {
+            float4 xv[kStatsXChunk];
+#pragma unroll
+            for (int j = 0; j < kStatsXChunk; ++j)
+              if (d0 + 4 * j < dw1) xv[j] = *reinterpret_cast<const float4*>(xr + d0 + 4 * j);
+#pragma unroll
+            for (int j = 0; j < kStatsXChunk; ++j) {
+              const int d = d0 + 4 * j;
+              if (d >= dw1) break;
+              const float4 mv = *reinterpret_cast<const float4*>(s_mu + d);
+              const float v4[4] = {xv[j].x - mv.x, xv[j].y - mv.y, xv[j].z - mv.z, xv[j].w - mv.w};
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                const float* vr = s_V + (d + k) * VS;
+#pragma unroll
+                for (int h4 = 0; h4 < VS; h4 += 4) {
+                  const float4 w = *reinterpret_cast<const float4*>(vr + h4);
+                  if (h4 + 0 < NZ) acc[h4 + 0] = fmaf(w.x, v4[k], acc[h4 + 0]);
+                  if (h4 + 1 < NZ) acc[h4 + 1] = fmaf(w.y, v4[k], acc[h4 + 1]);
+                  if (h4 + 2 < NZ) acc[h4 + 2] = fmaf(w.z, v4[k], acc[h4 + 2]);
+                  if (h4 + 3 < NZ) acc[h4 + 3] = fmaf(w.w, v4[k], acc[h4 + 3]);
+                }
+              }
+            }
+          }
+        } else if (lane < nb) {
           for (int d = dw0; d < dw1; d += 4) {
             const float4 xv = *reinterpret_cast<const float4*>(xr + d);
             const float4 mv = *reinterpret_cast<const float4*>(s_mu + d);
@@ -957,37 +970,41 @@ __global__ void __launch_bounds__(kStatsThreads, NH1 > 9 ? 1 : 2) k_stats(StatsA
 #pragma unroll
               for (int h4 = 0; h4 < VS; h4 += 4) {
                 const float4 w = *reinterpret_cast<const float4*>(vr + h4);
-                if (h4 + 0 < NH1) acc[h4 + 0] = fmaf(w.x, v4[k], acc[h4 + 0]);
-                if (h4 + 1 < NH1) acc[h4 + 1] = fmaf(w.y, v4[k], acc[h4 + 1]);
-                if (h4 + 2 < NH1) acc[h4 + 2] = fmaf(w.z, v4[k], acc[h4 + 2]);
-                if (h4 + 3 < NH1) acc[h4 + 3] = fmaf(w.w, v4[k], acc[h4 + 3]);
+                if (h4 + 0 < NZ) acc[h4 + 0] = fmaf(w.x, v4[k], acc[h4 + 0]);
+                if (h4 + 1 < NZ) acc[h4 + 1] = fmaf(w.y, v4[k], acc[h4 + 1]);
+                if (h4 + 2 < NZ) acc[h4 + 2] = fmaf(w.z, v4[k], acc[h4 + 2]);
+                if (h4 + 3 < NZ) acc[h4 + 3] = fmaf(w.w, v4[k], acc[h4 + 3]);
               }
             }
           }
         }
-        float* pz = s_pz + ((int64_t)warp * kStatsBatch + lane) * NH1;
+        float* pz = s_pz + ((int64_t)warp * kStatsBatch + lane) * NZ;
 #pragma unroll
-        for (int h = 0; h < NH1; ++h) pz[h] = acc[h];
+        for (int h = 0; h < NZ; ++h) pz[h] = acc[h];
       }
       SPROF(4);
       __syncthreads();
       SPROF(5);
+      if (nbuf >= 2 && bi + nbuf - 1 < nbat) issue_rows(bi + nbuf - 1, (bi + nbuf - 1) % nbuf);
+      SPROF(9);
       for (int i = tid; i < kStatsBatch * ZS; i += kStatsThreads) {
         const int r = i / ZS, h = i - r * ZS;
+        const int hh = col0 + h;
         float z = 0.f;
-        if (h < NH1) {
+        if (h < NZ && hh < H) {
 #pragma unroll
-          for (int w = 0; w < 8; ++w) z += s_pz[((int64_t)w * kStatsBatch + r) * NH1 + h];
-          const int hh = col0 + h;
-          z = hh < H ? z : (hh == H ? 1.f : 0.f);
+          for (int w = 0; w < 8; ++w) z += s_pz[((int64_t)w * kStatsBatch + r) * NZ + h];
+        } else if (h < NH1 && hh == H) {
+          z = 1.f;
         }
         s_zf[i] = z;
       }
       SPROF(6);
       __syncthreads();
       SPROF(7);
+      const double* s_q = s_qall + bi * kStatsBatch;
+      const float* s_qf = s_qfall + bi * kStatsBatch;
       if (ei >= 0) {  // E(ei, ej) += q z_i z_j: fp32 z products are exact in fp64
-        const double* s_q = s_qb[buf];
         double acc = s_accE[tid];
         for (int r = eg; r < nb; r += EG)
           acc = fma(s_q[r], static_cast<double>(s_zf[r * ZS + ei]) * static_cast<double>(s_zf[r * ZS + ej]), acc);
@@ -995,14 +1012,15 @@ __global__ void __launch_bounds__(kStatsThreads, NH1 > 9 ? 1 : 2) k_stats(StatsA
       }
       // (ii) register tiles: 4 "dimensions" x NH1 columns, rows my_rg::RG
       if (tile_on) {
-        const double* s_q = s_qb[buf];
         for (int r = my_rg; r < nb; r += RG) {
-          const float qf = static_cast<float>(s_q[r]);
+          const float qf = s_qf[r];
           const float* xr = xb + (int64_t)r * XS;
-          const float* zr = s_zf + r * ZS;
-          float zf[NH1];
+          float zf[ZS];
 #pragma unroll
-          for (int h = 0; h < NH1; ++h) zf[h] = zr[h];
+          for (int h4 = 0; h4 < ZS; h4 += 4) {
+            const float4 z4 = *reinterpret_cast<const float4*>(s_zf + r * ZS + h4);
+            zf[h4] = z4.x, zf[h4 + 1] = z4.y, zf[h4 + 2] = z4.z, zf[h4 + 3] = z4.w;
+          }
 #pragma unroll
           for (int k = 0; k < ND; ++k) {
             const int g = my_dg + k * GD;
@@ -1011,11 +1029,10 @@ __global__ void __launch_bounds__(kStatsThreads, NH1 > 9 ? 1 : 2) k_stats(StatsA
             const int d = 4 * g;
             if (vec || d + 3 < D) {
               const float4 xv = *reinterpret_cast<const float4*>(xr + d);
-              const float4 mv = *reinterpret_cast<const float4*>(s_mu + d);
-              vs[0] = xv.x - mv.x, vs[1] = xv.y - mv.y, vs[2] = xv.z - mv.z, vs[3] = xv.w - mv.w;
+              vs[0] = xv.x - mreg[k][0], vs[1] = xv.y - mreg[k][1], vs[2] = xv.z - mreg[k][2], vs[3] = xv.w - mreg[k][3];
             } else {
 #pragma unroll
-              for (int i = 0; i < 4; ++i) vs[i] = d + i < D ? xr[d + i] - s_mu[d + i] : 0.f;
+              for (int i = 0; i < 4; ++i) vs[i] = d + i < D ? xr[d + i] - mreg[k][i] : 0.f;
             }
             float qv[4];
 #pragma unroll
@@ -1032,8 +1049,7 @@ __global__ void __launch_bounds__(kStatsThreads, NH1 > 9 ? 1 : 2) k_stats(StatsA
         }
       }
       SPROF(8);
-      __syncthreads();
-      SPROF(9);
+      if (nbuf == 1) __syncthreads();  // the next issue reuses this batch's buffer
     }
     // combine the row groups of each dimension group through smem (fp64),
     // reusing the row buffers, then write (direct or partial) scaled by qmax
@@ -1864,10 +1880,11 @@ template <int NH1>
 static void stats_pass(const StatsArgs& a, const int* itemoff, int rpi, int grid, int col0,
                        double* part, int64_t ps, cudaStream_t s) {
   const int D = a.dm.D;
-  constexpr int VS = (NH1 + 3) / 4 * 4;
+  constexpr int NZ = NH1 == kStatsMaxH1 ? NH1 : NH1 - 1;
+  constexpr int VS = (NZ + 3) / 4 * 4, ZS = (NH1 + 3) / 4 * 4;
   const size_t XS = (D + 3) / 4 * 4 + kXPad;
-  const size_t fixed = (static_cast<size_t>(D) * VS + (D + 3) / 4 * 4 + 4 + 8 * kStatsBatch * NH1 +
-                        kStatsBatch * VS + 8) * sizeof(float);
+  const size_t fixed = (static_cast<size_t>(D) * VS + (D + 3) / 4 * 4 + 4 + 8 * kStatsBatch * NZ +
+                        kStatsBatch * ZS + 8) * sizeof(float);
   const size_t per_buf = static_cast<size_t>(kStatsBatch) * XS * sizeof(float);
   // the row-group reduction reuses the row buffers: RG-1 slices of GD*4*(NH1+1) doubles
   const int GD = (D + 3) / 4;

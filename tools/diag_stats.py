@@ -1,4 +1,8 @@
-"""Phase timing of k_stats on CTA 0 (diagnostics; vmfa_diag_stats_cycles)."""
+"""Phase timing of k_stats on CTA 0 (diagnostics; vmfa_diag_stats_cycles).
+
+Needs a library built with the marks compiled in:
+    VMFA_NVCC_EXTRA=-DVMFA_STATS_PROF python -c "from paper_2501_12299_b200 import build as B; B.build(force=True)"
+"""
 import ctypes as C
 import os
 import sys
@@ -27,10 +31,11 @@ f.argtypes = [C.c_int, C.c_void_p]
 out = np.zeros(16, np.uint64)
 f(1, None)
 s.variational_e_step(0, 10)
+import time
 s.accumulate_suffstats()
 f(1, out.ctypes.data_as(C.c_void_p))
 f(0, None)
-names = ["", "stage+sync+issue", "wait rows", "sync", "phase i", "sync", "z reduce", "sync", "E + phase ii", "sync"]
+names = ["", "-", "wait rows", "-", "phase i", "sync A", "z reduce", "sync B", "E + phase ii", "issue"]
 tot = out[1:10].sum()
 for i in range(1, 10):
     print(f"{names[i]:18s} {int(out[i]):12d} {100 * out[i] / tot:5.1f}%")
