@@ -693,8 +693,8 @@ __global__ void __launch_bounds__(kGupdThreads) k_gselect_dense(Dims dm, long lo
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
-__device__ __forceinline__ void xbar_init(uint64_t* bar) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(bar)) : "memory");
+__device__ __forceinline__ void xbar_init(uint64_t* bar, int count = 1) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
 __device__ __forceinline__ void xbar_expect(uint64_t* bar, uint32_t bytes) {
@@ -776,7 +776,7 @@ __global__ void __launch_bounds__(kStatsThreads, NH1 > 9 ? 1 : 2) k_stats(StatsA
   __shared__ double s_red[kStatsThreads / 32];
   __shared__ double s_accE[kStatsThreads];  // E entry of thread tid (fp64)
   __shared__ uint64_t s_xbar[kStatsMaxBuf];  // row-batch arrival (bulk copies, D % 4 == 0)
-  __shared__ int s_eall[kStatsMaxRows];      // the item's entries
+  __shared__ int s_eall[kStatsMaxRows];      // the item's rows of X
   __shared__ double s_qall[kStatsMaxRows];   // ... and responsibilities / qmax
   __shared__ float s_qfall[kStatsMaxRows];   // the same in fp32 (phase ii)
   const Dims dm = a.dm;
@@ -786,6 +786,7 @@ __global__ void __launch_bounds__(kStatsThreads, NH1 > 9 ? 1 : 2) k_stats(StatsA
   float* s_mu = s_V + (int64_t)D * VS;
   float* s_pz = s_mu + (D + 3) / 4 * 4 + 4;  // [8][B][NZ]
   float* s_zf = s_pz + 8 * kStatsBatch * NZ;  // [B][ZS]
+  double* s_zd = reinterpret_cast<double*>(s_zf + kStatsBatch * ZS);  // [B][ZS] (E)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const bool first = col0 == 0;
   const bool full_e = first && (H1 <= NH1);
@@ -814,8 +815,12 @@ __global__ void __launch_bounds__(kStatsThreads, NH1 > 9 ? 1 : 2) k_stats(StatsA
   const int dsl = ((D + 7) / 8 + 3) / 4 * 4;  // phase (i) dims per warp, multiple of 4
   const int dw0 = warp * dsl, dw1 = min(D, dw0 + dsl);
   const int total = __ldg(itemoff + dm.C);
+  // row gather: one bulk copy per row (D % 4 == 0; lane-parallel 16-byte
+  // cp.async measured slower), else 4-byte cp.async with completion tracked by
+  // the buffer's mbarrier (every thread's cp.async.mbarrier.arrive.noinc)
+  const bool bulk = vec;
   if (tid == 0)
-    for (int i = 0; i < kStatsMaxBuf; ++i) xbar_init(&s_xbar[i]);
+    for (int i = 0; i < kStatsMaxBuf; ++i) xbar_init(&s_xbar[i], bulk ? 1 : kStatsThreads);
   __syncthreads();
   uint32_t xpar = 0u;  // bit b: phase parity of row buffer b's barrier (same in every thread)
 #ifdef VMFA_STATS_PROF
@@ -845,7 +850,7 @@ __global__ void __launch_bounds__(kStatsThreads, NH1 > 9 ? 1 : 2) k_stats(StatsA
     for (int i = tid; i < nr; i += kStatsThreads) {
       const int e = a.ent[r0 + i];
       const double q = a.resp[e];
-      s_eall[i] = e;
+      s_eall[i] = e / dm.Cp;  // the row of X
       s_qall[i] = q;
       qmax = fmax(qmax, q);
     }
@@ -886,7 +891,7 @@ __global__ void __launch_bounds__(kStatsThreads, NH1 > 9 ? 1 : 2) k_stats(StatsA
       float* dst = s_x + (int64_t)buf * kStatsBatch * XS;
       const int nb = min(kStatsBatch, nr - b * kStatsBatch);
       const int* eb = s_eall + b * kStatsBatch;
-      if (vec) {
+      if (bulk) {
         // one bulk copy per row, issued by four lanes of every warp (the
         // copies of a warp are issued one after another, so the batch is
         // spread over the warps); thread 0 arms the barrier with the total
@@ -894,16 +899,16 @@ __global__ void __launch_bounds__(kStatsThreads, NH1 > 9 ? 1 : 2) k_stats(StatsA
         if (tid == 0) xbar_expect(&s_xbar[buf], static_cast<uint32_t>(nb) * D * 4u);
         if (lane < kStatsBatch / (kStatsThreads / 32)) {
           const int r = warp * (kStatsBatch / (kStatsThreads / 32)) + lane;
-          if (r < nb) bulk_row(smem_addr(dst + (int64_t)r * XS), a.X + (int64_t)(eb[r] / dm.Cp) * D, D * 4u, &s_xbar[buf]);
+          if (r < nb) bulk_row(smem_addr(dst + (int64_t)r * XS), a.X + (int64_t)eb[r] * D, D * 4u, &s_xbar[buf]);
         }
       } else {
         for (int i = tid; i < nb * D; i += kStatsThreads) {
           const int r = i / D, f = i - r * D;
-          const float* src = a.X + (int64_t)(eb[r] / dm.Cp) * D + f;
+          const float* src = a.X + (int64_t)eb[r] * D + f;
           const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(dst + (int64_t)r * XS + f));
           asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(src) : "memory");
         }
-        asm volatile("cp.async.commit_group;" ::: "memory");
+        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_addr(&s_xbar[buf])) : "memory");
       }
     };
     // ring of nbuf row buffers: batch bi + nbuf - 1 is issued once every
@@ -915,13 +920,8 @@ __global__ void __launch_bounds__(kStatsThreads, NH1 > 9 ? 1 : 2) k_stats(StatsA
       const int nb = min(kStatsBatch, nr - bi * kStatsBatch);
       SPROF(0);
       if (nbuf == 1) issue_rows(bi, 0);
-      if (vec) {
-        xbar_wait(&s_xbar[buf], (xpar >> buf) & 1u);
-        xpar ^= 1u << buf;
-      } else {
-        asm volatile("cp.async.wait_group 0;" ::: "memory");  // batch bi is the only group in flight
-        __syncthreads();
-      }
+      xbar_wait(&s_xbar[buf], (xpar >> buf) & 1u);
+      xpar ^= 1u << buf;
       SPROF(2);
       const float* xb = s_x + (int64_t)buf * kStatsBatch * XS;
       // (i) partial mz over this warp's dimension slice, lane = row
@@ -998,42 +998,54 @@ __global__ void __launch_bounds__(kStatsThreads, NH1 > 9 ? 1 : 2) k_stats(StatsA
           z = 1.f;
         }
         s_zf[i] = z;
+        s_zd[i] = z;
       }
       SPROF(6);
       __syncthreads();
       SPROF(7);
       const double* s_q = s_qall + bi * kStatsBatch;
       const float* s_qf = s_qfall + bi * kStatsBatch;
-      if (ei >= 0) {  // E(ei, ej) += q z_i z_j: fp32 z products are exact in fp64
+      if (ei >= 0) {  // E(ei, ej) += q z_i z_j (z kept in fp64 too: fp32 z products are exact in fp64)
         double acc = s_accE[tid];
-        for (int r = eg; r < nb; r += EG)
-          acc = fma(s_q[r], static_cast<double>(s_zf[r * ZS + ei]) * static_cast<double>(s_zf[r * ZS + ej]), acc);
+        for (int r = eg; r < nb; r += EG) acc = fma(s_q[r], s_zd[r * ZS + ei] * s_zd[r * ZS + ej], acc);
         s_accE[tid] = acc;
       }
-      // (ii) register tiles: 4 "dimensions" x NH1 columns, rows my_rg::RG
+      // (ii) register tiles: 4 "dimensions" x NH1 columns, rows my_rg::RG;
+      // rows in pairs: both rows' operands are loaded before the FMAs
       if (tile_on) {
-        for (int r = my_rg; r < nb; r += RG) {
-          const float qf = s_qf[r];
-          const float* xr = xb + (int64_t)r * XS;
-          float zf[ZS];
+        auto load_row = [&](int r, float4 (&xo)[ND], float (&zo)[NH1], float& qo) {
+          qo = s_qf[r];
+          const float* zr = s_zf + r * ZS;
 #pragma unroll
-          for (int h4 = 0; h4 < ZS; h4 += 4) {
-            const float4 z4 = *reinterpret_cast<const float4*>(s_zf + r * ZS + h4);
-            zf[h4] = z4.x, zf[h4 + 1] = z4.y, zf[h4 + 2] = z4.z, zf[h4 + 3] = z4.w;
-          }
-#pragma unroll
-          for (int k = 0; k < ND; ++k) {
-            const int g = my_dg + k * GD;
-            if (k > 0 && g >= GD) break;
-            float vs[4];
-            const int d = 4 * g;
-            if (vec || d + 3 < D) {
-              const float4 xv = *reinterpret_cast<const float4*>(xr + d);
-              vs[0] = xv.x - mreg[k][0], vs[1] = xv.y - mreg[k][1], vs[2] = xv.z - mreg[k][2], vs[3] = xv.w - mreg[k][3];
+          for (int h4 = 0; h4 < NH1; h4 += 4) {
+            if (h4 + 4 <= NH1) {
+              const float4 z4 = *reinterpret_cast<const float4*>(zr + h4);
+              zo[h4] = z4.x, zo[h4 + 1] = z4.y, zo[h4 + 2] = z4.z, zo[h4 + 3] = z4.w;
             } else {
 #pragma unroll
-              for (int i = 0; i < 4; ++i) vs[i] = d + i < D ? xr[d + i] - mreg[k][i] : 0.f;
+              for (int h = h4; h < NH1; ++h) zo[h] = zr[h];
             }
+          }
+          const float* xr = xb + (int64_t)r * XS;
+#pragma unroll
+          for (int k = 0; k < ND; ++k) {
+            const int d = 4 * (my_dg + k * GD);
+            if (vec || d + 3 < D) {
+              xo[k] = *reinterpret_cast<const float4*>(xr + d);
+            } else {  // tail dimensions contribute v = 0
+              xo[k].x = d + 0 < D ? xr[d + 0] : mreg[k][0];
+              xo[k].y = d + 1 < D ? xr[d + 1] : mreg[k][1];
+              xo[k].z = d + 2 < D ? xr[d + 2] : mreg[k][2];
+              xo[k].w = d + 3 < D ? xr[d + 3] : mreg[k][3];
+            }
+          }
+        };
+        auto fma_row = [&](const float4 (&xv)[ND], const float (&zv)[NH1], float qf) {
+#pragma unroll
+          for (int k = 0; k < ND; ++k) {
+            if (k > 0 && my_dg + k * GD >= GD) break;
+            const float vs[4] = {xv[k].x - mreg[k][0], xv[k].y - mreg[k][1], xv[k].z - mreg[k][2],
+                                 xv[k].w - mreg[k][3]};
             float qv[4];
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
@@ -1043,9 +1055,26 @@ __global__ void __launch_bounds__(kStatsThreads, NH1 > 9 ? 1 : 2) k_stats(StatsA
 #pragma unroll
             for (int h = 0; h < NH1; ++h) {
 #pragma unroll
-              for (int i = 0; i < 4; ++i) accY[k][i][h] = fmaf(qv[i], zf[h], accY[k][i][h]);
+              for (int i = 0; i < 4; ++i) accY[k][i][h] = fmaf(qv[i], zv[h], accY[k][i][h]);
             }
           }
+        };
+        int r = my_rg;
+        for (; r + RG < nb; r += 2 * RG) {  // two rows' operands in flight
+          float4 xa[ND], xb2[ND];
+          float za[NH1], zb[NH1];
+          float qa, qb;
+          load_row(r, xa, za, qa);
+          load_row(r + RG, xb2, zb, qb);
+          fma_row(xa, za, qa);
+          fma_row(xb2, zb, qb);
+        }
+        if (r < nb) {
+          float4 xa[ND];
+          float za[NH1];
+          float qa;
+          load_row(r, xa, za, qa);
+          fma_row(xa, za, qa);
         }
       }
       SPROF(8);
@@ -1884,7 +1913,7 @@ static void stats_pass(const StatsArgs& a, const int* itemoff, int rpi, int grid
   constexpr int VS = (NZ + 3) / 4 * 4, ZS = (NH1 + 3) / 4 * 4;
   const size_t XS = (D + 3) / 4 * 4 + kXPad;
   const size_t fixed = (static_cast<size_t>(D) * VS + (D + 3) / 4 * 4 + 4 + 8 * kStatsBatch * NZ +
-                        kStatsBatch * ZS + 8) * sizeof(float);
+                        kStatsBatch * ZS + 8) * sizeof(float) + kStatsBatch * ZS * sizeof(double);
   const size_t per_buf = static_cast<size_t>(kStatsBatch) * XS * sizeof(float);
   // the row-group reduction reuses the row buffers: RG-1 slices of GD*4*(NH1+1) doubles
   const int GD = (D + 3) / 4;
@@ -1896,7 +1925,7 @@ static void stats_pass(const StatsArgs& a, const int* itemoff, int rpi, int grid
   }();
   int nbuf = (2 * per_buf + fixed <= 200 * 1024) ? 2 : 1;
   if (static_cast<size_t>(nbuf) * per_buf < red) nbuf = 2;
-  if (a.dm.D % 4 == 0)  // bulk-copy path: deeper ring when it fits
+  if (want > 2)  // deeper ring when it fits
     for (int nb = std::min(kStatsMaxBuf, want > 0 ? want : 2); nb > nbuf; --nb)
       if (nb * per_buf + fixed <= 200 * 1024) {
         nbuf = nb;
