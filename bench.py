@@ -45,6 +45,7 @@ def parse():
     ap.add_argument("--n", type=int, default=0, help="override rows per rank (testing only)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-exact-ll", action="store_true")
     ap.add_argument("--profile-only", action="store_true",
                     help="run warm-up + 2 steps only (for ncu launch lists)")
     return ap.parse_args()
@@ -355,6 +356,28 @@ def main():
     ach_tfs = J_local * Fj / (sc_ms * 1e-3) / 1e12 if sc_ms > 0 else None
     phase_ms = {k: v["ms"] / args.steps for k, v in kt.items()}
 
+    # exact log-likelihood (all N x C pairs, dense
+    # tcgen05 pass) once after the timed region, on device time
+    exact = None
+    if not args.no_exact_ll:
+        try:
+            sess.exact_log_likelihood()  # first call allocates its buffers
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(ext)
+            ll = sess.exact_log_likelihood()
+            e1.record(ext)
+            e1.synchronize()
+            t = e0.elapsed_time(e1)
+            pairs = float(b - a) * C
+            exact = {"ms": t, "log_likelihood": ll, "joints": pairs, "joints_per_s": pairs / (t * 1e-3),
+                     "achieved_tflops": pairs * Fj / (t * 1e-3) / 1e12,
+                     "roof_ms": max((b - a) * D * 4 / (pk["hbm"] * 1e9), pairs * Fj / (pk["bf16"] * 1e12 / 3)) * 1e3,
+                     "roof": "max(X once at HBM peak, N*C*F_j at bf16-dense/3 (3-pass fp16 split))",
+                     "how": "one vmfa_exact_log_likelihood call (images, row-tile-major dense jobs, "
+                            "per-row LSE, fixed-order sum) between CUDA events"}
+        except Exception as ex:
+            exact = {"error": str(ex)}
+
     # launches per step (CUPTI), outside the timed region
     n_launch, names = count_launches(sess, step)
 
@@ -420,6 +443,7 @@ def main():
                          "per_unit": f"B_j = 4D+8 = {Bj} B per joint (SURVEY §8(d)), J={J_local:.0f} joints per launch pair",
                          "flops_view": {"achieved_tflops": ach_tfs, "F_j": Fj}},
             "iteration_roofline": iter_roof,
+            "exact_ll": exact,
             "gpu_launches": int(n_launch * args.steps),
             "launches_per_step": n_launch,
             "clocks": clk_sum,

@@ -10,6 +10,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <limits>
 #include <vector>
 
 #include "vmfa_b200.h"
@@ -47,11 +48,12 @@ enum KernelFamily : int {
   kFamScoreTruncF,
   kFamSort,
   kFamOther,
+  kFamExactLL,
   kNumFamilies
 };
 const char* const kFamilyNames[kNumFamilies] = {
     "score_anchor", "score_extra", "select", "gupdate", "stats",
-    "update", "precompute", "score_truncF", "csr_sort", "other"};
+    "update", "precompute", "score_truncF", "csr_sort", "other", "exact_ll"};
 
 __global__ void k_pack_scalar_u64(const unsigned long long* src, double* dst) { *dst = static_cast<double>(*src); }
 __global__ void k_add_f64(const double* src, double* dst) { *dst = *src; }
@@ -139,6 +141,13 @@ struct vmfa_ctx {
   unsigned long long* st_update = nullptr;
   IterStatus* hstat = nullptr;  // pinned host readback of one iteration's statuses and scalars
   int* n_empty = nullptr;
+  // exact_log_likelihood's dense pass (allocated on first use)
+  int *dense_g = nullptr, *dense_gcnt = nullptr, *dense_ent = nullptr, *dense_items = nullptr,
+      *dense_off = nullptr;
+  int4* dense_jobs = nullptr;
+  float* dense_LJ = nullptr;
+  double *dense_lse = nullptr, *dense_out = nullptr;
+  int64_t dense_R = 0;
   bool kinv_for_current_K = false;
   // the anchor pass of the next E-step already ran (under the current K, g
   // and parameters) while computing the truncated free energy: LJ's anchor
@@ -1142,10 +1151,77 @@ int vmfa_truncated_free_energy(vmfa_ctx* x, double* F) {
   return VMFA_OK;
 }
 
+// exact_log_likelihood (model.cpp:139-148): sum over this context's rows of
+// LSE_c l(n, c) over all C components, through the scorer's anchor pass on
+// pseudo-anchor blocks (launch_dense_chunk; the warp-specialised tcgen05
+// scorer, or the single-role one for shapes it does not take); rows in
+// chunks of <= 1 GiB of log-joints. Leaves K, g, LJ and the lookahead state
+// untouched (only the anchor B images / records are overwritten, which the
+// next E-step rebuilds whenever it runs its own anchor pass).
 int vmfa_exact_log_likelihood(vmfa_ctx* x, double* ll) {
   TRY(check_ctx(x));
-  (void)ll;
-  return fail(VMFA_ERR_UNSUPPORTED, "exact_log_likelihood is SURVEY §8(f) 'next' item 1 (not in this build)");
+  if (!ll) return fail(VMFA_ERR_INVALID_ARGUMENT, "null output");
+  const Dims& dm = x->dm;
+  const int C = dm.C, G = dm.G, D = dm.D;
+  const int nb = (C + G - 1) / G;
+  const int SL = nb * G;
+  int64_t R = std::max<int64_t>(128, (int64_t(1) << 30) / (4 * static_cast<int64_t>(SL)));
+  R = std::min<int64_t>(R, (std::numeric_limits<int>::max() - nb) / nb);  // flat entries n * nb + b
+  R = std::min<int64_t>(R, dm.N);
+  if (!x->dense_g) {
+    TRY(x->alloc(x->dense_g, static_cast<size_t>(C) * G));
+    TRY(x->alloc(x->dense_gcnt, C));
+    TRY(x->alloc(x->dense_items, C + 1));
+    TRY(x->alloc(x->dense_off, C + 1));
+    TRY(x->alloc(x->dense_ent, static_cast<size_t>(nb) * R));
+    TRY(x->alloc(x->dense_jobs, static_cast<size_t>(dense_jobs(nb, static_cast<int>(R)))));
+    TRY(x->alloc(x->dense_LJ, static_cast<size_t>(R) * SL));
+    TRY(x->alloc(x->dense_lse, dm.N));
+    TRY(x->alloc(x->dense_out, 1));
+    x->dense_R = R;
+  }
+  R = std::min<int64_t>(R, x->dense_R);
+  cudaStream_t s = x->stream;
+  const int tok = x->begin(kFamExactLL, dm.N * static_cast<int64_t>(C));
+  const bool ws = x->scorer == 2;
+  CU(launch_dense_groups(C, G, x->dense_g, x->dense_gcnt, s));
+  if (ws) {
+    CU(launch_ws_images(dm, 0, x->WT, x->mu32, x->ipsi32, x->dense_g, x->dense_gcnt, x->bimg, x->bscl, s));
+    CU(launch_ws_records(dm, 0, x->WT, x->mu32, x->ipsi32, x->kconst, x->dense_g, x->dense_gcnt, x->bscl, x->brec,
+                         s));
+  }
+  for (int64_t r0 = 0; r0 < dm.N; r0 += R) {
+    const int Rc = static_cast<int>(std::min<int64_t>(R, dm.N - r0));
+    CU(launch_dense_chunk(C, G, nb, Rc, x->dense_ent, x->dense_jobs, x->dense_items, s));
+    Dims dd = dm;
+    dd.N = Rc;
+    dd.Cp = nb;
+    dd.SL = SL;
+    ScoreArgs a = score_args(x);
+    a.dm = dd;
+    a.X = x->X + r0 * D;
+    a.off = nullptr;
+    a.ent = x->dense_ent;
+    a.itemoff = x->dense_items;
+    a.g = x->dense_g;
+    a.gcnt = x->dense_gcnt;
+    a.out = x->dense_LJ;
+    if (ws) {
+      const WsOperands op{x->xmax + r0, x->mumax, x->mu32, x->brec, x->srec, x->bimg, x->bscl, x->simg, x->sscl};
+      CU(launch_score_ws(kModeAnchor, a, op, x->dense_jobs, s, false));
+    } else {  // single-role scorers (shapes the warp-specialised one does not take): CSR items
+      CU(launch_dense_csr(C, G, Rc, x->score_rows, x->dense_off, x->dense_items, s));
+      a.off = x->dense_off;
+      CU(run_score(x, kModeAnchor, a));
+    }
+    CU(launch_lse_dense(x->dense_LJ, Rc, SL, C, x->dense_lse + r0, s));
+  }
+  CU(launch_sum_f64(x->dense_lse, dm.N, x->partials, x->dense_out, s));
+  x->end(tok);
+  CU(cudaMemcpyAsync(&x->hstat->scal[3], x->dense_out, sizeof(double), cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  *ll = x->hstat->scal[3];
+  return VMFA_OK;
 }
 
 int vmfa_iterate(vmfa_ctx* x, uint64_t seed, uint64_t iteration, int mode, vmfa_iter_report* rep) {

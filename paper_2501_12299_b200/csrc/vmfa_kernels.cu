@@ -1724,6 +1724,29 @@ __global__ void k_lse_rows(const float* LJK, int64_t N, int Cp, double* lse) {
   }
 }
 
+// per-row log-sum-exp over the C dense slots (exact_log_likelihood,
+// model.cpp:101-148): warp per row, fixed-order butterflies (deterministic)
+__global__ void k_lse_dense(const float* LJ, int64_t R, int SL, int C, double* lse) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t n = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; n < R; n += nw) {
+    const float* l = LJ + n * SL;
+    double mx = -INFINITY;
+    for (int c = lane; c < C; c += 32) mx = fmax(mx, static_cast<double>(l[c]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(kFull, mx, o));
+    double out = mx;
+    if (isfinite(mx)) {
+      double sum = 0.0;
+      for (int c = lane; c < C; c += 32) sum += exp(static_cast<double>(l[c]) - mx);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(kFull, sum, o);
+      out = mx + log(sum);
+    }
+    if (lane == 0) lse[n] = out;
+  }
+}
+
 // LJK[n][j] = the anchor-pass log-joint of (n, K(n)[j]) under the current
 // parameters: anchor c = K(n)[j] scores itself in slot j*G + pos(c in g_c)
 // (mu_c centring, delta = 0 -- the same arithmetic as a one-component pass).
@@ -2018,6 +2041,10 @@ cudaError_t launch_self_slots(const Dims& dm, const int* K, const int* g, const 
 }
 cudaError_t launch_lse_rows(const float* LJK, int64_t N, int Cp, double* lse, cudaStream_t s) {
   k_lse_rows<<<grid_for(N, 256, 8192), 256, 0, s>>>(LJK, N, Cp, lse);
+  return cudaGetLastError();
+}
+cudaError_t launch_lse_dense(const float* LJ, int64_t R, int SL, int C, double* lse, cudaStream_t s) {
+  k_lse_dense<<<grid_for(R * 32, 256, 16384), 256, 0, s>>>(LJ, R, SL, C, lse);
   return cudaGetLastError();
 }
 cudaError_t launch_sum_f64(const double* v, int64_t n, double* partials, double* out, cudaStream_t s) {

@@ -228,7 +228,15 @@ struct WsOperands {
   const void* simg;    // one-component B stage images (extra / truncated F), per precompute
   const float* sscl;
 };
-cudaError_t launch_score_ws(int mode, const ScoreArgs& s, const WsOperands& op, int4* jobs, cudaStream_t st);
+cudaError_t launch_score_ws(int mode, const ScoreArgs& s, const WsOperands& op, int4* jobs, cudaStream_t st,
+                            bool build_jobs = true);
+// dense all-pairs pass (exact_log_likelihood): pseudo-anchor groups, per-chunk
+// entries / row-tile-major jobs / item total, and the per-row LSE over C slots
+cudaError_t launch_dense_groups(int C, int G, int* g, int* gcnt, cudaStream_t s);
+cudaError_t launch_dense_chunk(int C, int G, int nb, int R, int* ent, int4* jobs, int* itemoff, cudaStream_t s);
+cudaError_t launch_dense_csr(int C, int G, int R, int rows, int* off, int* itemoff, cudaStream_t s);
+int64_t dense_jobs(int nb, int R);
+cudaError_t launch_lse_dense(const float* LJ, int64_t R, int SL, int C, double* lse, cudaStream_t s);
 int64_t ws_record_floats(const Dims& dm, int single);
 cudaError_t launch_ws_records(const Dims& dm, int single, const float* WT, const float* mu32, const float* ipsi32,
                               const double* kconst, const int* g, const int* gcnt, const float* scl, float* rec,

@@ -886,6 +886,62 @@ cudaError_t launch_rowmax(int64_t N, int D, const float* X, float* xmax, cudaStr
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- dense all-pairs pass
+// exact_log_likelihood (model.cpp:139-148) scores every (n, c): components are
+// blocked into pseudo-anchors a = bG with g'_a = {bG, ..., bG+G-1} (rows
+// centred on mu_a), and a chunk of R rows gets the fake candidate list
+// K'(n) = (0, G, 2G, ...), so the anchor pass writes l(n, c) to slot c of row
+// n (slot j*G + i with j = c / G). Jobs are row-tile major (all blocks of one
+// 128-row tile are adjacent): a tile of X is read from HBM once and the
+// blocks' B images stay in L2.
+__global__ void k_dense_groups(int C, int G, int* g, int* gcnt) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (int64_t)C * G;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int c = static_cast<int>(i / G), k = static_cast<int>(i - (int64_t)c * G);
+    const bool anchor = c % G == 0;
+    g[i] = anchor && c + k < C ? c + k : 0;
+    if (k == 0) gcnt[c] = anchor ? min(G, C - c) : 0;
+  }
+}
+__global__ void k_dense_chunk(int C, int G, int nb, int R, int* ent, int4* jobs, int* itemoff) {
+  const int ntile = (R + kRows - 1) / kRows;
+  const int64_t nent = (int64_t)nb * R, njob = (int64_t)nb * ntile;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nent + njob;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (i < nent) {  // block b's rows in ascending order: e = n * nb + b (row n relative to the chunk)
+      const int b = static_cast<int>(i / R), t = static_cast<int>(i - (int64_t)b * R);
+      ent[i] = t * nb + b;
+    } else {
+      const int it = static_cast<int>(i - nent);
+      const int tile = it / nb, b = it - tile * nb;
+      jobs[it] = make_int4(b * G, b * R + tile * kRows, min(kRows, R - tile * kRows), min(G, C - b * G));
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) itemoff[C] = static_cast<int>(njob);
+}
+cudaError_t launch_dense_groups(int C, int G, int* g, int* gcnt, cudaStream_t s) {
+  k_dense_groups<<<sm_count() * 4, 256, 0, s>>>(C, G, g, gcnt);
+  return cudaGetLastError();
+}
+// CSR form of the same chunk for the single-role scorers (items of `rows` rows
+// per pseudo-anchor, component-major): off[c] = ceil(c/G) R
+__global__ void k_dense_csr(int C, int G, int R, int rows, int* off, int* itemoff) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c <= C; c += gridDim.x * blockDim.x) {
+    const int k = (c + G - 1) / G;  // pseudo-anchors before c
+    off[c] = k * R;
+    itemoff[c] = k * ((R + rows - 1) / rows);
+  }
+}
+cudaError_t launch_dense_chunk(int C, int G, int nb, int R, int* ent, int4* jobs, int* itemoff, cudaStream_t s) {
+  k_dense_chunk<<<sm_count() * 4, 256, 0, s>>>(C, G, nb, R, ent, jobs, itemoff);
+  return cudaGetLastError();
+}
+cudaError_t launch_dense_csr(int C, int G, int R, int rows, int* off, int* itemoff, cudaStream_t s) {
+  k_dense_csr<<<(C + 256) / 256, 256, 0, s>>>(C, G, R, rows, off, itemoff);
+  return cudaGetLastError();
+}
+int64_t dense_jobs(int nb, int R) { return (int64_t)nb * ((R + kRows - 1) / kRows); }
+
 unsigned long long* g_ws_prof = nullptr;  // set by vmfa_diag_scorer_cycles
 int g_ws_dbg = 0;                          // diagnostics flags (enable >> 1)
 constexpr int kProfWords = 16 + 8 * kTraceEvents;
@@ -908,7 +964,8 @@ bool ws_smem_plan(int Hp, uint32_t stage_bytes, int* xslots, int* nb, size_t* dy
   return false;
 }
 
-cudaError_t launch_score_ws(int mode, const ScoreArgs& s, const WsOperands& op, int4* jobs, cudaStream_t st) {
+cudaError_t launch_score_ws(int mode, const ScoreArgs& s, const WsOperands& op, int4* jobs, cudaStream_t st,
+                            bool build_jobs) {
   WsArgs a{};
   a.dm = s.dm;
   a.mode = mode;
@@ -940,7 +997,7 @@ cudaError_t launch_score_ws(int mode, const ScoreArgs& s, const WsOperands& op, 
   a.out = s.out;
   a.prof = g_ws_prof;
   a.dbg = g_ws_prof ? g_ws_dbg : 0;
-  k_build_jobs<<<(s.dm.C + 255) / 256, 256, 0, st>>>(s.dm.C, mode, s.off, s.itemoff, s.gcnt, jobs);
+  if (build_jobs) k_build_jobs<<<(s.dm.C + 255) / 256, 256, 0, st>>>(s.dm.C, mode, s.off, s.itemoff, s.gcnt, jobs);
   auto go = [&](auto kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn));
     kern<<<sm_count(), kThreads, dyn, st>>>(a);

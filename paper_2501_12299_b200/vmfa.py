@@ -227,6 +227,13 @@ class Session:
         check(lib().vmfa_truncated_free_energy(self._h, C.byref(F)))
         return F.value
 
+    def exact_log_likelihood(self) -> float:
+        """exact_log_likelihood (model.cpp:139-148) over this session's rows:
+        sum_n log sum_c p(x_n, c) over all C components (dense tcgen05 pass)."""
+        ll = C.c_double()
+        check(lib().vmfa_exact_log_likelihood(self._h, C.byref(ll)))
+        return ll.value
+
     def iterate(self, seed: int, iteration: int, mode: int = KL) -> dict:
         r = IterReport()
         check(lib().vmfa_iterate(self._h, seed, iteration, mode, C.byref(r)))

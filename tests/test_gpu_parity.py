@@ -326,6 +326,43 @@ def test_lookahead_free_energy_is_exact(oracle, gpu, scorer, monkeypatch):
         assert np.array_equal(getattr(p1, f), getattr(p0, f)), f
 
 
+@pytest.mark.parametrize("case", [dict(N=3000, D=64, C=57, H=4, G=5, frozen=()),
+                                  dict(N=2500, D=100, C=40, H=8, G=10, frozen=(3, 17)),
+                                  dict(N=700, D=30, C=23, H=3, G=23, frozen=(0,))])
+def test_exact_log_likelihood_matches_oracle(oracle, gpu, case):
+    # exact_log_likelihood (model.cpp:139-148): all-pairs N x C log-joints and
+    # the per-row LSE; C not a multiple of G (short last block), D % 4 != 0 and
+    # frozen components (pi = 0 -> l = -inf) included; calling it leaves the
+    # lookahead state of the training loop intact
+    O, V = oracle, gpu
+    X, _ = gaussian_problem(case["N"], case["D"], max(4, case["C"] // 2), 3, seed=5)
+    C, H, G = case["C"], case["H"], case["G"]
+    p, st, floor, sess = _setup(O, V, X, C, H, 2, G)
+    sess.variational_e_step(0, 0)
+    r1 = sess.iterate(0, 1)
+    pc = sess.download_params()
+    if case["frozen"]:
+        pi = pc.pi.copy()
+        pi[list(case["frozen"])] = 0.0
+        pi /= pi.sum()
+        pc = V.Params(pi, pc.mu, pc.lam, pc.psi)
+        sess.upload_params(pc)
+    ll = sess.exact_log_likelihood()
+    po = to_oracle_params(O, pc)
+    ll_or = O.exact_log_likelihood(X, po, O.precompute_all(po), threads=4)
+    assert np.isfinite(ll) and abs(ll - ll_or) <= 1e-5 * abs(ll_or), (ll, ll_or)
+    print("exact LL rel err", abs(ll - ll_or) / abs(ll_or))
+    assert sess.exact_log_likelihood() == ll  # deterministic
+    if not case["frozen"]:  # the next iteration is unaffected by the dense pass
+        r2 = sess.iterate(0, 2)
+        p2, st2, _, s2 = _setup(O, V, X, C, H, 2, G)
+        s2.variational_e_step(0, 0)
+        assert s2.iterate(0, 1)["F"] == r1["F"]
+        assert s2.iterate(0, 2)["F"] == r2["F"]
+        s2.close()
+    sess.close()
+
+
 def test_upload_state_validates_K_on_device(gpu):
     # VarState::validate (estep.cpp:15-68): K rows sorted, distinct, in range
     V = gpu
