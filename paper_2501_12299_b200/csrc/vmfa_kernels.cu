@@ -241,11 +241,19 @@ __device__ __forceinline__ unsigned long long sel_key(float l, int c) {
 
 template <int NS>
 __global__ void __launch_bounds__(256) k_select(SelectArgs a) {
+  // per-warp bitmap of the components already seen in earlier slot rounds
+  // (first-occurrence dedup across rounds; bits are cleared after each row)
+  extern __shared__ unsigned s_seen[];
   const Dims dm = a.dm;
   const int lane = threadIdx.x & 31;
+  const int W = (dm.C + 31) >> 5;
+  for (int i = threadIdx.x; i < W * (blockDim.x >> 5); i += blockDim.x) s_seen[i] = 0u;
+  __syncthreads();
+  unsigned* seen = s_seen + (threadIdx.x >> 5) * W;
   const int64_t warp0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int CpG = dm.Cp * dm.G;
+  const float invG = 1.0f / static_cast<float>(dm.G);
   const unsigned lt_mask = (1u << lane) - 1u;
   for (int64_t n = warp0; n < dm.N; n += nwarps) {
     int comp[NS];
@@ -256,7 +264,8 @@ __global__ void __launch_bounds__(256) k_select(SelectArgs a) {
       const int s = k * 32 + lane;
       int cmp = -1;
       if (s < CpG) {
-        const int j = s / dm.G, i = s - j * dm.G;
+        // s / G exactly: (s + 0.5) / G stays >= 0.5 / G away from an integer
+        const int j = __float2int_rz((static_cast<float>(s) + 0.5f) * invG), i = s - j * dm.G;
         const int an = a.K[n * dm.Cp + j];
         if (i < a.gcnt[an]) cmp = a.g[(int64_t)an * dm.G + i];
       } else if (s == CpG) {
@@ -265,22 +274,22 @@ __global__ void __launch_bounds__(256) k_select(SelectArgs a) {
       comp[k] = cmp;
     }
     // first-occurrence dedup in slot order (s = k*32 + lane): within a round by
-    // __match_any_sync (keep the lowest lane), across rounds by broadcast compares
+    // __match_any_sync (keep the lowest lane), across rounds by the bitmap
 #pragma unroll
     for (int k = 0; k < NS; ++k) {
       const unsigned m = __match_any_sync(kFull, comp[k]);
-      uniq[k] = comp[k] >= 0 && (m & lt_mask) == 0u;
-    }
-#pragma unroll
-    for (int k = 1; k < NS; ++k) {
-#pragma unroll
-      for (int k0 = 0; k0 < k; ++k0) {
-        for (int src = 0; src < 32; ++src) {
-          const int ct = __shfl_sync(kFull, comp[k0], src);
-          if (ct >= 0 && ct == comp[k]) uniq[k] = false;
-        }
+      bool u = comp[k] >= 0 && (m & lt_mask) == 0u;
+      if (k > 0 && u) u = ((seen[comp[k] >> 5] >> (comp[k] & 31)) & 1u) == 0u;
+      uniq[k] = u;
+      if (k + 1 < NS) {
+        __syncwarp();
+        if (u) atomicOr(&seen[comp[k] >> 5], 1u << (comp[k] & 31));
+        __syncwarp();
       }
     }
+#pragma unroll
+    for (int k = 0; k + 1 < NS; ++k)
+      if (uniq[k]) atomicAnd(&seen[comp[k] >> 5], ~(1u << (comp[k] & 31)));
 #pragma unroll
     for (int k = 0; k < NS; ++k) {
       float v = 0.f;
@@ -303,12 +312,15 @@ __global__ void __launch_bounds__(256) k_select(SelectArgs a) {
       base += __popc(b);
     }
     const int m = base;
-    // top-C' by (l desc, index asc) on packed keys; 0 = no candidate
+    // top-C' by (l desc, index asc) on packed keys (0 = no candidate); round
+    // r's winner is held by lane r
     unsigned long long key[NS];
 #pragma unroll
     for (int k = 0; k < NS; ++k) key[k] = uniq[k] ? sel_key(lj[k], comp[k]) : 0ull;
-    int kc[8];
-    float kl[8];
+    int myc = 0;
+    float myl = -INFINITY;
+    int best_c = 0;
+    float best_l = -INFINITY;
     for (int r = 0; r < dm.Cp; ++r) {
       unsigned long long best = 0ull;
 #pragma unroll
@@ -320,61 +332,39 @@ __global__ void __launch_bounds__(256) k_select(SelectArgs a) {
       best = (static_cast<unsigned long long>(hi) << 32) | lo;
       if (best == 0ull) {
         if (lane == 0) atomicOr(a.status, 1);  // InsufficientCandidates
-        kc[r] = 0;
-        kl[r] = -INFINITY;
         continue;
       }
       const int c = 0x7fffffff - static_cast<int>(best & 0xffffffffu);
       unsigned u = static_cast<unsigned>(best >> 32);
       u = (u & 0x80000000u) ? (u & 0x7fffffffu) : ~u;
-      kc[r] = c;
-      kl[r] = __uint_as_float(u);
+      const float l = __uint_as_float(u);
+      if (lane == r) myc = c, myl = l;
+      // label (estep.cpp:157-166): the first member of the sorted K replaced
+      // only by a strictly larger l = the largest l, ties to the smaller index
+      if (r == 0) best_c = c, best_l = l;
 #pragma unroll
       for (int k = 0; k < NS; ++k)
         if (key[k] == best) key[k] = 0ull;  // unique keys: only the owner matches
     }
-    // sort (kc, kl) ascending by component (estep.cpp:121)
-    for (int i = 1; i < dm.Cp; ++i) {
-      const int c0 = kc[i];
-      const float l0 = kl[i];
-      int j = i - 1;
-      while (j >= 0 && kc[j] > c0) {
-        kc[j + 1] = kc[j];
-        kl[j + 1] = kl[j];
-        --j;
-      }
-      kc[j + 1] = c0;
-      kl[j + 1] = l0;
-    }
-    // label: first member, replaced only by a strictly larger l (estep.cpp:157-166)
-    int best_c = kc[0];
-    float best_l = kl[0];
-    for (int j = 1; j < dm.Cp; ++j)
-      if (kl[j] > best_l) {
-        best_l = kl[j];
-        best_c = kc[j];
-      }
+    // K sorted ascending by component (estep.cpp:121): rank of member `lane`
+    int rank = 0;
+    for (int j = 0; j < dm.Cp; ++j) rank += __shfl_sync(kFull, myc, j) < myc;
     // block 4: fp64 log-sum-exp and responsibilities (numerics.hpp:15-22); lane j
-    // evaluates member j's exponentials, the terms are summed in member order
-    double mx = -INFINITY;
-    for (int j = 0; j < dm.Cp; ++j) mx = fmax(mx, static_cast<double>(kl[j]));
-    int myc = kc[0];
-    float myl = kl[0];
-    for (int j = 1; j < dm.Cp; ++j)
-      if (j == lane) {
-        myc = kc[j];
-        myl = kl[j];
-      }
+    // evaluates member j's exponential, the terms are summed in K order
+    const double mx = static_cast<double>(best_l);
     const double term = (lane < dm.Cp && isfinite(mx)) ? exp(static_cast<double>(myl) - mx) : 0.0;
     double l = mx;
     if (isfinite(mx)) {
       double s2 = 0.0;
-      for (int j = 0; j < dm.Cp; ++j) s2 += __shfl_sync(kFull, term, j);
+      for (int k = 0; k < dm.Cp; ++k) {
+        const int src = __ffs(__ballot_sync(kFull, lane < dm.Cp && rank == k)) - 1;
+        s2 += __shfl_sync(kFull, term, src < 0 ? 0 : src);
+      }
       l = mx + log(s2);
     }
     if (lane < dm.Cp) {
-      a.K[n * dm.Cp + lane] = myc;
-      a.resp[n * dm.Cp + lane] = exp(static_cast<double>(myl) - l);
+      a.K[n * dm.Cp + rank] = myc;
+      a.resp[n * dm.Cp + rank] = exp(static_cast<double>(myl) - l);
     }
     if (lane == 0) {
       a.labels[n] = best_c;
@@ -1895,15 +1885,21 @@ cudaError_t launch_score(int mode, const ScoreArgs& a, int grid, cudaStream_t s)
 cudaError_t launch_select(const SelectArgs& a, cudaStream_t s) {
   const int ns = (a.dm.SL + 31) / 32;
   const int grid = grid_for(a.dm.N * 32, 256, sm_count() * 16);
+  const size_t smem = static_cast<size_t>((a.dm.C + 31) / 32) * 8 * sizeof(unsigned);  // 8 warps' bitmaps
+  if (smem > 200 * 1024) return cudaErrorInvalidValue;
+  auto go = [&](auto kern) {
+    if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    kern<<<grid, 256, smem, s>>>(a);
+  };
   switch (ns) {
-    case 1: k_select<1><<<grid, 256, 0, s>>>(a); break;
-    case 2: k_select<2><<<grid, 256, 0, s>>>(a); break;
-    case 3: k_select<3><<<grid, 256, 0, s>>>(a); break;
-    case 4: k_select<4><<<grid, 256, 0, s>>>(a); break;
-    case 5: k_select<5><<<grid, 256, 0, s>>>(a); break;
-    case 6: k_select<6><<<grid, 256, 0, s>>>(a); break;
-    case 7: k_select<7><<<grid, 256, 0, s>>>(a); break;
-    case 8: k_select<8><<<grid, 256, 0, s>>>(a); break;
+    case 1: go(k_select<1>); break;
+    case 2: go(k_select<2>); break;
+    case 3: go(k_select<3>); break;
+    case 4: go(k_select<4>); break;
+    case 5: go(k_select<5>); break;
+    case 6: go(k_select<6>); break;
+    case 7: go(k_select<7>); break;
+    case 8: go(k_select<8>); break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
