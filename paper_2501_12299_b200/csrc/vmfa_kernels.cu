@@ -430,6 +430,7 @@ __global__ void __launch_bounds__(kGupdThreads) k_gupdate(GupdArgs a, int capmax
   int* t_key = reinterpret_cast<int*>(t_lo + capmax);
   int* t_cnt = t_key + capmax;
   __shared__ KeyMin red[kGupdThreads / 32];
+  __shared__ int red_i[kGupdThreads / 32];
   __shared__ int s_sel[64];
   __shared__ int s_nsel;
   const Dims dm = a.dm;
@@ -572,34 +573,44 @@ __global__ void __launch_bounds__(kGupdThreads) k_gupdate(GupdArgs a, int capmax
       __syncthreads();
       continue;
     }
-    // update_g: G-1 rounds of a block-wide argmin over (avg, ct)
+    // update_g: the keys (avg, ct) are computed once, in place of the sums
+    // (+inf: no key; averages are finite, the values saturate at 2^31), then
+    // G-1 rounds of a block-wide argmin, the winner's key set to +inf
+    double* kv = reinterpret_cast<double*>(use_smem ? t_hi : g_hi);
+    for (int i = tid; i < tab_n; i += kGupdThreads) {
+      int ct;
+      long long cnt, hi, lo;
+      entry(i, ct, cnt, hi, lo);
+      kv[i] = (ct < 0 || cnt <= 0) ? INFINITY : from_fixed(hi, lo) / static_cast<double>(cnt);
+    }
     if (tid == 0) s_nsel = 0;
     __syncthreads();
     for (int r = 0; r < dm.G - 1 && npts > 0; ++r) {
       KeyMin best{INFINITY, 0x7fffffff};
+      int bi = -1;
       for (int i = tid; i < tab_n; i += kGupdThreads) {
-        int ct;
-        long long cnt, hi, lo;
-        entry(i, ct, cnt, hi, lo);
-        if (ct < 0 || cnt <= 0) continue;
-        bool taken = false;
-        for (int q = 0; q < s_nsel; ++q) taken |= (s_sel[q] == ct);
-        if (taken) continue;
-        const KeyMin k{from_fixed(hi, lo) / static_cast<double>(cnt), ct};
-        if (kless(k, best)) best = k;
+        const double v = kv[i];
+        if (v == INFINITY) continue;
+        const KeyMin k{v, use_smem ? t_key[i] : i};
+        if (kless(k, best)) best = k, bi = i;
       }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
         KeyMin oth{__shfl_xor_sync(kFull, best.v, o), __shfl_xor_sync(kFull, best.c, o)};
-        if (kless(oth, best)) best = oth;
+        const int obi = __shfl_xor_sync(kFull, bi, o);
+        if (kless(oth, best)) best = oth, bi = obi;
       }
-      if (lane == 0) red[warp] = best;
+      if (lane == 0) red[warp] = best, red_i[warp] = bi;
       __syncthreads();
       if (tid == 0) {
         KeyMin b = red[0];
+        int ib = red_i[0];
         for (int w = 1; w < nw; ++w)
-          if (kless(red[w], b)) b = red[w];
-        if (b.c != 0x7fffffff) s_sel[s_nsel++] = b.c;
+          if (kless(red[w], b)) b = red[w], ib = red_i[w];
+        if (b.c != 0x7fffffff) {
+          s_sel[s_nsel++] = b.c;
+          kv[ib] = INFINITY;
+        }
       }
       __syncthreads();
       if (s_nsel <= r) break;  // no more keys
