@@ -246,11 +246,7 @@ int csr_by_key(vmfa_ctx* x, const unsigned* keys, int64_t n, int* off, int* ent,
   CU(cub::DeviceRadixSort::SortPairs(x->cub_tmp, tb, keys, x->keys_alt, x->vals, ent,
                                      static_cast<int>(n), 0, bits_for(static_cast<unsigned>(C)), s));
   CU(launch_offsets_sorted(x->keys_alt, n, C, off, s));
-  if (items) {
-    CU(launch_chunks_from_off(off, C, rows_per_item, 0, x->chunks, s));
-    tb = x->cub_bytes;
-    CU(cub::DeviceScan::ExclusiveSum(x->cub_tmp, tb, x->chunks, items, C + 1, s));
-  }
+  if (items) CU(launch_items_scan(off, C, rows_per_item, 0, items, s));
   x->end(tok);
   return VMFA_OK;
 }
@@ -406,11 +402,7 @@ int estep_local(vmfa_ctx* x, uint64_t seed, uint64_t it, int mode, bool exchange
   // block 2: partition by label (stable => ascending n per component)
   CU(launch_keys_from_i32(x->labels, x->keys, dm.N, s));
   TRY(csr_by_key(x, x->keys, dm.N, x->part_off, x->part_ent, nullptr, 1));
-  {
-    size_t tb = x->cub_bytes;
-    CU(launch_chunks_from_off(x->part_off, dm.C, x->gupd_pts, 1, x->chunks, s));
-    CU(cub::DeviceScan::ExclusiveSum(x->cub_tmp, tb, x->chunks, x->part_items, dm.C + 1, s));
-  }
+  CU(launch_items_scan(x->part_off, dm.C, x->gupd_pts, 1, x->part_items, s));
   // block 3 (local accumulation; selection unless exchanging)
   CU(launch_logpi(x->pi, dm.C, x->logpi, s));
   {
@@ -494,9 +486,7 @@ int stats_local(vmfa_ctx* x) {
   a.sq = x->sq;
   a.qctr = x->qctr;
   const int tok = x->begin(kFamStats, x->dm.N * x->dm.Cp);
-  size_t tb = x->cub_bytes;
-  CU(launch_chunks_from_off(x->kinv_off, x->dm.C, x->stats_rows, 0, x->chunks, x->stream));
-  CU(cub::DeviceScan::ExclusiveSum(x->cub_tmp, tb, x->chunks, x->stats_items, x->dm.C + 1, x->stream));
+  CU(launch_items_scan(x->kinv_off, x->dm.C, x->stats_rows, 0, x->stats_items, x->stream));
   CU(launch_stats(a, x->stats_items, x->stats_rows, x->stats_part, x->stream));
   x->end(tok);
   return VMFA_OK;

@@ -67,6 +67,49 @@ __global__ void k_hist(const unsigned* keys, int64_t n, int C, int* cnt) {
     if (k < static_cast<unsigned>(C)) atomicAdd(cnt + k, 1);
   }
 }
+// CSR offsets from sorted keys in [0, C] by one pass over the keys:
+// off[c] = #keys < c; row i writes the c in (key[i-1], key[i]] (the
+// intervals partition [0, C], each offset is written once)
+__global__ void k_offsets_scan(const unsigned* sorted, int64_t n, int C, int* off) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int prev = i > 0 ? static_cast<int>(sorted[i - 1]) : -1;
+    const int cur = i < n ? static_cast<int>(sorted[i]) : C;
+    for (int c = prev + 1; c <= cur; ++c) off[c] = static_cast<int>(i);
+  }
+}
+// items = exclusive scan of max(min1, ceil((off[c+1] - off[c]) / rows)) over
+// c < C (items[C] = total), one 1024-thread block (C is at most ~10^5)
+__global__ void __launch_bounds__(1024) k_items_scan(const int* off, int C, int rows, int min1, int* items) {
+  __shared__ int s_warp[32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int per = (C + 1 + 1023) / 1024;
+  const int c0 = tid * per, c1 = min(C + 1, c0 + per);
+  int sum = 0;
+  for (int c = c0; c < c1; ++c) sum += c < C ? max(min1, (off[c + 1] - off[c] + rows - 1) / rows) : 0;
+  int incl = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(kFull, incl, o);
+    if (lane >= o) incl += t;
+  }
+  if (lane == 31) s_warp[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    int w = s_warp[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(kFull, w, o);
+      if (lane >= o) w += t;
+    }
+    s_warp[lane] = w;  // inclusive over warps
+  }
+  __syncthreads();
+  int run = incl - sum + (warp > 0 ? s_warp[warp - 1] : 0);
+  for (int c = c0; c < c1; ++c) {
+    items[c] = run;
+    run += c < C ? max(min1, (off[c + 1] - off[c] + rows - 1) / rows) : 0;
+  }
+}
 __global__ void k_chunks_from_off(const int* off, int C, int rows, int min1, int* chunks) {
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c <= C; c += gridDim.x * blockDim.x) {
     if (c == C) {
@@ -1782,9 +1825,12 @@ __global__ void __launch_bounds__(256) k_sum_stage1(const double* v, int64_t n, 
   if (threadIdx.x == 0) partials[blockIdx.x] = red[0];
 }
 __global__ void __launch_bounds__(32) k_sum_stage2(const double* partials, int m, double* out) {
+  __shared__ double s_p[kSumBlocks];
+  for (int i = threadIdx.x; i < m; i += 32) s_p[i] = partials[i];  // lane-parallel loads
+  __syncwarp();
   if (threadIdx.x == 0) {
     double s = 0.0;
-    for (int i = 0; i < m; ++i) s += partials[i];
+    for (int i = 0; i < m; ++i) s += s_p[i];  // fixed order
     *out = s;
   }
 }
@@ -1858,7 +1904,11 @@ cudaError_t launch_hist(const unsigned* keys, int64_t n, int C, int* cnt, cudaSt
   return cudaGetLastError();
 }
 cudaError_t launch_offsets_sorted(const unsigned* sorted, int64_t n, int C, int* off, cudaStream_t s) {
-  k_offsets_sorted<<<grid_for(C + 1, 256, 4096), 256, 0, s>>>(sorted, n, C, off);
+  k_offsets_scan<<<grid_for(n + 1, 256, 8192), 256, 0, s>>>(sorted, n, C, off);
+  return cudaGetLastError();
+}
+cudaError_t launch_items_scan(const int* off, int C, int rows, int min1, int* items, cudaStream_t s) {
+  k_items_scan<<<1, 1024, 0, s>>>(off, C, rows, min1, items);
   return cudaGetLastError();
 }
 cudaError_t launch_chunks(const int* cnt, int C, int rows, int* chunks, cudaStream_t s) {

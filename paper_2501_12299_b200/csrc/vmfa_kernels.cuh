@@ -178,6 +178,7 @@ cudaError_t launch_keys_from_i32(const int* src, unsigned* keys, int64_t n, cuda
 cudaError_t launch_hist(const unsigned* keys, int64_t n, int C, int* cnt, cudaStream_t s);
 cudaError_t launch_chunks(const int* cnt, int C, int rows, int* chunks, cudaStream_t s);
 cudaError_t launch_offsets_sorted(const unsigned* sorted, int64_t n, int C, int* off, cudaStream_t s);
+cudaError_t launch_items_scan(const int* off, int C, int rows, int min1, int* items, cudaStream_t s);
 cudaError_t launch_extra(const Dims& dm, const int* K, const int* g, const int* gcnt,
                          uint64_t seed, uint64_t it, int* rx, unsigned* rkey, cudaStream_t s);
 cudaError_t launch_score(int mode, const ScoreArgs& a, int grid, cudaStream_t s);
