@@ -97,6 +97,17 @@ int vmfa_ctx_device_bytes(const vmfa_ctx* ctx, size_t* bytes);
  * local rows [row_begin, row_begin+rows). Host memory may be pageable or
  * pinned.                                                                   */
 int vmfa_upload_data(vmfa_ctx* ctx, const float* X, int64_t row_begin, int64_t rows);
+/* The same, asynchronous: the rows are copied on a second stream while the
+ * context keeps working (parameter / state uploads, the E-step's CSR and image
+ * builds); the first kernel that reads X waits for the copy. X must stay
+ * valid and unchanged until the next call that synchronises the context
+ * (iterate, any download, ...). Page-locked X gives a truly asynchronous copy. */
+int vmfa_upload_data_async(vmfa_ctx* ctx, const float* X, int64_t row_begin, int64_t rows);
+/* Lookahead (default on, env VMFA_LOOKAHEAD=0 turns it off): the truncated
+ * free energy after the M-step is read from the next E-step's anchor pass,
+ * which that E-step then skips. Off: F gets its own one-component pass (same
+ * value) -- cheaper when the caller re-uploads data or state every iteration. */
+int vmfa_set_lookahead(vmfa_ctx* ctx, int enable);
 /* Variance floor max(1e-8, 1e-6 var_d) (dataset.cpp:37-39), computed by the
  * caller over ALL n_total rows (global).                  */
 int vmfa_set_floor(vmfa_ctx* ctx, const double* floor);

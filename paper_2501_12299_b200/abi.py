@@ -60,6 +60,8 @@ _SIGS = {
     "vmfa_ctx_destroy": (_I, [_P]),
     "vmfa_ctx_device_bytes": (_I, [_P, C.POINTER(C.c_size_t)]),
     "vmfa_upload_data": (_I, [_P, _P, _I64, _I64]),
+    "vmfa_upload_data_async": (_I, [_P, _P, _I64, _I64]),
+    "vmfa_set_lookahead": (_I, [_P, _I]),
     "vmfa_set_floor": (_I, [_P, _P]),
     "vmfa_upload_params": (_I, [_P, _P, _P, _P, _P]),
     "vmfa_download_params": (_I, [_P, _P, _P, _P, _P]),

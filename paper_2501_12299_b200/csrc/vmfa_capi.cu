@@ -153,7 +153,11 @@ struct vmfa_ctx {
   // and parameters) while computing the truncated free energy: LJ's anchor
   // slots are valid and the next estep_local skips block 1's anchor scoring
   bool prescored = false;
-  bool lookahead = true;  // VMFA_LOOKAHEAD=0 scores the truncated F with its own pass
+  bool lookahead = true;  // VMFA_LOOKAHEAD=0 (or vmfa_set_lookahead) scores the truncated F with its own pass
+  // vmfa_upload_data_async: rows copied on a second stream; X consumers wait on x_ready
+  cudaStream_t cstream = nullptr;
+  cudaEvent_t x_ready = nullptr, x_free = nullptr;
+  bool x_pending = false;
   bool have_estep = false;
   // dumps (parity only)
   bool dump = false;
@@ -254,7 +258,15 @@ int csr_by_key(vmfa_ctx* x, const unsigned* keys, int64_t n, int* off, int* ent,
 int score_grid() { return sm_count() * 8; }
 constexpr size_t kImageBudget = size_t(16) << 30;  // scorer B stage images (bytes)
 
+// the compute stream waits for a pending asynchronous row upload (first X consumer)
+cudaError_t wait_x(vmfa_ctx* x) {
+  if (!x->x_pending) return cudaSuccess;
+  x->x_pending = false;
+  return cudaStreamWaitEvent(x->stream, x->x_ready, 0);
+}
+
 cudaError_t run_score(vmfa_ctx* x, int mode, const ScoreArgs& a) {
+  if (cudaError_t e = wait_x(x); e != cudaSuccess) return e;
   if (x->scorer == 2)
     return launch_score_ws(mode, a, WsOperands{x->xmax, x->mumax, x->mu32, x->brec, x->srec, x->bimg, x->bscl, x->simg, x->sscl},
                            x->jobs, x->stream);
@@ -471,6 +483,7 @@ int estep_finish(vmfa_ctx* x, bool exchange, bool sync = true) {
 int stats_local(vmfa_ctx* x) {
   if (!x->have_estep) return fail(VMFA_ERR_INVALID_ARGUMENT, "accumulate_suffstats needs a preceding E-step (responsibilities)");
   TRY(ensure_kinv_current(x));
+  CU(wait_x(x));
   StatsArgs a{};
   a.dm = x->dm;
   a.X = x->X;
@@ -823,6 +836,12 @@ int vmfa_ctx_destroy(vmfa_ctx* x) {
   if (!x) return VMFA_OK;
   cudaSetDevice(x->device);
   if (x->stream) cudaStreamSynchronize(x->stream);
+  if (x->cstream) {
+    cudaStreamSynchronize(x->cstream);
+    cudaStreamDestroy(x->cstream);
+    cudaEventDestroy(x->x_ready);
+    cudaEventDestroy(x->x_free);
+  }
   for (void* p : x->allocs) cudaFree(p);
   if (x->hstat) cudaFreeHost(x->hstat);
   for (auto& e : x->pending) {
@@ -848,11 +867,39 @@ int vmfa_synchronize(vmfa_ctx* x) {
   return VMFA_OK;
 }
 
+int vmfa_upload_data_async(vmfa_ctx* x, const float* X, int64_t row_begin, int64_t rows) {
+  TRY(check_ctx(x));
+  x->prescored = false;
+  if (!X || row_begin < 0 || rows < 0 || row_begin + rows > x->dm.N)
+    return fail(VMFA_ERR_INVALID_ARGUMENT, "vmfa_upload_data_async: row range outside the shard");
+  if (!x->cstream) {
+    CU(cudaStreamCreateWithFlags(&x->cstream, cudaStreamNonBlocking));
+    CU(cudaEventCreateWithFlags(&x->x_ready, cudaEventDisableTiming));
+    CU(cudaEventCreateWithFlags(&x->x_free, cudaEventDisableTiming));
+  }
+  // after everything already enqueued (which may still read the old rows)
+  CU(cudaEventRecord(x->x_free, x->stream));
+  CU(cudaStreamWaitEvent(x->cstream, x->x_free, 0));
+  CU(cudaMemcpyAsync(x->X + row_begin * x->dm.D, X, sizeof(float) * rows * x->dm.D, cudaMemcpyHostToDevice,
+                     x->cstream));
+  if (x->xmax) CU(launch_rowmax(rows, x->dm.D, x->X + row_begin * x->dm.D, x->xmax + row_begin, x->cstream));
+  CU(cudaEventRecord(x->x_ready, x->cstream));
+  x->x_pending = true;
+  return VMFA_OK;
+}
+
+int vmfa_set_lookahead(vmfa_ctx* x, int enable) {
+  TRY(check_ctx(x));
+  x->lookahead = enable != 0;
+  return VMFA_OK;
+}
+
 int vmfa_upload_data(vmfa_ctx* x, const float* X, int64_t row_begin, int64_t rows) {
   TRY(check_ctx(x));
   x->prescored = false;
   if (!X || row_begin < 0 || rows < 0 || row_begin + rows > x->dm.N)
     return fail(VMFA_ERR_INVALID_ARGUMENT, "vmfa_upload_data: row range outside the shard");
+  CU(wait_x(x));
   CU(cudaMemcpyAsync(x->X + row_begin * x->dm.D, X, sizeof(float) * rows * x->dm.D,
                      cudaMemcpyHostToDevice, x->stream));
   if (x->xmax) CU(launch_rowmax(rows, x->dm.D, x->X + row_begin * x->dm.D, x->xmax + row_begin, x->stream));
@@ -1196,6 +1243,7 @@ int vmfa_exact_log_likelihood(vmfa_ctx* x, double* ll) {
     a.g = x->dense_g;
     a.gcnt = x->dense_gcnt;
     a.out = x->dense_LJ;
+    CU(wait_x(x));
     if (ws) {
       const WsOperands op{x->xmax + r0, x->mumax, x->mu32, x->brec, x->srec, x->bimg, x->bscl, x->simg, x->sscl};
       CU(launch_score_ws(kModeAnchor, a, op, x->dense_jobs, s, false));

@@ -124,9 +124,22 @@ class Session:
         check(lib().vmfa_ctx_device_bytes(self._h, C.byref(b)))
         return b.value
 
-    def upload_data(self, X: np.ndarray, row_begin: int = 0):
+    def upload_data(self, X: np.ndarray, row_begin: int = 0, asynchronous: bool = False):
+        """Rows [row_begin, row_begin + len(X)) of this shard. asynchronous:
+        vmfa_upload_data_async -- the copy overlaps the work enqueued next (X
+        must stay unchanged until the next synchronising call; the session
+        keeps a reference to it)."""
         X = _c(X, np.float32)
-        check(lib().vmfa_upload_data(self._h, ptr(X), row_begin, X.shape[0]))
+        if asynchronous:
+            check(lib().vmfa_upload_data_async(self._h, ptr(X), row_begin, X.shape[0]))
+            self._pending_x = X
+        else:
+            check(lib().vmfa_upload_data(self._h, ptr(X), row_begin, X.shape[0]))
+
+    def set_lookahead(self, enable: bool):
+        """vmfa_set_lookahead: truncated F from the next E-step's anchor pass
+        (default) or from its own one-component pass (same value)."""
+        check(lib().vmfa_set_lookahead(self._h, 1 if enable else 0))
 
     # -- params / caches
     def set_floor(self, floor):

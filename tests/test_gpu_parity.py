@@ -363,6 +363,32 @@ def test_exact_log_likelihood_matches_oracle(oracle, gpu, case):
     sess.close()
 
 
+def test_async_upload_matches_sync(oracle, gpu):
+    # vmfa_upload_data_async: the copy runs on a second stream, ordered after
+    # the work already enqueued and before the first X consumer; with lookahead
+    # off (vmfa_set_lookahead) the iteration is unchanged
+    O, V = oracle, gpu
+    X, _ = gaussian_problem(5000, 64, 20, 3, seed=8)
+    X2 = (X + np.float32(0.25)).astype(np.float32)
+    C, H, Cp, G = 30, 4, 3, 5
+    out = []
+    for asynchronous in (False, True):
+        p, st, floor, sess = _setup(O, V, X, C, H, Cp, G)
+        sess.variational_e_step(0, 0)
+        sess.iterate(0, 1)
+        sess.set_lookahead(not asynchronous)
+        pinned = np.empty_like(X2)
+        pinned[...] = X2
+        sess.upload_data(pinned, asynchronous=asynchronous)  # replaces the rows the last iteration used
+        r = sess.iterate(0, 2)
+        r3 = sess.iterate(0, 3)
+        out.append((r["F"], r3["F"], sess.download_state().K, sess.download_params().mu))
+        sess.close()
+    (a, a3, Ka, mua), (b, b3, Kb, mub) = out
+    assert a == b and a3 == b3
+    assert np.array_equal(Ka, Kb) and np.array_equal(mua, mub)
+
+
 def test_upload_state_validates_K_on_device(gpu):
     # VarState::validate (estep.cpp:15-68): K rows sorted, distinct, in range
     V = gpu
