@@ -221,6 +221,15 @@ inline double truncated_free_energy(Session& s, const VarState& ksets) {
   return F;
 }
 
+// exact_log_likelihood (model.hpp:108-111): sum_n log sum_c p(x_n, c) over all
+// C components under the session's parameters (the NLL of trainer.cpp:49-56,
+// 79-85 is -exact_log_likelihood / N).
+inline double exact_log_likelihood(Session& s) {
+  double ll = 0.0;
+  check(vmfa_exact_log_likelihood(s.handle(), &ll));
+  return ll;
+}
+
 // train_vmfa's loop (trainer.cpp:111-186) with fixed warm-up / main counts.
 struct IterationRecord {
   bool warmup = false;
