@@ -346,7 +346,7 @@ int score_anchors(vmfa_ctx* x) {
   TRY(ensure_kinv_current(x));
   if (x->scorer == 2) {
     const int tok = x->begin(kFamOther, dm.C);
-    CU(launch_ws_images(dm, 0, x->WT, x->mu32, x->ipsi32, x->g, x->gcnt, x->bimg, x->bscl, s));
+    CU(launch_ws_images(dm, 0, x->WT, x->mu32, x->ipsi32, x->g, x->gcnt, x->bimg, x->bscl, s, x->sscl));
     CU(launch_ws_records(dm, 0, x->WT, x->mu32, x->ipsi32, x->kconst, x->g, x->gcnt, x->bscl, x->brec, s));
     x->end(tok);
   }
@@ -1223,7 +1223,8 @@ int vmfa_exact_log_likelihood(vmfa_ctx* x, double* ll) {
   const bool ws = x->scorer == 2;
   CU(launch_dense_groups(C, G, x->dense_g, x->dense_gcnt, s));
   if (ws) {
-    CU(launch_ws_images(dm, 0, x->WT, x->mu32, x->ipsi32, x->dense_g, x->dense_gcnt, x->bimg, x->bscl, s));
+    CU(launch_ws_images(dm, 0, x->WT, x->mu32, x->ipsi32, x->dense_g, x->dense_gcnt, x->bimg, x->bscl, s,
+                        x->sscl));
     CU(launch_ws_records(dm, 0, x->WT, x->mu32, x->ipsi32, x->kconst, x->dense_g, x->dense_gcnt, x->bscl, x->brec,
                          s));
   }

@@ -246,7 +246,8 @@ cudaError_t launch_ws_records(const Dims& dm, int single, const float* WT, const
 int64_t ws_image_halves(const Dims& dm, int single);
 int64_t ws_scale_floats(const Dims& dm, int single);
 cudaError_t launch_ws_images(const Dims& dm, int single, const float* WT, const float* mu32, const float* ipsi32,
-                             const int* g, const int* gcnt, void* img, float* bscl, cudaStream_t s);
+                             const int* g, const int* gcnt, void* img, float* bscl, cudaStream_t s,
+                             const float* sscl = nullptr);
 // per-row max |value| of an N x D fp32 matrix (A-row scale bounds)
 cudaError_t launch_rowmax(int64_t N, int D, const float* X, float* xmax, cudaStream_t s);
 

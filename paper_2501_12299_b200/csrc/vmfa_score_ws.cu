@@ -746,13 +746,16 @@ __global__ void __launch_bounds__(256) k_build_records(Dims dm, int Hp, int qg, 
 // one component (q = a), lin = 0 (extra candidates, truncated F).
 __global__ void __launch_bounds__(256) k_build_images(Dims dm, int Hp, int qg, int ngroups, int N1max, int single,
                                                       const float* WT, const float* mu32, const float* ipsi32,
-                                                      const int* g, const int* gcnt, __half* img, float* bscl) {
+                                                      const int* g, const int* gcnt, __half* img, float* bscl,
+                                                      const float* sscl, int N1max1) {
   const int lane = threadIdx.x & 31;
   const int nchunk = (dm.D + kKC - 1) / kKC;
   const int ng = single ? 1 : ngroups;
   const int nrow = N1max + kNL;
+  const int nrow1 = N1max1 + kNL;  // rows of a one-component image (sscl layout)
   const int64_t stage_h = 2 * 64 * (int64_t)nrow;  // halves per stage
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const bool vec = (dm.D & 3) == 0;
   for (int64_t wi = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; wi < (int64_t)dm.C * ng * nrow;
        wi += nw) {
     const int row = static_cast<int>(wi % nrow);
@@ -773,19 +776,59 @@ __global__ void __launch_bounds__(256) k_build_images(Dims dm, int Hp, int qg, i
     } else if (row - N1max < nq) {
       kind = 3, q = single ? a : g[(int64_t)a * dm.G + slot0 + (row - N1max)];
     }
-    auto value = [&](int d) -> float {
-      if (kind == 1)
-        return -2.f * ipsi32[(int64_t)q * dm.D + d] * (mu32[(int64_t)q * dm.D + d] - mu32[(int64_t)a * dm.D + d]);
-      if (kind == 2) return WT[((int64_t)q * Hp + h) * dm.D + d];
-      if (kind == 3) return ipsi32[(int64_t)q * dm.D + d];
-      return 0.f;
-    };
-    float mx = 0.f;
-    if (kind != 0)
-      for (int d = lane; d < dm.D; d += 32) mx = fmaxf(mx, fabsf(value(d)));
+    const float* src = kind == 2 ? WT + ((int64_t)q * Hp + h) * dm.D : ipsi32 + (int64_t)q * dm.D;
+    const float* mq = mu32 + (int64_t)q * dm.D;
+    const float* ma = mu32 + (int64_t)a * dm.D;
+    // 8 consecutive values from d0 (vector loads when aligned and in range)
+    auto load8 = [&](int d0, float* v) {
+      if (kind == 0) {
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    const int k = scale_exp(mx);
+        for (int i = 0; i < 8; ++i) v[i] = 0.f;
+        return;
+      }
+      if (vec && d0 + 8 <= dm.D) {
+        const float4 s0 = *reinterpret_cast<const float4*>(src + d0), s1 = *reinterpret_cast<const float4*>(src + d0 + 4);
+        v[0] = s0.x, v[1] = s0.y, v[2] = s0.z, v[3] = s0.w, v[4] = s1.x, v[5] = s1.y, v[6] = s1.z, v[7] = s1.w;
+        if (kind == 1) {
+          const float4 q0 = *reinterpret_cast<const float4*>(mq + d0), q1 = *reinterpret_cast<const float4*>(mq + d0 + 4);
+          const float4 a0 = *reinterpret_cast<const float4*>(ma + d0), a1 = *reinterpret_cast<const float4*>(ma + d0 + 4);
+          const float dq[8] = {q0.x - a0.x, q0.y - a0.y, q0.z - a0.z, q0.w - a0.w,
+                               q1.x - a1.x, q1.y - a1.y, q1.z - a1.z, q1.w - a1.w};
+#pragma unroll
+          for (int i = 0; i < 8; ++i) v[i] = -2.f * v[i] * dq[i];
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int d = d0 + i;
+          float x = 0.f;
+          if (d < dm.D) {
+            x = src[d];
+            if (kind == 1) x = -2.f * x * (mq[d] - ma[d]);
+          }
+          v[i] = x;
+        }
+      }
+    };
+    // row scale: W / psi rows reuse the one-component images' scales (same
+    // row of the same component); lin rows depend on the anchor: max pass
+    int k = 0;
+    if (!single && sscl && (kind == 2 || kind == 3)) {
+      const int r1 = kind == 2 ? kNL + h : N1max1;
+      k = -static_cast<int>(((__float_as_uint(sscl[(int64_t)q * nrow1 + r1]) >> 23) & 0xffu)) + 127;
+    } else {
+      float mx = 0.f;
+      if (kind != 0)
+        for (int d0 = 8 * lane; d0 < dm.D; d0 += 256) {
+          float v[8];
+          load8(d0, v);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) mx = fmaxf(mx, fabsf(v[i]));
+        }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      k = scale_exp(mx);
+    }
     const float sc = exp2i(k);
     if (lane == 0) bscl[((int64_t)a * ng + grp) * nrow + row] = exp2i(-k);
     // matrix offsets (halves) within a stage: B1 hi 0, B1 lo N1max*64, B2 hi 2*N1max*64, B2 lo +16*64
@@ -795,14 +838,11 @@ __global__ void __launch_bounds__(256) k_build_images(Dims dm, int Hp, int qg, i
     __half* base = img + ((int64_t)a * ng + grp) * nchunk * stage_h;
     for (int u = lane; u < nchunk * (kKC / 8); u += 32) {  // one 16-byte unit (8 halves) per lane
       const int ch = u / (kKC / 8), j = u - ch * (kKC / 8);
+      float v[8];
+      load8(ch * kKC + 8 * j, v);
       uint32_t hw[4], lw[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int d0 = ch * kKC + 8 * j + 2 * i;
-        const float v0 = (kind != 0 && d0 < dm.D) ? value(d0) * sc : 0.f;
-        const float v1 = (kind != 0 && d0 + 1 < dm.D) ? value(d0 + 1) * sc : 0.f;
-        split2(v0, v1, hw[i], lw[i]);
-      }
+      for (int i = 0; i < 4; ++i) split2(v[2 * i] * sc, v[2 * i + 1] * sc, hw[i], lw[i]);
       const int pos = rr * 64 + (((j ^ (rr & 7)) & 7) << 3);  // 128B swizzle: 16-byte unit j of row rr
       __half* st = base + ch * stage_h;
       *reinterpret_cast<uint4*>(st + off_hi + pos) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
@@ -865,10 +905,12 @@ int64_t ws_record_floats(const Dims& dm, int single) {
 }
 
 cudaError_t launch_ws_images(const Dims& dm, int single, const float* WT, const float* mu32, const float* ipsi32,
-                             const int* g, const int* gcnt, void* img, float* bscl, cudaStream_t s) {
+                             const int* g, const int* gcnt, void* img, float* bscl, cudaStream_t s,
+                             const float* sscl) {
   k_build_images<<<sm_count() * 8, 256, 0, s>>>(dm, ws_hp(dm.H), ws_qg(dm, single), ws_groups(dm),
                                                 ws_n1max(dm, single), single, WT, mu32, ipsi32, g, gcnt,
-                                                static_cast<__half*>(img), bscl);
+                                                static_cast<__half*>(img), bscl, single ? nullptr : sscl,
+                                                ws_n1max(dm, 1));
   return cudaGetLastError();
 }
 
