@@ -1129,6 +1129,7 @@ __global__ void __launch_bounds__(kStatsThreads, NH1 > 9 ? 1 : 2) k_stats(StatsA
     double* red = reinterpret_cast<double*>(s_x);  // >= RG * GD * 4 * (NH1 + 1) doubles
     double* pp = direct ? nullptr : part + (int64_t)item * part_stride;
     double* pe = direct ? a.E + (int64_t)c * H1 * H1 : pp + (int64_t)NH1 * D + D;
+    __syncthreads();  // every row group's E entry (and phase ii) done
     if (ei >= 0 && eg == 0) {
       double e = 0.0;
       for (int g = 0; g < EG; ++g) e += s_accE[tid + g * NE];
