@@ -89,6 +89,22 @@ def test_estep_teacher_forced(oracle, gpu, case, scorer, monkeypatch):
     sess.close()
 
 
+@pytest.mark.parametrize("scorer", ["ws", "tc"])
+def test_estep_config3_shape(oracle, gpu, scorer, monkeypatch):
+    # BASELINE config 3's shape (D = 784, H = 16, C' = 5, G = 10) at a small N
+    # (the FFMA cross-check scorer's tile stops at D = 775)
+    O, V = oracle, gpu
+    monkeypatch.setenv("VMFA_SCORER", scorer)
+    X, _ = gaussian_problem(1500, 784, 20, 4, seed=13)
+    C, H, Cp, G = 40, 16, 5, 10
+    p, st, floor, sess = _setup(O, V, X, C, H, Cp, G)
+    for it in range(2):
+        e_or, st_or, F, J, ret, st_g, k = _estep_both(O, V, sess, X, p, st, 3, it)
+        compare_estep(O, e_or, st_or, F, J, ret, st_g, Cp)
+        st = st_or
+    sess.close()
+
+
 def test_estep_euclid_and_frozen(oracle, gpu):
     O, V = oracle, gpu
     X, _ = gaussian_problem(3000, 48, 30, 3, seed=3)
@@ -104,10 +120,17 @@ def test_estep_euclid_and_frozen(oracle, gpu):
     sess.close()
 
 
-def test_mstep_parity(oracle, gpu):
+@pytest.mark.parametrize("case", [
+    dict(N=5000, D=40, C=30, H=3, Cp=3, G=5),     # 5-column statistics pass
+    dict(N=4000, D=256, C=60, H=8, Cp=5, G=10),   # config 2 shape: 9-column pass, bulk row gather
+    dict(N=3000, D=30, C=25, H=16, Cp=3, G=5),    # 17-column pass, D % 4 != 0 (4-byte gather)
+    dict(N=2500, D=64, C=20, H=20, Cp=3, G=4),    # H + 1 > 17: two column passes + separate E pass
+    dict(N=1500, D=784, C=24, H=16, Cp=5, G=10),  # config 3 shape (D = 784)
+])
+def test_mstep_parity(oracle, gpu, case):
     O, V = oracle, gpu
-    X, _ = gaussian_problem(5000, 40, 20, 3, seed=5)
-    C, H, Cp, G = 30, 3, 3, 5
+    X, _ = gaussian_problem(case["N"], case["D"], max(4, case["C"] // 2), min(case["H"], 4), seed=5)
+    C, H, Cp, G = case["C"], case["H"], case["Cp"], case["G"]
     p, st, floor, sess = _setup(O, V, X, C, H, Cp, G)
     sess.variational_e_step(0, 0)
     _, _, _, resp = sess.download_estep()
