@@ -407,6 +407,19 @@ def main():
         "update_precompute": C * (4 * D * H * H + 2 * D * (H + 1) ** 2 + H ** 3) / fp32_peak,
     }
     t_roof = sum(roof.values())
+    # the statistics pass (the other large kernel) against its own roof
+    st_ms = phase_ms.get("stats", 0.0)
+    stats_roof = None
+    if st_ms > 0:
+        pairs = n_loc * Cp
+        stats_roof = {"kernel": "statistics (k_stats + reduce + uncenter + Sigma_z)", "ms": st_ms,
+                      "achieved_gbs": pairs * Bm / (st_ms * 1e-3) / 1e9, "peak_gbs": pk["hbm"],
+                      "frac_hbm": pairs * Bm / (st_ms * 1e-3) / 1e9 / pk["hbm"],
+                      "achieved_tflops": pairs * Fm / (st_ms * 1e-3) / 1e12,
+                      "fp32_peak_tflops_est": fp32_peak / 1e12,
+                      "frac_fp32": pairs * Fm / (st_ms * 1e-3) / fp32_peak,
+                      "per_unit": f"B_m = 4D+12 = {Bm} B, F_m = 4DH+5D+3H^2 = {Fm} flop per (n, c in K(n)) pair "
+                                  f"(SURVEY §8(d)), {pairs} pairs"}
     iter_roof = {"t_roof_ms": t_roof * 1e3, "t_iter_ms": ms_step, "frac": t_roof * 1e3 / ms_step,
                  "phases_ms": {k: v * 1e3 for k, v in roof.items()},
                  "how": "SURVEY §8(d): per phase max(F/P_pipe, B/BW); scoring/F at J and N*C' joints "
@@ -443,6 +456,7 @@ def main():
                          "per_unit": f"B_j = 4D+8 = {Bj} B per joint (SURVEY §8(d)), J={J_local:.0f} joints per launch pair",
                          "flops_view": {"achieved_tflops": ach_tfs, "F_j": Fj}},
             "iteration_roofline": iter_roof,
+            "roofline_statistics": stats_roof,
             "exact_ll": exact,
             "gpu_launches": int(n_launch * args.steps),
             "launches_per_step": n_launch,
