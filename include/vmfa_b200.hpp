@@ -15,6 +15,9 @@
 #include <cstdint>
 #include <stdexcept>
 #include <string>
+#include <chrono>
+#include <cmath>
+#include <limits>
 #include <vector>
 
 #include "vmfa_b200.h"
@@ -263,6 +266,104 @@ inline std::vector<IterationRecord> train_fixed(Session& s, uint64_t seed, int w
     recs.push_back(r);
   }
   return recs;
+}
+
+// check_convergence (trainer.hpp:76-80).
+inline bool check_convergence(double f_prev, double f_curr, double epsilon, bool literal = false) {
+  if (literal) return (f_curr - f_prev) / f_prev < epsilon;
+  return std::abs(f_curr - f_prev) < epsilon * std::abs(f_prev);
+}
+
+// The TrainConfig / InitConfig fields train_vmfa's loop reads (trainer.hpp:19-37,
+// seeding.hpp:18-19).
+struct TrainConfig {
+  uint64_t seed = 0;
+  double epsilon = 1e-4;
+  int max_iters = 500;
+  DistanceMode distance_mode = DistanceMode::kl;
+  int eval_nll_every = 0;
+  bool literal_eq14 = false;
+  bool halt_on_max_iters = true;
+  double warmup_epsilon = 1e-4;
+  int warmup_max_iters = 1000;
+};
+struct TrainRecord {
+  int t = 0;
+  bool warmup = false;
+  double F = 0.0;
+  uint64_t joint_evals = 0;
+  double wall_ms = 0.0;
+  int empty_components = 0;
+  double nll_train = std::numeric_limits<double>::quiet_NaN();
+};
+struct TrainReport {
+  std::vector<TrainRecord> iterations;
+  int warmup_iterations = 0;
+  int main_iterations = 0;
+  bool converged = false;
+  uint64_t joint_evals = 0;
+  double total_wall_ms = 0.0;
+  double nll_train = std::numeric_limits<double>::quiet_NaN();
+};
+
+// train_vmfa's loop (trainer.cpp:111-186) on the device after the caller's
+// initialisation: convergence-gated warm-up (MaxIterExceeded at the cap),
+// main iterations until check_convergence, exact NLL every eval_nll_every
+// iterations (excluded from the wall time) and at the end (finalize_nll).
+inline TrainReport train_vmfa(Session& s, const TrainConfig& cfg) {
+  using clk = std::chrono::steady_clock;
+  auto ms = [](clk::time_point a) { return std::chrono::duration<double, std::milli>(clk::now() - a).count(); };
+  auto nll = [&]() { return -exact_log_likelihood(s) / static_cast<double>(s.rows()); };
+  TrainReport rep;
+  const auto t_start = clk::now();
+  double excluded = 0.0;
+  uint64_t it = 0;
+  double prev = std::numeric_limits<double>::quiet_NaN();
+  for (int w = 0; w < cfg.warmup_max_iters; ++w) {
+    const auto t0 = clk::now();
+    TrainRecord r;
+    uint64_t j = 0;
+    check(vmfa_estep(s.handle(), cfg.seed, it++, static_cast<int>(cfg.distance_mode), &r.F, &j));
+    rep.joint_evals += j;
+    r.t = ++rep.warmup_iterations;
+    r.warmup = true;
+    r.joint_evals = rep.joint_evals;
+    r.wall_ms = ms(t0);
+    rep.iterations.push_back(r);
+    if (std::isfinite(prev) && check_convergence(prev, r.F, cfg.warmup_epsilon, cfg.literal_eq14)) break;
+    prev = r.F;
+    if (w + 1 == cfg.warmup_max_iters) throw MaxIterExceeded("warm-up did not converge");
+  }
+  double prev_f = std::numeric_limits<double>::quiet_NaN();
+  for (int t = 1; t <= cfg.max_iters; ++t) {
+    const auto t0 = clk::now();
+    vmfa_iter_report ir{};
+    check(vmfa_iterate(s.handle(), cfg.seed, it++, static_cast<int>(cfg.distance_mode), &ir));
+    rep.joint_evals += ir.joints;
+    ++rep.main_iterations;
+    TrainRecord r;
+    r.t = t;
+    r.F = ir.free_energy;
+    r.joint_evals = rep.joint_evals;
+    r.wall_ms = ms(t0);
+    r.empty_components = ir.empty_components;
+    if (cfg.eval_nll_every > 0 && t % cfg.eval_nll_every == 0) {
+      const auto t1 = clk::now();
+      r.nll_train = nll();
+      excluded += ms(t1);
+    }
+    rep.iterations.push_back(r);
+    if (std::isfinite(prev_f) && check_convergence(prev_f, r.F, cfg.epsilon, cfg.literal_eq14)) {
+      rep.converged = true;
+      break;
+    }
+    prev_f = r.F;
+  }
+  if (!rep.converged && cfg.halt_on_max_iters)
+    throw MaxIterExceeded("training did not converge within " + std::to_string(cfg.max_iters) + " iterations");
+  rep.total_wall_ms = ms(t_start) - excluded;
+  rep.nll_train = nll();
+  return rep;
 }
 
 }  // namespace vmfa_b200

@@ -396,5 +396,103 @@ def train_fixed(sess: Session, seed: int, warmup: int, iters: int, mode: int = K
     return recs
 
 
+def check_convergence(f_prev: float, f_curr: float, epsilon: float, literal: bool = False) -> bool:
+    """check_convergence (trainer.hpp:76-80): |F - F_prev| < eps |F_prev|;
+    literal Eq. 14 uses the signed ratio (F - F_prev) / F_prev < eps."""
+    if literal:
+        return (f_curr - f_prev) / f_prev < epsilon
+    return abs(f_curr - f_prev) < epsilon * abs(f_prev)
+
+
+@dataclass
+class TrainConfig:
+    """The training-loop fields of TrainConfig / InitConfig (trainer.hpp:19-37,
+    seeding.hpp:18-19) that train_vmfa's loop reads."""
+    seed: int = 0
+    epsilon: float = 1e-4
+    max_iters: int = 500
+    mode: int = 0  # KL
+    eval_nll_every: int = 0
+    literal_eq14: bool = False
+    halt_on_max_iters: bool = True
+    warmup_epsilon: float = 1e-4
+    warmup_max_iters: int = 1000
+
+
+def train_vmfa(sess: Session, cfg: TrainConfig, testset: Session | None = None) -> dict:
+    """train_vmfa's loop (trainer.cpp:111-186) on the device, after the
+    caller's initialisation (parameters, floor and state uploaded): warm-up
+    E-steps at fixed parameters until check_convergence(warmup_epsilon) or
+    MaxIterExceeded, then main iterations (E-step, statistics, update,
+    precompute, truncated F) until check_convergence(epsilon); optional exact
+    NLL every eval_nll_every iterations (train, and test on a second session
+    holding the test rows and the same parameters); final NLL. Returns the
+    TrainReport fields (trainer.hpp:39-64) with per-iteration records."""
+    import math
+    import time
+
+    def nll(s):  # nll_per_point (trainer.cpp:79-85) over one context's rows
+        return -s.exact_log_likelihood() / s.N
+
+    def sync_test():
+        if testset is not None:
+            testset.upload_params(sess.download_params())
+
+    recs, joints = [], 0
+    t_start = time.perf_counter()
+    empty0 = int((sess.download_params().pi == 0.0).sum())  # count_empty (fixed during warm-up)
+    excluded = 0.0
+    it_index = 0
+    warm, main = 0, 0
+    prev = math.nan
+    for it in range(cfg.warmup_max_iters):  # trainer.cpp:115-142
+        t0 = time.perf_counter()
+        F, J = sess.variational_e_step(cfg.seed, it_index, cfg.mode)
+        it_index += 1
+        warm += 1
+        joints += J
+        recs.append(dict(t=warm, warmup=True, F=F, joint_evals=joints,
+                         wall_ms=(time.perf_counter() - t0) * 1e3, empty_components=empty0))
+        if math.isfinite(prev) and check_convergence(prev, F, cfg.warmup_epsilon, cfg.literal_eq14):
+            break
+        prev = F
+        if it + 1 == cfg.warmup_max_iters:
+            raise VmfaError(6, "warm-up did not converge")
+    prev_f, converged = math.nan, False
+    for t in range(1, cfg.max_iters + 1):  # trainer.cpp:147-186
+        t0 = time.perf_counter()
+        r = sess.iterate(cfg.seed, it_index, cfg.mode)
+        it_index += 1
+        main += 1
+        joints += r["joints"]
+        rec = dict(t=t, warmup=False, F=r["F"], F_estep=r["F_estep"], joint_evals=joints,
+                   wall_ms=(time.perf_counter() - t0) * 1e3, empty_components=r["empty"],
+                   nll_train=math.nan, nll_test=math.nan)
+        if cfg.eval_nll_every > 0 and t % cfg.eval_nll_every == 0:
+            t1 = time.perf_counter()
+            rec["nll_train"] = nll(sess)
+            if testset is not None:
+                sync_test()
+                rec["nll_test"] = nll(testset)
+            excluded += time.perf_counter() - t1
+        recs.append(rec)
+        if math.isfinite(prev_f) and check_convergence(prev_f, r["F"], cfg.epsilon, cfg.literal_eq14):
+            converged = True
+            break
+        prev_f = r["F"]
+    if not converged and cfg.halt_on_max_iters:
+        raise VmfaError(6, f"training did not converge within {cfg.max_iters} iterations")
+    report = dict(algo="vmfa", iterations=recs, warmup_iterations=warm, main_iterations=main,
+                  converged=converged, joint_evals=joints,
+                  empty_components=recs[-1]["empty_components"],
+                  total_wall_ms=(time.perf_counter() - t_start - excluded) * 1e3)
+    report["nll_train"] = nll(sess)  # finalize_nll (trainer.cpp:49-56)
+    if testset is not None:
+        sync_test()
+        report["nll_test"] = nll(testset)
+    return report
+
+
 __all__ = ["Params", "State", "Stats", "Session", "CONFIGS", "synth_spec", "gen_synthetic",
-           "initialize", "train_fixed", "device_available", "VmfaError", "KL", "EUCLID"]
+           "initialize", "train_fixed", "train_vmfa", "TrainConfig", "check_convergence",
+           "device_available", "VmfaError", "KL", "EUCLID"]

@@ -2,6 +2,7 @@
 // the reference's initialisation, then train_vmfa's loop with fixed counts.
 // Prints one line per iteration: warmup F F_estep joints.
 #include <cstdio>
+#include <string>
 #include <vector>
 
 #include "vmfa_b200.hpp"
@@ -33,9 +34,23 @@ int main(int argc, char** argv) {
     s.set_floor(floor);
     s.upload(p);
     s.upload(st);
-    for (const auto& r : vmfa_b200::train_fixed(s, 0, 2, 20))
-      std::printf("%d %.10f %.10f %llu\n", r.warmup ? 1 : 0, r.F, r.F_estep,
-                  static_cast<unsigned long long>(r.joint_evals));
+    if (argc > 2 && std::string(argv[2]) == "converge") {  // train_vmfa's convergence-gated loop
+      vmfa_b200::TrainConfig cfg;
+      cfg.epsilon = 1e-4;
+      cfg.max_iters = 60;
+      cfg.eval_nll_every = 5;
+      cfg.warmup_epsilon = 1e-3;
+      cfg.halt_on_max_iters = false;
+      const auto rep = vmfa_b200::train_vmfa(s, cfg);
+      for (const auto& r : rep.iterations)
+        std::printf("%d %.10f %.10f %llu\n", r.warmup ? 1 : 0, r.F, r.nll_train,
+                    static_cast<unsigned long long>(r.joint_evals));
+      std::printf("final %d %d %.10f\n", rep.converged ? 1 : 0, rep.main_iterations, rep.nll_train);
+    } else {
+      for (const auto& r : vmfa_b200::train_fixed(s, 0, 2, 20))
+        std::printf("%d %.10f %.10f %llu\n", r.warmup ? 1 : 0, r.F, r.F_estep,
+                    static_cast<unsigned long long>(r.joint_evals));
+    }
   } catch (const vmfa_b200::DeviceError& e) {
     std::fprintf(stderr, "device error: %s\n", e.what());
     return 3;

@@ -319,6 +319,25 @@ def test_cpp_mirror_matches_python_path(gpu, tmp_path):
     for r, q in zip(rows, recs):
         assert float(r[1]) == pytest.approx(q["F"], rel=1e-12, abs=0)
     s.close()
+    # train_vmfa (convergence-gated loop) through both mirrors
+    out = subprocess.run([str(exe), "20000", "converge"], capture_output=True, text=True, check=True).stdout
+    lines = out.strip().splitlines()
+    fin = lines[-1].split()
+    rows = [l.split() for l in lines[:-1]]
+    s = V.Session(100, 64, 4, 3, 5, X)
+    s.set_floor(floor)
+    s.upload_params(p)
+    s.upload_state(st)
+    rep = V.train_vmfa(s, V.TrainConfig(epsilon=1e-4, max_iters=60, eval_nll_every=5, warmup_epsilon=1e-3,
+                                        halt_on_max_iters=False))
+    s.close()
+    assert len(rows) == len(rep["iterations"])
+    for r, q in zip(rows, rep["iterations"]):
+        assert float(r[1]) == pytest.approx(q["F"], rel=1e-12, abs=0)
+        if not q["warmup"] and q["t"] % 5 == 0:
+            assert float(r[2]) == pytest.approx(q["nll_train"], rel=1e-12)
+    assert int(fin[1]) == int(rep["converged"]) and int(fin[2]) == rep["main_iterations"]
+    assert float(fin[3]) == pytest.approx(rep["nll_train"], rel=1e-12)
 
 
 @pytest.mark.parametrize("scorer", ["ws", "tc"])
@@ -407,6 +426,42 @@ def test_no_truncation_limit_device(oracle, gpu):
         print("it", it, "F vs oracle LL", abs(r["F"] - ll_or) / abs(ll_or), "dense LL vs oracle", abs(ll - ll_or) / abs(ll_or))
         assert abs(ll - ll_or) <= 1e-5 * abs(ll_or) and abs(r["F"] - ll_or) <= 1e-5 * abs(ll_or)
     sess.close()
+
+
+def test_train_vmfa_convergence_loop(oracle, gpu):
+    # train_vmfa's loop (trainer.cpp:111-186): warm-up until check_convergence
+    # (warmup_epsilon), main iterations until check_convergence (epsilon), NLL
+    # every eval_nll_every iterations and at the end; the F sequence is the
+    # fixed-count loop's, and the stop points follow the rule on it
+    O, V = oracle, gpu
+    X, _ = gaussian_problem(4000, 32, 12, 2, seed=4)
+    C, H, Cp, G = 16, 2, 3, 4
+    cfg = V.TrainConfig(seed=3, epsilon=1e-3, max_iters=200, eval_nll_every=5, warmup_epsilon=1e-3,
+                        halt_on_max_iters=False)
+    _, _, _, sess = _setup(O, V, X, C, H, Cp, G)
+    rep = V.train_vmfa(sess, cfg)
+    sess.close()
+    assert rep["converged"]
+    _, _, _, s2 = _setup(O, V, X, C, H, Cp, G)
+    fixed = V.train_fixed(s2, 3, rep["warmup_iterations"], rep["main_iterations"])
+    s2.close()
+    Fw = [r["F"] for r in fixed if r["warmup"]]
+    Fm = [r["F"] for r in fixed if not r["warmup"]]
+    assert [r["F"] for r in rep["iterations"]] == Fw + Fm
+    # warm-up stopped at the first converged step (or ran to the cap)
+    stops = [i for i in range(1, len(Fw)) if V.check_convergence(Fw[i - 1], Fw[i], cfg.warmup_epsilon)]
+    assert stops == [len(Fw) - 1]
+    if rep["converged"]:
+        stops = [i for i in range(1, len(Fm)) if V.check_convergence(Fm[i - 1], Fm[i], cfg.epsilon)]
+        assert stops == [len(Fm) - 1]
+    nll_recs = [r for r in rep["iterations"] if not r["warmup"] and r["t"] % 5 == 0]
+    assert nll_recs and all(np.isfinite(r["nll_train"]) for r in nll_recs)
+    assert rep["nll_train"] > 0 and np.isfinite(rep["nll_train"])
+    # halt_on_max_iters: MaxIterExceeded at the cap
+    _, _, _, s3 = _setup(O, V, X, C, H, Cp, G)
+    with pytest.raises(V.VmfaError, match="MaxIterExceeded"):
+        V.train_vmfa(s3, V.TrainConfig(seed=3, epsilon=1e-12, max_iters=3, warmup_epsilon=1e-3))
+    s3.close()
 
 
 def test_async_upload_matches_sync(oracle, gpu):
