@@ -493,6 +493,28 @@ def train_vmfa(sess: Session, cfg: TrainConfig, testset: Session | None = None) 
     return report
 
 
+def write_report_jsonl(report: dict, out) -> None:
+    """TrainReport as JSON lines (SPEC.md 'External Interfaces'): one object
+    per iteration, then a final summary object. `out`: path or text stream;
+    NaN NLLs (not evaluated) are written as null."""
+    import json
+    import math
+
+    def clean(v):
+        return None if isinstance(v, float) and math.isnan(v) else v
+
+    f = open(out, "w") if isinstance(out, (str, os.PathLike)) else out
+    try:
+        for r in report["iterations"]:
+            f.write(json.dumps({k: clean(v) for k, v in r.items()}) + "\n")
+        summary = {k: clean(v) for k, v in report.items() if k != "iterations"}
+        summary["summary"] = True
+        f.write(json.dumps(summary) + "\n")
+    finally:
+        if f is not out:
+            f.close()
+
+
 __all__ = ["Params", "State", "Stats", "Session", "CONFIGS", "synth_spec", "gen_synthetic",
-           "initialize", "train_fixed", "train_vmfa", "TrainConfig", "check_convergence",
+           "initialize", "train_fixed", "train_vmfa", "TrainConfig", "check_convergence", "write_report_jsonl",
            "device_available", "VmfaError", "KL", "EUCLID"]

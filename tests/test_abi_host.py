@@ -124,3 +124,23 @@ def test_cpp_mirror_compiles_and_reports_no_device(vmfa, tmp_path):
         pytest.skip("a GPU is visible")
     r = subprocess.run([str(exe), "200"], capture_output=True, text=True)
     assert r.returncode == 3 and "no sm_100" in r.stderr
+
+
+def test_report_jsonl_and_convergence_rule():
+    # SPEC.md 'External Interfaces': one JSON object per iteration + a final
+    # summary; check_convergence (trainer.hpp:76-80) in both readings
+    import io
+    import json
+    import math
+    from paper_2501_12299_b200 import vmfa as V
+    assert V.check_convergence(-100.0, -100.005, 1e-4)
+    assert not V.check_convergence(-100.0, -100.02, 1e-4)
+    assert V.check_convergence(-100.0, -99.0, 1e-4, literal=True)  # any improvement fires
+    rep = dict(algo="vmfa", iterations=[dict(t=1, warmup=True, F=-5.0, nll_train=math.nan),
+                                        dict(t=1, warmup=False, F=-4.0, nll_train=2.5)],
+               warmup_iterations=1, main_iterations=1, converged=True, joint_evals=10, nll_train=2.4)
+    buf = io.StringIO()
+    V.write_report_jsonl(rep, buf)
+    lines = [json.loads(l) for l in buf.getvalue().splitlines()]
+    assert len(lines) == 3 and lines[0]["nll_train"] is None and lines[1]["nll_train"] == 2.5
+    assert lines[2]["summary"] and lines[2]["converged"] and "iterations" not in lines[2]
