@@ -61,6 +61,7 @@ typedef enum vmfa_status {
   VMFA_ERR_BAD_MAGIC = 9,              /* vmfa::BadMagic         errors.hpp:51 */
   VMFA_ERR_TRUNCATED_FILE = 10,        /* vmfa::TruncatedFile    errors.hpp:56 */
   VMFA_ERR_UNSUPPORTED_VERSION = 11,   /* vmfa::UnsupportedVersion errors.hpp:61 */
+  VMFA_ERR_IO = 12,                    /* vmfa::Error (errors.hpp:9): cannot open / write, invalid header sizes */
   VMFA_ERR_CUDA = 100,                 /* CUDA runtime failure (no reference twin) */
   VMFA_ERR_NO_DEVICE = 101,            /* no usable sm_100 device          */
   VMFA_ERR_UNSUPPORTED = 102           /* shape/feature outside this build */
@@ -254,6 +255,31 @@ int vmfa_host_initialize(const float* X, int64_t N, int D, int C, int H, int Cpr
                          uint64_t seed, double scale, int loading_init, double* floor,
                          double* pi, double* mu, double* lambda, double* dnoise, int32_t* K,
                          int32_t* g, int32_t* g_count, int64_t* seeds);
+
+/* ---- on-disk containers, host only, no device needed ----
+ * MFAD dataset (io.hpp:12-16, io.cpp:91-125): "MFAD", u32 version 1, u64 N,
+ * u32 D, u8 dtype 0 (f32), 7 reserved bytes, N x D f32 row-major, little-endian.
+ * Loads take a row range so each rank reads only its shard.                 */
+int vmfa_save_dataset(const char* path, const float* X, int64_t N, int D);
+int vmfa_dataset_info(const char* path, int64_t* N, int* D);
+int vmfa_load_dataset(const char* path, int64_t row_begin, int64_t rows, int D, float* X);
+/* MFAM checkpoint (io.hpp:18-23, io.cpp:127-179): "MFAM", u32 version 1, u32 C,
+ * D, H, then pi, mu, Lambda (row-major D x H per component in the file; this
+ * ABI's column-major blocks in memory), dnoise as f64. Save validates like
+ * MfaParams::validate (model.cpp:14-41).                                      */
+int vmfa_save_checkpoint(const char* path, int C, int D, int H, const double* pi, const double* mu,
+                         const double* lambda, const double* dnoise);
+int vmfa_checkpoint_info(const char* path, int* C, int* D, int* H);
+int vmfa_load_checkpoint(const char* path, int C, int D, int H, double* pi, double* mu, double* lambda,
+                         double* dnoise);
+/* MFAK variational-state sidecar (this project, for exact resume): "MFAK",
+ * u32 version 1, u64 N, u32 C', u32 C, u32 G, then K (i32 N x C'), g (i32
+ * C x G), g_count (i32 C).                                                    */
+int vmfa_save_state(const char* path, int64_t N, int Cprime, int C, int G, const int32_t* K,
+                    const int32_t* g, const int32_t* g_count);
+int vmfa_state_info(const char* path, int64_t* N, int* Cprime, int* C, int* G);
+int vmfa_load_state(const char* path, int64_t row_begin, int64_t rows, int Cprime, int C, int G,
+                    int32_t* K, int32_t* g, int32_t* g_count);
 
 #ifdef __cplusplus
 }

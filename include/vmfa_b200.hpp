@@ -55,6 +55,7 @@ inline void check(int code) {
     case VMFA_ERR_BAD_MAGIC: throw BadMagic(msg);
     case VMFA_ERR_TRUNCATED_FILE: throw TruncatedFile(msg);
     case VMFA_ERR_UNSUPPORTED_VERSION: throw UnsupportedVersion(msg);
+    case VMFA_ERR_IO: throw Error(msg);
     default: throw DeviceError(msg);
   }
 }
@@ -266,6 +267,33 @@ inline std::vector<IterationRecord> train_fixed(Session& s, uint64_t seed, int w
     recs.push_back(r);
   }
   return recs;
+}
+
+// ---- on-disk containers (io.hpp:12-23) ----------------------------------------
+inline void save_dataset(const Dataset& data, const std::string& path) {
+  check(vmfa_save_dataset(path.c_str(), data.rows.data(), data.N, data.D));
+}
+inline Dataset load_dataset(const std::string& path) {
+  Dataset d;
+  check(vmfa_dataset_info(path.c_str(), &d.N, &d.D));
+  d.rows.resize(static_cast<size_t>(d.N) * d.D);
+  check(vmfa_load_dataset(path.c_str(), 0, d.N, d.D, d.rows.data()));
+  return d;
+}
+inline void save_checkpoint(const MfaParams& p, const std::string& path) {
+  check(vmfa_save_checkpoint(path.c_str(), p.C, p.D, p.H, p.pi.data(), p.mu.data(), p.Lambda.data(),
+                             p.dnoise.data()));
+}
+inline MfaParams load_checkpoint(const std::string& path) {
+  MfaParams p;
+  check(vmfa_checkpoint_info(path.c_str(), &p.C, &p.D, &p.H));
+  p.pi.resize(p.C);
+  p.mu.resize(static_cast<size_t>(p.C) * p.D);
+  p.Lambda.resize(static_cast<size_t>(p.C) * p.D * p.H);
+  p.dnoise.resize(static_cast<size_t>(p.C) * p.D);
+  check(vmfa_load_checkpoint(path.c_str(), p.C, p.D, p.H, p.pi.data(), p.mu.data(), p.Lambda.data(),
+                             p.dnoise.data()));
+  return p;
 }
 
 // check_convergence (trainer.hpp:76-80).

@@ -18,7 +18,7 @@ STATUS = {
     0: "OK", 1: "InvalidArgument", 2: "CholeskyFailure", 3: "EmptyKSet",
     4: "InsufficientCandidates", 5: "SingularEc", 6: "MaxIterExceeded",
     7: "TargetUnreachable", 8: "DegenerateData", 9: "BadMagic", 10: "TruncatedFile",
-    11: "UnsupportedVersion", 100: "CudaError", 101: "NoDevice", 102: "Unsupported",
+    11: "UnsupportedVersion", 12: "IoError", 100: "CudaError", 101: "NoDevice", 102: "Unsupported",
 }
 
 
@@ -62,6 +62,15 @@ _SIGS = {
     "vmfa_upload_data": (_I, [_P, _P, _I64, _I64]),
     "vmfa_upload_data_async": (_I, [_P, _P, _I64, _I64]),
     "vmfa_set_lookahead": (_I, [_P, _I]),
+    "vmfa_save_dataset": (_I, [C.c_char_p, _P, _I64, _I]),
+    "vmfa_dataset_info": (_I, [C.c_char_p, _P, _P]),
+    "vmfa_load_dataset": (_I, [C.c_char_p, _I64, _I64, _I, _P]),
+    "vmfa_save_checkpoint": (_I, [C.c_char_p, _I, _I, _I, _P, _P, _P, _P]),
+    "vmfa_checkpoint_info": (_I, [C.c_char_p, _P, _P, _P]),
+    "vmfa_load_checkpoint": (_I, [C.c_char_p, _I, _I, _I, _P, _P, _P, _P]),
+    "vmfa_save_state": (_I, [C.c_char_p, _I64, _I, _I, _I, _P, _P, _P]),
+    "vmfa_state_info": (_I, [C.c_char_p, _P, _P, _P, _P]),
+    "vmfa_load_state": (_I, [C.c_char_p, _I64, _I64, _I, _I, _I, _P, _P, _P]),
     "vmfa_set_floor": (_I, [_P, _P]),
     "vmfa_upload_params": (_I, [_P, _P, _P, _P, _P]),
     "vmfa_download_params": (_I, [_P, _P, _P, _P, _P]),

@@ -23,7 +23,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 # extra nvcc flags for diagnostic builds (e.g. -DVMFA_STATS_PROF; rebuild with force=True)
 EXTRA = os.environ.get("VMFA_NVCC_EXTRA", "").split()
 CU_SOURCES = ["vmfa_kernels.cu", "vmfa_score_tc.cu", "vmfa_score_ws.cu", "vmfa_capi.cu"]
-CXX_SOURCES = ["host/vmfa_host.cpp"]
+CXX_SOURCES = ["host/vmfa_host.cpp", "host/vmfa_io.cpp"]
 DEPS_H = ["vmfa_kernels.cuh", "vmfa_internal.hpp", "vmfa_rng.hpp"]
 
 

@@ -493,6 +493,69 @@ def train_vmfa(sess: Session, cfg: TrainConfig, testset: Session | None = None) 
     return report
 
 
+# ---- on-disk containers (io.hpp:12-23; host only) -----------------------------
+def _path(p) -> bytes:
+    return os.fsencode(os.fspath(p))
+
+
+def save_dataset(path, X: np.ndarray) -> None:
+    """MFAD (io.cpp:91-104): bit-exact f32 rows."""
+    X = _c(X, np.float32)
+    check(lib().vmfa_save_dataset(_path(path), ptr(X), X.shape[0], X.shape[1]))
+
+
+def dataset_info(path) -> tuple[int, int]:
+    n, d = C.c_int64(), C.c_int()
+    check(lib().vmfa_dataset_info(_path(path), C.byref(n), C.byref(d)))
+    return n.value, d.value
+
+
+def load_dataset(path, row_begin: int = 0, rows: int | None = None) -> np.ndarray:
+    """MFAD (io.cpp:106-125); a row range reads one shard."""
+    n, d = dataset_info(path)
+    rows = n - row_begin if rows is None else rows
+    X = np.empty((rows, d), np.float32)
+    check(lib().vmfa_load_dataset(_path(path), row_begin, rows, d, ptr(X)))
+    return X
+
+
+def save_checkpoint(path, p: Params) -> None:
+    """MFAM (io.cpp:127-149), MfaParams::validate first."""
+    C_, D = p.mu.shape
+    H = p.lam.shape[1]
+    check(lib().vmfa_save_checkpoint(_path(path), C_, D, H, ptr(_c(p.pi, np.float64)), ptr(_c(p.mu, np.float64)),
+                                     ptr(_c(p.lam, np.float64)), ptr(_c(p.psi, np.float64))))
+
+
+def load_checkpoint(path) -> Params:
+    """MFAM (io.cpp:151-179)."""
+    c, d, h = C.c_int(), C.c_int(), C.c_int()
+    check(lib().vmfa_checkpoint_info(_path(path), C.byref(c), C.byref(d), C.byref(h)))
+    C_, D, H = c.value, d.value, h.value
+    p = Params(np.empty(C_), np.empty((C_, D)), np.empty((C_, H, D)), np.empty((C_, D)))
+    check(lib().vmfa_load_checkpoint(_path(path), C_, D, H, ptr(p.pi), ptr(p.mu), ptr(p.lam), ptr(p.psi)))
+    return p
+
+
+def save_state(path, st: State) -> None:
+    """MFAK sidecar: K, g, g_count (exact resume)."""
+    K = _c(st.K, np.int32)
+    g = _c(st.g, np.int32)
+    check(lib().vmfa_save_state(_path(path), K.shape[0], K.shape[1], g.shape[0], g.shape[1], ptr(K), ptr(g),
+                                ptr(_c(st.g_count, np.int32))))
+
+
+def load_state(path, row_begin: int = 0, rows: int | None = None) -> State:
+    n, cp, c, gg = C.c_int64(), C.c_int(), C.c_int(), C.c_int()
+    check(lib().vmfa_state_info(_path(path), C.byref(n), C.byref(cp), C.byref(c), C.byref(gg)))
+    rows = n.value - row_begin if rows is None else rows
+    st = State(np.empty((rows, cp.value), np.int32), np.empty((c.value, gg.value), np.int32),
+               np.empty(c.value, np.int32))
+    check(lib().vmfa_load_state(_path(path), row_begin, rows, cp.value, c.value, gg.value, ptr(st.K), ptr(st.g),
+                                ptr(st.g_count)))
+    return st
+
+
 def write_report_jsonl(report: dict, out) -> None:
     """TrainReport as JSON lines (SPEC.md 'External Interfaces'): one object
     per iteration, then a final summary object. `out`: path or text stream;
@@ -517,4 +580,6 @@ def write_report_jsonl(report: dict, out) -> None:
 
 __all__ = ["Params", "State", "Stats", "Session", "CONFIGS", "synth_spec", "gen_synthetic",
            "initialize", "train_fixed", "train_vmfa", "TrainConfig", "check_convergence", "write_report_jsonl",
+           "save_dataset", "load_dataset", "dataset_info", "save_checkpoint", "load_checkpoint", "save_state",
+           "load_state",
            "device_available", "VmfaError", "KL", "EUCLID"]
