@@ -464,6 +464,34 @@ def test_train_vmfa_convergence_loop(oracle, gpu):
     s3.close()
 
 
+def test_checkpoint_resume_is_exact(oracle, gpu, tmp_path):
+    # MFAD + MFAM + MFAK: stop after 3 iterations, write
+    # the containers, resume in a fresh session from the files -> the same
+    # trajectory as the uninterrupted run, bit for bit
+    O, V = oracle, gpu
+    X, _ = gaussian_problem(3000, 40, 10, 2, seed=6)
+    C, H, Cp, G = 14, 2, 3, 4
+    V.save_dataset(tmp_path / "x.mfad", X)
+    p, st, floor, a = _setup(O, V, X, C, H, Cp, G)
+    a.variational_e_step(0, 0)
+    full = [a.iterate(0, it)["F"] for it in range(1, 7)]
+    a.close()
+    _, _, _, b = _setup(O, V, X, C, H, Cp, G)
+    b.variational_e_step(0, 0)
+    first = [b.iterate(0, it)["F"] for it in range(1, 4)]
+    V.save_checkpoint(tmp_path / "m.mfam", b.download_params())
+    V.save_state(tmp_path / "s.mfak", b.download_state())
+    b.close()
+    Xr = V.load_dataset(tmp_path / "x.mfad")
+    r = V.Session(C, Xr.shape[1], H, Cp, G, Xr)
+    r.set_floor(floor)
+    r.upload_params(V.load_checkpoint(tmp_path / "m.mfam"))
+    r.upload_state(V.load_state(tmp_path / "s.mfak"))
+    rest = [r.iterate(0, it)["F"] for it in range(4, 7)]
+    r.close()
+    assert first + rest == full
+
+
 def test_async_upload_matches_sync(oracle, gpu):
     # vmfa_upload_data_async: the copy runs on a second stream, ordered after
     # the work already enqueued and before the first X consumer; with lookahead
