@@ -33,6 +33,7 @@
 //              NB-deep ring (few large copies keep many bytes in flight).
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include <cuda_fp16.h>
 
@@ -55,8 +56,10 @@ constexpr int kThreads = (kLoadWarp + 1) * 32;
 constexpr int kMaxNB = 8;             // B ring stages (smem)
 constexpr int kMaxXSlots = 4;         // X ring slots (row chunks); prefetch depth = slots - 1
 constexpr int kXSeg = kElem / 4;      // 16-byte pieces per thread per chunk
-constexpr int kXRow = kKC + 4;        // floats per row chunk in the X ring (padded: conflict-free LDS.128)
-constexpr uint32_t kXSlotBytes = kRows * kXRow * 4;
+constexpr int kMaxCps = 2;             // K chunks per X-ring slot, at most
+// floats per row of a slot holding `cps` chunks (padded: conflict-free LDS.128)
+__host__ __device__ constexpr int x_row(int cps) { return cps * kKC + 4; }
+__host__ __device__ constexpr uint32_t x_slot_bytes(int cps) { return kRows * x_row(cps) * 4; }
 constexpr int kMaxD = 1024;
 constexpr int kNL = 16;               // lin rows / psi rows per group (qg <= 16)
 constexpr int kTargetExp = 14;        // operands scaled to |value| <= 2^14
@@ -73,6 +76,7 @@ struct WsArgs {
   int N1max;         // 16 + round16(qg * Hp)
   int nbstage;       // B ring depth
   int xslots;        // X ring slots (2..kMaxXSlots)
+  int cps;           // K chunks per X-ring slot (one bulk copy per row and slot)
   int nacc;          // accumulator buffers in TMEM (2 when they fit beside the A stages)
   uint32_t tmem_cols;
   uint32_t TB;       // TMEM columns per accumulator buffer
@@ -362,7 +366,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_ws(WsArgs a) {
     const int ar = 32 * (warp & 3) + lane, ah = warp >> 2;  // row, K slice
     const int quad = warp & 3;
     const int XS = a.xslots;
-    const int ahead = min(XS - 1, nchunk);
+    const int CPS = a.cps;
+    const int XR = x_row(CPS);
+    const uint32_t SLOT = x_slot_bytes(CPS);
+    const int nslot = (nchunk + CPS - 1) / CPS;  // X-ring slots per job
+    const int ahead = min(XS - 1, nslot);
     const uint32_t xbase = sbase + NB * a.stage_bytes;
     Prof pf{};
     if (PROF) pf.start();
@@ -371,22 +379,25 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_ws(WsArgs a) {
     wn.advance(a.jobs, a.qg, total);
     int n_cur = w.valid(total) ? job_row(a, w.J, ar) : -1;
     int n_nxt = wn.valid(total) ? job_row(a, wn.J, ar) : -1;
-    // issue unit `unit` (chunk ch of row n) of this quadrant (slice-0 warps only)
-    auto issue_x = [&](int n, int ch, uint32_t unit) {
+    // issue unit `unit` (slot p = chunks [p*CPS, (p+1)*CPS) of row n) of this
+    // quadrant (slice-0 warps only): one bulk copy per row covers CPS chunks
+    // (the SM accepts a bulk copy only every ~26 cycles, tools/micro/bulk_issue.cu)
+    auto issue_x = [&](int n, int p, uint32_t unit) {
       const int sl = static_cast<int>(unit % XS);
       const uint32_t use = unit / XS;
       if (use >= 1) mbar_wait(&s_xempty[sl][quad], (use - 1) & 1u);
-      const int d0 = ch * kKC;
-      const uint32_t bytes = static_cast<uint32_t>(min(kKC, dm.D - d0)) * 4u;
+      const int d0 = p * CPS * kKC;
+      const uint32_t bytes = static_cast<uint32_t>(min(CPS * kKC, dm.D - d0)) * 4u;
       const bool valid = n >= 0 && d0 < dm.D && !(PROF && (a.dbg & 1));
       const unsigned vm = __ballot_sync(0xffffffffu, valid);
       if (lane == 0) mbar_arrive_expect_tx(&s_xfull[sl][quad], static_cast<uint32_t>(__popc(vm)) * bytes);
       __syncwarp();
       if (valid)
-        bulk_copy(xbase + sl * kXSlotBytes + ar * (kXRow * 4), a.X + (int64_t)n * dm.D + d0, bytes,
-                  &s_xfull[sl][quad]);
+        bulk_copy(xbase + sl * SLOT + ar * (XR * 4), a.X + (int64_t)n * dm.D + d0, bytes, &s_xfull[sl][quad]);
     };
-    uint32_t sc = 0;  // flat chunk counter
+    uint32_t sc = 0;  // flat chunk counter (A stages)
+    uint32_t su = 0;  // flat X-ring slot counter
+    int xs = 0;
     if (w.valid(total) && ah == 0)
       for (int k = 0; k < ahead; ++k) issue_x(n_cur, k, static_cast<uint32_t>(k));
     int jb = 0;
@@ -396,18 +407,21 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_ws(WsArgs a) {
       mbar_wait(&s_mufull[mslot], (jb >> 1) & 1);
       const float* mu_s = s_mu[mslot] + s_muoff[mslot];
       for (int ch = 0; ch < nchunk; ++ch, ++sc) {
-        if (ah == 0) {  // prefetch chunk sc + ahead (this job or the next)
-          const int c2 = ch + ahead;
-          if (c2 < nchunk) issue_x(n_cur, c2, sc + ahead);
-          else issue_x(wn.valid(total) ? n_nxt : -1, c2 - nchunk, sc + ahead);
+        const int within = ch % CPS;
+        if (within == 0) {
+          if (ah == 0) {  // prefetch slot su + ahead (this job or the next)
+            const int p2 = ch / CPS + ahead;
+            if (p2 < nslot) issue_x(n_cur, p2, su + ahead);
+            else issue_x(wn.valid(total) ? n_nxt : -1, p2 - nslot, su + ahead);
+          }
+          xs = static_cast<int>(su % XS);
+          mbar_wait(&s_xfull[xs][quad], (su / XS) & 1u);
         }
-        const int xs = static_cast<int>(sc % XS);
-        mbar_wait(&s_xfull[xs][quad], (sc / XS) & 1u);
         if (PROF) pf.lap(kPBuild);  // (waiting for the row pieces)
         const int s = static_cast<int>(sc & 1u);
         const uint32_t use = sc >> 1;
         const int d0 = ch * kKC + kElem * ah;
-        const uint32_t xrow = xbase + xs * kXSlotBytes + ar * (kXRow * 4) + kElem * ah * 4;
+        const uint32_t xrow = xbase + xs * SLOT + ar * (XR * 4) + (within * kKC + kElem * ah) * 4;
         uint32_t vh[kElem / 2], vl[kElem / 2], qh[kElem / 2], ql[kElem / 2];
 #pragma unroll
         for (int jj = 0; jj < kXSeg; ++jj) {
@@ -430,8 +444,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_ws(WsArgs a) {
           split2(q[0], q[1], qh[2 * jj], ql[2 * jj]);
           split2(q[2], q[3], qh[2 * jj + 1], ql[2 * jj + 1]);
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&s_xempty[xs][quad]);  // this warp is done with the row slot
+        if (within == CPS - 1 || ch == nchunk - 1) {  // this warp is done with the row slot
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&s_xempty[xs][quad]);
+          ++su;
+        }
         if (PROF) pf.lap(kPSplit);
         if (use >= 1) mbar_wait(&s_aempty[s], (use - 1) & 1u);
         if (PROF) pf.lap(kPWaitEmpty);
@@ -461,8 +478,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_ws(WsArgs a) {
       if (PROF) pf.lap(kPSync);
     }
     // drain: the slots issued beyond the last chunk (nothing is read from them)
-    if (ah == 0 && sc > 0)
-      for (uint32_t u = sc; u < sc + static_cast<uint32_t>(ahead); ++u)
+    if (ah == 0 && su > 0)
+      for (uint32_t u = su; u < su + static_cast<uint32_t>(ahead); ++u)
         mbar_wait(&s_xfull[u % XS][quad], (u / XS) & 1u);
     if (PROF && a.prof && lane == 0) {
       atomicAdd(a.prof + kPSync, pf.acc[kPSync]);
@@ -879,14 +896,15 @@ int ws_groups(const Dims& dm) {
   return (dm.G + qg - 1) / qg;
 }
 
-bool ws_smem_plan(int Hp, uint32_t stage_bytes, int* xslots, int* nb, size_t* dyn);
+bool ws_smem_plan(int Hp, uint32_t stage_bytes, int* xslots, int* nb, size_t* dyn, int* cps);
 
 bool score_ws_supported(const Dims& dm) {
   if (dm.D > kMaxD || dm.D % 4 != 0 || dm.H > 64 || dm.G > 64) return false;
-  int xs, nb;
+  int xs, nb, cps;
   size_t dyn;
   for (int single = 0; single < 2; ++single)
-    if (!ws_smem_plan(ws_hp(dm.H), static_cast<uint32_t>(2 * 128 * (ws_n1max(dm, single) + kNL)), &xs, &nb, &dyn))
+    if (!ws_smem_plan(ws_hp(dm.H), static_cast<uint32_t>(2 * 128 * (ws_n1max(dm, single) + kNL)), &xs, &nb, &dyn,
+                      &cps))
       return false;
   return true;
 }
@@ -990,19 +1008,26 @@ constexpr int kProfWords = 16 + 8 * kTraceEvents;
 
 // Shared-memory plan: X ring slots and B ring stages within the opt-in limit
 // (227 KB minus the kernel's static shared memory). false: does not fit.
-bool ws_smem_plan(int Hp, uint32_t stage_bytes, int* xslots, int* nb, size_t* dyn) {
+// Slots of two K chunks (half the bulk copies) when they fit, else one.
+bool ws_smem_plan(int Hp, uint32_t stage_bytes, int* xslots, int* nb, size_t* dyn, int* cps_out) {
   const size_t limit = 227 * 1024;
   const size_t stat = 2 * (kMaxD + 8) * 4 + 4 * qg_max(Hp) * rec_stride(Hp) * 4 + 1024;  // s_mu, s_rec, barriers
   const size_t avail = limit - stat - 1024;  // 1024: stage alignment slack
-  for (int xs = kMaxXSlots; xs >= 2; --xs) {
-    const size_t xb = static_cast<size_t>(xs) * kXSlotBytes;
-    if (xb + 2 * stage_bytes > avail) continue;
-    *xslots = xs;
-    *nb = std::min(kMaxNB, static_cast<int>((avail - xb) / stage_bytes));
-    if (*nb > 4 && xs < kMaxXSlots) *nb = 4;
-    *dyn = static_cast<size_t>(*nb) * stage_bytes + xb + 1024;
-    return true;
-  }
+  static const int want_cps = [] {
+    const char* v = std::getenv("VMFA_WS_CPS");
+    return v ? std::max(1, std::min(kMaxCps, std::atoi(v))) : kMaxCps;
+  }();
+  for (int cps = want_cps; cps >= 1; --cps)
+    for (int xs = kMaxXSlots; xs >= 2; --xs) {
+      const size_t xb = static_cast<size_t>(xs) * x_slot_bytes(cps);
+      if (xb + 2 * stage_bytes > avail) continue;
+      *xslots = xs;
+      *cps_out = cps;
+      *nb = std::min(kMaxNB, static_cast<int>((avail - xb) / stage_bytes));
+      if (*nb > 4 && xs < kMaxXSlots) *nb = 4;
+      *dyn = static_cast<size_t>(*nb) * stage_bytes + xb + 1024;
+      return true;
+    }
   return false;
 }
 
@@ -1023,7 +1048,7 @@ cudaError_t launch_score_ws(int mode, const ScoreArgs& s, const WsOperands& op, 
   a.stage_bytes = static_cast<uint32_t>(2 * 128 * (a.N1max + kNL));
   // shared memory: the producers' X ring + the B ring (>= 2 stages each)
   size_t dyn = 0;
-  if (!ws_smem_plan(a.Hp, a.stage_bytes, &a.xslots, &a.nbstage, &dyn)) return cudaErrorInvalidValue;
+  if (!ws_smem_plan(a.Hp, a.stage_bytes, &a.xslots, &a.nbstage, &dyn, &a.cps)) return cudaErrorInvalidValue;
   a.X = s.X;
   a.xmax = op.xmax;
   a.mumax = op.mumax;
