@@ -35,6 +35,7 @@
 #include <cstdint>
 #include <cstdlib>
 
+#include <cuda.h>  // CUtensorMap (the encoder is fetched through cudaGetDriverEntryPoint)
 #include <cuda_fp16.h>
 
 #include "vmfa_b200.h"
@@ -58,7 +59,9 @@ constexpr int kMaxXSlots = 4;         // X ring slots (row chunks); prefetch dep
 constexpr int kXSeg = kElem / 4;      // 16-byte pieces per thread per chunk
 constexpr int kMaxCps = 2;             // K chunks per X-ring slot, at most
 // floats per row of a slot holding `cps` chunks (padded: conflict-free LDS.128)
-__host__ __device__ constexpr int x_row(int cps) { return cps * kKC + 4; }
+// (cps * 64 + 8 floats: a 4-row gather4 group is 4 * 544 bytes, a multiple of
+// 128; the 32-byte row skew leaves 2-way conflicts on the producers' LDS.128)
+__host__ __device__ constexpr int x_row(int cps) { return cps * kKC + 8; }
 __host__ __device__ constexpr uint32_t x_slot_bytes(int cps) { return kRows * x_row(cps) * 4; }
 constexpr int kMaxD = 1024;
 constexpr int kNL = 16;               // lin rows / psi rows per group (qg <= 16)
@@ -77,6 +80,7 @@ struct WsArgs {
   int nbstage;       // B ring depth
   int xslots;        // X ring slots (2..kMaxXSlots)
   int cps;           // K chunks per X-ring slot (one bulk copy per row and slot)
+  int gather;        // 1: rows arrive by tile::gather4 (4 rows per TMA operation)
   int nacc;          // accumulator buffers in TMEM (2 when they fit beside the A stages)
   uint32_t tmem_cols;
   uint32_t TB;       // TMEM columns per accumulator buffer
@@ -220,6 +224,16 @@ __device__ __forceinline__ void bulk_copy(uint32_t dst, const void* src, uint32_
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+// four rows (r0..r3) x box-width columns from col of a 2-D tensor map into
+// consecutive smem rows (sm_100a tile::gather4)
+__device__ __forceinline__ void gather4(uint32_t dst, const CUtensorMap* map, int col, int r0, int r1, int r2, int r3,
+                                        uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3)
+      : "memory");
+}
 __device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
@@ -300,7 +314,7 @@ __device__ __forceinline__ int row_exp(const WsArgs& a, int n, int c) {
 }
 
 template <int HP, bool PROF>
-__global__ void __launch_bounds__(kThreads, 1) k_score_ws(WsArgs a) {
+__global__ void __launch_bounds__(kThreads, 1) k_score_ws(WsArgs a, const __grid_constant__ CUtensorMap xmap) {
   extern __shared__ __align__(1024) unsigned char smem_dyn[];
   __shared__ uint64_t s_afull[2], s_aempty[2], s_tfull[2], s_tempty[2];
   __shared__ uint64_t s_bfull[kMaxNB], s_bempty[kMaxNB];
@@ -387,13 +401,33 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_ws(WsArgs a) {
       const uint32_t use = unit / XS;
       if (use >= 1) mbar_wait(&s_xempty[sl][quad], (use - 1) & 1u);
       const int d0 = p * CPS * kKC;
-      const uint32_t bytes = static_cast<uint32_t>(min(CPS * kKC, dm.D - d0)) * 4u;
       const bool valid = n >= 0 && d0 < dm.D && !(PROF && (a.dbg & 1));
       const unsigned vm = __ballot_sync(0xffffffffu, valid);
-      if (lane == 0) mbar_arrive_expect_tx(&s_xfull[sl][quad], static_cast<uint32_t>(__popc(vm)) * bytes);
-      __syncwarp();
-      if (valid)
-        bulk_copy(xbase + sl * SLOT + ar * (XR * 4), a.X + (int64_t)n * dm.D + d0, bytes, &s_xfull[sl][quad]);
+      if (a.gather) {
+        // lane g < 8 moves the quadrant's rows 4g..4g+3 with one gather4 (the
+        // full box width; padding rows repeat a valid row of the group)
+        int rr[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) rr[k] = __shfl_sync(0xffffffffu, n, (4 * lane + k) & 31);
+        const unsigned gm = lane < 8 ? (vm >> (4 * lane)) & 0xfu : 0u;
+        const unsigned ops = __ballot_sync(0xffffffffu, gm != 0u);
+        if (lane == 0)
+          mbar_arrive_expect_tx(&s_xfull[sl][quad], static_cast<uint32_t>(__popc(ops)) * 4u * XR * 4u);
+        __syncwarp();
+        if (gm != 0u) {
+          const int any = rr[__ffs(gm) - 1];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) rr[k] = ((gm >> k) & 1u) ? rr[k] : any;
+          gather4(xbase + sl * SLOT + (32 * quad + 4 * lane) * (XR * 4), &xmap, d0, rr[0], rr[1], rr[2], rr[3],
+                  &s_xfull[sl][quad]);
+        }
+      } else {
+        const uint32_t bytes = static_cast<uint32_t>(min(CPS * kKC, dm.D - d0)) * 4u;
+        if (lane == 0) mbar_arrive_expect_tx(&s_xfull[sl][quad], static_cast<uint32_t>(__popc(vm)) * bytes);
+        __syncwarp();
+        if (valid)
+          bulk_copy(xbase + sl * SLOT + ar * (XR * 4), a.X + (int64_t)n * dm.D + d0, bytes, &s_xfull[sl][quad]);
+      }
     };
     uint32_t sc = 0;  // flat chunk counter (A stages)
     uint32_t su = 0;  // flat X-ring slot counter
@@ -1031,6 +1065,30 @@ bool ws_smem_plan(int Hp, uint32_t stage_bytes, int* xslots, int* nb, size_t* dy
   return false;
 }
 
+// 2-D tensor map of X (D fp32 columns x N rows) with a box of one slot row
+// (x_row(cps) columns x 1 row) for tile::gather4
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+bool x_tensor_map(CUtensorMap* map, const float* X, int64_t N, int D, int box_cols) {
+  static EncodeTiledFn encode = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return static_cast<EncodeTiledFn>(nullptr);
+    return reinterpret_cast<EncodeTiledFn>(fn);
+  }();
+  if (!encode || N < 1) return false;
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(D), static_cast<cuuint64_t>(N)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(D) * 4};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(box_cols), 1};
+  const cuuint32_t estr[2] = {1, 1};
+  return encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(X), dims, strides, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 cudaError_t launch_score_ws(int mode, const ScoreArgs& s, const WsOperands& op, int4* jobs, cudaStream_t st,
                             bool build_jobs) {
   WsArgs a{};
@@ -1049,6 +1107,12 @@ cudaError_t launch_score_ws(int mode, const ScoreArgs& s, const WsOperands& op, 
   // shared memory: the producers' X ring + the B ring (>= 2 stages each)
   size_t dyn = 0;
   if (!ws_smem_plan(a.Hp, a.stage_bytes, &a.xslots, &a.nbstage, &dyn, &a.cps)) return cudaErrorInvalidValue;
+  static const int want_gather = [] {
+    const char* v = std::getenv("VMFA_WS_GATHER4");
+    return v ? std::atoi(v) : 1;
+  }();
+  CUtensorMap xmap{};
+  a.gather = want_gather && x_tensor_map(&xmap, s.X, s.dm.N, s.dm.D, x_row(a.cps)) ? 1 : 0;
   a.X = s.X;
   a.xmax = op.xmax;
   a.mumax = op.mumax;
@@ -1067,7 +1131,7 @@ cudaError_t launch_score_ws(int mode, const ScoreArgs& s, const WsOperands& op, 
   if (build_jobs) k_build_jobs<<<(s.dm.C + 255) / 256, 256, 0, st>>>(s.dm.C, mode, s.off, s.itemoff, s.gcnt, jobs);
   auto go = [&](auto kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn));
-    kern<<<sm_count(), kThreads, dyn, st>>>(a);
+    kern<<<sm_count(), kThreads, dyn, st>>>(a, xmap);
   };
   const bool prof = g_ws_prof != nullptr;
   switch (a.Hp) {
