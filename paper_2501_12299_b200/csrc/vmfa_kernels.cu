@@ -1699,18 +1699,9 @@ __global__ void __launch_bounds__(128) k_precompute(PrecompArgs a) {
       a.logpi[c] = lp;
       a.kconst[c] = lp - 0.5 * (D * kLog2Pi + logdet);
     }
-    // fp32 scoring rows
+    // fp32 scoring rows: W = U R^-T (P, WT) and V = R^-T W (V32) per dimension
     const int HP = a.L.HP, Hc = a.L.Hc;
-    for (int d = tid; d < D; d += blockDim.x) {
-      double u[kMaxH1];
-      const double ip = 1.0 / psi[d];
-      for (int h = 0; h < H; ++h) u[h] = lam[(int64_t)h * D + d] * ip;  // U = Psi^-1 Lambda
-      // forward: w = R^-1 u
-      for (int i = 0; i < H; ++i) {
-        double t = u[i];
-        for (int k = 0; k < i; ++k) t -= sR[i * H + k] * u[k];
-        u[i] = t / sR[i * H + i];
-      }
+    auto write_rows = [&](int d, const double* u, double ip) {
       float* row = a.P + ((int64_t)c * D + d) * HP;
       for (int h = 0; h < Hc; ++h) row[h] = h < H ? static_cast<float>(u[h]) : 0.f;
       // K-major copy for the tensor-core scorer: WT[c][h][d], h < Hp (zero padded)
@@ -1720,14 +1711,56 @@ __global__ void __launch_bounds__(128) k_precompute(PrecompArgs a) {
       row[Hc + 1] = static_cast<float>(ip);
       row[Hc + 2] = 0.f;
       row[Hc + 3] = 0.f;
-      // backward: v = R^-T w  => V column d
-      for (int i = H - 1; i >= 0; --i) {
-        double t = u[i];
-        for (int k = i + 1; k < H; ++k) t -= sR[k * H + i] * u[k];
-        u[i] = t / sR[i * H + i];
-      }
-      for (int h = 0; h < H; ++h) a.V32[((int64_t)c * D + d) * H + h] = static_cast<float>(u[h]);
       a.mu32[(int64_t)c * D + d] = static_cast<float>(a.mu[(int64_t)c * D + d]);
+    };
+    if (H <= kPreFastH) {  // compile-time loops: the solves stay in registers
+      for (int d = tid; d < D; d += blockDim.x) {
+        double u[kPreFastH];
+        const double ip = 1.0 / psi[d];
+#pragma unroll
+        for (int h = 0; h < kPreFastH; ++h) u[h] = h < H ? lam[(int64_t)h * D + d] * ip : 0.0;  // U = Psi^-1 Lambda
+#pragma unroll
+        for (int i = 0; i < kPreFastH; ++i) {  // forward: w = R^-1 u
+          if (i < H) {
+            double t = u[i];
+#pragma unroll
+            for (int k = 0; k < i; ++k) t -= sR[i * H + k] * u[k];
+            u[i] = t / sR[i * H + i];
+          }
+        }
+        write_rows(d, u, ip);
+#pragma unroll
+        for (int i = kPreFastH - 1; i >= 0; --i) {  // backward: v = R^-T w => V column d
+          if (i < H) {
+            double t = u[i];
+#pragma unroll
+            for (int k = i + 1; k < kPreFastH; ++k)
+              if (k < H) t -= sR[k * H + i] * u[k];
+            u[i] = t / sR[i * H + i];
+          }
+        }
+#pragma unroll
+        for (int h = 0; h < kPreFastH; ++h)
+          if (h < H) a.V32[((int64_t)c * D + d) * H + h] = static_cast<float>(u[h]);
+      }
+    } else {
+      for (int d = tid; d < D; d += blockDim.x) {
+        double u[kMaxH1];
+        const double ip = 1.0 / psi[d];
+        for (int h = 0; h < H; ++h) u[h] = lam[(int64_t)h * D + d] * ip;  // U = Psi^-1 Lambda
+        for (int i = 0; i < H; ++i) {  // forward: w = R^-1 u
+          double t = u[i];
+          for (int k = 0; k < i; ++k) t -= sR[i * H + k] * u[k];
+          u[i] = t / sR[i * H + i];
+        }
+        write_rows(d, u, ip);
+        for (int i = H - 1; i >= 0; --i) {  // backward: v = R^-T w => V column d
+          double t = u[i];
+          for (int k = i + 1; k < H; ++k) t -= sR[k * H + i] * u[k];
+          u[i] = t / sR[i * H + i];
+        }
+        for (int h = 0; h < H; ++h) a.V32[((int64_t)c * D + d) * H + h] = static_cast<float>(u[h]);
+      }
     }
     __syncthreads();
   }
