@@ -436,6 +436,7 @@ int estep_local(vmfa_ctx* x, uint64_t seed, uint64_t it, int mode, bool exchange
     a.itemoff = x->part_items;
     a.pts_per_item = x->gupd_pts;
     a.exchange = exchange ? 1 : 0;
+    a.force_rows = (x->xc && dm.C - 1 > kGupdCap / 2) ? 1 : 0;
     a.xc = x->xc;
     a.dump = x->dump ? 1 : 0;
     if (x->dump) {
@@ -450,7 +451,8 @@ int estep_local(vmfa_ctx* x, uint64_t seed, uint64_t it, int mode, bool exchange
     }
     const int tok = x->begin(kFamGupdate, dm.N);
     CU(launch_gupdate(a, x->gupd_grid, s));
-    if (!exchange && x->xc) CU(launch_gselect_dense(dm, x->xc, x->part_items, 0, x->g_new, x->gcnt_new, s));
+    if (!exchange && x->xc)
+      CU(launch_gselect_dense(dm, x->xc, x->part_items, a.force_rows, x->g_new, x->gcnt_new, s));
     x->end(tok);
   }
   // scalars: F_estep = sum lse, joints = sum ret_cnt
@@ -769,8 +771,9 @@ int vmfa_ctx_create(vmfa_ctx** out, int device, int C, int D, int H, int Cp, int
     const int64_t max_items = C + (pairs + x->stats_rows - 1) / x->stats_rows;
     A(x->stats_part, static_cast<size_t>(max_items) * stats_part_stride(dm));
     const int64_t bal = std::max<int64_t>(128, static_cast<int64_t>(N) / (4 * sm_count()));
-    const int64_t capb = (C - 1 <= kGupdCap / 2) ? (int64_t{1} << 30)
-                                                 : std::max<int64_t>(1, (kGupdCap / 2) / std::max(1, dm.stride - 1));
+    // large C (with the dense rows): every item adds into the rows through a
+    // small hash (k_gupdate force_rows); items of up to 512 points
+    const int64_t capb = (C - 1 <= kGupdCap / 2) ? (int64_t{1} << 30) : 512;
     x->gupd_pts = static_cast<int>(std::min(bal, capb));
   }
   // dense C x C rows (count, fixed-point hi, lo) for split components and the

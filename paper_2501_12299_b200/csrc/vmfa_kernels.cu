@@ -490,11 +490,17 @@ __global__ void __launch_bounds__(kGupdThreads) k_gupdate(GupdArgs a, int capmax
     const int p0 = a.part_off[c] + (item - a.itemoff[c]) * a.pts_per_item;
     const int p1 = min(a.part_off[c + 1], p0 + a.pts_per_item);
     const int npts = max(0, p1 - p0);
-    const bool to_rows = a.exchange || nitems > 1;
+    const bool to_rows = a.exchange || nitems > 1 || a.force_rows;
     const long long bound = llmin((long long)dm.C - 1, (long long)npts * (dm.stride - 1));
     int cap = 32;
-    while (cap < 2 * bound && cap < 2 * capmax) cap <<= 1;
-    const bool use_smem = cap <= capmax;
+    bool use_smem;
+    if (to_rows && a.xc) {  // small table sized for the typical key count; overflow adds into row c of xc
+      while (cap < 2 * bound && cap < min(capmax, kGupdRowsCap)) cap <<= 1;
+      use_smem = true;
+    } else {
+      while (cap < 2 * bound && cap < 2 * capmax) cap <<= 1;
+      use_smem = cap <= capmax;
+    }
     if (npts > 0) {
       if (use_smem) {
         for (int i = tid; i < cap; i += kGupdThreads) {
@@ -554,14 +560,27 @@ __global__ void __launch_bounds__(kGupdThreads) k_gupdate(GupdArgs a, int capmax
           to_fixed(v, hi, lo);
           if (use_smem) {
             unsigned h = hash_key(ct) & (cap - 1);
+            int probes = 0;
+            bool full = false;
             while (true) {
               const int prev = atomicCAS(t_key + h, -1, ct);
               if (prev == -1 || prev == ct) break;
               h = (h + 1) & (cap - 1);
+              if (++probes >= cap) {
+                full = true;
+                break;
+              }
             }
-            atomicAdd(t_cnt + h, 1);
-            atomicAdd(reinterpret_cast<unsigned long long*>(t_hi + h), static_cast<unsigned long long>(hi));
-            atomicAdd(reinterpret_cast<unsigned long long*>(t_lo + h), static_cast<unsigned long long>(lo));
+            if (full) {  // (to_rows items only: exact integer adds straight into row c)
+              const int64_t at = (int64_t)c * dm.C + ct;
+              atomicAdd(reinterpret_cast<unsigned long long*>(a.xc + at), 1ULL);
+              atomicAdd(reinterpret_cast<unsigned long long*>(a.xc + CC + at), static_cast<unsigned long long>(hi));
+              atomicAdd(reinterpret_cast<unsigned long long*>(a.xc + 2 * CC + at), static_cast<unsigned long long>(lo));
+            } else {
+              atomicAdd(t_cnt + h, 1);
+              atomicAdd(reinterpret_cast<unsigned long long*>(t_hi + h), static_cast<unsigned long long>(hi));
+              atomicAdd(reinterpret_cast<unsigned long long*>(t_lo + h), static_cast<unsigned long long>(lo));
+            }
           } else {
             atomicAdd(reinterpret_cast<unsigned long long*>(g_cnt + ct), 1ULL);
             atomicAdd(reinterpret_cast<unsigned long long*>(g_hi + ct), static_cast<unsigned long long>(hi));
@@ -2007,7 +2026,8 @@ int gupd_capmax(const Dims& dm, int pts_per_item) {
   return cap;
 }
 cudaError_t launch_gupdate(const GupdArgs& a, int grid, cudaStream_t s) {
-  const int capmax = gupd_capmax(a.dm, a.pts_per_item);
+  int capmax = gupd_capmax(a.dm, a.pts_per_item);
+  if (a.force_rows) capmax = std::min(capmax, kGupdRowsCap);
   const size_t smem = static_cast<size_t>(capmax) * (2 * sizeof(long long) + 2 * sizeof(int));
   cudaFuncSetAttribute(k_gupdate, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   k_gupdate<<<grid, kGupdThreads, smem, s>>>(a, capmax);

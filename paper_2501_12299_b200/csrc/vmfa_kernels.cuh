@@ -23,6 +23,7 @@ constexpr int kXsStride = kScoreRows + 2;  // transposed x tile stride (floats)
 constexpr int kStatsThreads = 256;
 constexpr int kGupdCap = 8192;      // smem hash capacity of the block-3 accumulator (24 B per entry)
 constexpr int kGupdThreads = 256;
+constexpr int kGupdRowsCap = 2048;  // hash of an item that adds into the dense rows (overflow goes to xc)
 
 // Packed fp32 scoring parameters of one component (precompute output):
 // per dimension d a row of HP floats: [W_0 .. W_{Hc-1}, mu_d, 1/psi_d, 0, 0]
@@ -105,6 +106,7 @@ struct GupdArgs {
   const int* itemoff;     // items over the partition: chunks of pts_per_item points
   int pts_per_item;
   int exchange;           // 1: write dense C x C rows to xc_* instead of selecting
+  int force_rows;         // 1: every item adds into the dense rows (large C); small hash, overflow -> xc
   long long* xc;          // 3*C*C int64: [cnt | hi | lo]
   int dump;               // 1: append (c, ct, cnt, hi, lo) rows to dump arrays
   int* dump_c;

@@ -105,6 +105,28 @@ def test_estep_config3_shape(oracle, gpu, scorer, monkeypatch):
     sess.close()
 
 
+def test_estep_large_C_dense_rows(oracle, gpu):
+    # C - 1 > kGupdCap / 2: every block-3 item adds its exact partial table into
+    # the dense rows through a small hash (overflowing keys go straight to the
+    # rows), selection from the rows for all components
+    O, V = oracle, gpu
+    X, _ = gaussian_problem(24000, 8, 3000, 2, seed=17)
+    C, H, Cp, G = 4500, 2, 3, 5
+    p, st, floor, sess = _setup(O, V, X, C, H, Cp, G)
+    for it in range(2):
+        e_or, st_or, F, J, ret, st_g, k = _estep_both(O, V, sess, X, p, st, 5, it)
+        compare_estep(O, e_or, st_or, F, J, ret, st_g, Cp)
+        same_part = np.ones(C, bool)
+        diff_rows = np.any(st_g.K != st_or.K, axis=1) | (st_g.labels != st_or.labels)
+        for n in np.nonzero(diff_rows)[0]:
+            same_part[st_or.labels[n]] = False
+            same_part[st_g.labels[n]] = False
+        bad = compare_g(st_g.g, st_g.g_count, st_or.g, st_or.g_count, e_or.dist, same_part)
+        assert not bad, f"g differs outside near-ties for components {bad[:10]}"
+        st = st_or
+    sess.close()
+
+
 def test_estep_euclid_and_frozen(oracle, gpu):
     O, V = oracle, gpu
     X, _ = gaussian_problem(3000, 48, 30, 3, seed=3)
