@@ -14,6 +14,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>
+#include <cstring>
 
 #include "vmfa_kernels.cuh"
 #include "vmfa_rng.hpp"
@@ -806,7 +807,7 @@ __device__ int g_stats_prof_on;
 // deterministic; no atomics.
 constexpr int kStatsBatch = 32;
 constexpr int kStatsMaxRows = 1024;  // K-pairs per statistics item (upper bound)
-constexpr int kStatsMaxBuf = 4;      // row-batch ring depth (bulk-copy path)
+constexpr int kStatsMaxBuf = 6;      // row-batch ring depth (bulk-copy path)
 constexpr int kStatsMaxH1 = 17;   // columns of Y per pass
 
 // Items are (component, chunk of <= rows_per_item K-pairs): large components
@@ -1267,6 +1268,295 @@ __global__ void __launch_bounds__(kStatsThreads) k_stats_E(StatsArgs a, const in
       for (int k = 0; k < 9; ++k) {
         const int idx = idx0 + tid + k * kStatsThreads;
         if (idx < H1 * H1) pe[idx] = accE[k];
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------- K5 on the tensor cores (H + 1 <= 16)
+// The same statistics as k_stats (accumulate_point, mstep.cpp:47-67, centred
+// on the fp32 mean as there), with both contractions as warp-level
+// mma.sync.m16n8k8 tf32 in 3xTF32 split precision (x = hi + lo, products
+// hi*hi + hi*lo + lo*hi, fp32 accumulation: ~21 significant bits, the fp32
+// FFMA form's accuracy at a quarter of its instructions; tools/micro/
+// mma_sync_tput.cu measures 0.465 mma/clk/SM = 476 FMA/clk against FFMA's 125):
+//   (i)  Z = Vc V^T: M = 16 rows of the batch, N = 8 latent columns, K = D
+//        (split in quarters over the warps, partials summed in smem);
+//   (ii) Y_v^T += (Q Zhat)^T Vc: M = 16 columns of [zhat; 1] (padded),
+//        N = 8 dimensions, K = 8 rows; each warp owns D/64 dimension tiles for
+//        the whole item, so its accumulators are the item's Y_v columns (no
+//        cross-warp reduction); sq_v = sum q v^2 rides on the phase (ii) loads.
+// E stays fp64 on the CUDA cores (one thread per upper-triangle entry and row
+// group), as in k_stats. Items, work queue, qmax scaling, the direct/partial
+// split and the partial layout (nh1 = 5/9/17) are k_stats's, so
+// k_stats_reduce / k_stats_uncenter / k_stats_sz are shared.
+constexpr int kSmBatch = 32;  // rows per batch (2 m-tiles of phase i, 4 k-steps of phase ii)
+constexpr int kSmZD = 17;     // s_zd row stride (fp64)
+
+__device__ __forceinline__ float tf32_hi(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+__device__ __forceinline__ void mma_tf32(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+// acc += a * b in 3xTF32 (small terms first). The three products of one
+// k-step go into a fresh accumulator and are added to acc with round-to-
+// nearest FADDs: the tensor core's internal accumulation truncates, and
+// chaining hundreds of k-steps through it biases long sums (measured ~30x the
+// FFMA error on the statistics; tools/diag_stats_err.py)
+__device__ __forceinline__ void mma3(float (&acc)[4], const float (&ah)[4], const float (&al)[4], float b0h,
+                                     float b1h, float b0l, float b1l) {
+  const uint32_t h[4] = {__float_as_uint(ah[0]), __float_as_uint(ah[1]), __float_as_uint(ah[2]),
+                         __float_as_uint(ah[3])};
+  const uint32_t l[4] = {__float_as_uint(al[0]), __float_as_uint(al[1]), __float_as_uint(al[2]),
+                         __float_as_uint(al[3])};
+  float c[4] = {0.f, 0.f, 0.f, 0.f};
+  mma_tf32(c, l, __float_as_uint(b0h), __float_as_uint(b1h));
+  mma_tf32(c, h, __float_as_uint(b0l), __float_as_uint(b1l));
+  mma_tf32(c, h, __float_as_uint(b0h), __float_as_uint(b1h));
+#pragma unroll
+  for (int k = 0; k < 4; ++k) acc[k] += c[k];
+}
+
+template <int NTH, int NTW>
+__global__ void __launch_bounds__(kStatsThreads, 2) k_stats_mma(StatsArgs a, const int* __restrict__ itemoff,
+                                                               int rows_per_item, int nh1, double* part,
+                                                               int64_t part_stride, int nbuf) {
+  // smem (dynamic): s_x [nbuf][B][XS] | s_Vb [KS][NTH][32] float4 | s_mu [D]
+  extern __shared__ __align__(16) float s_x[];
+  __shared__ __align__(16) float s_pz[4][kSmBatch][16];  // phase (i) K-quarter partials
+  __shared__ __align__(16) float4 s_Af[4][32][2];         // phase (ii) A fragments (hi, lo) per k-step, lane
+  __shared__ double s_zd[kSmBatch * kSmZD];               // [zhat; 1] rows in fp64 (E)
+  __shared__ double s_red[kStatsThreads / 32];
+  __shared__ double s_accE[kStatsThreads];
+  __shared__ uint64_t s_xbar[kStatsMaxBuf];
+  __shared__ int s_eall[kStatsMaxRows];
+  __shared__ double s_qall[kStatsMaxRows];
+  __shared__ int s_item;
+  const Dims dm = a.dm;
+  const int H = dm.H, H1 = H + 1, D = dm.D;
+  const int XS = D + 4;  // row stride: XS % 32 == 4 for D % 32 == 0 (conflict-free phase i)
+  const int KS = D / 8;  // k-steps of phase (i) / dimension tiles of phase (ii)
+  float4* s_Vb = reinterpret_cast<float4*>(s_x + (int64_t)nbuf * kSmBatch * XS);
+  float* s_mu = reinterpret_cast<float*>(s_Vb + (int64_t)KS * NTH * 32);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int gid = lane >> 2, tig = lane & 3;
+  // E: thread = (upper-triangle entry, row group)
+  const int NE = H1 * (H1 + 1) / 2;
+  const int EG = max(1, kStatsThreads / NE);
+  const int eg = tid / NE;
+  int ei = -1, ej = -1;
+  if (eg < EG) {
+    int t = tid - eg * NE;
+    for (int i = 0; i < H1 && ei < 0; ++i) {
+      if (t < H1 - i) ei = i, ej = i + t;
+      else t -= H1 - i;
+    }
+  }
+  // phase (i): warp = (m-tile, K quarter)
+  const int pm = warp & 1, pq = warp >> 1;
+  const int ks0 = pq * KS / 4, ks1 = (pq + 1) * KS / 4;
+  const int total = __ldg(itemoff + dm.C);
+  if (tid == 0)
+    for (int i = 0; i < kStatsMaxBuf; ++i) xbar_init(&s_xbar[i], 1);
+  __syncthreads();
+  uint32_t xpar = 0u;
+  auto next_item = [&](int cur) -> int {
+    if (!a.qctr) return cur < 0 ? static_cast<int>(blockIdx.x) : cur + static_cast<int>(gridDim.x);
+    __syncthreads();
+    if (tid == 0) s_item = atomicAdd(a.qctr, 1);
+    __syncthreads();
+    return s_item;
+  };
+  for (int item = next_item(-1); item < total; item = next_item(item)) {
+    const int c = find_item(itemoff, dm.C, item);
+    const int r0 = a.off[c] + (item - itemoff[c]) * rows_per_item;
+    const int r1 = min(a.off[c + 1], r0 + rows_per_item);
+    const int nr = r1 - r0;
+    const bool direct = itemoff[c + 1] - itemoff[c] == 1;
+    double qmax = 0.0;
+    __syncthreads();
+    for (int i = tid; i < nr; i += kStatsThreads) {
+      const int e = a.ent[r0 + i];
+      const double q = a.resp[e];
+      s_eall[i] = e / dm.Cp;
+      s_qall[i] = q;
+      qmax = fmax(qmax, q);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) qmax = fmax(qmax, __shfl_xor_sync(kFull, qmax, o));
+    if (lane == 0) s_red[warp] = qmax;
+    // V^T fragments of phase (i), split: b0 = V[h][d = 8ks + tig], b1 = V[h][d + 4], h = 8nt + gid
+    const float* Vc = a.V32 + (int64_t)c * D * H;
+    for (int i = tid; i < KS * NTH * 32; i += kStatsThreads) {
+      const int l = i & 31, t = i >> 5;
+      const int ks = t / NTH, nt = t - ks * NTH;
+      const int h = 8 * nt + (l >> 2), d = 8 * ks + (l & 3);
+      const float b0 = h < H ? __ldg(Vc + (int64_t)d * H + h) : 0.f;
+      const float b1 = h < H ? __ldg(Vc + (int64_t)(d + 4) * H + h) : 0.f;
+      const float b0h = tf32_hi(b0), b1h = tf32_hi(b1);
+      s_Vb[i] = make_float4(b0h, b1h, b0 - b0h, b1 - b1h);
+    }
+    for (int d = tid; d < D; d += kStatsThreads) s_mu[d] = __ldg(a.mu32 + (int64_t)c * D + d);
+    __syncthreads();
+    qmax = 0.0;
+#pragma unroll
+    for (int w = 0; w < kStatsThreads / 32; ++w) qmax = fmax(qmax, s_red[w]);
+    const double qdiv = qmax > 0.0 ? qmax : 1.0;
+    for (int i = tid; i < nr; i += kStatsThreads) {
+      const double q = s_qall[i] / qdiv;
+      s_qall[i] = q;
+    }
+    if (ei >= 0) s_accE[tid] = 0.0;
+    float acc[NTW][4];
+    double sqd[NTW];  // sq_v: fp32 over a batch's 8 rows per lane, then fp64
+    float muj[NTW];
+#pragma unroll
+    for (int i = 0; i < NTW; ++i) {
+      sqd[i] = 0.0;
+      acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
+      const int j = warp + 8 * i;
+      muj[i] = j < KS ? s_mu[8 * j + gid] : 0.f;
+    }
+    const int nbat = (nr + kSmBatch - 1) / kSmBatch;
+    auto issue_rows = [&](int b, int buf) {
+      float* dst = s_x + (int64_t)buf * kSmBatch * XS;
+      const int nb = min(kSmBatch, nr - b * kSmBatch);
+      const int* eb = s_eall + b * kSmBatch;
+      if (tid == 0) xbar_expect(&s_xbar[buf], static_cast<uint32_t>(nb) * D * 4u);
+      if (lane < kSmBatch / (kStatsThreads / 32)) {
+        const int r = warp * (kSmBatch / (kStatsThreads / 32)) + lane;
+        if (r < nb) bulk_row(smem_addr(dst + (int64_t)r * XS), a.X + (int64_t)eb[r] * D, D * 4u, &s_xbar[buf]);
+      }
+    };
+    for (int b = 0; b < min(nbuf - 1, nbat); ++b) issue_rows(b, b);
+    for (int bi = 0; bi < nbat; ++bi) {
+      const int buf = bi % nbuf;
+      const int nb = min(kSmBatch, nr - bi * kSmBatch);
+      xbar_wait(&s_xbar[buf], (xpar >> buf) & 1u);
+      xpar ^= 1u << buf;
+      const float* xb = s_x + (int64_t)buf * kSmBatch * XS;
+      // (i) Z partial over this warp's K quarter: A = v rows 16pm.., B = V^T
+      {
+        float z[NTH][4];
+#pragma unroll
+        for (int nt = 0; nt < NTH; ++nt) z[nt][0] = z[nt][1] = z[nt][2] = z[nt][3] = 0.f;
+        const float* xr0 = xb + (int64_t)(16 * pm + gid) * XS + tig;
+        const float* xr1 = xr0 + 8 * XS;
+#pragma unroll 4
+        for (int ks = ks0; ks < ks1; ++ks) {
+          const int d = 8 * ks;
+          const float m0 = s_mu[d + tig], m1 = s_mu[d + tig + 4];
+          const float v[4] = {xr0[d] - m0, xr1[d] - m0, xr0[d + 4] - m1, xr1[d + 4] - m1};
+          float ah[4], al[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            ah[k] = tf32_hi(v[k]);
+            al[k] = v[k] - ah[k];
+          }
+#pragma unroll
+          for (int nt = 0; nt < NTH; ++nt) {
+            const float4 bv = s_Vb[((int64_t)ks * NTH + nt) * 32 + lane];
+            mma3(z[nt], ah, al, bv.x, bv.y, bv.z, bv.w);
+          }
+        }
+#pragma unroll
+        for (int nt = 0; nt < NTH; ++nt) {
+          *reinterpret_cast<float2*>(&s_pz[pq][16 * pm + gid][8 * nt + 2 * tig]) = make_float2(z[nt][0], z[nt][1]);
+          *reinterpret_cast<float2*>(&s_pz[pq][16 * pm + gid + 8][8 * nt + 2 * tig]) =
+              make_float2(z[nt][2], z[nt][3]);
+        }
+      }
+      __syncthreads();
+      if (nbuf >= 2 && bi + nbuf - 1 < nbat) issue_rows(bi + nbuf - 1, (bi + nbuf - 1) % nbuf);
+      // combine: zhat rows (fp64 for E) and the q-scaled phase (ii) A fragments
+      const double* s_q = s_qall + bi * kSmBatch;
+      for (int i = tid; i < kSmBatch * 16; i += kStatsThreads) {
+        const int r = i >> 4, h = i & 15;
+        float z = 0.f;
+        if (r < nb) {
+          if (h < H) z = s_pz[0][r][h] + s_pz[1][r][h] + s_pz[2][r][h] + s_pz[3][r][h];
+          else if (h == H) z = 1.f;
+        }
+        if (h < H1) s_zd[r * kSmZD + h] = z;
+        const float qz = r < nb ? static_cast<float>(s_q[r]) * z : 0.f;
+        const float hi = tf32_hi(qz);
+        const int ks = r >> 3, rr = r & 7;
+        const int ln = (h & 7) * 4 + (rr & 3), reg = (h >> 3) + 2 * (rr >> 2);
+        reinterpret_cast<float*>(&s_Af[ks][ln][0])[reg] = hi;
+        reinterpret_cast<float*>(&s_Af[ks][ln][1])[reg] = qz - hi;
+      }
+      __syncthreads();
+      if (ei >= 0) {
+        double e = s_accE[tid];
+        for (int r = eg; r < nb; r += EG) e = fma(s_q[r], s_zd[r * kSmZD + ei] * s_zd[r * kSmZD + ej], e);
+        s_accE[tid] = e;
+      }
+      // (ii) Y_v^T += (Q zhat)^T v over the batch's 4 k-steps
+      float sqa[NTW];
+#pragma unroll
+      for (int i = 0; i < NTW; ++i) sqa[i] = 0.f;
+#pragma unroll
+      for (int ks = 0; ks < kSmBatch / 8; ++ks) {
+        const float4 Ah = s_Af[ks][lane][0], Al = s_Af[ks][lane][1];
+        const float ah[4] = {Ah.x, Ah.y, Ah.z, Ah.w}, al[4] = {Al.x, Al.y, Al.z, Al.w};
+        const int ra = 8 * ks + tig, rb = ra + 4;
+        const bool oka = ra < nb, okb = rb < nb;
+        const float qa = oka ? static_cast<float>(s_q[ra]) : 0.f, qb = okb ? static_cast<float>(s_q[rb]) : 0.f;
+        const float* xa = xb + (int64_t)ra * XS + gid;
+        const float* xb2 = xb + (int64_t)rb * XS + gid;
+#pragma unroll
+        for (int i = 0; i < NTW; ++i) {
+          const int j = warp + 8 * i;
+          if (NTW > 1 && j >= KS) break;
+          const float va = oka ? xa[8 * j] - muj[i] : 0.f;
+          const float vb = okb ? xb2[8 * j] - muj[i] : 0.f;
+          sqa[i] = fmaf(qa * va, va, sqa[i]);
+          sqa[i] = fmaf(qb * vb, vb, sqa[i]);
+          const float vah = tf32_hi(va), vbh = tf32_hi(vb);
+          mma3(acc[i], ah, al, vah, vbh, va - vah, vb - vbh);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < NTW; ++i) sqd[i] += sqa[i];
+      if (nbuf == 1) __syncthreads();
+    }
+    // write: E (fp64, row groups summed in order), Y_v columns and sq_v, scaled by qmax
+    double* pp = direct ? nullptr : part + (int64_t)item * part_stride;
+    double* pe = direct ? a.E + (int64_t)c * H1 * H1 : pp + (int64_t)nh1 * D + D;
+    __syncthreads();
+    if (ei >= 0 && eg == 0) {
+      double e = 0.0;
+      for (int g = 0; g < EG; ++g) e += s_accE[tid + g * NE];
+      pe[ej * H1 + ei] = e * qmax;
+      pe[ei * H1 + ej] = e * qmax;
+    }
+#pragma unroll
+    for (int i = 0; i < NTW; ++i) {
+      const int j = warp + 8 * i;
+      double s = sqd[i];
+      s += __shfl_xor_sync(kFull, s, 1);
+      s += __shfl_xor_sync(kFull, s, 2);
+      if (j >= KS) continue;
+      const int d = 8 * j + 2 * tig;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int h = gid + 8 * (k >> 1), dd = d + (k & 1);
+        if (h >= H1) continue;
+        const double y = static_cast<double>(acc[i][k]) * qmax;
+        if (direct) a.Y[((int64_t)c * H1 + h) * D + dd] = y;
+        else pp[(int64_t)h * D + dd] = y;
+      }
+      if (tig == 0) {
+        const double v = s * qmax;
+        if (direct) a.sq[(int64_t)c * D + 8 * j + gid] = v;
+        else pp[(int64_t)nh1 * D + 8 * j + gid] = v;
       }
     }
   }
@@ -2078,6 +2368,14 @@ int64_t stats_part_stride(const Dims& dm) {
   const int nh1 = H1 <= 5 ? 5 : (H1 <= 9 ? 9 : kStatsMaxH1);
   return static_cast<int64_t>(nh1) * dm.D + dm.D + static_cast<int64_t>(H1) * H1 + 1;
 }
+// the tensor-core statistics kernel covers H + 1 <= 16 (one m16 tile of
+// [zhat; 1]) and D % 8 == 0, D <= 512 (<= 8 dimension tiles per warp);
+// VMFA_STATS=ffma selects k_stats (the cross-check in the parity tests)
+bool stats_mma_ok(const Dims& dm) {
+  const char* v = std::getenv("VMFA_STATS");
+  const bool ffma = v && std::strcmp(v, "ffma") == 0;
+  return !ffma && dm.H + 1 <= 16 && dm.D % 8 == 0 && dm.D <= 512;
+}
 cudaError_t launch_stats(const StatsArgs& a, const int* itemoff, int rows_per_item, double* part,
                          cudaStream_t s) {
   if (a.dm.D > 4 * kStatsThreads) return cudaErrorInvalidValue;
@@ -2085,6 +2383,49 @@ cudaError_t launch_stats(const StatsArgs& a, const int* itemoff, int rows_per_it
   const int H1 = a.dm.H + 1;
   const int nh1 = H1 <= 5 ? 5 : (H1 <= 9 ? 9 : kStatsMaxH1);
   const int64_t ps = stats_part_stride(a.dm);
+  if (stats_mma_ok(a.dm)) {
+    if (a.qctr) {
+      cudaError_t e = cudaMemsetAsync(a.qctr, 0, sizeof(int), s);
+      if (e != cudaSuccess) return e;
+    }
+    const int KS = a.dm.D / 8, NTH = a.dm.H > 8 ? 2 : 1;
+    const int ntw = (KS + 7) / 8;
+    const size_t per_buf = static_cast<size_t>(kSmBatch) * (a.dm.D + 4) * sizeof(float);
+    const size_t fixed = static_cast<size_t>(KS) * NTH * 32 * 16 + a.dm.D * sizeof(float);
+    // row-batch ring: 2 deep at 2 CTAs per SM (deeper rings at 1 CTA per SM
+    // measured slower: 0.93 vs 0.67 ms on config 2)
+    static const int want = [] {
+      const char* v = std::getenv("VMFA_STATS_NBUF");
+      return v ? std::atoi(v) : 0;
+    }();
+    const size_t budget = 200 * 1024 - 32 * 1024;  // minus the static smem
+    int nbuf = want > 0 ? std::min(want, kStatsMaxBuf) : 2;
+    while (nbuf > 2 && nbuf * per_buf + fixed > budget) --nbuf;
+    const int per_sm = nbuf <= 2 ? 2 : 1;  // 2 x (66.5 + 17 KB dynamic + 30 KB static) fits at D = 256
+    const size_t smem = nbuf * per_buf + fixed;
+    auto go = [&](auto kern) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+      kern<<<sm_count() * per_sm, kStatsThreads, smem, s>>>(a, itemoff, rows_per_item, nh1, part, ps, nbuf);
+    };
+    if (NTH == 1) {
+      if (ntw <= 1) go(k_stats_mma<1, 1>);
+      else if (ntw <= 2) go(k_stats_mma<1, 2>);
+      else if (ntw <= 4) go(k_stats_mma<1, 4>);
+      else go(k_stats_mma<1, 8>);
+    } else {
+      if (ntw <= 1) go(k_stats_mma<2, 1>);
+      else if (ntw <= 2) go(k_stats_mma<2, 2>);
+      else if (ntw <= 4) go(k_stats_mma<2, 4>);
+      else go(k_stats_mma<2, 8>);
+    }
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    k_stats_reduce<<<sm_count() * 8, 256, 0, s>>>(a.dm, itemoff, part, ps, 0, 0, nh1, 1, a.Nc, a.E, a.Y, a.sq);
+    k_stats_uncenter<<<grid_for((int64_t)a.dm.C * a.dm.D, 256, 8192), 256, 0, s>>>(a.dm, a.mu32, a.Nc, a.E, a.Y,
+                                                                                  a.sq);
+    k_stats_sz<<<grid_for((int64_t)a.dm.C * a.dm.H * a.dm.H, 256, 4096), 256, 0, s>>>(a.dm, a.Nc, a.Sz, a.E);
+    return cudaGetLastError();
+  }
   for (int col0 = 0; col0 < H1; col0 += nh1) {
     if (a.qctr) {
       cudaError_t e = cudaMemsetAsync(a.qctr, 0, sizeof(int), s);

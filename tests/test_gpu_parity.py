@@ -148,9 +148,18 @@ def test_estep_euclid_and_frozen(oracle, gpu):
     dict(N=3000, D=30, C=25, H=16, Cp=3, G=5),    # 17-column pass, D % 4 != 0 (4-byte gather)
     dict(N=2500, D=64, C=20, H=20, Cp=3, G=4),    # H + 1 > 17: two column passes + separate E pass
     dict(N=1500, D=784, C=24, H=16, Cp=5, G=10),  # config 3 shape (D = 784)
+    dict(N=4000, D=64, C=40, H=4, Cp=3, G=5),     # config 1 shape (tensor-core pass: 1 dim tile per warp)
+    dict(N=3000, D=256, C=30, H=15, Cp=3, G=5),   # H + 1 = 16: two latent n-tiles, full m16 tile
+    dict(N=3000, D=512, C=30, H=8, Cp=3, G=5),    # 8 dimension tiles per warp
+    dict(N=3000, D=48, C=30, H=10, Cp=3, G=5),    # D/8 = 6 tiles < 8 warps, XS % 32 != 4
 ])
-def test_mstep_parity(oracle, gpu, case):
+@pytest.mark.parametrize("stats", ["mma", "ffma"])
+def test_mstep_parity(oracle, gpu, case, stats, monkeypatch):
     O, V = oracle, gpu
+    if stats == "ffma":
+        monkeypatch.setenv("VMFA_STATS", "ffma")
+    else:
+        monkeypatch.delenv("VMFA_STATS", raising=False)
     X, _ = gaussian_problem(case["N"], case["D"], max(4, case["C"] // 2), min(case["H"], 4), seed=5)
     C, H, Cp, G = case["C"], case["H"], case["Cp"], case["G"]
     p, st, floor, sess = _setup(O, V, X, C, H, Cp, G)
@@ -557,4 +566,41 @@ def test_upload_state_validates_K_on_device(gpu):
     bad[42, 0] = 10  # out of range
     with pytest.raises(V.VmfaError, match=r"n=42"):
         sess.upload_state(V.State(bad, st.g, st.g_count))
+    sess.close()
+
+
+def test_config5_shape_h64(oracle, gpu):
+    # BASELINE config 5's model shape (D = 768, H = 64, C' = 5, G = 20) at a
+    # small N and C: caches, a teacher-forced E-step, the statistics (two column
+    # passes + the separate E pass of k_stats) and update_params vs the oracle
+    O, V = oracle, gpu
+    X, _ = gaussian_problem(2000, 768, 8, 16, seed=21)
+    C, H, Cp, G = 24, 64, 5, 20
+    p, st, floor, sess = _setup(O, V, X, C, H, Cp, G)
+    k = O.precompute_all(p)
+    got = sess.download_caches()
+    for name in ("Lmat", "Sz", "logdet"):
+        np.testing.assert_allclose(got[name], getattr(k, name), rtol=1e-9, atol=1e-12, err_msg=name)
+    e_or, st_or, F, J, ret, st_g, k = _estep_both(O, V, sess, X, p, st, 5, 0)
+    compare_estep(O, e_or, st_or, F, J, ret, st_g, Cp)
+    _, _, _, resp = sess.download_estep()
+    s_or = O.accumulate_suffstats(X, p, k, st_g.K, resp, threads=4)
+    sess.accumulate_suffstats()
+    s_g = sess.download_suffstats()
+    np.testing.assert_allclose(s_g.E, s_or.E, rtol=1e-5, atol=1e-6 * np.abs(s_or.E).max())
+    np.testing.assert_allclose(s_g.Y, s_or.Y, rtol=1e-5, atol=1e-6 * np.abs(s_or.Y).max())
+    np.testing.assert_allclose(s_g.sq, s_or.sq, rtol=1e-5)
+    sess.upload_suffstats(s_or)
+    sess.update_params()
+    p_g = sess.download_params()
+    p_or = O.update_params(s_or, X.shape[0], p, floor)
+    for f in ("pi", "mu", "lam", "psi"):
+        np.testing.assert_allclose(getattr(p_g, f), getattr(p_or, f), rtol=1e-8, atol=1e-11, err_msg=f)
+    k2 = O.precompute_all(p_or)
+    got = sess.download_caches()
+    for name in ("Lmat", "Sz", "logdet"):
+        np.testing.assert_allclose(got[name], getattr(k2, name), rtol=1e-8, atol=1e-11, err_msg=name)
+    F_g = sess.truncated_free_energy()
+    F_or = O.truncated_free_energy(X, p_or, k2, st_g.K, threads=4)
+    assert abs(F_g - F_or) <= 1e-5 * abs(F_or)
     sess.close()
