@@ -1293,10 +1293,11 @@ __global__ void __launch_bounds__(kStatsThreads) k_stats_E(StatsArgs a, const in
 constexpr int kSmBatch = 32;  // rows per batch (2 m-tiles of phase i, 4 k-steps of phase ii)
 constexpr int kSmZD = 17;     // s_zd row stride (fp64)
 
+// round to the nearest tf32 (ties away) by integer add + mask: two ALU
+// instructions (cvt.rna.tf32.f32 lowers to ~6 with its inf/nan guards);
+// finite inputs only (the statistics operands are finite)
 __device__ __forceinline__ float tf32_hi(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return __uint_as_float(r);
+  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xffffe000u);
 }
 __device__ __forceinline__ void mma_tf32(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
   asm volatile(
@@ -1323,6 +1324,17 @@ __device__ __forceinline__ void mma3(float (&acc)[4], const float (&ah)[4], cons
 #pragma unroll
   for (int k = 0; k < 4; ++k) acc[k] += c[k];
 }
+// the same three products chained into acc (callers keep the chain short)
+__device__ __forceinline__ void mma3c(float (&acc)[4], const float (&ah)[4], const float (&al)[4], float b0h,
+                                      float b1h, float b0l, float b1l) {
+  const uint32_t h[4] = {__float_as_uint(ah[0]), __float_as_uint(ah[1]), __float_as_uint(ah[2]),
+                         __float_as_uint(ah[3])};
+  const uint32_t l[4] = {__float_as_uint(al[0]), __float_as_uint(al[1]), __float_as_uint(al[2]),
+                         __float_as_uint(al[3])};
+  mma_tf32(acc, l, __float_as_uint(b0h), __float_as_uint(b1h));
+  mma_tf32(acc, h, __float_as_uint(b0l), __float_as_uint(b1l));
+  mma_tf32(acc, h, __float_as_uint(b0h), __float_as_uint(b1h));
+}
 
 template <int NTH, int NTW>
 __global__ void __launch_bounds__(kStatsThreads, 2) k_stats_mma(StatsArgs a, const int* __restrict__ itemoff,
@@ -1339,6 +1351,7 @@ __global__ void __launch_bounds__(kStatsThreads, 2) k_stats_mma(StatsArgs a, con
   __shared__ int s_eall[kStatsMaxRows];
   __shared__ double s_qall[kStatsMaxRows];
   __shared__ int s_item;
+  __shared__ float s_qb[kSmBatch];  // the batch's responsibilities (fp32; 0 past the item end)
   const Dims dm = a.dm;
   const int H = dm.H, H1 = H + 1, D = dm.D;
   const int XS = D + 4;  // row stride: XS % 32 == 4 for D % 32 == 0 (conflict-free phase i)
@@ -1365,6 +1378,9 @@ __global__ void __launch_bounds__(kStatsThreads, 2) k_stats_mma(StatsArgs a, con
   const int total = __ldg(itemoff + dm.C);
   if (tid == 0)
     for (int i = 0; i < kStatsMaxBuf; ++i) xbar_init(&s_xbar[i], 1);
+  // rows past an item's end keep a previous batch's (finite) rows and get q = 0;
+  // zeroed once so the first batches never see uninitialised (NaN) words
+  for (int i = tid; i < nbuf * kSmBatch * XS; i += kStatsThreads) s_x[i] = 0.f;
   __syncthreads();
   uint32_t xpar = 0u;
   auto next_item = [&](int cur) -> int {
@@ -1409,10 +1425,8 @@ __global__ void __launch_bounds__(kStatsThreads, 2) k_stats_mma(StatsArgs a, con
 #pragma unroll
     for (int w = 0; w < kStatsThreads / 32; ++w) qmax = fmax(qmax, s_red[w]);
     const double qdiv = qmax > 0.0 ? qmax : 1.0;
-    for (int i = tid; i < nr; i += kStatsThreads) {
-      const double q = s_qall[i] / qdiv;
-      s_qall[i] = q;
-    }
+    const int nbat = (nr + kSmBatch - 1) / kSmBatch;
+    for (int i = tid; i < nbat * kSmBatch; i += kStatsThreads) s_qall[i] = i < nr ? s_qall[i] / qdiv : 0.0;
     if (ei >= 0) s_accE[tid] = 0.0;
     float acc[NTW][4];
     double sqd[NTW];  // sq_v: fp32 over a batch's 8 rows per lane, then fp64
@@ -1421,10 +1435,8 @@ __global__ void __launch_bounds__(kStatsThreads, 2) k_stats_mma(StatsArgs a, con
     for (int i = 0; i < NTW; ++i) {
       sqd[i] = 0.0;
       acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
-      const int j = warp + 8 * i;
-      muj[i] = j < KS ? s_mu[8 * j + gid] : 0.f;
+      muj[i] = s_mu[8 * min(warp + 8 * i, KS - 1) + gid];
     }
-    const int nbat = (nr + kSmBatch - 1) / kSmBatch;
     auto issue_rows = [&](int b, int buf) {
       float* dst = s_x + (int64_t)buf * kSmBatch * XS;
       const int nb = min(kSmBatch, nr - b * kSmBatch);
@@ -1444,9 +1456,12 @@ __global__ void __launch_bounds__(kStatsThreads, 2) k_stats_mma(StatsArgs a, con
       const float* xb = s_x + (int64_t)buf * kSmBatch * XS;
       // (i) Z partial over this warp's K quarter: A = v rows 16pm.., B = V^T
       {
-        float z[NTH][4];
+        // three independent chains (lo*hi, hi*lo, hi*hi) hide the HMMA latency
+        float z3[3][NTH][4];
 #pragma unroll
-        for (int nt = 0; nt < NTH; ++nt) z[nt][0] = z[nt][1] = z[nt][2] = z[nt][3] = 0.f;
+        for (int t = 0; t < 3; ++t)
+#pragma unroll
+          for (int nt = 0; nt < NTH; ++nt) z3[t][nt][0] = z3[t][nt][1] = z3[t][nt][2] = z3[t][nt][3] = 0.f;
         const float* xr0 = xb + (int64_t)(16 * pm + gid) * XS + tig;
         const float* xr1 = xr0 + 8 * XS;
 #pragma unroll 4
@@ -1463,9 +1478,20 @@ __global__ void __launch_bounds__(kStatsThreads, 2) k_stats_mma(StatsArgs a, con
 #pragma unroll
           for (int nt = 0; nt < NTH; ++nt) {
             const float4 bv = s_Vb[((int64_t)ks * NTH + nt) * 32 + lane];
-            mma3(z[nt], ah, al, bv.x, bv.y, bv.z, bv.w);
+            const uint32_t h[4] = {__float_as_uint(ah[0]), __float_as_uint(ah[1]), __float_as_uint(ah[2]),
+                                   __float_as_uint(ah[3])};
+            const uint32_t l[4] = {__float_as_uint(al[0]), __float_as_uint(al[1]), __float_as_uint(al[2]),
+                                   __float_as_uint(al[3])};
+            mma_tf32(z3[0][nt], l, __float_as_uint(bv.x), __float_as_uint(bv.y));
+            mma_tf32(z3[1][nt], h, __float_as_uint(bv.z), __float_as_uint(bv.w));
+            mma_tf32(z3[2][nt], h, __float_as_uint(bv.x), __float_as_uint(bv.y));
           }
         }
+        float z[NTH][4];
+#pragma unroll
+        for (int nt = 0; nt < NTH; ++nt)
+#pragma unroll
+          for (int k = 0; k < 4; ++k) z[nt][k] = (z3[0][nt][k] + z3[1][nt][k]) + z3[2][nt][k];
 #pragma unroll
         for (int nt = 0; nt < NTH; ++nt) {
           *reinterpret_cast<float2*>(&s_pz[pq][16 * pm + gid][8 * nt + 2 * tig]) = make_float2(z[nt][0], z[nt][1]);
@@ -1477,20 +1503,24 @@ __global__ void __launch_bounds__(kStatsThreads, 2) k_stats_mma(StatsArgs a, con
       if (nbuf >= 2 && bi + nbuf - 1 < nbat) issue_rows(bi + nbuf - 1, (bi + nbuf - 1) % nbuf);
       // combine: zhat rows (fp64 for E) and the q-scaled phase (ii) A fragments
       const double* s_q = s_qall + bi * kSmBatch;
-      for (int i = tid; i < kSmBatch * 16; i += kStatsThreads) {
-        const int r = i >> 4, h = i & 15;
-        float z = 0.f;
-        if (r < nb) {
-          if (h < H) z = s_pz[0][r][h] + s_pz[1][r][h] + s_pz[2][r][h] + s_pz[3][r][h];
-          else if (h == H) z = 1.f;
-        }
-        if (h < H1) s_zd[r * kSmZD + h] = z;
-        const float qz = r < nb ? static_cast<float>(s_q[r]) * z : 0.f;
-        const float hi = tf32_hi(qz);
-        const int ks = r >> 3, rr = r & 7;
-        const int ln = (h & 7) * 4 + (rr & 3), reg = (h >> 3) + 2 * (rr >> 2);
-        reinterpret_cast<float*>(&s_Af[ks][ln][0])[reg] = hi;
-        reinterpret_cast<float*>(&s_Af[ks][ln][1])[reg] = qz - hi;
+      {
+        // thread = (k-step, lane, row half): row r, columns gid and gid + 8
+        const int ks = tid >> 6, ln = (tid >> 1) & 31, up = tid & 1;
+        const int r = 8 * ks + (ln & 3) + 4 * up, h0 = ln >> 2, h1 = h0 + 8;
+        auto zval = [&](int h) -> float {
+          if (r >= nb || h > H) return 0.f;
+          if (h == H) return 1.f;
+          return s_pz[0][r][h] + s_pz[1][r][h] + s_pz[2][r][h] + s_pz[3][r][h];
+        };
+        const float z0 = zval(h0), z1 = zval(h1);
+        if (h0 < H1) s_zd[r * kSmZD + h0] = z0;
+        if (h1 < H1) s_zd[r * kSmZD + h1] = z1;
+        const float qf = static_cast<float>(s_q[r]);
+        if (h0 == 0) s_qb[r] = qf;
+        const float qz0 = qf * z0, qz1 = qf * z1;
+        const float hi0 = tf32_hi(qz0), hi1 = tf32_hi(qz1);
+        reinterpret_cast<float2*>(&s_Af[ks][ln][0])[up] = make_float2(hi0, hi1);
+        reinterpret_cast<float2*>(&s_Af[ks][ln][1])[up] = make_float2(qz0 - hi0, qz1 - hi1);
       }
       __syncthreads();
       if (ei >= 0) {
@@ -1498,33 +1528,39 @@ __global__ void __launch_bounds__(kStatsThreads, 2) k_stats_mma(StatsArgs a, con
         for (int r = eg; r < nb; r += EG) e = fma(s_q[r], s_zd[r * kSmZD + ei] * s_zd[r * kSmZD + ej], e);
         s_accE[tid] = e;
       }
-      // (ii) Y_v^T += (Q zhat)^T v over the batch's 4 k-steps
+      // (ii) Y_v^T += (Q zhat)^T v over the batch's 4 k-steps (rows past nb:
+      // q = 0 and A = 0, stale finite v), chained per batch, then one FADD
+      // per accumulator into the item's sums
       float sqa[NTW];
+      float accb[NTW][4];
 #pragma unroll
-      for (int i = 0; i < NTW; ++i) sqa[i] = 0.f;
+      for (int i = 0; i < NTW; ++i) sqa[i] = accb[i][0] = accb[i][1] = accb[i][2] = accb[i][3] = 0.f;
 #pragma unroll
       for (int ks = 0; ks < kSmBatch / 8; ++ks) {
         const float4 Ah = s_Af[ks][lane][0], Al = s_Af[ks][lane][1];
         const float ah[4] = {Ah.x, Ah.y, Ah.z, Ah.w}, al[4] = {Al.x, Al.y, Al.z, Al.w};
         const int ra = 8 * ks + tig, rb = ra + 4;
-        const bool oka = ra < nb, okb = rb < nb;
-        const float qa = oka ? static_cast<float>(s_q[ra]) : 0.f, qb = okb ? static_cast<float>(s_q[rb]) : 0.f;
+        const float qa = s_qb[ra], qb = s_qb[rb];
         const float* xa = xb + (int64_t)ra * XS + gid;
         const float* xb2 = xb + (int64_t)rb * XS + gid;
 #pragma unroll
         for (int i = 0; i < NTW; ++i) {
-          const int j = warp + 8 * i;
-          if (NTW > 1 && j >= KS) break;
-          const float va = oka ? xa[8 * j] - muj[i] : 0.f;
-          const float vb = okb ? xb2[8 * j] - muj[i] : 0.f;
+          // tiles past D/8 (D < 64 NTW) repeat the last tile; their sums are not written
+          const int j = min(warp + 8 * i, KS - 1);
+          const float va = xa[8 * j] - muj[i];
+          const float vb = xb2[8 * j] - muj[i];
           sqa[i] = fmaf(qa * va, va, sqa[i]);
           sqa[i] = fmaf(qb * vb, vb, sqa[i]);
           const float vah = tf32_hi(va), vbh = tf32_hi(vb);
-          mma3(acc[i], ah, al, vah, vbh, va - vah, vb - vbh);
+          mma3c(accb[i], ah, al, vah, vbh, va - vah, vb - vbh);
         }
       }
 #pragma unroll
-      for (int i = 0; i < NTW; ++i) sqd[i] += sqa[i];
+      for (int i = 0; i < NTW; ++i) {
+        sqd[i] += sqa[i];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) acc[i][k] += accb[i][k];
+      }
       if (nbuf == 1) __syncthreads();
     }
     // write: E (fp64, row groups summed in order), Y_v columns and sq_v, scaled by qmax
