@@ -439,6 +439,7 @@ __device__ __forceinline__ double from_fixed(long long hi, long long lo) {
   return static_cast<double>(hi) * (1.0 / 1024.0) + static_cast<double>(lo) * (1.0 / 1125899906842624.0);
 }
 constexpr int kGupdBatch = 4;  // points in flight per warp in k_gupdate
+constexpr int kGupdProbes = 32;  // probe limit of a dense-rows item's hash
 __device__ __forceinline__ unsigned hash_key(int k) { return static_cast<unsigned>(k) * 2654435761u; }
 
 struct KeyMin {
@@ -560,14 +561,20 @@ __global__ void __launch_bounds__(kGupdThreads) k_gupdate(GupdArgs a, int capmax
           long long hi, lo;
           to_fixed(v, hi, lo);
           if (use_smem) {
+            // linear probing; an item adding into the dense rows stops after
+            // kGupdProbes slots and adds straight into row c (exact integer
+            // sums, so where a key's parts land does not matter): a table
+            // filled by a large component (config 3: ~4000 keys in 2048 slots)
+            // would otherwise scan every slot per insertion
             unsigned h = hash_key(ct) & (cap - 1);
+            const int plim = to_rows ? min(cap, kGupdProbes) : cap;
             int probes = 0;
             bool full = false;
             while (true) {
               const int prev = atomicCAS(t_key + h, -1, ct);
               if (prev == -1 || prev == ct) break;
               h = (h + 1) & (cap - 1);
-              if (++probes >= cap) {
+              if (++probes >= plim) {
                 full = true;
                 break;
               }
@@ -1448,8 +1455,7 @@ __global__ void __launch_bounds__(kStatsThreads, 2) k_stats_mma(StatsArgs a, con
       }
     };
     for (int b = 0; b < min(nbuf - 1, nbat); ++b) issue_rows(b, b);
-    for (int bi = 0; bi < nbat; ++bi) {
-      const int buf = bi % nbuf;
+    for (int bi = 0, buf = 0; bi < nbat; ++bi, buf = buf + 1 == nbuf ? 0 : buf + 1) {
       const int nb = min(kSmBatch, nr - bi * kSmBatch);
       xbar_wait(&s_xbar[buf], (xpar >> buf) & 1u);
       xpar ^= 1u << buf;
@@ -1500,7 +1506,7 @@ __global__ void __launch_bounds__(kStatsThreads, 2) k_stats_mma(StatsArgs a, con
         }
       }
       __syncthreads();
-      if (nbuf >= 2 && bi + nbuf - 1 < nbat) issue_rows(bi + nbuf - 1, (bi + nbuf - 1) % nbuf);
+      if (nbuf >= 2 && bi + nbuf - 1 < nbat) issue_rows(bi + nbuf - 1, buf == 0 ? nbuf - 1 : buf - 1);
       // combine: zhat rows (fp64 for E) and the q-scaled phase (ii) A fragments
       const double* s_q = s_qall + bi * kSmBatch;
       {
