@@ -1538,9 +1538,13 @@ __global__ void __launch_bounds__(kStatsThreads, 2) k_stats_mma(StatsArgs a, con
       // q = 0 and A = 0, stale finite v), chained per batch, then one FADD
       // per accumulator into the item's sums
       float sqa[NTW];
-      float accb[NTW][4];
+      float accb[NTW][4], accl[NTW][4];  // hi*hi chain and the two correction products' chain
 #pragma unroll
-      for (int i = 0; i < NTW; ++i) sqa[i] = accb[i][0] = accb[i][1] = accb[i][2] = accb[i][3] = 0.f;
+      for (int i = 0; i < NTW; ++i) {
+        sqa[i] = 0.f;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) accb[i][k] = accl[i][k] = 0.f;
+      }
 #pragma unroll
       for (int ks = 0; ks < kSmBatch / 8; ++ks) {
         const float4 Ah = s_Af[ks][lane][0], Al = s_Af[ks][lane][1];
@@ -1558,14 +1562,20 @@ __global__ void __launch_bounds__(kStatsThreads, 2) k_stats_mma(StatsArgs a, con
           sqa[i] = fmaf(qa * va, va, sqa[i]);
           sqa[i] = fmaf(qb * vb, vb, sqa[i]);
           const float vah = tf32_hi(va), vbh = tf32_hi(vb);
-          mma3c(accb[i], ah, al, vah, vbh, va - vah, vb - vbh);
+          const uint32_t h[4] = {__float_as_uint(ah[0]), __float_as_uint(ah[1]), __float_as_uint(ah[2]),
+                                 __float_as_uint(ah[3])};
+          const uint32_t l[4] = {__float_as_uint(al[0]), __float_as_uint(al[1]), __float_as_uint(al[2]),
+                                 __float_as_uint(al[3])};
+          mma_tf32(accl[i], l, __float_as_uint(vah), __float_as_uint(vbh));
+          mma_tf32(accl[i], h, __float_as_uint(va - vah), __float_as_uint(vb - vbh));
+          mma_tf32(accb[i], h, __float_as_uint(vah), __float_as_uint(vbh));
         }
       }
 #pragma unroll
       for (int i = 0; i < NTW; ++i) {
         sqd[i] += sqa[i];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) acc[i][k] += accb[i][k];
+        for (int k = 0; k < 4; ++k) acc[i][k] += accl[i][k] + accb[i][k];
       }
       if (nbuf == 1) __syncthreads();
     }
