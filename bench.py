@@ -261,13 +261,18 @@ def main():
                                                  data=(ptr, False), version=3)
 
     xb = {}
+    sparse = world > 1 and sess.cooc_sparse()
     if world > 1:
-        for w in (0, 1, 2):
+        for w in ((1, 2) if sparse else (0, 1, 2)):
             xb[w] = torch.as_tensor(_View(*sess.exchange_buffer(w)), device=f"cuda:{local}")
 
     def allreduce(w):
         with torch.cuda.stream(ext):
-            dist.all_reduce(xb[w])
+            if w == 0 and sparse:  # large C: owner-routed (c, c~) lists + int32 all-reduce of g
+                from paper_2501_12299_b200.exchange import cooc_exchange
+                cooc_exchange(sess, rank, world)
+            else:
+                dist.all_reduce(xb[w])
         ext.synchronize()
 
     it_counter = [0]

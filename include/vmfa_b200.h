@@ -190,8 +190,13 @@ int vmfa_iterate(vmfa_ctx* ctx, uint64_t seed, uint64_t iteration, int mode,
  *   vmfa_phase_estep_local -> allreduce(COOC) -> vmfa_phase_estep_finish ->
  *   vmfa_phase_stats_local -> allreduce(STATS) -> vmfa_phase_update ->
  *   vmfa_phase_free_energy_local -> allreduce(SCALARS).                    */
-typedef enum vmfa_exchange { VMFA_XCHG_COOC = 0, VMFA_XCHG_STATS = 1, VMFA_XCHG_SCALARS = 2 } vmfa_exchange;
-typedef enum vmfa_dtype { VMFA_DT_INT64 = 0, VMFA_DT_FLOAT64 = 1 } vmfa_dtype;
+typedef enum vmfa_exchange {
+  VMFA_XCHG_COOC = 0,
+  VMFA_XCHG_STATS = 1,
+  VMFA_XCHG_SCALARS = 2,
+  VMFA_XCHG_G = 3
+} vmfa_exchange;
+typedef enum vmfa_dtype { VMFA_DT_INT64 = 0, VMFA_DT_FLOAT64 = 1, VMFA_DT_INT32 = 2 } vmfa_dtype;
 int vmfa_exchange_buffer(vmfa_ctx* ctx, int which, void** device_ptr, size_t* count, int* dtype);
 int vmfa_phase_estep_local(vmfa_ctx* ctx, uint64_t seed, uint64_t iteration, int mode);
 int vmfa_phase_estep_finish(vmfa_ctx* ctx);
@@ -201,6 +206,27 @@ int vmfa_phase_free_energy_local(vmfa_ctx* ctx);
 /* Reads the (reduced) scalars buffer: F_estep, joints, F_post.             */
 int vmfa_phase_scalars(vmfa_ctx* ctx, double* free_energy_estep, uint64_t* joints,
                        double* free_energy);
+/* Sparse co-occurrence exchange (SURVEY §8(e) sparse variant; used when C is
+ * too large for the dense table, C > ~18900, or with VMFA_COOC=sparse at
+ * context creation). In place of allreduce(COOC):
+ *   vmfa_phase_estep_local   (each rank reduces its (c, c~) list by key)
+ *   vmfa_cooc_local_list     (device arrays key u32 = c << b | c~, cnt/hi/lo
+ *                             int64, sorted by key; counts[r] = entries owned
+ *                             by rank r = components [rC/p, (r+1)C/p), which
+ *                             are contiguous)
+ *   all-to-all of the four arrays with those counts (NCCL send/recv)
+ *   vmfa_cooc_select         (the received lists, concatenated: reduced by key
+ *                             and g_c selected for this rank's components into
+ *                             the VMFA_XCHG_G buffer, other rows zero)
+ *   allreduce(G, int32 sum) -> vmfa_phase_estep_finish.
+ * The per-key sums are exact integers, so g is bit-identical to the dense
+ * path for every rank count. Replaces estep.cpp:286-312's accumulator +
+ * update_g (estep.cpp:204-220) across ranks.                              */
+int vmfa_cooc_sparse(vmfa_ctx* ctx, int* sparse);
+int vmfa_cooc_local_list(vmfa_ctx* ctx, int world, void** key, void** cnt, void** hi, void** lo,
+                         int64_t* counts);
+int vmfa_cooc_select(vmfa_ctx* ctx, const void* key, const void* cnt, const void* hi, const void* lo,
+                     int64_t n, int rank, int world);
 
 /* ------------------------------------------------------------------ timing / profiling */
 /* Records CUDA events around the scoring kernels of subsequent calls;

@@ -95,6 +95,9 @@ _SIGS = {
     "vmfa_phase_update": (_I, [_P, C.POINTER(_I)]),
     "vmfa_phase_free_energy_local": (_I, [_P]),
     "vmfa_phase_scalars": (_I, [_P, C.POINTER(_D), C.POINTER(_U64), C.POINTER(_D)]),
+    "vmfa_cooc_sparse": (_I, [_P, C.POINTER(_I)]),
+    "vmfa_cooc_local_list": (_I, [_P, _I, C.POINTER(_P), C.POINTER(_P), C.POINTER(_P), C.POINTER(_P), _P]),
+    "vmfa_cooc_select": (_I, [_P, _P, _P, _P, _P, C.c_int64, _I, _I]),
     "vmfa_profile_enable": (_I, [_P, _I]),
     "vmfa_kernel_times": (_I, [_P, _I, _P, _P, _P, C.POINTER(_I)]),
     "vmfa_kernel_name": (C.c_char_p, [_I]),

@@ -128,6 +128,20 @@ struct vmfa_ctx {
   int gupd_grid = 0;
   long long *gt_cnt = nullptr, *gt_hi = nullptr, *gt_lo = nullptr;
   long long* xc = nullptr;  // multi-rank exchange (lazy)
+  // sparse co-occurrence lists (C too large for the dense rows, or
+  // VMFA_COOC=sparse): raw appended entries, their sort, the reduced list
+  bool sparse = false;
+  long long cl_cap = 0;
+  int cl_kb = 0;
+  unsigned *cl_key = nullptr, *cl_skey = nullptr, *cu_key = nullptr;
+  long long *cl_cnt = nullptr, *cl_hi = nullptr, *cl_lo = nullptr;
+  long long *cu_cnt = nullptr, *cu_hi = nullptr, *cu_lo = nullptr;
+  int *cl_iota = nullptr, *cl_perm = nullptr, *cu_off = nullptr;
+  unsigned long long* cl_n = nullptr;
+  int* cl_ovf = nullptr;
+  int64_t cu_n = 0;  // unique entries of the last reduction (host)
+  void* cl_tmp = nullptr;
+  size_t cl_tmp_bytes = 0;
   // stats: packed [Nc | E | Y | sq]
   double* stats = nullptr;
   size_t stats_len = 0;
@@ -361,6 +375,68 @@ int score_anchors(vmfa_ctx* x) {
   return VMFA_OK;
 }
 
+// Sparse co-occurrence: reduce the n raw entries in cl_* (sorted by key,
+// exact sums per unique key) into cu_* and the per-component offsets cu_off.
+int cooc_reduce(vmfa_ctx* x, int64_t n) {
+  cudaStream_t s = x->stream;
+  if (n > x->cl_cap) return fail(VMFA_ERR_UNSUPPORTED, "co-occurrence list of %lld entries exceeds its capacity %lld",
+                                 static_cast<long long>(n), static_cast<long long>(x->cl_cap));
+  CU(launch_iota(x->cl_iota, n, s));
+  size_t tb = x->cl_tmp_bytes;
+  CU(cub::DeviceRadixSort::SortPairs(x->cl_tmp, tb, x->cl_key, x->cl_skey, x->cl_iota, x->cl_perm,
+                                     static_cast<int>(n), 0, 2 * x->cl_kb, s));
+  CoocArgs a{};
+  a.dm = x->dm;
+  a.kb = x->cl_kb;
+  a.key = x->cl_skey;
+  a.perm = x->cl_perm;
+  a.cnt = x->cl_cnt;
+  a.hi = x->cl_hi;
+  a.lo = x->cl_lo;
+  a.n = static_cast<int>(n);
+  a.head = x->cl_iota;  // reused: heads, then their inclusive scan
+  a.u_key = x->cu_key;
+  a.u_cnt = x->cu_cnt;
+  a.u_hi = x->cu_hi;
+  a.u_lo = x->cu_lo;
+  a.u_off = x->cu_off;
+  CU(launch_cooc_heads(a, s));
+  tb = x->cl_tmp_bytes;
+  if (n > 0) CU(cub::DeviceScan::InclusiveSum(x->cl_tmp, tb, x->cl_iota, x->cl_iota, static_cast<int>(n), s));
+  for (long long* q : {x->cu_cnt, x->cu_hi, x->cu_lo})
+    CU(cudaMemsetAsync(q, 0, static_cast<size_t>(std::max<int64_t>(n, 1)) * sizeof(long long), s));
+  CU(launch_cooc_sums(a, s));
+  int un = 0;
+  if (n > 0) CU(cudaMemcpyAsync(&un, x->cl_iota + n - 1, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  x->cu_n = un;
+  return VMFA_OK;
+}
+CoocArgs cooc_args(vmfa_ctx* x) {
+  CoocArgs a{};
+  a.dm = x->dm;
+  a.kb = x->cl_kb;
+  a.u_key = x->cu_key;
+  a.u_cnt = x->cu_cnt;
+  a.u_hi = x->cu_hi;
+  a.u_lo = x->cu_lo;
+  a.u_off = x->cu_off;
+  return a;
+}
+// entries appended by the last k_gupdate (host read; overflow is an error)
+int cooc_count(vmfa_ctx* x, int64_t* n) {
+  unsigned long long c = 0;
+  int ovf = 0;
+  CU(cudaMemcpyAsync(&c, x->cl_n, sizeof c, cudaMemcpyDeviceToHost, x->stream));
+  CU(cudaMemcpyAsync(&ovf, x->cl_ovf, sizeof ovf, cudaMemcpyDeviceToHost, x->stream));
+  CU(cudaStreamSynchronize(x->stream));
+  if (ovf || static_cast<long long>(c) > x->cl_cap)
+    return fail(VMFA_ERR_UNSUPPORTED, "co-occurrence list overflow (%llu entries, capacity %lld)", c,
+                static_cast<long long>(x->cl_cap));
+  *n = static_cast<int64_t>(c);
+  return VMFA_OK;
+}
+
 // E-step blocks 1, 2, 4 and the local part of block 3.
 int estep_local(vmfa_ctx* x, uint64_t seed, uint64_t it, int mode, bool exchange) {
   const Dims& dm = x->dm;
@@ -436,8 +512,21 @@ int estep_local(vmfa_ctx* x, uint64_t seed, uint64_t it, int mode, bool exchange
     a.itemoff = x->part_items;
     a.pts_per_item = x->gupd_pts;
     a.exchange = exchange ? 1 : 0;
-    a.force_rows = (x->xc && dm.C - 1 > kGupdCap / 2) ? 1 : 0;
+    a.force_rows = ((x->xc && dm.C - 1 > kGupdCap / 2) || x->sparse) ? 1 : 0;
     a.xc = x->xc;
+    if (x->sparse) {
+      a.list = 1;
+      a.cl_key = x->cl_key;
+      a.cl_cnt = x->cl_cnt;
+      a.cl_hi = x->cl_hi;
+      a.cl_lo = x->cl_lo;
+      a.cl_n = x->cl_n;
+      a.cl_cap = x->cl_cap;
+      a.cl_kb = x->cl_kb;
+      a.cl_ovf = x->cl_ovf;
+      CU(cudaMemsetAsync(x->cl_n, 0, sizeof(unsigned long long), s));
+      CU(cudaMemsetAsync(x->cl_ovf, 0, sizeof(int), s));
+    }
     a.dump = x->dump ? 1 : 0;
     if (x->dump) {
       CU(cudaMemsetAsync(x->dump_n, 0, sizeof(unsigned long long), s));
@@ -453,6 +542,14 @@ int estep_local(vmfa_ctx* x, uint64_t seed, uint64_t it, int mode, bool exchange
     CU(launch_gupdate(a, x->gupd_grid, s));
     if (!exchange && x->xc)
       CU(launch_gselect_dense(dm, x->xc, x->part_items, a.force_rows, x->g_new, x->gcnt_new, s));
+    if (x->sparse) {
+      // the rank-local list reduced by key (sent as it is in exchange mode);
+      // single context: every component's g from it
+      int64_t n = 0;
+      TRY(cooc_count(x, &n));
+      TRY(cooc_reduce(x, n));
+      if (!exchange) CU(launch_cooc_select(cooc_args(x), 0, dm.C, 0, x->g_new, x->gcnt_new, s));
+    }
     x->end(tok);
   }
   // scalars: F_estep = sum lse, joints = sum ret_cnt
@@ -467,7 +564,7 @@ int estep_local(vmfa_ctx* x, uint64_t seed, uint64_t it, int mode, bool exchange
 int estep_finish(vmfa_ctx* x, bool exchange, bool sync = true) {
   const Dims& dm = x->dm;
   cudaStream_t s = x->stream;
-  if (exchange) {
+  if (exchange && !x->sparse) {
     const int tok = x->begin(kFamGupdate, dm.C);
     CU(launch_gselect_dense(dm, x->xc, x->part_items, 1, x->g_new, x->gcnt_new, s));
     x->end(tok);
@@ -706,7 +803,10 @@ int vmfa_ctx_create(vmfa_ctx** out, int device, int C, int D, int H, int Cp, int
   auto A = [&](auto*& p, size_t n) {
     if (r == VMFA_OK) r = x->alloc(p, n);
   };
-  const bool dense_rows = 3.0 * Cs * Cs * sizeof(long long) <= 8.0 * (1ull << 30);
+  const char* cooc_env = std::getenv("VMFA_COOC");
+  const bool force_sparse = cooc_env && std::string(cooc_env) == "sparse";
+  const bool dense_rows = !force_sparse && 3.0 * Cs * Cs * sizeof(long long) <= 8.0 * (1ull << 30);
+  x->sparse = !dense_rows;
   A(x->X, N * D);
   A(x->floor, D);
   for (double** p : {&x->pi, &x->pi2}) A(*p, Cs);
@@ -735,10 +835,14 @@ int vmfa_ctx_create(vmfa_ctx** out, int device, int C, int D, int H, int Cp, int
   }
   A(x->ipsi32, Cs * D);
   A(x->K, N * Cp);
-  A(x->g, Cs * G);
-  A(x->gcnt, Cs);
-  A(x->g_new, Cs * G);
-  A(x->gcnt_new, Cs);
+  // g and its counts contiguous ([C*G | C] int32), so the sparse exchange can
+  // all-reduce a rank's selected rows as one buffer (VMFA_XCHG_G)
+  A(x->g, Cs * G + Cs);
+  A(x->g_new, Cs * G + Cs);
+  if (r == VMFA_OK) {
+    x->gcnt = x->g + Cs * G;
+    x->gcnt_new = x->g_new + Cs * G;
+  }
   A(x->labels, N);
   A(x->lablj, N);
   A(x->LJ, N * dm.SL);
@@ -782,13 +886,36 @@ int vmfa_ctx_create(vmfa_ctx** out, int device, int C, int D, int H, int Cp, int
     A(x->xc, 3 * Cs * Cs);
     if (r == VMFA_OK) cudaMemsetAsync(x->xc, 0, 3 * Cs * Cs * sizeof(long long), x->stream);
   } else {
-    x->gupd_pts = 1 << 30;
+    // sparse lists: every block-3 item appends its exact partial table (items
+    // of up to 512 points); capacity for 8 distinct keys per point on average
+    // (typical: a few per point; overflow is reported, never silent)
+    const int64_t bal = std::max<int64_t>(128, static_cast<int64_t>(N) / (4 * sm_count()));
+    x->gupd_pts = static_cast<int>(std::min<int64_t>(bal, 512));
+    x->cl_kb = bits_for(static_cast<unsigned>(C));
+    x->cl_cap = std::max<int64_t>(int64_t{1} << 20, static_cast<int64_t>(N) * 8);
+    if (2 * x->cl_kb > 32) r = fail(VMFA_ERR_UNSUPPORTED, "sparse co-occurrence keys need C < 65536");
+    const size_t L = static_cast<size_t>(x->cl_cap);
+    A(x->cl_key, L);
+    A(x->cl_skey, L);
+    A(x->cu_key, L);
+    A(x->cl_cnt, L);
+    A(x->cl_hi, L);
+    A(x->cl_lo, L);
+    A(x->cu_cnt, L);
+    A(x->cu_hi, L);
+    A(x->cu_lo, L);
+    A(x->cl_iota, L);
+    A(x->cl_perm, L);
+    A(x->cu_off, Cs + 1);
+    A(x->cl_n, 1);
+    A(x->cl_ovf, 1);
   }
   A(x->cnt, Cs + 1);
   A(x->chunks, Cs + 1);
   x->gupd_grid = sm_count() * 4;
   // per-CTA dense fallback tables: only needed without the dense C x C rows
-  const size_t gt_n = dense_rows ? 1 : static_cast<size_t>(x->gupd_grid) * Cs;
+  // (every item of the sparse mode adds into the list, so neither mode needs them)
+  const size_t gt_n = (dense_rows || x->sparse) ? 1 : static_cast<size_t>(x->gupd_grid) * Cs;
   A(x->gt_cnt, gt_n);
   A(x->gt_hi, gt_n);
   A(x->gt_lo, gt_n);
@@ -825,6 +952,21 @@ int vmfa_ctx_create(vmfa_ctx** out, int device, int C, int D, int H, int Cp, int
   x->allocs.push_back(tmp);
   x->bytes += x->cub_bytes;
   x->cub_tmp = tmp;
+  if (x->sparse) {
+    size_t c1 = 0, c2 = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, c1, x->cl_key, x->cl_skey, x->cl_iota, x->cl_perm,
+                                    static_cast<int>(x->cl_cap), 0, 32, x->stream);
+    cub::DeviceScan::InclusiveSum(nullptr, c2, x->cl_iota, x->cl_perm, static_cast<int>(x->cl_cap), x->stream);
+    x->cl_tmp_bytes = std::max(c1, c2) + 256;
+    void* t2 = nullptr;
+    if (cudaMalloc(&t2, x->cl_tmp_bytes) != cudaSuccess) {
+      vmfa_ctx_destroy(x);
+      return fail(VMFA_ERR_CUDA, "cudaMalloc(co-occurrence sort temp) failed");
+    }
+    x->allocs.push_back(t2);
+    x->bytes += x->cl_tmp_bytes;
+    x->cl_tmp = t2;
+  }
   cudaMemsetAsync(x->scal, 0, 4 * sizeof(double), x->stream);
   cudaMemsetAsync(x->labels, 0, N * sizeof(int), x->stream);
   if (cudaStreamSynchronize(x->stream) != cudaSuccess) {
@@ -1323,7 +1465,8 @@ int vmfa_exchange_buffer(vmfa_ctx* x, int which, void** ptr, size_t* count, int*
   if (which == VMFA_XCHG_COOC) {
     const size_t n = 3 * static_cast<size_t>(x->dm.C) * x->dm.C;
     if (!x->xc)
-      return fail(VMFA_ERR_UNSUPPORTED, "dense co-occurrence exchange limited to C <= ~18900 in this build");
+      return fail(VMFA_ERR_UNSUPPORTED, "no dense co-occurrence table in sparse mode (C > ~18900 or "
+                                        "VMFA_COOC=sparse): use vmfa_cooc_local_list / vmfa_cooc_select");
     *ptr = x->xc;
     *count = n;
     *dtype = VMFA_DT_INT64;
@@ -1335,6 +1478,10 @@ int vmfa_exchange_buffer(vmfa_ctx* x, int which, void** ptr, size_t* count, int*
     *ptr = x->scal;
     *count = 3;
     *dtype = VMFA_DT_FLOAT64;
+  } else if (which == VMFA_XCHG_G) {
+    *ptr = x->g_new;
+    *count = static_cast<size_t>(x->dm.C) * x->dm.G + x->dm.C;
+    *dtype = VMFA_DT_INT32;
   } else {
     return fail(VMFA_ERR_INVALID_ARGUMENT, "unknown exchange buffer %d", which);
   }
@@ -1343,7 +1490,7 @@ int vmfa_exchange_buffer(vmfa_ctx* x, int which, void** ptr, size_t* count, int*
 
 int vmfa_phase_estep_local(vmfa_ctx* x, uint64_t seed, uint64_t iteration, int mode) {
   TRY(check_ctx(x));
-  if (!x->xc) {
+  if (!x->xc && !x->sparse) {
     void* p;
     size_t n;
     int dt;
@@ -1381,6 +1528,51 @@ int vmfa_phase_scalars(vmfa_ctx* x, double* Fe, uint64_t* joints, double* F) {
   if (Fe) *Fe = sc[0];
   if (joints) *joints = static_cast<uint64_t>(sc[1]);
   if (F) *F = sc[2];
+  return VMFA_OK;
+}
+
+int vmfa_cooc_sparse(vmfa_ctx* x, int* sparse) {
+  TRY(check_ctx(x));
+  if (!sparse) return fail(VMFA_ERR_INVALID_ARGUMENT, "null output");
+  *sparse = x->sparse ? 1 : 0;
+  return VMFA_OK;
+}
+int vmfa_cooc_local_list(vmfa_ctx* x, int world, void** key, void** cnt, void** hi, void** lo, int64_t* counts) {
+  TRY(check_ctx(x));
+  if (!x->sparse) return fail(VMFA_ERR_INVALID_ARGUMENT, "context has the dense co-occurrence table");
+  if (world < 1 || !key || !cnt || !hi || !lo || !counts) return fail(VMFA_ERR_INVALID_ARGUMENT, "bad arguments");
+  *key = x->cu_key;
+  *cnt = x->cu_cnt;
+  *hi = x->cu_hi;
+  *lo = x->cu_lo;
+  // owner r holds components [floor(rC/p), floor((r+1)C/p)): contiguous in the sorted list
+  std::vector<int> b(world + 1);
+  for (int r = 0; r <= world; ++r) {
+    const int c = static_cast<int>(static_cast<int64_t>(r) * x->dm.C / world);
+    CU(cudaMemcpyAsync(&b[r], x->cu_off + c, sizeof(int), cudaMemcpyDeviceToHost, x->stream));
+  }
+  CU(cudaStreamSynchronize(x->stream));
+  for (int r = 0; r < world; ++r) counts[r] = b[r + 1] - b[r];
+  return VMFA_OK;
+}
+int vmfa_cooc_select(vmfa_ctx* x, const void* key, const void* cnt, const void* hi, const void* lo, int64_t n,
+                     int rank, int world) {
+  TRY(check_ctx(x));
+  if (!x->sparse) return fail(VMFA_ERR_INVALID_ARGUMENT, "context has the dense co-occurrence table");
+  if (world < 1 || rank < 0 || rank >= world || n < 0) return fail(VMFA_ERR_INVALID_ARGUMENT, "bad rank/world/n");
+  if (n > x->cl_cap) return fail(VMFA_ERR_UNSUPPORTED, "received co-occurrence list exceeds the capacity");
+  cudaStream_t s = x->stream;
+  if (n > 0) {
+    CU(cudaMemcpyAsync(x->cl_key, key, n * sizeof(unsigned), cudaMemcpyDeviceToDevice, s));
+    CU(cudaMemcpyAsync(x->cl_cnt, cnt, n * sizeof(long long), cudaMemcpyDeviceToDevice, s));
+    CU(cudaMemcpyAsync(x->cl_hi, hi, n * sizeof(long long), cudaMemcpyDeviceToDevice, s));
+    CU(cudaMemcpyAsync(x->cl_lo, lo, n * sizeof(long long), cudaMemcpyDeviceToDevice, s));
+  }
+  TRY(cooc_reduce(x, n));
+  const int c0 = static_cast<int>(static_cast<int64_t>(rank) * x->dm.C / world);
+  const int c1 = static_cast<int>(static_cast<int64_t>(rank + 1) * x->dm.C / world);
+  CU(launch_cooc_select(cooc_args(x), c0, c1, 1, x->g_new, x->gcnt_new, s));
+  CU(cudaStreamSynchronize(s));
   return VMFA_OK;
 }
 

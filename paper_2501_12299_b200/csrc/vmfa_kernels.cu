@@ -492,11 +492,11 @@ __global__ void __launch_bounds__(kGupdThreads) k_gupdate(GupdArgs a, int capmax
     const int p0 = a.part_off[c] + (item - a.itemoff[c]) * a.pts_per_item;
     const int p1 = min(a.part_off[c + 1], p0 + a.pts_per_item);
     const int npts = max(0, p1 - p0);
-    const bool to_rows = a.exchange || nitems > 1 || a.force_rows;
+    const bool to_rows = a.exchange || nitems > 1 || a.force_rows || a.list;
     const long long bound = llmin((long long)dm.C - 1, (long long)npts * (dm.stride - 1));
     int cap = 32;
     bool use_smem;
-    if (to_rows && a.xc) {  // small table sized for the typical key count; overflow adds into row c of xc
+    if (to_rows && (a.xc || a.list)) {  // small table sized for the typical key count; overflow adds into row c of xc (or the list)
       while (cap < 2 * bound && cap < min(capmax, kGupdRowsCap)) cap <<= 1;
       use_smem = true;
     } else {
@@ -579,7 +579,17 @@ __global__ void __launch_bounds__(kGupdThreads) k_gupdate(GupdArgs a, int capmax
                 break;
               }
             }
-            if (full) {  // (to_rows items only: exact integer adds straight into row c)
+            if (full && a.list) {  // (to_rows items only: one list entry for this occurrence)
+              const unsigned long long w = atomicAdd(a.cl_n, 1ULL);
+              if ((long long)w < a.cl_cap) {
+                a.cl_key[w] = (static_cast<unsigned>(c) << a.cl_kb) | static_cast<unsigned>(ct);
+                a.cl_cnt[w] = 1;
+                a.cl_hi[w] = hi;
+                a.cl_lo[w] = lo;
+              } else {
+                atomicExch(a.cl_ovf, 1);
+              }
+            } else if (full) {  // (to_rows items only: exact integer adds straight into row c)
               const int64_t at = (int64_t)c * dm.C + ct;
               atomicAdd(reinterpret_cast<unsigned long long*>(a.xc + at), 1ULL);
               atomicAdd(reinterpret_cast<unsigned long long*>(a.xc + CC + at), static_cast<unsigned long long>(hi));
@@ -628,6 +638,35 @@ __global__ void __launch_bounds__(kGupdThreads) k_gupdate(GupdArgs a, int capmax
           a.dump_lo[w] = lo;
         }
       }
+    }
+    if (to_rows && a.list) {
+      // the item's table appended to the list, one slot reservation per warp
+      for (int i0 = 0; i0 < tab_n; i0 += kGupdThreads) {
+        const int i = i0 + tid;
+        int ct = -1;
+        long long cnt = 0, hi = 0, lo = 0;
+        if (i < tab_n) entry(i, ct, cnt, hi, lo);
+        const bool valid = ct >= 0 && cnt > 0;
+        const unsigned m = __ballot_sync(kFull, valid);
+        if (!m) continue;
+        const int leader = __ffs(m) - 1;
+        unsigned long long base = 0;
+        if (lane == leader) base = atomicAdd(a.cl_n, static_cast<unsigned long long>(__popc(m)));
+        base = __shfl_sync(kFull, base, leader);
+        if (valid) {
+          const unsigned long long w = base + __popc(m & ((1u << lane) - 1u));
+          if ((long long)w < a.cl_cap) {
+            a.cl_key[w] = (static_cast<unsigned>(c) << a.cl_kb) | static_cast<unsigned>(ct);
+            a.cl_cnt[w] = cnt;
+            a.cl_hi[w] = hi;
+            a.cl_lo[w] = lo;
+          } else {
+            atomicExch(a.cl_ovf, 1);
+          }
+        }
+      }
+      __syncthreads();
+      continue;
     }
     if (to_rows) {
       for (int i = tid; i < tab_n; i += kGupdThreads) {
@@ -757,6 +796,89 @@ __global__ void __launch_bounds__(kGupdThreads) k_gselect_dense(Dims dm, long lo
       rc[2 * CC + ct] = 0;
     }
     __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------- sparse co-occurrence (large C)
+// The list of exact (c, c~) partial sums appended by k_gupdate (list mode)
+// is sorted by key = c << kb | c~ (cub radix sort over 2 kb bits), reduced
+// by key (exact int64 sums: the order of the parts does not matter, so g is
+// bit-identical to the dense rows' for any item split or rank count), and g_c
+// is selected per component from its unique entries exactly as
+// k_gselect_dense does from a dense row (update_g, estep.cpp:204-220).
+__global__ void k_cooc_heads(CoocArgs a) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += gridDim.x * blockDim.x)
+    a.head[i] = (i == 0 || a.key[i] != a.key[i - 1]) ? 1 : 0;
+}
+// after the inclusive scan of the heads: head[i] = 1 + unique index of entry i
+__global__ void k_cooc_sums(CoocArgs a) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += gridDim.x * blockDim.x) {
+    const int u = a.head[i] - 1;
+    const int src = a.perm[i];
+    if (i == 0 || a.key[i] != a.key[i - 1]) a.u_key[u] = a.key[i];
+    atomicAdd(reinterpret_cast<unsigned long long*>(a.u_cnt + u), static_cast<unsigned long long>(a.cnt[src]));
+    atomicAdd(reinterpret_cast<unsigned long long*>(a.u_hi + u), static_cast<unsigned long long>(a.hi[src]));
+    atomicAdd(reinterpret_cast<unsigned long long*>(a.u_lo + u), static_cast<unsigned long long>(a.lo[src]));
+  }
+}
+// u_off[c] = first unique entry of component >= c (binary search; nu from the scan)
+__global__ void k_cooc_offsets(CoocArgs a) {
+  const int nu = a.n > 0 ? a.head[a.n - 1] : 0;
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c <= a.dm.C; c += gridDim.x * blockDim.x) {
+    int lo = 0, hi = nu;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (static_cast<int>(a.u_key[mid] >> a.kb) < c) lo = mid + 1;
+      else hi = mid;
+    }
+    a.u_off[c] = lo;
+  }
+}
+// warp per component: G - 1 rounds of a warp argmin over (avg, c~)
+__global__ void k_cooc_select(CoocArgs a, int c0, int c1, int zero_others, int* g_new, int* gcnt_new) {
+  const int lane = threadIdx.x & 31;
+  const int wpb = blockDim.x >> 5;
+  const unsigned cmask = (1u << a.kb) - 1u;
+  for (int c = blockIdx.x * wpb + (threadIdx.x >> 5); c < a.dm.C; c += gridDim.x * wpb) {
+    if (c < c0 || c >= c1) {
+      if (zero_others) {
+        for (int i = lane; i < a.dm.G; i += 32) g_new[(int64_t)c * a.dm.G + i] = 0;
+        if (lane == 0) gcnt_new[c] = 0;
+      }
+      continue;
+    }
+    const int e0 = a.u_off[c], e1 = a.u_off[c + 1];
+    int sel[64];
+    int ns = 0;
+    for (int r = 0; r < a.dm.G - 1; ++r) {
+      KeyMin best{INFINITY, 0x7fffffff};
+      for (int e = e0 + lane; e < e1; e += 32) {
+        const long long cnt = a.u_cnt[e];
+        if (cnt <= 0) continue;
+        const int ct = static_cast<int>(a.u_key[e] & cmask);
+        bool taken = false;
+        for (int q = 0; q < ns; ++q) taken |= (sel[q] == ct);
+        if (taken) continue;
+        const KeyMin k{from_fixed(a.u_hi[e], a.u_lo[e]) / static_cast<double>(cnt), ct};
+        if (kless(k, best)) best = k;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        KeyMin oth{__shfl_xor_sync(kFull, best.v, o), __shfl_xor_sync(kFull, best.c, o)};
+        if (kless(oth, best)) best = oth;
+      }
+      if (best.c == 0x7fffffff) break;
+      sel[ns++] = best.c;
+    }
+    if (lane == 0) {
+      int out[64];
+      int m = 0;
+      out[m++] = c;
+      for (int q = 0; q < ns; ++q) out[m++] = sel[q];
+      sort_small(out, m);
+      for (int i = 0; i < a.dm.G; ++i) g_new[(int64_t)c * a.dm.G + i] = i < m ? out[i] : -1;
+      gcnt_new[c] = m;
+    }
   }
 }
 
@@ -2373,6 +2495,20 @@ cudaError_t launch_gupdate(const GupdArgs& a, int grid, cudaStream_t s) {
   const size_t smem = static_cast<size_t>(capmax) * (2 * sizeof(long long) + 2 * sizeof(int));
   cudaFuncSetAttribute(k_gupdate, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   k_gupdate<<<grid, kGupdThreads, smem, s>>>(a, capmax);
+  return cudaGetLastError();
+}
+cudaError_t launch_cooc_heads(const CoocArgs& a, cudaStream_t s) {
+  if (a.n > 0) k_cooc_heads<<<grid_for(a.n, 256, sm_count() * 8), 256, 0, s>>>(a);
+  return cudaGetLastError();
+}
+cudaError_t launch_cooc_sums(const CoocArgs& a, cudaStream_t s) {
+  if (a.n > 0) k_cooc_sums<<<grid_for(a.n, 256, sm_count() * 8), 256, 0, s>>>(a);
+  k_cooc_offsets<<<grid_for(a.dm.C + 1, 256, sm_count() * 4), 256, 0, s>>>(a);
+  return cudaGetLastError();
+}
+cudaError_t launch_cooc_select(const CoocArgs& a, int c0, int c1, int zero_others, int* g_new, int* gcnt_new,
+                               cudaStream_t s) {
+  k_cooc_select<<<grid_for(a.dm.C, 8, sm_count() * 8), 256, 0, s>>>(a, c0, c1, zero_others, g_new, gcnt_new);
   return cudaGetLastError();
 }
 cudaError_t launch_gselect_dense(const Dims& dm, long long* xc, const int* itemoff, int all,

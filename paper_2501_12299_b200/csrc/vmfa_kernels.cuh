@@ -116,6 +116,35 @@ struct GupdArgs {
   long long* dump_lo;
   unsigned long long* dump_n;
   long long dump_cap;
+  // sparse co-occurrence list (large C; SURVEY §8(e) sparse variant): every
+  // item appends its exact (c, c~) partial sums; key = c << cl_kb | c~
+  int list;
+  unsigned* cl_key;
+  long long* cl_cnt;
+  long long* cl_hi;
+  long long* cl_lo;
+  unsigned long long* cl_n;
+  long long cl_cap;
+  int cl_kb;
+  int* cl_ovf;
+};
+
+// reduced (unique-key) co-occurrence list and its selection
+struct CoocArgs {
+  Dims dm;
+  int kb;                    // key = c << kb | c~
+  const unsigned* key;       // sorted keys (n)
+  const int* perm;           // sorted position -> source entry
+  const long long* cnt;      // source entries (n)
+  const long long* hi;
+  const long long* lo;
+  int n;
+  int* head;                 // scratch (n): segment heads, then inclusive scan
+  unsigned* u_key;           // unique keys (<= n)
+  long long* u_cnt;
+  long long* u_hi;
+  long long* u_lo;
+  int* u_off;                // C + 1: unique entries of component c
 };
 
 struct StatsArgs {
@@ -186,6 +215,13 @@ cudaError_t launch_extra(const Dims& dm, const int* K, const int* g, const int* 
 cudaError_t launch_score(int mode, const ScoreArgs& a, int grid, cudaStream_t s);
 cudaError_t launch_select(const SelectArgs& a, cudaStream_t s);
 cudaError_t launch_gupdate(const GupdArgs& a, int grid, cudaStream_t s);
+// sparse co-occurrence: heads of the sorted keys, (after an inclusive scan of
+// the heads) exact per-key sums and per-component offsets, and g selection
+// for components [c0, c1) (rows outside are zeroed when zero_others)
+cudaError_t launch_cooc_heads(const CoocArgs& a, cudaStream_t s);
+cudaError_t launch_cooc_sums(const CoocArgs& a, cudaStream_t s);
+cudaError_t launch_cooc_select(const CoocArgs& a, int c0, int c1, int zero_others, int* g_new, int* gcnt_new,
+                               cudaStream_t s);
 cudaError_t launch_gselect_dense(const Dims& dm, long long* xc, const int* itemoff, int all,
                                  int* g_new, int* gcnt_new, cudaStream_t s);
 cudaError_t launch_chunks_from_off(const int* off, int C, int rows, int min1, int* chunks,

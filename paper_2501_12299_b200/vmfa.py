@@ -261,6 +261,27 @@ class Session:
         check(lib().vmfa_exchange_buffer(self._h, which, C.byref(p), C.byref(n), C.byref(dt)))
         return p.value, n.value, dt.value
 
+    def cooc_sparse(self) -> bool:
+        """vmfa_cooc_sparse: True when block 3 runs on sparse (c, c~) lists
+        (C too large for the dense table, or VMFA_COOC=sparse at creation)."""
+        v = C.c_int()
+        check(lib().vmfa_cooc_sparse(self._h, C.byref(v)))
+        return bool(v.value)
+
+    def cooc_local_list(self, world: int):
+        """vmfa_cooc_local_list: device pointers (key u32, cnt, hi, lo int64) of
+        this rank's reduced list, sorted by key, and the entry count per owner
+        rank (block ownership of components)."""
+        ps = [C.c_void_p() for _ in range(4)]
+        counts = np.zeros(world, np.int64)
+        check(lib().vmfa_cooc_local_list(self._h, world, *[C.byref(q) for q in ps], ptr(counts)))
+        return tuple(q.value for q in ps), counts
+
+    def cooc_select(self, ptrs, n: int, rank: int, world: int):
+        """vmfa_cooc_select: reduce the received lists (device pointers) and
+        select g for this rank's components into the VMFA_XCHG_G buffer."""
+        check(lib().vmfa_cooc_select(self._h, *[C.c_void_p(q) for q in ptrs], int(n), rank, world))
+
     def phase_estep_local(self, seed, it, mode=KL):
         check(lib().vmfa_phase_estep_local(self._h, seed, it, mode))
 

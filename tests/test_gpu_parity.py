@@ -604,3 +604,115 @@ def test_config5_shape_h64(oracle, gpu):
     F_or = O.truncated_free_energy(X, p_or, k2, st_g.K, threads=4)
     assert abs(F_g - F_or) <= 1e-5 * abs(F_or)
     sess.close()
+
+
+@pytest.mark.parametrize("case", [dict(N=4000, D=64, C=100, H=4, Cp=3, G=5),
+                                  dict(N=6000, D=256, C=300, H=8, Cp=5, G=10)])
+def test_sparse_cooc_matches_dense(oracle, gpu, case, monkeypatch):
+    """Block 3 on sparse (c, c~) lists (the large-C path, forced by
+    VMFA_COOC=sparse) reproduces the dense rows' g bit for bit (exact integer
+    sums), and the oracle's g outside near-ties."""
+    O, V = oracle, gpu
+    X, _ = gaussian_problem(case["N"], case["D"], max(case["C"] // 2, 2), min(case["H"], 4), seed=17)
+    C, H, Cp, G = case["C"], case["H"], case["Cp"], case["G"]
+    monkeypatch.delenv("VMFA_COOC", raising=False)
+    p, st, floor, dense = _setup(O, V, X, C, H, Cp, G)
+    monkeypatch.setenv("VMFA_COOC", "sparse")
+    _, _, _, sparse = _setup(O, V, X, C, H, Cp, G)
+    monkeypatch.delenv("VMFA_COOC", raising=False)
+    assert sparse.cooc_sparse() and not dense.cooc_sparse()
+    for it in range(3):
+        Fd, Jd = dense.variational_e_step(5, it)
+        Fs, Js = sparse.variational_e_step(5, it)
+        a, b = dense.download_state(), sparse.download_state()
+        assert Jd == Js and Fd == Fs
+        assert np.array_equal(a.K, b.K) and np.array_equal(a.labels, b.labels)
+        assert np.array_equal(a.g, b.g) and np.array_equal(a.g_count, b.g_count)
+    # against the oracle (teacher-forced step)
+    e_or, st_or, F, J, ret, st_g, k = _estep_both(O, V, sparse, X, p, st, 7, 5)
+    compare_estep(O, e_or, st_or, F, J, ret, st_g, Cp)
+    same_part = ~np.zeros(C, bool)
+    for n in np.nonzero(np.any(st_g.K != st_or.K, axis=1) | (st_g.labels != st_or.labels))[0]:
+        same_part[st_or.labels[n]] = same_part[st_g.labels[n]] = False
+    assert not compare_g(st_g.g, st_g.g_count, st_or.g, st_or.g_count, e_or.dist, same_part)
+    dense.close()
+    sparse.close()
+
+
+def test_sparse_cooc_multishard(gpu, oracle, monkeypatch):
+    """Three row shards in sparse mode, the owner-routed list exchange done on
+    the host (the all-to-all of paper_2501_12299_b200.exchange.route_lists,
+    emulated in-process), must give the single dense context's K, g and joint
+    counts bit for bit, iteration after iteration."""
+    import torch
+    from paper_2501_12299_b200.exchange import XCHG_G, XCHG_SCALARS, XCHG_STATS, device_view
+    O, V = oracle, gpu
+    X, _ = gaussian_problem(6000, 32, 20, 3, seed=23)
+    C, H, Cp, G, W = 45, 3, 3, 5, 3
+    p, st, floor, _ = O.initialize(X, C, H, Cp, G, seed=0, scale=0.1, loading_init=1)
+    monkeypatch.delenv("VMFA_COOC", raising=False)
+    single = V.Session(C, 32, H, Cp, G, X)
+    single.set_floor(floor)
+    single.upload_params(to_vmfa_params(V, p))
+    single.upload_state(to_vmfa_state(V, st))
+    monkeypatch.setenv("VMFA_COOC", "sparse")
+    N = X.shape[0]
+    shards = []
+    for r in range(W):
+        a, b = r * N // W, (r + 1) * N // W
+        s = V.Session(C, 32, H, Cp, G, X[a:b], n_offset=a, n_total=N)
+        s.set_floor(floor)
+        s.upload_params(to_vmfa_params(V, p))
+        s.upload_state(V.State(st.K[a:b].copy(), st.g.copy(), st.g_count.copy()))
+        shards.append(s)
+    monkeypatch.delenv("VMFA_COOC", raising=False)
+
+    def view(s, which):
+        ptr, n, dt = s.exchange_buffer(which)
+        return device_view(ptr, n, {0: "<i8", 1: "<f8", 2: "<i4"}[dt])
+
+    def allreduce(which):
+        vs = [view(s, which) for s in shards]
+        tot = sum(vs[1:], vs[0].clone())
+        for v in vs:
+            v.copy_(tot)
+        torch.cuda.synchronize()
+
+    def cooc_exchange():
+        sent = []
+        for s in shards:
+            (pk, pc, ph, pl), counts = s.cooc_local_list(W)
+            n = int(counts.sum())
+            arrs = [device_view(pk, n, "<i4").clone(), device_view(pc, n, "<i8").clone(),
+                    device_view(ph, n, "<i8").clone(), device_view(pl, n, "<i8").clone()]
+            sent.append((arrs, np.concatenate([[0], np.cumsum(counts)])))
+        for r, s in enumerate(shards):  # rank r receives the r-th slice of every source, in source order
+            got = [torch.cat([arrs[i][off[r]:off[r + 1]] for arrs, off in sent]) for i in range(4)]
+            n = got[0].numel()
+            torch.cuda.synchronize()
+            s.cooc_select([int(t.data_ptr()) if n else 0 for t in got], n, r, W)
+        allreduce(XCHG_G)
+
+    for it in range(3):
+        rep = single.iterate(3, it)
+        for s in shards:
+            s.phase_estep_local(3, it)
+        cooc_exchange()
+        for s in shards:
+            s.phase_estep_finish()
+            s.phase_stats_local()
+        allreduce(XCHG_STATS)
+        for s in shards:
+            s.phase_update()
+            s.phase_free_energy_local()
+        allreduce(XCHG_SCALARS)
+        Fe, J, F = shards[0].phase_scalars()
+        assert J == rep["joints"]
+        assert abs(F - rep["F"]) <= 1e-7 * abs(rep["F"])
+        st1 = single.download_state()
+        parts = [s.download_state() for s in shards]
+        assert np.array_equal(np.concatenate([q.K for q in parts]), st1.K)
+        for q in parts:
+            assert np.array_equal(q.g, st1.g) and np.array_equal(q.g_count, st1.g_count)
+    for s in shards + [single]:
+        s.close()

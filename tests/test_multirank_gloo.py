@@ -132,3 +132,68 @@ def test_fixed_point_sums_are_order_and_partition_independent():
     assert (hi, lo) == (hi2, lo2)
     exact = hi / 1024.0 + lo / 2.0 ** 50
     assert abs(exact - vals.sum()) <= 1e-9 * np.abs(vals).sum()
+
+
+def _sparse_worker(rank, port, ret):
+    """The sparse co-occurrence exchange protocol of
+    paper_2501_12299_b200.exchange (owner-routed lists via route_lists, owner
+    reduce + select, int32 all-reduce of the selected rows) on the oracle's
+    per-shard block-3 accumulators."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=WORLD)
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from oracle import oracle as O
+    from paper_2501_12299_b200.exchange import owner_ranges, route_lists
+    X, _ = gaussian_problem(1500, 8, 12, 2, seed=6)
+    C, H, Cp, G = 21, 2, 3, 4
+    p, st, floor, _ = O.initialize(X, C, H, Cp, G, seed=2, scale=0.1, loading_init=1)
+    k = O.precompute_all(p)
+    N = X.shape[0]
+    a, b = rank * N // WORLD, (rank + 1) * N // WORLD
+    shard = O.State(st.K[a:b].copy(), st.g.copy(), st.g_count.copy())
+    e = O.variational_e_step(X[a:b], p, k, shard, 4, 2, threads=1, dump_distances=True, n_offset=a)
+    dc, dct, ds, dn = e.dist
+    kb = int(C).bit_length()
+    key = (dc.astype(np.int64) << kb) | dct.astype(np.int64)
+    order = np.argsort(key, kind="stable")
+    key, cnt, ssum, cc = key[order], dn[order].astype(np.int64), ds[order], dc[order]
+    own = owner_ranges(C, WORLD)
+    counts = [int(((cc >= lo) & (cc < hi)).sum()) for lo, hi in own]
+    (rk, rn, rs), rc = route_lists([torch.from_numpy(key.astype(np.int32)), torch.from_numpy(cnt),
+                                    torch.from_numpy(ssum)], counts)
+    rk, rn, rs = rk.numpy().astype(np.int64), rn.numpy(), rs.numpy()
+    # owner: reduce by key, select g for its components (rows of others stay 0)
+    cnt_t, sum_t = np.zeros((C, C)), np.zeros((C, C))
+    np.add.at(cnt_t, (rk >> kb, rk & ((1 << kb) - 1)), rn)
+    np.add.at(sum_t, (rk >> kb, rk & ((1 << kb) - 1)), rs)
+    g_all, gc_all = select_g(cnt_t, sum_t, G)
+    lo, hi = own[rank]
+    g = np.zeros((C, G), np.int32)
+    gc = np.zeros(C, np.int32)
+    g[lo:hi], gc[lo:hi] = g_all[lo:hi], gc_all[lo:hi]
+    assert (rk >> kb).min(initial=lo) >= lo and (rk >> kb).max(initial=lo) < max(hi, lo + 1)
+    buf = torch.from_numpy(np.concatenate([g.ravel(), gc]))
+    dist.all_reduce(buf)
+    out = buf.numpy()
+    if rank == 0:
+        ret["g"], ret["gc"] = out[:C * G].reshape(C, G), out[C * G:]
+        ret["sent"], ret["recv"] = counts, rc
+    dist.destroy_process_group()
+
+
+def test_sparse_cooc_exchange_protocol(oracle):
+    """Owner-routed sparse lists reproduce the unsharded E-step's g."""
+    O = oracle
+    mgr = mp.Manager()
+    ret = mgr.dict()
+    mp.spawn(_sparse_worker, args=(_free_port(), ret), nprocs=WORLD, join=True)
+    X, _ = gaussian_problem(1500, 8, 12, 2, seed=6)
+    C, H, Cp, G = 21, 2, 3, 4
+    p, st, floor, _ = O.initialize(X, C, H, Cp, G, seed=2, scale=0.1, loading_init=1)
+    k = O.precompute_all(p)
+    O.variational_e_step(X, p, k, st, 4, 2, threads=1)
+    assert sum(ret["recv"]) > 0 and sum(ret["sent"]) > 0
+    assert np.array_equal(ret["gc"], st.g_count)
+    assert np.array_equal(ret["g"], st.g)
