@@ -375,6 +375,54 @@ int score_anchors(vmfa_ctx* x) {
   return VMFA_OK;
 }
 
+// Sparse co-occurrence lists: every block-3 item appends its exact partial
+// table (items of up to 512 points, all of them adding into the list). Set up
+// at creation with VMFA_COOC=sparse, else on the first multi-rank E-step of a
+// context without the dense rows. Capacity N (S - 1) entries (a random
+// initial state gives nearly distinct candidates), bounded by 16 GB at 60 B
+// per entry; overflow is reported, never silent.
+int enable_lists(vmfa_ctx* x) {
+  if (x->sparse) return VMFA_OK;
+  const Dims& dm = x->dm;
+  const int64_t N = dm.N;
+  const int64_t bal = std::max<int64_t>(128, N / (4 * sm_count()));
+  x->cl_kb = bits_for(static_cast<unsigned>(dm.C));
+  if (2 * x->cl_kb > 32) return fail(VMFA_ERR_UNSUPPORTED, "sparse co-occurrence keys need C < 65536");
+  const int64_t budget = (int64_t{16} << 30) / 60;
+  x->cl_cap = std::max<int64_t>(int64_t{1} << 20, std::min<int64_t>(N * (dm.stride - 1), budget));
+  const size_t L = static_cast<size_t>(x->cl_cap);
+  int r = VMFA_OK;
+  auto A = [&](auto*& p, size_t n) {
+    if (r == VMFA_OK) r = x->alloc(p, n);
+  };
+  A(x->cl_key, L);
+  A(x->cl_skey, L);
+  A(x->cu_key, L);
+  A(x->cl_cnt, L);
+  A(x->cl_hi, L);
+  A(x->cl_lo, L);
+  A(x->cu_cnt, L);
+  A(x->cu_hi, L);
+  A(x->cu_lo, L);
+  A(x->cl_iota, L);
+  A(x->cl_perm, L);
+  A(x->cu_off, static_cast<size_t>(dm.C) + 1);
+  A(x->cl_n, 1);
+  A(x->cl_ovf, 1);
+  if (r != VMFA_OK) return r;
+  size_t c1 = 0, c2 = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, c1, x->cl_key, x->cl_skey, x->cl_iota, x->cl_perm,
+                                  static_cast<int>(x->cl_cap), 0, 32, x->stream);
+  cub::DeviceScan::InclusiveSum(nullptr, c2, x->cl_iota, x->cl_perm, static_cast<int>(x->cl_cap), x->stream);
+  x->cl_tmp_bytes = std::max(c1, c2) + 256;
+  unsigned char* tmp = nullptr;
+  TRY(x->alloc(tmp, x->cl_tmp_bytes));
+  x->cl_tmp = tmp;
+  x->gupd_pts = static_cast<int>(std::min<int64_t>(bal, 512));
+  x->sparse = true;
+  return VMFA_OK;
+}
+
 // Sparse co-occurrence: reduce the n raw entries in cl_* (sorted by key,
 // exact sums per unique key) into cu_* and the per-component offsets cu_off.
 int cooc_reduce(vmfa_ctx* x, int64_t n) {
@@ -806,7 +854,6 @@ int vmfa_ctx_create(vmfa_ctx** out, int device, int C, int D, int H, int Cp, int
   const char* cooc_env = std::getenv("VMFA_COOC");
   const bool force_sparse = cooc_env && std::string(cooc_env) == "sparse";
   const bool dense_rows = !force_sparse && 3.0 * Cs * Cs * sizeof(long long) <= 8.0 * (1ull << 30);
-  x->sparse = !dense_rows;
   A(x->X, N * D);
   A(x->floor, D);
   for (double** p : {&x->pi, &x->pi2}) A(*p, Cs);
@@ -886,36 +933,16 @@ int vmfa_ctx_create(vmfa_ctx** out, int device, int C, int D, int H, int Cp, int
     A(x->xc, 3 * Cs * Cs);
     if (r == VMFA_OK) cudaMemsetAsync(x->xc, 0, 3 * Cs * Cs * sizeof(long long), x->stream);
   } else {
-    // sparse lists: every block-3 item appends its exact partial table (items
-    // of up to 512 points); capacity for 8 distinct keys per point on average
-    // (typical: a few per point; overflow is reported, never silent)
-    const int64_t bal = std::max<int64_t>(128, static_cast<int64_t>(N) / (4 * sm_count()));
-    x->gupd_pts = static_cast<int>(std::min<int64_t>(bal, 512));
-    x->cl_kb = bits_for(static_cast<unsigned>(C));
-    x->cl_cap = std::max<int64_t>(int64_t{1} << 20, static_cast<int64_t>(N) * 8);
-    if (2 * x->cl_kb > 32) r = fail(VMFA_ERR_UNSUPPORTED, "sparse co-occurrence keys need C < 65536");
-    const size_t L = static_cast<size_t>(x->cl_cap);
-    A(x->cl_key, L);
-    A(x->cl_skey, L);
-    A(x->cu_key, L);
-    A(x->cl_cnt, L);
-    A(x->cl_hi, L);
-    A(x->cl_lo, L);
-    A(x->cu_cnt, L);
-    A(x->cu_hi, L);
-    A(x->cu_lo, L);
-    A(x->cl_iota, L);
-    A(x->cl_perm, L);
-    A(x->cu_off, Cs + 1);
-    A(x->cl_n, 1);
-    A(x->cl_ovf, 1);
+    // single context without the dense rows: components are not split (the
+    // per-CTA global tables below take the keys a shared-memory hash cannot);
+    // the sparse lists are set up for the multi-rank exchange (enable_lists)
+    x->gupd_pts = 1 << 30;
   }
   A(x->cnt, Cs + 1);
   A(x->chunks, Cs + 1);
   x->gupd_grid = sm_count() * 4;
   // per-CTA dense fallback tables: only needed without the dense C x C rows
-  // (every item of the sparse mode adds into the list, so neither mode needs them)
-  const size_t gt_n = (dense_rows || x->sparse) ? 1 : static_cast<size_t>(x->gupd_grid) * Cs;
+  const size_t gt_n = dense_rows ? 1 : static_cast<size_t>(x->gupd_grid) * Cs;
   A(x->gt_cnt, gt_n);
   A(x->gt_hi, gt_n);
   A(x->gt_lo, gt_n);
@@ -952,20 +979,10 @@ int vmfa_ctx_create(vmfa_ctx** out, int device, int C, int D, int H, int Cp, int
   x->allocs.push_back(tmp);
   x->bytes += x->cub_bytes;
   x->cub_tmp = tmp;
-  if (x->sparse) {
-    size_t c1 = 0, c2 = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, c1, x->cl_key, x->cl_skey, x->cl_iota, x->cl_perm,
-                                    static_cast<int>(x->cl_cap), 0, 32, x->stream);
-    cub::DeviceScan::InclusiveSum(nullptr, c2, x->cl_iota, x->cl_perm, static_cast<int>(x->cl_cap), x->stream);
-    x->cl_tmp_bytes = std::max(c1, c2) + 256;
-    void* t2 = nullptr;
-    if (cudaMalloc(&t2, x->cl_tmp_bytes) != cudaSuccess) {
-      vmfa_ctx_destroy(x);
-      return fail(VMFA_ERR_CUDA, "cudaMalloc(co-occurrence sort temp) failed");
-    }
-    x->allocs.push_back(t2);
-    x->bytes += x->cl_tmp_bytes;
-    x->cl_tmp = t2;
+  if (force_sparse && r == VMFA_OK) r = enable_lists(x);
+  if (r != VMFA_OK) {
+    vmfa_ctx_destroy(x);
+    return r;
   }
   cudaMemsetAsync(x->scal, 0, 4 * sizeof(double), x->stream);
   cudaMemsetAsync(x->labels, 0, N * sizeof(int), x->stream);
@@ -1490,6 +1507,7 @@ int vmfa_exchange_buffer(vmfa_ctx* x, int which, void** ptr, size_t* count, int*
 
 int vmfa_phase_estep_local(vmfa_ctx* x, uint64_t seed, uint64_t iteration, int mode) {
   TRY(check_ctx(x));
+  if (!x->xc) TRY(enable_lists(x));  // multi-rank without the dense rows: sparse lists
   if (!x->xc && !x->sparse) {
     void* p;
     size_t n;
@@ -1534,7 +1552,7 @@ int vmfa_phase_scalars(vmfa_ctx* x, double* Fe, uint64_t* joints, double* F) {
 int vmfa_cooc_sparse(vmfa_ctx* x, int* sparse) {
   TRY(check_ctx(x));
   if (!sparse) return fail(VMFA_ERR_INVALID_ARGUMENT, "null output");
-  *sparse = x->sparse ? 1 : 0;
+  *sparse = (x->sparse || !x->xc) ? 1 : 0;  // (lists are set up on the first multi-rank E-step)
   return VMFA_OK;
 }
 int vmfa_cooc_local_list(vmfa_ctx* x, int world, void** key, void** cnt, void** hi, void** lo, int64_t* counts) {
