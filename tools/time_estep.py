@@ -43,6 +43,10 @@ try:
     e1.record(ext)
     e1.synchronize()
     out["iteration"] = {"ms": e0.elapsed_time(e1), "joints": r["joints"]}
+    s.profile(True)
+    s.iterate(0, 6)
+    out["iteration_phase_ms"] = {k: round(v["ms"], 3) for k, v in s.kernel_times().items() if v["ms"] > 0}
+    s.profile(False)
 except Exception as ex:  # noqa: BLE001
     out["iteration"] = {"error": str(ex)}
 print(json.dumps(out), flush=True)
