@@ -1339,15 +1339,31 @@ __global__ void __launch_bounds__(kStatsThreads, NH1 > 9 ? 1 : 2) k_stats(StatsA
 }
 
 // E for H+1 > kStatsMaxH1: item-based, full zhat per row; partial [E | -].
+// zhat = [V (x - mu); 1] by a warp per row with lanes over the latent columns
+// (coalesced V rows, x and mu broadcast); E += q zhat zhat^T in fp64 by 4x4
+// register tiles of the upper triangle (16 DFMA per 8 shared loads), the
+// lower triangle mirrored at the end.
+constexpr int kEZS = 68;  // padded zhat row (H1 <= 65 -> 17 tiles of 4)
 __global__ void __launch_bounds__(kStatsThreads) k_stats_E(StatsArgs a, const int* __restrict__ itemoff,
                                                           int rows_per_item, double* part,
                                                           int64_t part_stride) {
-  extern __shared__ __align__(16) double s_zz[];  // [kStatsBatch][H1]
-  __shared__ double s_q[kStatsBatch];
+  extern __shared__ __align__(16) double s_zz[];  // [2][kStatsBatch][kEZS]: q zhat, zhat
+  double* s_qz = s_zz;
+  double* s_z = s_zz + kStatsBatch * kEZS;
   const Dims dm = a.dm;
   const int H = dm.H, H1 = H + 1, D = dm.D;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nw = kStatsThreads / 32;
+  const int NT = (H1 + 3) / 4;  // 4-blocks per side
+  // this thread's upper-triangle tile (bi <= bj), or none
+  int bi = -1, bj = -1;
+  {
+    int t = tid;
+    for (int i = 0; i < NT && bi < 0; ++i) {
+      if (t < NT - i) bi = i, bj = i + t;
+      else t -= NT - i;
+    }
+  }
   const int total = __ldg(itemoff + dm.C);
   for (int item = blockIdx.x; item < total; item += gridDim.x) {
     const int c = find_item(itemoff, dm.C, item);
@@ -1355,49 +1371,63 @@ __global__ void __launch_bounds__(kStatsThreads) k_stats_E(StatsArgs a, const in
     const int r1 = min(a.off[c + 1], r0 + rows_per_item);
     const float* Vc = a.V32 + (int64_t)c * D * H;
     const float* mc = a.mu32 + (int64_t)c * D;
-    double* pe = part + (int64_t)item * part_stride;
-    for (int idx0 = 0; idx0 < H1 * H1; idx0 += kStatsThreads * 9) {
-      double accE[9];
+    double acc[4][4];
 #pragma unroll
-      for (int k = 0; k < 9; ++k) accE[k] = 0.0;
-      for (int b0 = r0; b0 < r1; b0 += kStatsBatch) {
-        const int nb = min(kStatsBatch, r1 - b0);
-        for (int r = warp; r < nb; r += nw) {
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+    for (int b0 = r0; b0 < r1; b0 += kStatsBatch) {
+      const int nb = min(kStatsBatch, r1 - b0);
+      __syncthreads();  // previous batch's tiles done with s_qz / s_z
+      for (int r = warp; r < kStatsBatch; r += nw) {
+        double q = 0.0;
+        float z0 = 0.f, z1 = 0.f;  // columns lane, lane + 32
+        if (r < nb) {
           const int e = a.ent[b0 + r];
-          const int n = e / dm.Cp;
-          const float* x = a.X + (int64_t)n * D;
-          for (int h = 0; h < H; ++h) {
-            float v = 0.f;
-            for (int d = lane; d < D; d += 32)
-              v = fmaf(__ldg(Vc + (int64_t)d * H + h), __ldg(x + d) - __ldg(mc + d), v);
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
-            if (lane == 0) s_zz[r * H1 + h] = v;
-          }
-          if (lane == 0) {
-            s_zz[r * H1 + H] = 1.0;
-            s_q[r] = a.resp[e];
+          const float* x = a.X + (int64_t)(e / dm.Cp) * D;
+          q = a.resp[e];
+          const bool h0 = lane < H, h1 = lane + 32 < H;
+          for (int d = 0; d < D; ++d) {
+            const float v = __ldg(x + d) - __ldg(mc + d);
+            const float* vr = Vc + (int64_t)d * H;
+            if (h0) z0 = fmaf(__ldg(vr + lane), v, z0);
+            if (h1) z1 = fmaf(__ldg(vr + lane + 32), v, z1);
           }
         }
-        __syncthreads();
+        for (int h = lane; h < kEZS; h += 32) {
+          const double z = r >= nb ? 0.0 : (h < H ? static_cast<double>(h < 32 ? z0 : z1)
+                                                  : (h == H ? 1.0 : 0.0));
+          s_z[r * kEZS + h] = z;
+          s_qz[r * kEZS + h] = q * z;
+        }
+      }
+      __syncthreads();
+      if (bi >= 0) {
         for (int r = 0; r < nb; ++r) {
-          const double q = s_q[r];
+          const double* qr = s_qz + r * kEZS + 4 * bi;
+          const double* zr = s_z + r * kEZS + 4 * bj;
+          const double q0 = qr[0], q1 = qr[1], q2 = qr[2], q3 = qr[3];
+          const double z0 = zr[0], z1 = zr[1], z2 = zr[2], z3 = zr[3];
+          const double qv[4] = {q0, q1, q2, q3}, zv[4] = {z0, z1, z2, z3};
 #pragma unroll
-          for (int k = 0; k < 9; ++k) {
-            const int idx = idx0 + tid + k * kStatsThreads;
-            if (idx < H1 * H1) {
-              const int i = idx % H1, j = idx / H1;
-              accE[k] = fma(q * s_zz[r * H1 + i], s_zz[r * H1 + j], accE[k]);
-            }
-          }
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[i][j] = fma(qv[i], zv[j], acc[i][j]);
         }
-        __syncthreads();
       }
+    }
+    double* pe = part + (int64_t)item * part_stride;
+    if (bi >= 0) {
 #pragma unroll
-      for (int k = 0; k < 9; ++k) {
-        const int idx = idx0 + tid + k * kStatsThreads;
-        if (idx < H1 * H1) pe[idx] = accE[k];
-      }
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int ii = 4 * bi + i, jj = 4 * bj + j;
+          if (ii >= H1 || jj >= H1) continue;
+          if (bi == bj && ii > jj) continue;  // the diagonal tile's lower half comes from its upper
+          pe[jj * H1 + ii] = acc[i][j];
+          pe[ii * H1 + jj] = acc[i][j];
+        }
     }
   }
 }
@@ -2628,7 +2658,7 @@ cudaError_t launch_stats(const StatsArgs& a, const int* itemoff, int rows_per_it
                                                   a.Nc, a.E, a.Y, a.sq);
   }
   if (H1 > nh1) {
-    const size_t smem = static_cast<size_t>(kStatsBatch) * H1 * sizeof(double);
+    const size_t smem = 2 * static_cast<size_t>(kStatsBatch) * kEZS * sizeof(double);
     cudaFuncSetAttribute(k_stats_E, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     k_stats_E<<<grid, kStatsThreads, smem, s>>>(a, itemoff, rows_per_item, part, ps);
     k_stats_reduce<<<sm_count() * 8, 256, 0, s>>>(a.dm, itemoff, part, ps, 1, 0, nh1, 1, a.Nc, a.E, a.Y, a.sq);
