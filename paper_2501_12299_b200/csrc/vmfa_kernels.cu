@@ -2092,6 +2092,7 @@ __global__ void __launch_bounds__(1024) k_renorm(Dims dm, double* pi, unsigned l
 // Sigma_z = L^-1, log|Sigma| = 2 sum log R_hh + sum log psi, log pi; fp32
 // scoring rows W = U R^-T (| W^T v |^2 = (U^T v).(V v)), V32 = R^-T R^-1 U^T.
 constexpr int kPreFastH = 8;  // precompute's register-blocked M for H <= 8
+constexpr int kPreDC = 32;    // dimensions per staged chunk of the general-H path
 
 __global__ void __launch_bounds__(128) k_precompute(PrecompArgs a) {
   extern __shared__ __align__(16) double s_pre[];
@@ -2102,6 +2103,10 @@ __global__ void __launch_bounds__(128) k_precompute(PrecompArgs a) {
   const int H = dm.H, D = dm.D;
   double* sL = s_pre;
   double* sR = s_pre + H * H;
+  // general H: staged chunks of kPreDC dimensions (H4 x kPreDC each)
+  const int H4 = (H + 3) & ~3;
+  double* sA = s_pre + 2 * H * H;
+  double* sB = sA + H4 * kPreDC;
   const int tid = threadIdx.x;
   for (int c = blockIdx.x; c < dm.C; c += gridDim.x) {
     const double* lam = a.lam + (int64_t)c * D * H;
@@ -2147,12 +2152,53 @@ __global__ void __launch_bounds__(128) k_precompute(PrecompArgs a) {
         sL[jj * H + ii] = v;
       }
     } else {
-      for (int p = tid; p < H * H; p += blockDim.x) {
-        const int i = p % H, j = p / H;
-        if (i > j) continue;
-        double s = 0.0;
-        for (int d = 0; d < D; ++d) s += lam[(int64_t)i * D + d] * (lam[(int64_t)j * D + d] / psi[d]);
-        sL[j * H + i] = s;
+      // 4x4 register tiles of the upper triangle over staged chunks of
+      // Lambda and Psi^-1 Lambda (rounds of 128 tiles)
+      const int NT = H4 / 4, ntile = NT * (NT + 1) / 2;
+      for (int t0 = 0; t0 < ntile; t0 += blockDim.x) {
+        int bi = -1, bj = -1;
+        for (int t = t0 + tid, i = 0; i < NT && bi < 0 && t0 + tid < ntile; ++i) {
+          if (t < NT - i) bi = i, bj = i + t;
+          else t -= NT - i;
+        }
+        double acc[4][4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+        for (int d0 = 0; d0 < D; d0 += kPreDC) {
+          __syncthreads();
+          for (int i = tid; i < H4 * kPreDC; i += blockDim.x) {
+            const int h = i / kPreDC, d = d0 + (i - h * kPreDC);
+            const double v = (h < H && d < D) ? lam[(int64_t)h * D + d] : 0.0;
+            sA[i] = v;
+            sB[i] = d < D ? v * (1.0 / psi[d]) : 0.0;
+          }
+          __syncthreads();
+          if (bi >= 0) {
+            for (int dd = 0; dd < kPreDC; ++dd) {
+              double av[4], bv[4];
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                av[k] = sA[(4 * bi + k) * kPreDC + dd];
+                bv[k] = sB[(4 * bj + k) * kPreDC + dd];
+              }
+#pragma unroll
+              for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
+            }
+          }
+        }
+        if (bi >= 0) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int ii = 4 * bi + i, jj = 4 * bj + j;
+              if (ii < H && jj < H && ii <= jj) sL[jj * H + ii] = acc[i][j];
+            }
+        }
       }
     }
     __syncthreads();
@@ -2257,22 +2303,81 @@ __global__ void __launch_bounds__(128) k_precompute(PrecompArgs a) {
           if (h < H) a.V32[((int64_t)c * D + d) * H + h] = static_cast<float>(u[h]);
       }
     } else {
-      for (int d = tid; d < D; d += blockDim.x) {
-        double u[kMaxH1];
-        const double ip = 1.0 / psi[d];
-        for (int h = 0; h < H; ++h) u[h] = lam[(int64_t)h * D + d] * ip;  // U = Psi^-1 Lambda
-        for (int i = 0; i < H; ++i) {  // forward: w = R^-1 u
-          double t = u[i];
-          for (int k = 0; k < i; ++k) t -= sR[i * H + k] * u[k];
-          u[i] = t / sR[i * H + i];
+      // W^T = R^-1 U^T and V = Sigma_z U^T (= L^-1 U^T, model.cpp:64) as
+      // register-tiled products over staged chunks of U^T = (Psi^-1 Lambda)^T:
+      // R^-1 (lower, one column per thread) into sL, Sigma_z into sR
+      __syncthreads();
+      for (int p = tid; p < H * H; p += blockDim.x) sL[p] = 0.0;
+      __syncthreads();
+      for (int j = tid; j < H; j += blockDim.x)
+        for (int i = j; i < H; ++i) {
+          double t = i == j ? 1.0 : 0.0;
+          for (int k = j; k < i; ++k) t -= sR[i * H + k] * sL[k * H + j];
+          sL[i * H + j] = t / sR[i * H + i];
         }
-        write_rows(d, u, ip);
-        for (int i = H - 1; i >= 0; --i) {  // backward: v = R^-T w => V column d
-          double t = u[i];
-          for (int k = i + 1; k < H; ++k) t -= sR[k * H + i] * u[k];
-          u[i] = t / sR[i * H + i];
+      __syncthreads();
+      for (int p = tid; p < H * H; p += blockDim.x) sR[p] = a.Sz[(int64_t)c * H * H + p];
+      const int TD = kPreDC / 4, ntile = (H4 / 4) * TD;
+      for (int d0 = 0; d0 < D; d0 += kPreDC) {
+        __syncthreads();
+        for (int i = tid; i < H4 * kPreDC; i += blockDim.x) {
+          const int h = i / kPreDC, d = d0 + (i - h * kPreDC);
+          sA[i] = (h < H && d < D) ? lam[(int64_t)h * D + d] * (1.0 / psi[d]) : 0.0;  // U = Psi^-1 Lambda
         }
-        for (int h = 0; h < H; ++h) a.V32[((int64_t)c * D + d) * H + h] = static_cast<float>(u[h]);
+        __syncthreads();
+        for (int t = tid; t < ntile; t += blockDim.x) {
+          const int h0 = 4 * (t / TD), dd0 = 4 * (t - (t / TD) * TD);
+          double w[4][4], v[4][4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) w[i][j] = v[i][j] = 0.0;
+          for (int k = 0; k < H; ++k) {
+            double ri[4], si[4], uk[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const int h = h0 + i;
+              ri[i] = (h < H && k <= h) ? sL[h * H + k] : 0.0;
+              si[i] = h < H ? sR[h * H + k] : 0.0;  // Sigma_z (symmetric): row h
+              uk[i] = sA[k * kPreDC + dd0 + i];
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                w[i][j] = fma(ri[i], uk[j], w[i][j]);
+                v[i][j] = fma(si[i], uk[j], v[i][j]);
+              }
+          }
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int d = d0 + dd0 + j;
+            if (d >= D) continue;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const int h = h0 + i;
+              if (h >= H) continue;
+              a.P[((int64_t)c * D + d) * HP + h] = static_cast<float>(w[i][j]);
+              a.WT[((int64_t)c * a.Hp + h) * D + d] = static_cast<float>(w[i][j]);
+              a.V32[((int64_t)c * D + d) * H + h] = static_cast<float>(v[i][j]);
+            }
+          }
+        }
+        // the per-dimension tail of the rows: zero padding, mean, Psi^-1
+        for (int dd = tid; dd < kPreDC; dd += blockDim.x) {
+          const int d = d0 + dd;
+          if (d >= D) continue;
+          const double ip = 1.0 / psi[d];
+          float* row = a.P + ((int64_t)c * D + d) * HP;
+          for (int h = H; h < Hc; ++h) row[h] = 0.f;
+          for (int h = H; h < a.Hp; ++h) a.WT[((int64_t)c * a.Hp + h) * D + d] = 0.f;
+          a.ipsi32[(int64_t)c * D + d] = static_cast<float>(ip);
+          row[Hc] = static_cast<float>(a.mu[(int64_t)c * D + d]);
+          row[Hc + 1] = static_cast<float>(ip);
+          row[Hc + 2] = 0.f;
+          row[Hc + 3] = 0.f;
+          a.mu32[(int64_t)c * D + d] = static_cast<float>(a.mu[(int64_t)c * D + d]);
+        }
       }
     }
     __syncthreads();
@@ -2694,7 +2799,9 @@ cudaError_t launch_renorm(const Dims& dm, double* pi, unsigned long long* status
   return cudaGetLastError();
 }
 cudaError_t launch_precompute(const PrecompArgs& a, cudaStream_t s) {
-  const size_t smem = 2 * static_cast<size_t>(a.dm.H) * a.dm.H * sizeof(double);
+  const size_t H4 = (static_cast<size_t>(a.dm.H) + 3) & ~size_t{3};
+  const size_t smem = (2 * static_cast<size_t>(a.dm.H) * a.dm.H +
+                       (a.dm.H > kPreFastH ? 2 * H4 * kPreDC : 0)) * sizeof(double);
   cudaFuncSetAttribute(k_precompute, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   k_precompute<<<min(a.dm.C, sm_count() * 8), 128, smem, s>>>(a);
   return cudaGetLastError();
