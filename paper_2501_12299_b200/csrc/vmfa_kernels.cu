@@ -1495,28 +1495,40 @@ __device__ __forceinline__ void mma3c(float (&acc)[4], const float (&ah)[4], con
   mma_tf32(acc, h, __float_as_uint(b0h), __float_as_uint(b1h));
 }
 
-template <int NTH, int NTW>
-__global__ void __launch_bounds__(kStatsThreads, 2) k_stats_mma(StatsArgs a, const int* __restrict__ itemoff,
+// BIG (D > 512 or H + 1 = 17, e.g. config 3: D = 784, H = 16): 16-row
+// batches, one CTA per SM (up to 255 registers: 13-16 dimension tiles per
+// warp), V fragments split on the fly (the pre-split table would not fit next
+// to the row ring), fresh accumulators per k-step, and with H + 1 = 17 the
+// constant column of [zhat; 1] (Y_v[:, H] = sum q v) accumulated by FFMA next
+// to sq_v while the m16 tile holds the 16 latent columns.
+template <int NTH, int NTW, bool BIG>
+__global__ void __launch_bounds__(kStatsThreads, BIG ? 1 : 2) k_stats_mma(StatsArgs a, const int* __restrict__ itemoff,
                                                                int rows_per_item, int nh1, double* part,
                                                                int64_t part_stride, int nbuf) {
-  // smem (dynamic): s_x [nbuf][B][XS] | s_Vb [KS][NTH][32] float4 | s_mu [D]
+  constexpr int BR = BIG ? 16 : kSmBatch;  // rows per batch
+  constexpr int MT = BR / 16;              // phase (i) m-tiles
+  constexpr int KP = 8 / MT;               // phase (i) K parts
+  // smem (dynamic): s_x [nbuf][BR][XS] | s_Vb [KS][NTH][32] float4 (BIG: float2) | s_mu [D]
   extern __shared__ __align__(16) float s_x[];
-  __shared__ __align__(16) float s_pz[4][kSmBatch][16];  // phase (i) K-quarter partials
-  __shared__ __align__(16) float4 s_Af[4][32][2];         // phase (ii) A fragments (hi, lo) per k-step, lane
-  __shared__ double s_zd[kSmBatch * kSmZD];               // [zhat; 1] rows in fp64 (E)
+  __shared__ __align__(16) float s_pz[KP][BR][16];  // phase (i) K-part partials
+  __shared__ __align__(16) float4 s_Af[BR / 8][32][2];  // phase (ii) A fragments (hi, lo) per k-step, lane
+  __shared__ double s_zd[BR * kSmZD];  // [zhat; 1] rows in fp64 (E)
   __shared__ double s_red[kStatsThreads / 32];
   __shared__ double s_accE[kStatsThreads];
   __shared__ uint64_t s_xbar[kStatsMaxBuf];
   __shared__ int s_eall[kStatsMaxRows];
   __shared__ double s_qall[kStatsMaxRows];
   __shared__ int s_item;
-  __shared__ float s_qb[kSmBatch];  // the batch's responsibilities (fp32; 0 past the item end)
+  __shared__ float s_qb[BR];  // the batch's responsibilities (fp32; 0 past the item end)
   const Dims dm = a.dm;
   const int H = dm.H, H1 = H + 1, D = dm.D;
   const int XS = D + 4;  // row stride: XS % 32 == 4 for D % 32 == 0 (conflict-free phase i)
   const int KS = D / 8;  // k-steps of phase (i) / dimension tiles of phase (ii)
-  float4* s_Vb = reinterpret_cast<float4*>(s_x + (int64_t)nbuf * kSmBatch * XS);
-  float* s_mu = reinterpret_cast<float*>(s_Vb + (int64_t)KS * NTH * 32);
+  float4* s_Vb = reinterpret_cast<float4*>(s_x + (int64_t)nbuf * BR * XS);
+  float2* s_Vu = reinterpret_cast<float2*>(s_Vb);  // BIG: unsplit (b0, b1)
+  float* s_mu = BIG ? reinterpret_cast<float*>(s_Vu + (int64_t)KS * NTH * 32)
+                    : reinterpret_cast<float*>(s_Vb + (int64_t)KS * NTH * 32);
+  const bool cfma = H1 > 16;  // constant column by FFMA (BIG only)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int gid = lane >> 2, tig = lane & 3;
   // E: thread = (upper-triangle entry, row group)
@@ -1531,15 +1543,15 @@ __global__ void __launch_bounds__(kStatsThreads, 2) k_stats_mma(StatsArgs a, con
       else t -= H1 - i;
     }
   }
-  // phase (i): warp = (m-tile, K quarter)
-  const int pm = warp & 1, pq = warp >> 1;
-  const int ks0 = pq * KS / 4, ks1 = (pq + 1) * KS / 4;
+  // phase (i): warp = (m-tile, K part)
+  const int pm = warp % MT, pq = warp / MT;
+  const int ks0 = pq * KS / KP, ks1 = (pq + 1) * KS / KP;
   const int total = __ldg(itemoff + dm.C);
   if (tid == 0)
     for (int i = 0; i < kStatsMaxBuf; ++i) xbar_init(&s_xbar[i], 1);
   // rows past an item's end keep a previous batch's (finite) rows and get q = 0;
   // zeroed once so the first batches never see uninitialised (NaN) words
-  for (int i = tid; i < nbuf * kSmBatch * XS; i += kStatsThreads) s_x[i] = 0.f;
+  for (int i = tid; i < nbuf * BR * XS; i += kStatsThreads) s_x[i] = 0.f;
   __syncthreads();
   uint32_t xpar = 0u;
   auto next_item = [&](int cur) -> int {
@@ -1575,8 +1587,12 @@ __global__ void __launch_bounds__(kStatsThreads, 2) k_stats_mma(StatsArgs a, con
       const int h = 8 * nt + (l >> 2), d = 8 * ks + (l & 3);
       const float b0 = h < H ? __ldg(Vc + (int64_t)d * H + h) : 0.f;
       const float b1 = h < H ? __ldg(Vc + (int64_t)(d + 4) * H + h) : 0.f;
-      const float b0h = tf32_hi(b0), b1h = tf32_hi(b1);
-      s_Vb[i] = make_float4(b0h, b1h, b0 - b0h, b1 - b1h);
+      if (BIG) {
+        s_Vu[i] = make_float2(b0, b1);
+      } else {
+        const float b0h = tf32_hi(b0), b1h = tf32_hi(b1);
+        s_Vb[i] = make_float4(b0h, b1h, b0 - b0h, b1 - b1h);
+      }
     }
     for (int d = tid; d < D; d += kStatsThreads) s_mu[d] = __ldg(a.mu32 + (int64_t)c * D + d);
     __syncthreads();
@@ -1584,34 +1600,36 @@ __global__ void __launch_bounds__(kStatsThreads, 2) k_stats_mma(StatsArgs a, con
 #pragma unroll
     for (int w = 0; w < kStatsThreads / 32; ++w) qmax = fmax(qmax, s_red[w]);
     const double qdiv = qmax > 0.0 ? qmax : 1.0;
-    const int nbat = (nr + kSmBatch - 1) / kSmBatch;
-    for (int i = tid; i < nbat * kSmBatch; i += kStatsThreads) s_qall[i] = i < nr ? s_qall[i] / qdiv : 0.0;
+    const int nbat = (nr + BR - 1) / BR;
+    for (int i = tid; i < nbat * BR; i += kStatsThreads) s_qall[i] = i < nr ? s_qall[i] / qdiv : 0.0;
     if (ei >= 0) s_accE[tid] = 0.0;
     float acc[NTW][4];
-    double sqd[NTW];  // sq_v: fp32 over a batch's 8 rows per lane, then fp64
+    double sqd[NTW];  // sq_v: fp32 over a batch's rows per lane, then fp64
+    double yhd[NTW];  // Y_v[:, H] when cfma
     float muj[NTW];
 #pragma unroll
     for (int i = 0; i < NTW; ++i) {
       sqd[i] = 0.0;
+      yhd[i] = 0.0;
       acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
       muj[i] = s_mu[8 * min(warp + 8 * i, KS - 1) + gid];
     }
     auto issue_rows = [&](int b, int buf) {
-      float* dst = s_x + (int64_t)buf * kSmBatch * XS;
-      const int nb = min(kSmBatch, nr - b * kSmBatch);
-      const int* eb = s_eall + b * kSmBatch;
+      float* dst = s_x + (int64_t)buf * BR * XS;
+      const int nb = min(BR, nr - b * BR);
+      const int* eb = s_eall + b * BR;
       if (tid == 0) xbar_expect(&s_xbar[buf], static_cast<uint32_t>(nb) * D * 4u);
-      if (lane < kSmBatch / (kStatsThreads / 32)) {
-        const int r = warp * (kSmBatch / (kStatsThreads / 32)) + lane;
+      if (lane < BR / (kStatsThreads / 32)) {
+        const int r = warp * (BR / (kStatsThreads / 32)) + lane;
         if (r < nb) bulk_row(smem_addr(dst + (int64_t)r * XS), a.X + (int64_t)eb[r] * D, D * 4u, &s_xbar[buf]);
       }
     };
     for (int b = 0; b < min(nbuf - 1, nbat); ++b) issue_rows(b, b);
     for (int bi = 0, buf = 0; bi < nbat; ++bi, buf = buf + 1 == nbuf ? 0 : buf + 1) {
-      const int nb = min(kSmBatch, nr - bi * kSmBatch);
+      const int nb = min(BR, nr - bi * BR);
       xbar_wait(&s_xbar[buf], (xpar >> buf) & 1u);
       xpar ^= 1u << buf;
-      const float* xb = s_x + (int64_t)buf * kSmBatch * XS;
+      const float* xb = s_x + (int64_t)buf * BR * XS;
       // (i) Z partial over this warp's K quarter: A = v rows 16pm.., B = V^T
       {
         // three independent chains (lo*hi, hi*lo, hi*hi) hide the HMMA latency
@@ -1635,7 +1653,14 @@ __global__ void __launch_bounds__(kStatsThreads, 2) k_stats_mma(StatsArgs a, con
           }
 #pragma unroll
           for (int nt = 0; nt < NTH; ++nt) {
-            const float4 bv = s_Vb[((int64_t)ks * NTH + nt) * 32 + lane];
+            float4 bv;
+            if (BIG) {
+              const float2 u = s_Vu[((int64_t)ks * NTH + nt) * 32 + lane];
+              const float b0h = tf32_hi(u.x), b1h = tf32_hi(u.y);
+              bv = make_float4(b0h, b1h, u.x - b0h, u.y - b1h);
+            } else {
+              bv = s_Vb[((int64_t)ks * NTH + nt) * 32 + lane];
+            }
             const uint32_t h[4] = {__float_as_uint(ah[0]), __float_as_uint(ah[1]), __float_as_uint(ah[2]),
                                    __float_as_uint(ah[3])};
             const uint32_t l[4] = {__float_as_uint(al[0]), __float_as_uint(al[1]), __float_as_uint(al[2]),
@@ -1660,19 +1685,23 @@ __global__ void __launch_bounds__(kStatsThreads, 2) k_stats_mma(StatsArgs a, con
       __syncthreads();
       if (nbuf >= 2 && bi + nbuf - 1 < nbat) issue_rows(bi + nbuf - 1, buf == 0 ? nbuf - 1 : buf - 1);
       // combine: zhat rows (fp64 for E) and the q-scaled phase (ii) A fragments
-      const double* s_q = s_qall + bi * kSmBatch;
-      {
+      const double* s_q = s_qall + bi * BR;
+      if (tid < BR * 8) {
         // thread = (k-step, lane, row half): row r, columns gid and gid + 8
         const int ks = tid >> 6, ln = (tid >> 1) & 31, up = tid & 1;
         const int r = 8 * ks + (ln & 3) + 4 * up, h0 = ln >> 2, h1 = h0 + 8;
         auto zval = [&](int h) -> float {
           if (r >= nb || h > H) return 0.f;
           if (h == H) return 1.f;
-          return s_pz[0][r][h] + s_pz[1][r][h] + s_pz[2][r][h] + s_pz[3][r][h];
+          float z = 0.f;
+#pragma unroll
+          for (int k = 0; k < KP; ++k) z += s_pz[k][r][h];
+          return z;
         };
         const float z0 = zval(h0), z1 = zval(h1);
         if (h0 < H1) s_zd[r * kSmZD + h0] = z0;
         if (h1 < H1) s_zd[r * kSmZD + h1] = z1;
+        if (cfma && h0 == 0) s_zd[r * kSmZD + H] = r < nb ? 1.0 : 0.0;
         const float qf = static_cast<float>(s_q[r]);
         if (h0 == 0) s_qb[r] = qf;
         const float qz0 = qf * z0, qz1 = qf * z1;
@@ -1689,16 +1718,16 @@ __global__ void __launch_bounds__(kStatsThreads, 2) k_stats_mma(StatsArgs a, con
       // (ii) Y_v^T += (Q zhat)^T v over the batch's 4 k-steps (rows past nb:
       // q = 0 and A = 0, stale finite v), chained per batch, then one FADD
       // per accumulator into the item's sums
-      float sqa[NTW];
-      float accb[NTW][4], accl[NTW][4];  // hi*hi chain and the two correction products' chain
+      float sqa[NTW], yha[NTW];
+      float accb[BIG ? 1 : NTW][4], accl[BIG ? 1 : NTW][4];  // hi*hi chain and the correction products' chain
 #pragma unroll
-      for (int i = 0; i < NTW; ++i) {
-        sqa[i] = 0.f;
+      for (int i = 0; i < NTW; ++i) sqa[i] = yha[i] = 0.f;
+#pragma unroll
+      for (int i = 0; i < (BIG ? 1 : NTW); ++i)
 #pragma unroll
         for (int k = 0; k < 4; ++k) accb[i][k] = accl[i][k] = 0.f;
-      }
 #pragma unroll
-      for (int ks = 0; ks < kSmBatch / 8; ++ks) {
+      for (int ks = 0; ks < BR / 8; ++ks) {
         const float4 Ah = s_Af[ks][lane][0], Al = s_Af[ks][lane][1];
         const float ah[4] = {Ah.x, Ah.y, Ah.z, Ah.w}, al[4] = {Al.x, Al.y, Al.z, Al.w};
         const int ra = 8 * ks + tig, rb = ra + 4;
@@ -1711,23 +1740,33 @@ __global__ void __launch_bounds__(kStatsThreads, 2) k_stats_mma(StatsArgs a, con
           const int j = min(warp + 8 * i, KS - 1);
           const float va = xa[8 * j] - muj[i];
           const float vb = xb2[8 * j] - muj[i];
-          sqa[i] = fmaf(qa * va, va, sqa[i]);
-          sqa[i] = fmaf(qb * vb, vb, sqa[i]);
+          const float qva = qa * va, qvb = qb * vb;
+          sqa[i] = fmaf(qva, va, sqa[i]);
+          sqa[i] = fmaf(qvb, vb, sqa[i]);
+          if (BIG) yha[i] += qva + qvb;
           const float vah = tf32_hi(va), vbh = tf32_hi(vb);
-          const uint32_t h[4] = {__float_as_uint(ah[0]), __float_as_uint(ah[1]), __float_as_uint(ah[2]),
-                                 __float_as_uint(ah[3])};
-          const uint32_t l[4] = {__float_as_uint(al[0]), __float_as_uint(al[1]), __float_as_uint(al[2]),
-                                 __float_as_uint(al[3])};
-          mma_tf32(accl[i], l, __float_as_uint(vah), __float_as_uint(vbh));
-          mma_tf32(accl[i], h, __float_as_uint(va - vah), __float_as_uint(vb - vbh));
-          mma_tf32(accb[i], h, __float_as_uint(vah), __float_as_uint(vbh));
+          if (BIG) {
+            mma3(acc[i], ah, al, vah, vbh, va - vah, vb - vbh);
+          } else {
+            const int ii = BIG ? 0 : i;
+            const uint32_t h[4] = {__float_as_uint(ah[0]), __float_as_uint(ah[1]), __float_as_uint(ah[2]),
+                                   __float_as_uint(ah[3])};
+            const uint32_t l[4] = {__float_as_uint(al[0]), __float_as_uint(al[1]), __float_as_uint(al[2]),
+                                   __float_as_uint(al[3])};
+            mma_tf32(accl[ii], l, __float_as_uint(vah), __float_as_uint(vbh));
+            mma_tf32(accl[ii], h, __float_as_uint(va - vah), __float_as_uint(vb - vbh));
+            mma_tf32(accb[ii], h, __float_as_uint(vah), __float_as_uint(vbh));
+          }
         }
       }
 #pragma unroll
       for (int i = 0; i < NTW; ++i) {
         sqd[i] += sqa[i];
+        if (BIG) yhd[i] += yha[i];
+        if (!BIG) {
 #pragma unroll
-        for (int k = 0; k < 4; ++k) acc[i][k] += accl[i][k] + accb[i][k];
+          for (int k = 0; k < 4; ++k) acc[i][k] += accl[BIG ? 0 : i][k] + accb[BIG ? 0 : i][k];
+        }
       }
       if (nbuf == 1) __syncthreads();
     }
@@ -1744,9 +1783,13 @@ __global__ void __launch_bounds__(kStatsThreads, 2) k_stats_mma(StatsArgs a, con
 #pragma unroll
     for (int i = 0; i < NTW; ++i) {
       const int j = warp + 8 * i;
-      double s = sqd[i];
+      double s = sqd[i], yh = yhd[i];
       s += __shfl_xor_sync(kFull, s, 1);
       s += __shfl_xor_sync(kFull, s, 2);
+      if (BIG) {
+        yh += __shfl_xor_sync(kFull, yh, 1);
+        yh += __shfl_xor_sync(kFull, yh, 2);
+      }
       if (j >= KS) continue;
       const int d = 8 * j + 2 * tig;
 #pragma unroll
@@ -1761,6 +1804,11 @@ __global__ void __launch_bounds__(kStatsThreads, 2) k_stats_mma(StatsArgs a, con
         const double v = s * qmax;
         if (direct) a.sq[(int64_t)c * D + 8 * j + gid] = v;
         else pp[(int64_t)nh1 * D + 8 * j + gid] = v;
+        if (cfma) {  // Y_v[:, H] (the constant column)
+          const double y = yh * qmax;
+          if (direct) a.Y[((int64_t)c * H1 + H) * D + 8 * j + gid] = y;
+          else pp[(int64_t)H * D + 8 * j + gid] = y;
+        }
       }
     }
   }
@@ -2691,14 +2739,17 @@ int64_t stats_part_stride(const Dims& dm) {
   const int nh1 = H1 <= 5 ? 5 : (H1 <= 9 ? 9 : kStatsMaxH1);
   return static_cast<int64_t>(nh1) * dm.D + dm.D + static_cast<int64_t>(H1) * H1 + 1;
 }
-// the tensor-core statistics kernel covers H + 1 <= 16 (one m16 tile of
-// [zhat; 1]) and D % 8 == 0, D <= 512 (<= 8 dimension tiles per warp);
+// the tensor-core statistics kernel covers H + 1 <= 17 (one m16 tile of
+// [zhat; 1], the 17th column by FFMA) and D % 8 == 0, D <= 1024;
 // VMFA_STATS=ffma selects k_stats (the cross-check in the parity tests)
 bool stats_mma_ok(const Dims& dm) {
   const char* v = std::getenv("VMFA_STATS");
   const bool ffma = v && std::strcmp(v, "ffma") == 0;
-  return !ffma && dm.H + 1 <= 16 && dm.D % 8 == 0 && dm.D <= 512;
+  return !ffma && dm.D % 8 == 0 && ((dm.H + 1 <= 16 && dm.D <= 512) || (dm.H + 1 <= 17 && dm.D <= 1024));
 }
+// BIG variant: 16-row batches, one CTA per SM (D > 256: the 2-CTA variant
+// would spill its 8 dimension tiles per warp; or H + 1 = 17)
+static bool stats_mma_big(const Dims& dm) { return dm.D > 256 || dm.H + 1 > 16; }
 cudaError_t launch_stats(const StatsArgs& a, const int* itemoff, int rows_per_item, double* part,
                          cudaStream_t s) {
   if (a.dm.D > 4 * kStatsThreads) return cudaErrorInvalidValue;
@@ -2711,12 +2762,14 @@ cudaError_t launch_stats(const StatsArgs& a, const int* itemoff, int rows_per_it
       cudaError_t e = cudaMemsetAsync(a.qctr, 0, sizeof(int), s);
       if (e != cudaSuccess) return e;
     }
-    const int KS = a.dm.D / 8, NTH = a.dm.H > 8 ? 2 : 1;
+    const bool big = stats_mma_big(a.dm);
+    const int KS = a.dm.D / 8, NTH = (big || a.dm.H > 8) ? 2 : 1;
     const int ntw = (KS + 7) / 8;
-    const size_t per_buf = static_cast<size_t>(kSmBatch) * (a.dm.D + 4) * sizeof(float);
-    const size_t fixed = static_cast<size_t>(KS) * NTH * 32 * 16 + a.dm.D * sizeof(float);
+    const int BR = big ? 16 : kSmBatch;
+    const size_t per_buf = static_cast<size_t>(BR) * (a.dm.D + 4) * sizeof(float);
+    const size_t fixed = static_cast<size_t>(KS) * NTH * 32 * (big ? 8 : 16) + a.dm.D * sizeof(float);
     // row-batch ring: 2 deep at 2 CTAs per SM (deeper rings at 1 CTA per SM
-    // measured slower: 0.93 vs 0.67 ms on config 2)
+    // measured slower: 0.93 vs 0.67 ms on config 2); BIG: 1 CTA per SM
     static const int want = [] {
       const char* v = std::getenv("VMFA_STATS_NBUF");
       return v ? std::atoi(v) : 0;
@@ -2724,22 +2777,25 @@ cudaError_t launch_stats(const StatsArgs& a, const int* itemoff, int rows_per_it
     const size_t budget = 200 * 1024 - 32 * 1024;  // minus the static smem
     int nbuf = want > 0 ? std::min(want, kStatsMaxBuf) : 2;
     while (nbuf > 2 && nbuf * per_buf + fixed > budget) --nbuf;
-    const int per_sm = nbuf <= 2 ? 2 : 1;  // 2 x (66.5 + 17 KB dynamic + 30 KB static) fits at D = 256
+    const int per_sm = (!big && nbuf <= 2) ? 2 : 1;  // 2 x (66.5 + 17 KB dynamic + 30 KB static) fits at D = 256
     const size_t smem = nbuf * per_buf + fixed;
     auto go = [&](auto kern) {
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
       kern<<<sm_count() * per_sm, kStatsThreads, smem, s>>>(a, itemoff, rows_per_item, nh1, part, ps, nbuf);
     };
-    if (NTH == 1) {
-      if (ntw <= 1) go(k_stats_mma<1, 1>);
-      else if (ntw <= 2) go(k_stats_mma<1, 2>);
-      else if (ntw <= 4) go(k_stats_mma<1, 4>);
-      else go(k_stats_mma<1, 8>);
+    if (big) {
+      if (ntw <= 4) go(k_stats_mma<2, 4, true>);
+      else if (ntw <= 8) go(k_stats_mma<2, 8, true>);
+      else if (ntw <= 13) go(k_stats_mma<2, 13, true>);
+      else go(k_stats_mma<2, 16, true>);
+    } else if (NTH == 1) {
+      if (ntw <= 1) go(k_stats_mma<1, 1, false>);
+      else if (ntw <= 2) go(k_stats_mma<1, 2, false>);
+      else go(k_stats_mma<1, 4, false>);
     } else {
-      if (ntw <= 1) go(k_stats_mma<2, 1>);
-      else if (ntw <= 2) go(k_stats_mma<2, 2>);
-      else if (ntw <= 4) go(k_stats_mma<2, 4>);
-      else go(k_stats_mma<2, 8>);
+      if (ntw <= 1) go(k_stats_mma<2, 1, false>);
+      else if (ntw <= 2) go(k_stats_mma<2, 2, false>);
+      else go(k_stats_mma<2, 4, false>);
     }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;

@@ -152,6 +152,8 @@ def test_estep_euclid_and_frozen(oracle, gpu):
     dict(N=3000, D=256, C=30, H=15, Cp=3, G=5),   # H + 1 = 16: two latent n-tiles, full m16 tile
     dict(N=3000, D=512, C=30, H=8, Cp=3, G=5),    # 8 dimension tiles per warp
     dict(N=3000, D=48, C=30, H=10, Cp=3, G=5),    # D/8 = 6 tiles < 8 warps, XS % 32 != 4
+    dict(N=3000, D=64, C=30, H=16, Cp=3, G=5),    # H + 1 = 17: constant column by FFMA (16-row batches)
+    dict(N=2000, D=1000, C=16, H=6, Cp=3, G=5),   # 16 dimension tiles per warp (D > 832)
 ])
 @pytest.mark.parametrize("stats", ["mma", "ffma"])
 def test_mstep_parity(oracle, gpu, case, stats, monkeypatch):

@@ -13,7 +13,7 @@ from oracle import oracle as O  # noqa: E402
 from paper_2501_12299_b200 import vmfa as V  # noqa: E402
 
 for (N, D, C, H, Cp, G) in [(20000, 256, 20, 8, 5, 10), (4000, 64, 40, 4, 3, 5), (5000, 40, 30, 3, 3, 5),
-                            (3000, 256, 30, 15, 3, 5)]:
+                            (3000, 256, 30, 15, 3, 5), (3000, 784, 24, 16, 5, 10), (3000, 64, 30, 16, 3, 5)]:
     X, _ = gaussian_problem(N, D, max(4, C // 2), min(H, 4), seed=5)
     p, st, floor, _ = O.initialize(X, C, H, Cp, G, seed=0, scale=0.1, loading_init=1)
     s = V.Session(C, D, H, Cp, G, X)
