@@ -162,6 +162,12 @@ int vmfa_update_params(vmfa_ctx* ctx, int* failed);
 int vmfa_truncated_free_energy(vmfa_ctx* ctx, double* free_energy);
 /* exact_log_likelihood (model.hpp:108-111) over this context's rows.        */
 int vmfa_exact_log_likelihood(vmfa_ctx* ctx, double* log_likelihood);
+/* em_full_step (mstep.cpp:164-208, used by run_emmfa_loop trainer.cpp:228):
+ * every (n, c) log-joint (the dense pass above), q(n, c) = exp(l - LSE_n)
+ * over all C, and the sufficient statistics over every pair; returns
+ * sum_n LSE_n and N*C joints. The statistics stay in the context
+ * (vmfa_download_suffstats / vmfa_update_params follow).                   */
+int vmfa_em_full_step(vmfa_ctx* ctx, double* log_likelihood, uint64_t* joints);
 
 /* One main-loop iteration of train_vmfa (trainer.cpp:149-160): E-step,
  * statistics, update, precompute, post-M-step truncated free energy.

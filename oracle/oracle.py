@@ -336,6 +336,23 @@ def exact_log_likelihood(X, p: Params, k: Caches, threads: int = 1) -> float:
     return F.value
 
 
+def em_full_step(X, p: Params, k: Caches, threads: int = 1):
+    """em_full_step (mstep.cpp:164-208): log_joint of every (n, c)
+    (model.cpp:81-95, via orc_truncated_F with K = all components), per-row
+    log_sum_exp (numerics.hpp:15-22), q = exp(l - lse) over all C and
+    accumulate_point for every pair (the orc_suffstats restatement of
+    mstep.cpp:47-67 with K = all components, merged in worker order).
+    Returns (stats, ll, joints = N*C)."""
+    X = _f32(X)
+    N = X.shape[0]
+    K = np.tile(np.arange(p.C, dtype=np.int32), (N, 1))
+    ll, lj = truncated_free_energy(X, p, k, K, threads=threads, return_lj=True)
+    lse = np.array([log_sum_exp(row) for row in lj])
+    resp = np.exp(lj - lse[:, None])
+    stats = accumulate_suffstats(X, p, k, K, resp, threads=threads)
+    return stats, ll, N * p.C
+
+
 # ------------------------------------------------------------------ init (trainer.cpp:32-47, 107)
 INIT_SALT = 0x1217F01D   # trainer.cpp:36
 STATE_SALT = 0x7A57A7E5  # trainer.cpp:107

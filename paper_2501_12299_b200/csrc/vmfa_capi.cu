@@ -162,6 +162,11 @@ struct vmfa_ctx {
   float* dense_LJ = nullptr;
   double *dense_lse = nullptr, *dense_out = nullptr;
   int64_t dense_R = 0;
+  // em_full_step's full-posterior pairs of a row chunk (allocated on first use)
+  double *em_resp = nullptr, *em_part = nullptr, *em_acc = nullptr;
+  int *em_ent = nullptr, *em_off = nullptr, *em_items = nullptr;
+  int64_t em_R = 0;
+  int dense_SL = 0;
   bool kinv_for_current_K = false;
   // the anchor pass of the next E-step already ran (under the current K, g
   // and parameters) while computing the truncated free energy: LJ's anchor
@@ -777,6 +782,85 @@ int check_ctx(const vmfa_ctx* x) {
 }  // namespace vmfa_b200
 
 // ============================================================================ C-ABI
+constexpr int kStatsMaxRowsHost = 1024;  // K-pairs per statistics item (kernels: kStatsMaxRows)
+
+// ---- dense pass helpers (exact_log_likelihood, em_full_step)
+// rows per dense chunk (<= 1 GiB of log-joints) and the dense buffers
+int ensure_dense(vmfa_ctx* x, int64_t* Rout) {
+  const Dims& dm = x->dm;
+  const int C = dm.C, G = dm.G;
+  const int nb = (C + G - 1) / G;
+  const int SL = nb * G;
+  int64_t R = std::max<int64_t>(128, (int64_t(1) << 30) / (4 * static_cast<int64_t>(SL)));
+  R = std::min<int64_t>(R, (std::numeric_limits<int>::max() - nb) / nb);  // flat entries n * nb + b
+  R = std::min<int64_t>(R, dm.N);
+  if (!x->dense_g) {
+    TRY(x->alloc(x->dense_g, static_cast<size_t>(C) * G));
+    TRY(x->alloc(x->dense_gcnt, C));
+    TRY(x->alloc(x->dense_items, C + 1));
+    TRY(x->alloc(x->dense_off, C + 1));
+    TRY(x->alloc(x->dense_ent, static_cast<size_t>(nb) * R));
+    TRY(x->alloc(x->dense_jobs, static_cast<size_t>(dense_jobs(nb, static_cast<int>(R)))));
+    TRY(x->alloc(x->dense_LJ, static_cast<size_t>(R) * SL));
+    TRY(x->alloc(x->dense_lse, dm.N));
+    TRY(x->alloc(x->dense_out, 1));
+    x->dense_R = R;
+    x->dense_SL = SL;
+  }
+  *Rout = std::min<int64_t>(R, x->dense_R);
+  return VMFA_OK;
+}
+// pseudo-anchor blocks of G components and their scorer images
+int dense_prepare(vmfa_ctx* x) {
+  const Dims& dm = x->dm;
+  cudaStream_t s = x->stream;
+  CU(launch_dense_groups(dm.C, dm.G, x->dense_g, x->dense_gcnt, s));
+  if (x->scorer == 2) {
+    CU(launch_ws_images(dm, 0, x->WT, x->mu32, x->ipsi32, x->dense_g, x->dense_gcnt, x->bimg, x->bscl, s,
+                        x->sscl));
+    CU(launch_ws_records(dm, 0, x->WT, x->mu32, x->ipsi32, x->kconst, x->dense_g, x->dense_gcnt, x->bscl, x->brec,
+                         s));
+  }
+  return VMFA_OK;
+}
+// log-joints of rows [r0, r0 + Rc) against every component into dense_LJ
+// (row stride dense_SL, slot c = component c) and their LSE into dense_lse
+int dense_chunk(vmfa_ctx* x, int64_t r0, int Rc) {
+  const Dims& dm = x->dm;
+  const int C = dm.C, G = dm.G, D = dm.D;
+  const int nb = (C + G - 1) / G;
+  const int SL = x->dense_SL;
+  cudaStream_t s = x->stream;
+  const bool ws = x->scorer == 2;
+  {
+    CU(launch_dense_chunk(C, G, nb, Rc, x->dense_ent, x->dense_jobs, x->dense_items, s));
+    Dims dd = dm;
+    dd.N = Rc;
+    dd.Cp = nb;
+    dd.SL = SL;
+    ScoreArgs a = score_args(x);
+    a.dm = dd;
+    a.X = x->X + r0 * D;
+    a.off = nullptr;
+    a.ent = x->dense_ent;
+    a.itemoff = x->dense_items;
+    a.g = x->dense_g;
+    a.gcnt = x->dense_gcnt;
+    a.out = x->dense_LJ;
+    CU(wait_x(x));
+    if (ws) {
+      const WsOperands op{x->xmax + r0, x->mumax, x->mu32, x->brec, x->srec, x->bimg, x->bscl, x->simg, x->sscl};
+      CU(launch_score_ws(kModeAnchor, a, op, x->dense_jobs, s, false));
+    } else {  // single-role scorers (shapes the warp-specialised one does not take): CSR items
+      CU(launch_dense_csr(C, G, Rc, x->score_rows, x->dense_off, x->dense_items, s));
+      a.off = x->dense_off;
+      CU(run_score(x, kModeAnchor, a));
+    }
+    CU(launch_lse_dense(x->dense_LJ, Rc, SL, C, x->dense_lse + r0, s));
+  }
+  return VMFA_OK;
+}
+
 extern "C" {
 
 int vmfa_abi_version(void) { return VMFA_ABI_VERSION; }
@@ -1361,67 +1445,87 @@ int vmfa_exact_log_likelihood(vmfa_ctx* x, double* ll) {
   TRY(check_ctx(x));
   if (!ll) return fail(VMFA_ERR_INVALID_ARGUMENT, "null output");
   const Dims& dm = x->dm;
-  const int C = dm.C, G = dm.G, D = dm.D;
-  const int nb = (C + G - 1) / G;
-  const int SL = nb * G;
-  int64_t R = std::max<int64_t>(128, (int64_t(1) << 30) / (4 * static_cast<int64_t>(SL)));
-  R = std::min<int64_t>(R, (std::numeric_limits<int>::max() - nb) / nb);  // flat entries n * nb + b
-  R = std::min<int64_t>(R, dm.N);
-  if (!x->dense_g) {
-    TRY(x->alloc(x->dense_g, static_cast<size_t>(C) * G));
-    TRY(x->alloc(x->dense_gcnt, C));
-    TRY(x->alloc(x->dense_items, C + 1));
-    TRY(x->alloc(x->dense_off, C + 1));
-    TRY(x->alloc(x->dense_ent, static_cast<size_t>(nb) * R));
-    TRY(x->alloc(x->dense_jobs, static_cast<size_t>(dense_jobs(nb, static_cast<int>(R)))));
-    TRY(x->alloc(x->dense_LJ, static_cast<size_t>(R) * SL));
-    TRY(x->alloc(x->dense_lse, dm.N));
-    TRY(x->alloc(x->dense_out, 1));
-    x->dense_R = R;
-  }
-  R = std::min<int64_t>(R, x->dense_R);
+  int64_t R = 0;
+  TRY(ensure_dense(x, &R));
   cudaStream_t s = x->stream;
-  const int tok = x->begin(kFamExactLL, dm.N * static_cast<int64_t>(C));
-  const bool ws = x->scorer == 2;
-  CU(launch_dense_groups(C, G, x->dense_g, x->dense_gcnt, s));
-  if (ws) {
-    CU(launch_ws_images(dm, 0, x->WT, x->mu32, x->ipsi32, x->dense_g, x->dense_gcnt, x->bimg, x->bscl, s,
-                        x->sscl));
-    CU(launch_ws_records(dm, 0, x->WT, x->mu32, x->ipsi32, x->kconst, x->dense_g, x->dense_gcnt, x->bscl, x->brec,
-                         s));
-  }
+  const int tok = x->begin(kFamExactLL, dm.N * static_cast<int64_t>(dm.C));
+  TRY(dense_prepare(x));
   for (int64_t r0 = 0; r0 < dm.N; r0 += R) {
     const int Rc = static_cast<int>(std::min<int64_t>(R, dm.N - r0));
-    CU(launch_dense_chunk(C, G, nb, Rc, x->dense_ent, x->dense_jobs, x->dense_items, s));
-    Dims dd = dm;
-    dd.N = Rc;
-    dd.Cp = nb;
-    dd.SL = SL;
-    ScoreArgs a = score_args(x);
-    a.dm = dd;
-    a.X = x->X + r0 * D;
-    a.off = nullptr;
-    a.ent = x->dense_ent;
-    a.itemoff = x->dense_items;
-    a.g = x->dense_g;
-    a.gcnt = x->dense_gcnt;
-    a.out = x->dense_LJ;
-    CU(wait_x(x));
-    if (ws) {
-      const WsOperands op{x->xmax + r0, x->mumax, x->mu32, x->brec, x->srec, x->bimg, x->bscl, x->simg, x->sscl};
-      CU(launch_score_ws(kModeAnchor, a, op, x->dense_jobs, s, false));
-    } else {  // single-role scorers (shapes the warp-specialised one does not take): CSR items
-      CU(launch_dense_csr(C, G, Rc, x->score_rows, x->dense_off, x->dense_items, s));
-      a.off = x->dense_off;
-      CU(run_score(x, kModeAnchor, a));
-    }
-    CU(launch_lse_dense(x->dense_LJ, Rc, SL, C, x->dense_lse + r0, s));
+    TRY(dense_chunk(x, r0, Rc));
   }
   CU(launch_sum_f64(x->dense_lse, dm.N, x->partials, x->dense_out, s));
   x->end(tok);
   CU(cudaMemcpyAsync(&x->hstat->scal[3], x->dense_out, sizeof(double), cudaMemcpyDeviceToHost, s));
   CU(cudaStreamSynchronize(s));
   *ll = x->hstat->scal[3];
+  return VMFA_OK;
+}
+
+// em_full_step (mstep.cpp:164-208): every (n, c) log-joint through the dense
+// pass, q(n, c) = exp(l - LSE_n) for all C, and the statistics over every
+// pair by the K5 kernels (a row chunk's pairs are the K-pairs of a "K" holding
+// all components), chunk statistics summed in fp64 in chunk order. Returns
+// sum_n LSE_n and the N*C joints; the statistics stay in the context for
+// vmfa_update_params (run_emmfa_loop, trainer.cpp:228-233).
+int vmfa_em_full_step(vmfa_ctx* x, double* ll, uint64_t* joints) {
+  TRY(check_ctx(x));
+  if (!ll) return fail(VMFA_ERR_INVALID_ARGUMENT, "null output");
+  const Dims& dm = x->dm;
+  const int C = dm.C, D = dm.D;
+  int64_t R = 0;
+  TRY(ensure_dense(x, &R));
+  // chunk rows: ~32 B per pair (fp64 q, int32 entry, statistics partials) within 4 GB
+  const int rpi = kStatsMaxRowsHost;
+  int64_t Re = std::max<int64_t>(1, (int64_t{4} << 30) / (32 * static_cast<int64_t>(C)));
+  Re = std::min<int64_t>({Re, R, static_cast<int64_t>(dm.N), (std::numeric_limits<int>::max() - 1) / C});
+  if (const char* v = std::getenv("VMFA_EM_CHUNK")) Re = std::max<int64_t>(1, std::min<int64_t>(Re, std::atoll(v)));
+  if (!x->em_resp) {
+    const int64_t items = C + (Re * C + rpi - 1) / rpi;
+    TRY(x->alloc(x->em_resp, static_cast<size_t>(Re) * C));
+    TRY(x->alloc(x->em_ent, static_cast<size_t>(Re) * C));
+    TRY(x->alloc(x->em_off, static_cast<size_t>(C) + 1));
+    TRY(x->alloc(x->em_items, static_cast<size_t>(C) + 1));
+    TRY(x->alloc(x->em_part, static_cast<size_t>(items) * stats_part_stride(dm)));
+    TRY(x->alloc(x->em_acc, x->stats_len));
+    x->em_R = Re;
+  }
+  Re = std::min<int64_t>(Re, x->em_R);
+  cudaStream_t s = x->stream;
+  const int tok = x->begin(kFamExactLL, dm.N * static_cast<int64_t>(C));
+  TRY(dense_prepare(x));
+  int chunk = 0;
+  for (int64_t r0 = 0; r0 < dm.N; r0 += Re, ++chunk) {
+    const int Rc = static_cast<int>(std::min<int64_t>(Re, dm.N - r0));
+    TRY(dense_chunk(x, r0, Rc));
+    CU(launch_em_resp(x->dense_LJ, Rc, x->dense_SL, C, x->dense_lse + r0, x->em_resp, x->em_ent, x->em_off, s));
+    CU(launch_items_scan(x->em_off, C, rpi, 0, x->em_items, s));
+    StatsArgs a{};
+    a.dm = dm;
+    a.dm.N = Rc;
+    a.dm.Cp = C;  // entry e = n * C + c: row e / C
+    a.X = x->X + r0 * D;
+    a.resp = x->em_resp;
+    a.off = x->em_off;
+    a.ent = x->em_ent;
+    a.V32 = x->V32;
+    a.mu32 = x->mu32;
+    a.Sz = x->Sz;
+    a.Nc = x->Nc;
+    a.E = x->E;
+    a.Y = x->Y;
+    a.sq = x->sq;
+    a.qctr = x->qctr;
+    CU(launch_stats(a, x->em_items, rpi, x->em_part, s));
+    CU(launch_add_f64(x->stats, x->em_acc, static_cast<int64_t>(x->stats_len), chunk == 0 ? 1 : 0, s));
+  }
+  CU(cudaMemcpyAsync(x->stats, x->em_acc, x->stats_len * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  CU(launch_sum_f64(x->dense_lse, dm.N, x->partials, x->dense_out, s));
+  x->end(tok);
+  CU(cudaMemcpyAsync(&x->hstat->scal[3], x->dense_out, sizeof(double), cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  *ll = x->hstat->scal[3];
+  if (joints) *joints = static_cast<uint64_t>(dm.N) * static_cast<uint64_t>(C);
   return VMFA_OK;
 }
 

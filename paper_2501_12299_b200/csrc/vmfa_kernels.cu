@@ -2468,6 +2468,26 @@ __global__ void k_lse_rows(const float* LJK, int64_t N, int Cp, double* lse) {
   }
 }
 
+// em_full_step (mstep.cpp:164-208): full responsibilities of a row chunk
+// from its dense log-joints, q(n, c) = exp(l(n, c) - LSE_n) in fp64, laid
+// out as the "K-pairs" of a context whose K rows are all C components (entry
+// n * C + c), plus the component-major CSR of those entries (rows ascending)
+__global__ void k_em_resp(const float* LJ, int64_t R, int SL, int C, const double* lse, double* resp, int* ent,
+                          int* off) {
+  const int64_t total = R * C;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t n = i / C;
+    const int c = static_cast<int>(i - n * C);
+    resp[i] = exp(static_cast<double>(LJ[n * SL + c]) - lse[n]);  // NaN rows as the reference's (App. E.4)
+    ent[(int64_t)c * R + n] = static_cast<int>(i);
+    if (i <= C) off[i] = static_cast<int>(i * R);  // off[c] = c * R (c = 0..C)
+  }
+}
+__global__ void k_add_f64(const double* a, double* acc, int64_t n, int first) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    acc[i] = first ? a[i] : acc[i] + a[i];
+}
+
 // per-row log-sum-exp over the C dense slots (exact_log_likelihood,
 // model.cpp:101-148): warp per row, fixed-order butterflies (deterministic)
 __global__ void k_lse_dense(const float* LJ, int64_t R, int SL, int C, double* lse) {
@@ -2878,6 +2898,15 @@ cudaError_t launch_lse_rows(const float* LJK, int64_t N, int Cp, double* lse, cu
 }
 cudaError_t launch_lse_dense(const float* LJ, int64_t R, int SL, int C, double* lse, cudaStream_t s) {
   k_lse_dense<<<grid_for(R * 32, 256, 16384), 256, 0, s>>>(LJ, R, SL, C, lse);
+  return cudaGetLastError();
+}
+cudaError_t launch_em_resp(const float* LJ, int64_t R, int SL, int C, const double* lse, double* resp, int* ent,
+                           int* off, cudaStream_t s) {
+  k_em_resp<<<grid_for(R * C, 256, sm_count() * 16), 256, 0, s>>>(LJ, R, SL, C, lse, resp, ent, off);
+  return cudaGetLastError();
+}
+cudaError_t launch_add_f64(const double* a, double* acc, int64_t n, int first, cudaStream_t s) {
+  k_add_f64<<<grid_for(n, 256, sm_count() * 16), 256, 0, s>>>(a, acc, n, first);
   return cudaGetLastError();
 }
 cudaError_t launch_sum_f64(const double* v, int64_t n, double* partials, double* out, cudaStream_t s) {

@@ -247,6 +247,15 @@ class Session:
         check(lib().vmfa_exact_log_likelihood(self._h, C.byref(ll)))
         return ll.value
 
+    def em_full_step(self):
+        """em_full_step (mstep.cpp:164-208): full-posterior statistics over
+        every (n, c) pair left in the session (update_params follows, as in
+        run_emmfa_loop, trainer.cpp:228-233). Returns (log-likelihood, joints)."""
+        ll = C.c_double()
+        j = C.c_uint64()
+        check(lib().vmfa_em_full_step(self._h, C.byref(ll), C.byref(j)))
+        return ll.value, j.value
+
     def iterate(self, seed: int, iteration: int, mode: int = KL) -> dict:
         r = IterReport()
         check(lib().vmfa_iterate(self._h, seed, iteration, mode, C.byref(r)))

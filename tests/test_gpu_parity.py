@@ -718,3 +718,34 @@ def test_sparse_cooc_multishard(gpu, oracle, monkeypatch):
             assert np.array_equal(q.g, st1.g) and np.array_equal(q.g_count, st1.g_count)
     for s in shards + [single]:
         s.close()
+
+
+@pytest.mark.parametrize("chunk", [0, 700])
+def test_em_full_step_matches_oracle(oracle, gpu, chunk, monkeypatch):
+    """em_full_step (mstep.cpp:164-208) on the device: log-likelihood and the
+    full-posterior statistics vs the oracle (q from fp32-accurate log-joints:
+    relative errors ~|dl|), then update_params from them; chunk > 0 splits the
+    rows into several dense chunks whose statistics are summed."""
+    O, V = oracle, gpu
+    if chunk:
+        monkeypatch.setenv("VMFA_EM_CHUNK", str(chunk))
+    else:
+        monkeypatch.delenv("VMFA_EM_CHUNK", raising=False)
+    X, _ = gaussian_problem(3000, 64, 12, 4, seed=31)
+    C, H, Cp, G = 24, 4, 3, 5
+    p, st, floor, sess = _setup(O, V, X, C, H, Cp, G)
+    k = O.precompute_all(p)
+    s_or, ll_or, j_or = O.em_full_step(X, p, k, threads=4)
+    ll, j = sess.em_full_step()
+    assert j == j_or == X.shape[0] * C
+    assert abs(ll - ll_or) <= 1e-5 * abs(ll_or)
+    s_g = sess.download_suffstats()
+    np.testing.assert_allclose(s_g.Nc, s_or.Nc, rtol=2e-3, atol=1e-6 * X.shape[0])
+    for f in ("E", "Y", "sq"):
+        a, b = getattr(s_g, f), getattr(s_or, f)
+        np.testing.assert_allclose(a, b, rtol=2e-3, atol=2e-4 * np.abs(b).max(), err_msg=f)
+    sess.upload_suffstats(s_or)
+    sess.update_params()
+    p_or = O.update_params(s_or, X.shape[0], p, floor)
+    np.testing.assert_allclose(sess.download_params().mu, p_or.mu, rtol=1e-9, atol=1e-12)
+    sess.close()

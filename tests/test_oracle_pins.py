@@ -334,3 +334,24 @@ def test_update_params_ldlt_semantics(oracle):
     s.Y[3] = 1e10
     with pytest.raises(oracle.OracleError, match="component 3"):
         oracle.update_params(s, 10, prev, floor)
+
+
+def test_em_full_step_is_the_no_truncation_limit(oracle):
+    """em_full_step's log-likelihood is exact_log_likelihood, its responsibilities
+    sum to 1 per point, and with C' = C (no truncation) the
+    variational E-step's statistics equal em_full_step's."""
+    O = oracle
+    from _helpers import gaussian_problem
+    X, _ = gaussian_problem(600, 12, 5, 2, seed=8)
+    C, H = 6, 2
+    p, st, floor, _ = O.initialize(X, C, H, C, C, seed=0, scale=0.1, loading_init=1)
+    k = O.precompute_all(p)
+    s_em, ll, joints = O.em_full_step(X, p, k, threads=2)
+    assert joints == X.shape[0] * C
+    assert abs(ll - O.exact_log_likelihood(X, p, k)) <= 1e-10 * abs(ll)
+    np.testing.assert_allclose(s_em.Nc.sum(), X.shape[0], rtol=1e-12)
+    e = O.variational_e_step(X, p, k, st, 0, 0, threads=2)
+    assert abs(e.F - ll) <= 1e-10 * abs(ll)
+    s_v = O.accumulate_suffstats(X, p, k, st.K, e.resp, threads=2)
+    for f in ("Nc", "E", "Y", "sq"):
+        np.testing.assert_allclose(getattr(s_v, f), getattr(s_em, f), rtol=1e-10, atol=1e-10, err_msg=f)
