@@ -382,6 +382,23 @@ def main():
                             "per-row LSE, fixed-order sum) between CUDA events"}
         except Exception as ex:
             exact = {"error": str(ex)}
+    # SURVEY §8(f) item 1, second half: em_full_step (mstep.cpp:164-208) --
+    # every pair's log-joint, full responsibilities and statistics
+    em = None
+    if not args.no_exact_ll:
+        try:
+            sess.em_full_step()  # first call allocates its buffers
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(ext)
+            ll, jn = sess.em_full_step()
+            e1.record(ext)
+            e1.synchronize()
+            t = e0.elapsed_time(e1)
+            em = {"ms": t, "log_likelihood": ll, "joints": jn, "joints_per_s": jn / (t * 1e-3),
+                  "how": "one vmfa_em_full_step call (dense log-joints, q for all N x C pairs, statistics "
+                         "over every pair) between CUDA events; not part of the timed v-MFA step"}
+        except Exception as ex:
+            em = {"error": str(ex)}
 
     # launches per step (CUPTI), outside the timed region
     n_launch, names = count_launches(sess, step)
@@ -463,6 +480,7 @@ def main():
             "iteration_roofline": iter_roof,
             "roofline_statistics": stats_roof,
             "exact_ll": exact,
+            "em_full_step": em,
             "gpu_launches": int(n_launch * args.steps),
             "launches_per_step": n_launch,
             "clocks": clk_sum,

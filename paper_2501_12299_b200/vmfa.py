@@ -523,6 +523,45 @@ def train_vmfa(sess: Session, cfg: TrainConfig, testset: Session | None = None) 
     return report
 
 
+def train_emmfa(sess: Session, cfg: TrainConfig) -> dict:
+    """run_emmfa_loop (trainer.cpp:205-260, train_emmfa trainer.hpp:90) on the
+    device, after the caller's initialisation: full-posterior EM iterations
+    (em_full_step, update_params + precompute, exact log-likelihood F) until
+    check_convergence(epsilon) on F, or max_iters; NLL every eval_nll_every
+    iterations. Joint evaluations count N*C per em_full_step (the exact-F pass
+    is not counted, as the reference's `scratch` counter)."""
+    import math
+    import time
+
+    recs, joints = [], 0
+    t_start = time.perf_counter()
+    excluded = 0.0
+    prev_f, converged = math.nan, False
+    for t in range(1, cfg.max_iters + 1):
+        t0 = time.perf_counter()
+        _, j = sess.em_full_step()
+        joints += j
+        sess.update_params()
+        f = sess.exact_log_likelihood()
+        empty = int((sess.download_params().pi == 0.0).sum())
+        rec = dict(t=t, warmup=False, F=f, joint_evals=joints, wall_ms=(time.perf_counter() - t0) * 1e3,
+                   empty_components=empty, nll_train=math.nan)
+        if cfg.eval_nll_every > 0 and t % cfg.eval_nll_every == 0:
+            t1 = time.perf_counter()
+            rec["nll_train"] = -f / sess.N  # nll_per_point (trainer.cpp:79-85) of the same parameters
+            excluded += time.perf_counter() - t1
+        recs.append(rec)
+        if math.isfinite(prev_f) and check_convergence(prev_f, f, cfg.epsilon, cfg.literal_eq14):
+            converged = True
+            break
+        prev_f = f
+    report = dict(algo="emmfa", iterations=recs, warmup_iterations=0, main_iterations=len(recs),
+                  converged=converged, joint_evals=joints, empty_components=recs[-1]["empty_components"],
+                  total_wall_ms=(time.perf_counter() - t_start - excluded) * 1e3)
+    report["nll_train"] = -sess.exact_log_likelihood() / sess.N
+    return report
+
+
 # ---- on-disk containers (io.hpp:12-23; host only) -----------------------------
 def _path(p) -> bytes:
     return os.fsencode(os.fspath(p))

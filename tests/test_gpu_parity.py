@@ -749,3 +749,24 @@ def test_em_full_step_matches_oracle(oracle, gpu, chunk, monkeypatch):
     p_or = O.update_params(s_or, X.shape[0], p, floor)
     np.testing.assert_allclose(sess.download_params().mu, p_or.mu, rtol=1e-9, atol=1e-12)
     sess.close()
+
+
+def test_train_emmfa_loop_matches_oracle(oracle, gpu):
+    """run_emmfa_loop's iterations (em_full_step, update_params, exact F) on the
+    device vs the oracle, free-running from the same initialisation: F per
+    iteration within 1e-4 relative."""
+    O, V = oracle, gpu
+    X, _ = gaussian_problem(2000, 32, 6, 3, seed=41)
+    C, H = 8, 3
+    p, st, floor, sess = _setup(O, V, X, C, H, 3, 4)
+    cfg = V.TrainConfig(max_iters=6, epsilon=0.0)
+    rep = V.train_emmfa(sess, cfg)
+    k = O.precompute_all(p)
+    for r in rep["iterations"]:
+        s_or, _, _ = O.em_full_step(X, p, k, threads=4)
+        p = O.update_params(s_or, X.shape[0], p, floor)
+        k = O.precompute_all(p)
+        f_or = O.exact_log_likelihood(X, p, k, threads=4)
+        assert abs(r["F"] - f_or) <= 1e-4 * abs(f_or), (r["t"], r["F"], f_or)
+    assert rep["joint_evals"] == len(rep["iterations"]) * X.shape[0] * C
+    sess.close()
