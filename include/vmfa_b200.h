@@ -168,6 +168,13 @@ int vmfa_exact_log_likelihood(vmfa_ctx* ctx, double* log_likelihood);
  * sum_n LSE_n and N*C joints. The statistics stay in the context
  * (vmfa_download_suffstats / vmfa_update_params follow).                   */
 int vmfa_em_full_step(vmfa_ctx* ctx, double* log_likelihood, uint64_t* joints);
+/* afkmc2_seed (seeding.cpp:60-121; the reference's default InitConfig
+ * method): C seed rows of this context's data (the whole dataset), the
+ * xoshiro256++ stream state after the draws (init_params continues it,
+ * trainer.cpp:36-44) and the squared-distance count (EvalCounter::distances).
+ * DegenerateData when fewer than C distinct rows exist.                    */
+int vmfa_afkmc2_seed(vmfa_ctx* ctx, int C, int chain_length, uint64_t stream_seed, int64_t* seeds,
+                     uint64_t* stream_state, uint64_t* distances);
 
 /* One main-loop iteration of train_vmfa (trainer.cpp:149-160): E-step,
  * statistics, update, precompute, post-M-step truncated free energy.

@@ -82,6 +82,7 @@ def lib():
         L.orc_exact_ll.argtypes = [i64, i32, i32, i32, f32p, f64p, f64p, f64p, f64p, f64p, f64p,
                                    f64p, f64p, i32, C.POINTER(C.c_double)]
         L.orc_random_points_seed.argtypes = [f32p, i64, i32, i32, u64, i64p, u64p]
+        L.orc_afkmc2.argtypes = [f32p, i64, i32, i32, i32, u64, i64p, u64p, u64p]
         L.orc_init_params.argtypes = [f32p, i64, i32, i32, i32, i64p, u64p, f64, i32, f64p, f64p,
                                       f64p, f64p, f64p]
         L.orc_init_varstate.argtypes = [i64, i32, i32, i32, i64p, i32, u64, i32p, i32p, i32p]
@@ -365,6 +366,17 @@ def random_points_seed(X, C_: int, stream_seed: int):
     state = np.zeros(4, np.uint64)
     _check(lib().orc_random_points_seed(X, X.shape[0], X.shape[1], C_, stream_seed, seeds, state))
     return seeds, state
+
+
+def afkmc2_seed(X, C_: int, chain_length: int, stream_seed: int):
+    """afkmc2_seed (seeding.cpp:60-121); returns (seeds, stream state after,
+    squared_distance calls)."""
+    X = _f32(X)
+    seeds = np.zeros(C_, np.int64)
+    state = np.zeros(4, np.uint64)
+    cnt = np.zeros(1, np.uint64)
+    _check(lib().orc_afkmc2(X, X.shape[0], X.shape[1], C_, chain_length, stream_seed, seeds, state, cnt))
+    return seeds, state, int(cnt[0])
 
 
 def init_params(X, C_: int, H: int, seeds, stream_state, floor, scale: float = 1.0,

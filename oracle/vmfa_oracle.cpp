@@ -856,6 +856,88 @@ int orc_random_points_seed(const float* X, i64 N, int D, int C, u64 stream_seed,
   return OK;
 }
 
+// afkmc2_seed (seeding.cpp:60-121): AFK-MC^2 seeding, the reference's default
+// InitConfig::Method (seeding.hpp:14-17). squared_distance (:34-39) in fp64
+// summed over d in ascending order (Eigen's squaredNorm order is unpinned),
+// distance_to_centers (:41-49), draw_from_cdf (:51-56); the proposal q and its
+// cdf are built sequentially (:75-86). *dist_count receives the number of
+// squared_distance calls (EvalCounter::distances).
+int orc_afkmc2(const float* X, i64 N, int D, int C, int chain_length, u64 stream_seed, i64* seeds,
+               u64* stream_state_out, u64* dist_count) {
+  if (C < 1 || C > N || chain_length < 1) return INVALID_ARGUMENT;
+  {  // count_distinct_rows (:16-32): at least C distinct rows
+    std::unordered_set<std::string> distinct;
+    for (i64 i = 0; i < N && (i64)distinct.size() < C; ++i)
+      distinct.insert(std::string(reinterpret_cast<const char*>(X + i * D), (size_t)D * sizeof(float)));
+    if ((i64)distinct.size() < C) return DEGENERATE_DATA;
+  }
+  u64 count = 0;
+  auto sqd = [&](i64 a, i64 b) {
+    ++count;
+    double t = 0.0;
+    for (int d = 0; d < D; ++d) {
+      const double v = static_cast<double>(X[a * D + d]) - static_cast<double>(X[b * D + d]);
+      t = std::fma(v, v, t);  // explicit fma: identical on the host and the device
+    }
+    return t;
+  };
+  std::vector<i64> centers;
+  auto to_centers = [&](i64 n) {
+    double best = std::numeric_limits<double>::infinity();
+    for (i64 c : centers) best = std::min(best, sqd(n, c));
+    return best;
+  };
+  Stream s(stream_seed);
+  centers.push_back(s.below(N));
+  std::vector<double> q(N), cdf(N);
+  double sum_d2 = 0.0;
+  for (i64 i = 0; i < N; ++i) {
+    q[i] = sqd(i, centers[0]);
+    sum_d2 += q[i];
+  }
+  const double uniform_part = 0.5 / static_cast<double>(N);
+  for (i64 i = 0; i < N; ++i) q[i] = (sum_d2 > 0.0 ? 0.5 * q[i] / sum_d2 : 0.0) + uniform_part;
+  double acc = 0.0;
+  for (i64 i = 0; i < N; ++i) cdf[i] = acc += q[i];
+  auto draw = [&]() {
+    const double u = s.unit() * cdf.back();
+    const i64 it = std::upper_bound(cdf.begin(), cdf.end(), u) - cdf.begin();
+    return std::min<i64>(it, N - 1);
+  };
+  while (static_cast<int>(centers.size()) < C) {
+    i64 x = draw();
+    double dx = to_centers(x);
+    for (int step = 1; step < chain_length; ++step) {
+      const i64 y = draw();
+      const double dy = to_centers(y);
+      if (dy <= 0.0) continue;
+      bool accept = dx <= 0.0;
+      if (!accept) accept = s.unit() < (dy * q[x]) / (dx * q[y]);
+      if (accept) {
+        x = y;
+        dx = dy;
+      }
+    }
+    if (dx <= 0.0) {  // :105-117 farthest point from its nearest center
+      double best = -1.0;
+      i64 best_i = -1;
+      for (i64 i = 0; i < N; ++i) {
+        const double d = to_centers(i);
+        if (d > best) {
+          best = d;
+          best_i = i;
+        }
+      }
+      x = best_i;
+    }
+    centers.push_back(x);
+  }
+  for (int c = 0; c < C; ++c) seeds[c] = centers[c];
+  if (stream_state_out) std::memcpy(stream_state_out, s.w, sizeof(s.w));
+  if (dist_count) *dist_count = count;
+  return OK;
+}
+
 // init_params (seeding.cpp:151-181), continuing the same stream (trainer.cpp:36-44).
 // loading_init 0: reference Lambda ~ U[0, scale); 1: BASELINE's N(0, scale^2)
 // (Box-Muller from the same stream, same c->d->h order).

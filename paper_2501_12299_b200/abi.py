@@ -88,6 +88,7 @@ _SIGS = {
     "vmfa_truncated_free_energy": (_I, [_P, C.POINTER(_D)]),
     "vmfa_exact_log_likelihood": (_I, [_P, C.POINTER(_D)]),
     "vmfa_em_full_step": (_I, [_P, C.POINTER(_D), C.POINTER(_U64)]),
+    "vmfa_afkmc2_seed": (_I, [_P, _I, _I, _U64, _P, _P, C.POINTER(_U64)]),
     "vmfa_iterate": (_I, [_P, _U64, _U64, _I, C.POINTER(IterReport)]),
     "vmfa_exchange_buffer": (_I, [_P, _I, C.POINTER(_P), C.POINTER(C.c_size_t), C.POINTER(_I)]),
     "vmfa_phase_estep_local": (_I, [_P, _U64, _U64, _I]),

@@ -15,6 +15,7 @@
 
 #include "vmfa_b200.h"
 #include "vmfa_internal.hpp"
+#include "vmfa_rng.hpp"
 #include "vmfa_kernels.cuh"
 
 namespace vmfa_b200 {
@@ -1526,6 +1527,56 @@ int vmfa_em_full_step(vmfa_ctx* x, double* ll, uint64_t* joints) {
   CU(cudaStreamSynchronize(s));
   *ll = x->hstat->scal[3];
   if (joints) *joints = static_cast<uint64_t>(dm.N) * static_cast<uint64_t>(C);
+  return VMFA_OK;
+}
+
+// afkmc2_seed (seeding.cpp:60-121) over the context's rows: the first center
+// is drawn on the host from the stream (trainer.cpp:36), the proposal and the
+// chains run on the device (k_afk_*). Returns the C seed rows, the stream
+// state after the draws (init_params continues it, trainer.cpp:43) and the
+// squared_distance count (EvalCounter::distances).
+int vmfa_afkmc2_seed(vmfa_ctx* x, int C, int chain_length, uint64_t stream_seed, int64_t* seeds,
+                     uint64_t* stream_state, uint64_t* distances) {
+  TRY(check_ctx(x));
+  const Dims& dm = x->dm;
+  const int64_t N = dm.N;
+  if (!seeds) return fail(VMFA_ERR_INVALID_ARGUMENT, "null output");
+  if (C < 1 || C > N) return fail(VMFA_ERR_INVALID_ARGUMENT, "C out of range");
+  if (chain_length < 1) return fail(VMFA_ERR_INVALID_ARGUMENT, "chain_length < 1");
+  if (dm.n0 != 0 || dm.Ntot != dm.N)
+    return fail(VMFA_ERR_UNSUPPORTED, "AFK-MC2 seeding needs the whole dataset in one context");
+  HostStream hs(stream_seed);
+  const int64_t first = hs.uniform_int(N);
+  cudaStream_t s = x->stream;
+  double *q = nullptr, *cdf = nullptr;
+  int64_t* centers = nullptr;
+  unsigned long long *st = nullptr, *cnt = nullptr;
+  int* deg = nullptr;
+  CU(cudaMallocAsync(&q, N * sizeof(double), s));
+  CU(cudaMallocAsync(&cdf, N * sizeof(double), s));
+  CU(cudaMallocAsync(&centers, C * sizeof(int64_t), s));
+  CU(cudaMallocAsync(&st, 6 * sizeof(unsigned long long), s));
+  cnt = st + 4;
+  deg = reinterpret_cast<int*>(st + 5);
+  unsigned long long init[6] = {hs.w[0], hs.w[1], hs.w[2], hs.w[3], 0, 0};
+  CU(cudaMemcpyAsync(st, init, sizeof init, cudaMemcpyHostToDevice, s));
+  CU(cudaMemcpyAsync(centers, &first, sizeof first, cudaMemcpyHostToDevice, s));
+  CU(wait_x(x));
+  CU(launch_afkmc2(x->X, N, dm.D, C, chain_length, q, cdf, centers, st, cnt, deg, s));
+  unsigned long long out[6];
+  CU(cudaMemcpyAsync(out, st, sizeof out, cudaMemcpyDeviceToHost, s));
+  CU(cudaMemcpyAsync(seeds, centers, C * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  CU(cudaFreeAsync(q, s));
+  CU(cudaFreeAsync(cdf, s));
+  CU(cudaFreeAsync(centers, s));
+  CU(cudaFreeAsync(st, s));
+  CU(cudaStreamSynchronize(s));
+  int degenerate = 0;
+  std::memcpy(&degenerate, &out[5], sizeof degenerate);
+  if (degenerate) return fail(VMFA_ERR_DEGENERATE_DATA, "fewer distinct rows than requested seeds");
+  if (stream_state)
+    for (int k = 0; k < 4; ++k) stream_state[k] = out[k];
+  if (distances) *distances = out[4] + static_cast<uint64_t>(N);  // + the first center's proposal pass
   return VMFA_OK;
 }
 

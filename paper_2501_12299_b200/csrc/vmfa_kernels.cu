@@ -2488,6 +2488,162 @@ __global__ void k_add_f64(const double* a, double* acc, int64_t n, int first) {
     acc[i] = first ? a[i] : acc[i] + a[i];
 }
 
+// ---------------------------------------------------------------- AFK-MC^2 seeding (seeding.cpp:60-121)
+// The reference's default seeding (seeding.hpp:14-17). Bit-identical to the
+// oracle's restatement: squared distances in fp64 by explicit fma over d in
+// ascending order, the proposal q and its cdf built sequentially, the
+// xoshiro256++ stream (rng.hpp:30-86) advanced in the reference's order.
+// k_afk_q: distances of every row to the first center (one thread per row);
+// k_afk_cdf: q normalised and its cdf (one thread, the reference's order);
+// k_afk_chain: the Metropolis chains (one CTA; thread 0 draws, the block
+// computes distance_to_centers as a min over centers, exact in any order).
+__device__ __forceinline__ double afk_sqd(const float* X, int D, int64_t a, int64_t b) {
+  const float* xa = X + a * D;
+  const float* xb = X + b * D;
+  double t = 0.0;
+  for (int d = 0; d < D; ++d) {
+    const double v = static_cast<double>(__ldg(xa + d)) - static_cast<double>(__ldg(xb + d));
+    t = fma(v, v, t);
+  }
+  return t;
+}
+struct AfkState {
+  unsigned long long w[4];
+};
+__device__ __forceinline__ unsigned long long afk_next(AfkState& s) {
+  auto rotl = [](unsigned long long x, int k) { return (x << k) | (x >> (64 - k)); };
+  const unsigned long long out = rotl(s.w[0] + s.w[3], 23) + s.w[0];
+  const unsigned long long t = s.w[1] << 17;
+  s.w[2] ^= s.w[0];
+  s.w[3] ^= s.w[1];
+  s.w[1] ^= s.w[2];
+  s.w[0] ^= s.w[3];
+  s.w[2] ^= t;
+  s.w[3] = rotl(s.w[3], 45);
+  return out;
+}
+__device__ __forceinline__ double afk_unit(AfkState& s) { return static_cast<double>(afk_next(s) >> 11) * 0x1.0p-53; }
+
+__global__ void k_afk_q(const float* X, int64_t N, int D, const int64_t* centers, double* q) {
+  const int64_t c0 = centers[0];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x)
+    q[i] = afk_sqd(X, D, i, c0);
+}
+__global__ void k_afk_cdf(int64_t N, double* q, double* cdf) {
+  double sum = 0.0;
+  for (int64_t i = 0; i < N; ++i) sum += q[i];
+  const double uniform_part = 0.5 / static_cast<double>(N);
+  double acc = 0.0;
+  for (int64_t i = 0; i < N; ++i) {
+    const double a = sum > 0.0 ? 0.5 * q[i] / sum : 0.0;
+    q[i] = a + uniform_part;
+    acc += q[i];
+    cdf[i] = acc;
+  }
+}
+constexpr int kAfkThreads = 1024;
+__global__ void __launch_bounds__(kAfkThreads) k_afk_chain(const float* X, int64_t N, int D, int C, int m,
+                                                          const double* q, const double* cdf, int64_t* centers,
+                                                          unsigned long long* state, unsigned long long* count,
+                                                          int* degenerate) {
+  __shared__ AfkState s_rng;
+  __shared__ double s_red[kAfkThreads / 32];
+  __shared__ int64_t s_idx[kAfkThreads / 32];
+  __shared__ int64_t s_pick;
+  __shared__ int s_flag;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    for (int k = 0; k < 4; ++k) s_rng.w[k] = state[k];
+  }
+  unsigned long long cnt = 0;  // thread 0's squared_distance tally
+  __syncthreads();
+  // distance_to_centers (seeding.cpp:41-49) of row n to the first nc centers
+  auto to_centers = [&](int64_t n, int nc) -> double {
+    double best = INFINITY;
+    for (int k = tid; k < nc; k += kAfkThreads) best = fmin(best, afk_sqd(X, D, n, centers[k]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) best = fmin(best, __shfl_xor_sync(kFull, best, o));
+    __syncthreads();
+    if (lane == 0) s_red[warp] = best;
+    __syncthreads();
+    best = INFINITY;
+    for (int w = 0; w < kAfkThreads / 32; ++w) best = fmin(best, s_red[w]);
+    if (tid == 0) cnt += nc;
+    return best;
+  };
+  // draw_from_cdf (seeding.cpp:51-56) by thread 0, broadcast
+  auto draw = [&]() -> int64_t {
+    __syncthreads();
+    if (tid == 0) {
+      const double u = afk_unit(s_rng) * cdf[N - 1];
+      int64_t lo = 0, hi = N;  // first index with cdf > u
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (cdf[mid] > u) hi = mid;
+        else lo = mid + 1;
+      }
+      s_pick = lo < N - 1 ? lo : N - 1;
+    }
+    __syncthreads();
+    return s_pick;
+  };
+  for (int nc = 1; nc < C; ++nc) {
+    int64_t x = draw();
+    double dx = to_centers(x, nc);
+    for (int step = 1; step < m; ++step) {
+      const int64_t y = draw();
+      const double dy = to_centers(y, nc);
+      if (dy <= 0.0) continue;  // duplicates of chosen centers never accepted
+      bool accept = dx <= 0.0;
+      if (!accept) {
+        __syncthreads();
+        if (tid == 0) s_flag = afk_unit(s_rng) < (dy * q[x]) / (dx * q[y]) ? 1 : 0;
+        __syncthreads();
+        accept = s_flag != 0;
+      }
+      if (accept) {
+        x = y;
+        dx = dy;
+      }
+    }
+    if (dx <= 0.0) {  // every proposal duplicated a chosen center: farthest point (first on ties)
+      double best = -1.0;
+      int64_t bi = -1;
+      for (int64_t i = tid; i < N; i += kAfkThreads) {
+        double d = INFINITY;
+        for (int k = 0; k < nc; ++k) d = fmin(d, afk_sqd(X, D, i, centers[k]));
+        if (d > best) best = d, bi = i;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(kFull, best, o);
+        const int64_t oi = __shfl_xor_sync(kFull, bi, o);
+        if (ob > best || (ob == best && oi >= 0 && (bi < 0 || oi < bi))) best = ob, bi = oi;
+      }
+      __syncthreads();
+      if (lane == 0) s_red[warp] = best, s_idx[warp] = bi;
+      __syncthreads();
+      if (tid == 0) {
+        double b = -1.0;
+        int64_t ib = -1;
+        for (int w = 0; w < kAfkThreads / 32; ++w)
+          if (s_red[w] > b || (s_red[w] == b && s_idx[w] >= 0 && (ib < 0 || s_idx[w] < ib))) b = s_red[w], ib = s_idx[w];
+        s_pick = ib;
+        cnt += static_cast<unsigned long long>(N) * nc;
+        if (!(b > 0.0)) *degenerate = 1;  // fewer than C distinct rows (count_distinct_rows, :65-67)
+      }
+      __syncthreads();
+      x = s_pick;
+    }
+    if (tid == 0) centers[nc] = x;
+    __syncthreads();
+  }
+  if (tid == 0) {
+    for (int k = 0; k < 4; ++k) state[k] = s_rng.w[k];
+    *count = cnt;
+  }
+}
+
 // per-row log-sum-exp over the C dense slots (exact_log_likelihood,
 // model.cpp:101-148): warp per row, fixed-order butterflies (deterministic)
 __global__ void k_lse_dense(const float* LJ, int64_t R, int SL, int C, double* lse) {
@@ -2907,6 +3063,13 @@ cudaError_t launch_em_resp(const float* LJ, int64_t R, int SL, int C, const doub
 }
 cudaError_t launch_add_f64(const double* a, double* acc, int64_t n, int first, cudaStream_t s) {
   k_add_f64<<<grid_for(n, 256, sm_count() * 16), 256, 0, s>>>(a, acc, n, first);
+  return cudaGetLastError();
+}
+cudaError_t launch_afkmc2(const float* X, int64_t N, int D, int C, int m, double* q, double* cdf, int64_t* centers,
+                          unsigned long long* state, unsigned long long* count, int* degenerate, cudaStream_t s) {
+  k_afk_q<<<grid_for(N, 256, sm_count() * 8), 256, 0, s>>>(X, N, D, centers, q);
+  k_afk_cdf<<<1, 1, 0, s>>>(N, q, cdf);
+  k_afk_chain<<<1, kAfkThreads, 0, s>>>(X, N, D, C, m, q, cdf, centers, state, count, degenerate);
   return cudaGetLastError();
 }
 cudaError_t launch_sum_f64(const double* v, int64_t n, double* partials, double* out, cudaStream_t s) {

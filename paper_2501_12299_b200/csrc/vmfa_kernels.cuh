@@ -278,6 +278,8 @@ int64_t dense_jobs(int nb, int R);
 cudaError_t launch_em_resp(const float* LJ, int64_t R, int SL, int C, const double* lse, double* resp, int* ent,
                            int* off, cudaStream_t s);
 cudaError_t launch_add_f64(const double* a, double* acc, int64_t n, int first, cudaStream_t s);
+cudaError_t launch_afkmc2(const float* X, int64_t N, int D, int C, int m, double* q, double* cdf, int64_t* centers,
+                          unsigned long long* state, unsigned long long* count, int* degenerate, cudaStream_t s);
 cudaError_t launch_lse_dense(const float* LJ, int64_t R, int SL, int C, double* lse, cudaStream_t s);
 int64_t ws_record_floats(const Dims& dm, int single);
 cudaError_t launch_ws_records(const Dims& dm, int single, const float* WT, const float* mu32, const float* ipsi32,

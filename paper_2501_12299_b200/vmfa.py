@@ -256,6 +256,17 @@ class Session:
         check(lib().vmfa_em_full_step(self._h, C.byref(ll), C.byref(j)))
         return ll.value, j.value
 
+    def afkmc2_seed(self, C_: int, chain_length: int, stream_seed: int):
+        """afkmc2_seed (seeding.cpp:60-121) on the device over this session's
+        rows (the whole dataset). Returns (seed rows, stream state after,
+        squared-distance count); init_params continues the stream."""
+        seeds = np.zeros(C_, np.int64)
+        state = np.zeros(4, np.uint64)
+        cnt = C.c_uint64()
+        check(lib().vmfa_afkmc2_seed(self._h, C_, chain_length, stream_seed, ptr(seeds), ptr(state),
+                                     C.byref(cnt)))
+        return seeds, state, cnt.value
+
     def iterate(self, seed: int, iteration: int, mode: int = KL) -> dict:
         r = IterReport()
         check(lib().vmfa_iterate(self._h, seed, iteration, mode, C.byref(r)))

@@ -770,3 +770,34 @@ def test_train_emmfa_loop_matches_oracle(oracle, gpu):
         assert abs(r["F"] - f_or) <= 1e-4 * abs(f_or), (r["t"], r["F"], f_or)
     assert rep["joint_evals"] == len(rep["iterations"]) * X.shape[0] * C
     sess.close()
+
+
+@pytest.mark.parametrize("C,m", [(12, 10), (40, 3), (5, 1)])
+def test_afkmc2_seed_matches_oracle(oracle, gpu, C, m):
+    """AFK-MC^2 seeding (seeding.cpp:60-121, the reference's default init) on
+    the device: the same seed rows, the same stream state after the draws and
+    the same squared-distance count as the oracle (bit-identical fp64
+    distances by explicit fma in ascending d)."""
+    O, V = oracle, gpu
+    X, _ = gaussian_problem(2500, 24, 8, 2, seed=51)
+    seed = O.hash_combine(3, O.INIT_SALT)
+    s_or, st_or, n_or = O.afkmc2_seed(X, C, m, seed)
+    sess = V.Session(C, X.shape[1], 2, 2, 2, X)
+    s_g, st_g, n_g = sess.afkmc2_seed(C, m, seed)
+    assert np.array_equal(s_g, s_or)
+    assert np.array_equal(st_g, st_or)
+    assert n_g == n_or
+    sess.close()
+
+
+def test_afkmc2_degenerate_data(gpu, oracle):
+    """Fewer distinct rows than seeds: DegenerateData on both sides (seeding.cpp:65-67)."""
+    O, V = oracle, gpu
+    X = np.repeat(np.arange(4, dtype=np.float32)[:, None], 8, axis=1)
+    X = np.repeat(X, 50, axis=0)
+    with pytest.raises(O.OracleError):
+        O.afkmc2_seed(X, 6, 5, 1)
+    sess = V.Session(6, 8, 1, 2, 2, X)
+    with pytest.raises(V.VmfaError):
+        sess.afkmc2_seed(6, 5, 1)
+    sess.close()

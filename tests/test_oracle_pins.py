@@ -355,3 +355,20 @@ def test_em_full_step_is_the_no_truncation_limit(oracle):
     s_v = O.accumulate_suffstats(X, p, k, st.K, e.resp, threads=2)
     for f in ("Nc", "E", "Y", "sq"):
         np.testing.assert_allclose(getattr(s_v, f), getattr(s_em, f), rtol=1e-10, atol=1e-10, err_msg=f)
+
+
+def test_afkmc2_oracle_properties(oracle):
+    """afkmc2_seed restatement: the first seed is the stream's first
+    uniform_int(N) (seeding.cpp:70), seeds are distinct rows, chain_length = 1
+    makes every later seed the first cdf draw, and the squared-distance count
+    is N + m * sum_{k<C} k (seeding.cpp:77-101, no fallback)."""
+    O = oracle
+    from _helpers import gaussian_problem
+    X, _ = gaussian_problem(800, 6, 4, 2, seed=9)
+    seed = O.hash_combine(1, O.INIT_SALT)
+    C, m = 15, 4
+    s, st, n = O.afkmc2_seed(X, C, m, seed)
+    first = O.rng_ops(seed, [2], [X.shape[0]])  # op 2: uniform_int(bound)
+    assert s[0] == int(first[0])
+    assert len(set(s.tolist())) == C
+    assert n == X.shape[0] + m * sum(range(1, C))
