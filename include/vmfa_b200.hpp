@@ -234,6 +234,35 @@ inline double exact_log_likelihood(Session& s) {
   return ll;
 }
 
+// em_full_step (mstep.hpp; mstep.cpp:164-208): full-posterior statistics of
+// every (n, c) pair under the session's parameters; returns sum_n LSE_n.
+inline double em_full_step(Session& s, SuffStats& stats, uint64_t* joints = nullptr) {
+  double ll = 0.0;
+  uint64_t j = 0;
+  check(vmfa_em_full_step(s.handle(), &ll, &j));
+  if (joints) *joints = j;
+  const size_t C = s.C(), D = s.D(), H1 = s.H() + 1;
+  stats.Nc.resize(C);
+  stats.Y.resize(C * D * H1);
+  stats.E.resize(C * H1 * H1);
+  stats.sq_sum.resize(C * D);
+  check(vmfa_download_suffstats(s.handle(), stats.Nc.data(), stats.Y.data(), stats.E.data(),
+                                stats.sq_sum.data()));
+  return ll;
+}
+
+// afkmc2_seed (seeding.hpp:29-31; seeding.cpp:60-121) over the session's rows;
+// `stream_state` receives the xoshiro256++ state init_params continues from.
+inline std::vector<int64_t> afkmc2_seed(Session& s, int C, int chain_length, uint64_t stream_seed,
+                                        uint64_t stream_state[4] = nullptr, uint64_t* distances = nullptr) {
+  std::vector<int64_t> seeds(C);
+  uint64_t st[4];
+  check(vmfa_afkmc2_seed(s.handle(), C, chain_length, stream_seed, seeds.data(), st, distances));
+  if (stream_state)
+    for (int k = 0; k < 4; ++k) stream_state[k] = st[k];
+  return seeds;
+}
+
 // train_vmfa's loop (trainer.cpp:111-186) with fixed warm-up / main counts.
 struct IterationRecord {
   bool warmup = false;
