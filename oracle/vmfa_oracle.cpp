@@ -858,7 +858,7 @@ int orc_random_points_seed(const float* X, i64 N, int D, int C, u64 stream_seed,
 
 // afkmc2_seed (seeding.cpp:60-121): AFK-MC^2 seeding, the reference's default
 // InitConfig::Method (seeding.hpp:14-17). squared_distance (:34-39) in fp64
-// summed over d in ascending order (Eigen's squaredNorm order is unpinned),
+// in the device's warp order (below; Eigen's squaredNorm order is unpinned),
 // distance_to_centers (:41-49), draw_from_cdf (:51-56); the proposal q and its
 // cdf are built sequentially (:75-86). *dist_count receives the number of
 // squared_distance calls (EvalCounter::distances).
@@ -872,14 +872,23 @@ int orc_afkmc2(const float* X, i64 N, int D, int C, int chain_length, u64 stream
     if ((i64)distinct.size() < C) return DEGENERATE_DATA;
   }
   u64 count = 0;
+  // squared_distance's summation order (Eigen's is unpinned): 32 partials over
+  // d = l, l + 32, ... (explicit fma, ascending), then the halving tree
+  // v[l] += v[l + o] for o = 16, 8, 4, 2, 1 -- the device's warp order
   auto sqd = [&](i64 a, i64 b) {
     ++count;
-    double t = 0.0;
-    for (int d = 0; d < D; ++d) {
-      const double v = static_cast<double>(X[a * D + d]) - static_cast<double>(X[b * D + d]);
-      t = std::fma(v, v, t);  // explicit fma: identical on the host and the device
+    double v[32];
+    for (int l = 0; l < 32; ++l) {
+      double t = 0.0;
+      for (int d = l; d < D; d += 32) {
+        const double u = static_cast<double>(X[a * D + d]) - static_cast<double>(X[b * D + d]);
+        t = std::fma(u, u, t);
+      }
+      v[l] = t;
     }
-    return t;
+    for (int o = 16; o > 0; o >>= 1)
+      for (int l = 0; l < o; ++l) v[l] = v[l] + v[l + o];
+    return v[0];
   };
   std::vector<i64> centers;
   auto to_centers = [&](i64 n) {

@@ -2497,14 +2497,19 @@ __global__ void k_add_f64(const double* a, double* acc, int64_t n, int first) {
 // k_afk_cdf: q normalised and its cdf (one thread, the reference's order);
 // k_afk_chain: the Metropolis chains (one CTA; thread 0 draws, the block
 // computes distance_to_centers as a min over centers, exact in any order).
-__device__ __forceinline__ double afk_sqd(const float* X, int D, int64_t a, int64_t b) {
+// squared_distance by one warp: lane l sums d = l, l + 32, ... (explicit fma,
+// ascending), then the xor butterfly (every lane ends with the same value:
+// the halving tree v[l] += v[l + o], o = 16..1, that the oracle restates)
+__device__ __forceinline__ double afk_sqd_warp(const float* X, int D, int64_t a, int64_t b, int lane) {
   const float* xa = X + a * D;
   const float* xb = X + b * D;
   double t = 0.0;
-  for (int d = 0; d < D; ++d) {
+  for (int d = lane; d < D; d += 32) {
     const double v = static_cast<double>(__ldg(xa + d)) - static_cast<double>(__ldg(xb + d));
     t = fma(v, v, t);
   }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(kFull, t, o);
   return t;
 }
 struct AfkState {
@@ -2526,8 +2531,12 @@ __device__ __forceinline__ double afk_unit(AfkState& s) { return static_cast<dou
 
 __global__ void k_afk_q(const float* X, int64_t N, int D, const int64_t* centers, double* q) {
   const int64_t c0 = centers[0];
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x)
-    q[i] = afk_sqd(X, D, i, c0);
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; i < N; i += nw) {
+    const double d = afk_sqd_warp(X, D, i, c0, lane);
+    if (lane == 0) q[i] = d;
+  }
 }
 __global__ void k_afk_cdf(int64_t N, double* q, double* cdf) {
   double sum = 0.0;
@@ -2559,8 +2568,8 @@ __global__ void __launch_bounds__(kAfkThreads) k_afk_chain(const float* X, int64
   __syncthreads();
   // distance_to_centers (seeding.cpp:41-49) of row n to the first nc centers
   auto to_centers = [&](int64_t n, int nc) -> double {
-    double best = INFINITY;
-    for (int k = tid; k < nc; k += kAfkThreads) best = fmin(best, afk_sqd(X, D, n, centers[k]));
+    double best = INFINITY;  // warp per center
+    for (int k = warp; k < nc; k += kAfkThreads / 32) best = fmin(best, afk_sqd_warp(X, D, n, centers[k], lane));
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) best = fmin(best, __shfl_xor_sync(kFull, best, o));
     __syncthreads();
@@ -2607,11 +2616,11 @@ __global__ void __launch_bounds__(kAfkThreads) k_afk_chain(const float* X, int64
       }
     }
     if (dx <= 0.0) {  // every proposal duplicated a chosen center: farthest point (first on ties)
-      double best = -1.0;
+      double best = -1.0;  // warp per row (rows ascending within a warp: first max kept)
       int64_t bi = -1;
-      for (int64_t i = tid; i < N; i += kAfkThreads) {
+      for (int64_t i = warp; i < N; i += kAfkThreads / 32) {
         double d = INFINITY;
-        for (int k = 0; k < nc; ++k) d = fmin(d, afk_sqd(X, D, i, centers[k]));
+        for (int k = 0; k < nc; ++k) d = fmin(d, afk_sqd_warp(X, D, i, centers[k], lane));
         if (d > best) best = d, bi = i;
       }
 #pragma unroll
