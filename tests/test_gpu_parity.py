@@ -801,3 +801,21 @@ def test_afkmc2_degenerate_data(gpu, oracle):
     with pytest.raises(V.VmfaError):
         sess.afkmc2_seed(6, 5, 1)
     sess.close()
+
+
+def test_afkmc2_fallback_path(oracle, gpu):
+    """Many duplicated rows: chains whose every proposal duplicates a chosen
+    center take the farthest-point fallback (seeding.cpp:105-117); seeds,
+    stream state and distance count still match the oracle bit for bit."""
+    O, V = oracle, gpu
+    rng = np.random.default_rng(4)
+    base = rng.normal(0, 3, (7, 16)).astype(np.float32)
+    X = np.repeat(base, 60, axis=0)
+    rng.shuffle(X)
+    seed = O.hash_combine(9, O.INIT_SALT)
+    s_or, st_or, n_or = O.afkmc2_seed(X, 7, 2, seed)
+    assert n_or > X.shape[0] + 2 * sum(range(1, 7))  # the fallback ran
+    sess = V.Session(7, 16, 1, 2, 2, X)
+    s_g, st_g, n_g = sess.afkmc2_seed(7, 2, seed)
+    assert np.array_equal(s_g, s_or) and np.array_equal(st_g, st_or) and n_g == n_or
+    sess.close()
