@@ -1004,6 +1004,8 @@ int vmfa_ctx_create(vmfa_ctx** out, int device, int C, int D, int H, int Cp, int
     const int64_t pairs = static_cast<int64_t>(N) * Cp;
     const int64_t target = (pairs + sm_count() * 8 - 1) / (sm_count() * 8);
     x->stats_rows = static_cast<int>(std::min<int64_t>(1024, std::max<int64_t>(256, (target + 31) / 32 * 32)));
+    if (const char* v = std::getenv("VMFA_STATS_ROWS"))  // experiments: K-pairs per statistics item
+      x->stats_rows = static_cast<int>(std::min<int64_t>(1024, std::max<int64_t>(32, std::atoll(v) / 32 * 32)));
     const int64_t max_items = C + (pairs + x->stats_rows - 1) / x->stats_rows;
     A(x->stats_part, static_cast<size_t>(max_items) * stats_part_stride(dm));
     const int64_t bal = std::max<int64_t>(128, static_cast<int64_t>(N) / (4 * sm_count()));
