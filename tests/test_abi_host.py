@@ -29,7 +29,9 @@ def test_header_declares_the_boundary():
     names = declared_functions()
     for must in ("vmfa_ctx_create", "vmfa_estep", "vmfa_iterate", "vmfa_accumulate_suffstats",
                  "vmfa_update_params", "vmfa_precompute", "vmfa_truncated_free_energy",
-                 "vmfa_exchange_buffer", "vmfa_host_initialize", "vmfa_gen_synthetic"):
+                 "vmfa_exchange_buffer", "vmfa_host_initialize", "vmfa_gen_synthetic",
+                 "vmfa_exact_log_likelihood", "vmfa_em_full_step", "vmfa_afkmc2_seed",
+                 "vmfa_cooc_sparse", "vmfa_cooc_local_list", "vmfa_cooc_select"):
         assert must in names
 
 
