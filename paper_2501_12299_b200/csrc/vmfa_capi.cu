@@ -179,6 +179,24 @@ struct vmfa_ctx {
   cudaEvent_t x_ready = nullptr, x_free = nullptr;
   bool x_pending = false;
   bool have_estep = false;
+  // CUDA graphs of vmfa_iterate (default; VMFA_GRAPH=0 disables): one per host-side pre-state
+  // (pointer parities, lookahead flags); replays restore the recorded post-state
+  unsigned long long* sit = nullptr;  // (seed, E-step index) read by k_extra
+  bool capturing = false;
+  bool graph_off = false;
+  struct HostState {
+    int *g, *gcnt, *g_new, *gcnt_new;
+    double *pi, *pi2, *mu, *mu2, *lam, *lam2, *psi, *psi2;
+    bool prescored, kinv, have_estep;
+    int mode;
+    bool lookahead;
+    bool operator==(const HostState& o) const { return std::memcmp(this, &o, sizeof *this) == 0; }
+  };
+  struct GraphEntry {
+    HostState pre, post;
+    cudaGraphExec_t exec;
+  };
+  std::vector<GraphEntry> graphs;
   // dumps (parity only)
   bool dump = false;
   int *dump_c = nullptr, *dump_ct = nullptr;
@@ -503,7 +521,11 @@ int estep_local(vmfa_ctx* x, uint64_t seed, uint64_t it, int mode, bool exchange
   // extras not already covered by U g_a
   {
     const int tok = x->begin(kFamOther, dm.N);
-    CU(launch_extra(dm, x->K, x->g, x->gcnt, seed, it, x->rx, x->rkey, s));
+    if (!x->capturing) {  // (a captured iteration gets them from vmfa_iterate, outside the graph)
+      const unsigned long long sit[2] = {seed, it};
+      CU(cudaMemcpyAsync(x->sit, sit, sizeof sit, cudaMemcpyHostToDevice, s));  // pageable: staged
+    }
+    CU(launch_extra(dm, x->K, x->g, x->gcnt, x->sit, x->rx, x->rkey, s));
     x->end(tok);
   }
   TRY(csr_by_key(x, x->rkey, dm.N, x->ex_off, x->ex_ent, x->ex_items, x->score_rows));
@@ -998,6 +1020,7 @@ int vmfa_ctx_create(vmfa_ctx** out, int device, int C, int D, int H, int Cp, int
   A(x->part_off, Cs + 1);
   A(x->part_ent, N);
   A(x->part_items, Cs + 1);
+  A(x->sit, 2);
   A(x->stats_items, Cs + 1);
   A(x->qctr, 1);
   {
@@ -1085,6 +1108,8 @@ int vmfa_ctx_destroy(vmfa_ctx* x) {
   if (!x) return VMFA_OK;
   cudaSetDevice(x->device);
   if (x->stream) cudaStreamSynchronize(x->stream);
+  for (auto& g : x->graphs) cudaGraphExecDestroy(g.exec);
+  x->graphs.clear();
   if (x->cstream) {
     cudaStreamSynchronize(x->cstream);
     cudaStreamDestroy(x->cstream);
@@ -1582,19 +1607,43 @@ int vmfa_afkmc2_seed(vmfa_ctx* x, int C, int chain_length, uint64_t stream_seed,
   return VMFA_OK;
 }
 
-int vmfa_iterate(vmfa_ctx* x, uint64_t seed, uint64_t iteration, int mode, vmfa_iter_report* rep) {
-  TRY(check_ctx(x));
-  if (mode != VMFA_DIST_KL && mode != VMFA_DIST_EUCLID) return fail(VMFA_ERR_INVALID_ARGUMENT, "mode");
-  int failed = -1;
+namespace {
+vmfa_ctx::HostState host_state(const vmfa_ctx* x, int mode) {
+  vmfa_ctx::HostState h;
+  std::memset(&h, 0, sizeof h);  // (padding compared by memcmp)
+  h.g = x->g, h.gcnt = x->gcnt, h.g_new = x->g_new, h.gcnt_new = x->gcnt_new;
+  h.pi = x->pi, h.pi2 = x->pi2, h.mu = x->mu, h.mu2 = x->mu2;
+  h.lam = x->lam, h.lam2 = x->lam2, h.psi = x->psi, h.psi2 = x->psi2;
+  h.prescored = x->prescored, h.kinv = x->kinv_for_current_K, h.have_estep = x->have_estep;
+  h.mode = mode;
+  h.lookahead = x->lookahead;
+  return h;
+}
+void set_host_state(vmfa_ctx* x, const vmfa_ctx::HostState& h) {
+  x->g = h.g, x->gcnt = h.gcnt, x->g_new = h.g_new, x->gcnt_new = h.gcnt_new;
+  x->pi = h.pi, x->pi2 = h.pi2, x->mu = h.mu, x->mu2 = h.mu2;
+  x->lam = h.lam, x->lam2 = h.lam2, x->psi = h.psi, x->psi2 = h.psi2;
+  x->prescored = h.prescored, x->kinv_for_current_K = h.kinv, x->have_estep = h.have_estep;
+}
+bool graphs_enabled(const vmfa_ctx* x) {
+  static const bool on = [] {  // VMFA_GRAPH=0: plain launches
+    const char* v = std::getenv("VMFA_GRAPH");
+    return !(v && v[0] == '0');
+  }();
+  return on && !x->graph_off && !x->sparse && !x->profile && !x->dump && !x->x_pending;
+}
+}  // namespace
+
+// One main iteration enqueued without a host synchronisation; the statuses
+// of selection, update and precompute land in the pinned readback.
+int iterate_enqueue(vmfa_ctx* x, uint64_t seed, uint64_t iteration, int mode, int* failed) {
   cudaStream_t s = x->stream;
-  // the whole iteration is enqueued without a host synchronisation; the
-  // statuses of selection, update and precompute are read back once at the end
   TRY(estep_local(x, seed, iteration, mode, false));
   TRY(estep_finish(x, false, false));
   TRY(stats_local(x));
   TRY(launch_update_params(x));
   swap_params(x);
-  TRY(run_precompute(x, &failed, false));
+  TRY(run_precompute(x, failed, false));
   TRY(free_energy_local(x, x->lookahead));
   CU(launch_count_empty(x->pi, x->dm.C, x->n_empty, s));
   IterStatus* h = x->hstat;
@@ -1603,6 +1652,51 @@ int vmfa_iterate(vmfa_ctx* x, uint64_t seed, uint64_t iteration, int mode, vmfa_
   CU(cudaMemcpyAsync(&h->model, x->st_model, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
   CU(cudaMemcpyAsync(&h->empty, x->n_empty, sizeof(int), cudaMemcpyDeviceToHost, s));
   CU(cudaMemcpyAsync(h->scal, x->scal, 4 * sizeof(double), cudaMemcpyDeviceToHost, s));
+  return VMFA_OK;
+}
+
+int vmfa_iterate(vmfa_ctx* x, uint64_t seed, uint64_t iteration, int mode, vmfa_iter_report* rep) {
+  TRY(check_ctx(x));
+  if (mode != VMFA_DIST_KL && mode != VMFA_DIST_EUCLID) return fail(VMFA_ERR_INVALID_ARGUMENT, "mode");
+  int failed = -1;
+  cudaStream_t s = x->stream;
+  bool done = false;
+  if (graphs_enabled(x)) {
+    // the same launch sequence as a CUDA graph, captured once per host-side
+    // pre-state (in steady state two: g and the parameter sets alternate)
+    const unsigned long long sit[2] = {seed, iteration};
+    CU(cudaMemcpyAsync(x->sit, sit, sizeof sit, cudaMemcpyHostToDevice, s));
+    const vmfa_ctx::HostState pre = host_state(x, mode);
+    vmfa_ctx::GraphEntry* e = nullptr;
+    for (auto& g : x->graphs)
+      if (g.pre == pre) e = &g;
+    if (e) {
+      set_host_state(x, e->post);
+    } else {
+      x->capturing = true;
+      cudaGraph_t graph = nullptr;
+      cudaError_t ce = cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal);
+      int r = ce == cudaSuccess ? iterate_enqueue(x, seed, iteration, mode, &failed) : VMFA_ERR_CUDA;
+      if (ce == cudaSuccess) ce = cudaStreamEndCapture(s, &graph);
+      x->capturing = false;
+      cudaGraphExec_t exec = nullptr;
+      if (r == VMFA_OK && ce == cudaSuccess && cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess) {
+        x->graphs.push_back({pre, host_state(x, mode), exec});
+        e = &x->graphs.back();
+      } else {  // not capturable here: plain launches from now on
+        cudaGetLastError();
+        set_host_state(x, pre);
+        x->graph_off = true;
+      }
+      if (graph) cudaGraphDestroy(graph);
+    }
+    if (e) {
+      CU(cudaGraphLaunch(e->exec, s));
+      done = true;
+    }
+  }
+  if (!done) TRY(iterate_enqueue(x, seed, iteration, mode, &failed));
+  IterStatus* h = x->hstat;
   CU(cudaStreamSynchronize(s));
   if (h->sel) {
     x->prescored = false;

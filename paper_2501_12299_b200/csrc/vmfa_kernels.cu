@@ -131,8 +131,10 @@ __global__ void k_chunks(const int* cnt, int C, int rows, int* chunks) {
 // estep.cpp:259-260). rkey = r_n if it is not already in U_{a in K(n)} g_a,
 // else the sentinel C (the reference pushes it and the epoch-stamp drops it).
 __global__ void k_extra(Dims dm, const int* __restrict__ K, const int* __restrict__ g,
-                        const int* __restrict__ gcnt, uint64_t seed, uint64_t it, int* rx,
+                        const int* __restrict__ gcnt, const unsigned long long* __restrict__ sit, int* rx,
                         unsigned* rkey) {
+  // (seed, E-step index) from device memory: one captured CUDA graph serves every iteration
+  const uint64_t seed = sit[0], it = sit[1];
   for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < dm.N; n += (int64_t)gridDim.x * blockDim.x) {
     const int r = extra_candidate(seed, it, static_cast<uint64_t>(dm.n0 + n), dm.C);
     bool dup = false;
@@ -2804,9 +2806,9 @@ cudaError_t launch_chunks_from_off(const int* off, int C, int rows, int min1, in
   k_chunks_from_off<<<grid_for(C + 1, 256, 4096), 256, 0, s>>>(off, C, rows, min1, chunks);
   return cudaGetLastError();
 }
-cudaError_t launch_extra(const Dims& dm, const int* K, const int* g, const int* gcnt, uint64_t seed,
-                         uint64_t it, int* rx, unsigned* rkey, cudaStream_t s) {
-  k_extra<<<grid_for(dm.N, 256, 8192), 256, 0, s>>>(dm, K, g, gcnt, seed, it, rx, rkey);
+cudaError_t launch_extra(const Dims& dm, const int* K, const int* g, const int* gcnt,
+                         const unsigned long long* sit, int* rx, unsigned* rkey, cudaStream_t s) {
+  k_extra<<<grid_for(dm.N, 256, 8192), 256, 0, s>>>(dm, K, g, gcnt, sit, rx, rkey);
   return cudaGetLastError();
 }
 

@@ -211,7 +211,7 @@ cudaError_t launch_chunks(const int* cnt, int C, int rows, int* chunks, cudaStre
 cudaError_t launch_offsets_sorted(const unsigned* sorted, int64_t n, int C, int* off, cudaStream_t s);
 cudaError_t launch_items_scan(const int* off, int C, int rows, int min1, int* items, cudaStream_t s);
 cudaError_t launch_extra(const Dims& dm, const int* K, const int* g, const int* gcnt,
-                         uint64_t seed, uint64_t it, int* rx, unsigned* rkey, cudaStream_t s);
+                         const unsigned long long* sit, int* rx, unsigned* rkey, cudaStream_t s);
 cudaError_t launch_score(int mode, const ScoreArgs& a, int grid, cudaStream_t s);
 cudaError_t launch_select(const SelectArgs& a, cudaStream_t s);
 cudaError_t launch_gupdate(const GupdArgs& a, int grid, cudaStream_t s);
