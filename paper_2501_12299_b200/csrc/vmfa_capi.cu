@@ -190,7 +190,12 @@ struct vmfa_ctx {
     bool prescored, kinv, have_estep;
     int mode;
     bool lookahead;
-    bool operator==(const HostState& o) const { return std::memcmp(this, &o, sizeof *this) == 0; }
+    bool operator==(const HostState& o) const {
+      return g == o.g && gcnt == o.gcnt && g_new == o.g_new && gcnt_new == o.gcnt_new && pi == o.pi &&
+             pi2 == o.pi2 && mu == o.mu && mu2 == o.mu2 && lam == o.lam && lam2 == o.lam2 && psi == o.psi &&
+             psi2 == o.psi2 && prescored == o.prescored && kinv == o.kinv && have_estep == o.have_estep &&
+             mode == o.mode && lookahead == o.lookahead;
+    }
   };
   struct GraphEntry {
     HostState pre, post;
@@ -910,6 +915,9 @@ int vmfa_ctx_create(vmfa_ctx** out, int device, int C, int D, int H, int Cp, int
                 static_cast<long long>(n_local));
   if (H + 1 > 65) return fail(VMFA_ERR_UNSUPPORTED, "H > 64 not supported by this build");
   if (Cp > 8 || Cp * G + 1 > 256) return fail(VMFA_ERR_UNSUPPORTED, "C' <= 8 and C'G+1 <= 256 required");
+  // the g-selection kernels hold the G-1 picks and the output row in fixed
+  // 64-entry arrays (k_gupdate, k_gselect_dense, k_cooc_select)
+  if (G > 64) return fail(VMFA_ERR_UNSUPPORTED, "G <= 64 required by this build");
   if (n_local * Cp >= (int64_t{1} << 31)) return fail(VMFA_ERR_UNSUPPORTED, "shard too large (N*C' >= 2^31)");
   if (!vmfa_device_available()) return fail(VMFA_ERR_NO_DEVICE, "no sm_100 CUDA device visible");
   CU(cudaSetDevice(device));
@@ -1609,8 +1617,7 @@ int vmfa_afkmc2_seed(vmfa_ctx* x, int C, int chain_length, uint64_t stream_seed,
 
 namespace {
 vmfa_ctx::HostState host_state(const vmfa_ctx* x, int mode) {
-  vmfa_ctx::HostState h;
-  std::memset(&h, 0, sizeof h);  // (padding compared by memcmp)
+  vmfa_ctx::HostState h{};
   h.g = x->g, h.gcnt = x->gcnt, h.g_new = x->g_new, h.gcnt_new = x->gcnt_new;
   h.pi = x->pi, h.pi2 = x->pi2, h.mu = x->mu, h.mu2 = x->mu2;
   h.lam = x->lam, h.lam2 = x->lam2, h.psi = x->psi, h.psi2 = x->psi2;
@@ -1630,7 +1637,9 @@ bool graphs_enabled(const vmfa_ctx* x) {
     const char* v = std::getenv("VMFA_GRAPH");
     return !(v && v[0] == '0');
   }();
-  return on && !x->graph_off && !x->sparse && !x->profile && !x->dump && !x->x_pending;
+  // (a captured graph records the scorer-diagnostics pointer and kernel
+  // variant: no graphs while those counters are armed)
+  return on && !x->graph_off && !x->sparse && !x->profile && !x->dump && !x->x_pending && !ws_diag_armed();
 }
 }  // namespace
 

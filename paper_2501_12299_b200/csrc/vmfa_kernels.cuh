@@ -267,6 +267,8 @@ struct WsOperands {
   const void* simg;    // one-component B stage images (extra / truncated F), per precompute
   const float* sscl;
 };
+// true while vmfa_diag_scorer_cycles has the scorer counters armed
+bool ws_diag_armed();
 cudaError_t launch_score_ws(int mode, const ScoreArgs& s, const WsOperands& op, int4* jobs, cudaStream_t st,
                             bool build_jobs = true);
 // dense all-pairs pass (exact_log_likelihood): pseudo-anchor groups, per-chunk

@@ -1037,6 +1037,7 @@ cudaError_t launch_dense_csr(int C, int G, int R, int rows, int* off, int* itemo
 int64_t dense_jobs(int nb, int R) { return (int64_t)nb * ((R + kRows - 1) / kRows); }
 
 unsigned long long* g_ws_prof = nullptr;  // set by vmfa_diag_scorer_cycles
+bool ws_diag_armed() { return g_ws_prof != nullptr; }
 int g_ws_dbg = 0;                          // diagnostics flags (enable >> 1)
 constexpr int kProfWords = 16 + 8 * kTraceEvents;
 

@@ -63,10 +63,29 @@ def route_lists(arrays, counts, group=None):
     return out, rc
 
 
+def _on_ctx_stream(sess):
+    """Collectives on the context's own stream: the phase calls enqueue their
+    kernels there, so an all-reduce issued on it is ordered after the
+    producer and before the consumer without a host synchronisation (NCCL
+    orders its work on torch's current stream)."""
+    import torch
+    return torch.cuda.stream(torch.cuda.ExternalStream(sess.stream()))
+
+
 def allreduce_buffer(sess, which: int, group=None):
+    """Sum an exchange buffer across ranks. Stream contract: the reduction is
+    enqueued on the context's stream (NCCL) and the call returns once it is
+    complete, so the next phase call may read the buffer."""
+    import torch
     import torch.distributed as dist
     ptr, n, dt = sess.exchange_buffer(which)
-    dist.all_reduce(device_view(ptr, n, _TYPESTR[dt]), group=group)
+    t = device_view(ptr, n, _TYPESTR[dt])
+    if t.is_cuda:
+        with _on_ctx_stream(sess):
+            dist.all_reduce(t, group=group)
+        torch.cuda.ExternalStream(sess.stream()).synchronize()
+    else:
+        dist.all_reduce(t, group=group)
 
 
 def cooc_exchange(sess, rank: int, world: int, group=None):

@@ -566,6 +566,8 @@ def train_emmfa(sess: Session, cfg: TrainConfig) -> dict:
             converged = True
             break
         prev_f = f
+    if not converged and cfg.halt_on_max_iters:  # run_emmfa_loop, use_eq14 path (trainer.cpp:262-266)
+        raise VmfaError(6, f"full EM did not converge within {cfg.max_iters} iterations")
     report = dict(algo="emmfa", iterations=recs, warmup_iterations=0, main_iterations=len(recs),
                   converged=converged, joint_evals=joints, empty_components=recs[-1]["empty_components"],
                   total_wall_ms=(time.perf_counter() - t_start - excluded) * 1e3)

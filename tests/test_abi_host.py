@@ -61,6 +61,15 @@ def test_invalid_arguments_map_to_invalid_argument(vmfa):
     assert b"invalid sizes" in abi.lib().vmfa_last_error()
 
 
+def test_unsupported_shapes_are_rejected_before_any_device_work(vmfa):
+    from paper_2501_12299_b200 import abi
+    h = C.c_void_p()
+    # G > 64: the g-selection kernels hold the picks in 64-entry arrays; C'=1 keeps C'G+1 <= 256
+    assert abi.lib().vmfa_ctx_create(C.byref(h), 0, 200, 8, 2, 1, 65, 100, 0, 100, None) == 102
+    assert b"G <= 64" in abi.lib().vmfa_last_error()
+    assert abi.lib().vmfa_ctx_create(C.byref(h), 0, 200, 8, 2, 9, 5, 100, 0, 100, None) == 102
+
+
 def test_host_initialize_matches_oracle(oracle, vmfa):
     X = vmfa.gen_synthetic(vmfa.synth_spec(1, N=3000))
     for li, sc in ((1, 0.1), (0, 1.0)):

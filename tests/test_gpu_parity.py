@@ -138,7 +138,11 @@ def test_estep_euclid_and_frozen(oracle, gpu):
     for mode in (1, 0):
         e_or, st_or, F, J, ret, st_g, k = _estep_both(O, V, sess, X, p, st, 5, 2, mode=mode)
         compare_estep(O, e_or, st_or, F, J, ret, st_g, Cp)
-        assert not np.isin(st_g.g[st_g.g >= 0], [1, 5, 9]).any() or True
+        # block 3 skips frozen candidates (pi = 0, estep.cpp:301): a frozen
+        # component appears in no neighbourhood but its own
+        for c in range(C):
+            others = [v for v in st_g.g[c, :st_g.g_count[c]] if v != c]
+            assert not np.isin(others, [1, 5, 9]).any(), (c, others)
     sess.close()
 
 
@@ -759,7 +763,7 @@ def test_train_emmfa_loop_matches_oracle(oracle, gpu):
     X, _ = gaussian_problem(2000, 32, 6, 3, seed=41)
     C, H = 8, 3
     p, st, floor, sess = _setup(O, V, X, C, H, 3, 4)
-    cfg = V.TrainConfig(max_iters=6, epsilon=0.0)
+    cfg = V.TrainConfig(max_iters=6, epsilon=0.0, halt_on_max_iters=False)
     rep = V.train_emmfa(sess, cfg)
     k = O.precompute_all(p)
     for r in rep["iterations"]:
@@ -769,6 +773,10 @@ def test_train_emmfa_loop_matches_oracle(oracle, gpu):
         f_or = O.exact_log_likelihood(X, p, k, threads=4)
         assert abs(r["F"] - f_or) <= 1e-4 * abs(f_or), (r["t"], r["F"], f_or)
     assert rep["joint_evals"] == len(rep["iterations"]) * X.shape[0] * C
+    # halt_on_max_iters (the default): MaxIterExceeded, as run_emmfa_loop's
+    # use_eq14 path (trainer.cpp:262-266)
+    with pytest.raises(V.VmfaError, match="MaxIterExceeded"):
+        V.train_emmfa(sess, V.TrainConfig(max_iters=2, epsilon=0.0))
     sess.close()
 
 
