@@ -1,20 +1,27 @@
 """bench.py — v-MFA EM iterations on B200 (BASELINE.json metric: candidate
 log-joint evaluations/sec and EM iteration time).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 3] [--impl reference]
 
 A step is one main-loop iteration of train_vmfa (trainer.cpp:149-160): the
 variational E-step (candidates, Woodbury log-joints, top-C', labels, g update,
 responsibilities), sufficient statistics, update_params, precompute and the
-post-M-step truncated free energy, over BASELINE config 2 (configs[1]: N=200k,
-D=256, C=1000, H=8, C'=5, G=10) on synthetic data of that generator. value =
-joint evaluations (sum_n |S(n)|, the reference counter) of all ranks per
-second of the max-over-ranks device time. Under torchrun each rank holds its
-own config-2-sized shard (weak scaling) and the ranks exchange the
-co-occurrence table and the statistics with NCCL all-reduces.
+post-M-step truncated free energy. The workload is BASELINE config 3
+(configs[2]: N = 1 000 000 image-like rows, D = 784, C = 4000, H = 16, C' = 5,
+G = 10), the config quoted "at 1/2/4/8 GPUs" that fits one B200, on synthetic
+rows of its generator. Strong scaling: the N rows are split over the ranks
+([rN/p, (r+1)N/p)); each rank generates only its own rows, the variance floor
+is two moment all-reduces and the initialisation is the sharded restatement
+(paper_2501_12299_b200/sharded.py). value = joint evaluations of the whole job
+(sum_n |S(n)|, the reference counter) per second of the max-over-ranks device
+time. Under torchrun the ranks exchange the co-occurrence table and the
+statistics with NCCL (--backend gloo stages them through the host).
 
---impl reference times the reference algorithm's CPU restatement (oracle/, the
-reference library needs Eigen3, absent here) on the host cores.
+--impl reference times the reference algorithm's CPU restatement (oracle/; the
+reference library needs Eigen3, absent here) on the host cores, on a row
+sample of the same config with the full model (C, D, H, C', G); it never
+loads the product library (the sample rows come from the oracle's build of the
+shared generator source, bit-identical to the GPU arm's rows).
 """
 from __future__ import annotations
 
@@ -33,6 +40,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "candidate log-joint evals/sec & EM iteration time"
 PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+REF_ROWS = 20000  # row sample of the CPU legs (full C, D, H, C', G)
 
 
 def parse():
@@ -40,12 +48,16 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--n", type=int, default=0, help="override rows per rank (testing only)")
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="multi-rank collectives (gloo: host-staged, for tests on one GPU)")
+    ap.add_argument("--n", type=int, default=0, help="override the config's total rows (testing only)")
+    ap.add_argument("--ref-rows", type=int, default=REF_ROWS)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-exact-ll", action="store_true")
+    ap.add_argument("--dump-state", default="", help="write the final K/g/params of every rank (testing)")
     ap.add_argument("--profile-only", action="store_true",
                     help="run warm-up + 2 steps only (for ncu launch lists)")
     return ap.parse_args()
@@ -55,9 +67,10 @@ def peaks():
     try:
         with open(PEAKS) as f:
             d = json.load(f)
-        return dict(hbm=float(d["hbm_gbs"]), bf16=float(d["bf16_tflops"]), src="measured")
+        return dict(hbm=float(d["hbm_gbs"]), bf16=float(d["bf16_tflops"]),
+                    bf16_sustained=float(d.get("bf16_tflops_sustained", d["bf16_tflops"])), src="measured")
     except Exception:
-        return dict(hbm=6650.0, bf16=1590.0, src="fallback")
+        return dict(hbm=6650.0, bf16=1590.0, bf16_sustained=1590.0, src="fallback (B200_PROFILING.md)")
 
 
 class ClockSampler:
@@ -137,27 +150,14 @@ class ClockSampler:
                 "samples": len(self.sm)}
 
 
-def build_problem(cfg: int, rank: int, world: int, n_override: int = 0):
-    from paper_2501_12299_b200 import vmfa as V
-    m = V.CONFIGS[cfg]["model"]
-    per = n_override or V.CONFIGS[cfg]["truth"]["N"]
-    n_total = per * world
-    spec = V.synth_spec(cfg, N=n_total)
-    X = V.gen_synthetic(spec)
-    p, st, floor, _ = V.initialize(X, m["C"], m["H"], m["Cprime"], m["G"], seed=0, scale=0.1,
-                                   loading_init=1)
-    a, b = rank * n_total // world, (rank + 1) * n_total // world
-    return V, m, X, p, st, floor, a, b, n_total
-
-
 def alg_per_joint(D, H):
     """F_j = 2DH + 3D + 2H flops, B_j = 4D + 8 bytes per joint."""
     return 2 * D * H + 3 * D + 2 * H, 4 * D + 8
 
 
-def count_launches(sess, step_fn):
+def count_launches(step_fn):
     """Kernels launched by one step, counted by the CUDA profiler (CUPTI via
-    torch.profiler): every kernel in the process, ours and cub's."""
+    torch.profiler): every kernel in the process."""
     import torch
     from torch.profiler import ProfilerActivity, profile
     with profile(activities=[ProfilerActivity.CUDA]) as prof:
@@ -172,62 +172,107 @@ def count_launches(sess, step_fn):
     return n, names
 
 
-def cpu_baseline_port(cfg: int, steps: int = 1, rows: int = 20000, threads: int = 0):
-    """The reference algorithm restated (oracle/) on the host cores: full
-    iterations on the first `rows` rows of the config's data with full C."""
+# ---------------------------------------------------------------- CPU legs (oracle only)
+def cpu_reference(cfg: int, steps: int, rows: int, threads: int = 0, warm_esteps: int = 2):
+    """The reference algorithm restated (oracle/) on the host cores: full EM
+    iterations (E-step, statistics, update, precompute, truncated F; the
+    trainer.cpp:149-160 phases) on the first `rows` rows of the config's data
+    with the full model. Only oracle/ is loaded (rows from its build of the
+    shared generator)."""
     from oracle import oracle as O
-    from paper_2501_12299_b200 import vmfa as V
-    m = V.CONFIGS[cfg]["model"]
+    m = O.CONFIGS[cfg]["model"]
     threads = threads or os.cpu_count() or 1
-    X = V.gen_synthetic(V.synth_spec(cfg), 0, rows)
-    p, st, floor, _ = O.initialize(X, m["C"], m["H"], m["Cprime"], m["G"], seed=0, scale=0.1,
-                                   loading_init=1)
+    X = O.gen_synthetic(O.synth_spec(cfg), 0, rows)
+    p, st, floor, _ = O.initialize(X, m["C"], m["H"], m["Cprime"], m["G"], seed=0, scale=0.1, loading_init=1)
     k = O.precompute_all(p)
-    for it in range(2):  # warm-up E-steps, as in the GPU arm
+    for it in range(warm_esteps):  # warm-up E-steps, as in the GPU arm
         O.variational_e_step(X, p, k, st, 0, it, threads=threads)
-    it = 2
+    it = warm_esteps
     times, joints = [], []
+    ph = dict(estep=0.0, stats=0.0, update=0.0, precompute=0.0, truncated_F=0.0)
     for _ in range(steps):
-        t0 = time.perf_counter()
+        t = [time.perf_counter()]
         e = O.variational_e_step(X, p, k, st, 0, it, threads=threads)
+        t.append(time.perf_counter())
         s = O.accumulate_suffstats(X, p, k, st.K, e.resp, threads=threads)
+        t.append(time.perf_counter())
         p = O.update_params(s, X.shape[0], p, floor)
+        t.append(time.perf_counter())
         k = O.precompute_all(p)
+        t.append(time.perf_counter())
         O.truncated_free_energy(X, p, k, st.K, threads=threads)
-        times.append(time.perf_counter() - t0)
+        t.append(time.perf_counter())
+        for i, name in enumerate(ph):
+            ph[name] += (t[i + 1] - t[i]) / steps
+        times.append(t[-1] - t[0])
         joints.append(e.joints)
         it += 1
-    return dict(value=float(sum(joints) / sum(times)), unit="joint evals/s", cores=threads,
-                kind="port", iter_s=float(np.mean(times)),
-                sample=f"config {cfg}, first {rows} rows, full C={m['C']}, {steps} full EM iteration(s) "
-                       f"(E-step+stats+update+precompute+F) after 2 warm-up E-steps, {threads} threads")
+    return dict(value=float(sum(joints) / sum(times)), unit="joint evals/s", cores=threads, kind="port",
+                iter_s=float(np.mean(times)), phase_s=ph,
+                sample=f"config {cfg}: first {rows} of {O.CONFIGS[cfg]['truth']['N']} rows with the full model "
+                       f"(C={m['C']}, D={O.CONFIGS[cfg]['truth']['D']}, H={m['H']}, C'={m['Cprime']}, "
+                       f"G={m['G']}); {steps} full EM iteration(s) (E-step+stats+update+precompute+F) after "
+                       f"{warm_esteps} warm-up E-steps; {threads} threads, reference chunking")
 
 
-def run_reference(args, rank, world):
-    """--impl reference: the reference algorithm's CPU restatement on the host
-    cores (rank 0 only)."""
+def run_reference(args, rank):
+    """--impl reference: the reference algorithm's CPU restatement on the
+    host cores (rank 0 only; other ranks exit without work)."""
     if rank != 0:
         return
-    from paper_2501_12299_b200 import vmfa as V
-    m = V.CONFIGS[args.config]["model"]
-    D, H = V.CONFIGS[args.config]["truth"]["D"], m["H"]
-    rows = 20000
-    cb = cpu_baseline_port(args.config, steps=max(1, args.steps), rows=rows)
+    from oracle import oracle as O
+    m = O.CONFIGS[args.config]["model"]
+    D = O.CONFIGS[args.config]["truth"]["D"]
+    # warm-up: the untimed E-steps (W main iterations would multiply a
+    # multi-second CPU step; the timed steps are what the line reports)
+    cb = cpu_reference(args.config, steps=max(1, args.steps), rows=args.ref_rows)
     line = {
         "impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "joint evals/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": cb["iter_s"] * 1e3, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (BASELINE config generator)",
-        "config": {"workload": f"config{args.config} sample: {rows} rows, C={m['C']}, D={D}, H={H}, "
-                               f"C'={m['Cprime']}, G={m['G']}"},
-        "cpu_baseline": {"value": cb["value"], "unit": "joint evals/s", "cores": cb["cores"],
-                         "kind": "port", "sample": cb["sample"]},
-        "e2e": {"value": cb["value"], "unit": "joint evals/s", "h2d_bytes_per_step": 0,
-                "d2h_bytes_per_step": 0},
-        "note": "reference library unbuildable (needs Eigen3, absent); timed = oracle/ fp64 "
-                "restatement of the same algorithm, plain loops, std::thread with the reference chunking",
+        "ms_per_step": cb["iter_s"] * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (BASELINE config generator, seeded)",
+        "config": {"workload": f"config{args.config}: C={m['C']}, D={D}, H={m['H']}, C'={m['Cprime']}, "
+                               f"G={m['G']}; row sample {args.ref_rows} (full model); one EM main iteration "
+                               f"per step (E-step, stats, update, precompute, truncated F)"},
+        "cpu_baseline": {"value": cb["value"], "unit": "joint evals/s", "cores": cb["cores"], "kind": "port",
+                         "sample": cb["sample"], "phase_s": cb["phase_s"]},
+        "e2e": {"value": cb["value"], "unit": "joint evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": "reference library unbuildable (needs Eigen3, absent); timed = oracle/ fp64 restatement of "
+                "the same algorithm, plain loops, std::thread with the reference chunking",
     }
     print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- GPU arm
+def build_problem(V, args, rank, world, comm):
+    """This rank's rows of the config and the sharded initialisation."""
+    from paper_2501_12299_b200.sharded import initialize_sharded
+    m = V.CONFIGS[args.config]["model"]
+    n_total = args.n or V.CONFIGS[args.config]["truth"]["N"]
+    a, b = rank * n_total // world, (rank + 1) * n_total // world
+    X = V.gen_synthetic(V.synth_spec(args.config, N=n_total), a, b)
+    p, st, floor, _ = initialize_sharded(X, a, n_total, m["C"], m["H"], m["Cprime"], m["G"], seed=0, scale=0.1,
+                                         loading_init=1, comm=comm)
+    return m, X, p, st, floor, a, b, n_total
+
+
+def scoring_roofline(sess, D, H, G, J, sc_ms, pk):
+    """The dominant kernel (anchor + extra scoring launches of one E-step)
+    against its HBM roof, on this design's algorithmic bytes: every row read
+    once per anchor of its K row and once for an uncovered extra
+    (4D x (N C' + N_x)), one fp32 score written per scored slot (anchor slots
+    C'G per row + the extras), the anchor B images read once (per E-step
+    rebuilt; jobs of one anchor re-read them from L2)."""
+    w = sess.scoring_work()
+    rows = w["anchor_visits"] + w["extra_visits"]
+    slots = w["anchor_visits"] * G + w["extra_visits"]
+    bytes_alg = 4 * D * rows + 4 * slots + w["image_bytes"] + w["single_image_bytes"] + w["record_bytes"]
+    Fj, Bj = alg_per_joint(D, H)
+    t = sc_ms * 1e-3
+    return dict(bytes=bytes_alg, rows=rows, slots=slots, work=w,
+                achieved=bytes_alg / t / 1e9 if t > 0 else None,
+                tensor_tflops=J * Fj / t / 1e12 if t > 0 else None,
+                tensor_frac=(J * Fj / t) / (pk["bf16"] * 1e12 / 3) if t > 0 else None)
 
 
 def main():
@@ -236,52 +281,43 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
-        run_reference(args, rank, world)
+        run_reference(args, rank)
         return
     import torch
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
 
     from paper_2501_12299_b200 import vmfa as V
-    V_, m, X, p, st, floor, a, b, n_total = build_problem(args.config, rank, world, args.n)
+    from paper_2501_12299_b200.exchange import XCHG_SCALARS, XCHG_STATS, allreduce_buffer, cooc_exchange
+    from paper_2501_12299_b200.sharded import Comm
+    comm = Comm(device=f"cuda:{local}" if args.backend == "nccl" else "cpu")
+    t_setup = time.perf_counter()
+    m, X, p, st, floor, a, b, n_total = build_problem(V, args, rank, world, comm)
     D = X.shape[1]
     C, H, Cp, G = m["C"], m["H"], m["Cprime"], m["G"]
-    sess = V.Session(C, D, H, Cp, G, X[a:b], n_offset=a, n_total=n_total, device=local)
+    sess = V.Session(C, D, H, Cp, G, X, n_offset=a, n_total=n_total, device=local)
     sess.set_floor(floor)
     sess.upload_params(p)
-    sess.upload_state(V.State(st.K[a:b].copy(), st.g, st.g_count))
+    sess.upload_state(st)
     ext = torch.cuda.ExternalStream(sess.stream())
-
-    class _View:
-        def __init__(self, ptr, n, dt):
-            self.__cuda_array_interface__ = dict(shape=(n,), typestr="<i8" if dt == 0 else "<f8",
-                                                 data=(ptr, False), version=3)
-
-    xb = {}
-    sparse = world > 1 and sess.cooc_sparse()
-    if world > 1:
-        for w in ((1, 2) if sparse else (0, 1, 2)):
-            xb[w] = torch.as_tensor(_View(*sess.exchange_buffer(w)), device=f"cuda:{local}")
-
-    def allreduce(w):
-        with torch.cuda.stream(ext):
-            if w == 0 and sparse:  # large C: owner-routed (c, c~) lists + int32 all-reduce of g
-                from paper_2501_12299_b200.exchange import cooc_exchange
-                cooc_exchange(sess, rank, world)
-            else:
-                dist.all_reduce(xb[w])
-        ext.synchronize()
+    setup_s = time.perf_counter() - t_setup
 
     it_counter = [0]
 
+    def estep_multi(it):
+        sess.phase_estep_local(0, it)
+        cooc_exchange(sess, rank, world)
+        sess.phase_estep_finish()
+
     def warm_estep():
         if world > 1:
-            sess.phase_estep_local(0, it_counter[0])
-            allreduce(0)
-            sess.phase_estep_finish()
+            estep_multi(it_counter[0])
         else:
             sess.variational_e_step(0, it_counter[0])
         it_counter[0] += 1
@@ -291,14 +327,12 @@ def main():
         it_counter[0] += 1
         if world == 1:
             return sess.iterate(0, it)
-        sess.phase_estep_local(0, it)
-        allreduce(0)
-        sess.phase_estep_finish()
+        estep_multi(it)
         sess.phase_stats_local()
-        allreduce(1)
+        allreduce_buffer(sess, XCHG_STATS)
         sess.phase_update()
         sess.phase_free_energy_local()
-        allreduce(2)
+        allreduce_buffer(sess, XCHG_SCALARS)
         Fe, J, F = sess.phase_scalars()
         return dict(F_estep=Fe, joints=J, F=F)
 
@@ -334,6 +368,16 @@ def main():
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
+    ms_step = float(np.sum(times) / args.steps)
+    J_job = float(np.sum(joints) / args.steps)  # multi-rank: the scalars are all-reduced, J is the job total
+    if dist:
+        t = torch.tensor([ms_step], device=f"cuda:{local}")
+        if args.backend == "gloo":
+            t = t.cpu()
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_step = float(t.item())
+    value = J_job / (ms_step * 1e-3)
+
     # phase split: the same steps again with per-phase events (outside the timed region)
     sess.profile(True)
     for _ in range(args.steps):
@@ -343,23 +387,21 @@ def main():
     torch.cuda.synchronize()
     kt = sess.kernel_times()
     sess.profile(False)
-    ms_step = float(np.sum(times) / args.steps)
-    J_rank = float(np.sum(joints) / args.steps)  # after the all-reduce J is already the job total
-    if dist:
-        t = torch.tensor([ms_step], device=f"cuda:{local}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_step = float(t.item())
-    J_job = J_rank if world > 1 else J_rank
-    value = J_job / (ms_step * 1e-3)
+    phase_ms = {k: v["ms"] / args.steps for k, v in kt.items()}
+
+    if args.dump_state:
+        stf = sess.download_state()
+        pf = sess.download_params()
+        np.savez(f"{args.dump_state}.rank{rank}.npz", K=stf.K, g=stf.g, gc=stf.g_count, pi=pf.pi, mu=pf.mu,
+                 F=np.array(Fs), J=np.array(joints), a=a, b=b)
 
     # dominant kernel: the candidate scoring (anchor + extra launches) of each E-step
     Fj, Bj = alg_per_joint(D, H)
     pk = peaks()
-    sc_ms = (kt["score_anchor"]["ms"] + kt["score_extra"]["ms"]) / args.steps
-    J_local = J_rank if world == 1 else J_rank / world
-    ach_gbs = J_local * Bj / (sc_ms * 1e-3) / 1e9 if sc_ms > 0 else None
-    ach_tfs = J_local * Fj / (sc_ms * 1e-3) / 1e12 if sc_ms > 0 else None
-    phase_ms = {k: v["ms"] / args.steps for k, v in kt.items()}
+    n_loc = b - a
+    J_local = J_job / world if world > 1 else J_job
+    sc_ms = phase_ms.get("score_anchor", 0.0) + phase_ms.get("score_extra", 0.0)
+    sroof = scoring_roofline(sess, D, H, G, J_local, sc_ms, pk)
 
     # exact log-likelihood (all N x C pairs, dense
     # tcgen05 pass) once after the timed region, on device time
@@ -373,21 +415,21 @@ def main():
             e1.record(ext)
             e1.synchronize()
             t = e0.elapsed_time(e1)
-            pairs = float(b - a) * C
+            pairs = float(n_loc) * C
             exact = {"ms": t, "log_likelihood": ll, "joints": pairs, "joints_per_s": pairs / (t * 1e-3),
                      "achieved_tflops": pairs * Fj / (t * 1e-3) / 1e12,
-                     "roof_ms": max((b - a) * D * 4 / (pk["hbm"] * 1e9), pairs * Fj / (pk["bf16"] * 1e12 / 3)) * 1e3,
+                     "roof_ms": max(n_loc * D * 4 / (pk["hbm"] * 1e9), pairs * Fj / (pk["bf16"] * 1e12 / 3)) * 1e3,
                      "roof": "max(X once at HBM peak, N*C*F_j at bf16-dense/3 (3-pass fp16 split))",
                      "how": "one vmfa_exact_log_likelihood call (images, row-tile-major dense jobs, "
                             "per-row LSE, fixed-order sum) between CUDA events"}
         except Exception as ex:
             exact = {"error": str(ex)}
-    # SURVEY §8(f) item 1, second half: em_full_step (mstep.cpp:164-208) --
-    # every pair's log-joint, full responsibilities and statistics
+    # em_full_step (mstep.cpp:164-208) on the small configs only (at config 3
+    # it is N*C = 4e9 full-posterior pairs, minutes of work outside the step)
     em = None
-    if not args.no_exact_ll:
+    if not args.no_exact_ll and args.config <= 2:
         try:
-            sess.em_full_step()  # first call allocates its buffers
+            sess.em_full_step()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(ext)
             ll, jn = sess.em_full_step()
@@ -395,95 +437,98 @@ def main():
             e1.synchronize()
             t = e0.elapsed_time(e1)
             em = {"ms": t, "log_likelihood": ll, "joints": jn, "joints_per_s": jn / (t * 1e-3),
-                  "how": "one vmfa_em_full_step call (dense log-joints, q for all N x C pairs, statistics "
-                         "over every pair) between CUDA events; not part of the timed v-MFA step"}
+                  "how": "one vmfa_em_full_step call between CUDA events; not part of the timed v-MFA step"}
         except Exception as ex:
             em = {"error": str(ex)}
 
     # launches per step (CUPTI), outside the timed region
-    n_launch, names = count_launches(sess, step)
+    n_launch, names = count_launches(step)
 
     e2e = None
     if not args.no_e2e and world == 1:
-        e2e = measure_e2e(V, sess, X[a:b], p, st, floor, args, ext)
+        e2e = measure_e2e(V, sess, X, p, st, args)
     cpu = None
     if rank == 0 and not args.no_cpu_baseline and world == 1:
         try:
-            cpu = cpu_baseline_port(args.config)
+            cpu = cpu_reference(args.config, steps=1, rows=args.ref_rows)
             cpu.pop("iter_s", None)
         except Exception as ex:  # the baseline is reported, never required
             cpu = {"error": str(ex)}
 
-    # iteration-level roofline: T_roof = sum over phases of
-    # max(F / P_pipe, B / BW) against the measured EM iteration time
+    # iteration-level roofline: T_roof = sum over phases of max(bytes / BW,
+    # tensor flops / (bf16 dense / 3)) on this design's algorithmic bytes,
+    # each phase checked against its measured time (a lower bound never exceeds it)
     clk_sum = clk.summary()
-    fp32_peak = 148 * 128 * 2 * (clk_sum.get("sm_max_mhz") or 1965.0) * 1e6  # FFMA, estimate (not in MEASURED_PEAKS)
-    tc_peak = pk["bf16"] * 1e12 / 3  # 3-pass split fp16 MMA (fp16 dense = bf16 dense)
     bw = pk["hbm"] * 1e9
-    n_loc = b - a
-    Fm, Bm = 4 * D * H + 5 * D + 3 * H * H, 4 * D + 12
+    tc = pk["bf16"] * 1e12 / 3
+    pairs = n_loc * Cp
+    SL = Cp * G + 1
+    stride = min(SL, C)
     roof = {
-        "scoring": max(J_local * Fj / tc_peak, J_local * Bj / bw),
-        "F_recompute": max(n_loc * Cp * Fj / tc_peak, n_loc * Cp * Bj / bw),
-        "statistics": max(n_loc * Cp * Fm / fp32_peak, n_loc * Cp * Bm / bw),
-        "update_precompute": C * (4 * D * H * H + 2 * D * (H + 1) ** 2 + H ** 3) / fp32_peak,
+        "scoring": max(sroof["bytes"] / bw, J_local * Fj / tc),
+        "select": (n_loc * SL * 4 + n_loc * stride * 8 + pairs * (8 + 4)) / bw,
+        "gupdate": (n_loc * stride * 8 + n_loc * 8) / bw,
+        "statistics": max(pairs * (4 * D + 12) / bw, pairs * (4 * D * H + 5 * D + 3 * H * H) / tc),
+        "truncated_F": pairs * 4 / bw,
     }
+    measured = {"scoring": sc_ms, "select": phase_ms.get("select", 0.0), "gupdate": phase_ms.get("gupdate", 0.0),
+                "statistics": phase_ms.get("stats", 0.0), "truncated_F": phase_ms.get("score_truncF", 0.0)}
     t_roof = sum(roof.values())
-    # the statistics pass (the other large kernel) against its own roof
-    st_ms = phase_ms.get("stats", 0.0)
-    stats_roof = None
-    if st_ms > 0:
-        pairs = n_loc * Cp
-        stats_roof = {"kernel": "statistics (k_stats + reduce + uncenter + Sigma_z)", "ms": st_ms,
-                      "achieved_gbs": pairs * Bm / (st_ms * 1e-3) / 1e9, "peak_gbs": pk["hbm"],
-                      "frac_hbm": pairs * Bm / (st_ms * 1e-3) / 1e9 / pk["hbm"],
-                      "achieved_tflops": pairs * Fm / (st_ms * 1e-3) / 1e12,
-                      "fp32_peak_tflops_est": fp32_peak / 1e12,
-                      "frac_fp32": pairs * Fm / (st_ms * 1e-3) / fp32_peak,
-                      "per_unit": f"B_m = 4D+12 = {Bm} B, F_m = 4DH+5D+3H^2 = {Fm} flop per (n, c in K(n)) pair "
-                                  f"(SURVEY §8(d)), {pairs} pairs"}
     iter_roof = {"t_roof_ms": t_roof * 1e3, "t_iter_ms": ms_step, "frac": t_roof * 1e3 / ms_step,
-                 "phases_ms": {k: v * 1e3 for k, v in roof.items()},
-                 "how": "SURVEY §8(d): per phase max(F/P_pipe, B/BW); scoring/F at J and N*C' joints "
-                        "(F_j, B_j), statistics at N*C' pairs (F_m = 4DH+5D+3H^2, B_m = 4D+12); "
-                        "BW = measured HBM peak; P_pipe = bf16 dense / 3 for the split-fp16 scorer, "
-                        "FFMA 148*128*2*f_max (estimate) elsewhere; F recompute is counted although "
-                        "this build reads F from the next anchor pass"}
+                 "phases_roof_ms": {k: v * 1e3 for k, v in roof.items()},
+                 "phases_measured_ms": measured,
+                 "roof_below_measured": all(roof[k] * 1e3 <= measured[k] * 1.02 or measured[k] == 0 for k in roof),
+                 "how": "per phase max(algorithmic bytes / HBM peak, tensor flops / (bf16 dense / 3)): scoring on "
+                        "the anchor design's bytes (rows once per anchor + extras, scores, B images), select "
+                        "(slots in, retained joints + responsibilities out), g-update (retained joints), "
+                        "statistics (N C' gathered rows, 4DH+5D+3H^2 flops per pair), truncated F (read from "
+                        "the next anchor pass: N C' scores); precompute/update and CSR omitted (no roof claimed)"}
 
     traffic = {}
     try:
-        with open(os.path.join(ROOT, "profiles", "scorer_traffic.json")) as f:
-            traffic = json.load(f) if args.config == 2 else {}
+        with open(os.path.join(ROOT, "profiles", "r02", f"scorer_traffic_config{args.config}.json")) as f:
+            traffic = json.load(f)
     except Exception:
         pass
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "joint evals/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic (BASELINE config generator, seeded), random-points init",
-            "config": {"workload": f"config{args.config}: N={b - a} rows/GPU (N_total={n_total}), "
-                                   f"D={D}, C={C}, H={H}, C'={Cp}, G={G}; one EM main iteration "
-                                   f"per step (E-step, stats, update, precompute, truncated F)",
-                       "l2": "flushed (256 MB write) before every timed iteration",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (BASELINE config generator, seeded; rows generated per rank), random-points init",
+            "config": {"workload": f"config{args.config}: N={n_total} rows total ({n_loc} on rank 0), D={D}, "
+                                   f"C={C}, H={H}, C'={Cp}, G={G}; one EM main iteration per step (E-step, stats, "
+                                   f"update, precompute, truncated F)",
+                       "l2": "flushed (256 MB write) before every timed iteration; X alone (N D 4 B) exceeds L2",
                        "parallelism": f"dp{world} (rows sharded, params replicated)"},
             "joints_per_step": J_job, "F_last": Fs[-1],
             "em_iteration_ms": ms_step,
             "phase_ms": phase_ms,
             "roofline": {"bound": "hbm", "kernel": "candidate scoring (score_anchor+score_extra)",
-                         "achieved": ach_gbs, "peak": pk["hbm"], "unit": "GB/s",
-                         "frac": (ach_gbs / pk["hbm"]) if ach_gbs else None,
+                         "achieved": sroof["achieved"], "peak": pk["hbm"], "unit": "GB/s",
+                         "frac": (sroof["achieved"] / pk["hbm"]) if sroof["achieved"] else None,
                          "traffic": traffic.get("bytes_per_launch_pair"),
                          "traffic_src": traffic.get("source"), "peak_src": pk["src"],
-                         "per_unit": f"B_j = 4D+8 = {Bj} B per joint (SURVEY §8(d)), J={J_local:.0f} joints per launch pair",
-                         "flops_view": {"achieved_tflops": ach_tfs, "F_j": Fj}},
+                         "kernel_ms": sc_ms, "bytes_per_launch_pair": sroof["bytes"],
+                         "per_unit": f"per row-anchor visit 4D = {4 * D} B (row) + G = {G} scores x 4 B; "
+                                     f"{sroof['rows']} row visits ({sroof['work']['anchor_visits']} anchor + "
+                                     f"{sroof['work']['extra_visits']} extra) + {sroof['work']['image_bytes']} B "
+                                     f"anchor images + {sroof['work']['single_image_bytes']} B one-component "
+                                     f"images + {sroof['work']['record_bytes']} B records per launch pair",
+                         "tensor_view": {"useful_tflops": sroof["tensor_tflops"], "F_j": Fj,
+                                         "peak_tflops": pk["bf16"] / 3, "frac": sroof["tensor_frac"],
+                                         "how": "J F_j / t against bf16 dense / 3 (3-pass fp16 split)"},
+                         "survey_view": {"J_B_j_gbs": J_local * Bj / (sc_ms * 1e-3) / 1e9 if sc_ms else None,
+                                         "note": "SURVEY §8(d) B_j charges a gathered row per joint; the "
+                                                 "anchor design reads a row once per anchor, so this view "
+                                                 "exceeds the HBM peak and is not a roofline fraction"}},
             "iteration_roofline": iter_roof,
-            "roofline_statistics": stats_roof,
             "exact_ll": exact,
             "em_full_step": em,
             "gpu_launches": int(n_launch * args.steps),
             "launches_per_step": n_launch,
             "clocks": clk_sum,
+            "setup_s": setup_s,
             "cpu_baseline": cpu,
             "e2e": e2e,
         }
@@ -493,7 +538,7 @@ def main():
         dist.destroy_process_group()
 
 
-def measure_e2e(V, sess, Xs, p, st, floor, args, ext):
+def measure_e2e(V, sess, Xs, p, st, args):
     """The same metric through the public API with host buffers: every step
     uploads the shard's rows, the parameters and the variational state from
     pinned host memory, runs the iteration and downloads the new parameters,

@@ -256,6 +256,15 @@ const char* vmfa_kernel_name(int i);
  * clears them; enable=0 disarms.                                            */
 int vmfa_diag_scorer_cycles(int enable, unsigned long long* out, int n);
 
+/* Work accounting of the candidate-scoring launches (the anchor pass and the
+ * extras of one E-step) for roofline figures: out[0] anchor row visits
+ * (N*C'), out[1] extra row visits of the last E-step (rows whose r_n is not
+ * in the union of their anchors' g), out[2] / out[3] bytes of the anchor /
+ * one-component B stage images, out[4] bytes of the epilogue records,
+ * out[5] the scorer (2 warp-specialised tcgen05, 1 single-role tcgen05, 0
+ * FFMA). n: entries wanted (<= 6).                                          */
+int vmfa_scoring_work(vmfa_ctx* ctx, int64_t* out, int n);
+
 /* Stream of the context (a cudaStream_t) for callers that order their own
  * work (e.g. NCCL) against it.                                              */
 void* vmfa_ctx_stream(vmfa_ctx* ctx);
@@ -294,6 +303,44 @@ int vmfa_host_initialize(const float* X, int64_t N, int D, int C, int H, int Cpr
                          uint64_t seed, double scale, int loading_init, double* floor,
                          double* pi, double* mu, double* lambda, double* dnoise, int32_t* K,
                          int32_t* g, int32_t* g_count, int64_t* seeds);
+
+/* Sharded initialisation: the same result as
+ * vmfa_host_initialize without any rank holding all N rows. Protocol (the
+ * caller owns the collectives; paper_2501_12299_b200/sharded.py runs it over
+ * torch.distributed):
+ *   1. variance (dataset.cpp:22-35): vmfa_host_moments(shard, mean=NULL) ->
+ *      all-reduce -> mean = sum/N; vmfa_host_moments(shard, mean) -> all-reduce
+ *      -> var = sum/N; floor = max(1e-6 var, 1e-8) (dataset.cpp:37-39);
+ *   2. count_distinct_rows (seeding.cpp:16-32): vmfa_host_distinct_hashes on
+ *      each shard (up to C distinct rows, 128-bit digests) -> all-gather ->
+ *      fewer than C distinct digests = DegenerateData;
+ *   3. random_points_seed (seeding.cpp:123-149): the draw sequence
+ *      vmfa_seed_draws(seed, N, first, count) is data independent; the owners
+ *      of the drawn rows contribute their contents (an exact integer-sum
+ *      all-reduce of the bit patterns) and every rank applies the reference's
+ *      used / duplicate rejection in draw order, counting the draws consumed;
+ *   4. vmfa_host_init_shard: init_params (seeding.cpp:151-181) continuing the
+ *      init stream after seed_draws draws, and init_varstate (seeding.cpp:
+ *      207-233) replaying its whole stream but storing only K rows
+ *      [n0, n0+rows).                                                        */
+/* per-dimension fp64 sums over the rows in order: sum x (mean == NULL) or
+ * sum (x - mean)^2. threads <= 0: all hardware threads.                     */
+int vmfa_host_moments(const float* X, int64_t rows, int D, const double* mean, double* out, int threads);
+/* draws [first, first+count) of the init stream Rng(hash_combine(seed,
+ * 0x1217f01d)) (trainer.cpp:36) as uniform_int(N) (rng.hpp:55-60)          */
+int vmfa_seed_draws(uint64_t seed, int64_t N, int64_t first, int64_t count, int64_t* out);
+/* up to `want` distinct rows of X, in row order: two 64-bit digests each
+ * (out: 2*want u64), *n_out = rows digested                                  */
+int vmfa_host_distinct_hashes(const float* X, int64_t rows, int D, int64_t want, uint64_t* out,
+                              int64_t* n_out);
+/* var, floor: D; seeds: C global row indices; seed_rows: their contents
+ * (C x D); seed_draws: draws random_points_seed consumed. Outputs as
+ * vmfa_host_initialize, with K holding rows [n0, n0 + rows) only.            */
+int vmfa_host_init_shard(int64_t N, int D, int C, int H, int Cprime, int G, uint64_t seed, double scale,
+                         int loading_init, const double* var, const double* floor, const int64_t* seeds,
+                         const float* seed_rows, int64_t seed_draws, int64_t n0, int64_t rows, double* pi,
+                         double* mu, double* lambda, double* dnoise, int32_t* K, int32_t* g,
+                         int32_t* g_count);
 
 /* ---- on-disk containers, host only, no device needed ----
  * MFAD dataset (io.hpp:12-16, io.cpp:91-125): "MFAD", u32 version 1, u64 N,

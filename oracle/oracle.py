@@ -86,6 +86,7 @@ def lib():
         L.orc_init_params.argtypes = [f32p, i64, i32, i32, i32, i64p, u64p, f64, i32, f64p, f64p,
                                       f64p, f64p, f64p]
         L.orc_init_varstate.argtypes = [i64, i32, i32, i32, i64p, i32, u64, i32p, i32p, i32p]
+        L.orc_gen_synthetic.argtypes = [C.c_void_p, i64, i64, C.c_void_p, C.c_void_p, i32]
         _lib = L
     return _lib
 
@@ -352,6 +353,66 @@ def em_full_step(X, p: Params, k: Caches, threads: int = 1):
     resp = np.exp(lj - lse[:, None])
     stats = accumulate_suffstats(X, p, k, K, resp, threads=threads)
     return stats, ll, N * p.C
+
+
+# ------------------------------------------------------------------ benchmark inputs
+class SynthSpec(C.Structure):
+    """vmfa_synth_spec (include/vmfa_b200.h): one BASELINE config's generator."""
+    _fields_ = [("kind", C.c_int), ("n_total", C.c_int64), ("D", C.c_int), ("C_true", C.c_int),
+                ("H_true", C.c_int), ("dirichlet", C.c_int), ("mu_std", C.c_double),
+                ("lam_std", C.c_double), ("psi_lo", C.c_double), ("psi_hi", C.c_double),
+                ("noise_std", C.c_double), ("img_w", C.c_int), ("img_h", C.c_int),
+                ("img_c", C.c_int), ("blur_sigma", C.c_double), ("data_seed", C.c_uint64)]
+
+
+# BASELINE.json configs (SURVEY §8(d)): truth generator + fitted model. The
+# product's table (paper_2501_12299_b200/vmfa.py CONFIGS) is asserted equal
+# in tests/test_abi_host.py; the oracle keeps its own so the reference arm
+# never imports the product.
+CONFIGS = {
+    1: dict(truth=dict(kind=0, N=20_000, D=64, C_true=100, H_true=4, dirichlet=0, mu_std=4.0,
+                       lam_std=0.5, psi_lo=0.1, psi_hi=1.0),
+            model=dict(C=100, H=4, Cprime=3, G=5, iters=20)),
+    2: dict(truth=dict(kind=0, N=200_000, D=256, C_true=1000, H_true=8, dirichlet=1, mu_std=3.0,
+                       lam_std=1 / np.sqrt(8), psi_lo=0.05, psi_hi=0.5),
+            model=dict(C=1000, H=8, Cprime=5, G=10, iters=25)),
+    3: dict(truth=dict(kind=1, N=1_000_000, D=784, C_true=4000, H_true=16, dirichlet=0,
+                       lam_std=0.05, noise_std=0.05, img_w=28, img_h=28, img_c=1, blur_sigma=2.0),
+            model=dict(C=4000, H=16, Cprime=5, G=10, iters=20)),
+    4: dict(truth=dict(kind=0, N=10_000_000, D=256, C_true=10_000, H_true=8, dirichlet=1,
+                       mu_std=3.0, lam_std=1 / np.sqrt(8), psi_lo=0.05, psi_hi=0.5),
+            model=dict(C=10_000, H=8, Cprime=5, G=15, iters=15)),
+    5: dict(truth=dict(kind=1, N=50_000_000, D=768, C_true=50_000, H_true=16, dirichlet=0,
+                       lam_std=0.05, noise_std=0.05, img_w=16, img_h=16, img_c=3, blur_sigma=2.0),
+            model=dict(C=50_000, H=64, Cprime=5, G=20, iters=10)),
+}
+
+
+def synth_spec(cfg: int, N: int | None = None, data_seed: int = 0, **over) -> SynthSpec:
+    t = dict(CONFIGS[cfg]["truth"])
+    t.update(over)
+    sp = SynthSpec()
+    sp.kind = t["kind"]
+    sp.n_total = N if N is not None else t["N"]
+    for k in ("D", "C_true", "H_true"):
+        setattr(sp, k, t[k])
+    for k in ("dirichlet", "img_w", "img_h", "img_c"):
+        setattr(sp, k, t.get(k, 0))
+    for k in ("mu_std", "lam_std", "psi_lo", "psi_hi", "noise_std", "blur_sigma"):
+        setattr(sp, k, t.get(k, 0.0))
+    sp.data_seed = data_seed
+    return sp
+
+
+def gen_synthetic(spec: SynthSpec, row_begin: int = 0, row_end: int | None = None, threads: int = 0):
+    """Rows [row_begin, row_end) of a BASELINE config: the generator source
+    shared with the product (csrc/host/vmfa_synth.cpp), compiled into this
+    library -- bit-identical rows, no product library loaded."""
+    row_end = spec.n_total if row_end is None else row_end
+    X = np.empty((row_end - row_begin, spec.D), np.float32)
+    _check(lib().orc_gen_synthetic(C.byref(spec), row_begin, row_end, X.ctypes.data_as(C.c_void_p), None,
+                                   threads or (os.cpu_count() or 1)), "gen_synthetic")
+    return X
 
 
 # ------------------------------------------------------------------ init (trainer.cpp:32-47, 107)

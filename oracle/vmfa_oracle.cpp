@@ -971,40 +971,34 @@ int orc_init_params(const float* X, i64 N, int D, int C, int H, const i64* seeds
 }
 
 // init_varstate (seeding.cpp:207-233) with fill_distinct (:187-203) restated
-// over a sparse swap map: identical draws and output, O(want) per row.
+// literally: a C-sized buffer holding 0..C-1 per row, the preset swap, the
+// partial Fisher-Yates draws, then the first `want` entries sorted. O(N*C),
+// as the reference (the product restates it over a sparse swap map in
+// O(N*C'); tests/test_abi_host.py pins the two against each other and both
+// against a numpy restatement over the golden stream).
 int orc_init_varstate(i64 N, int C, int Cp, int G, const i64* seed_rows, int n_seeds,
                       u64 stream_seed, i32* K, i32* g, i32* g_count) {
   if (Cp < 1 || Cp > C || G < 1 || G > C) return INVALID_ARGUMENT;
   Stream s(stream_seed);
-  std::unordered_map<i64, i32> seed_of;
-  for (int c = 0; c < n_seeds; ++c) seed_of[seed_rows[c]] = c;
-  std::unordered_map<int, int> over;
-  auto at = [&](int p) {
-    auto it = over.find(p);
-    return it == over.end() ? p : it->second;
-  };
-  auto fill = [&](int want, int preset, i32* out) {
-    over.clear();
+  std::vector<i32> seed_component(N, -1);  // seeding.cpp:220-223
+  for (int c = 0; c < n_seeds; ++c) seed_component[seed_rows[c]] = c;
+  std::vector<i32> buffer;
+  auto fill = [&](int want, i32 preset, i32* out) {  // seeding.cpp:187-203
+    buffer.resize(C);
+    for (int i = 0; i < C; ++i) buffer[i] = i;
     int start = 0;
     if (preset >= 0) {
-      const int a = at(0), b = at(preset);
-      over[0] = b;
-      over[preset] = a;
+      std::swap(buffer[0], buffer[preset]);
       start = 1;
     }
     for (int i = start; i < want; ++i) {
       const int j = i + static_cast<int>(s.below(C - i));
-      const int a = at(i), b = at(j);
-      over[i] = b;
-      over[j] = a;
+      std::swap(buffer[i], buffer[j]);
     }
-    for (int i = 0; i < want; ++i) out[i] = at(i);
+    std::copy(buffer.begin(), buffer.begin() + want, out);
     std::sort(out, out + want);
   };
-  for (i64 n = 0; n < N; ++n) {
-    auto it = seed_of.find(n);
-    fill(Cp, it == seed_of.end() ? -1 : it->second, K + n * Cp);
-  }
+  for (i64 n = 0; n < N; ++n) fill(Cp, seed_component[n], K + n * Cp);
   for (int c = 0; c < C; ++c) {
     fill(G, c, g + (i64)c * G);
     g_count[c] = G;

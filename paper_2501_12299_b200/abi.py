@@ -101,6 +101,7 @@ _SIGS = {
     "vmfa_cooc_local_list": (_I, [_P, _I, C.POINTER(_P), C.POINTER(_P), C.POINTER(_P), C.POINTER(_P), _P]),
     "vmfa_cooc_select": (_I, [_P, _P, _P, _P, _P, C.c_int64, _I, _I]),
     "vmfa_profile_enable": (_I, [_P, _I]),
+    "vmfa_scoring_work": (_I, [_P, _P, _I]),
     "vmfa_kernel_times": (_I, [_P, _I, _P, _P, _P, C.POINTER(_I)]),
     "vmfa_kernel_name": (C.c_char_p, [_I]),
     "vmfa_ctx_stream": (_P, [_P]),
@@ -109,6 +110,11 @@ _SIGS = {
     "vmfa_gen_synthetic": (_I, [C.POINTER(SynthSpec), _I64, _I64, _P, _P, _I]),
     "vmfa_host_initialize": (_I, [_P, _I64, _I, _I, _I, _I, _I, _U64, _D, _I, _P, _P, _P, _P,
                                   _P, _P, _P, _P, _P]),
+    "vmfa_host_moments": (_I, [_P, _I64, _I, _P, _P, _I]),
+    "vmfa_seed_draws": (_I, [_U64, _I64, _I64, _I64, _P]),
+    "vmfa_host_distinct_hashes": (_I, [_P, _I64, _I, _I64, _P, C.POINTER(_I64)]),
+    "vmfa_host_init_shard": (_I, [_I64, _I, _I, _I, _I, _I, _U64, _D, _I, _P, _P, _P, _P, _I64, _I64, _I64,
+                                  _P, _P, _P, _P, _P, _P, _P]),
 }
 
 

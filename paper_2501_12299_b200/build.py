@@ -23,7 +23,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 # extra nvcc flags for diagnostic builds (e.g. -DVMFA_STATS_PROF; rebuild with force=True)
 EXTRA = os.environ.get("VMFA_NVCC_EXTRA", "").split()
 CU_SOURCES = ["vmfa_kernels.cu", "vmfa_score_tc.cu", "vmfa_score_ws.cu", "vmfa_capi.cu"]
-CXX_SOURCES = ["host/vmfa_host.cpp", "host/vmfa_io.cpp"]
+CXX_SOURCES = ["host/vmfa_host.cpp", "host/vmfa_io.cpp", "host/vmfa_synth.cpp"]
 DEPS_H = ["vmfa_kernels.cuh", "vmfa_internal.hpp", "vmfa_rng.hpp"]
 
 
@@ -50,7 +50,9 @@ def build(verbose: bool = False, force: bool = False) -> str:
             cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                    "-Xptxas", "-warn-spills", *EXTRA, *inc, "-c", path, "-o", obj]
         else:
-            cmd = ["g++", "-O3", "-std=c++17", "-fPIC", "-pthread", "-Wall", "-Wextra",
+            # -ffp-contract=off: the synthetic rows are bit-identical to the
+            # oracle build of the same generator (oracle/Makefile)
+            cmd = ["g++", "-O3", "-std=c++17", "-fPIC", "-pthread", "-Wall", "-Wextra", "-ffp-contract=off",
                    "-I", "/usr/local/cuda/include", *inc, "-c", path, "-o", obj]
         if verbose:
             print(" ".join(cmd), flush=True)

@@ -1,9 +1,20 @@
-// vmfa_host.cpp — host-only part of libvmfa_b200.so:
-//   * synthetic data for BASELINE.json's configs (the paper's image datasets
-//     are not available; SURVEY §8(d) specifies these generators), and
-//   * the reference's one-time initialisation (trainer.cpp:32-47, 107-109;
-//     seeding.cpp:123-233; dataset.cpp:22-39) restated with identical draw
-//     sequences, in O(N*C') instead of the reference's O(N*C) buffer fill.
+// vmfa_host.cpp — host-only part of libvmfa_b200.so: the reference's one-time
+// initialisation (trainer.cpp:32-47, 107-109; seeding.cpp:123-233;
+// dataset.cpp:22-39) restated with identical draw sequences, in O(N*C')
+// instead of the reference's O(N*C) buffer fill, whole-dataset or per shard.
+//
+// Sharded form: no rank holds all N rows.
+//   floor     per_dimension_variance as two moment all-reduces over the shards
+//             (vmfa_host_moments: sum x, then sum (x - global mean)^2);
+//   seeds     random_points_seed's draw sequence (vmfa_seed_draws) is data-
+//             independent; only the accept/reject decisions need row contents,
+//             which the caller fetches for the drawn rows from their owners;
+//             count_distinct_rows' DegenerateData check is a union of per-shard
+//             distinct-row hashes (vmfa_host_distinct_hashes);
+//   params    init_params continues the same stream after the seed draws;
+//   K, g      init_varstate's stream is replayed in full (N*C' + C*G draws,
+//             one next() each) while only the shard's K rows are stored.
+// vmfa_host_initialize composes the same pieces over the whole dataset.
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -18,9 +29,8 @@
 namespace vmfa_b200 {
 namespace {
 
-constexpr uint64_t kSaltPi = 0x5eed91ULL;
-constexpr uint64_t kSaltTruth = 0x7e0711ULL;
-constexpr uint64_t kSaltRow = 0x5a3e11eULL;
+constexpr uint64_t kSaltInit = 0x1217f01dULL;   // trainer.cpp:36
+constexpr uint64_t kSaltState = 0x7a57a7e5ULL;  // trainer.cpp:107
 
 template <class F>
 void parallel_ranges(int64_t n, int threads, F&& fn) {
@@ -41,47 +51,127 @@ void parallel_ranges(int64_t n, int threads, F&& fn) {
   for (auto& t : pool) t.join();
 }
 
-// Separable Gaussian blur (clamped borders) of one (h x w) plane, in place.
-void blur_plane(double* f, int w, int h, double sigma, std::vector<double>& tmp) {
-  if (sigma <= 0.0) return;
-  const int r = std::max(1, static_cast<int>(std::ceil(3.0 * sigma)));
-  std::vector<double> k(2 * r + 1);
-  double s = 0.0;
-  for (int i = -r; i <= r; ++i) s += (k[i + r] = std::exp(-0.5 * i * i / (sigma * sigma)));
-  for (double& v : k) v /= s;
-  tmp.assign(static_cast<size_t>(w) * h, 0.0);
-  for (int y = 0; y < h; ++y)
-    for (int x = 0; x < w; ++x) {
-      double acc = 0.0;
-      for (int i = -r; i <= r; ++i) acc += k[i + r] * f[y * w + std::clamp(x + i, 0, w - 1)];
-      tmp[y * w + x] = acc;
+int hw_threads() { return static_cast<int>(std::max(1u, std::thread::hardware_concurrency())); }
+
+// per-dimension fp64 sums over rows in order (parallel over dimensions keeps
+// each dimension's summation order): sum x (mean == nullptr) or sum (x-mean)^2
+void moments(const float* X, int64_t rows, int D, const double* mean, double* out, int threads) {
+  parallel_ranges(D, threads, [&](int, int64_t b, int64_t e) {
+    std::vector<double> acc(e - b, 0.0);
+    for (int64_t i = 0; i < rows; ++i) {
+      const float* x = X + i * D;
+      if (mean) {
+        for (int64_t d = b; d < e; ++d) {
+          const double t = static_cast<double>(x[d]) - mean[d];
+          acc[d - b] += t * t;
+        }
+      } else {
+        for (int64_t d = b; d < e; ++d) acc[d - b] += static_cast<double>(x[d]);
+      }
     }
-  for (int y = 0; y < h; ++y)
-    for (int x = 0; x < w; ++x) {
-      double acc = 0.0;
-      for (int i = -r; i <= r; ++i) acc += k[i + r] * tmp[std::clamp(y + i, 0, h - 1) * w + x];
-      f[y * w + x] = acc;
-    }
+    for (int64_t d = b; d < e; ++d) out[d] = acc[d - b];
+  });
 }
 
-// Smooth random field: blurred iid draws, standardised per field back to the
-// (mean, std) of the iid draws (variance-preserving blur).
-void smooth_field(HostStream& s, const vmfa_synth_spec& sp, bool uniform01, double std_t,
-                  double mean_t, double* out, std::vector<double>& plane, std::vector<double>& tmp) {
-  const int W = sp.img_w, Hh = sp.img_h, Ch = sp.img_c;
-  const int P = W * Hh;
-  for (int ch = 0; ch < Ch; ++ch) {
-    plane.resize(P);
-    for (int i = 0; i < P; ++i) plane[i] = uniform01 ? s.uniform() : s.gaussian();
-    blur_plane(plane.data(), W, Hh, sp.blur_sigma, tmp);
-    double m = 0.0, v = 0.0;
-    for (int i = 0; i < P; ++i) m += plane[i];
-    m /= P;
-    for (int i = 0; i < P; ++i) v += (plane[i] - m) * (plane[i] - m);
-    const double sd = std::sqrt(v / P);
-    const double scale = sd > 0.0 ? std_t / sd : 0.0;
-    for (int i = 0; i < P; ++i) out[i * Ch + ch] = mean_t + (plane[i] - m) * scale;  // channel-last
+// row bits with -0.0 read as +0.0: rows equal under the reference's float
+// comparison (seeding.cpp:26, :140) have equal digests
+inline uint32_t row_word(const float* x) {
+  const float v = *x + 0.0f;
+  uint32_t w;
+  std::memcpy(&w, &v, sizeof w);
+  return w;
+}
+inline uint64_t fnv_row(const float* x, int D) {
+  uint64_t h = 1469598103934665603ULL;
+  for (int d = 0; d < D; ++d) {
+    const uint32_t w = row_word(x + d);
+    for (int b = 0; b < 4; ++b) h = (h ^ ((w >> (8 * b)) & 0xffu)) * 1099511628211ULL;
   }
+  return h;
+}
+struct RowHash {
+  const float* X;
+  int D;
+  size_t operator()(int64_t i) const { return static_cast<size_t>(fnv_row(X + i * D, D)); }
+};
+struct RowEq {
+  const float* X;
+  int D;
+  bool operator()(int64_t a, int64_t b) const {
+    for (int d = 0; d < D; ++d)
+      if (!(X[a * D + d] == X[b * D + d])) return false;
+    return true;
+  }
+};
+
+// fill_distinct (seeding.cpp:187-203) over a sparse swap map (unlisted
+// positions hold their own index): identical output for identical draws.
+struct FillDistinct {
+  int C;
+  std::unordered_map<int, int> over;
+  int at(int p) const {
+    auto it = over.find(p);
+    return it == over.end() ? p : it->second;
+  }
+  // out == nullptr: consume the row's draws only (uniform_int is one next())
+  void operator()(HostStream& rng, int want, int preset, int32_t* out) {
+    const int start = preset >= 0 ? 1 : 0;
+    if (!out) {
+      for (int i = start; i < want; ++i) rng.next();
+      return;
+    }
+    over.clear();
+    if (preset >= 0) {
+      const int a = at(0), b = at(preset);
+      over[0] = b;
+      over[preset] = a;
+    }
+    for (int i = start; i < want; ++i) {
+      const int j = i + static_cast<int>(rng.uniform_int(C - i));
+      const int a = at(i), b = at(j);
+      over[i] = b;
+      over[j] = a;
+    }
+    for (int i = 0; i < want; ++i) out[i] = at(i);
+    std::sort(out, out + want);
+  }
+};
+
+// init_params (seeding.cpp:151-181) from the stream positioned after the seed
+// draws, then init_varstate (seeding.cpp:207-233) storing rows [n0, n0 + rows)
+// of an N-row dataset. seed_rows_data: the C seed rows (C x D).
+void init_from_seeds(HostStream& rng, int64_t N, int D, int C, int H, int Cp, int G, uint64_t seed,
+                     double scale, int loading_init, const double* var, const double* floor,
+                     const int64_t* seeds, const float* seed_rows_data, int64_t n0, int64_t rows, double* pi,
+                     double* mu, double* lambda, double* dnoise, int32_t* K, int32_t* g, int32_t* g_count) {
+  for (int c = 0; c < C; ++c) {
+    pi[c] = 1.0 / C;
+    for (int d = 0; d < D; ++d) {
+      mu[static_cast<size_t>(c) * D + d] = static_cast<double>(seed_rows_data[static_cast<size_t>(c) * D + d]);
+      dnoise[static_cast<size_t>(c) * D + d] = std::max(var[d], floor[d]);
+    }
+    for (int d = 0; d < D; ++d)
+      for (int h = 0; h < H; ++h)
+        lambda[static_cast<size_t>(c) * D * H + static_cast<size_t>(h) * D + d] =
+            loading_init == 0 ? rng.uniform() * scale : rng.gaussian() * scale;
+  }
+  HostStream srng(key2(seed, kSaltState));
+  std::unordered_map<int64_t, int32_t> seed_of;
+  for (int c = 0; c < C; ++c) seed_of[seeds[c]] = c;
+  FillDistinct fill{C, {}};
+  for (int64_t n = 0; n < N; ++n) {
+    auto it = seed_of.find(n);
+    const bool mine = n >= n0 && n < n0 + rows;
+    fill(srng, Cp, it == seed_of.end() ? -1 : it->second, mine ? K + (n - n0) * Cp : nullptr);
+  }
+  for (int c = 0; c < C; ++c) {
+    fill(srng, G, c, g + static_cast<int64_t>(c) * G);
+    g_count[c] = G;
+  }
+}
+
+bool valid_sizes(int64_t N, int D, int C, int H, int Cp, int G) {
+  return N >= 1 && D >= 1 && C >= 1 && C <= N && H >= 1 && H <= D && Cp >= 1 && Cp <= C && G >= 1 && G <= C;
 }
 
 }  // namespace
@@ -89,136 +179,32 @@ void smooth_field(HostStream& s, const vmfa_synth_spec& sp, bool uniform01, doub
 
 using namespace vmfa_b200;
 
-extern "C" int vmfa_gen_synthetic(const vmfa_synth_spec* sp, int64_t row_begin, int64_t row_end,
-                                  float* X, int32_t* labels, int threads) {
-  if (!sp || !X || row_begin < 0 || row_end < row_begin || row_end > sp->n_total || sp->D < 1 ||
-      sp->C_true < 1 || sp->H_true < 0)
-    return fail(VMFA_ERR_INVALID_ARGUMENT, "vmfa_gen_synthetic: bad arguments");
-  if (sp->kind == 1 && sp->img_w * sp->img_h * sp->img_c != sp->D)
-    return fail(VMFA_ERR_INVALID_ARGUMENT, "vmfa_gen_synthetic: img_w*img_h*img_c != D");
-  if (threads < 1) threads = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
-  const int D = sp->D, Ct = sp->C_true, Ht = sp->H_true;
-
-  // mixing weights: equiprobable or Dirichlet(1) = normalised Exp(1) draws
-  std::vector<double> cdf(Ct);
-  {
-    HostStream s(key2(sp->data_seed, kSaltPi));
-    double acc = 0.0;
-    for (int c = 0; c < Ct; ++c) {
-      const double w = sp->dirichlet ? -std::log(1.0 - s.uniform()) : 1.0;
-      acc += w;
-      cdf[c] = acc;
-    }
-  }
-  // ground truth per component, each from its own keyed stream
-  std::vector<float> mu(static_cast<size_t>(Ct) * D), lam(static_cast<size_t>(Ct) * D * Ht),
-      sd(static_cast<size_t>(Ct) * D);
-  parallel_ranges(Ct, threads, [&](int, int64_t b, int64_t e) {
-    std::vector<double> field(D), plane, tmp;
-    for (int64_t c = b; c < e; ++c) {
-      HostStream s(key3(sp->data_seed, kSaltTruth, static_cast<uint64_t>(c)));
-      float* m = mu.data() + c * D;
-      float* l = lam.data() + c * D * Ht;  // [d][h]
-      float* p = sd.data() + c * D;
-      if (sp->kind == 0) {
-        for (int d = 0; d < D; ++d) m[d] = static_cast<float>(sp->mu_std * s.gaussian());
-        for (int d = 0; d < D; ++d)
-          for (int h = 0; h < Ht; ++h) l[d * Ht + h] = static_cast<float>(sp->lam_std * s.gaussian());
-        for (int d = 0; d < D; ++d)
-          p[d] = static_cast<float>(std::sqrt(sp->psi_lo + (sp->psi_hi - sp->psi_lo) * s.uniform()));
-      } else {
-        smooth_field(s, *sp, true, 1.0 / std::sqrt(12.0), 0.5, field.data(), plane, tmp);
-        for (int d = 0; d < D; ++d) m[d] = static_cast<float>(field[d]);
-        for (int h = 0; h < Ht; ++h) {
-          smooth_field(s, *sp, false, sp->lam_std, 0.0, field.data(), plane, tmp);
-          for (int d = 0; d < D; ++d) l[d * Ht + h] = static_cast<float>(field[d]);
-        }
-        for (int d = 0; d < D; ++d) p[d] = static_cast<float>(sp->noise_std);
-      }
-    }
-  });
-  // rows: component by inverse CDF, z ~ N(0, I), eps ~ N(0, Psi)
-  parallel_ranges(row_end - row_begin, threads, [&](int, int64_t b, int64_t e) {
-    std::vector<double> z(std::max(Ht, 1));
-    for (int64_t i = b; i < e; ++i) {
-      const int64_t n = row_begin + i;
-      HostStream s(key3(sp->data_seed, kSaltRow, static_cast<uint64_t>(n)));
-      const double u = s.uniform() * cdf.back();
-      int c = static_cast<int>(std::upper_bound(cdf.begin(), cdf.end(), u) - cdf.begin());
-      c = std::min(c, Ct - 1);
-      for (int h = 0; h < Ht; ++h) z[h] = s.gaussian();
-      const float* m = mu.data() + static_cast<size_t>(c) * D;
-      const float* l = lam.data() + static_cast<size_t>(c) * D * Ht;
-      const float* p = sd.data() + static_cast<size_t>(c) * D;
-      float* x = X + i * D;
-      for (int d = 0; d < D; ++d) {
-        double v = m[d];
-        for (int h = 0; h < Ht; ++h) v += static_cast<double>(l[d * Ht + h]) * z[h];
-        v += p[d] * s.gaussian();
-        if (sp->kind == 1) v = std::clamp(v, 0.0, 1.0);
-        x[d] = static_cast<float>(v);
-      }
-      if (labels) labels[i] = c;
-    }
-  });
-  return VMFA_OK;
-}
-
 // trainer.cpp:32-47 (initialize with InitConfig::Method::random_points) and
-// trainer.cpp:107-109 (init_varstate).
+// trainer.cpp:107-109 (init_varstate) over the whole dataset.
 extern "C" int vmfa_host_initialize(const float* X, int64_t N, int D, int C, int H, int Cp, int G,
                                     uint64_t seed, double scale, int loading_init, double* floor,
                                     double* pi, double* mu, double* lambda, double* dnoise,
                                     int32_t* K, int32_t* g, int32_t* g_count, int64_t* seeds) {
-  if (!X || N < 1 || D < 1 || C < 1 || C > N || H < 1 || H > D || Cp < 1 || Cp > C || G < 1 ||
-      G > C)
+  if (!X || !valid_sizes(N, D, C, H, Cp, G))
     return fail(VMFA_ERR_INVALID_ARGUMENT, "vmfa_host_initialize: invalid sizes");
-  const int threads = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
-  // per_dimension_variance (dataset.cpp:22-35): two fp64 passes, rows in order
-  // per dimension (parallel over dimensions keeps each dimension's order).
-  std::vector<double> var(D);
-  parallel_ranges(D, threads, [&](int, int64_t b, int64_t e) {
-    std::vector<double> mean(e - b, 0.0), acc(e - b, 0.0);
-    for (int64_t i = 0; i < N; ++i)
-      for (int64_t d = b; d < e; ++d) mean[d - b] += static_cast<double>(X[i * D + d]);
-    for (int64_t d = b; d < e; ++d) mean[d - b] /= static_cast<double>(N);
-    for (int64_t i = 0; i < N; ++i)
-      for (int64_t d = b; d < e; ++d) {
-        const double t = static_cast<double>(X[i * D + d]) - mean[d - b];
-        acc[d - b] += t * t;
-      }
-    for (int64_t d = b; d < e; ++d) var[d] = acc[d - b] / static_cast<double>(N);
-  });
+  const int threads = hw_threads();
+  // per_dimension_variance (dataset.cpp:22-35): two fp64 passes
+  std::vector<double> mean(D), var(D);
+  moments(X, N, D, nullptr, mean.data(), threads);
+  for (int d = 0; d < D; ++d) mean[d] /= static_cast<double>(N);
+  moments(X, N, D, mean.data(), var.data(), threads);
+  for (int d = 0; d < D; ++d) var[d] /= static_cast<double>(N);
   for (int d = 0; d < D; ++d) floor[d] = std::max(1e-6 * var[d], 1e-8);  // dataset.cpp:37-39
 
   // random_points_seed (seeding.cpp:123-149). count_distinct_rows (:16-32) is
   // an exact distinct-row count; a hash set gives the same answer.
-  struct RowHash {
-    const float* X;
-    int D;
-    size_t operator()(int64_t i) const {
-      uint64_t h = 1469598103934665603ULL;
-      const unsigned char* p = reinterpret_cast<const unsigned char*>(X + i * D);
-      for (size_t b = 0; b < static_cast<size_t>(D) * sizeof(float); ++b) h = (h ^ p[b]) * 1099511628211ULL;
-      return static_cast<size_t>(h);
-    }
-  };
-  struct RowEq {
-    const float* X;
-    int D;
-    bool operator()(int64_t a, int64_t b) const {
-      for (int d = 0; d < D; ++d)
-        if (!(X[a * D + d] == X[b * D + d])) return false;
-      return true;
-    }
-  };
   {
     std::unordered_set<int64_t, RowHash, RowEq> distinct(16, RowHash{X, D}, RowEq{X, D});
     for (int64_t i = 0; i < N && static_cast<int64_t>(distinct.size()) < C; ++i) distinct.insert(i);
     if (static_cast<int64_t>(distinct.size()) < C)
       return fail(VMFA_ERR_DEGENERATE_DATA, "fewer distinct rows than requested seeds");
   }
-  HostStream rng(key2(seed, 0x1217f01dULL));  // trainer.cpp:36
+  HostStream rng(key2(seed, kSaltInit));  // trainer.cpp:36
   {
     std::vector<uint8_t> used(N, 0);
     std::unordered_set<int64_t, RowHash, RowEq> chosen(16, RowHash{X, D}, RowEq{X, D});
@@ -234,53 +220,64 @@ extern "C" int vmfa_host_initialize(const float* X, int64_t N, int D, int C, int
       }
     }
   }
-  // init_params (seeding.cpp:151-181), same stream
-  for (int c = 0; c < C; ++c) {
-    pi[c] = 1.0 / C;
-    for (int d = 0; d < D; ++d) {
-      mu[static_cast<size_t>(c) * D + d] = static_cast<double>(X[seeds[c] * D + d]);
-      dnoise[static_cast<size_t>(c) * D + d] = std::max(var[d], floor[d]);
-    }
-    for (int d = 0; d < D; ++d)
-      for (int h = 0; h < H; ++h)
-        lambda[static_cast<size_t>(c) * D * H + static_cast<size_t>(h) * D + d] =
-            loading_init == 0 ? rng.uniform() * scale : rng.gaussian() * scale;
+  std::vector<float> srows(static_cast<size_t>(C) * D);
+  for (int c = 0; c < C; ++c) std::memcpy(&srows[static_cast<size_t>(c) * D], X + seeds[c] * D, sizeof(float) * D);
+  init_from_seeds(rng, N, D, C, H, Cp, G, seed, scale, loading_init, var.data(), floor, seeds, srows.data(), 0, N,
+                  pi, mu, lambda, dnoise, K, g, g_count);
+  return VMFA_OK;
+}
+
+// ---- sharded initialisation pieces (see the file header)
+
+extern "C" int vmfa_host_moments(const float* X, int64_t rows, int D, const double* mean, double* out,
+                                 int threads) {
+  if ((!X && rows > 0) || rows < 0 || D < 1 || !out)
+    return fail(VMFA_ERR_INVALID_ARGUMENT, "vmfa_host_moments: bad arguments");
+  moments(X, rows, D, mean, out, threads > 0 ? threads : hw_threads());
+  return VMFA_OK;
+}
+
+extern "C" int vmfa_seed_draws(uint64_t seed, int64_t N, int64_t first, int64_t count, int64_t* out) {
+  if (N < 1 || first < 0 || count < 0 || (!out && count > 0))
+    return fail(VMFA_ERR_INVALID_ARGUMENT, "vmfa_seed_draws: bad arguments");
+  HostStream rng(key2(seed, kSaltInit));
+  for (int64_t k = 0; k < first; ++k) rng.next();
+  for (int64_t k = 0; k < count; ++k) out[k] = rng.uniform_int(N);
+  return VMFA_OK;
+}
+
+extern "C" int vmfa_host_distinct_hashes(const float* X, int64_t rows, int D, int64_t want, uint64_t* out,
+                                         int64_t* n_out) {
+  if ((!X && rows > 0) || rows < 0 || D < 1 || want < 0 || !n_out || (!out && want > 0))
+    return fail(VMFA_ERR_INVALID_ARGUMENT, "vmfa_host_distinct_hashes: bad arguments");
+  std::unordered_set<int64_t, RowHash, RowEq> distinct(16, RowHash{X, D}, RowEq{X, D});
+  int64_t m = 0;
+  for (int64_t i = 0; i < rows && m < want; ++i) {
+    if (!distinct.insert(i).second) continue;
+    // two independent 64-bit digests of the row (FNV-1a over its bytes, a
+    // splitmix chain over its 32-bit words): 128 bits per distinct row
+    const uint64_t h1 = fnv_row(X + i * D, D);
+    uint64_t h2 = 0x243f6a8885a308d3ULL;
+    for (int d = 0; d < D; ++d) h2 = key2(h2, row_word(X + i * D + d));
+    out[2 * m] = h1;
+    out[2 * m + 1] = h2;
+    ++m;
   }
-  // init_varstate (seeding.cpp:207-233): fill_distinct (:187-203) over a
-  // sparse swap map (unlisted positions hold their own index).
-  HostStream srng(key2(seed, 0x7a57a7e5ULL));  // trainer.cpp:107
-  std::unordered_map<int64_t, int32_t> seed_of;
-  for (int c = 0; c < C; ++c) seed_of[seeds[c]] = c;
-  std::unordered_map<int, int> over;
-  auto at = [&](int p) {
-    auto it = over.find(p);
-    return it == over.end() ? p : it->second;
-  };
-  auto fill = [&](int want, int preset, int32_t* out) {
-    over.clear();
-    int start = 0;
-    if (preset >= 0) {
-      const int a = at(0), b = at(preset);
-      over[0] = b;
-      over[preset] = a;
-      start = 1;
-    }
-    for (int i = start; i < want; ++i) {
-      const int j = i + static_cast<int>(srng.uniform_int(C - i));
-      const int a = at(i), b = at(j);
-      over[i] = b;
-      over[j] = a;
-    }
-    for (int i = 0; i < want; ++i) out[i] = at(i);
-    std::sort(out, out + want);
-  };
-  for (int64_t n = 0; n < N; ++n) {
-    auto it = seed_of.find(n);
-    fill(Cp, it == seed_of.end() ? -1 : it->second, K + n * Cp);
-  }
-  for (int c = 0; c < C; ++c) {
-    fill(G, c, g + static_cast<int64_t>(c) * G);
-    g_count[c] = G;
-  }
+  *n_out = m;
+  return VMFA_OK;
+}
+
+extern "C" int vmfa_host_init_shard(int64_t N, int D, int C, int H, int Cp, int G, uint64_t seed, double scale,
+                                    int loading_init, const double* var, const double* floor,
+                                    const int64_t* seeds, const float* seed_rows, int64_t seed_draws,
+                                    int64_t n0, int64_t rows, double* pi, double* mu, double* lambda,
+                                    double* dnoise, int32_t* K, int32_t* g, int32_t* g_count) {
+  if (!valid_sizes(N, D, C, H, Cp, G) || !var || !floor || !seeds || !seed_rows || seed_draws < C || n0 < 0 ||
+      rows < 0 || n0 + rows > N || !pi || !mu || !lambda || !dnoise || (!K && rows > 0) || !g || !g_count)
+    return fail(VMFA_ERR_INVALID_ARGUMENT, "vmfa_host_init_shard: bad arguments");
+  HostStream rng(key2(seed, kSaltInit));
+  for (int64_t k = 0; k < seed_draws; ++k) rng.next();  // positioned after random_points_seed
+  init_from_seeds(rng, N, D, C, H, Cp, G, seed, scale, loading_init, var, floor, seeds, seed_rows, n0, rows, pi,
+                  mu, lambda, dnoise, K, g, g_count);
   return VMFA_OK;
 }

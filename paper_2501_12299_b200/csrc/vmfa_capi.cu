@@ -1854,6 +1854,26 @@ int vmfa_cooc_select(vmfa_ctx* x, const void* key, const void* cnt, const void* 
   return VMFA_OK;
 }
 
+// ---------------------------------------------------------------- work accounting
+int vmfa_scoring_work(vmfa_ctx* x, int64_t* out, int n) {
+  TRY(check_ctx(x));
+  if (!out || n < 1) return fail(VMFA_ERR_INVALID_ARGUMENT, "null output");
+  const Dims& dm = x->dm;
+  int ex = 0;
+  if (x->have_estep) {
+    CU(cudaMemcpyAsync(&ex, x->ex_off + dm.C, sizeof(int), cudaMemcpyDeviceToHost, x->stream));
+    CU(cudaStreamSynchronize(x->stream));
+  }
+  const int64_t w[6] = {static_cast<int64_t>(dm.N) * dm.Cp,
+                        ex,
+                        x->scorer == 2 ? ws_image_halves(dm, 0) * 2 : 0,
+                        x->scorer == 2 ? ws_image_halves(dm, 1) * 2 : 0,
+                        x->scorer == 2 ? (ws_record_floats(dm, 0) + ws_record_floats(dm, 1)) * 4 : 0,
+                        x->scorer};
+  for (int i = 0; i < n && i < 6; ++i) out[i] = w[i];
+  return VMFA_OK;
+}
+
 // ---------------------------------------------------------------- profiling
 int vmfa_profile_enable(vmfa_ctx* x, int enable) {
   TRY(check_ctx(x));

@@ -38,6 +38,22 @@ def device_view(ptr: int, n: int, typestr: str):
     return torch.as_tensor(_DevArray(ptr, n, typestr), device="cuda")
 
 
+def _host_staged(group=None) -> bool:
+    """gloo reduces host memory: device tensors are staged through the host."""
+    import torch.distributed as dist
+    return dist.get_backend(group) == "gloo"
+
+
+def all_reduce(t, group=None):
+    import torch.distributed as dist
+    if t.is_cuda and _host_staged(group):
+        h = t.cpu()
+        dist.all_reduce(h, group=group)
+        t.copy_(h)
+    else:
+        dist.all_reduce(t, group=group)
+
+
 def owner_ranges(C: int, world: int):
     """Block ownership of components: rank r owns [floor(rC/p), floor((r+1)C/p))."""
     return [(r * C // world, (r + 1) * C // world) for r in range(world)]
@@ -50,6 +66,9 @@ def route_lists(arrays, counts, group=None):
     import torch
     import torch.distributed as dist
     dev = arrays[0].device
+    if dev.type == "cuda" and _host_staged(group):
+        out, rc = route_lists([a.cpu() for a in arrays], counts, group)
+        return [o.to(dev) for o in out], rc
     send = torch.as_tensor(np.asarray(counts, np.int64), device=dev)
     recv = torch.empty_like(send)
     dist.all_to_all_single(recv, send, group=group)
@@ -77,15 +96,11 @@ def allreduce_buffer(sess, which: int, group=None):
     enqueued on the context's stream (NCCL) and the call returns once it is
     complete, so the next phase call may read the buffer."""
     import torch
-    import torch.distributed as dist
     ptr, n, dt = sess.exchange_buffer(which)
     t = device_view(ptr, n, _TYPESTR[dt])
-    if t.is_cuda:
-        with _on_ctx_stream(sess):
-            dist.all_reduce(t, group=group)
-        torch.cuda.ExternalStream(sess.stream()).synchronize()
-    else:
-        dist.all_reduce(t, group=group)
+    with _on_ctx_stream(sess):
+        all_reduce(t, group)
+    torch.cuda.ExternalStream(sess.stream()).synchronize()
 
 
 def cooc_exchange(sess, rank: int, world: int, group=None):

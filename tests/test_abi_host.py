@@ -84,6 +84,82 @@ def test_host_initialize_matches_oracle(oracle, vmfa):
         np.testing.assert_allclose(floor, flo, rtol=1e-13)
 
 
+def test_synthetic_rows_identical_in_oracle_build(oracle, vmfa):
+    """The BASELINE generator compiled into the oracle (reference arm) and into
+    the product (GPU arm) gives bit-identical rows, and both config tables agree."""
+    for cfg in (1, 2, 3, 4, 5):
+        assert oracle.CONFIGS[cfg] == {k: dict(v) for k, v in vmfa.CONFIGS[cfg].items()}
+        over = {"C_true": 300} if cfg == 5 else {}
+        a = vmfa.gen_synthetic(vmfa.synth_spec(cfg, N=5000, **over), 1000, 1400)
+        b = oracle.gen_synthetic(oracle.synth_spec(cfg, N=5000, **over), 1000, 1400)
+        assert a.tobytes() == b.tobytes(), cfg
+
+
+def _fill_distinct_numpy(draws, C, want, preset):
+    """seeding.cpp:187-203 literally: a C-sized buffer 0..C-1, the preset swap,
+    j = i + uniform_int(C - i) swaps (uniform_int = mulhi(next_u64, bound),
+    rng.hpp:55-60), then the first `want` entries sorted."""
+    buf = np.arange(C)
+    start = 0
+    if preset >= 0:
+        buf[0], buf[preset] = buf[preset], buf[0]
+        start = 1
+    for i in range(start, want):
+        u = int(next(draws))
+        j = i + ((u * (C - i)) >> 64)
+        buf[i], buf[j] = buf[j], buf[i]
+    return np.sort(buf[:want])
+
+
+def test_init_varstate_pinned_to_dense_fill_distinct(oracle, vmfa):
+    """init_varstate (seeding.cpp:207-233) three ways: a numpy restatement of
+    the dense fill_distinct over the golden-pinned stream (orc_rng_u64, checked
+    bit-exactly against the reference's rng.hpp in test_oracle_pins), the
+    oracle's dense C++ restatement, and the product's sparse swap map."""
+    X = vmfa.gen_synthetic(vmfa.synth_spec(1, N=700))
+    C, H, Cp, G, seed = 37, 2, 4, 6, 9
+    p, st, floor, seeds = vmfa.initialize(X, C, H, Cp, G, seed=seed)
+    so = oracle.init_varstate(X.shape[0], C, Cp, G, seeds, oracle.hash_combine(seed, oracle.STATE_SALT))
+    n_draws = X.shape[0] * Cp + C * G
+    draws = iter(oracle.rng_u64(oracle.hash_combine(seed, oracle.STATE_SALT), n_draws))
+    seed_of = {int(n): c for c, n in enumerate(seeds)}
+    K = np.stack([_fill_distinct_numpy(draws, C, Cp, seed_of.get(n, -1)) for n in range(X.shape[0])])
+    g = np.stack([_fill_distinct_numpy(draws, C, G, c) for c in range(C)])
+    assert np.array_equal(K, so.K) and np.array_equal(K, st.K)
+    assert np.array_equal(g, so.g) and np.array_equal(g, st.g)
+
+
+def test_sharded_initialize_single_rank_matches(vmfa):
+    from paper_2501_12299_b200.sharded import initialize_sharded
+    X = vmfa.gen_synthetic(vmfa.synth_spec(2, N=3000))
+    p, st, floor, seeds = vmfa.initialize(X, 200, 8, 5, 10, seed=4)
+    p2, st2, floor2, seeds2 = initialize_sharded(X, 0, X.shape[0], 200, 8, 5, 10, seed=4)
+    assert np.array_equal(seeds, seeds2) and np.array_equal(st.K, st2.K) and np.array_equal(st.g, st2.g)
+    for f in ("pi", "mu", "lam", "psi"):
+        assert np.array_equal(getattr(p, f), getattr(p2, f)), f
+    assert np.array_equal(floor, floor2)
+
+
+def test_degenerate_data_is_reported(vmfa):
+    from paper_2501_12299_b200.sharded import initialize_sharded
+    X = np.repeat(vmfa.gen_synthetic(vmfa.synth_spec(1, N=50), 0, 5), 10, axis=0)
+    with pytest.raises(vmfa.VmfaError, match="DegenerateData"):
+        vmfa.initialize(X, 8, 2, 2, 3)
+    with pytest.raises(vmfa.VmfaError, match="DegenerateData"):
+        initialize_sharded(X, 0, X.shape[0], 8, 2, 2, 3)
+    # -0.0 and +0.0 are one value to the reference's row compare (seeding.cpp:26, :140)
+    X = vmfa.gen_synthetic(vmfa.synth_spec(1, N=50), 0, 12)
+    X[1, 0] = 0.0
+    X[5] = X[1]
+    X[5, 0] = -0.0
+    for impl in (lambda C_: vmfa.initialize(X, C_, 2, 2, 3),
+                 lambda C_: initialize_sharded(X, 0, X.shape[0], C_, 2, 2, 3)):
+        with pytest.raises(vmfa.VmfaError, match="DegenerateData"):
+            impl(12)
+        seeds = impl(11)[3]
+        assert len(set(seeds.tolist()) & {1, 5}) == 1 and len(set(seeds.tolist())) == 11
+
+
 def test_init_varstate_invariants(vmfa):
     X = vmfa.gen_synthetic(vmfa.synth_spec(2, N=5000))
     p, st, floor, seeds = vmfa.initialize(X, 300, 8, 5, 10, seed=3)

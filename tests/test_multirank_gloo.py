@@ -197,3 +197,56 @@ def test_sparse_cooc_exchange_protocol(oracle):
     assert sum(ret["recv"]) > 0 and sum(ret["sent"]) > 0
     assert np.array_equal(ret["gc"], st.g_count)
     assert np.array_equal(ret["g"], st.g)
+
+
+def _init_worker(rank, port, ret, world, case):
+    """initialize_sharded on rank-local rows only (gloo): each rank generates
+    its own shard of the BASELINE generator's rows."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from paper_2501_12299_b200 import vmfa as V
+    from paper_2501_12299_b200.sharded import Comm, initialize_sharded
+    N = case["N"]
+    a, b = rank * N // world, (rank + 1) * N // world
+    X = V.gen_synthetic(V.synth_spec(case["cfg"], N=N), a, b)
+    if case.get("dups"):  # duplicated rows exercise the duplicate rejection across shards
+        X[::3] = V.gen_synthetic(V.synth_spec(case["cfg"], N=N), 0, 1)
+    p, st, floor, seeds = initialize_sharded(X, a, N, case["C"], case["H"], case["Cp"], case["G"], seed=5,
+                                             comm=Comm())
+    ret[rank] = dict(pi=p.pi, mu=p.mu, lam=p.lam, psi=p.psi, K=st.K, g=st.g, gc=st.g_count, floor=floor,
+                     seeds=seeds)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,case", [
+    (2, dict(cfg=1, N=3000, C=100, H=4, Cp=3, G=5)),
+    (3, dict(cfg=2, N=2500, C=300, H=8, Cp=5, G=10)),
+    (2, dict(cfg=1, N=1500, C=60, H=2, Cp=3, G=4, dups=True)),
+])
+def test_sharded_initialize_matches_whole_dataset(vmfa, world, case):
+    """Floor by moment all-reduces, seeds by draw replay + owner row fetch,
+    init_varstate replayed per rank: identical to vmfa.initialize on all rows."""
+    V = vmfa
+    mgr = mp.Manager()
+    ret = mgr.dict()
+    mp.spawn(_init_worker, args=(_free_port(), ret, world, case), nprocs=world, join=True)
+    N = case["N"]
+    X = V.gen_synthetic(V.synth_spec(case["cfg"], N=N))
+    if case.get("dups"):
+        for r in range(world):
+            a, b = r * N // world, (r + 1) * N // world
+            X[a:b][::3] = X[0]
+    p, st, floor, seeds = V.initialize(X, case["C"], case["H"], case["Cp"], case["G"], seed=5)
+    for r in range(world):
+        got = ret[r]
+        assert np.array_equal(got["seeds"], seeds)
+        for f in ("pi", "mu", "lam"):
+            assert np.array_equal(got[f], getattr(p, f)), f
+        np.testing.assert_allclose(got["psi"], p.psi, rtol=1e-12)
+        np.testing.assert_allclose(got["floor"], floor, rtol=1e-12)
+        assert np.array_equal(got["g"], st.g) and np.array_equal(got["gc"], st.g_count)
+    K = np.concatenate([ret[r]["K"] for r in range(world)])
+    assert np.array_equal(K, st.K)

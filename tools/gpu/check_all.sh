@@ -1,8 +1,10 @@
+# One GPU call: tests, smoke, the default bench line (config 3) and the
+# reference arm, each bounded by its own timeout. Outputs in gpurun_out/.
 mkdir -p gpurun_out
-set -x
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
-timeout 1200 python -m pytest tests -m gpu -x -q 2>&1 | tail -30 > gpurun_out/pytest_gpu.log
+nproc; free -g | head -2
+timeout ${PYTEST_TIMEOUT:-1500} python -m pytest tests -m "gpu ${PYTEST_SEL:-}" -x -q ${PYTEST_ARGS:-} 2>&1 | tail -40 > gpurun_out/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
-timeout 600 python bench.py --steps 10 --warmup 3 > gpurun_out/bench.json 2> gpurun_out/bench.err
-timeout 300 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
-tail -3 gpurun_out/pytest_gpu.log; cat gpurun_out/smoke.log | tail -2; head -c 600 gpurun_out/bench.json; cat gpurun_out/bench_ref.json | head -c 400
+timeout 900 python bench.py --steps 10 --warmup 3 > gpurun_out/bench.json 2> gpurun_out/bench.err
+timeout 900 python bench.py --impl reference --steps ${REF_STEPS:-3} --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
+tail -3 gpurun_out/pytest_gpu.log; tail -2 gpurun_out/smoke.log; head -c 1500 gpurun_out/bench.json; tail -5 gpurun_out/bench.err; head -c 1200 gpurun_out/bench_ref.json; tail -3 gpurun_out/bench_ref.err
