@@ -1412,7 +1412,7 @@ int vmfa_download_distances(vmfa_ctx* x, int64_t cap, int32_t* c, int32_t* ct, d
     if (w < cap) {
       if (c) c[w] = vc[k];
       if (ct) ct[w] = vct[k];
-      if (sum) sum[w] = static_cast<double>(hi) / 1024.0 + static_cast<double>(lo) / 1125899906842624.0;
+      if (sum) sum[w] = static_cast<double>(hi) / 1024.0 + static_cast<double>(lo) / 1073741824.0;  // from_fixed
       if (count) count[w] = n;
     }
     ++w;

@@ -426,19 +426,25 @@ __global__ void __launch_bounds__(256) k_select(SelectArgs a) {
 // pi_ct > 0, accumulate value = (l(n,c) - log pi_c) - (l(n,ct) - log pi_ct)
 // [kl] or -l(n,ct) [euclid] into (sum, count) per ct; then update_g
 // (estep.cpp:204-220): g_c = {c} U the G-1 smallest (sum/count, ct), sorted.
-// Sums are exact fixed-point integers (2^-50 resolution, split hi/lo int64),
-// so the accumulation order — and the number of ranks — cannot change them.
+// Sums are exact fixed-point integers (split hi/lo int64), so the
+// accumulation order -- and the number of ranks -- cannot change them.
+// value = hi 2^-10 + lo 2^-30, lo in [0, 2^20): |value| saturates at 2^40
+// (1.1e12; a term's hi stays below 2^50, so a key's sum overflows only past
+// 2^53 in total, i.e. ~8e6 terms of 1e9 each), and lo sums overflow only past
+// 2^43 terms. The resolution 2^-30 is far below the fp32 log-joints the
+// values are formed from (tests/test_multirank_gloo.py restates the encoding,
+// tests/test_gpu_parity.py drives values past the saturation bound).
 __device__ __forceinline__ void to_fixed(double v, long long& hi, long long& lo) {
-  const double kMax = 2147483648.0;  // |value| saturates at 2^31
+  const double kMax = 1099511627776.0;  // 2^40
   if (!(v == v)) v = kMax;
   v = fmin(fmax(v, -kMax), kMax);
   const double y = v * 1024.0;  // 2^10
   const double f = floor(y);
   hi = static_cast<long long>(f);
-  lo = static_cast<long long>((y - f) * 1099511627776.0);  // 2^40
+  lo = static_cast<long long>((y - f) * 1048576.0);  // 2^20
 }
 __device__ __forceinline__ double from_fixed(long long hi, long long lo) {
-  return static_cast<double>(hi) * (1.0 / 1024.0) + static_cast<double>(lo) * (1.0 / 1125899906842624.0);
+  return static_cast<double>(hi) * (1.0 / 1024.0) + static_cast<double>(lo) * (1.0 / 1073741824.0);
 }
 constexpr int kGupdBatch = 4;  // points in flight per warp in k_gupdate
 constexpr int kGupdProbes = 32;  // probe limit of a dense-rows item's hash
@@ -685,7 +691,7 @@ __global__ void __launch_bounds__(kGupdThreads) k_gupdate(GupdArgs a, int capmax
       continue;
     }
     // update_g: the keys (avg, ct) are computed once, in place of the sums
-    // (+inf: no key; averages are finite, the values saturate at 2^31), then
+    // (+inf: no key; averages are finite, the values saturate at 2^40), then
     // G-1 rounds of a block-wide argmin, the winner's key set to +inf
     double* kv = reinterpret_cast<double*>(use_smem ? t_hi : g_hi);
     for (int i = tid; i < tab_n; i += kGupdThreads) {

@@ -112,11 +112,11 @@ def test_two_rank_shard_algebra_matches_single(oracle):
 
 def to_fixed(v):
     """Host restatement of the device's fixed-point split (vmfa_kernels.cu
-    to_fixed): value = hi * 2^-10 + lo * 2^-50 exactly, hi/lo int64."""
-    v = float(np.clip(v, -2.0 ** 31, 2.0 ** 31))
+    to_fixed): value = hi * 2^-10 + lo * 2^-30, hi/lo int64, |value| <= 2^40."""
+    v = float(np.clip(v, -2.0 ** 40, 2.0 ** 40))
     y = v * 1024.0
     f = np.floor(y)
-    return int(f), int((y - f) * 2.0 ** 40)
+    return int(f), int((y - f) * 2.0 ** 20)
 
 
 def test_fixed_point_sums_are_order_and_partition_independent():
@@ -130,8 +130,15 @@ def test_fixed_point_sums_are_order_and_partition_independent():
     hi2 = sum(p[0] for p in shard[:1234]) + sum(p[0] for p in shard[1234:])
     lo2 = sum(p[1] for p in shard[:1234]) + sum(p[1] for p in shard[1234:])
     assert (hi, lo) == (hi2, lo2)
-    exact = hi / 1024.0 + lo / 2.0 ** 50
+    exact = hi / 1024.0 + lo / 2.0 ** 30
     assert abs(exact - vals.sum()) <= 1e-9 * np.abs(vals).sum()
+    # the range: terms up to 2^40 in magnitude (a floored psi makes v^2/psi
+    # huge), ~1e6 of them, still exact and order independent
+    big = rng.uniform(-2.0 ** 40, 2.0 ** 40, 4096) * rng.choice([1e-9, 1.0], 4096)
+    parts = [to_fixed(v) for v in big]
+    hi, lo = sum(p[0] for p in parts), sum(p[1] for p in parts)
+    assert abs(hi) < 2 ** 63 and 0 <= lo < 2 ** 63
+    assert abs((hi / 1024.0 + lo / 2.0 ** 30) - float(np.sum(big))) <= 1e-12 * np.abs(big).sum()
 
 
 def _sparse_worker(rank, port, ret):
