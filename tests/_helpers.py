@@ -147,3 +147,47 @@ def ldlt_cases(O):
     prev = O.Params(np.full(C_, 1.0 / C_), rng.normal(size=(C_, D)), rng.normal(size=(C_, H, D)),
                     np.ones((C_, D)))
     return s, prev, np.full(D, 1e-6), want
+
+
+def near_tie_rows_fast(lj_or, cnt, Cp, tau):
+    """Vectorised near_tie_rows: the oracle's C'-th and (C'+1)-th largest
+    log-joints of S(n) within tau[n]."""
+    N, S = lj_or.shape
+    live = np.arange(S)[None, :] < cnt[:, None]
+    v = np.where(live & np.isfinite(lj_or), lj_or, -np.inf)
+    v = -np.sort(-v, axis=1)
+    out = np.zeros(N, bool)
+    ok = cnt > Cp
+    a, b = v[ok, Cp - 1], v[ok, Cp]
+    out[ok] = (a - b) <= tau[ok]
+    out[ok & ~np.isfinite(b)] = False
+    return out
+
+
+def compare_g_tau(g_gpu, gc_gpu, g_or, gc_or, dist_or, tau, touched):
+    """g_c (update_g, estep.cpp:204-220) per component: identical, or a
+    near-tie at the selection boundary -- the oracle's (G-1)-th and G-th
+    smallest averages within tau (each average carries at most 2 max|dl| of
+    the log-joint error, so tau = 4 max|dl|) -- or a component whose partition
+    changed because a near-tie row changed its label (`touched`). Returns
+    (diff, ties, touched_diff, bad) component lists."""
+    C, G = g_or.shape
+    dc, dct, dsum, dcnt = dist_or
+    starts = np.searchsorted(dc, np.arange(C + 1))
+    diff, ties, tdiff, bad = [], [], [], []
+    for c in range(C):
+        a = g_gpu[c, :gc_gpu[c]]
+        b = g_or[c, :gc_or[c]]
+        if gc_gpu[c] == gc_or[c] and np.array_equal(a, b):
+            continue
+        diff.append(c)
+        if touched[c]:
+            tdiff.append(c)
+            continue
+        s, e = starts[c], starts[c + 1]
+        avg = np.sort(dsum[s:e] / dcnt[s:e])
+        if len(avg) >= G and abs(avg[G - 1] - avg[G - 2]) <= tau:
+            ties.append(c)
+            continue
+        bad.append(c)
+    return diff, ties, tdiff, bad

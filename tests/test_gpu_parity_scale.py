@@ -1,0 +1,147 @@
+"""GPU parity at the BASELINE configs' scale:
+teacher-forced main iterations (E-step, statistics, update, precompute,
+truncated F) on config 3 (100 000 rows of its generator, the full model
+D=784, H=16, C=4000, C'=5, G=10), the config-4 shape (200 000 rows, D=256,
+H=8, C=10 000, C'=5, G=15) and the whole of config 2 (200 000 rows). Every
+step restarts both sides from the same parameters and state; the bar:
+  * identical joint counts and search spaces (reference insertion order);
+  * log-joints and both free energies within 1e-4 relative;
+  * every K row that differs is a near-tie (the oracle's C'-th and
+    (C'+1)-th log-joints within tau = 2 max|dl| of that row), every label
+    that differs is a near-tie within the K row, every g_c that differs is a
+    near-tie at its (G-1)/G boundary (tau_g = 4 max|dl|) or a component
+    whose partition a near-tie row changed;
+  * statistics from the same K and responsibilities within 1e-5 relative;
+  * updated parameters (the device's statistics vs the oracle's) within the
+    tolerances stated in _PARAM_TOL.
+Counts per config land in $PARITY_REPORT_DIR/parity_<case>.json.
+The estep.cpp:103-122, :144-173, :204-220 tie rules and mstep.cpp:103-162
+update are the semantics checked.
+"""
+import json
+import os
+import time
+
+import numpy as np
+import pytest
+
+from _helpers import LJ_RTOL, compare_estep, compare_g_tau, near_tie_rows_fast, to_vmfa_params, to_vmfa_state
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+# updated parameters from the device's statistics vs the oracle's (same K and
+# q): relative to each component's largest magnitude of that parameter;
+# "q999" is the 99.9th percentile over components, "max" the worst component
+# (a component holding a handful of points has a near-singular E_c, whose
+# solve amplifies the ~1e-6 statistics error)
+_PARAM_TOL = {"pi": dict(q999=1e-6, max=1e-5), "mu": dict(q999=1e-4, max=1e-2),
+              "lam": dict(q999=1e-3, max=5e-2), "psi": dict(q999=1e-4, max=1e-2)}
+
+
+def _rel_per_component(a, b):
+    a = a.reshape(a.shape[0], -1)
+    b = b.reshape(b.shape[0], -1)
+    scale = np.maximum(np.abs(b).max(axis=1), 1e-300)
+    return np.abs(a - b).max(axis=1) / scale
+
+
+def _report(name, rep):
+    d = os.environ.get("PARITY_REPORT_DIR")
+    if d:
+        os.makedirs(d, exist_ok=True)
+        with open(os.path.join(d, f"parity_{name}.json"), "w") as f:
+            json.dump(rep, f, indent=1, default=float)
+
+
+def teacher_forced(O, V, X, C, H, Cp, G, iters, name, seed=0):
+    threads = os.cpu_count() or 8
+    N = X.shape[0]
+    t0 = time.time()
+    p, st, floor, _ = O.initialize(X, C, H, Cp, G, seed=seed, scale=0.1, loading_init=1)
+    sess = V.Session(C, X.shape[1], H, Cp, G, X)
+    sess.set_floor(floor)
+    rep = dict(case=name, N=N, D=X.shape[1], C=C, H=H, Cp=Cp, G=G, iterations=[])
+    for it in range(iters):
+        r = {}
+        k = O.precompute_all(p)
+        sess.upload_params(to_vmfa_params(V, p))
+        # --- E-step (block 1-4), same inputs on both sides
+        st_or = st.copy()
+        e_or = O.variational_e_step(X, p, k, st_or, seed, it, threads=threads, dump_distances=True)
+        sess.upload_state(to_vmfa_state(V, st))
+        F, J = sess.variational_e_step(seed, it)
+        ret = sess.download_estep()
+        st_g = sess.download_state()
+        info = compare_estep(O, e_or, st_or, F, J, ret, st_g, Cp)  # asserts the K / label / q bar
+        r.update(info)
+        r["F_estep_rel"] = abs(F - e_or.F) / abs(e_or.F)
+        r["joints"] = int(J)
+        # g: every differing component a near-tie or a consequence of one
+        cnt_g, idx_g, lj_g, _ = ret
+        fin = np.isfinite(e_or.lj) & (idx_g >= 0)
+        dl = float(np.where(fin, np.abs(lj_g - e_or.lj), 0.0).max())
+        touched = np.zeros(C, bool)
+        rows = np.nonzero(np.any(st_g.K != st_or.K, axis=1) | (st_g.labels != st_or.labels))[0]
+        touched[st_or.labels[rows]] = True
+        touched[st_g.labels[rows]] = True
+        diff, ties, tdiff, bad = compare_g_tau(st_g.g, st_g.g_count, st_or.g, st_or.g_count, e_or.dist,
+                                               4 * dl, touched)
+        assert not bad, f"{name} it {it}: g differs outside near-ties for components {bad[:10]}"
+        r.update(g_diff=len(diff), g_near_ties=len(ties), g_touched=len(tdiff), max_abs_dl=dl)
+        # --- statistics from the device's K and q (pre-update caches)
+        resp_g = ret[3]
+        sess.accumulate_suffstats()
+        s_g = sess.download_suffstats()
+        s_or = O.accumulate_suffstats(X, p, k, st_g.K, resp_g, threads=threads)
+        np.testing.assert_allclose(s_g.Nc, s_or.Nc, rtol=1e-6, atol=0)
+        assert np.array_equal(s_g.Nc == 0.0, s_or.Nc == 0.0)
+        for f in ("E", "Y", "sq"):
+            a, b = getattr(s_g, f), getattr(s_or, f)
+            np.testing.assert_allclose(a, b, rtol=1e-5, atol=1e-6 * np.abs(b).max(), err_msg=f)
+            r[f"stats_{f}_maxrel"] = float((np.abs(a - b) / np.maximum(np.abs(b), 1e-6 * np.abs(b).max())).max())
+        # --- update + precompute (the device's own statistics)
+        sess.update_params()
+        p_g = sess.download_params()
+        p_or = O.update_params(s_or, N, p, floor)
+        for f, tol in _PARAM_TOL.items():
+            rel = _rel_per_component(getattr(p_g, f), getattr(p_or, f))
+            live = p_or.pi > 0
+            rel = rel[live]
+            r[f"param_{f}_q999"] = float(np.quantile(rel, 0.999))
+            r[f"param_{f}_max"] = float(rel.max())
+            assert r[f"param_{f}_q999"] <= tol["q999"] and r[f"param_{f}_max"] <= tol["max"], (f, r)
+        assert np.array_equal(p_g.pi == 0.0, p_or.pi == 0.0)
+        # --- post-M-step truncated free energy (trainer.cpp:158-160)
+        F_post = sess.truncated_free_energy()
+        F_post_or = O.truncated_free_energy(X, p_or, O.precompute_all(p_or), st_g.K, threads=threads)
+        r["F_post_rel"] = abs(F_post - F_post_or) / abs(F_post_or)
+        assert r["F_post_rel"] <= LJ_RTOL, r
+        rep["iterations"].append(r)
+        # teacher forcing: the next step starts from the oracle's state and
+        # the oracle's update of these statistics
+        p, st = p_or, st_or
+    rep["seconds"] = time.time() - t0
+    _report(name, rep)
+    sess.close()
+    return rep
+
+
+def test_config3_teacher_forced_100k(oracle, gpu):
+    O, V = oracle, gpu
+    X = V.gen_synthetic(V.synth_spec(3), 0, 100_000)
+    m = V.CONFIGS[3]["model"]
+    teacher_forced(O, V, X, m["C"], m["H"], m["Cprime"], m["G"], 2, "config3_100k")
+
+
+def test_config4_shape_teacher_forced_200k(oracle, gpu):
+    O, V = oracle, gpu
+    X = V.gen_synthetic(V.synth_spec(4), 0, 200_000)
+    m = V.CONFIGS[4]["model"]
+    teacher_forced(O, V, X, m["C"], m["H"], m["Cprime"], m["G"], 2, "config4_shape_200k")
+
+
+def test_config2_full_teacher_forced(oracle, gpu):
+    O, V = oracle, gpu
+    X = V.gen_synthetic(V.synth_spec(2))
+    m = V.CONFIGS[2]["model"]
+    teacher_forced(O, V, X, m["C"], m["H"], m["Cprime"], m["G"], 3, "config2_full")
