@@ -347,6 +347,7 @@ def main():
         torch.cuda.synchronize()
         return
 
+    sess.scoring_work()  # clears the fp64 re-scoring counter
     # L2 flush buffer (> 126 MB L2), written between timed iterations
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{local}")
     times, joints, Fs = [], [], []
@@ -368,6 +369,7 @@ def main():
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
+    rescored = sess.scoring_work()["fp64_rescored"] / args.steps
     ms_step = float(np.sum(times) / args.steps)
     J_job = float(np.sum(joints) / args.steps)  # multi-rank: the scalars are all-reduced, J is the job total
     if dist:
@@ -502,6 +504,7 @@ def main():
                        "l2": "flushed (256 MB write) before every timed iteration; X alone (N D 4 B) exceeds L2",
                        "parallelism": f"dp{world} (rows sharded, params replicated)"},
             "joints_per_step": J_job, "F_last": Fs[-1],
+            "fp64_rescored_per_step": rescored,
             "em_iteration_ms": ms_step,
             "phase_ms": phase_ms,
             "roofline": {"bound": "hbm", "kernel": "candidate scoring (score_anchor+score_extra)",

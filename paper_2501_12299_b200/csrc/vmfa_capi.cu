@@ -50,11 +50,12 @@ enum KernelFamily : int {
   kFamSort,
   kFamOther,
   kFamExactLL,
+  kFamFixup,
   kNumFamilies
 };
 const char* const kFamilyNames[kNumFamilies] = {
     "score_anchor", "score_extra", "select", "gupdate", "stats",
-    "update", "precompute", "score_truncF", "csr_sort", "other", "exact_ll"};
+    "update", "precompute", "score_truncF", "csr_sort", "other", "exact_ll", "fixup_f64"};
 
 __global__ void k_pack_scalar_u64(const unsigned long long* src, double* dst) { *dst = static_cast<double>(*src); }
 __global__ void k_add_f64(const double* src, double* dst) { *dst = *src; }
@@ -97,6 +98,14 @@ struct vmfa_ctx {
   uint16_t *bimg = nullptr, *simg = nullptr;  // scorer B stage images (fp16; anchor / single)
   float *bscl = nullptr, *sscl = nullptr;     // their row scales
   float *xmax = nullptr, *mumax = nullptr;    // A-row scale bounds
+  unsigned long long* nfix = nullptr;         // scores re-evaluated in fp64 (vmfa_fixup.cu), accumulated
+  long long* fix_list = nullptr;              // flagged scores of one scoring launch
+  unsigned long long* fix_cnt = nullptr;      // [count, overflow]
+  long long fix_cap = 0;
+  int *fix_qkey = nullptr, *fix_qcnt = nullptr, *fix_qoff = nullptr, *fix_qfill = nullptr, *fix_iof = nullptr;
+  int* fix_sorted = nullptr;
+  unsigned long long* fix_ovf = nullptr;
+  bool fix_ok = false;  // re-scoring pipeline on (warp-specialised scorer, N SL < 2^31)
   int scorer = 2;           // 2: warp-specialised tcgen05 (default), 1: single-role tcgen05, 0: FFMA
   bool use_tc = true;
   int score_rows = kScoreRowsTc;
@@ -310,11 +319,22 @@ cudaError_t wait_x(vmfa_ctx* x) {
 
 cudaError_t run_score(vmfa_ctx* x, int mode, const ScoreArgs& a) {
   if (cudaError_t e = wait_x(x); e != cudaSuccess) return e;
-  if (x->scorer == 2)
-    return launch_score_ws(mode, a, WsOperands{x->xmax, x->mumax, x->mu32, x->brec, x->srec, x->bimg, x->bscl, x->simg, x->sscl},
+  if (x->scorer == 2) {
+    if (cudaError_t e = cudaMemsetAsync(x->fix_cnt, 0, 2 * sizeof(unsigned long long), x->stream); e != cudaSuccess)
+      return e;
+    return launch_score_ws(mode, a,
+                           WsOperands{x->xmax, x->mumax, x->mu32, x->brec, x->srec, x->bimg, x->bscl, x->simg, x->sscl,
+                                      x->fix_list, x->fix_cnt, x->fix_cap},
                            x->jobs, x->stream);
+  }
   if (x->scorer == 1) return launch_score_tc(mode, a, x->WT, x->ipsi32, x->mu32, x->stream);
   return launch_score(mode, a, score_grid(), x->stream);
+}
+
+FixArgs fix_args(vmfa_ctx* x) {
+  return FixArgs{x->X,       x->mu,      x->psi,         x->lam,  x->R,       x->kconst, x->fix_list, x->fix_cnt,
+                 x->fix_cap, x->nfix,    x->fix_qkey,    x->fix_sorted, x->fix_qcnt, x->fix_qoff, x->fix_qfill,
+                 x->fix_iof, x->fix_ovf};
 }
 
 ScoreArgs score_args(vmfa_ctx* x) {
@@ -327,6 +347,39 @@ ScoreArgs score_args(vmfa_ctx* x) {
   a.g = x->g;
   a.gcnt = x->gcnt;
   return a;
+}
+
+// The scores the last scoring launch flagged (their terms cancel, see
+// vmfa_fixup.cu): grouped by component and re-scored by the one-component
+// tensor pass (rows centred on the candidate itself: no anchor expansion),
+// then what is still flagged (a collapsed component's own Woodbury
+// cancellation) is re-evaluated in fp64. All counts stay on the device (the
+// iteration graph replays it); list overflows fall back to scanning kernels.
+int rescore(vmfa_ctx* x, int mode, float* out) {
+  if (!x->fix_ok) return VMFA_OK;
+  const Dims& dm = x->dm;
+  cudaStream_t s = x->stream;
+  const int tf = x->begin(kFamFixup, 0);
+  const FixArgs f = fix_args(x);
+  CU(launch_fix_ovf(f, 1, s));
+  CU(launch_fix_group(dm, f, mode, x->K, x->g, x->rx, s));
+  ScoreArgs a = score_args(x);
+  a.off = x->fix_qoff;
+  a.ent = x->fix_sorted;
+  a.itemoff = x->fix_iof;
+  a.out = out;
+  a.list_div = mode == kModeTruncF ? dm.Cp : dm.SL;
+  CU(run_score(x, kModeList, a));
+  CU(launch_fix_ovf(f, 0, s));
+  CU(launch_fix_f64(dm, f, mode, x->K, x->g, x->rx, out, s));
+  if (mode == kModeAnchor)
+    CU(launch_fix_scan_anchor(dm, f, x->g, x->gcnt, x->kinv_off, x->kinv_ent, out, s));
+  else if (mode == kModeExtra)
+    CU(launch_fix_scan_single(dm, f, x->ex_off, x->ex_ent, dm.SL, dm.Cp * dm.G, out, s));
+  else
+    CU(launch_fix_scan_single(dm, f, x->kinv_off, x->kinv_ent, 0, dm.Cp, out, s));
+  x->end(tf);
+  return VMFA_OK;
 }
 
 int run_precompute(vmfa_ctx* x, int* failed, bool sync = true) {
@@ -401,6 +454,7 @@ int score_anchors(vmfa_ctx* x) {
   const int tok = x->begin(kFamScoreAnchor, dm.N * dm.Cp);
   CU(run_score(x, kModeAnchor, a));
   x->end(tok);
+  TRY(rescore(x, kModeAnchor, x->LJ));
   return VMFA_OK;
 }
 
@@ -545,6 +599,7 @@ int estep_local(vmfa_ctx* x, uint64_t seed, uint64_t it, int mode, bool exchange
     const int tok2 = x->begin(kFamScoreExtra, dm.N);
     CU(run_score(x, kModeExtra, a));
     x->end(tok2);
+    TRY(rescore(x, kModeExtra, x->LJ));
   }
   // selection, labels, block 4
   {
@@ -788,6 +843,7 @@ int free_energy_local(vmfa_ctx* x, bool lookahead) {
     a.out = x->LJK;
     const int tok = x->begin(kFamScoreTruncF, dm.N * dm.Cp);
     CU(run_score(x, kModeTruncF, a));
+    TRY(rescore(x, kModeTruncF, x->LJK));
     CU(launch_lse_rows(x->LJK, dm.N, dm.Cp, x->lse, s));
     x->end(tok);
   }
@@ -985,7 +1041,9 @@ int vmfa_ctx_create(vmfa_ctx** out, int device, int C, int D, int H, int Cp, int
   A(x->mu32, Cs * D);
   A(x->WT, Cs * x->Hp * D);
   if (x->scorer == 2) {
-    A(x->jobs, N * Cp / 128 + Cs + 2);  // items <= sum_c ceil(rows_c / 128)
+    // items <= sum_c ceil(rows_c / 128); the re-scoring lists hold <= fix_cap entries
+    x->fix_cap = std::max<long long>(1 << 20, static_cast<long long>(N) * Cp);
+    A(x->jobs, static_cast<size_t>(x->fix_cap) / 128 + Cs + 2);
     A(x->bimg, ws_image_halves(dm, 0));
     A(x->simg, ws_image_halves(dm, 1));
     A(x->bscl, ws_scale_floats(dm, 0));
@@ -996,6 +1054,18 @@ int vmfa_ctx_create(vmfa_ctx** out, int device, int C, int D, int H, int Cp, int
     A(x->mumax, Cs);
   }
   A(x->ipsi32, Cs * D);
+  A(x->nfix, 1);
+  A(x->fix_cnt, 2);
+  A(x->fix_ovf, 2);
+  x->fix_ok = x->scorer == 2 && static_cast<int64_t>(N) * dm.SL < (int64_t{1} << 31);
+  A(x->fix_list, static_cast<size_t>(x->fix_cap));
+  A(x->fix_sorted, static_cast<size_t>(x->fix_cap));
+  A(x->fix_qkey, static_cast<size_t>(x->fix_cap));
+  A(x->fix_qcnt, Cs);
+  A(x->fix_qoff, Cs + 1);
+  A(x->fix_qfill, Cs);
+  A(x->fix_iof, Cs + 1);
+  if (r == VMFA_OK) cudaMemsetAsync(x->nfix, 0, sizeof(unsigned long long), x->stream);
   A(x->K, N * Cp);
   // g and its counts contiguous ([C*G | C] int32), so the sparse exchange can
   // all-reduce a rank's selected rows as one buffer (VMFA_XCHG_G)
@@ -1864,13 +1934,17 @@ int vmfa_scoring_work(vmfa_ctx* x, int64_t* out, int n) {
     CU(cudaMemcpyAsync(&ex, x->ex_off + dm.C, sizeof(int), cudaMemcpyDeviceToHost, x->stream));
     CU(cudaStreamSynchronize(x->stream));
   }
-  const int64_t w[6] = {static_cast<int64_t>(dm.N) * dm.Cp,
+  unsigned long long nfl = 0;  // read and cleared
+  CU(cudaMemcpyAsync(&nfl, x->nfix, sizeof nfl, cudaMemcpyDeviceToHost, x->stream));
+  CU(cudaMemsetAsync(x->nfix, 0, sizeof(unsigned long long), x->stream));
+  CU(cudaStreamSynchronize(x->stream));
+  const int64_t w[7] = {static_cast<int64_t>(dm.N) * dm.Cp,
                         ex,
                         x->scorer == 2 ? ws_image_halves(dm, 0) * 2 : 0,
                         x->scorer == 2 ? ws_image_halves(dm, 1) * 2 : 0,
                         x->scorer == 2 ? (ws_record_floats(dm, 0) + ws_record_floats(dm, 1)) * 4 : 0,
-                        x->scorer};
-  for (int i = 0; i < n && i < 6; ++i) out[i] = w[i];
+                        x->scorer, static_cast<int64_t>(nfl)};
+  for (int i = 0; i < n && i < 7; ++i) out[i] = w[i];
   return VMFA_OK;
 }
 

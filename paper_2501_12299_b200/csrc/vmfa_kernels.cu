@@ -266,6 +266,11 @@ k_score(ScoreArgs a) {
 // asc) (estep.cpp:103-122), labels the row by the first strict maximum over the
 // ascending K row (estep.cpp:157-166) and computes the fp64 responsibilities
 // and LSE of block 4 (estep.cpp:316-335).
+// A component scored by several anchors keeps the value of its most accurate
+// slot: the anchor-centred expansion of (x - mu_q) around mu_a loses
+// sum (x - mu_a)^2 / psi_q relative precision, so a self slot (q == a: the
+// expansion is exact, delta = 0) or the uncovered extra (one-component pass)
+// wins, else the anchor closest to x (largest own log-joint l(n, a)).
 struct Cand {
   float l;
   int c;
@@ -296,6 +301,8 @@ __global__ void __launch_bounds__(256) k_select(SelectArgs a) {
   for (int i = threadIdx.x; i < W * (blockDim.x >> 5); i += blockDim.x) s_seen[i] = 0u;
   __syncthreads();
   unsigned* seen = s_seen + (threadIdx.x >> 5) * W;
+  // per warp: own log-joint of each anchor j (its self slot), <= 8 anchors
+  float* qual = reinterpret_cast<float*>(s_seen + W * (blockDim.x >> 5)) + (threadIdx.x >> 5) * 8;
   const int64_t warp0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int CpG = dm.Cp * dm.G;
@@ -336,15 +343,64 @@ __global__ void __launch_bounds__(256) k_select(SelectArgs a) {
 #pragma unroll
     for (int k = 0; k + 1 < NS; ++k)
       if (uniq[k]) atomicAnd(&seen[comp[k] >> 5], ~(1u << (comp[k] & 31)));
+    // slot values; the extra slot holds a value only when it is not a
+    // duplicate (k_extra leaves covered extras unscored)
+    float pri[NS];
 #pragma unroll
     for (int k = 0; k < NS; ++k) {
-      float v = 0.f;
-      if (uniq[k]) {
-        v = a.LJ[n * dm.SL + k * 32 + lane];
+      const int s = k * 32 + lane;
+      float v = -INFINITY;
+      const bool scored = comp[k] >= 0 && (s < CpG || uniq[k]);
+      if (scored) {
+        v = a.LJ[n * dm.SL + s];
         if (v != v) v = -INFINITY;  // NaN ranks last (reference comparator undefined)
       }
       lj[k] = v;
+      pri[k] = -INFINITY;
+      if (s < CpG && comp[k] >= 0) {
+        const int j = __float2int_rz((static_cast<float>(s) + 0.5f) * invG);
+        if (comp[k] == a.K[n * dm.Cp + j]) {
+          qual[j] = v;
+          pri[k] = INFINITY;
+        }
+      } else if (s == CpG && scored) {
+        pri[k] = INFINITY;
+      }
     }
+    __syncwarp();
+    bool dups = false;
+#pragma unroll
+    for (int k = 0; k < NS; ++k) {
+      const int s = k * 32 + lane;
+      if (s < CpG && comp[k] >= 0 && pri[k] != INFINITY)
+        pri[k] = qual[__float2int_rz((static_cast<float>(s) + 0.5f) * invG)];
+      dups |= comp[k] >= 0 && !uniq[k];
+    }
+    // the first occurrence takes the value of the best slot of its component
+    if (__any_sync(kFull, dups)) {
+      float bp[NS];
+#pragma unroll
+      for (int k = 0; k < NS; ++k) bp[k] = pri[k];
+#pragma unroll
+      for (int k2 = 0; k2 < NS; ++k2) {
+        for (int t = 0; t < 32; ++t) {
+          const int oc = __shfl_sync(kFull, comp[k2], t);
+          const float op = __shfl_sync(kFull, pri[k2], t);
+          const float ov = __shfl_sync(kFull, lj[k2], t);
+          if (oc < 0) continue;
+#pragma unroll
+          for (int k = 0; k < NS; ++k)
+            if (uniq[k] && oc == comp[k] && op > bp[k]) {
+              bp[k] = op;
+              lj[k] = ov;
+            }
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < NS; ++k)
+      if (!uniq[k]) lj[k] = 0.f;
+    __syncwarp();
     // compaction of the retained joints (reference layout, insertion order)
     int base = 0;
 #pragma unroll
@@ -2839,7 +2895,8 @@ cudaError_t launch_score(int mode, const ScoreArgs& a, int grid, cudaStream_t s)
 cudaError_t launch_select(const SelectArgs& a, cudaStream_t s) {
   const int ns = (a.dm.SL + 31) / 32;
   const int grid = grid_for(a.dm.N * 32, 256, sm_count() * 16);
-  const size_t smem = static_cast<size_t>((a.dm.C + 31) / 32) * 8 * sizeof(unsigned);  // 8 warps' bitmaps
+  // 8 warps' bitmaps + their anchor log-joints
+  const size_t smem = static_cast<size_t>((a.dm.C + 31) / 32) * 8 * sizeof(unsigned) + 64 * sizeof(float);
   if (smem > 200 * 1024) return cudaErrorInvalidValue;
   auto go = [&](auto kern) {
     if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));

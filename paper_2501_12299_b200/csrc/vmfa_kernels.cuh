@@ -52,7 +52,10 @@ struct Dims {
 };
 
 // scoring modes
-enum ScoreMode : int { kModeAnchor = 0, kModeExtra = 1, kModeTruncF = 2 };
+// kModeList: one-component re-scoring of listed output indices (the scores
+// the anchor / extra / truncated-F passes flagged, grouped by component);
+// entry = output index, row = entry / ScoreArgs.list_div
+enum ScoreMode : int { kModeAnchor = 0, kModeExtra = 1, kModeTruncF = 2, kModeList = 3 };
 
 struct ScoreArgs {
   Dims dm;
@@ -66,6 +69,7 @@ struct ScoreArgs {
   const int* g;           // neighbourhoods C x G
   const int* gcnt;
   float* out;             // LJ slots (N x SL) or LJK (N x Cp)
+  int list_div = 1;       // kModeList: row = entry / list_div (SL or C')
 };
 
 struct SelectArgs {
@@ -266,7 +270,39 @@ struct WsOperands {
   const float* bscl;   // their row scales
   const void* simg;    // one-component B stage images (extra / truncated F), per precompute
   const float* sscl;
+  long long* fix_list = nullptr;           // flagged scores: output indices (vmfa_fixup.cu)
+  unsigned long long* fix_cnt = nullptr;   // [0] count, [1] overflow
+  long long fix_cap = 0;
 };
+// fp64 re-evaluation of the scores the tensor-core scorer flagged (vmfa_fixup.cu)
+struct FixArgs {
+  const float* X;
+  const double* mu;
+  const double* psi;
+  const double* lam;
+  const double* R;
+  const double* kconst;
+  const long long* list;         // flagged output indices appended by the scorer
+  unsigned long long* cnt;       // [0] entries appended, [1] overflow (list full: scan instead)
+  long long cap;                 // list capacity
+  unsigned long long* nfix;      // scores re-evaluated (accumulated)
+  int* qkey;                     // grouping scratch: component per entry (cap)
+  int* sorted;                   // entries grouped by component (cap)
+  int* qcnt;                     // per component (C), offsets (C+1), fill cursors (C)
+  int* qoff;
+  int* qfill;
+  int* iof;                      // work-item offsets per component (C+1)
+  unsigned long long* ovf;       // [1]: a list overflowed (the scan kernels run)
+};
+cudaError_t launch_fix_ovf(const FixArgs& f, int first, cudaStream_t s);
+cudaError_t launch_fix_group(const Dims& dm, const FixArgs& f, int mode, const int* K, const int* g, const int* rx,
+                             cudaStream_t s);
+cudaError_t launch_fix_f64(const Dims& dm, const FixArgs& f, int mode, const int* K, const int* g, const int* rx,
+                           float* out, cudaStream_t s);
+cudaError_t launch_fix_scan_anchor(const Dims& dm, const FixArgs& f, const int* g, const int* gcnt,
+                                   const int* kinv_off, const int* kinv_ent, float* LJ, cudaStream_t s);
+cudaError_t launch_fix_scan_single(const Dims& dm, const FixArgs& f, const int* off, const int* ent, int extra_stride,
+                                   int extra_col, float* out, cudaStream_t s);
 // true while vmfa_diag_scorer_cycles has the scorer counters armed
 bool ws_diag_armed();
 cudaError_t launch_score_ws(int mode, const ScoreArgs& s, const WsOperands& op, int4* jobs, cudaStream_t st,

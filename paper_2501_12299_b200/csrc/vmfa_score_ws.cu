@@ -67,6 +67,10 @@ constexpr int kMaxD = 1024;
 constexpr int kNL = 16;               // lin rows / psi rows per group (qg <= 16)
 constexpr int kTargetExp = 14;        // operands scaled to |value| <= 2^14
 __host__ __device__ constexpr int rec_stride(int Hp) { return 8 + 2 * Hp; }  // floats per epilogue record
+// a score whose terms B exceed kCancel M, M a lower bound of the log-joint's
+// term magnitude (_helpers.lj_term_scale), is re-evaluated in fp64: the
+// ~1e-6 B error of the fp32-accurate terms then stays below 1e-4 M
+constexpr float kCancel = 32.f;
 // components per anchor job: the accumulator [16 lin | qg*Hp W | 16 psi] must
 // fit one 256-column TMEM buffer
 __host__ __device__ constexpr int qg_max(int Hp) { return (256 - 2 * kNL) / Hp < kNL ? (256 - 2 * kNL) / Hp : kNL; }
@@ -98,6 +102,10 @@ struct WsArgs {
   const int* g;
   const int* gcnt;
   float* out;
+  int list_div;              // kModeList: row = entry / list_div
+  long long* fix_list;       // flagged scores (output indices), nullptr: flags only
+  unsigned long long* fix_cnt;
+  long long fix_cap;
   unsigned long long* prof;  // optional per-role cycle counters (nullptr: off)
   int dbg;                   // diagnostics only: bit0 skip x loads, bit2 skip MMAs
 };
@@ -306,7 +314,7 @@ __device__ __forceinline__ Walk walk_begin(const int4* jobs, int total) {
 __device__ __forceinline__ int job_row(const WsArgs& a, const int4& J, int r) {
   if (r >= J.z) return -1;
   const int e = __ldg(a.ent + J.y + r);
-  return a.mode == kModeExtra ? e : e / a.dm.Cp;
+  return a.mode == kModeExtra ? e : e / (a.mode == kModeList ? a.list_div : a.dm.Cp);
 }
 // A-row scale exponent of row n centred on component c (same in producer and epilogue)
 __device__ __forceinline__ int row_exp(const WsArgs& a, int n, int c) {
@@ -624,7 +632,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_ws(WsArgs a, const __grid
       const int c = w.J.x;
       const int nq = min(a.qg, w.J.w - w.g0);
       const int e = r < w.J.z ? __ldg(a.ent + w.J.y + r) : -1;
-      const int n = e < 0 ? -1 : (a.mode == kModeExtra ? e : e / dm.Cp);
+      const int n = e < 0 ? -1 : (a.mode == kModeExtra ? e : e / (a.mode == kModeList ? a.list_div : dm.Cp));
       {
         const float4* src = reinterpret_cast<const float4*>(
             a.rec + ((int64_t)c * (a.mode == kModeAnchor ? dm.G : 1) + w.g0) * R);
@@ -656,8 +664,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_ws(WsArgs a, const __grid
           obase = e;
         }
       }
-      // one component's log-joint from |y|^2 (yy), its lin / psi accumulators and record
-      auto finish = [&](int qi, float yy) {
+      // one component's log-joint from |y|^2 (yy), its lin / psi accumulators and record.
+      // Cancellation check: the fp32-accurate terms carry ~1e-6 of their
+      // magnitude B = sum u^2/psi + |lin| + m + 2 sum |t|(|y| + |b|); when B
+      // exceeds kCancel M (M <= the log-joint's term magnitude) the result
+      // could miss the 1e-4 bar, so the
+      // slot is flagged in the lowest mantissa bit of its score (every other
+      // score has that bit cleared: 1 ulp) and vmfa_fixup.cu re-evaluates it
+      // in fp64.
+      auto finish = [&](int qi, float yy, float ey) {
         const float* rc = srec + qi * R;
         float linq = 0.f, d2q = 0.f;
 #pragma unroll
@@ -670,8 +685,25 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_ws(WsArgs a, const __grid
         d2q *= invQ * rc[4];
         const double kc = static_cast<double>(rc[1]) + static_cast<double>(rc[5]);
         const double diag = static_cast<double>(d2q) + static_cast<double>(linq) + static_cast<double>(rc[2]);
-        const float lj = static_cast<float>(kc - 0.5 * (diag - static_cast<double>(yy)));
-        if (e >= 0) a.out[obase + (a.mode == kModeAnchor ? qi : 0)] = lj;
+        const double Q = diag - static_cast<double>(yy);
+        float lj = static_cast<float>(kc - 0.5 * Q);
+        // the test's scale (_helpers.lj_term_scale) is >= max(0.92 D, |kconst| - |log pi|, |Q| / 2)
+        const float B = fabsf(d2q) + fabsf(linq) + fabsf(rc[2]) + 2.f * ey + yy;
+        const float M = fmaxf(fmaxf(0.9f * static_cast<float>(dm.D), fabsf(static_cast<float>(kc)) - 20.f),
+                              0.5f * fabsf(static_cast<float>(Q)));
+        const bool flag = B > kCancel * M;
+        unsigned bits = __float_as_uint(lj);
+        if (isfinite(lj)) bits = flag ? (bits | 1u) : (bits & ~1u);
+        lj = __uint_as_float(bits);
+        if (e >= 0) {
+          const int64_t o = obase + (a.mode == kModeAnchor ? qi : 0);
+          a.out[o] = lj;
+          if (flag && a.fix_list && isfinite(lj)) {
+            const unsigned long long pos = atomicAdd(a.fix_cnt, 1ull);
+            if (static_cast<long long>(pos) < a.fix_cap) a.fix_list[pos] = o;
+            else a.fix_cnt[1] = 1ull;
+          }
+        }
       };
       if constexpr (HP <= 16) {
         for (int q0 = 0; q0 < nq; q0 += kEpiBatch) {
@@ -686,19 +718,21 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_ws(WsArgs a, const __grid
           for (int qi = 0; qi < kEpiBatch; ++qi) {
             if (qi >= nb) break;
             const float* rc = srec + (q0 + qi) * R;
-            float yy = 0.f;
+            float yy = 0.f, ey = 0.f;
 #pragma unroll
             for (int h = 0; h < HP; ++h) {
-              const float t = y[qi][h] * (invA * rc[8 + HP + h]) - rc[8 + h];
+              const float ys = y[qi][h] * (invA * rc[8 + HP + h]);
+              const float t = ys - rc[8 + h];
               yy = fmaf(t, t, yy);
+              ey = fmaf(fabsf(t), fabsf(ys) + fabsf(rc[8 + h]), ey);
             }
-            finish(q0 + qi, yy);
+            finish(q0 + qi, yy, ey);
           }
         }
       } else {  // wide factors: 16 columns at a time
         for (int qi = 0; qi < nq; ++qi) {
           const float* rc = srec + qi * R;
-          float yy = 0.f;
+          float yy = 0.f, ey = 0.f;
           for (int h0 = 0; h0 < HP; h0 += 16) {
             float y[16];
             tmem_ld_nowait<16>(trow + kNL + qi * HP + h0, y);
@@ -706,11 +740,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_ws(WsArgs a, const __grid
             pin_regs<16>(y);
 #pragma unroll
             for (int h = 0; h < 16; ++h) {
-              const float t = y[h] * (invA * rc[8 + HP + h0 + h]) - rc[8 + h0 + h];
+              const float ys = y[h] * (invA * rc[8 + HP + h0 + h]);
+              const float t = ys - rc[8 + h0 + h];
               yy = fmaf(t, t, yy);
+              ey = fmaf(fabsf(t), fabsf(ys) + fabsf(rc[8 + h0 + h]), ey);
             }
           }
-          finish(qi, yy);
+          finish(qi, yy, ey);
         }
       }
       fence_before();
@@ -1127,6 +1163,10 @@ cudaError_t launch_score_ws(int mode, const ScoreArgs& s, const WsOperands& op, 
   a.g = s.g;
   a.gcnt = s.gcnt;
   a.out = s.out;
+  a.list_div = s.list_div;
+  a.fix_list = op.fix_list;
+  a.fix_cnt = op.fix_cnt;
+  a.fix_cap = op.fix_cap;
   a.prof = g_ws_prof;
   a.dbg = g_ws_prof ? g_ws_dbg : 0;
   if (build_jobs) k_build_jobs<<<(s.dm.C + 255) / 256, 256, 0, st>>>(s.dm.C, mode, s.off, s.itemoff, s.gcnt, jobs);

