@@ -176,6 +176,52 @@ int vmfa_em_full_step(vmfa_ctx* ctx, double* log_likelihood, uint64_t* joints);
 int vmfa_afkmc2_seed(vmfa_ctx* ctx, int C, int chain_length, uint64_t stream_seed, int64_t* seeds,
                      uint64_t* stream_state, uint64_t* distances);
 
+/* ---- reference entry points with caller-supplied state (mstep.hpp:27-31,
+ * model.hpp:116-119). Both replace the context's K with `K` (N x C', rows
+ * sorted, validated like vmfa_upload_state).
+ * accumulate_suffstats(params, caches, data, ksets, resp): statistics of the
+ * given K rows and responsibilities (N x C' fp64, aligned with K) under the
+ * context's (pre-update) parameters, into the statistics buffer -- e.g. the
+ * per-cluster FA fit of kmeans.cpp:195-210 (C = C' = 1, K = 0, resp = 1).  */
+int vmfa_accumulate_suffstats_k(vmfa_ctx* ctx, const int32_t* K, const double* resp);
+/* truncated_free_energy(params, caches, data, ksets): sum_n LSE over the
+ * given K rows under the context's parameters (EmptyKSet for K == NULL).   */
+int vmfa_truncated_free_energy_k(vmfa_ctx* ctx, const int32_t* K, double* free_energy);
+
+/* ---- log_joint (model.hpp:83-86, model.cpp:81-95), batched: out[i] =
+ * log p(c_i, x_i) for n rows X (n x D, host) and components comp[i], in fp64
+ * under the context's parameters (the reference's EvalCounter adds n).     */
+int vmfa_log_joint(vmfa_ctx* ctx, const float* X, int64_t n, const int32_t* comp, double* out);
+
+/* ---- the E-step's per-operation pieces (estep.hpp:82-117), each batched
+ * over the context's N rows (stride = min(C'G+1, C)); host arrays in the
+ * reference layouts (RetainedJoints: count N, idx / lj N x stride).
+ *   build_search_space (estep.cpp:126-133): S(n) of the context's K and g
+ *     with extra r_n = extras[n], or (extras == NULL) uniform_component(seed,
+ *     iteration, n_offset + n, C) (rng.hpp:91-98), insertion order, -1 pad;
+ *   update_k (estep.cpp:135-142): top-C' of each row by (l desc, index asc),
+ *     sorted ascending; InsufficientCandidates if count < C';
+ *   hard_partition (estep.cpp:144-173): labels and the partition as offsets
+ *     (C+1) and rows (N, ascending within each component);
+ *   accumulate_distances (estep.cpp:175-202): block 3's accumulator as rows
+ *     (c, ct, sum, count) in (c, ct) order (fp64 sums in the reference's
+ *     per-key order); pass cap = 0 to query the row count in *n_rows;
+ *   update_g (estep.cpp:204-220): g rows (C x G, -1 padded) + counts from
+ *     accumulator rows;
+ *   responsibilities_row (estep.cpp:222-228): rows x width softmax.        */
+int vmfa_build_search_space(vmfa_ctx* ctx, uint64_t seed, uint64_t iteration, const int32_t* extras,
+                            int32_t* count, int32_t* idx);
+int vmfa_update_k(vmfa_ctx* ctx, const int32_t* count, const int32_t* idx, const double* lj, int32_t* K);
+int vmfa_hard_partition(vmfa_ctx* ctx, const int32_t* K, const int32_t* count, const int32_t* idx,
+                        const double* lj, int32_t* labels, int32_t* part_off, int32_t* part_ent);
+int vmfa_accumulate_distances(vmfa_ctx* ctx, int mode, const int32_t* part_off, const int32_t* part_ent,
+                              const int32_t* count, const int32_t* idx, const double* lj, const double* pi,
+                              int64_t cap, int32_t* c, int32_t* ct, double* sum, int64_t* count_out,
+                              int64_t* n_rows);
+int vmfa_update_g(vmfa_ctx* ctx, int64_t n_rows, const int32_t* c, const int32_t* ct, const double* sum,
+                  const int64_t* count, int32_t* g, int32_t* g_count);
+int vmfa_responsibilities(vmfa_ctx* ctx, int64_t rows, int width, const double* lj, double* resp);
+
 /* One main-loop iteration of train_vmfa (trainer.cpp:149-160): E-step,
  * statistics, update, precompute, post-M-step truncated free energy.
  * Single-context only (use the phase API for multi-GPU).                    */

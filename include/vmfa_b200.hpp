@@ -194,9 +194,7 @@ inline EStepResult variational_e_step(Session& s, VarState& state, uint64_t seed
   return r;
 }
 
-// accumulate_suffstats (mstep.hpp:27-31) of the last E-step on the device.
-inline SuffStats accumulate_suffstats(Session& s) {
-  check(vmfa_accumulate_suffstats(s.handle()));
+inline SuffStats download_suffstats(Session& s) {
   SuffStats st;
   const size_t C = s.C(), D = s.D(), H1 = s.H() + 1;
   st.Nc.resize(C);
@@ -205,6 +203,24 @@ inline SuffStats accumulate_suffstats(Session& s) {
   st.sq_sum.resize(C * D);
   check(vmfa_download_suffstats(s.handle(), st.Nc.data(), st.Y.data(), st.E.data(), st.sq_sum.data()));
   return st;
+}
+
+// accumulate_suffstats (mstep.hpp:27-31) of the last E-step's K and
+// responsibilities, on the device.
+inline SuffStats accumulate_suffstats(Session& s) {
+  check(vmfa_accumulate_suffstats(s.handle()));
+  return download_suffstats(s);
+}
+
+// accumulate_suffstats(params, caches, data, ksets, resp) with the caller's K
+// rows (N x C') and responsibilities (N x C', aligned with K) under the
+// session's parameters; the session's K becomes ksets.
+inline SuffStats accumulate_suffstats(Session& s, const std::vector<int32_t>& ksets,
+                                      const std::vector<double>& resp) {
+  if (ksets.size() != size_t(s.rows()) * s.Cprime() || resp.size() != ksets.size())
+    throw std::invalid_argument("ksets / resp sizes");
+  check(vmfa_accumulate_suffstats_k(s.handle(), ksets.data(), resp.data()));
+  return download_suffstats(s);
 }
 
 // update_params (mstep.hpp:39-41) from `stats`; the session keeps the result
@@ -217,30 +233,128 @@ inline MfaParams update_params(Session& s, const SuffStats& stats) {
   return s.download_params();
 }
 
-// truncated_free_energy (model.hpp:116-119) under the session's parameters.
-inline double truncated_free_energy(Session& s, const VarState& ksets) {
-  (void)ksets;  // the session's K is the state of the last E-step / upload
+// truncated_free_energy (model.hpp:116-119) under the session's parameters
+// over the caller's K rows (the session's K becomes ksets); adds N C' to the
+// counter, as the reference does.
+inline double truncated_free_energy(Session& s, const std::vector<int32_t>& ksets, EvalCounter& counter) {
+  if (ksets.empty()) throw EmptyKSet("empty K collection");
+  if (ksets.size() != size_t(s.rows()) * s.Cprime()) throw std::invalid_argument("ksets size");
   double F = 0.0;
-  check(vmfa_truncated_free_energy(s.handle(), &F));
+  check(vmfa_truncated_free_energy_k(s.handle(), ksets.data(), &F));
+  counter.joints += static_cast<uint64_t>(s.rows()) * s.Cprime();
   return F;
+}
+inline double truncated_free_energy(Session& s, const VarState& state, EvalCounter& counter) {
+  return truncated_free_energy(s, state.K, counter);
+}
+
+// log_joint (model.hpp:83-86): log p(c, x) in fp64 under the session's
+// parameters; counter.joints += 1 per pair. Batched: rows X (n x D).
+inline std::vector<double> log_joint(Session& s, const std::vector<float>& X, const std::vector<int32_t>& comp,
+                                     EvalCounter& counter) {
+  if (X.size() != comp.size() * size_t(s.D())) throw std::invalid_argument("X / comp sizes");
+  std::vector<double> out(comp.size());
+  check(vmfa_log_joint(s.handle(), X.data(), static_cast<int64_t>(comp.size()), comp.data(), out.data()));
+  counter.joints += comp.size();
+  return out;
+}
+inline double log_joint(Session& s, int c, const float* x, EvalCounter& counter) {
+  double out = 0.0;
+  const int32_t cc = c;
+  check(vmfa_log_joint(s.handle(), x, 1, &cc, &out));
+  counter.joints += 1;
+  return out;
+}
+
+// ---- the E-step's per-operation pieces (estep.hpp:82-117), batched over the
+// session's rows; RetainedJoints / partition in the reference layouts
+struct RetainedJoints {  // estep.hpp:48-70
+  int stride = 0;
+  std::vector<int32_t> count, idx;
+  std::vector<double> lj;
+};
+// build_search_space for every row of the session's K / g: extra r_n from
+// `extras` (N entries) or uniform_component(seed, iteration, n_offset + n, C)
+inline RetainedJoints build_search_space(Session& s, uint64_t seed, uint64_t iteration,
+                                         const std::vector<int32_t>* extras = nullptr) {
+  RetainedJoints r;
+  r.stride = s.stride();
+  r.count.resize(s.rows());
+  r.idx.resize(size_t(s.rows()) * r.stride);
+  check(vmfa_build_search_space(s.handle(), seed, iteration, extras ? extras->data() : nullptr, r.count.data(),
+                                r.idx.data()));
+  return r;
+}
+// update_k for every row: top-C' by (l desc, index asc), sorted ascending
+inline std::vector<int32_t> update_k(Session& s, const RetainedJoints& r) {
+  std::vector<int32_t> K(size_t(s.rows()) * s.Cprime());
+  check(vmfa_update_k(s.handle(), r.count.data(), r.idx.data(), r.lj.data(), K.data()));
+  return K;
+}
+// hard_partition: labels and the partition (offsets C+1, rows ascending per cell)
+inline void hard_partition(Session& s, const std::vector<int32_t>& K, const RetainedJoints& r,
+                           std::vector<int32_t>& labels, std::vector<int32_t>& part_off,
+                           std::vector<int32_t>& part_ent) {
+  labels.resize(s.rows());
+  part_off.resize(s.C() + 1);
+  part_ent.resize(s.rows());
+  check(vmfa_hard_partition(s.handle(), K.data(), r.count.data(), r.idx.data(), r.lj.data(), labels.data(),
+                            part_off.data(), part_ent.data()));
+}
+struct DistanceRows {  // DistanceAccumulator (estep.hpp:34-44) as sorted rows
+  std::vector<int32_t> c, ct;
+  std::vector<double> sum;
+  std::vector<int64_t> count;
+};
+inline DistanceRows accumulate_distances(Session& s, const std::vector<int32_t>& part_off,
+                                         const std::vector<int32_t>& part_ent, const RetainedJoints& r,
+                                         DistanceMode mode, const MfaParams& params) {
+  DistanceRows d;
+  int64_t n = 0;
+  check(vmfa_accumulate_distances(s.handle(), static_cast<int>(mode), part_off.data(), part_ent.data(),
+                                  r.count.data(), r.idx.data(), r.lj.data(), params.pi.data(), 0, nullptr, nullptr,
+                                  nullptr, nullptr, &n));
+  d.c.resize(n), d.ct.resize(n), d.sum.resize(n), d.count.resize(n);
+  check(vmfa_accumulate_distances(s.handle(), static_cast<int>(mode), part_off.data(), part_ent.data(),
+                                  r.count.data(), r.idx.data(), r.lj.data(), params.pi.data(), n, d.c.data(),
+                                  d.ct.data(), d.sum.data(), d.count.data(), &n));
+  return d;
+}
+// update_g for every component: g rows (C x G, -1 padded) and counts
+inline void update_g(Session& s, const DistanceRows& d, std::vector<int32_t>& g, std::vector<int32_t>& g_count) {
+  g.resize(size_t(s.C()) * s.G());
+  g_count.resize(s.C());
+  check(vmfa_update_g(s.handle(), static_cast<int64_t>(d.c.size()), d.c.data(), d.ct.data(), d.sum.data(),
+                      d.count.data(), g.data(), g_count.data()));
+}
+// responsibilities_row for `rows` rows of `width` log-joints
+inline std::vector<double> responsibilities(Session& s, const std::vector<double>& lj, int width) {
+  std::vector<double> out(lj.size());
+  check(vmfa_responsibilities(s.handle(), static_cast<int64_t>(lj.size() / width), width, lj.data(), out.data()));
+  return out;
 }
 
 // exact_log_likelihood (model.hpp:108-111): sum_n log sum_c p(x_n, c) over all
 // C components under the session's parameters (the NLL of trainer.cpp:49-56,
-// 79-85 is -exact_log_likelihood / N).
-inline double exact_log_likelihood(Session& s) {
+// 79-85 is -exact_log_likelihood / N); adds N C to the counter.
+inline double exact_log_likelihood(Session& s, EvalCounter& counter) {
   double ll = 0.0;
   check(vmfa_exact_log_likelihood(s.handle(), &ll));
+  counter.joints += static_cast<uint64_t>(s.rows()) * s.C();
   return ll;
+}
+inline double exact_log_likelihood(Session& s) {
+  EvalCounter scratch;
+  return exact_log_likelihood(s, scratch);
 }
 
 // em_full_step (mstep.hpp; mstep.cpp:164-208): full-posterior statistics of
 // every (n, c) pair under the session's parameters; returns sum_n LSE_n.
-inline double em_full_step(Session& s, SuffStats& stats, uint64_t* joints = nullptr) {
+inline double em_full_step(Session& s, SuffStats& stats, EvalCounter& counter) {
   double ll = 0.0;
   uint64_t j = 0;
   check(vmfa_em_full_step(s.handle(), &ll, &j));
-  if (joints) *joints = j;
+  counter.joints += j;
   const size_t C = s.C(), D = s.D(), H1 = s.H() + 1;
   stats.Nc.resize(C);
   stats.Y.resize(C * D * H1);

@@ -102,6 +102,15 @@ _SIGS = {
     "vmfa_cooc_select": (_I, [_P, _P, _P, _P, _P, C.c_int64, _I, _I]),
     "vmfa_profile_enable": (_I, [_P, _I]),
     "vmfa_scoring_work": (_I, [_P, _P, _I]),
+    "vmfa_accumulate_suffstats_k": (_I, [_P, _P, _P]),
+    "vmfa_truncated_free_energy_k": (_I, [_P, _P, C.POINTER(_D)]),
+    "vmfa_log_joint": (_I, [_P, _P, _I64, _P, _P]),
+    "vmfa_build_search_space": (_I, [_P, _U64, _U64, _P, _P, _P]),
+    "vmfa_update_k": (_I, [_P, _P, _P, _P, _P]),
+    "vmfa_hard_partition": (_I, [_P, _P, _P, _P, _P, _P, _P, _P]),
+    "vmfa_accumulate_distances": (_I, [_P, _I, _P, _P, _P, _P, _P, _P, _I64, _P, _P, _P, _P, C.POINTER(_I64)]),
+    "vmfa_update_g": (_I, [_P, _I64, _P, _P, _P, _P, _P, _P]),
+    "vmfa_responsibilities": (_I, [_P, _I64, _I, _P, _P]),
     "vmfa_kernel_times": (_I, [_P, _I, _P, _P, _P, C.POINTER(_I)]),
     "vmfa_kernel_name": (C.c_char_p, [_I]),
     "vmfa_ctx_stream": (_P, [_P]),

@@ -1924,6 +1924,263 @@ int vmfa_cooc_select(vmfa_ctx* x, const void* key, const void* cnt, const void* 
   return VMFA_OK;
 }
 
+// ---------------------------------------------------------------- per-operation pieces
+}  // extern "C"
+namespace {
+// a device copy of a host array for the duration of one call (stream-ordered)
+template <class T>
+struct DevTmp {
+  T* p = nullptr;
+  cudaStream_t s = nullptr;
+  cudaError_t make(const T* host, size_t n, cudaStream_t st) {
+    s = st;
+    if (cudaError_t e = cudaMallocAsync(&p, std::max<size_t>(n, 1) * sizeof(T), s); e != cudaSuccess) return e;
+    return host ? cudaMemcpyAsync(p, host, n * sizeof(T), cudaMemcpyHostToDevice, s) : cudaSuccess;
+  }
+  ~DevTmp() {
+    if (p) cudaFreeAsync(p, s);
+  }
+};
+}  // namespace
+extern "C" {
+
+int vmfa_log_joint(vmfa_ctx* x, const float* X, int64_t n, const int32_t* comp, double* out) {
+  TRY(check_ctx(x));
+  if (n < 0 || (n > 0 && (!X || !comp || !out))) return fail(VMFA_ERR_INVALID_ARGUMENT, "vmfa_log_joint: bad arguments");
+  if (n == 0) return VMFA_OK;
+  const Dims& dm = x->dm;
+  for (int64_t i = 0; i < n; ++i)
+    if (comp[i] < 0 || comp[i] >= dm.C) return fail(VMFA_ERR_INVALID_ARGUMENT, "component index out of range");
+  cudaStream_t s = x->stream;
+  DevTmp<float> dx;
+  DevTmp<int> dc;
+  DevTmp<double> dout;
+  CU(dx.make(X, static_cast<size_t>(n) * dm.D, s));
+  CU(dc.make(comp, n, s));
+  CU(dout.make(nullptr, n, s));
+  CU(launch_log_joint_pairs(dm.D, dm.H, dx.p, dc.p, n, x->mu, x->psi, x->lam, x->R, x->kconst, dout.p, s));
+  CU(cudaMemcpyAsync(out, dout.p, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  return VMFA_OK;
+}
+
+int vmfa_build_search_space(vmfa_ctx* x, uint64_t seed, uint64_t iteration, const int32_t* extras, int32_t* count,
+                            int32_t* idx) {
+  TRY(check_ctx(x));
+  if (!count || !idx) return fail(VMFA_ERR_INVALID_ARGUMENT, "null output");
+  const Dims& dm = x->dm;
+  cudaStream_t s = x->stream;
+  DevTmp<int> de, dcnt, didx;
+  if (extras) CU(de.make(extras, dm.N, s));
+  CU(dcnt.make(nullptr, dm.N, s));
+  CU(didx.make(nullptr, static_cast<size_t>(dm.N) * dm.stride, s));
+  CU(launch_search_space(dm, x->K, x->g, x->gcnt, extras ? de.p : nullptr, seed, iteration, dcnt.p, didx.p, s));
+  CU(cudaMemcpyAsync(count, dcnt.p, sizeof(int) * dm.N, cudaMemcpyDeviceToHost, s));
+  CU(cudaMemcpyAsync(idx, didx.p, sizeof(int) * dm.N * dm.stride, cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  return VMFA_OK;
+}
+
+int vmfa_update_k(vmfa_ctx* x, const int32_t* count, const int32_t* idx, const double* lj, int32_t* K) {
+  TRY(check_ctx(x));
+  if (!count || !idx || !lj || !K) return fail(VMFA_ERR_INVALID_ARGUMENT, "null argument");
+  const Dims& dm = x->dm;
+  cudaStream_t s = x->stream;
+  const size_t NS = static_cast<size_t>(dm.N) * dm.stride;
+  DevTmp<int> dcnt, didx, dK, dst;
+  DevTmp<double> dl;
+  CU(dcnt.make(count, dm.N, s));
+  CU(didx.make(idx, NS, s));
+  CU(dl.make(lj, NS, s));
+  CU(dK.make(nullptr, static_cast<size_t>(dm.N) * dm.Cp, s));
+  CU(dst.make(nullptr, 1, s));
+  CU(cudaMemsetAsync(dst.p, 0, sizeof(int), s));
+  CU(launch_update_k(dm, dcnt.p, didx.p, dl.p, dK.p, dst.p, s));
+  int status = 0;
+  CU(cudaMemcpyAsync(K, dK.p, sizeof(int) * dm.N * dm.Cp, cudaMemcpyDeviceToHost, s));
+  CU(cudaMemcpyAsync(&status, dst.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  if (status) return fail(VMFA_ERR_INSUFFICIENT_CANDIDATES, "search space smaller than C'");
+  return VMFA_OK;
+}
+
+int vmfa_hard_partition(vmfa_ctx* x, const int32_t* K, const int32_t* count, const int32_t* idx, const double* lj,
+                        int32_t* labels, int32_t* part_off, int32_t* part_ent) {
+  TRY(check_ctx(x));
+  if (!K || !count || !idx || !lj || !labels) return fail(VMFA_ERR_INVALID_ARGUMENT, "null argument");
+  const Dims& dm = x->dm;
+  cudaStream_t s = x->stream;
+  const size_t NS = static_cast<size_t>(dm.N) * dm.stride;
+  DevTmp<int> dK, dcnt, didx, dlab;
+  DevTmp<double> dl;
+  CU(dK.make(K, static_cast<size_t>(dm.N) * dm.Cp, s));
+  CU(dcnt.make(count, dm.N, s));
+  CU(didx.make(idx, NS, s));
+  CU(dl.make(lj, NS, s));
+  CU(dlab.make(nullptr, dm.N, s));
+  CU(launch_hard_labels(dm, dK.p, dcnt.p, didx.p, dl.p, dlab.p, s));
+  // the partition: stable by label, so every cell lists its rows ascending
+  CU(launch_keys_from_i32(dlab.p, x->keys, dm.N, s));
+  TRY(csr_by_key(x, x->keys, dm.N, x->part_off, x->part_ent, nullptr, 1));
+  CU(cudaMemcpyAsync(labels, dlab.p, sizeof(int) * dm.N, cudaMemcpyDeviceToHost, s));
+  if (part_off) CU(cudaMemcpyAsync(part_off, x->part_off, sizeof(int) * (dm.C + 1), cudaMemcpyDeviceToHost, s));
+  if (part_ent) CU(cudaMemcpyAsync(part_ent, x->part_ent, sizeof(int) * dm.N, cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  return VMFA_OK;
+}
+
+int vmfa_accumulate_distances(vmfa_ctx* x, int mode, const int32_t* part_off, const int32_t* part_ent,
+                              const int32_t* count, const int32_t* idx, const double* lj, const double* pi,
+                              int64_t cap, int32_t* c_out, int32_t* ct_out, double* sum_out, int64_t* cnt_out,
+                              int64_t* n_rows) {
+  TRY(check_ctx(x));
+  if (!part_off || !part_ent || !count || !idx || !lj || !pi || !n_rows || (mode != 0 && mode != 1))
+    return fail(VMFA_ERR_INVALID_ARGUMENT, "bad arguments");
+  const Dims& dm = x->dm;
+  if (part_off[0] != 0 || part_off[dm.C] != dm.N) return fail(VMFA_ERR_INVALID_ARGUMENT, "partition does not cover the rows");
+  cudaStream_t s = x->stream;
+  // launch configuration: per component a hash table of 2x its entry bound
+  std::vector<int64_t> off(dm.C + 1, 0);
+  std::vector<int> tcap(dm.C);
+  for (int c = 0; c < dm.C; ++c) {
+    int64_t b = 0;
+    for (int e = part_off[c]; e < part_off[c + 1]; ++e) b += count[part_ent[e]];
+    int64_t p2 = 1;
+    while (p2 < 2 * b) p2 <<= 1;
+    tcap[c] = static_cast<int>(p2);
+    off[c + 1] = off[c] + p2;
+  }
+  const size_t NS = static_cast<size_t>(dm.N) * dm.stride, T = static_cast<size_t>(off[dm.C]);
+  DevTmp<int> dpo, dpe, dcnt, didx, dcap, dkey, dnk;
+  DevTmp<double> dl, dpi, dsum;
+  DevTmp<long long> dtc;
+  DevTmp<int64_t> doff;
+  CU(dpo.make(part_off, dm.C + 1, s));
+  CU(dpe.make(part_ent, dm.N, s));
+  CU(dcnt.make(count, dm.N, s));
+  CU(didx.make(idx, NS, s));
+  CU(dl.make(lj, NS, s));
+  CU(dpi.make(pi, dm.C, s));
+  CU(doff.make(off.data(), dm.C + 1, s));
+  CU(dcap.make(tcap.data(), dm.C, s));
+  CU(dkey.make(nullptr, T, s));
+  CU(dsum.make(nullptr, T, s));
+  CU(dtc.make(nullptr, T, s));
+  CU(dnk.make(nullptr, dm.C, s));
+  CU(launch_distances(dm, mode, dpo.p, dpe.p, dcnt.p, didx.p, dl.p, dpi.p, doff.p, dcap.p, dkey.p, dsum.p, dtc.p,
+                      dnk.p, s));
+  std::vector<int> nk(dm.C), hk(T);
+  std::vector<double> hs(T);
+  std::vector<long long> hc(T);
+  CU(cudaMemcpyAsync(nk.data(), dnk.p, sizeof(int) * dm.C, cudaMemcpyDeviceToHost, s));
+  CU(cudaMemcpyAsync(hk.data(), dkey.p, sizeof(int) * T, cudaMemcpyDeviceToHost, s));
+  CU(cudaMemcpyAsync(hs.data(), dsum.p, sizeof(double) * T, cudaMemcpyDeviceToHost, s));
+  CU(cudaMemcpyAsync(hc.data(), dtc.p, sizeof(long long) * T, cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  int64_t w = 0;  // (c, ct) ascending rows: each component's keys are at the front of its table, sorted
+  for (int c = 0; c < dm.C; ++c)
+    for (int i = 0; i < nk[c]; ++i, ++w) {
+      if (w >= cap) continue;
+      const int64_t k = off[c] + i;
+      if (c_out) c_out[w] = c;
+      if (ct_out) ct_out[w] = hk[k];
+      if (sum_out) sum_out[w] = hs[k];
+      if (cnt_out) cnt_out[w] = hc[k];
+    }
+  *n_rows = w;
+  return VMFA_OK;
+}
+
+int vmfa_update_g(vmfa_ctx* x, int64_t n_rows, const int32_t* c_in, const int32_t* ct, const double* sum,
+                  const int64_t* cnt, int32_t* g, int32_t* g_count) {
+  TRY(check_ctx(x));
+  if (n_rows < 0 || (n_rows > 0 && (!c_in || !ct || !sum || !cnt)) || !g || !g_count)
+    return fail(VMFA_ERR_INVALID_ARGUMENT, "bad arguments");
+  const Dims& dm = x->dm;
+  std::vector<int64_t> off(dm.C + 1, 0);
+  for (int64_t r = 0; r < n_rows; ++r) {
+    if (c_in[r] < 0 || c_in[r] >= dm.C || (r > 0 && c_in[r] < c_in[r - 1]))
+      return fail(VMFA_ERR_INVALID_ARGUMENT, "rows not sorted by component");
+    ++off[c_in[r] + 1];
+  }
+  for (int c = 0; c < dm.C; ++c) off[c + 1] += off[c];
+  cudaStream_t s = x->stream;
+  DevTmp<int64_t> doff;
+  DevTmp<int> dct, dg, dgc;
+  DevTmp<double> dsum;
+  DevTmp<long long> dcnt;
+  CU(doff.make(off.data(), dm.C + 1, s));
+  CU(dct.make(ct, n_rows, s));
+  CU(dsum.make(sum, n_rows, s));
+  CU(dcnt.make(reinterpret_cast<const long long*>(cnt), n_rows, s));
+  CU(dg.make(nullptr, static_cast<size_t>(dm.C) * dm.G, s));
+  CU(dgc.make(nullptr, dm.C, s));
+  CU(launch_update_g(dm.C, dm.G, doff.p, dct.p, dsum.p, dcnt.p, dg.p, dgc.p, s));
+  CU(cudaMemcpyAsync(g, dg.p, sizeof(int) * dm.C * dm.G, cudaMemcpyDeviceToHost, s));
+  CU(cudaMemcpyAsync(g_count, dgc.p, sizeof(int) * dm.C, cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  return VMFA_OK;
+}
+
+int vmfa_responsibilities(vmfa_ctx* x, int64_t rows, int width, const double* lj, double* resp) {
+  TRY(check_ctx(x));
+  if (rows < 0 || width < 1 || (rows > 0 && (!lj || !resp))) return fail(VMFA_ERR_INVALID_ARGUMENT, "bad arguments");
+  if (rows == 0) return VMFA_OK;
+  cudaStream_t s = x->stream;
+  const size_t n = static_cast<size_t>(rows) * width;
+  DevTmp<double> dl, dr;
+  CU(dl.make(lj, n, s));
+  CU(dr.make(nullptr, n, s));
+  CU(launch_responsibilities(rows, width, dl.p, dr.p, s));
+  CU(cudaMemcpyAsync(resp, dr.p, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  return VMFA_OK;
+}
+
+}  // extern "C"
+namespace {
+// caller-supplied K rows into the context (validated on the device)
+int set_K(vmfa_ctx* x, const int32_t* K) {
+  const Dims& dm = x->dm;
+  cudaStream_t s = x->stream;
+  CU(cudaMemcpyAsync(x->K, K, sizeof(int) * dm.N * dm.Cp, cudaMemcpyHostToDevice, s));
+  const long long none = 0x7fffffffffffffffLL;
+  long long* bad = reinterpret_cast<long long*>(x->u64tmp);
+  CU(cudaMemcpyAsync(bad, &none, sizeof none, cudaMemcpyHostToDevice, s));
+  CU(launch_validate_K(x->K, dm.N, dm.Cp, dm.C, bad, s));
+  long long first = none;
+  CU(cudaMemcpyAsync(&first, bad, sizeof first, cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  x->kinv_for_current_K = false;
+  x->prescored = false;
+  if (first != none) return fail(VMFA_ERR_INVALID_ARGUMENT, "K row not sorted distinct in-range indices (n=%lld)", first);
+  return VMFA_OK;
+}
+}  // namespace
+extern "C" {
+
+int vmfa_accumulate_suffstats_k(vmfa_ctx* x, const int32_t* K, const double* resp) {
+  TRY(check_ctx(x));
+  if (!K || !resp) return fail(VMFA_ERR_INVALID_ARGUMENT, "null argument");
+  TRY(set_K(x, K));
+  CU(cudaMemcpyAsync(x->resp, resp, sizeof(double) * x->dm.N * x->dm.Cp, cudaMemcpyHostToDevice, x->stream));
+  x->have_estep = true;
+  TRY(stats_local(x));
+  CU(cudaStreamSynchronize(x->stream));
+  return VMFA_OK;
+}
+
+int vmfa_truncated_free_energy_k(vmfa_ctx* x, const int32_t* K, double* F) {
+  TRY(check_ctx(x));
+  if (!K) return fail(VMFA_ERR_EMPTY_KSET, "empty K collection");  // model.cpp:150-159 EmptyKSet
+  TRY(set_K(x, K));
+  TRY(free_energy_local(x, false));
+  double sc[4];
+  TRY(read_scalars(x, sc));
+  if (F) *F = sc[2];
+  return VMFA_OK;
+}
+
 // ---------------------------------------------------------------- work accounting
 int vmfa_scoring_work(vmfa_ctx* x, int64_t* out, int n) {
   TRY(check_ctx(x));

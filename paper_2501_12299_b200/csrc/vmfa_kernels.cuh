@@ -303,6 +303,22 @@ cudaError_t launch_fix_scan_anchor(const Dims& dm, const FixArgs& f, const int* 
                                    const int* kinv_off, const int* kinv_ent, float* LJ, cudaStream_t s);
 cudaError_t launch_fix_scan_single(const Dims& dm, const FixArgs& f, const int* off, const int* ent, int extra_stride,
                                    int extra_col, float* out, cudaStream_t s);
+// per-operation E-step pieces and log_joint (vmfa_ops.cu)
+cudaError_t launch_log_joint_pairs(int D, int H, const float* X, const int* comp, int64_t n, const double* mu,
+                                   const double* psi, const double* lam, const double* R, const double* kconst,
+                                   double* out, cudaStream_t s);
+cudaError_t launch_search_space(const Dims& dm, const int* K, const int* g, const int* gcnt, const int* extras,
+                                uint64_t seed, uint64_t it, int* count, int* idx, cudaStream_t s);
+cudaError_t launch_update_k(const Dims& dm, const int* count, const int* idx, const double* lj, int* Kout,
+                            int* status, cudaStream_t s);
+cudaError_t launch_hard_labels(const Dims& dm, const int* K, const int* count, const int* idx, const double* lj,
+                               int* labels, cudaStream_t s);
+cudaError_t launch_responsibilities(int64_t rows, int width, const double* lj, double* resp, cudaStream_t s);
+cudaError_t launch_distances(const Dims& dm, int mode, const int* part_off, const int* part_ent, const int* count,
+                             const int* idx, const double* lj, const double* pi, const int64_t* tab_off,
+                             const int* tab_cap, int* key, double* sum, long long* cnt, int* nkeys, cudaStream_t s);
+cudaError_t launch_update_g(int C, int G, const int64_t* row_off, const int* ct, const double* sum,
+                            const long long* cnt, int* g, int* gcnt, cudaStream_t s);
 // true while vmfa_diag_scorer_cycles has the scorer counters armed
 bool ws_diag_armed();
 cudaError_t launch_score_ws(int mode, const ScoreArgs& s, const WsOperands& op, int4* jobs, cudaStream_t st,

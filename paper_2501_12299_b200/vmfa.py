@@ -240,6 +240,80 @@ class Session:
         check(lib().vmfa_truncated_free_energy(self._h, C.byref(F)))
         return F.value
 
+    # -- the reference's entry points with caller-supplied state / per-op pieces
+    def accumulate_suffstats_k(self, K: np.ndarray, resp: np.ndarray) -> Stats:
+        """accumulate_suffstats(params, caches, data, ksets, resp) (mstep.hpp:27-31)
+        with the caller's K rows and responsibilities (the context's K becomes K)."""
+        check(lib().vmfa_accumulate_suffstats_k(self._h, ptr(_c(K, np.int32)), ptr(_c(resp, np.float64))))
+        return self.download_suffstats()
+
+    def truncated_free_energy_k(self, K: np.ndarray) -> float:
+        """truncated_free_energy(params, caches, data, ksets) (model.hpp:116-119)."""
+        F = C.c_double()
+        check(lib().vmfa_truncated_free_energy_k(self._h, ptr(_c(K, np.int32)), C.byref(F)))
+        return F.value
+
+    def log_joint(self, X: np.ndarray, comp: np.ndarray) -> np.ndarray:
+        """log_joint (model.hpp:83-86) for rows X[i] and components comp[i], fp64."""
+        X = _c(X, np.float32).reshape(-1, self.D)
+        comp = _c(comp, np.int32)
+        out = np.zeros(X.shape[0])
+        check(lib().vmfa_log_joint(self._h, ptr(X), X.shape[0], ptr(comp), ptr(out)))
+        return out
+
+    def build_search_space(self, seed: int = 0, iteration: int = 0, extras: np.ndarray | None = None):
+        """build_search_space (estep.hpp:82-84) for every row: (count, idx)."""
+        cnt = np.zeros(self.N, np.int32)
+        idx = np.zeros((self.N, self.stride), np.int32)
+        check(lib().vmfa_build_search_space(self._h, seed, iteration,
+                                            None if extras is None else ptr(_c(extras, np.int32)), ptr(cnt),
+                                            ptr(idx)))
+        return cnt, idx
+
+    def update_k(self, count, idx, lj) -> np.ndarray:
+        """update_k (estep.hpp:88-90) for every row."""
+        K = np.zeros((self.N, self.Cp), np.int32)
+        check(lib().vmfa_update_k(self._h, ptr(_c(count, np.int32)), ptr(_c(idx, np.int32)), ptr(_c(lj, np.float64)),
+                                  ptr(K)))
+        return K
+
+    def hard_partition(self, K, count, idx, lj):
+        """hard_partition (estep.hpp:94-97): (labels, partition offsets, rows)."""
+        lab = np.zeros(self.N, np.int32)
+        off = np.zeros(self.C + 1, np.int32)
+        ent = np.zeros(self.N, np.int32)
+        check(lib().vmfa_hard_partition(self._h, ptr(_c(K, np.int32)), ptr(_c(count, np.int32)),
+                                        ptr(_c(idx, np.int32)), ptr(_c(lj, np.float64)), ptr(lab), ptr(off),
+                                        ptr(ent)))
+        return lab, off, ent
+
+    def accumulate_distances(self, mode, part_off, part_ent, count, idx, lj, pi):
+        """accumulate_distances (estep.hpp:103-106): (c, ct, sum, count) rows."""
+        args = [ptr(_c(part_off, np.int32)), ptr(_c(part_ent, np.int32)), ptr(_c(count, np.int32)),
+                ptr(_c(idx, np.int32)), ptr(_c(lj, np.float64)), ptr(_c(pi, np.float64))]
+        n = C.c_int64()
+        check(lib().vmfa_accumulate_distances(self._h, mode, *args, 0, None, None, None, None, C.byref(n)))
+        m = n.value
+        c, ct, sm, cn = np.zeros(m, np.int32), np.zeros(m, np.int32), np.zeros(m), np.zeros(m, np.int64)
+        check(lib().vmfa_accumulate_distances(self._h, mode, *args, m, ptr(c), ptr(ct), ptr(sm), ptr(cn),
+                                              C.byref(n)))
+        return c, ct, sm, cn
+
+    def update_g(self, c, ct, sm, cn):
+        """update_g (estep.hpp:111-112) for every component: (g, g_count)."""
+        g = np.zeros((self.C, self.G), np.int32)
+        gc = np.zeros(self.C, np.int32)
+        check(lib().vmfa_update_g(self._h, len(c), ptr(_c(c, np.int32)), ptr(_c(ct, np.int32)),
+                                  ptr(_c(sm, np.float64)), ptr(_c(cn, np.int64)), ptr(g), ptr(gc)))
+        return g, gc
+
+    def responsibilities(self, lj: np.ndarray) -> np.ndarray:
+        """responsibilities_row (estep.hpp:116-117) for every row of lj."""
+        lj = _c(lj, np.float64)
+        out = np.zeros_like(lj)
+        check(lib().vmfa_responsibilities(self._h, lj.shape[0], lj.shape[1], ptr(lj), ptr(out)))
+        return out
+
     def exact_log_likelihood(self) -> float:
         """exact_log_likelihood (model.cpp:139-148) over this session's rows:
         sum_n log sum_c p(x_n, c) over all C components (dense tcgen05 pass)."""

@@ -231,3 +231,17 @@ def test_report_jsonl_and_convergence_rule():
     lines = [json.loads(l) for l in buf.getvalue().splitlines()]
     assert len(lines) == 3 and lines[0]["nll_train"] is None and lines[1]["nll_train"] == 2.5
     assert lines[2]["summary"] and lines[2]["converged"] and "iterations" not in lines[2]
+
+
+def build_fit_fa(tmp_path):
+    import subprocess
+    exe = tmp_path / "fit_fa"
+    lib_dir = os.path.join(ROOT, "paper_2501_12299_b200", "_lib")
+    subprocess.run(["g++", "-std=c++17", "-O2", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "cpp", "fit_fa.cpp"), "-L", lib_dir,
+                    "-lvmfa_b200", f"-Wl,-rpath,{lib_dir}", "-o", str(exe)], check=True)
+    return exe
+
+
+def test_fit_fa_program_compiles(vmfa, tmp_path):
+    assert build_fit_fa(tmp_path).exists()
