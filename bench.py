@@ -52,7 +52,7 @@ def parse():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="multi-rank collectives (gloo: host-staged, for tests on one GPU)")
-    ap.add_argument("--n", type=int, default=0, help="override the config's total rows (testing only)")
+    ap.add_argument("--rows", type=int, default=0, help="override the config's total rows (testing only)")
     ap.add_argument("--ref-rows", type=int, default=REF_ROWS)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -248,7 +248,7 @@ def build_problem(V, args, rank, world, comm):
     """This rank's rows of the config and the sharded initialisation."""
     from paper_2501_12299_b200.sharded import initialize_sharded
     m = V.CONFIGS[args.config]["model"]
-    n_total = args.n or V.CONFIGS[args.config]["truth"]["N"]
+    n_total = args.rows or V.CONFIGS[args.config]["truth"]["N"]
     a, b = rank * n_total // world, (rank + 1) * n_total // world
     X = V.gen_synthetic(V.synth_spec(args.config, N=n_total), a, b)
     p, st, floor, _ = initialize_sharded(X, a, n_total, m["C"], m["H"], m["Cprime"], m["G"], seed=0, scale=0.1,
@@ -284,24 +284,25 @@ def main():
         run_reference(args, rank)
         return
     import torch
-    torch.cuda.set_device(local)
+    dev = local % max(torch.cuda.device_count(), 1)  # (ranks share the GPU when there are fewer: tests)
+    torch.cuda.set_device(dev)
     dist = None
     if world > 1:
         import torch.distributed as dist
         if args.backend == "nccl":
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
         else:
             dist.init_process_group("gloo")
 
     from paper_2501_12299_b200 import vmfa as V
     from paper_2501_12299_b200.exchange import XCHG_SCALARS, XCHG_STATS, allreduce_buffer, cooc_exchange
     from paper_2501_12299_b200.sharded import Comm
-    comm = Comm(device=f"cuda:{local}" if args.backend == "nccl" else "cpu")
+    comm = Comm(device=f"cuda:{dev}" if args.backend == "nccl" else "cpu")
     t_setup = time.perf_counter()
     m, X, p, st, floor, a, b, n_total = build_problem(V, args, rank, world, comm)
     D = X.shape[1]
     C, H, Cp, G = m["C"], m["H"], m["Cprime"], m["G"]
-    sess = V.Session(C, D, H, Cp, G, X, n_offset=a, n_total=n_total, device=local)
+    sess = V.Session(C, D, H, Cp, G, X, n_offset=a, n_total=n_total, device=dev)
     sess.set_floor(floor)
     sess.upload_params(p)
     sess.upload_state(st)
@@ -349,12 +350,12 @@ def main():
 
     sess.scoring_work()  # clears the fp64 re-scoring counter
     # L2 flush buffer (> 126 MB L2), written between timed iterations
-    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{local}")
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{dev}")
     times, joints, Fs = [], [], []
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
+    with ClockSampler(dev) as clk:
         for _ in range(args.steps):
             with torch.cuda.stream(ext):
                 flush.fill_(1.0)
@@ -373,12 +374,17 @@ def main():
     ms_step = float(np.sum(times) / args.steps)
     J_job = float(np.sum(joints) / args.steps)  # multi-rank: the scalars are all-reduced, J is the job total
     if dist:
-        t = torch.tensor([ms_step], device=f"cuda:{local}")
+        t = torch.tensor([ms_step], device=f"cuda:{dev}")
         if args.backend == "gloo":
             t = t.cpu()
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_step = float(t.item())
     value = J_job / (ms_step * 1e-3)
+    if args.dump_state:
+        stf = sess.download_state()
+        pf = sess.download_params()
+        np.savez(f"{args.dump_state}.rank{rank}.npz", K=stf.K, g=stf.g, gc=stf.g_count, pi=pf.pi, mu=pf.mu,
+                 F=np.array(Fs), J=np.array(joints), a=a, b=b)
 
     # phase split: the same steps again with per-phase events (outside the timed region)
     sess.profile(True)
@@ -391,11 +397,6 @@ def main():
     sess.profile(False)
     phase_ms = {k: v["ms"] / args.steps for k, v in kt.items()}
 
-    if args.dump_state:
-        stf = sess.download_state()
-        pf = sess.download_params()
-        np.savez(f"{args.dump_state}.rank{rank}.npz", K=stf.K, g=stf.g, gc=stf.g_count, pi=pf.pi, mu=pf.mu,
-                 F=np.array(Fs), J=np.array(joints), a=a, b=b)
 
     # dominant kernel: the candidate scoring (anchor + extra launches) of each E-step
     Fj, Bj = alg_per_joint(D, H)

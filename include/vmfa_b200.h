@@ -266,7 +266,8 @@ int vmfa_phase_free_energy_local(vmfa_ctx* ctx);
 int vmfa_phase_scalars(vmfa_ctx* ctx, double* free_energy_estep, uint64_t* joints,
                        double* free_energy);
 /* Sparse co-occurrence exchange (SURVEY §8(e) sparse variant; used when C is
- * too large for the dense table, C > ~18900, or with VMFA_COOC=sparse at
+ * too large for the dense table: C > 4096 in a sharded context (C > ~18900
+ * in a single one), or with VMFA_COOC=sparse at
  * context creation). In place of allreduce(COOC):
  *   vmfa_phase_estep_local   (each rank reduces its (c, c~) list by key)
  *   vmfa_cooc_local_list     (device arrays key u32 = c << b | c~, cnt/hi/lo

@@ -1024,7 +1024,13 @@ int vmfa_ctx_create(vmfa_ctx** out, int device, int C, int D, int H, int Cp, int
   };
   const char* cooc_env = std::getenv("VMFA_COOC");
   const bool force_sparse = cooc_env && std::string(cooc_env) == "sparse";
-  const bool dense_rows = !force_sparse && 3.0 * Cs * Cs * sizeof(long long) <= 8.0 * (1ull << 30);
+  // dense C x C co-occurrence rows (24 C^2 B): one context up to C ~ 18 900;
+  // a shard of a multi-rank run only up to C = 4096 (the rows are the
+  // all-reduce payload: 0.4 GB at C = 4096), beyond that the owner-routed
+  // sparse lists
+  const bool sharded = n_total > n_local;
+  const bool dense_rows = !force_sparse && 3.0 * Cs * Cs * sizeof(long long) <= 8.0 * (1ull << 30) &&
+                          (!sharded || C <= 4096);
   A(x->X, N * D);
   A(x->floor, D);
   for (double** p : {&x->pi, &x->pi2}) A(*p, Cs);
