@@ -98,6 +98,9 @@ struct vmfa_ctx {
   uint16_t *bimg = nullptr, *simg = nullptr;  // scorer B stage images (fp16; anchor / single)
   float *bscl = nullptr, *sscl = nullptr;     // their row scales
   float *xmax = nullptr, *mumax = nullptr;    // A-row scale bounds
+  unsigned char* svimg = nullptr;             // the tcgen05 statistics kernel's V images (per precompute)
+  int* svexp = nullptr;
+  float* svl1 = nullptr;
   unsigned long long* nfix = nullptr;         // scores re-evaluated in fp64 (vmfa_fixup.cu), accumulated
   long long* fix_list = nullptr;              // flagged scores of one scoring launch
   unsigned long long* fix_cnt = nullptr;      // [count, overflow]
@@ -412,6 +415,7 @@ int run_precompute(vmfa_ctx* x, int* failed, bool sync = true) {
     CU(launch_ws_records(x->dm, 1, x->WT, x->mu32, x->ipsi32, x->kconst, x->g, x->gcnt, x->sscl, x->srec, s));
     CU(launch_rowmax(x->dm.C, x->dm.D, x->mu32, x->mumax, s));
   }
+  if (x->svimg) CU(launch_stats_vimg(x->dm, x->V32, x->svimg, x->svexp, x->svl1, s));
   x->end(tok);
   if (!sync) return VMFA_OK;  // the caller checks st_model later
   unsigned long long st = 0;
@@ -733,6 +737,11 @@ int stats_local(vmfa_ctx* x) {
   a.Y = x->Y;
   a.sq = x->sq;
   a.qctr = x->qctr;
+  a.xmax = x->xmax;  // (the tcgen05 kernel's row scales; null without the warp-specialised scorer)
+  a.mumax = x->mumax;
+  a.vimg = x->svimg;
+  a.vexp = x->svexp;
+  a.vl1 = x->svl1;
   const int tok = x->begin(kFamStats, x->dm.N * x->dm.Cp);
   CU(launch_items_scan(x->kinv_off, x->dm.C, x->stats_rows, 0, x->stats_items, x->stream));
   CU(launch_stats(a, x->stats_items, x->stats_rows, x->stats_part, x->stream));
@@ -1113,6 +1122,12 @@ int vmfa_ctx_create(vmfa_ctx** out, int device, int C, int D, int H, int Cp, int
     x->stats_rows = static_cast<int>(std::min<int64_t>(1024, std::max<int64_t>(256, (target + 31) / 32 * 32)));
     if (const char* v = std::getenv("VMFA_STATS_ROWS"))  // experiments: K-pairs per statistics item
       x->stats_rows = static_cast<int>(std::min<int64_t>(1024, std::max<int64_t>(32, std::atoll(v) / 32 * 32)));
+    if (x->scorer == 2 && stats_use_tc(dm)) {  // the tcgen05 statistics kernel
+      x->stats_rows = stats_tc_rows();
+      A(x->svimg, static_cast<size_t>(stats_tc_image_bytes(dm)));
+      A(x->svexp, Cs * 16);
+      A(x->svl1, Cs * 16);
+    }
     const int64_t max_items = C + (pairs + x->stats_rows - 1) / x->stats_rows;
     A(x->stats_part, static_cast<size_t>(max_items) * stats_part_stride(dm));
     const int64_t bal = std::max<int64_t>(128, static_cast<int64_t>(N) / (4 * sm_count()));

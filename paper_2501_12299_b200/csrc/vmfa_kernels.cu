@@ -3000,6 +3000,14 @@ bool stats_mma_ok(const Dims& dm) {
 // BIG variant: 16-row batches, one CTA per SM (D > 256: the 2-CTA variant
 // would spill its 8 dimension tiles per warp; or H + 1 = 17)
 static bool stats_mma_big(const Dims& dm) { return dm.D > 256 || dm.H + 1 > 16; }
+// the tcgen05 statistics kernel (vmfa_stats_tc.cu) is opt-in (VMFA_STATS=tc):
+// parity-tested, but measured 2-3x slower than k_stats_mma on configs 1-3
+// (GEMM ii reduces over rows, so every row chunk is produced twice and the
+// synchronous cooperative fills stay latency-bound)
+bool stats_use_tc(const Dims& dm) {
+  const char* v = std::getenv("VMFA_STATS");
+  return v && std::strcmp(v, "tc") == 0 && stats_tc_ok(dm);
+}
 cudaError_t launch_stats(const StatsArgs& a, const int* itemoff, int rows_per_item, double* part,
                          cudaStream_t s) {
   if (a.dm.D > 4 * kStatsThreads) return cudaErrorInvalidValue;
@@ -3007,6 +3015,19 @@ cudaError_t launch_stats(const StatsArgs& a, const int* itemoff, int rows_per_it
   const int H1 = a.dm.H + 1;
   const int nh1 = H1 <= 5 ? 5 : (H1 <= 9 ? 9 : kStatsMaxH1);
   const int64_t ps = stats_part_stride(a.dm);
+  if (a.xmax && a.mumax && rows_per_item == stats_tc_rows() && stats_use_tc(a.dm)) {
+    if (a.qctr) {
+      cudaError_t e = cudaMemsetAsync(a.qctr, 0, sizeof(int), s);
+      if (e != cudaSuccess) return e;
+    }
+    cudaError_t e = launch_stats_tc(a, a.xmax, a.mumax, itemoff, nh1, part, ps, s);
+    if (e != cudaSuccess) return e;
+    k_stats_reduce<<<sm_count() * 8, 256, 0, s>>>(a.dm, itemoff, part, ps, 0, 0, nh1, 1, a.Nc, a.E, a.Y, a.sq);
+    k_stats_uncenter<<<grid_for((int64_t)a.dm.C * a.dm.D, 256, 8192), 256, 0, s>>>(a.dm, a.mu32, a.Nc, a.E, a.Y,
+                                                                                  a.sq);
+    k_stats_sz<<<grid_for((int64_t)a.dm.C * a.dm.H * a.dm.H, 256, 4096), 256, 0, s>>>(a.dm, a.Nc, a.Sz, a.E);
+    return cudaGetLastError();
+  }
   if (stats_mma_ok(a.dm)) {
     if (a.qctr) {
       cudaError_t e = cudaMemsetAsync(a.qctr, 0, sizeof(int), s);

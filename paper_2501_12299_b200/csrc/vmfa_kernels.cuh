@@ -165,7 +165,14 @@ struct StatsArgs {
   double* Y;              // C x (H+1) x D  (D x (H+1) col-major)
   double* sq;             // C x D
   int* qctr;              // work-queue counter (zeroed per pass; nullptr: static item order)
+  const float* xmax = nullptr;   // per-row max |x| and per-component max |mu32| (the tcgen05
+  const float* mumax = nullptr;  // kernel's row scales; nullptr: the mma.sync / FFMA kernels)
+  const void* vimg = nullptr;    // its GEMM i B images (launch_stats_vimg, per precompute)
+  const int* vexp = nullptr;
+  const float* vl1 = nullptr;
 };
+// the tcgen05 statistics kernel takes the pass (opt-in: VMFA_STATS=tc)
+bool stats_use_tc(const Dims& dm);
 
 struct UpdateArgs {
   Dims dm;
@@ -303,6 +310,14 @@ cudaError_t launch_fix_scan_anchor(const Dims& dm, const FixArgs& f, const int* 
                                    const int* kinv_off, const int* kinv_ent, float* LJ, cudaStream_t s);
 cudaError_t launch_fix_scan_single(const Dims& dm, const FixArgs& f, const int* off, const int* ent, int extra_stride,
                                    int extra_col, float* out, cudaStream_t s);
+// the statistics on tcgen05 (vmfa_stats_tc.cu): H <= 16, D % 4 == 0, D <= 832;
+// items of stats_tc_rows() K-pairs
+bool stats_tc_ok(const Dims& dm);
+int stats_tc_rows();
+int64_t stats_tc_image_bytes(const Dims& dm);
+cudaError_t launch_stats_vimg(const Dims& dm, const float* V32, void* img, int* vexp, float* vl1, cudaStream_t s);
+cudaError_t launch_stats_tc(const StatsArgs& a, const float* xmax, const float* mumax, const int* itemoff, int nh1,
+                            double* part, int64_t part_stride, cudaStream_t s);
 // per-operation E-step pieces and log_joint (vmfa_ops.cu)
 cudaError_t launch_log_joint_pairs(int D, int H, const float* X, const int* comp, int64_t n, const double* mu,
                                    const double* psi, const double* lam, const double* R, const double* kconst,
