@@ -310,8 +310,9 @@ int vmfa_diag_scorer_cycles(int enable, unsigned long long* out, int n);
  * one-component B stage images, out[4] bytes of the epilogue records,
  * out[5] the scorer (2 warp-specialised tcgen05, 1 single-role tcgen05, 0
  * FFMA), out[6] scores re-evaluated in fp64 since the last call (the
- * scorer flags scores whose terms cancel, vmfa_fixup.cu). n: entries wanted
- * (<= 7).                                                                    */
+ * scorer flags scores whose terms cancel, vmfa_fixup.cu), out[7] flagged
+ * scores re-scored by the one-component tensor pass since the last call
+ * (out[6] is what that pass still flagged). n: entries wanted (<= 8).       */
 int vmfa_scoring_work(vmfa_ctx* ctx, int64_t* out, int n);
 
 /* Stream of the context (a cudaStream_t) for callers that order their own

@@ -109,6 +109,8 @@ struct vmfa_ctx {
   int* fix_sorted = nullptr;
   unsigned long long* fix_ovf = nullptr;
   bool fix_ok = false;  // re-scoring pipeline on (warp-specialised scorer, N SL < 2^31)
+  bool fix_tc = false;  // VMFA_FIX_TC=1: flagged scores pass the one-component tensor re-scoring before fp64
+  double* W64 = nullptr;  // C x H x D fp64 W^T for the DMMA re-scoring (null: per-item staging)
   int scorer = 2;           // 2: warp-specialised tcgen05 (default), 1: single-role tcgen05, 0: FFMA
   bool use_tc = true;
   int score_rows = kScoreRowsTc;
@@ -337,7 +339,7 @@ cudaError_t run_score(vmfa_ctx* x, int mode, const ScoreArgs& a) {
 FixArgs fix_args(vmfa_ctx* x) {
   return FixArgs{x->X,       x->mu,      x->psi,         x->lam,  x->R,       x->kconst, x->fix_list, x->fix_cnt,
                  x->fix_cap, x->nfix,    x->fix_qkey,    x->fix_sorted, x->fix_qcnt, x->fix_qoff, x->fix_qfill,
-                 x->fix_iof, x->fix_ovf};
+                 x->fix_iof, x->fix_ovf, x->W64};
 }
 
 ScoreArgs score_args(vmfa_ctx* x) {
@@ -365,15 +367,17 @@ int rescore(vmfa_ctx* x, int mode, float* out) {
   const int tf = x->begin(kFamFixup, 0);
   const FixArgs f = fix_args(x);
   CU(launch_fix_ovf(f, 1, s));
-  CU(launch_fix_group(dm, f, mode, x->K, x->g, x->rx, s));
-  ScoreArgs a = score_args(x);
-  a.off = x->fix_qoff;
-  a.ent = x->fix_sorted;
-  a.itemoff = x->fix_iof;
-  a.out = out;
-  a.list_div = mode == kModeTruncF ? dm.Cp : dm.SL;
-  CU(run_score(x, kModeList, a));
-  CU(launch_fix_ovf(f, 0, s));
+  if (x->fix_tc) {
+    CU(launch_fix_group(dm, f, mode, x->K, x->g, x->rx, s));
+    ScoreArgs a = score_args(x);
+    a.off = x->fix_qoff;
+    a.ent = x->fix_sorted;
+    a.itemoff = x->fix_iof;
+    a.out = out;
+    a.list_div = mode == kModeTruncF ? dm.Cp : dm.SL;
+    CU(run_score(x, kModeList, a));
+    CU(launch_fix_ovf(f, 0, s));
+  }
   CU(launch_fix_f64(dm, f, mode, x->K, x->g, x->rx, out, s));
   if (mode == kModeAnchor)
     CU(launch_fix_scan_anchor(dm, f, x->g, x->gcnt, x->kinv_off, x->kinv_ent, out, s));
@@ -408,6 +412,7 @@ int run_precompute(vmfa_ctx* x, int* failed, bool sync = true) {
   a.ipsi32 = x->ipsi32;
   a.Hp = x->Hp;
   a.status = x->st_model;
+  a.W64 = x->W64;
   const int tok = x->begin(kFamPrecompute, x->dm.C);
   CU(launch_precompute(a, s));
   if (x->scorer == 2) {
@@ -1069,10 +1074,13 @@ int vmfa_ctx_create(vmfa_ctx** out, int device, int C, int D, int H, int Cp, int
     A(x->mumax, Cs);
   }
   A(x->ipsi32, Cs * D);
-  A(x->nfix, 1);
+  A(x->nfix, 2);
   A(x->fix_cnt, 2);
   A(x->fix_ovf, 2);
   x->fix_ok = x->scorer == 2 && static_cast<int64_t>(N) * dm.SL < (int64_t{1} << 31);
+  if (const char* v = std::getenv("VMFA_FIX_TC")) x->fix_tc = v[0] != '0';
+  if (x->fix_ok && fix_dmma_ok(D, dm.H) && static_cast<int64_t>(Cs) * dm.H * D * 8 <= (int64_t{4} << 30))
+    A(x->W64, static_cast<size_t>(Cs) * dm.H * D);
   A(x->fix_list, static_cast<size_t>(x->fix_cap));
   A(x->fix_sorted, static_cast<size_t>(x->fix_cap));
   A(x->fix_qkey, static_cast<size_t>(x->fix_cap));
@@ -1080,7 +1088,7 @@ int vmfa_ctx_create(vmfa_ctx** out, int device, int C, int D, int H, int Cp, int
   A(x->fix_qoff, Cs + 1);
   A(x->fix_qfill, Cs);
   A(x->fix_iof, Cs + 1);
-  if (r == VMFA_OK) cudaMemsetAsync(x->nfix, 0, sizeof(unsigned long long), x->stream);
+  if (r == VMFA_OK) cudaMemsetAsync(x->nfix, 0, 2 * sizeof(unsigned long long), x->stream);
   A(x->K, N * Cp);
   // g and its counts contiguous ([C*G | C] int32), so the sparse exchange can
   // all-reduce a rank's selected rows as one buffer (VMFA_XCHG_G)
@@ -2212,17 +2220,17 @@ int vmfa_scoring_work(vmfa_ctx* x, int64_t* out, int n) {
     CU(cudaMemcpyAsync(&ex, x->ex_off + dm.C, sizeof(int), cudaMemcpyDeviceToHost, x->stream));
     CU(cudaStreamSynchronize(x->stream));
   }
-  unsigned long long nfl = 0;  // read and cleared
-  CU(cudaMemcpyAsync(&nfl, x->nfix, sizeof nfl, cudaMemcpyDeviceToHost, x->stream));
-  CU(cudaMemsetAsync(x->nfix, 0, sizeof(unsigned long long), x->stream));
+  unsigned long long nfl[2] = {0, 0};  // read and cleared
+  CU(cudaMemcpyAsync(nfl, x->nfix, sizeof nfl, cudaMemcpyDeviceToHost, x->stream));
+  CU(cudaMemsetAsync(x->nfix, 0, sizeof nfl, x->stream));
   CU(cudaStreamSynchronize(x->stream));
-  const int64_t w[7] = {static_cast<int64_t>(dm.N) * dm.Cp,
+  const int64_t w[8] = {static_cast<int64_t>(dm.N) * dm.Cp,
                         ex,
                         x->scorer == 2 ? ws_image_halves(dm, 0) * 2 : 0,
                         x->scorer == 2 ? ws_image_halves(dm, 1) * 2 : 0,
                         x->scorer == 2 ? (ws_record_floats(dm, 0) + ws_record_floats(dm, 1)) * 4 : 0,
-                        x->scorer, static_cast<int64_t>(nfl)};
-  for (int i = 0; i < n && i < 7; ++i) out[i] = w[i];
+                        x->scorer, static_cast<int64_t>(nfl[0]), static_cast<int64_t>(nfl[1])};
+  for (int i = 0; i < n && i < 8; ++i) out[i] = w[i];
   return VMFA_OK;
 }
 

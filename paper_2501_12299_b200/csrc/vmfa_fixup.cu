@@ -312,6 +312,138 @@ __global__ void __launch_bounds__(kFixThreads) k_fix_grouped(FixParams p, Dims d
   }
 }
 
+// ---------------------------------------------------------------- DMMA path
+// The same fp64 re-evaluation as a grouped contraction on the fp64 tensor
+// cores: per work item (<= kFixChunk listed rows of one component q) the block
+// stages W_q^T (H x D, fp64, from the precompute), mu_q and 1/psi_q; each warp
+// takes 16 rows (two m8 tiles) and runs Y = V W_q with
+// mma.m8n8k4.f64 over k-steps of 4 dimensions, V = f64(x) - mu_q formed in
+// registers from float4 row loads. Dimension k-step j of chunk k0 holds
+// dimensions k0 + 4 t + j on lane (g, t), so every lane's A and B elements
+// are 4 consecutive dimensions (one float4 of x, two double2 of W / mu / ip).
+// m = sum v^2 / psi rides along on the FP64 pipe; Q = m - |y|^2.
+__device__ __forceinline__ void dmma_f64(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+size_t fix_dmma_smem(int D, int H) { return (static_cast<size_t>(H) * (D + 2) + 2 * static_cast<size_t>(D)) * sizeof(double); }
+
+template <int NT>
+__global__ void __launch_bounds__(kFixThreads) k_fix_dmma(FixParams p, const double* __restrict__ W64, Dims dm, int mode,
+                                                          const int* qoff, const int* iof, const int* sorted,
+                                                          unsigned long long* nfix, float* out) {
+  extern __shared__ __align__(16) double s_fx[];
+  const int D = p.D, Dp = D + 2;  // padded rows: the 8 g-lanes of a quarter-warp hit distinct banks
+  double* s_W = s_fx;             // (NT 8) x Dp
+  double* s_mu = s_W + NT * 8 * Dp;
+  double* s_ip = s_mu + D;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(nfix, static_cast<unsigned long long>(qoff[dm.C]));
+  const int items = iof[dm.C];
+  for (int it = blockIdx.x; it < items; it += gridDim.x) {
+    int lo = 0, hi = dm.C;  // the component q with iof[q] <= it < iof[q + 1]
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (iof[mid] <= it) lo = mid;
+      else hi = mid;
+    }
+    const int q = lo;
+    const int e0 = qoff[q] + (it - iof[q]) * kFixChunk, e1 = min(qoff[q + 1], e0 + kFixChunk);
+    __syncthreads();  // the previous item's readers are done
+    const double* wq = W64 + (int64_t)q * NT * 8 * D;
+    for (int i = threadIdx.x; i < NT * 8 * (D >> 1); i += blockDim.x) {
+      const int h = (2 * i) / D, d = 2 * i - h * D;
+      *reinterpret_cast<double2*>(s_W + h * Dp + d) = __ldg(reinterpret_cast<const double2*>(wq + (int64_t)h * D + d));
+    }
+    for (int d = threadIdx.x; d < D; d += blockDim.x) {
+      s_mu[d] = p.mu[(int64_t)q * D + d];
+      s_ip[d] = 1.0 / p.psi[(int64_t)q * D + d];
+    }
+    __syncthreads();
+    const int r0 = e0 + warp * 16;
+    if (r0 >= e1) continue;
+    int64_t o[2];
+    bool ok[2];
+    const float* xr[2];
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) {
+      const int r = r0 + mt * 8 + g;
+      ok[mt] = r < e1;
+      o[mt] = ok[mt] ? sorted[r] : 0;
+      const int64_t n = mode == 2 ? o[mt] / dm.Cp : o[mt] / dm.SL;
+      xr[mt] = p.X + n * D + 4 * t;
+    }
+    double acc[2][NT][2], m[2] = {0.0, 0.0};
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+    const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 xa[2];
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) xa[mt] = ok[mt] ? __ldg(reinterpret_cast<const float4*>(xr[mt])) : z4;
+    for (int k0 = 0; k0 < D; k0 += 16) {
+      float4 xn[2] = {z4, z4};
+      if (k0 + 16 < D) {
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+          if (ok[mt]) xn[mt] = __ldg(reinterpret_cast<const float4*>(xr[mt] + k0 + 16));
+      }
+      const int kb = k0 + 4 * t;
+      const double2 mu01 = *reinterpret_cast<const double2*>(s_mu + kb), mu23 = *reinterpret_cast<const double2*>(s_mu + kb + 2);
+      const double2 ip01 = *reinterpret_cast<const double2*>(s_ip + kb), ip23 = *reinterpret_cast<const double2*>(s_ip + kb + 2);
+      double v[2][4];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) {
+        v[mt][0] = ok[mt] ? static_cast<double>(xa[mt].x) - mu01.x : 0.0;
+        v[mt][1] = ok[mt] ? static_cast<double>(xa[mt].y) - mu01.y : 0.0;
+        v[mt][2] = ok[mt] ? static_cast<double>(xa[mt].z) - mu23.x : 0.0;
+        v[mt][3] = ok[mt] ? static_cast<double>(xa[mt].w) - mu23.y : 0.0;
+        m[mt] = fma(v[mt][0] * ip01.x, v[mt][0], m[mt]);
+        m[mt] = fma(v[mt][1] * ip01.y, v[mt][1], m[mt]);
+        m[mt] = fma(v[mt][2] * ip23.x, v[mt][2], m[mt]);
+        m[mt] = fma(v[mt][3] * ip23.y, v[mt][3], m[mt]);
+      }
+      double b[NT][4];
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const double* wr = s_W + (nt * 8 + g) * Dp + kb;
+        const double2 b01 = *reinterpret_cast<const double2*>(wr), b23 = *reinterpret_cast<const double2*>(wr + 2);
+        b[nt][0] = b01.x;
+        b[nt][1] = b01.y;
+        b[nt][2] = b23.x;
+        b[nt][3] = b23.y;
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) dmma_f64(acc[mt][nt], v[mt][j], b[nt][j]);
+      xa[0] = xn[0];
+      xa[1] = xn[1];
+    }
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) {
+      double yy = 0.0;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) yy = fma(acc[mt][nt][0], acc[mt][nt][0], fma(acc[mt][nt][1], acc[mt][nt][1], yy));
+      double mm = m[mt];
+#pragma unroll
+      for (int s = 1; s < 4; s <<= 1) {
+        yy += __shfl_xor_sync(0xffffffffu, yy, s);
+        mm += __shfl_xor_sync(0xffffffffu, mm, s);
+      }
+      if (t == 0 && ok[mt]) {
+        const double l = p.kconst[q] - 0.5 * (mm - yy);
+        out[o[mt]] = __uint_as_float(__float_as_uint(static_cast<float>(l)) & ~1u);
+      }
+    }
+  }
+}
+
 size_t fix_smem(int D, int H, bool* smem) {
   const size_t base = (2 * static_cast<size_t>(D) + kFixWarps * 64 + static_cast<size_t>(H) * H) * sizeof(double);
   const size_t lam = static_cast<size_t>(D) * H * sizeof(double);
@@ -321,12 +453,18 @@ size_t fix_smem(int D, int H, bool* smem) {
 
 }  // namespace
 
-// ovf[1] |= cnt[1] (first: =): a list overflow at either stage
-__global__ void k_fix_ovf(const unsigned long long* cnt, unsigned long long* ovf, int first) {
+bool fix_dmma_ok(int D, int H) {
+  return H % 8 == 0 && H <= 32 && D % 16 == 0 && fix_dmma_smem(D, H) <= 200 * 1024;
+}
+
+// ovf[1] |= cnt[1] (first: =): a list overflow at either stage; first also
+// counts the scores listed for the one-component tensor pass (nfix[1])
+__global__ void k_fix_ovf(const unsigned long long* cnt, unsigned long long* ovf, int first, unsigned long long* nfix) {
   ovf[1] = first ? cnt[1] : (ovf[1] | cnt[1]);
+  if (first) nfix[1] += cnt[0];
 }
 cudaError_t launch_fix_ovf(const FixArgs& f, int first, cudaStream_t s) {
-  k_fix_ovf<<<1, 1, 0, s>>>(f.cnt, f.ovf, first);
+  k_fix_ovf<<<1, 1, 0, s>>>(f.cnt, f.ovf, first, f.nfix);
   return cudaGetLastError();
 }
 
@@ -346,6 +484,21 @@ cudaError_t launch_fix_f64(const Dims& dm, const FixArgs& f, int mode, const int
                            float* out, cudaStream_t s) {
   if (cudaError_t e = launch_fix_group(dm, f, mode, K, g, rx, s); e != cudaSuccess) return e;
   bool sm = false;
+  if (f.W64 && fix_dmma_ok(dm.D, dm.H)) {
+    FixParams p{dm.D, dm.H, f.X, f.mu, f.psi, f.lam, f.R, f.kconst, false};
+    const size_t smem = fix_dmma_smem(dm.D, dm.H);
+    auto go = [&](auto kern) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+      kern<<<sm_count() * 2, kFixThreads, smem, s>>>(p, f.W64, dm, mode, f.qoff, f.iof, f.sorted, f.nfix, out);
+    };
+    switch (dm.H / 8) {
+      case 1: go(k_fix_dmma<1>); break;
+      case 2: go(k_fix_dmma<2>); break;
+      case 3: go(k_fix_dmma<3>); break;
+      default: go(k_fix_dmma<4>); break;
+    }
+    return cudaGetLastError();
+  }
   const size_t smem = fix_smem(dm.D, dm.H, &sm);
   FixParams p{dm.D, dm.H, f.X, f.mu, f.psi, f.lam, f.R, f.kconst, sm};
   if (smem > 48 * 1024)

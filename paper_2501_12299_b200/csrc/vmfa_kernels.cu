@@ -2377,6 +2377,8 @@ __global__ void __launch_bounds__(128) k_precompute(PrecompArgs a) {
       for (int h = 0; h < Hc; ++h) row[h] = h < H ? static_cast<float>(u[h]) : 0.f;
       // K-major copy for the tensor-core scorer: WT[c][h][d], h < Hp (zero padded)
       for (int h = 0; h < a.Hp; ++h) a.WT[((int64_t)c * a.Hp + h) * D + d] = h < H ? static_cast<float>(u[h]) : 0.f;
+      if (a.W64)
+        for (int h = 0; h < H; ++h) a.W64[((int64_t)c * H + h) * D + d] = u[h];
       a.ipsi32[(int64_t)c * D + d] = static_cast<float>(ip);
       row[Hc] = static_cast<float>(a.mu[(int64_t)c * D + d]);
       row[Hc + 1] = static_cast<float>(ip);
@@ -2471,6 +2473,7 @@ __global__ void __launch_bounds__(128) k_precompute(PrecompArgs a) {
               if (h >= H) continue;
               a.P[((int64_t)c * D + d) * HP + h] = static_cast<float>(w[i][j]);
               a.WT[((int64_t)c * a.Hp + h) * D + d] = static_cast<float>(w[i][j]);
+              if (a.W64) a.W64[((int64_t)c * H + h) * D + d] = w[i][j];
               a.V32[((int64_t)c * D + d) * H + h] = static_cast<float>(v[i][j]);
             }
           }

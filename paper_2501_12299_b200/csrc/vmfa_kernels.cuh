@@ -211,6 +211,7 @@ struct PrecompArgs {
   float* ipsi32;          // C x D
   int Hp;                 // H padded to {4, 8, 16, 32, 64}
   unsigned long long* status;
+  double* W64;            // C x H x D fp64 W^T = R^-1 Lambda^T Psi^-1 (fp64 re-scoring), or null
 };
 
 // launchers (return cudaError_t of the launch)
@@ -300,7 +301,11 @@ struct FixArgs {
   int* qfill;
   int* iof;                      // work-item offsets per component (C+1)
   unsigned long long* ovf;       // [1]: a list overflowed (the scan kernels run)
+  const double* W64;             // C x H x D fp64 W^T from the precompute (DMMA re-scoring), or null
 };
+// the fp64 tensor-core (DMMA) re-scoring applies: H a multiple of 8 up to 32,
+// D a multiple of 16, W^T of one component fits in shared memory
+bool fix_dmma_ok(int D, int H);
 cudaError_t launch_fix_ovf(const FixArgs& f, int first, cudaStream_t s);
 cudaError_t launch_fix_group(const Dims& dm, const FixArgs& f, int mode, const int* K, const int* g, const int* rx,
                              cudaStream_t s);

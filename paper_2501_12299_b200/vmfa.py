@@ -414,11 +414,11 @@ class Session:
 
     def scoring_work(self) -> dict:
         """vmfa_scoring_work: row visits, image / record bytes of the scoring launches."""
-        w = np.zeros(7, np.int64)
-        check(lib().vmfa_scoring_work(self._h, ptr(w), 7))
+        w = np.zeros(8, np.int64)
+        check(lib().vmfa_scoring_work(self._h, ptr(w), 8))
         return dict(anchor_visits=int(w[0]), extra_visits=int(w[1]), image_bytes=int(w[2]),
                     single_image_bytes=int(w[3]), record_bytes=int(w[4]), scorer=int(w[5]),
-                    fp64_rescored=int(w[6]))
+                    fp64_rescored=int(w[6]), tensor_rescored=int(w[7]))
 
     def stream(self) -> int:
         return lib().vmfa_ctx_stream(self._h)

@@ -27,7 +27,8 @@ import time
 import numpy as np
 import pytest
 
-from _helpers import LJ_RTOL, compare_estep, compare_g_tau, near_tie_rows_fast, to_vmfa_params, to_vmfa_state
+from _helpers import (LJ_RTOL, compare_estep, compare_g_tau, near_tie_rows_fast, to_oracle_params, to_oracle_state,
+                      to_vmfa_params, to_vmfa_state)
 
 pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 
@@ -68,15 +69,28 @@ def _report(name, rep):
             json.dump(rep, f, indent=1, default=float)
 
 
-def teacher_forced(O, V, X, C, H, Cp, G, iters, name, seed=0):
+def teacher_forced(O, V, X, C, H, Cp, G, iters, name, seed=0, free_iters=0):
+    """free_iters > 0: the device first runs that many main iterations on its
+    own from the initial state (components collapse onto few points, the
+    scorer flags their cancelling scores), then the teacher-forced steps
+    start from the device's parameters and state."""
     threads = os.cpu_count() or 8
     N = X.shape[0]
     t0 = time.time()
     p, st, floor, _ = O.initialize(X, C, H, Cp, G, seed=seed, scale=0.1, loading_init=1)
     sess = V.Session(C, X.shape[1], H, Cp, G, X)
     sess.set_floor(floor)
-    rep = dict(case=name, N=N, D=X.shape[1], C=C, H=H, Cp=Cp, G=G, iterations=[])
-    for it in range(iters):
+    rep = dict(case=name, N=N, D=X.shape[1], C=C, H=H, Cp=Cp, G=G, free_iters=free_iters, iterations=[])
+    if free_iters:
+        sess.upload_params(to_vmfa_params(V, p))
+        sess.upload_state(to_vmfa_state(V, st))
+        for _ in range(2):
+            sess.variational_e_step(seed, 0)
+        for it in range(free_iters):
+            sess.iterate(seed, it)
+        sess.scoring_work()
+        p, st = to_oracle_params(O, sess.download_params()), to_oracle_state(O, sess.download_state())
+    for it in range(free_iters, free_iters + iters):
         r = {}
         k = O.precompute_all(p)
         sess.upload_params(to_vmfa_params(V, p))
@@ -120,7 +134,9 @@ def teacher_forced(O, V, X, C, H, Cp, G, iters, name, seed=0):
         sess.update_params()
         p_g = sess.download_params()
         p_or = O.update_params(s_or, N, p, floor)
-        r["fp64_rescored"] = sess.scoring_work()["fp64_rescored"]
+        w = sess.scoring_work()
+        r["fp64_rescored"] = w["fp64_rescored"]
+        r["flagged"] = w["tensor_rescored"]
         for f, tol in _PARAM_TOL.items():
             rel = _param_rel(f, p_g, p_or, s_or)
             live = p_or.pi > 0
@@ -151,6 +167,23 @@ def test_config3_teacher_forced_100k(oracle, gpu):
     X = V.gen_synthetic(V.synth_spec(3), 0, 100_000)
     m = V.CONFIGS[3]["model"]
     teacher_forced(O, V, X, m["C"], m["H"], m["Cprime"], m["G"], 2, "config3_100k")
+
+
+@pytest.mark.parametrize("fix_tc", ["0", "1"])
+def test_config3_late_iteration_rescoring(oracle, gpu, monkeypatch, fix_tc):
+    """The cancellation re-scoring where it carries weight: after 12 free
+    device iterations on 100 000 config-3 rows (collapsed components, ~10%
+    of the retained scores flagged), one teacher-forced step at the full bar.
+    fix_tc "0": flagged scores straight to the fp64 DMMA pass (default);
+    "1": the one-component tensor pass first, fp64 for what stays flagged."""
+    O, V = oracle, gpu
+    monkeypatch.setenv("VMFA_FIX_TC", fix_tc)
+    X = V.gen_synthetic(V.synth_spec(3), 0, 100_000)
+    m = V.CONFIGS[3]["model"]
+    rep = teacher_forced(O, V, X, m["C"], m["H"], m["Cprime"], m["G"], 1, f"config3_late_fixtc{fix_tc}",
+                         free_iters=12)
+    assert rep["iterations"][0]["flagged"] > 1000, rep["iterations"][0]
+    assert rep["iterations"][0]["fp64_rescored"] > 1000, rep["iterations"][0]
 
 
 def test_config4_shape_teacher_forced_200k(oracle, gpu):
