@@ -303,6 +303,12 @@ const char* vmfa_kernel_name(int i);
  * clears them; enable=0 disarms.                                            */
 int vmfa_diag_scorer_cycles(int enable, unsigned long long* out, int n);
 
+/* Diagnostic: the K1 inversion's device radix sort (vmfa_sort.cu) on n host
+ * keys < 2^bits, run `reps` times; keys_out / vals_out get the stably sorted
+ * keys and their input indices. Returns the number of repetitions whose
+ * output differed from the first (0), or -1 on a CUDA error.              */
+int vmfa_diag_radix_sort(const uint32_t* keys, int64_t n, int bits, uint32_t* keys_out, int32_t* vals_out, int reps);
+
 /* Work accounting of the candidate-scoring launches (the anchor pass and the
  * extras of one E-step) for roofline figures: out[0] anchor row visits
  * (N*C'), out[1] extra row visits of the last E-step (rows whose r_n is not

@@ -115,6 +115,7 @@ _SIGS = {
     "vmfa_kernel_name": (C.c_char_p, [_I]),
     "vmfa_ctx_stream": (_P, [_P]),
     "vmfa_diag_scorer_cycles": (_I, [_I, _P, _I]),
+    "vmfa_diag_radix_sort": (_I, [_P, _I64, _I, _P, _P, _I]),
     "vmfa_synchronize": (_I, [_P]),
     "vmfa_gen_synthetic": (_I, [C.POINTER(SynthSpec), _I64, _I64, _P, _P, _I]),
     "vmfa_host_initialize": (_I, [_P, _I64, _I, _I, _I, _I, _I, _U64, _D, _I, _P, _P, _P, _P,

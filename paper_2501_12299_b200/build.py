@@ -22,7 +22,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 # extra nvcc flags for diagnostic builds (e.g. -DVMFA_STATS_PROF; rebuild with force=True)
 EXTRA = os.environ.get("VMFA_NVCC_EXTRA", "").split()
-CU_SOURCES = ["vmfa_kernels.cu", "vmfa_score_tc.cu", "vmfa_score_ws.cu", "vmfa_fixup.cu", "vmfa_ops.cu", "vmfa_stats_tc.cu", "vmfa_capi.cu"]
+CU_SOURCES = ["vmfa_kernels.cu", "vmfa_score_tc.cu", "vmfa_score_ws.cu", "vmfa_fixup.cu", "vmfa_ops.cu", "vmfa_stats_tc.cu", "vmfa_sort.cu", "vmfa_capi.cu"]
 CXX_SOURCES = ["host/vmfa_host.cpp", "host/vmfa_io.cpp", "host/vmfa_synth.cpp"]
 DEPS_H = ["vmfa_kernels.cuh", "vmfa_internal.hpp", "vmfa_rng.hpp"]
 

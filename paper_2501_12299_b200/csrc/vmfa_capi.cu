@@ -3,7 +3,6 @@
 // replicated parameters/caches, the shard's variational state and all scratch.
 // Every phase is stream-ordered; host synchronisation happens only where a
 // result is returned through a host pointer.
-#include <cub/cub.cuh>
 
 #include <algorithm>
 #include <cmath>
@@ -127,7 +126,8 @@ struct vmfa_ctx {
   float* ret_lj = nullptr;
   double *resp = nullptr, *lse = nullptr;
   // CSR / sort scratch
-  unsigned *keys = nullptr, *keys_alt = nullptr;
+  unsigned *keys = nullptr, *keys_alt = nullptr, *keys_tmp = nullptr;
+  int* sort_hist = nullptr;  // radix-sort digit histograms + scan scratch (vmfa_sort.cu)
   int* vals = nullptr;
   int *kinv_off = nullptr, *kinv_ent = nullptr, *kinv_items = nullptr;
   int *ex_off = nullptr, *ex_ent = nullptr, *ex_items = nullptr;
@@ -137,8 +137,6 @@ struct vmfa_ctx {
   int gupd_pts = 256;       // partition points per block-3 item
   double* stats_part = nullptr;
   int *cnt = nullptr, *chunks = nullptr;
-  void* cub_tmp = nullptr;
-  size_t cub_bytes = 0;
   // block-3 scratch
   int gupd_grid = 0;
   long long *gt_cnt = nullptr, *gt_hi = nullptr, *gt_lo = nullptr;
@@ -155,8 +153,7 @@ struct vmfa_ctx {
   unsigned long long* cl_n = nullptr;
   int* cl_ovf = nullptr;
   int64_t cu_n = 0;  // unique entries of the last reduction (host)
-  void* cl_tmp = nullptr;
-  size_t cl_tmp_bytes = 0;
+  int* cl_hist = nullptr;  // the list sort's digit histograms and scan scratch
   // stats: packed [Nc | E | Y | sq]
   double* stats = nullptr;
   size_t stats_len = 0;
@@ -302,11 +299,32 @@ int csr_by_key(vmfa_ctx* x, const unsigned* keys, int64_t n, int* off, int* ent,
   const int C = x->dm.C;
   cudaStream_t s = x->stream;
   const int tok = x->begin(kFamSort, n);
-  CU(launch_iota(x->vals, n, s));
-  size_t tb = x->cub_bytes;
-  CU(cub::DeviceRadixSort::SortPairs(x->cub_tmp, tb, keys, x->keys_alt, x->vals, ent,
-                                     static_cast<int>(n), 0, bits_for(static_cast<unsigned>(C)), s));
+  CU(radix_sort_pairs(keys, nullptr, n, bits_for(static_cast<unsigned>(C)), x->keys_tmp, x->vals, x->keys_alt, ent,
+                      x->sort_hist, s));
   CU(launch_offsets_sorted(x->keys_alt, n, C, off, s));
+  static const bool check = [] {  // VMFA_SORT_CHECK=1: verify every CSR on the host (debugging)
+    const char* v = std::getenv("VMFA_SORT_CHECK");
+    return v && v[0] == '1';
+  }();
+  if (check && !x->capturing) {
+    std::vector<unsigned> k(n), ks(n);
+    std::vector<int> e(n);
+    CU(cudaMemcpyAsync(k.data(), keys, 4 * n, cudaMemcpyDeviceToHost, s));
+    CU(cudaMemcpyAsync(ks.data(), x->keys_alt, 4 * n, cudaMemcpyDeviceToHost, s));
+    CU(cudaMemcpyAsync(e.data(), ent, 4 * n, cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    const unsigned mask = (1u << bits_for(static_cast<unsigned>(C))) - 1u;
+    for (int64_t i = 0; i < n; ++i) {
+      const bool bad = e[i] < 0 || e[i] >= n || ks[i] != k[e[i]] ||
+                       (i > 0 && ((ks[i - 1] & mask) > (ks[i] & mask) ||
+                                  ((ks[i - 1] & mask) == (ks[i] & mask) && e[i - 1] >= e[i])));
+      if (bad) {
+        std::fprintf(stderr, "vmfa: csr_by_key check failed at %lld of %lld (key %u ent %d)\n",
+                     static_cast<long long>(i), static_cast<long long>(n), ks[i], e[i]);
+        return fail(VMFA_ERR_CUDA, "sort check failed");
+      }
+    }
+  }
   if (items) CU(launch_items_scan(off, C, rows_per_item, 0, items, s));
   x->end(tok);
   return VMFA_OK;
@@ -437,8 +455,8 @@ int run_precompute(vmfa_ctx* x, int* failed, bool sync = true) {
 int ensure_kinv_current(vmfa_ctx* x) {
   if (x->kinv_for_current_K) return VMFA_OK;
   const Dims& dm = x->dm;
-  CU(launch_keys_from_i32(x->K, x->keys, dm.N * dm.Cp, x->stream));
-  TRY(csr_by_key(x, x->keys, dm.N * dm.Cp, x->kinv_off, x->kinv_ent, x->kinv_items, x->score_rows));
+  TRY(csr_by_key(x, reinterpret_cast<const unsigned*>(x->K), dm.N * dm.Cp, x->kinv_off, x->kinv_ent, x->kinv_items,
+                 x->score_rows));
   x->kinv_for_current_K = true;
   return VMFA_OK;
 }
@@ -501,15 +519,8 @@ int enable_lists(vmfa_ctx* x) {
   A(x->cu_off, static_cast<size_t>(dm.C) + 1);
   A(x->cl_n, 1);
   A(x->cl_ovf, 1);
+  A(x->cl_hist, static_cast<size_t>(sort_hist_ints(x->cl_cap)));
   if (r != VMFA_OK) return r;
-  size_t c1 = 0, c2 = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, c1, x->cl_key, x->cl_skey, x->cl_iota, x->cl_perm,
-                                  static_cast<int>(x->cl_cap), 0, 32, x->stream);
-  cub::DeviceScan::InclusiveSum(nullptr, c2, x->cl_iota, x->cl_perm, static_cast<int>(x->cl_cap), x->stream);
-  x->cl_tmp_bytes = std::max(c1, c2) + 256;
-  unsigned char* tmp = nullptr;
-  TRY(x->alloc(tmp, x->cl_tmp_bytes));
-  x->cl_tmp = tmp;
   x->gupd_pts = static_cast<int>(std::min<int64_t>(bal, 512));
   x->sparse = true;
   return VMFA_OK;
@@ -521,10 +532,8 @@ int cooc_reduce(vmfa_ctx* x, int64_t n) {
   cudaStream_t s = x->stream;
   if (n > x->cl_cap) return fail(VMFA_ERR_UNSUPPORTED, "co-occurrence list of %lld entries exceeds its capacity %lld",
                                  static_cast<long long>(n), static_cast<long long>(x->cl_cap));
-  CU(launch_iota(x->cl_iota, n, s));
-  size_t tb = x->cl_tmp_bytes;
-  CU(cub::DeviceRadixSort::SortPairs(x->cl_tmp, tb, x->cl_key, x->cl_skey, x->cl_iota, x->cl_perm,
-                                     static_cast<int>(n), 0, 2 * x->cl_kb, s));
+  // (cu_key and cl_iota are free until the reduction: the sort's scratch)
+  CU(radix_sort_pairs(x->cl_key, nullptr, n, 2 * x->cl_kb, x->cu_key, x->cl_iota, x->cl_skey, x->cl_perm, x->cl_hist, s));
   CoocArgs a{};
   a.dm = x->dm;
   a.kb = x->cl_kb;
@@ -541,8 +550,7 @@ int cooc_reduce(vmfa_ctx* x, int64_t n) {
   a.u_lo = x->cu_lo;
   a.u_off = x->cu_off;
   CU(launch_cooc_heads(a, s));
-  tb = x->cl_tmp_bytes;
-  if (n > 0) CU(cub::DeviceScan::InclusiveSum(x->cl_tmp, tb, x->cl_iota, x->cl_iota, static_cast<int>(n), s));
+  if (n > 0) CU(scan_i32(x->cl_iota, x->cl_iota, n, true, x->cl_hist, s));
   for (long long* q : {x->cu_cnt, x->cu_hi, x->cu_lo})
     CU(cudaMemsetAsync(q, 0, static_cast<size_t>(std::max<int64_t>(n, 1)) * sizeof(long long), s));
   CU(launch_cooc_sums(a, s));
@@ -633,8 +641,7 @@ int estep_local(vmfa_ctx* x, uint64_t seed, uint64_t it, int mode, bool exchange
   }
   x->kinv_for_current_K = false;
   // block 2: partition by label (stable => ascending n per component)
-  CU(launch_keys_from_i32(x->labels, x->keys, dm.N, s));
-  TRY(csr_by_key(x, x->keys, dm.N, x->part_off, x->part_ent, nullptr, 1));
+  TRY(csr_by_key(x, reinterpret_cast<const unsigned*>(x->labels), dm.N, x->part_off, x->part_ent, nullptr, 1));
   CU(launch_items_scan(x->part_off, dm.C, x->gupd_pts, 1, x->part_items, s));
   // block 3 (local accumulation; selection unless exchanging)
   CU(launch_logpi(x->pi, dm.C, x->logpi, s));
@@ -1109,9 +1116,10 @@ int vmfa_ctx_create(vmfa_ctx** out, int device, int C, int D, int H, int Cp, int
   A(x->ret_lj, N * dm.stride);
   A(x->resp, N * Cp);
   A(x->lse, N);
-  A(x->keys, N * Cp);
   A(x->keys_alt, N * Cp);
+  A(x->keys_tmp, N * Cp);
   A(x->vals, N * Cp);
+  A(x->sort_hist, static_cast<size_t>(sort_hist_ints(static_cast<int64_t>(N * Cp))));
   A(x->kinv_off, Cs + 1);
   A(x->kinv_ent, N * Cp);
   A(x->kinv_items, Cs + 1);
@@ -1182,20 +1190,6 @@ int vmfa_ctx_create(vmfa_ctx** out, int device, int C, int D, int H, int Cp, int
   x->E = x->Nc + Cs;
   x->Y = x->E + Cs * H1 * H1;
   x->sq = x->Y + Cs * H1 * D;
-  // cub temp storage: max over the sorts / scans we run
-  size_t b1 = 0, b2 = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, b1, x->keys, x->keys_alt, x->vals, x->kinv_ent,
-                                  static_cast<int>(N * Cp), 0, 32, x->stream);
-  cub::DeviceScan::ExclusiveSum(nullptr, b2, x->cnt, x->kinv_off, C + 1, x->stream);
-  x->cub_bytes = std::max(b1, b2) + 256;
-  void* tmp = nullptr;
-  if (cudaMalloc(&tmp, x->cub_bytes) != cudaSuccess) {
-    vmfa_ctx_destroy(x);
-    return fail(VMFA_ERR_CUDA, "cudaMalloc(cub temp) failed");
-  }
-  x->allocs.push_back(tmp);
-  x->bytes += x->cub_bytes;
-  x->cub_tmp = tmp;
   if (force_sparse && r == VMFA_OK) r = enable_lists(x);
   if (r != VMFA_OK) {
     vmfa_ctx_destroy(x);
@@ -2049,8 +2043,7 @@ int vmfa_hard_partition(vmfa_ctx* x, const int32_t* K, const int32_t* count, con
   CU(dlab.make(nullptr, dm.N, s));
   CU(launch_hard_labels(dm, dK.p, dcnt.p, didx.p, dl.p, dlab.p, s));
   // the partition: stable by label, so every cell lists its rows ascending
-  CU(launch_keys_from_i32(dlab.p, x->keys, dm.N, s));
-  TRY(csr_by_key(x, x->keys, dm.N, x->part_off, x->part_ent, nullptr, 1));
+  TRY(csr_by_key(x, reinterpret_cast<const unsigned*>(dlab.p), dm.N, x->part_off, x->part_ent, nullptr, 1));
   CU(cudaMemcpyAsync(labels, dlab.p, sizeof(int) * dm.N, cudaMemcpyDeviceToHost, s));
   if (part_off) CU(cudaMemcpyAsync(part_off, x->part_off, sizeof(int) * (dm.C + 1), cudaMemcpyDeviceToHost, s));
   if (part_ent) CU(cudaMemcpyAsync(part_ent, x->part_ent, sizeof(int) * dm.N, cudaMemcpyDeviceToHost, s));

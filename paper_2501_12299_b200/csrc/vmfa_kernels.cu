@@ -865,7 +865,7 @@ __global__ void __launch_bounds__(kGupdThreads) k_gselect_dense(Dims dm, long lo
 
 // ---------------------------------------------------------------- sparse co-occurrence (large C)
 // The list of exact (c, c~) partial sums appended by k_gupdate (list mode)
-// is sorted by key = c << kb | c~ (cub radix sort over 2 kb bits), reduced
+// is sorted by key = c << kb | c~ (the radix sort of vmfa_sort.cu over 2 kb bits), reduced
 // by key (exact int64 sums: the order of the parts does not matter, so g is
 // bit-identical to the dense rows' for any item split or rank count), and g_c
 // is selected per component from its unique entries exactly as

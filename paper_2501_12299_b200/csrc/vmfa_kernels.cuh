@@ -215,6 +215,15 @@ struct PrecompArgs {
 };
 
 // launchers (return cudaError_t of the launch)
+// vmfa_sort.cu: stable LSD radix sort of (key, value) pairs over 8-bit
+// digits (vals null: value = input index; keys < 2^bits), the result in
+// (kout, vout); ktmp / vtmp scratch of n entries; hist: sort_hist_ints(n)
+// ints. scan_i32: int32 prefix sum (in == out allowed), tmp: scan_tmp_ints(n).
+int64_t sort_hist_ints(int64_t n);
+int64_t scan_tmp_ints(int64_t n);
+cudaError_t radix_sort_pairs(const unsigned* keys, const int* vals, int64_t n, int bits, unsigned* ktmp, int* vtmp,
+                             unsigned* kout, int* vout, int* hist, cudaStream_t s);
+cudaError_t scan_i32(const int* in, int* out, int64_t n, bool inclusive, int* tmp, cudaStream_t s);
 cudaError_t launch_iota(int* v, int64_t n, cudaStream_t s);
 cudaError_t launch_fill_i32(int* v, int64_t n, int value, cudaStream_t s);
 cudaError_t launch_keys_from_i32(const int* src, unsigned* keys, int64_t n, cudaStream_t s);

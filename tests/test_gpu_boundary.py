@@ -203,3 +203,30 @@ def test_torchrun_two_ranks_match_one(gpu, tmp_path, cooc):
     np.testing.assert_allclose(r0["J"], a["J"], rtol=1e-3)
     np.testing.assert_allclose(r0["F"], a["F"], rtol=1e-4)  # the north-star F tolerance
     np.testing.assert_allclose(r0["mu"], a["mu"], rtol=1e-3, atol=1e-3 * np.abs(a["mu"]).max())
+
+
+@pytest.mark.parametrize("C", [200, 4000, 40000])
+def test_partition_sort_at_scale(gpu, C):
+    """The K1 inversion's hand-written stable radix sort (vmfa_sort.cu; one,
+    two 8-bit passes) through hard_partition at 2M rows: labels are the
+    first strict maximum of each K row's log-joints, and the partition equals
+    numpy's stable argsort of the labels (rows ascending per component, the
+    reference's push order, estep.cpp:169-172)."""
+    V = gpu
+    N, D, Cp, G = 2_000_000, 8, 3, 2
+    rng = np.random.default_rng(C)
+    sess = V.Session(C, D, 1, Cp, G, np.zeros((N, D), np.float32))
+    S = sess.stride
+    K = np.sort(np.stack([rng.choice(C, Cp, replace=False) for _ in range(256)]), axis=1)
+    K = K[rng.integers(0, 256, N)].astype(np.int32)  # 256 distinct sorted rows, repeated
+    idx = np.full((N, S), -1, np.int32)
+    idx[:, :Cp] = K
+    lj = np.zeros((N, S))
+    lj[:, :Cp] = rng.integers(0, 4, (N, Cp)).astype(np.float64)  # ties: the first member wins
+    count = np.full(N, Cp, np.int32)
+    lab, off, ent = sess.hard_partition(K, count, idx, lj)
+    want = K[np.arange(N), np.argmax(lj[:, :Cp], axis=1)]
+    assert np.array_equal(lab, want)
+    assert np.array_equal(ent, np.argsort(want, kind="stable").astype(np.int32))
+    assert np.array_equal(off, np.searchsorted(np.sort(want), np.arange(C + 1)).astype(np.int32))
+    sess.close()
