@@ -469,8 +469,8 @@ int score_anchors(vmfa_ctx* x) {
   TRY(ensure_kinv_current(x));
   if (x->scorer == 2) {
     const int tok = x->begin(kFamOther, dm.C);
-    CU(launch_ws_images(dm, 0, x->WT, x->mu32, x->ipsi32, x->g, x->gcnt, x->bimg, x->bscl, s, x->sscl));
-    CU(launch_ws_records(dm, 0, x->WT, x->mu32, x->ipsi32, x->kconst, x->g, x->gcnt, x->bscl, x->brec, s));
+    CU(launch_ws_images(dm, 0, x->WT, x->mu32, x->ipsi32, x->g, x->gcnt, x->bimg, x->bscl, s, x->sscl, x->brec));
+    CU(launch_ws_records(dm, 0, x->WT, x->mu32, x->ipsi32, x->kconst, x->g, x->gcnt, x->bscl, x->brec, s, 1));
     x->end(tok);
   }
   ScoreArgs a = score_args(x);
@@ -1068,8 +1068,11 @@ int vmfa_ctx_create(vmfa_ctx** out, int device, int C, int D, int H, int Cp, int
   A(x->mu32, Cs * D);
   A(x->WT, Cs * x->Hp * D);
   if (x->scorer == 2) {
-    // items <= sum_c ceil(rows_c / 128); the re-scoring lists hold <= fix_cap entries
-    x->fix_cap = std::max<long long>(1 << 20, static_cast<long long>(N) * Cp);
+    // items <= sum_c ceil(rows_c / 128); the re-scoring lists hold <= fix_cap
+    // entries: every slot of the anchor pass up to 2^26 (16 B per entry), so
+    // that the scanning fallback (vmfa_fixup.cu, list overflow) stays rare --
+    // config 2 flags ~1e6 scores per pass
+    x->fix_cap = std::max<long long>(1 << 20, std::min<long long>(static_cast<long long>(N) * dm.SL, 1LL << 26));
     A(x->jobs, static_cast<size_t>(x->fix_cap) / 128 + Cs + 2);
     A(x->bimg, ws_image_halves(dm, 0));
     A(x->simg, ws_image_halves(dm, 1));

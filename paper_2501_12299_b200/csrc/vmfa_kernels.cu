@@ -301,8 +301,9 @@ __global__ void __launch_bounds__(256) k_select(SelectArgs a) {
   for (int i = threadIdx.x; i < W * (blockDim.x >> 5); i += blockDim.x) s_seen[i] = 0u;
   __syncthreads();
   unsigned* seen = s_seen + (threadIdx.x >> 5) * W;
-  // per warp: own log-joint of each anchor j (its self slot), <= 8 anchors
+  // per warp: own log-joint of each anchor j (its self slot) and its rank, <= 8 anchors
   float* qual = reinterpret_cast<float*>(s_seen + W * (blockDim.x >> 5)) + (threadIdx.x >> 5) * 8;
+  int* qrank = reinterpret_cast<int*>(s_seen + W * (blockDim.x >> 5)) + 64 + (threadIdx.x >> 5) * 8;
   const int64_t warp0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int CpG = dm.Cp * dm.G;
@@ -376,26 +377,61 @@ __global__ void __launch_bounds__(256) k_select(SelectArgs a) {
         pri[k] = qual[__float2int_rz((static_cast<float>(s) + 0.5f) * invG)];
       dups |= comp[k] >= 0 && !uniq[k];
     }
-    // the first occurrence takes the value of the best slot of its component
+    // the first occurrence takes the value of the best slot of its component:
+    // the largest priority, the smallest slot on a tie. Only duplicate slots
+    // can beat a first occurrence, so they alone are visited (warp-uniform
+    // loop over their ballot); priorities travel as ranks packed with the
+    // component (anchor j: #{j' : qual[j'] < qual[j]}, equal values equal
+    // ranks, -inf 0 like an unscored slot, +inf 15), the value is fetched once
     if (__any_sync(kFull, dups)) {
-      float bp[NS];
+      if (lane < dm.Cp) {
+        const float qj = qual[lane];
+        int r = 0;
+        for (int j2 = 0; j2 < dm.Cp; ++j2) r += qual[j2] < qj;
+        qrank[lane] = r;
+      }
+      __syncwarp();
+      unsigned pk[NS];
+      int br[NS], bs[NS];
 #pragma unroll
-      for (int k = 0; k < NS; ++k) bp[k] = pri[k];
+      for (int k = 0; k < NS; ++k) {
+        const int s = k * 32 + lane;
+        int rk = pri[k] == INFINITY ? 15 : 0;
+        if (s < CpG && comp[k] >= 0 && pri[k] != INFINITY)
+          rk = qrank[__float2int_rz((static_cast<float>(s) + 0.5f) * invG)];
+        pk[k] = comp[k] >= 0 ? (static_cast<unsigned>(comp[k]) << 4) | static_cast<unsigned>(rk) : 0xffffffffu;
+        br[k] = rk;
+        bs[k] = s;
+      }
 #pragma unroll
       for (int k2 = 0; k2 < NS; ++k2) {
-        for (int t = 0; t < 32; ++t) {
-          const int oc = __shfl_sync(kFull, comp[k2], t);
-          const float op = __shfl_sync(kFull, pri[k2], t);
-          const float ov = __shfl_sync(kFull, lj[k2], t);
-          if (oc < 0) continue;
+        unsigned dm2 = __ballot_sync(kFull, comp[k2] >= 0 && !uniq[k2]);
+        while (dm2) {
+          const int t = __ffs(dm2) - 1;
+          dm2 &= dm2 - 1;
+          const unsigned o = __shfl_sync(kFull, pk[k2], t);
+          const int orank = static_cast<int>(o & 15u);
 #pragma unroll
           for (int k = 0; k < NS; ++k)
-            if (uniq[k] && oc == comp[k] && op > bp[k]) {
-              bp[k] = op;
-              lj[k] = ov;
+            if (uniq[k] && static_cast<int>(o >> 4) == comp[k] && orank > br[k]) {
+              br[k] = orank;
+              bs[k] = k2 * 32 + t;
             }
         }
       }
+      float ljw[NS];
+#pragma unroll
+      for (int k = 0; k < NS; ++k) {
+        float w = lj[k];
+#pragma unroll
+        for (int k2 = 0; k2 < NS; ++k2) {
+          const float ov = __shfl_sync(kFull, lj[k2], bs[k] & 31);
+          if (k2 == (bs[k] >> 5)) w = ov;
+        }
+        ljw[k] = w;
+      }
+#pragma unroll
+      for (int k = 0; k < NS; ++k) lj[k] = ljw[k];
     }
 #pragma unroll
     for (int k = 0; k < NS; ++k)
@@ -541,7 +577,7 @@ __global__ void __launch_bounds__(kGupdThreads) k_gupdate(GupdArgs a, int capmax
   __shared__ KeyMin red[kGupdThreads / 32];
   __shared__ int red_i[kGupdThreads / 32];
   __shared__ int s_sel[64];
-  __shared__ int s_nsel;
+  __shared__ int s_nsel, s_win;
   const Dims dm = a.dm;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nw = kGupdThreads / 32;
@@ -758,15 +794,25 @@ __global__ void __launch_bounds__(kGupdThreads) k_gupdate(GupdArgs a, int capmax
     }
     if (tid == 0) s_nsel = 0;
     __syncthreads();
-    for (int r = 0; r < dm.G - 1 && npts > 0; ++r) {
-      KeyMin best{INFINITY, 0x7fffffff};
-      int bi = -1;
+    // G-1 rounds of a block-wide argmin over the threads' own minima (slot i
+    // belongs to thread i mod kGupdThreads); only the winner's owner rescans
+    // its slots after the winning key is retired
+    KeyMin mine{INFINITY, 0x7fffffff};
+    int mi = -1;
+    auto own_min = [&]() {
+      mine = KeyMin{INFINITY, 0x7fffffff};
+      mi = -1;
       for (int i = tid; i < tab_n; i += kGupdThreads) {
         const double v = kv[i];
         if (v == INFINITY) continue;
         const KeyMin k{v, use_smem ? t_key[i] : i};
-        if (kless(k, best)) best = k, bi = i;
+        if (kless(k, mine)) mine = k, mi = i;
       }
+    };
+    if (npts > 0) own_min();
+    for (int r = 0; r < dm.G - 1 && npts > 0; ++r) {
+      KeyMin best = mine;
+      int bi = mi;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
         KeyMin oth{__shfl_xor_sync(kFull, best.v, o), __shfl_xor_sync(kFull, best.c, o)};
@@ -780,13 +826,16 @@ __global__ void __launch_bounds__(kGupdThreads) k_gupdate(GupdArgs a, int capmax
         int ib = red_i[0];
         for (int w = 1; w < nw; ++w)
           if (kless(red[w], b)) b = red[w], ib = red_i[w];
-        if (b.c != 0x7fffffff) {
-          s_sel[s_nsel++] = b.c;
-          kv[ib] = INFINITY;
-        }
+        s_win = b.c != 0x7fffffff ? ib : -1;
+        if (b.c != 0x7fffffff) s_sel[s_nsel++] = b.c;
       }
       __syncthreads();
-      if (s_nsel <= r) break;  // no more keys
+      const int win = s_win;
+      if (win < 0) break;  // no more keys
+      if (tid == win % kGupdThreads) {
+        kv[win] = INFINITY;
+        own_min();
+      }
     }
     if (tid == 0) {
       int out[64];
@@ -1992,6 +2041,28 @@ __device__ __forceinline__ void chol_solve_thread(const double* R, double* b, in
   }
 }
 
+// chol_solve_thread with compile-time loop bounds (b stays in registers; n <= HM)
+template <int HM>
+__device__ __forceinline__ void chol_solve_thread_t(const double* R, double* b, int n) {
+#pragma unroll
+  for (int i = 0; i < HM; ++i)
+    if (i < n) {
+      double s = b[i];
+#pragma unroll
+      for (int k = 0; k < i; ++k) s -= R[i * n + k] * b[k];
+      b[i] = s / R[i * n + i];
+    }
+#pragma unroll
+  for (int i = HM - 1; i >= 0; --i)
+    if (i < n) {
+      double s = b[i];
+#pragma unroll
+      for (int k = i + 1; k < HM; ++k)
+        if (k < n) s -= R[k * n + i] * b[k];
+      b[i] = s / R[i * n + i];
+    }
+}
+
 __device__ __forceinline__ void set_status(unsigned long long* st, int c, int code) {
   atomicMin(st, (static_cast<unsigned long long>(c) << 8) | static_cast<unsigned long long>(code));
 }
@@ -2114,15 +2185,20 @@ __device__ __forceinline__ void ldlt_solve_thread(const double* A, const int* pe
 // pi = N_c/N, A^T = E^-1 Y^T by LDLT (one trace-scaled jitter retry on
 // failure or a non-finite solution, else SingularEc), Lambda / mu from A,
 // sigma^2 = max(floor, (sq - sum_h Y.A)/N_c).
+// HM != 0: H + 1 <= HM, the per-dimension solve in registers (the
+// transpositions composed once into s_idx: b is gathered permuted, the
+// solution scattered back to natural order through shared memory s_x)
+template <int HM>
 __global__ void __launch_bounds__(128) k_update(UpdateArgs a) {
   extern __shared__ __align__(16) double s_upd[];
   __shared__ int s_ok, s_fin;
-  __shared__ int s_perm[kMaxH1];
-  __shared__ double s_tmp[kMaxH1];
+  __shared__ int s_perm[kMaxH1], s_idx[kMaxH1];
+  __shared__ double s_tmp[kMaxH1], s_dinv[kMaxH1];
   const Dims dm = a.dm;
   const int H = dm.H, H1 = H + 1, D = dm.D;
   double* sE = s_upd;              // E_c (+ jitter)
   double* sF = s_upd + H1 * H1;    // LDLT factors
+  double* s_x = sF + H1 * H1;      // [H1][blockDim] natural-order solutions (HM != 0)
   const int tid = threadIdx.x;
   for (int c = blockIdx.x; c < dm.C; c += gridDim.x) {
     const double nc = a.Nc[c];
@@ -2155,6 +2231,63 @@ __global__ void __launch_bounds__(128) k_update(UpdateArgs a) {
       __syncthreads();
       if (!s_ok) continue;
       // solve per d and write (provisionally) -- all finite required
+      if constexpr (HM != 0) {
+        if (tid < H1) {
+          const double dd = sF[tid * H1 + tid];
+          s_dinv[tid] = fabs(dd) > DBL_MIN ? 1.0 / dd : 0.0;
+        }
+        if (tid == 0) {
+          for (int i = 0; i < H1; ++i) s_idx[i] = i;
+          for (int k = 0; k < H1; ++k) {
+            const int p = s_perm[k], t = s_idx[k];
+            s_idx[k] = s_idx[p];
+            s_idx[p] = t;
+          }
+        }
+        __syncthreads();
+        const double* Yc = a.Y + (int64_t)c * H1 * D;
+        for (int d = tid; d < D; d += blockDim.x) {
+          double b[HM];
+#pragma unroll
+          for (int i = 0; i < HM; ++i) b[i] = i < H1 ? Yc[(int64_t)s_idx[i] * D + d] : 0.0;  // P b
+#pragma unroll
+          for (int i = 0; i < HM; ++i)  // L^-1
+            if (i < H1) {
+              double t = b[i];
+#pragma unroll
+              for (int j = 0; j < i; ++j) t -= sF[j * H1 + i] * b[j];
+              b[i] = t;
+            }
+#pragma unroll
+          for (int i = 0; i < HM; ++i)  // D^+ (reciprocals formed once per component)
+            if (i < H1) b[i] *= s_dinv[i];
+#pragma unroll
+          for (int i = HM - 1; i >= 0; --i)  // L^-T
+            if (i < H1) {
+              double t = b[i];
+#pragma unroll
+              for (int j = i + 1; j < HM; ++j)
+                if (j < H1) t -= sF[i * H1 + j] * b[j];
+              b[i] = t;
+            }
+#pragma unroll
+          for (int i = 0; i < HM; ++i)  // P^T
+            if (i < H1) s_x[s_idx[i] * blockDim.x + tid] = b[i];
+          bool fin = true;
+          double fitted = 0.0;
+#pragma unroll
+          for (int h = 0; h < HM; ++h)
+            if (h < H1) {
+              const double x = s_x[h * blockDim.x + tid];
+              fin &= isfinite(x);
+              fitted += Yc[(int64_t)h * D + d] * x;
+              if (h < H) a.lam[(int64_t)c * D * H + (int64_t)h * D + d] = x;
+              else a.mu[(int64_t)c * D + d] = x;
+            }
+          if (!fin) s_fin = 0;
+          a.psi[(int64_t)c * D + d] = fmax((a.sq[(int64_t)c * D + d] - fitted) / nc, a.floor[d]);
+        }
+      } else
       for (int d = tid; d < D; d += blockDim.x) {
         double b[kMaxH1];
         for (int h = 0; h < H1; ++h) b[h] = a.Y[((int64_t)c * H1 + h) * D + d];
@@ -2206,27 +2339,35 @@ __global__ void __launch_bounds__(1024) k_renorm(Dims dm, double* pi, unsigned l
 constexpr int kPreFastH = 8;  // precompute's register-blocked M for H <= 8
 constexpr int kPreDC = 32;    // dimensions per staged chunk of the general-H path
 
+template <int HM>
 __global__ void __launch_bounds__(128) k_precompute(PrecompArgs a) {
   extern __shared__ __align__(16) double s_pre[];
   __shared__ double red[128];
   __shared__ double s_mpart[4][kPreFastH * (kPreFastH + 1) / 2];
+  __shared__ double s_ipc[kPreDC];
   __shared__ int s_ok;
   const Dims dm = a.dm;
   const int H = dm.H, D = dm.D;
   double* sL = s_pre;
   double* sR = s_pre + H * H;
-  // general H: staged chunks of kPreDC dimensions (H4 x kPreDC each)
+  // H > kPreFastH: staged chunks of kPreDC dimensions (H4 x kPreDC each) and
+  // the per-slice partial 4x4 tiles of M
   const int H4 = (H + 3) & ~3;
   double* sA = s_pre + 2 * H * H;
   double* sB = sA + H4 * kPreDC;
+  double* sP = sB + H4 * kPreDC;
+  const int NT = H4 / 4, ntile = NT * (NT + 1) / 2;
+  const int nsl = max(1, static_cast<int>(blockDim.x) / ntile);  // dimension slices per tile
   const int tid = threadIdx.x;
   for (int c = blockIdx.x; c < dm.C; c += gridDim.x) {
     const double* lam = a.lam + (int64_t)c * D * H;
     const double* psi = a.psi + (int64_t)c * D;
     // M = Lambda^T Psi^-1 Lambda (+I), symmetrised (model.cpp:51-53): every
     // thread sums its dimensions for all upper entries (H <= kPreFastH), then
-    // a warp-shuffle + fixed-order cross-warp reduction; else one entry per thread
-    if (H <= kPreFastH) {
+    // a warp-shuffle + fixed-order cross-warp reduction; else 4x4 register
+    // tiles of the upper triangle, each tile's dimensions split over nsl
+    // threads (slices), the slice partials summed in a fixed order
+    if constexpr (HM == kPreFastH) {
       const int np = H * (H + 1) / 2;
       double acc[kPreFastH * (kPreFastH + 1) / 2];
 #pragma unroll
@@ -2264,14 +2405,16 @@ __global__ void __launch_bounds__(128) k_precompute(PrecompArgs a) {
         sL[jj * H + ii] = v;
       }
     } else {
-      // 4x4 register tiles of the upper triangle over staged chunks of
-      // Lambda and Psi^-1 Lambda (rounds of 128 tiles)
-      const int NT = H4 / 4, ntile = NT * (NT + 1) / 2;
-      for (int t0 = 0; t0 < ntile; t0 += blockDim.x) {
-        int bi = -1, bj = -1;
-        for (int t = t0 + tid, i = 0; i < NT && bi < 0 && t0 + tid < ntile; ++i) {
-          if (t < NT - i) bi = i, bj = i + t;
-          else t -= NT - i;
+      const int nwork = ntile * nsl;
+      for (int t0 = 0; t0 < nwork; t0 += blockDim.x) {
+        const int t = t0 + tid;
+        const bool act = t < nwork;
+        const int tile = t % ntile, sl = t / ntile;
+        int bi = 0, bj = 0;
+        {
+          int r = tile;
+          while (r >= NT - bi) r -= NT - bi, ++bi;
+          bj = bi + r;
         }
         double acc[4][4];
 #pragma unroll
@@ -2280,15 +2423,17 @@ __global__ void __launch_bounds__(128) k_precompute(PrecompArgs a) {
           for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
         for (int d0 = 0; d0 < D; d0 += kPreDC) {
           __syncthreads();
+          if (tid < kPreDC) s_ipc[tid] = d0 + tid < D ? 1.0 / psi[d0 + tid] : 0.0;
+          __syncthreads();
           for (int i = tid; i < H4 * kPreDC; i += blockDim.x) {
-            const int h = i / kPreDC, d = d0 + (i - h * kPreDC);
+            const int h = i / kPreDC, dd = i - h * kPreDC, d = d0 + dd;
             const double v = (h < H && d < D) ? lam[(int64_t)h * D + d] : 0.0;
             sA[i] = v;
-            sB[i] = d < D ? v * (1.0 / psi[d]) : 0.0;
+            sB[i] = v * s_ipc[dd];
           }
           __syncthreads();
-          if (bi >= 0) {
-            for (int dd = 0; dd < kPreDC; ++dd) {
+          if (act) {
+            for (int dd = sl; dd < kPreDC; dd += nsl) {
               double av[4], bv[4];
 #pragma unroll
               for (int k = 0; k < 4; ++k) {
@@ -2302,15 +2447,24 @@ __global__ void __launch_bounds__(128) k_precompute(PrecompArgs a) {
             }
           }
         }
-        if (bi >= 0) {
+        if (act)
 #pragma unroll
           for (int i = 0; i < 4; ++i)
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              const int ii = 4 * bi + i, jj = 4 * bj + j;
-              if (ii < H && jj < H && ii <= jj) sL[jj * H + ii] = acc[i][j];
-            }
+            for (int j = 0; j < 4; ++j) sP[((int64_t)sl * ntile + tile) * 16 + i * 4 + j] = acc[i][j];
+        __syncthreads();
+        // this round's tiles: all of them (nsl > 1: one round) or [t0, t0 + blockDim)
+        const int tlo = nsl > 1 ? 0 : t0, thi = nsl > 1 ? ntile : min(ntile, t0 + static_cast<int>(blockDim.x));
+        for (int e = tid; e < (thi - tlo) * 16; e += blockDim.x) {
+          const int tl = tlo + e / 16, ij = e % 16;
+          double v = 0.0;
+          for (int s2 = 0; s2 < nsl; ++s2) v += sP[((int64_t)s2 * ntile + tl) * 16 + ij];
+          int ti = 0, r = tl;
+          while (r >= NT - ti) r -= NT - ti, ++ti;
+          const int ii = 4 * ti + ij / 4, jj = 4 * (ti + r) + ij % 4;
+          if (ii < H && jj < H && ii <= jj) sL[jj * H + ii] = v;
         }
+        __syncthreads();
       }
     }
     __syncthreads();
@@ -2346,10 +2500,20 @@ __global__ void __launch_bounds__(128) k_precompute(PrecompArgs a) {
     for (int p = tid; p < H * H; p += blockDim.x) a.R[(int64_t)c * H * H + p] = sR[p];
     // Sigma_z = L^-1 (model.cpp:65)
     for (int j = tid; j < H; j += blockDim.x) {
-      double b[kMaxH1];
-      for (int h = 0; h < H; ++h) b[h] = h == j ? 1.0 : 0.0;
-      chol_solve_thread(sR, b, H);
-      for (int h = 0; h < H; ++h) a.Sz[(int64_t)c * H * H + j * H + h] = b[h];
+      if constexpr (HM != 0) {
+        double b[HM];
+#pragma unroll
+        for (int h = 0; h < HM; ++h) b[h] = h == j ? 1.0 : 0.0;
+        chol_solve_thread_t<HM>(sR, b, H);
+#pragma unroll
+        for (int h = 0; h < HM; ++h)
+          if (h < H) a.Sz[(int64_t)c * H * H + j * H + h] = b[h];
+      } else {
+        double b[kMaxH1];
+        for (int h = 0; h < H; ++h) b[h] = h == j ? 1.0 : 0.0;
+        chol_solve_thread(sR, b, H);
+        for (int h = 0; h < H; ++h) a.Sz[(int64_t)c * H * H + j * H + h] = b[h];
+      }
     }
     // log|Sigma| (model.cpp:67-70): deterministic block reduction of sum log psi
     double s = 0.0;
@@ -2372,48 +2536,55 @@ __global__ void __launch_bounds__(128) k_precompute(PrecompArgs a) {
     }
     // fp32 scoring rows: W = U R^-T (P, WT) and V = R^-T W (V32) per dimension
     const int HP = a.L.HP, Hc = a.L.Hc;
-    auto write_rows = [&](int d, const double* u, double ip) {
-      float* row = a.P + ((int64_t)c * D + d) * HP;
-      for (int h = 0; h < Hc; ++h) row[h] = h < H ? static_cast<float>(u[h]) : 0.f;
-      // K-major copy for the tensor-core scorer: WT[c][h][d], h < Hp (zero padded)
-      for (int h = 0; h < a.Hp; ++h) a.WT[((int64_t)c * a.Hp + h) * D + d] = h < H ? static_cast<float>(u[h]) : 0.f;
-      if (a.W64)
-        for (int h = 0; h < H; ++h) a.W64[((int64_t)c * H + h) * D + d] = u[h];
-      a.ipsi32[(int64_t)c * D + d] = static_cast<float>(ip);
-      row[Hc] = static_cast<float>(a.mu[(int64_t)c * D + d]);
-      row[Hc + 1] = static_cast<float>(ip);
-      row[Hc + 2] = 0.f;
-      row[Hc + 3] = 0.f;
-      a.mu32[(int64_t)c * D + d] = static_cast<float>(a.mu[(int64_t)c * D + d]);
-    };
-    if (H <= kPreFastH) {  // compile-time loops: the solves stay in registers
+    if constexpr (HM != 0) {  // compile-time loops: the solves and rows stay in registers
+      __shared__ double s_rinv[HM];
+      if (tid < H) s_rinv[tid] = 1.0 / sR[tid * H + tid];
+      __syncthreads();
       for (int d = tid; d < D; d += blockDim.x) {
-        double u[kPreFastH];
+        double u[HM];
         const double ip = 1.0 / psi[d];
 #pragma unroll
-        for (int h = 0; h < kPreFastH; ++h) u[h] = h < H ? lam[(int64_t)h * D + d] * ip : 0.0;  // U = Psi^-1 Lambda
+        for (int h = 0; h < HM; ++h) u[h] = h < H ? lam[(int64_t)h * D + d] * ip : 0.0;  // U = Psi^-1 Lambda
 #pragma unroll
-        for (int i = 0; i < kPreFastH; ++i) {  // forward: w = R^-1 u
+        for (int i = 0; i < HM; ++i) {  // forward: w = R^-1 u
           if (i < H) {
             double t = u[i];
 #pragma unroll
             for (int k = 0; k < i; ++k) t -= sR[i * H + k] * u[k];
-            u[i] = t / sR[i * H + i];
+            u[i] = t * s_rinv[i];
           }
         }
-        write_rows(d, u, ip);
+        // fp32 scoring rows of dimension d (write_rows with compile-time indices)
+        float* row = a.P + ((int64_t)c * D + d) * HP;
 #pragma unroll
-        for (int i = kPreFastH - 1; i >= 0; --i) {  // backward: v = R^-T w => V column d
+        for (int h = 0; h < HM; ++h)
+          if (h < H) {
+            const float f = static_cast<float>(u[h]);
+            row[h] = f;
+            a.WT[((int64_t)c * a.Hp + h) * D + d] = f;
+            if (a.W64) a.W64[((int64_t)c * H + h) * D + d] = u[h];
+          }
+        for (int h = H; h < Hc; ++h) row[h] = 0.f;
+        for (int h = H; h < a.Hp; ++h) a.WT[((int64_t)c * a.Hp + h) * D + d] = 0.f;
+        const double mud = a.mu[(int64_t)c * D + d];
+        a.ipsi32[(int64_t)c * D + d] = static_cast<float>(ip);
+        row[Hc] = static_cast<float>(mud);
+        row[Hc + 1] = static_cast<float>(ip);
+        row[Hc + 2] = 0.f;
+        row[Hc + 3] = 0.f;
+        a.mu32[(int64_t)c * D + d] = static_cast<float>(mud);
+#pragma unroll
+        for (int i = HM - 1; i >= 0; --i) {  // backward: v = R^-T w => V column d
           if (i < H) {
             double t = u[i];
 #pragma unroll
-            for (int k = i + 1; k < kPreFastH; ++k)
+            for (int k = i + 1; k < HM; ++k)
               if (k < H) t -= sR[k * H + i] * u[k];
-            u[i] = t / sR[i * H + i];
+            u[i] = t * s_rinv[i];
           }
         }
 #pragma unroll
-        for (int h = 0; h < kPreFastH; ++h)
+        for (int h = 0; h < HM; ++h)
           if (h < H) a.V32[((int64_t)c * D + d) * H + h] = static_cast<float>(u[h]);
       }
     } else {
@@ -2898,8 +3069,8 @@ cudaError_t launch_score(int mode, const ScoreArgs& a, int grid, cudaStream_t s)
 cudaError_t launch_select(const SelectArgs& a, cudaStream_t s) {
   const int ns = (a.dm.SL + 31) / 32;
   const int grid = grid_for(a.dm.N * 32, 256, sm_count() * 16);
-  // 8 warps' bitmaps + their anchor log-joints
-  const size_t smem = static_cast<size_t>((a.dm.C + 31) / 32) * 8 * sizeof(unsigned) + 64 * sizeof(float);
+  // 8 warps' bitmaps + their anchor log-joints and ranks
+  const size_t smem = static_cast<size_t>((a.dm.C + 31) / 32) * 8 * sizeof(unsigned) + 64 * (sizeof(float) + sizeof(int));
   if (smem > 200 * 1024) return cudaErrorInvalidValue;
   auto go = [&](auto kern) {
     if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
@@ -3119,9 +3290,16 @@ extern "C" int vmfa_diag_stats_cycles(int enable, unsigned long long* out) {
 namespace vmfa_b200 {
 cudaError_t launch_update(const UpdateArgs& a, cudaStream_t s) {
   const int H1 = a.dm.H + 1;
-  const size_t smem = 2 * static_cast<size_t>(H1) * H1 * sizeof(double);
-  cudaFuncSetAttribute(k_update, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-  k_update<<<min(a.dm.C, sm_count() * 8), 128, smem, s>>>(a);
+  const size_t smem = (2 * static_cast<size_t>(H1) * H1 + static_cast<size_t>(H1) * 128) * sizeof(double);
+  auto go = [&](auto kern) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    kern<<<min(a.dm.C, sm_count() * 8), 128, smem, s>>>(a);
+  };
+  if (H1 <= 5) go(k_update<5>);
+  else if (H1 <= 9) go(k_update<9>);
+  else if (H1 <= 17) go(k_update<17>);
+  else if (H1 <= 33) go(k_update<33>);
+  else go(k_update<0>);
   return cudaGetLastError();
 }
 cudaError_t launch_renorm(const Dims& dm, double* pi, unsigned long long* status, cudaStream_t s) {
@@ -3129,11 +3307,19 @@ cudaError_t launch_renorm(const Dims& dm, double* pi, unsigned long long* status
   return cudaGetLastError();
 }
 cudaError_t launch_precompute(const PrecompArgs& a, cudaStream_t s) {
-  const size_t H4 = (static_cast<size_t>(a.dm.H) + 3) & ~size_t{3};
-  const size_t smem = (2 * static_cast<size_t>(a.dm.H) * a.dm.H +
-                       (a.dm.H > kPreFastH ? 2 * H4 * kPreDC : 0)) * sizeof(double);
-  cudaFuncSetAttribute(k_precompute, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-  k_precompute<<<min(a.dm.C, sm_count() * 8), 128, smem, s>>>(a);
+  const int H = a.dm.H;
+  const size_t H4 = (static_cast<size_t>(H) + 3) & ~size_t{3};
+  const size_t NT = H4 / 4, ntile = NT * (NT + 1) / 2, nsl = ntile < 128 ? 128 / ntile : 1;
+  const size_t smem = (2 * static_cast<size_t>(H) * H +
+                       (H > kPreFastH ? 2 * H4 * kPreDC + nsl * ntile * 16 : 0)) * sizeof(double);
+  auto go = [&](auto kern) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    kern<<<min(a.dm.C, sm_count() * 8), 128, smem, s>>>(a);
+  };
+  if (H <= kPreFastH) go(k_precompute<kPreFastH>);
+  else if (H <= 16) go(k_precompute<16>);
+  else if (H <= 32) go(k_precompute<32>);
+  else go(k_precompute<0>);
   return cudaGetLastError();
 }
 cudaError_t launch_caches_full(const Dims& dm, const double* lam, const double* psi, const double* R,

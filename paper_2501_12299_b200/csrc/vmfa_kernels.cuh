@@ -22,7 +22,7 @@ constexpr int kScoreThreads = 128;  // 4 warps; each warp scores one component x
 constexpr int kXsStride = kScoreRows + 2;  // transposed x tile stride (floats)
 constexpr int kStatsThreads = 256;
 constexpr int kGupdCap = 8192;      // smem hash capacity of the block-3 accumulator (24 B per entry)
-constexpr int kGupdThreads = 256;
+constexpr int kGupdThreads = 512;
 constexpr int kGupdRowsCap = 2048;  // hash of an item that adds into the dense rows (overflow goes to xc)
 
 // Packed fp32 scoring parameters of one component (precompute output):
@@ -367,13 +367,13 @@ cudaError_t launch_lse_dense(const float* LJ, int64_t R, int SL, int C, double* 
 int64_t ws_record_floats(const Dims& dm, int single);
 cudaError_t launch_ws_records(const Dims& dm, int single, const float* WT, const float* mu32, const float* ipsi32,
                               const double* kconst, const int* g, const int* gcnt, const float* scl, float* rec,
-                              cudaStream_t s);
+                              cudaStream_t s, int fused = 0);
 // B stage images (single != 0: one component per job), sizes in halves / floats
 int64_t ws_image_halves(const Dims& dm, int single);
 int64_t ws_scale_floats(const Dims& dm, int single);
 cudaError_t launch_ws_images(const Dims& dm, int single, const float* WT, const float* mu32, const float* ipsi32,
                              const int* g, const int* gcnt, void* img, float* bscl, cudaStream_t s,
-                             const float* sscl = nullptr);
+                             const float* sscl = nullptr, float* rec = nullptr);
 // per-row max |value| of an N x D fp32 matrix (A-row scale bounds)
 cudaError_t launch_rowmax(int64_t N, int D, const float* X, float* xmax, cudaStream_t s);
 

@@ -772,7 +772,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_ws(WsArgs a, const __grid
 __global__ void __launch_bounds__(256) k_build_records(Dims dm, int Hp, int qg, int ngroups, int N1max, int single,
                                                        const float* WT, const float* mu32, const float* ipsi32,
                                                        const double* kconst, const int* g, const int* gcnt,
-                                                       const float* scl, float* rec) {
+                                                       const float* scl, float* rec, int fused) {
   const int lane = threadIdx.x & 31;
   const int R = rec_stride(Hp);
   const int nslot = single ? 1 : dm.G;
@@ -787,24 +787,35 @@ __global__ void __launch_bounds__(256) k_build_records(Dims dm, int Hp, int qg, 
     const int grp = single ? 0 : i / qg, qi = single ? 0 : i - grp * qg;
     const float* sr = scl + ((int64_t)c * ng + grp) * (N1max + kNL);
     double m = 0.0;
-    if (!single) {
+    if (fused) {
+      // m and b were written by k_build_images (anchor images)
+    } else if (!single) {
       const float* mq = mu32 + (int64_t)q * dm.D;
       const float* ma = mu32 + (int64_t)c * dm.D;
       const float* ip = ipsi32 + (int64_t)q * dm.D;
-      for (int d = lane; d < dm.D; d += 32) {
-        const float dlf = mq[d] - ma[d];  // same fp32 rounding as the scorer's operands
-        m += static_cast<double>(ip[d]) * static_cast<double>(dlf) * static_cast<double>(dlf);
+      // b in blocks of 8 latent rows (8 independent loads and fp64 sums per
+      // lane and dimension), m beside the first block; the products of two
+      // fp32 values are exact in fp64, so only the summation order is fixed here
+      for (int h0 = 0; h0 < Hp; h0 += 8) {
+        double sb[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+        const float* wr = WT + ((int64_t)q * Hp + h0) * dm.D;
+        for (int d = lane; d < dm.D; d += 32) {
+          const float dlf = mq[d] - ma[d];  // same fp32 rounding as the scorer's operands
+          const double dl = static_cast<double>(dlf);
+          if (h0 == 0) m += static_cast<double>(ip[d]) * dl * dl;
+#pragma unroll
+          for (int h = 0; h < 8; ++h)
+            if (h0 + h < Hp) sb[h] += static_cast<double>(__ldg(wr + (int64_t)h * dm.D + d)) * dl;
+        }
+#pragma unroll
+        for (int h = 0; h < 8; ++h) {
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) sb[h] += __shfl_xor_sync(0xffffffffu, sb[h], o);
+          if (lane == 0 && h0 + h < Hp) out[8 + h0 + h] = static_cast<float>(sb[h]);
+        }
       }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) m += __shfl_xor_sync(0xffffffffu, m, o);
-      for (int h = 0; h < Hp; ++h) {
-        const float* wr = WT + ((int64_t)q * Hp + h) * dm.D;
-        double sb = 0.0;
-        for (int d = lane; d < dm.D; d += 32) sb += static_cast<double>(wr[d]) * static_cast<double>(mq[d] - ma[d]);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) sb += __shfl_xor_sync(0xffffffffu, sb, o);
-        if (lane == 0) out[8 + h] = static_cast<float>(sb);
-      }
     } else {
       for (int h = lane; h < Hp; h += 32) out[8 + h] = 0.f;
     }
@@ -814,7 +825,7 @@ __global__ void __launch_bounds__(256) k_build_records(Dims dm, int Hp, int qg, 
       const float hi = static_cast<float>(kc);
       out[0] = __int_as_float(q);
       out[1] = hi;
-      out[2] = static_cast<float>(m);
+      if (!fused) out[2] = static_cast<float>(m);
       out[3] = sr[qi];
       out[4] = sr[N1max + qi];
       out[5] = isfinite(kc) ? static_cast<float>(kc - static_cast<double>(hi)) : 0.f;
@@ -834,7 +845,7 @@ __global__ void __launch_bounds__(256) k_build_records(Dims dm, int Hp, int qg, 
 __global__ void __launch_bounds__(256) k_build_images(Dims dm, int Hp, int qg, int ngroups, int N1max, int single,
                                                       const float* WT, const float* mu32, const float* ipsi32,
                                                       const int* g, const int* gcnt, __half* img, float* bscl,
-                                                      const float* sscl, int N1max1) {
+                                                      const float* sscl, int N1max1, float* rec) {
   const int lane = threadIdx.x & 31;
   const int nchunk = (dm.D + kKC - 1) / kKC;
   const int ng = single ? 1 : ngroups;
@@ -923,10 +934,26 @@ __global__ void __launch_bounds__(256) k_build_images(Dims dm, int Hp, int qg, i
     const int64_t off_hi = row < N1max ? 0 : 2 * (int64_t)N1max * 64;
     const int64_t off_lo = row < N1max ? (int64_t)N1max * 64 : 2 * (int64_t)N1max * 64 + kNL * 64;
     __half* base = img + ((int64_t)a * ng + grp) * nchunk * stage_h;
+    // rec != null (anchor images): the record sums ride along -- a W row h of
+    // q gives b_h = sum_d W_q[h][d] (mu_q - mu_a)[d], the psi row of q gives
+    // m = sum_d psi_q^-1 (mu_q - mu_a)^2 (fp32 differences as the scorer's
+    // operands, exact fp32 products, fp64 sums); k_build_records skips them
+    const bool sums = rec != nullptr && (kind == 2 || kind == 3);
+    double acc = 0.0;
     for (int u = lane; u < nchunk * (kKC / 8); u += 32) {  // one 16-byte unit (8 halves) per lane
       const int ch = u / (kKC / 8), j = u - ch * (kKC / 8);
       float v[8];
       load8(ch * kKC + 8 * j, v);
+      if (sums) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int d = ch * kKC + 8 * j + i;
+          if (d < dm.D) {
+            const double dl = static_cast<double>(mq[d] - ma[d]);
+            acc += kind == 2 ? static_cast<double>(v[i]) * dl : static_cast<double>(v[i]) * dl * dl;
+          }
+        }
+      }
       uint32_t hw[4], lw[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i) split2(v[2 * i] * sc, v[2 * i + 1] * sc, hw[i], lw[i]);
@@ -934,6 +961,16 @@ __global__ void __launch_bounds__(256) k_build_images(Dims dm, int Hp, int qg, i
       __half* st = base + ch * stage_h;
       *reinterpret_cast<uint4*>(st + off_hi + pos) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
       *reinterpret_cast<uint4*>(st + off_lo + pos) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+    }
+    if (sums) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (lane == 0) {
+        const int qi = kind == 2 ? (row - kNL) / Hp : row - N1max;
+        float* out = rec + ((int64_t)a * dm.G + slot0 + qi) * rec_stride(Hp);
+        if (kind == 2) out[8 + h] = static_cast<float>(acc);
+        else out[2] = static_cast<float>(acc);
+      }
     }
   }
 }
@@ -994,20 +1031,20 @@ int64_t ws_record_floats(const Dims& dm, int single) {
 
 cudaError_t launch_ws_images(const Dims& dm, int single, const float* WT, const float* mu32, const float* ipsi32,
                              const int* g, const int* gcnt, void* img, float* bscl, cudaStream_t s,
-                             const float* sscl) {
+                             const float* sscl, float* rec) {
   k_build_images<<<sm_count() * 8, 256, 0, s>>>(dm, ws_hp(dm.H), ws_qg(dm, single), ws_groups(dm),
                                                 ws_n1max(dm, single), single, WT, mu32, ipsi32, g, gcnt,
                                                 static_cast<__half*>(img), bscl, single ? nullptr : sscl,
-                                                ws_n1max(dm, 1));
+                                                ws_n1max(dm, 1), single ? nullptr : rec);
   return cudaGetLastError();
 }
 
 cudaError_t launch_ws_records(const Dims& dm, int single, const float* WT, const float* mu32, const float* ipsi32,
                               const double* kconst, const int* g, const int* gcnt, const float* scl, float* rec,
-                              cudaStream_t s) {
+                              cudaStream_t s, int fused) {
   k_build_records<<<sm_count() * 8, 256, 0, s>>>(dm, ws_hp(dm.H), ws_qg(dm, single), ws_groups(dm),
                                                  ws_n1max(dm, single), single, WT, mu32, ipsi32, kconst, g, gcnt,
-                                                 scl, rec);
+                                                 scl, rec, single ? 0 : fused);
   return cudaGetLastError();
 }
 
