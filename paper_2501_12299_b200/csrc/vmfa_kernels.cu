@@ -2344,7 +2344,6 @@ __global__ void __launch_bounds__(128) k_precompute(PrecompArgs a) {
   extern __shared__ __align__(16) double s_pre[];
   __shared__ double red[128];
   __shared__ double s_mpart[4][kPreFastH * (kPreFastH + 1) / 2];
-  __shared__ double s_ipc[kPreDC];
   __shared__ int s_ok;
   const Dims dm = a.dm;
   const int H = dm.H, D = dm.D;
@@ -2355,7 +2354,8 @@ __global__ void __launch_bounds__(128) k_precompute(PrecompArgs a) {
   const int H4 = (H + 3) & ~3;
   double* sA = s_pre + 2 * H * H;
   double* sB = sA + H4 * kPreDC;
-  double* sP = sB + H4 * kPreDC;
+  double* s_ip = sA;  // Psi^-1 of the component (M stage; overlays sA / sB)
+  double* sP = sA + max(2 * H4 * kPreDC, D);
   const int NT = H4 / 4, ntile = NT * (NT + 1) / 2;
   const int nsl = max(1, static_cast<int>(blockDim.x) / ntile);  // dimension slices per tile
   const int tid = threadIdx.x;
@@ -2406,13 +2406,15 @@ __global__ void __launch_bounds__(128) k_precompute(PrecompArgs a) {
       }
     } else {
       const int nwork = ntile * nsl;
+      for (int d = tid; d < D; d += blockDim.x) s_ip[d] = 1.0 / psi[d];
+      __syncthreads();
       for (int t0 = 0; t0 < nwork; t0 += blockDim.x) {
         const int t = t0 + tid;
         const bool act = t < nwork;
-        const int tile = t % ntile, sl = t / ntile;
+        const int sl = t % nsl, tile = t / nsl;  // a tile's slices adjacent: neighbouring dimensions per warp
         int bi = 0, bj = 0;
         {
-          int r = tile;
+          int r = act ? tile : 0;
           while (r >= NT - bi) r -= NT - bi, ++bi;
           bj = bi + r;
         }
@@ -2421,30 +2423,39 @@ __global__ void __launch_bounds__(128) k_precompute(PrecompArgs a) {
         for (int i = 0; i < 4; ++i)
 #pragma unroll
           for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
-        for (int d0 = 0; d0 < D; d0 += kPreDC) {
-          __syncthreads();
-          if (tid < kPreDC) s_ipc[tid] = d0 + tid < D ? 1.0 / psi[d0 + tid] : 0.0;
-          __syncthreads();
-          for (int i = tid; i < H4 * kPreDC; i += blockDim.x) {
-            const int h = i / kPreDC, dd = i - h * kPreDC, d = d0 + dd;
-            const double v = (h < H && d < D) ? lam[(int64_t)h * D + d] : 0.0;
-            sA[i] = v;
-            sB[i] = v * s_ipc[dd];
-          }
-          __syncthreads();
-          if (act) {
-            for (int dd = sl; dd < kPreDC; dd += nsl) {
-              double av[4], bv[4];
+        if (act) {
+          // straight from global memory (no staging barriers), 2 dimensions in flight
+          const double* la = lam + (int64_t)(4 * bi) * D;
+          const double* lb = lam + (int64_t)(4 * bj) * D;
+          int d = sl;
+          for (; d + nsl < D; d += 2 * nsl) {
+            double av[2][4], bv[2][4];
+#pragma unroll
+            for (int e = 0; e < 2; ++e)
 #pragma unroll
               for (int k = 0; k < 4; ++k) {
-                av[k] = sA[(4 * bi + k) * kPreDC + dd];
-                bv[k] = sB[(4 * bj + k) * kPreDC + dd];
+                const int dd = d + e * nsl;
+                av[e][k] = 4 * bi + k < H ? la[(int64_t)k * D + dd] : 0.0;
+                bv[e][k] = 4 * bj + k < H ? lb[(int64_t)k * D + dd] * s_ip[dd] : 0.0;
               }
+#pragma unroll
+            for (int e = 0; e < 2; ++e)
 #pragma unroll
               for (int i = 0; i < 4; ++i)
 #pragma unroll
-                for (int j = 0; j < 4; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
+                for (int j = 0; j < 4; ++j) acc[i][j] = fma(av[e][i], bv[e][j], acc[i][j]);
+          }
+          for (; d < D; d += nsl) {
+            double av[4], bv[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              av[k] = 4 * bi + k < H ? la[(int64_t)k * D + d] : 0.0;
+              bv[k] = 4 * bj + k < H ? lb[(int64_t)k * D + d] * s_ip[d] : 0.0;
             }
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+              for (int j = 0; j < 4; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
           }
         }
         if (act)
@@ -2536,57 +2547,8 @@ __global__ void __launch_bounds__(128) k_precompute(PrecompArgs a) {
     }
     // fp32 scoring rows: W = U R^-T (P, WT) and V = R^-T W (V32) per dimension
     const int HP = a.L.HP, Hc = a.L.Hc;
-    if constexpr (HM != 0) {  // compile-time loops: the solves and rows stay in registers
-      __shared__ double s_rinv[HM];
-      if (tid < H) s_rinv[tid] = 1.0 / sR[tid * H + tid];
-      __syncthreads();
-      for (int d = tid; d < D; d += blockDim.x) {
-        double u[HM];
-        const double ip = 1.0 / psi[d];
-#pragma unroll
-        for (int h = 0; h < HM; ++h) u[h] = h < H ? lam[(int64_t)h * D + d] * ip : 0.0;  // U = Psi^-1 Lambda
-#pragma unroll
-        for (int i = 0; i < HM; ++i) {  // forward: w = R^-1 u
-          if (i < H) {
-            double t = u[i];
-#pragma unroll
-            for (int k = 0; k < i; ++k) t -= sR[i * H + k] * u[k];
-            u[i] = t * s_rinv[i];
-          }
-        }
-        // fp32 scoring rows of dimension d (write_rows with compile-time indices)
-        float* row = a.P + ((int64_t)c * D + d) * HP;
-#pragma unroll
-        for (int h = 0; h < HM; ++h)
-          if (h < H) {
-            const float f = static_cast<float>(u[h]);
-            row[h] = f;
-            a.WT[((int64_t)c * a.Hp + h) * D + d] = f;
-            if (a.W64) a.W64[((int64_t)c * H + h) * D + d] = u[h];
-          }
-        for (int h = H; h < Hc; ++h) row[h] = 0.f;
-        for (int h = H; h < a.Hp; ++h) a.WT[((int64_t)c * a.Hp + h) * D + d] = 0.f;
-        const double mud = a.mu[(int64_t)c * D + d];
-        a.ipsi32[(int64_t)c * D + d] = static_cast<float>(ip);
-        row[Hc] = static_cast<float>(mud);
-        row[Hc + 1] = static_cast<float>(ip);
-        row[Hc + 2] = 0.f;
-        row[Hc + 3] = 0.f;
-        a.mu32[(int64_t)c * D + d] = static_cast<float>(mud);
-#pragma unroll
-        for (int i = HM - 1; i >= 0; --i) {  // backward: v = R^-T w => V column d
-          if (i < H) {
-            double t = u[i];
-#pragma unroll
-            for (int k = i + 1; k < HM; ++k)
-              if (k < H) t -= sR[k * H + i] * u[k];
-            u[i] = t * s_rinv[i];
-          }
-        }
-#pragma unroll
-        for (int h = 0; h < HM; ++h)
-          if (h < H) a.V32[((int64_t)c * D + d) * H + h] = static_cast<float>(u[h]);
-      }
+    if constexpr (HM != 0) {
+      // the per-dimension rows: k_precompute_rows (fully parallel over (c, d))
     } else {
       // W^T = R^-1 U^T and V = Sigma_z U^T (= L^-1 U^T, model.cpp:64) as
       // register-tiled products over staged chunks of U^T = (Psi^-1 Lambda)^T:
@@ -2667,6 +2629,71 @@ __global__ void __launch_bounds__(128) k_precompute(PrecompArgs a) {
       }
     }
     __syncthreads();
+  }
+}
+
+// The fp32 scoring rows of k_precompute for H <= HM, a thread per (c, d): U =
+// Psi^-1 Lambda, w = R^-1 u (P, WT, W64), v = R^-T w = Sigma_z u (V32), with
+// the solves in registers (reciprocal diagonals) -- the per-component kernel
+// above only forms L, R, Sigma_z and the constants.
+template <int HM>
+__global__ void __launch_bounds__(128) k_precompute_rows(PrecompArgs a) {
+  __shared__ double sR[HM * HM];
+  __shared__ double s_rinv[HM];
+  const Dims dm = a.dm;
+  const int H = dm.H, D = dm.D, c = blockIdx.y, tid = threadIdx.x;
+  const int HP = a.L.HP, Hc = a.L.Hc;
+  for (int p = tid; p < H * H; p += blockDim.x) sR[p] = a.R[(int64_t)c * H * H + p];
+  __syncthreads();
+  if (tid < H) s_rinv[tid] = 1.0 / sR[tid * H + tid];
+  __syncthreads();
+  const double* lam = a.lam + (int64_t)c * D * H;
+  const double* psi = a.psi + (int64_t)c * D;
+  for (int d = blockIdx.x * blockDim.x + tid; d < D; d += gridDim.x * blockDim.x) {
+    double u[HM];
+    const double ip = 1.0 / psi[d];
+#pragma unroll
+    for (int h = 0; h < HM; ++h) u[h] = h < H ? lam[(int64_t)h * D + d] * ip : 0.0;  // U = Psi^-1 Lambda
+#pragma unroll
+    for (int i = 0; i < HM; ++i) {  // forward: w = R^-1 u
+      if (i < H) {
+        double t = u[i];
+#pragma unroll
+        for (int k = 0; k < i; ++k) t -= sR[i * H + k] * u[k];
+        u[i] = t * s_rinv[i];
+      }
+    }
+    float* row = a.P + ((int64_t)c * D + d) * HP;
+#pragma unroll
+    for (int h = 0; h < HM; ++h)
+      if (h < H) {
+        const float f = static_cast<float>(u[h]);
+        row[h] = f;
+        a.WT[((int64_t)c * a.Hp + h) * D + d] = f;
+        if (a.W64) a.W64[((int64_t)c * H + h) * D + d] = u[h];
+      }
+    for (int h = H; h < Hc; ++h) row[h] = 0.f;
+    for (int h = H; h < a.Hp; ++h) a.WT[((int64_t)c * a.Hp + h) * D + d] = 0.f;
+    const double mud = a.mu[(int64_t)c * D + d];
+    a.ipsi32[(int64_t)c * D + d] = static_cast<float>(ip);
+    row[Hc] = static_cast<float>(mud);
+    row[Hc + 1] = static_cast<float>(ip);
+    row[Hc + 2] = 0.f;
+    row[Hc + 3] = 0.f;
+    a.mu32[(int64_t)c * D + d] = static_cast<float>(mud);
+#pragma unroll
+    for (int i = HM - 1; i >= 0; --i) {  // backward: v = R^-T w => V column d
+      if (i < H) {
+        double t = u[i];
+#pragma unroll
+        for (int k = i + 1; k < HM; ++k)
+          if (k < H) t -= sR[k * H + i] * u[k];
+        u[i] = t * s_rinv[i];
+      }
+    }
+#pragma unroll
+    for (int h = 0; h < HM; ++h)
+      if (h < H) a.V32[((int64_t)c * D + d) * H + h] = static_cast<float>(u[h]);
   }
 }
 
@@ -3311,15 +3338,19 @@ cudaError_t launch_precompute(const PrecompArgs& a, cudaStream_t s) {
   const size_t H4 = (static_cast<size_t>(H) + 3) & ~size_t{3};
   const size_t NT = H4 / 4, ntile = NT * (NT + 1) / 2, nsl = ntile < 128 ? 128 / ntile : 1;
   const size_t smem = (2 * static_cast<size_t>(H) * H +
-                       (H > kPreFastH ? 2 * H4 * kPreDC + nsl * ntile * 16 : 0)) * sizeof(double);
-  auto go = [&](auto kern) {
+                       (H > kPreFastH ? std::max<size_t>(2 * H4 * kPreDC, a.dm.D) + nsl * ntile * 16 : 0)) *
+                      sizeof(double);
+  const dim3 rgrid((a.dm.D + 127) / 128, a.dm.C);
+  auto go = [&](auto kern, auto rows) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     kern<<<min(a.dm.C, sm_count() * 8), 128, smem, s>>>(a);
+    if (rows) rows<<<rgrid, 128, 0, s>>>(a);
   };
-  if (H <= kPreFastH) go(k_precompute<kPreFastH>);
-  else if (H <= 16) go(k_precompute<16>);
-  else if (H <= 32) go(k_precompute<32>);
-  else go(k_precompute<0>);
+  using RowsK = void (*)(PrecompArgs);
+  if (H <= kPreFastH) go(k_precompute<kPreFastH>, static_cast<RowsK>(k_precompute_rows<kPreFastH>));
+  else if (H <= 16) go(k_precompute<16>, static_cast<RowsK>(k_precompute_rows<16>));
+  else if (H <= 32) go(k_precompute<32>, static_cast<RowsK>(k_precompute_rows<32>));
+  else go(k_precompute<0>, static_cast<RowsK>(nullptr));
   return cudaGetLastError();
 }
 cudaError_t launch_caches_full(const Dims& dm, const double* lam, const double* psi, const double* R,
