@@ -100,6 +100,7 @@ struct vmfa_ctx {
   unsigned char* svimg = nullptr;             // the tcgen05 statistics kernel's V images (per precompute)
   int* svexp = nullptr;
   float* svl1 = nullptr;
+  float* szbuf = nullptr;  // its zhat per K-pair (N C' x H)
   unsigned long long* nfix = nullptr;         // scores re-evaluated in fp64 (vmfa_fixup.cu), accumulated
   long long* fix_list = nullptr;              // flagged scores of one scoring launch
   unsigned long long* fix_cnt = nullptr;      // [count, overflow]
@@ -754,6 +755,7 @@ int stats_local(vmfa_ctx* x) {
   a.vimg = x->svimg;
   a.vexp = x->svexp;
   a.vl1 = x->svl1;
+  a.zbuf = x->szbuf;
   const int tok = x->begin(kFamStats, x->dm.N * x->dm.Cp);
   CU(launch_items_scan(x->kinv_off, x->dm.C, x->stats_rows, 0, x->stats_items, x->stream));
   CU(launch_stats(a, x->stats_items, x->stats_rows, x->stats_part, x->stream));
@@ -1134,7 +1136,7 @@ int vmfa_ctx_create(vmfa_ctx** out, int device, int C, int D, int H, int Cp, int
   A(x->part_items, Cs + 1);
   A(x->sit, 2);
   A(x->stats_items, Cs + 1);
-  A(x->qctr, 1);
+  A(x->qctr, 2);
   {
     const int64_t pairs = static_cast<int64_t>(N) * Cp;
     const int64_t target = (pairs + sm_count() * 8 - 1) / (sm_count() * 8);
@@ -1146,6 +1148,7 @@ int vmfa_ctx_create(vmfa_ctx** out, int device, int C, int D, int H, int Cp, int
       A(x->svimg, static_cast<size_t>(stats_tc_image_bytes(dm)));
       A(x->svexp, Cs * 16);
       A(x->svl1, Cs * 16);
+      A(x->szbuf, static_cast<size_t>(pairs) * H);
     }
     const int64_t max_items = C + (pairs + x->stats_rows - 1) / x->stats_rows;
     A(x->stats_part, static_cast<size_t>(max_items) * stats_part_stride(dm));

@@ -3216,11 +3216,7 @@ cudaError_t launch_stats(const StatsArgs& a, const int* itemoff, int rows_per_it
   const int H1 = a.dm.H + 1;
   const int nh1 = H1 <= 5 ? 5 : (H1 <= 9 ? 9 : kStatsMaxH1);
   const int64_t ps = stats_part_stride(a.dm);
-  if (a.xmax && a.mumax && rows_per_item == stats_tc_rows() && stats_use_tc(a.dm)) {
-    if (a.qctr) {
-      cudaError_t e = cudaMemsetAsync(a.qctr, 0, sizeof(int), s);
-      if (e != cudaSuccess) return e;
-    }
+  if (a.xmax && a.mumax && a.zbuf && a.qctr && rows_per_item == stats_tc_rows() && stats_use_tc(a.dm)) {
     cudaError_t e = launch_stats_tc(a, a.xmax, a.mumax, itemoff, nh1, part, ps, s);
     if (e != cudaSuccess) return e;
     k_stats_reduce<<<sm_count() * 8, 256, 0, s>>>(a.dm, itemoff, part, ps, 0, 0, nh1, 1, a.Nc, a.E, a.Y, a.sq);

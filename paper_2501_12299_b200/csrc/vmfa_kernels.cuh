@@ -170,6 +170,7 @@ struct StatsArgs {
   const void* vimg = nullptr;    // its GEMM i B images (launch_stats_vimg, per precompute)
   const int* vexp = nullptr;
   const float* vl1 = nullptr;
+  float* zbuf = nullptr;         // the tcgen05 kernel's zhat per K-pair (>= pairs x H floats)
 };
 // the tcgen05 statistics kernel takes the pass (opt-in: VMFA_STATS=tc)
 bool stats_use_tc(const Dims& dm);

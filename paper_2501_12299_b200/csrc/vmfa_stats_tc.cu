@@ -1,38 +1,41 @@
 // vmfa_stats_tc.cu — the sufficient statistics (accumulate_suffstats,
 // mstep.cpp:47-101) on the 5th-generation tensor cores.
 //
-// Per item (component c, <= 256 of its K-pairs (n, q)), centred rows
+// Per item (component c, <= kTItemRows of its K-pairs (n, q)), centred rows
 // v_n = x_n - mu_c (fp32 mu, as the other statistics kernels; k_stats_uncenter
-// restores the raw sums):
+// restores the raw sums), in tiles of kTRows = 48 rows:
 //   GEMM i   Z   [rows x HP]  = [v] (rows x D) . [V_c^T] (D x HP)     mz = V_c v
-//   GEMM ii  Y_v [D x N2]     = [v]^T (D x rows) . [q zhat] (rows x N2)
-// with zhat = [mz; 1], plus E = sum q zhat zhat^T in fp64 from the fp32 mz and
-// sq_v = sum q v^2 (fp64 shared-memory sums of fp32 partials) on the CUDA
-// cores. Both GEMMs are tcgen05.mma.kind::f16 in 3xFP16 (hi*hi + hi*lo +
-// lo*hi, 22 significant bits, fp32 accumulation in TMEM), SS form: one smem
-// copy of each 64-dimension chunk of split v serves GEMM i as a K-major A
-// (rows x dims) and GEMM ii as an MN-major A (dims x rows, two adjacent chunks
-// = M 128). Row n of v is scaled by 2^k_n (|v| <= 2^14 from the bound
-// max|x_n| + max|mu_c|) for GEMM i; GEMM ii sums over rows (its K), so
-// 2^-k_n is folded into its B operand (q zhat), exactly, and every column of
-// that operand gets a power-of-two scale from an a-priori bound
-// (|V_h|_1 max_n bound_n^2; the fp16 split keeps 22 bits for values down to
-// 2^-17 of the bound, far below its looseness).
+//   GEMM ii  Y_v [D x N2]    += [v]^T (D x rows) . [q zhat] (rows x N2)
+// with zhat = [mz; 1], E = sum q zhat zhat^T in fp64 from the fp32 mz, and
+// sq_v = sum q v^2 (fp32 per thread over the item's rows, fp64 across
+// threads) on the CUDA cores. Both GEMMs are tcgen05.mma.kind::f16 in 3xFP16
+// (hi*hi + hi*lo + lo*hi, 22 significant bits, fp32 accumulation in TMEM), SS
+// form, M = 128 (GEMM i's rows 48..127 read the next smem bytes and are
+// ignored; an MMA costs the same ~46 cycles for M = 64 or 128 at these N).
 //
-// A tile is 128 rows; per tile GEMM i (Z in one of two TMEM buffers), the
-// CUDA-core work (mz, E, GEMM ii's B), then GEMM ii (Y_v accumulates in TMEM
-// over the item's tiles); the tiles are pipelined (GEMM i of tile t + 1 runs
-// during tile t's CUDA-core work), and each row chunk is produced twice, the
-// second time from L2. Roles: warps 0-7
-// produce chunks into a 4-slot ring (32 KB each: 128 rows x 64 dims, fp16 hi
-// and lo, 128-byte swizzle) and do the CUDA-core work; one thread of warp 8
-// issues the MMAs and commits to the ring / phase barriers. Outputs as the
-// other statistics kernels: a component's sole item writes Y_v, sq_v, E
-// directly, split components write item partials reduced by k_stats_reduce.
+// A tile's split rows stay RESIDENT in shared memory: every 64-dimension chunk
+// of the tile is produced once (global load, centring, power-of-two row scale
+// 2^k_n from the bound max|x_n| + max|mu_c|, fp16 hi/lo split, 128-byte
+// swizzle) into its own ring slot (12 KB: hi | lo, 48 lines of 128 B), read by
+// GEMM i as a K-major A (rows x dims) and, once the tile's zhat is known, by
+// GEMM ii as an MN-major A (dims x rows; two adjacent slots = M 128); GEMM ii
+// releases the slots to the next tile. The ring holds a whole number of tiles
+// (13 slots: one tile at D = 784, three at D = 256). GEMM ii sums over rows
+// (its K), so 2^-k_n is folded into its B operand (q zhat), exactly, and every
+// column of that operand gets a power-of-two scale from an a-priori bound
+// (|V_h|_1 max_n bound_n^2). V_c's image (GEMM i's B, prebuilt per precompute
+// by k_stats_vimg) is copied into shared memory once per item.
+//
+// Roles: warps 0-7 produce the tiles, run the Z epilogue (warps 0-1: TMEM lanes
+// = tile rows) and the CUDA-core work; lane 0 of warp 8 issues the MMAs and
+// commits to the slot / Z / B2 / Y barriers. Outputs as the other statistics
+// kernels: a component's sole item writes Y_v, sq_v, E directly, split
+// components write item partials reduced by k_stats_reduce.
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 
 #include "vmfa_kernels.cuh"
@@ -40,14 +43,19 @@
 namespace vmfa_b200 {
 namespace {
 
-constexpr int kTRows = 128;            // rows per tile (M of GEMM i, K of GEMM ii)
-constexpr int kTItemRows = 512;        // K-pairs per item (<= 4 tiles; Z of each in TMEM)
-constexpr int kTProd = 256;            // producer threads (warps 0-7)
-constexpr int kTThreads = kTProd + 32; // + the MMA warp
-constexpr int kTSlots = 4;
-constexpr uint32_t kTSlotBytes = 32768;  // hi (16 KB) + lo (16 KB)
-constexpr int kTMaxChunks = 13;        // D <= 832
-constexpr int kTargetE = 14;           // operands scaled to |value| <= 2^14
+constexpr int kTR = 128;                 // rows per tile (GEMM i's M, GEMM ii's K)
+constexpr int kTItemRows = 512;          // K-pairs per item (4 tiles)
+constexpr int kTMaxChunks = 13;          // D <= 832
+constexpr int kTFill = 16;               // fill warps (0-15)
+constexpr int kTFillThreads = kTFill * 32;
+constexpr int kTRowsPerThr = kTR * 16 / kTFillThreads;  // 4 rows x 4 dimensions per thread and chunk
+constexpr int kTEpi0 = kTFill;           // warps 16-19: Z epilogue (kernel Z) / B2 builders (kernel Y)
+constexpr int kTMma = kTFill + 4;        // warp 20 issues the MMAs
+constexpr int kTThreads = (kTFill + 5) * 32;
+constexpr uint32_t kTUnit = kTR * 128;   // one plane of one chunk: 128 rows x 64 fp16 (16 KB)
+constexpr uint32_t kTPairBytes = 4 * kTUnit;  // pair slot [hi c0 | hi c1 | lo c0 | lo c1]
+constexpr int kTPairs = 2;               // ring depth (pair slots)
+constexpr int kTargetE = 14;             // operands scaled to |value| <= 2^14
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
 __device__ __forceinline__ int sexp(float bound) {
@@ -87,8 +95,9 @@ __device__ __forceinline__ uint64_t desc(uint32_t saddr, uint32_t lbo_bytes) {
 // kind::f16 instruction descriptor: fp32 D, fp16 A/B, M = 128, A K- or MN-major
 __device__ __forceinline__ uint32_t idesc(int N, bool a_mn) {
   return (1u << 4) | (a_mn ? (1u << 15) : 0u) | (static_cast<uint32_t>(N >> 3) << 17) |
-         (static_cast<uint32_t>(kTRows >> 4) << 24);
+         (static_cast<uint32_t>(128 >> 4) << 24);
 }
+__device__ __forceinline__ uint32_t idesc_m(int N) { return idesc(N, false); }
 __device__ __forceinline__ void mma_ss(uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
   asm volatile(
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
@@ -136,7 +145,6 @@ __device__ __forceinline__ void tld8(uint32_t taddr, float* v) {
                : "r"(taddr));
 }
 __device__ __forceinline__ void tld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
-__device__ __forceinline__ void producers_sync() { asm volatile("bar.sync 1, %0;" ::"r"(kTProd) : "memory"); }
 
 __device__ __forceinline__ int find_item_t(const int* itemoff, int C, int item) {
   int lo = 0, hi = C;
@@ -148,12 +156,11 @@ __device__ __forceinline__ int find_item_t(const int* itemoff, int C, int item) 
   return lo;
 }
 
+// ---------------------------------------------------------------- layout
 struct TcLayout {
-  int nch;       // real 64-dimension chunks (ceil(D / 64))
-  int npair;     // chunk pairs (M = 128 dimensions of GEMM ii)
-  int HP, N2;    // GEMM i / GEMM ii N
-  uint32_t off_V, off_B2, off_z, off_sq, off_row, off_q, off_qf, off_k, total;
-  uint32_t tmem_cols;  // Z (2 x HP, at 0) + Y_v (npair x N2, at 64)
+  int nch, npair, HP, N2;
+  uint32_t off_V, off_B2, off_z, off_ep, off_sqw, off_row, off_q, off_k, total_z;
+  uint32_t off_row_y, off_q_y, off_k_y, total_y;
 };
 __host__ __device__ inline TcLayout tc_layout(int D, int H) {
   TcLayout L;
@@ -161,162 +168,216 @@ __host__ __device__ inline TcLayout tc_layout(int D, int H) {
   L.npair = (L.nch + 1) / 2;
   L.HP = ((H + 15) / 16) * 16;
   L.N2 = ((H + 1 + 15) / 16) * 16;  // (M = 128: N in steps of 16)
-  uint32_t o = kTSlots * kTSlotBytes;
+  const uint32_t ring = kTPairs * kTPairBytes;
+  // kernel Z: ring | V image | s_z | E partials (4 warps) | item arrays
+  uint32_t o = ring;
   L.off_V = o;
   o += static_cast<uint32_t>(L.nch) * 2 * L.HP * 128;
-  L.off_B2 = o;
-  o += 2u * 2 * L.N2 * 128;
   L.off_z = o;
-  o += static_cast<uint32_t>(kTRows) * (H + 1) * 4;
-  o = (o + 7u) & ~7u;
-  L.off_sq = o;
-  o += static_cast<uint32_t>(L.npair) * 128 * 8;
+  o += static_cast<uint32_t>(kTR) * (H + 1) * 4;
+  o = (o + 15u) & ~15u;
+  L.off_ep = o;
+  o += 4u * 6 * 2 * 32 * 8;
   L.off_row = o;
-  o += kTItemRows * 4;
-  L.off_q = (o + 7u) & ~7u;
-  o = L.off_q + kTItemRows * 8;
-  L.off_qf = o;
-  o += kTItemRows * 4;
-  L.off_k = o;
-  o += kTItemRows * 4;
-  L.total = o;
-  L.tmem_cols = 512;  // Z (4 tiles x HP <= 64) | Y_v hi*hi (<= 224) | Y_v corrections (<= 224)
+  L.off_q = (L.off_row + kTItemRows * 4 + 7u) & ~7u;
+  L.off_k = L.off_q + kTItemRows * 8;
+  L.total_z = L.off_k + kTItemRows * 4;
+  // kernel Y: ring | B2 x 2 | sq per fill warp (fp32) | item arrays
+  uint32_t p = ring;
+  L.off_B2 = p;
+  p += 2u * 2 * 2 * L.N2 * 128;  // 2 buffers x (hi, lo) x 2 line blocks (K 0-63, 64-127)
+  L.off_sqw = p;
+  p += static_cast<uint32_t>(kTFill) * kTMaxChunks * 64 * 4;
+  L.off_row_y = p;
+  L.off_q_y = (L.off_row_y + kTItemRows * 4 + 7u) & ~7u;
+  L.off_k_y = L.off_q_y + kTItemRows * 8;
+  L.total_y = L.off_k_y + kTItemRows * 4;
   return L;
 }
 
-template <int HP, int N2>
+// dbg & 4: block 0 prints per-role cycle counts (diagnostics)
+#define TC_T0() const long long _t0 = (dbg & 4) ? clock64() : 0
+#define TC_ACC(i) do { if ((dbg & 4) && blockIdx.x == 0) prof[i] += clock64() - _t0; } while (0)
+__device__ __forceinline__ void dmma_f64(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+__device__ __forceinline__ void fill_sync() { asm volatile("bar.sync 1, %0;" ::"r"(kTFillThreads) : "memory"); }
+__device__ __forceinline__ void producers_all_sync() { asm volatile("bar.sync 2, %0;" ::"r"(kTMma * 32) : "memory"); }
+
+// Item setup shared by both kernels (all producer warps 0-11): rows, q, row
+// scale exponents, and the bound max_n (max|x_n| + max|mu_c|) into s_bmax.
+struct ItemSetup {
+  int c, r0, nr, T;
+  bool direct;
+};
+__device__ __forceinline__ void item_rows(const StatsArgs& a, const float* __restrict__ xmax, float mb, int r0, int nr,
+                                          int* s_row, double* s_q, int* s_k, float* s_bmax) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  float bm = 0.f;
+  for (int i = tid; i < kTItemRows; i += kTMma * 32) {
+    int n = 0, k = 0;
+    double q = 0.0;
+    if (i < nr) {
+      const int e = a.ent[r0 + i];
+      n = e / a.dm.Cp;
+      q = a.resp[e];
+      const float bnd = __ldg(xmax + n) + mb;
+      k = sexp(bnd);
+      bm = fmaxf(bm, bnd);
+    }
+    s_row[i] = n;
+    s_q[i] = q;
+    s_k[i] = k;
+  }
+  for (int o = 16; o > 0; o >>= 1) bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, o));
+  if (lane == 0) s_bmax[warp] = bm;
+}
+
+// The fill role: unit f of an item = chunk u = f % U (U = 2 npair; chunks >=
+// nch are padding: no stores) of tile f / U, 128 rows x 64 dimensions; thread
+// (dg, rg) covers dimensions 4 dg .. + 3 of rows 8 rg .. + 7. A pair slot
+// holds the units 2p, 2p + 1 of a tile; its full barrier takes one arrival
+// per fill warp and unit. Loads run two units ahead (two register batches).
+template <bool SQ, typename F>
+__device__ __forceinline__ void fill_item(const StatsArgs& a, const TcLayout& L, int c, int nr, int T, uint32_t sbase,
+                                          const int* s_row, const double* s_q, const int* s_k, uint64_t* s_full,
+                                          uint64_t* s_empty, uint32_t gp0, float* s_sqw, int dbg, F&& on_tile_end) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int dg = tid & 15, rg = tid >> 4;
+  const int D = a.dm.D;
+  const int U = 2 * L.npair, nF = T * U;
+  const float* muc = a.mu32 + (int64_t)c * D;
+  float4 xa[kTRowsPerThr], xb[kTRowsPerThr], xc[kTRowsPerThr];
+  float4 ma = make_float4(0.f, 0.f, 0.f, 0.f), mbv = ma, mcv = ma;
+  auto ldu = [&](int f, float4* xv, float4& mv) {
+    const int t = f / U, k = f - t * U, d0 = k * 64 + 4 * dg;
+    const bool dl = k < L.nch && d0 < D;
+    mv = dl ? __ldg(reinterpret_cast<const float4*>(muc + d0)) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int i = 0; i < kTRowsPerThr; ++i) {
+      const int rt = t * kTR + rg * kTRowsPerThr + i;
+      xv[i] = (dl && rt < nr && !(dbg & 2)) ? __ldg(reinterpret_cast<const float4*>(a.X + (int64_t)s_row[rt] * D + d0))
+                                            : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  };
+  auto stu = [&](int f, const float4* xv, const float4& mv) {
+    const int t = f / U, k = f - t * U, d0 = k * 64 + 4 * dg;
+    const uint32_t gp = gp0 + static_cast<uint32_t>(f >> 1);
+    const int slot = static_cast<int>(gp % kTPairs);
+    const uint32_t use = gp / kTPairs;
+    if ((f & 1) == 0 && use > 0) bwait(&s_empty[slot], use);  // the pair slot's previous tile is done
+    if (k < L.nch) {
+      const uint32_t hi = sbase + slot * kTPairBytes + (f & 1) * kTUnit, lo = hi + 2 * kTUnit;
+      float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+#pragma unroll
+      for (int i = 0; i < kTRowsPerThr; ++i) {
+        const int r = rg * kTRowsPerThr + i, rt = t * kTR + r;
+        const bool on = rt < nr && d0 < D;
+        const float v0 = on ? xv[i].x - mv.x : 0.f, v1 = on ? xv[i].y - mv.y : 0.f;
+        const float v2 = on ? xv[i].z - mv.z : 0.f, v3 = on ? xv[i].w - mv.w : 0.f;
+        if (SQ) {
+          const float q = on ? static_cast<float>(s_q[rt]) : 0.f;
+          s0 = fmaf(q * v0, v0, s0);
+          s1 = fmaf(q * v1, v1, s1);
+          s2 = fmaf(q * v2, v2, s2);
+          s3 = fmaf(q * v3, v3, s3);
+        }
+        const float sc = on ? p2(s_k[rt]) : 0.f;
+        uint32_t h01, l01, h23, l23;
+        split(v0 * sc, v1 * sc, h01, l01);
+        split(v2 * sc, v3 * sc, h23, l23);
+        const uint32_t o = swz(r, dg >> 1) + (dg & 1) * 8;
+        asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(hi + o), "r"(h01), "r"(h23) : "memory");
+        asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(lo + o), "r"(l01), "r"(l23) : "memory");
+      }
+      if (SQ) {  // the warp's two row groups, then the warp's own fp64 row of sums
+        s0 += __shfl_xor_sync(0xffffffffu, s0, 16);
+        s1 += __shfl_xor_sync(0xffffffffu, s1, 16);
+        s2 += __shfl_xor_sync(0xffffffffu, s2, 16);
+        s3 += __shfl_xor_sync(0xffffffffu, s3, 16);
+        if (lane < 16 && d0 < D) {  // (fp32 over the warp's <= 32 rows of the item)
+          float* w = s_sqw + (int64_t)warp * kTMaxChunks * 64 + d0;
+          w[0] += s0;
+          w[1] += s1;
+          w[2] += s2;
+          w[3] += s3;
+        }
+      }
+      fence_async();
+    }
+    __syncwarp();
+    if (lane == 0) barrive(&s_full[slot]);
+    if (k == U - 1) on_tile_end(t);
+  };
+  ldu(0, xa, ma);
+  if (1 < nF) ldu(1, xb, mbv);
+  if (2 < nF) ldu(2, xc, mcv);
+  for (int f = 0; f < nF; f += 3) {
+    stu(f, xa, ma);
+    if (f + 3 < nF) ldu(f + 3, xa, ma);
+    if (f + 1 >= nF) break;
+    stu(f + 1, xb, mbv);
+    if (f + 4 < nF) ldu(f + 4, xb, mbv);
+    if (f + 2 >= nF) break;
+    stu(f + 2, xc, mcv);
+    if (f + 5 < nF) ldu(f + 5, xc, mcv);
+  }
+}
+
+// ---------------------------------------------------------------- kernel Z
+// GEMM i per tile of 128 rows (M = 128, every row live): Z = [v] . [V_c^T]
+// over the chunk pairs streamed through the ring (a slot is released as soon
+// as its two chunks are multiplied); Z double-buffered in TMEM so the
+// epilogue of tile t (warps 8-11: zhat = Z 2^-(k_n + e_h) to global memory,
+// and E = sum q [zhat; 1][zhat; 1]^T in fp64 by DMMA m8n8k4, each warp over
+// its own 32 rows) runs under GEMM i of tile t + 1.
+template <int HP>
 __global__ void __launch_bounds__(kTThreads, 1)
-    k_stats_tc(StatsArgs a, const float* __restrict__ xmax, const float* __restrict__ mumax,
-               const unsigned char* __restrict__ vimg, const int* __restrict__ vexp_g,
-               const float* __restrict__ vl1_g, const int* __restrict__ itemoff, int nh1, double* part,
-               int64_t part_stride, int dbg) {
+    k_stats_z(StatsArgs a, const float* __restrict__ xmax, const float* __restrict__ mumax,
+              const unsigned char* __restrict__ vimg, const int* __restrict__ vexp_g, const int* __restrict__ itemoff,
+              int nh1, double* part, int64_t part_stride, float* zout, int dbg) {
   extern __shared__ __align__(1024) unsigned char sm[];
-  // (a waiter may lag a barrier by at most one phase: each tile of an item
-  // has its own Z barrier, as all 4 can complete before the first is waited on)
-  __shared__ uint64_t s_full[kTSlots], s_empty[kTSlots], s_zdone[2], s_b2ready, s_b2free, s_ydone;
+  __shared__ uint64_t s_full[kTPairs], s_empty[kTPairs], s_zdone[2], s_zfree[2];
   __shared__ uint32_t s_tmem;
   __shared__ int s_item;
-  __shared__ double s_sqscale;  // the item's sq_v fixed-point scale 2^e (sums < 2^62)
-  __shared__ float s_bmax[8];
-  __shared__ int s_colexp[32];
-  __shared__ float s_colmax[8][32];
+  __shared__ float s_bmax[kTMma];
+  __shared__ int s_vexp[32];
+  long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  const long long tstart = clock64();
   const Dims dm = a.dm;
   const int D = dm.D, H = dm.H, H1 = H + 1;
   const TcLayout L = tc_layout(D, H);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t sbase = su32(sm);
-  float* s_z = reinterpret_cast<float*>(sm + L.off_z);           // [128][H1] fp32 zhat rows of one tile
-  unsigned long long* s_sq = reinterpret_cast<unsigned long long*>(sm + L.off_sq);  // [npair * 128] sq_v, fixed point
-  int* s_row = reinterpret_cast<int*>(sm + L.off_row);           // x row per item row
-  double* s_q = reinterpret_cast<double*>(sm + L.off_q);         // q (fp64)
-  float* s_qf = reinterpret_cast<float*>(sm + L.off_qf);         // q (fp32)
-  int* s_k = reinterpret_cast<int*>(sm + L.off_k);               // row scale exponents
+  float* s_z = reinterpret_cast<float*>(sm + L.off_z);
+  double (*s_epart)[6 * 2 * 32] = reinterpret_cast<double (*)[6 * 2 * 32]>(sm + L.off_ep);
+  int* s_row = reinterpret_cast<int*>(sm + L.off_row);
+  double* s_q = reinterpret_cast<double*>(sm + L.off_q);
+  int* s_k = reinterpret_cast<int*>(sm + L.off_k);
   if (tid == 0) {
-    for (int i = 0; i < kTSlots; ++i) {
-      binit(&s_full[i], kTProd);
+    for (int i = 0; i < kTPairs; ++i) {
+      binit(&s_full[i], 2 * kTFill);
       binit(&s_empty[i], 1);
     }
-    for (int i = 0; i < 2; ++i) binit(&s_zdone[i], 1);
-    binit(&s_b2ready, kTProd);
-    binit(&s_b2free, 1);
-    binit(&s_ydone, 1);
+    for (int i = 0; i < 2; ++i) {
+      binit(&s_zdone[i], 1);
+      binit(&s_zfree[i], 4);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 8) {  // TMEM: Z (2 tiles x HP columns) at 0, Y_v (npair x N2) at 64
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&s_tmem)),
-                 "r"(L.tmem_cols));
+  if (warp == kTMma) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&s_tmem)), "r"(32));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tfence_before();
   __syncthreads();
   tfence_after();
   const uint32_t tmem = s_tmem;
-  const uint32_t tY = tmem + 64, tYc = tmem + 288;  // Y_v: hi*hi products / the two correction products
   const int total = __ldg(itemoff + dm.C);
-  // barrier completion counts (identical bookkeeping in every role)
-  uint32_t fills[kTSlots] = {0, 0, 0, 0};  // completed fills per slot
-  uint32_t nzt[2] = {};                    // completions of each Z buffer's barrier
-  uint32_t nb2 = 0, ny = 0;                // b2ready+b2free / ydone completions
-  uint32_t gs = 0;                         // global stage counter (slot = gs % 4)
-  int c_cur = 0;                           // the item's component (for fill)
-
-  // ---- producers: one ring fill = split v of (tile t, chunk k). The rows
-  // of the NEXT fill are loaded into registers before this fill waits for its
-  // slot (two register sets, ping-pong), so every thread keeps 8-16 row
-  // pieces in flight. Thread: 4 dimensions (dg) x 8 rows (rg).
-  struct Piece {
-    float4 x[8];
-    float4 mu;
-  };
-  const int dg = tid & 15, rg = tid >> 4;
-  auto load = [&](int t, int k, int nr, Piece& P) {
-    const int d0 = k * 64 + 4 * dg;
-    P.mu = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (d0 < D) P.mu = __ldg(reinterpret_cast<const float4*>(a.mu32 + (int64_t)c_cur * D + d0));
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int rr = t * kTRows + rg * 8 + i;
-      P.x[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (rr < nr && d0 < D && !(dbg & 2)) P.x[i] = __ldg(reinterpret_cast<const float4*>(a.X + (int64_t)s_row[rr] * D + d0));
-    }
-  };
-  auto store = [&](int t, int k, int nr, const Piece& P, bool do_sq) {
-    const int slot = gs % kTSlots;
-    if (fills[slot] > 0) bwait(&s_empty[slot], fills[slot]);  // the MMAs of the previous fill are done
-    const uint32_t hi = sbase + slot * kTSlotBytes, lo = hi + 16384;
-    const int d0 = k * 64 + 4 * dg;
-    float sq0 = 0.f, sq1 = 0.f, sq2 = 0.f, sq3 = 0.f;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int r = rg * 8 + i, rr = t * kTRows + r;
-      const bool live = rr < nr && d0 < D;
-      const float v0 = live ? P.x[i].x - P.mu.x : 0.f, v1 = live ? P.x[i].y - P.mu.y : 0.f;
-      const float v2 = live ? P.x[i].z - P.mu.z : 0.f, v3 = live ? P.x[i].w - P.mu.w : 0.f;
-      if (do_sq && live) {
-        const float q = s_qf[rr];
-        sq0 = fmaf(q * v0, v0, sq0);
-        sq1 = fmaf(q * v1, v1, sq1);
-        sq2 = fmaf(q * v2, v2, sq2);
-        sq3 = fmaf(q * v3, v3, sq3);
-      }
-      const float sc = rr < nr ? p2(s_k[rr]) : 1.f;
-      uint32_t h01, l01, h23, l23;
-      split(v0 * sc, v1 * sc, h01, l01);
-      split(v2 * sc, v3 * sc, h23, l23);
-      const uint32_t o = swz(r, dg >> 1) + (dg & 1) * 8;
-      asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(hi + o), "r"(h01), "r"(h23) : "memory");
-      asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(lo + o), "r"(l01), "r"(l23) : "memory");
-    }
-    if (do_sq) {
-      // the warp's two row groups, then exact fixed-point sums (integer
-      // atomics: the order of the warps cannot change the result)
-      sq0 += __shfl_xor_sync(0xffffffffu, sq0, 16);
-      sq1 += __shfl_xor_sync(0xffffffffu, sq1, 16);
-      sq2 += __shfl_xor_sync(0xffffffffu, sq2, 16);
-      sq3 += __shfl_xor_sync(0xffffffffu, sq3, 16);
-      if (lane < 16 && d0 < D) {
-        const double f = s_sqscale;
-        atomicAdd(&s_sq[d0], static_cast<unsigned long long>(llrint(static_cast<double>(sq0) * f)));
-        atomicAdd(&s_sq[d0 + 1], static_cast<unsigned long long>(llrint(static_cast<double>(sq1) * f)));
-        atomicAdd(&s_sq[d0 + 2], static_cast<unsigned long long>(llrint(static_cast<double>(sq2) * f)));
-        atomicAdd(&s_sq[d0 + 3], static_cast<unsigned long long>(llrint(static_cast<double>(sq3) * f)));
-      }
-    }
-    fence_async();
-    barrive(&s_full[slot]);
-    ++fills[slot];
-    ++gs;
-  };
-  // ---- the MMA thread: consume one slot (GEMM i) or a slot pair (GEMM ii)
-  auto take = [&]() -> int {
-    const int slot = gs % kTSlots;
-    ++fills[slot];
-    bwait(&s_full[slot], fills[slot]);
-    tfence_after();
-    ++gs;
-    return slot;
-  };
-
+  uint32_t gp = 0;     // pair slots consumed so far (all items)
+  uint32_t ntile = 0;  // tiles so far (Z buffer = ntile & 1)
   for (;;) {
     __syncthreads();
     if (tid == 0) s_item = a.qctr ? atomicAdd(a.qctr, 1) : -1;
@@ -326,284 +387,358 @@ __global__ void __launch_bounds__(kTThreads, 1)
     const int c = find_item_t(itemoff, dm.C, item);
     const int r0 = a.off[c] + (item - itemoff[c]) * kTItemRows;
     const int nr = min(a.off[c + 1], r0 + kTItemRows) - r0;
-    const int T = (nr + kTRows - 1) / kTRows;
+    const int T = (nr + kTR - 1) / kTR;
     const bool direct = itemoff[c + 1] - itemoff[c] == 1;
-    c_cur = c;
-
-    if (warp < 8) {
-      // ---- item setup: rows, q, row scales, mu, V image (per-h scale), sq
-      const float mb = __ldg(mumax + c);
-      for (int i = tid; i < kTItemRows; i += kTProd) {
-        int n = 0, k = 0;
-        double q = 0.0;
-        if (i < nr) {
-          const int e = a.ent[r0 + i];
-          n = e / dm.Cp;
-          q = a.resp[e];
-          k = sexp(__ldg(xmax + n) + mb);
-        }
-        s_row[i] = n;
-        s_q[i] = q;
-        s_qf[i] = static_cast<float>(q);
-        s_k[i] = k;
-      }
-      for (int d = tid; d < L.npair * 128; d += kTProd) s_sq[d] = 0ull;
-      {  // sq_v <= nr max_n (max|x_n| + max|mu_c|)^2: the fixed-point scale
-        float bm = 0.f;
-        for (int i = tid; i < nr; i += kTProd) bm = fmaxf(bm, __ldg(xmax + s_row[i]) + mb);
-        for (int o = 16; o > 0; o >>= 1) bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, o));
-        if (lane == 0) s_bmax[warp] = bm;
-        producers_sync();
-        if (tid == 0) {
-          float m = 0.f;
-          for (int w = 0; w < 8; ++w) m = fmaxf(m, s_bmax[w]);
-          const double B = static_cast<double>(m) * m * static_cast<double>(nr) + 1e-300;
-          s_sqscale = ldexp(1.0, 61 - ilogb(B));
-        }
-      }
-      // V image (GEMM i's B, prebuilt per precompute by k_stats_vimg in this
-      // smem layout): a linear copy; its row scales and |V_h|_1 beside it
-      {
-        const uint32_t nb = static_cast<uint32_t>(L.nch) * 2 * HP * 128;
-        const uint4* src = reinterpret_cast<const uint4*>(vimg + (int64_t)c * nb);
-        uint4* dst = reinterpret_cast<uint4*>(sm + L.off_V);
-        for (uint32_t i = tid; i < nb / 16; i += kTProd) dst[i] = __ldg(src + i);
-        if (tid < HP) {
-          s_colexp[tid] = __ldg(vexp_g + (int64_t)c * HP + tid);
-          s_colmax[0][tid] = __ldg(vl1_g + (int64_t)c * HP + tid);
-        }
-      }
+    if (warp < kTMma) {
+      item_rows(a, xmax, __ldg(mumax + c), r0, nr, s_row, s_q, s_k, s_bmax);
+      const uint32_t nb = static_cast<uint32_t>(L.nch) * 2 * HP * 128;
+      const uint4* src = reinterpret_cast<const uint4*>(vimg + (int64_t)c * nb);
+      uint4* dst = reinterpret_cast<uint4*>(sm + L.off_V);
+      for (uint32_t i = tid; i < nb / 16; i += kTMma * 32) dst[i] = __ldg(src + i);
+      if (tid < HP) s_vexp[tid] = __ldg(vexp_g + (int64_t)c * HP + tid);
       fence_async();
-      producers_sync();
-      int vexp[HP];  // (kept in registers by the Z epilogue)
+      producers_all_sync();
+    }
+    if (warp < kTFill) {
+      TC_T0();
+      fill_item<false>(a, L, c, nr, T, sbase, s_row, s_q, s_k, s_full, s_empty, gp, nullptr, dbg, [](int) {});
+      TC_ACC(0);
+    } else if (warp < kTMma) {
+      // ---- Z epilogue + E (warps 8-11: TMEM lanes 32 (warp - 8) ..)
+      const int qd = warp - kTEpi0;
+      double ec[6][2];
 #pragma unroll
-      for (int h = 0; h < HP; ++h) vexp[h] = s_colexp[h];
-      producers_sync();
-      if (tid < N2) {  // GEMM ii's B column scales (from the bounds)
-        float mm = 0.f;
-        for (int w = 0; w < 8; ++w) mm = fmaxf(mm, s_bmax[w]);
-        const float bnd = tid < H ? 1.01f * s_colmax[0][tid] * mm * mm * p2(-13)
-                                  : (tid == H ? 1.01f * mm * p2(-13) : 0.f);
-        s_colexp[tid] = sexp(bnd);
-      }
-      producers_sync();
-      // ---- tiles, pipelined: GEMM i fills of tile t + 1 go before tile t's
-      // epilogue (the MMA computes Z of t + 1 in the other Z buffer meanwhile)
-      // and its GEMM ii fills (re-reading tile t's rows while they are in L2)
-      const int NE = H1 * (H1 + 1) / 2;
-      double eacc = 0.0;  // entry tid (tid < NE)
-      int ei = 0, ej = 0;
-      if (tid < NE) {
-        int t = tid;
-        while (t >= H1 - ei) t -= H1 - ei, ++ei;
-        ej = ei + t;
-      }
-      const int NK = 2 * L.npair;
-      // tile t's CUDA-core work, before its first GEMM ii fill
-      auto epilogue = [&](int t) {
-        // mz of tile t (warps 0-3: TMEM lanes = tile rows) into s_z
-        if (warp < 4) {
-          bwait(&s_zdone[t & 1], nzt[t & 1] + 1);
-          tfence_after();
-          const int r = warp * 32 + lane, rr = t * kTRows + r;
-          float z[HP];
-#pragma unroll
-          for (int h0 = 0; h0 < HP; h0 += 8)
-            tld8(tmem + (static_cast<uint32_t>(warp * 32) << 16) + (t & 1) * HP + h0, z + h0);
-          tld_wait();
-          const bool live = rr < nr;
-#pragma unroll
-          for (int h = 0; h < HP; ++h)
-            if (h < H) s_z[r * H1 + h] = live ? z[h] * p2(-(s_k[rr] + vexp[h])) : 0.f;
-          s_z[r * H1 + H] = live ? 1.f : 0.f;
-        }
-        ++nzt[t & 1];
-        if (nb2 > 0) bwait(&s_b2free, nb2);  // the previous tile's GEMM ii is done with B
-        producers_sync();
-        // E (fp64, a thread per upper-triangle entry, summed over the tiles)
-        const int nt = min(kTRows, nr - t * kTRows);
-        if (tid < NE)
-          for (int r = 0; r < nt; ++r)
-            eacc = fma(s_q[t * kTRows + r], static_cast<double>(s_z[r * H1 + ei]) * static_cast<double>(s_z[r * H1 + ej]),
-                       eacc);
-        // GEMM ii's B for tile t: q zhat_h 2^(e_h - k_r), K-major (h rows, 64
-        // tile rows per 128-byte line, two line blocks)
-        const uint32_t b2 = sbase + L.off_B2;
-        for (int i = tid; i < kTRows * N2; i += kTProd) {
-          const int r = i % kTRows, h = i / kTRows, rr = t * kTRows + r;
-          float b = 0.f;
-          if (rr < nr && h < H1) b = s_qf[rr] * s_z[r * H1 + h] * p2(s_colexp[h] - s_k[rr]);
-          __half bh, bl;
-          split1(b, bh, bl);
-          const int kc = r >> 6, rl = r & 63;
-          const uint32_t o = swz(h, rl >> 3) + (rl & 7) * 2;
-          const uint32_t base_h = b2 + (0 * 2 + kc) * N2 * 128, base_l = b2 + (1 * 2 + kc) * N2 * 128;
-          asm volatile("st.shared.b16 [%0], %1;" ::"r"(base_h + o), "h"(*reinterpret_cast<uint16_t*>(&bh)) : "memory");
-          asm volatile("st.shared.b16 [%0], %1;" ::"r"(base_l + o), "h"(*reinterpret_cast<uint16_t*>(&bl)) : "memory");
-        }
-        fence_async();
-        barrive(&s_b2ready);
-        ++nb2;
-        producers_sync();  // (s_z is rewritten by the next tile)
-      };
-      // the item's fills in MMA order: A(0), then per t: A(t + 1), B(t)
-      // (A = GEMM i, B = GEMM ii); rows loaded two fills ahead (3 register
-      // sets), the GEMM ii fills' loads also ahead of the epilogue
-      const int nF = 2 * T * NK;
-      auto fdesc = [&](int f, int& t, int& k, bool& b) {
-        if (f < NK) {
-          t = 0, k = f, b = false;
-          return;
-        }
-        const int j = (f - NK) / NK;
-        k = (f - NK) - j * NK;
-        if (j < 2 * (T - 1)) {
-          b = (j & 1) != 0;
-          t = b ? (j - 1) / 2 : j / 2 + 1;
-        } else {
-          t = T - 1, b = true;
-        }
-      };
-      auto ld = [&](int f, Piece& P) {
-        int t, k;
-        bool b;
-        fdesc(f, t, k, b);
-        load(t, k, nr, P);
-      };
-      auto st = [&](int f, const Piece& P) {
-        int t, k;
-        bool b;
-        fdesc(f, t, k, b);
-        if (b && k == 0) epilogue(t);
-        store(t, k, nr, P, b);
-      };
-      {
-        Piece P0, P1, P2;
-        ld(0, P0);
-        if (1 < nF) ld(1, P1);
-        for (int f = 0; f < nF; f += 3) {
-          if (f + 2 < nF) ld(f + 2, P2);
-          st(f, P0);
-          if (f + 1 >= nF) break;
-          if (f + 3 < nF) ld(f + 3, P0);
-          st(f + 1, P1);
-          if (f + 2 >= nF) break;
-          if (f + 4 < nF) ld(f + 4, P1);
-          st(f + 2, P2);
-        }
-      }
-      if (tid < NE) {
-        double* pe = direct ? a.E + (int64_t)c * H1 * H1 : part + (int64_t)item * part_stride + (int64_t)nh1 * D + D;
-        pe[ej * H1 + ei] = eacc;
-        pe[ei * H1 + ej] = eacc;
-      }
-      // ---- Y_v epilogue (warps 0-3: TMEM lanes = the pair's 128 dimensions)
-      producers_sync();
-      if (warp < 4) {
-        bwait(&s_ydone, ++ny);
-        tfence_after();
-        double* pp = direct ? nullptr : part + (int64_t)item * part_stride;
-        for (int j = 0; j < L.npair; ++j) {
-          float y[N2], yc[N2];
-#pragma unroll
-          for (int h0 = 0; h0 < N2; h0 += 8) {
-            tld8(tY + (static_cast<uint32_t>(warp * 32) << 16) + j * N2 + h0, y + h0);
-            tld8(tYc + (static_cast<uint32_t>(warp * 32) << 16) + j * N2 + h0, yc + h0);
-          }
-          tld_wait();
-#pragma unroll
-          for (int h = 0; h < N2; ++h) y[h] += yc[h];
-          const int d = j * 128 + warp * 32 + lane;
-          if (d < D) {
-#pragma unroll
-            for (int h = 0; h < N2; ++h) {
-              if (h >= H1) break;
-              const double v = static_cast<double>(y[h]) * static_cast<double>(p2(-s_colexp[h]));
-              if (direct) a.Y[((int64_t)c * H1 + h) * D + d] = v;
-              else pp[(int64_t)h * D + d] = v;
-            }
-          }
-        }
-      } else {
-        ++ny;
-      }
-      for (int d = tid; d < D; d += kTProd) {
-        const double v = static_cast<double>(s_sq[d]) / s_sqscale;
-        if (direct) a.sq[(int64_t)c * D + d] = v;
-        else part[(int64_t)item * part_stride + (int64_t)nh1 * D + d] = v;
-      }
-      tfence_before();
-    } else {
-      // ---- the MMA warp: every lane walks the schedule (the barrier waits,
-      // the counters), lane 0 issues the MMAs and commits
-      const bool leader = lane == 0;
-      const uint32_t id1 = idesc(HP, false), id2 = idesc(N2, true);
-      auto gemm_i = [&](int t) {  // Z of tile t into buffer t & 1
-        for (int k = 0; k < 2 * L.npair; ++k) {
-          const int slot = take();
-          if (k < L.nch && leader && !(dbg & 1)) {
-            const uint32_t ah = sbase + slot * kTSlotBytes, al = ah + 16384;
-            const uint32_t bh = sbase + L.off_V + (k * 2) * HP * 128, bl = bh + HP * 128;
-#pragma unroll
-            for (int kk = 0; kk < 4; ++kk) {
-              const uint32_t o = kk * 32;
-              const uint32_t acc = (k > 0 || kk > 0) ? 1u : 0u;
-              const uint32_t dz = tmem + (t & 1) * HP;
-              mma_ss(dz, desc(al + o, 16), desc(bh + o, 16), id1, acc);
-              mma_ss(dz, desc(ah + o, 16), desc(bl + o, 16), id1, 1u);
-              mma_ss(dz, desc(ah + o, 16), desc(bh + o, 16), id1, 1u);
-            }
-          }
-          if (leader) {
-            tcommit(&s_empty[slot]);
-            if (k == 2 * L.npair - 1) tcommit(&s_zdone[t & 1]);
-          }
-          __syncwarp();
-        }
-      };
-      gemm_i(0);
+      for (int i = 0; i < 6; ++i) ec[i][0] = ec[i][1] = 0.0;
       for (int t = 0; t < T; ++t) {
-        if (t + 1 < T) gemm_i(t + 1);
-        bwait(&s_b2ready, ++nb2);
-        tfence_after();
-        const uint32_t b2 = sbase + L.off_B2;
-        for (int j = 0; j < L.npair; ++j) {
-          const int s0 = take();
-          take();  // the adjacent slot (s0 even): the MN-major atoms 32 KB apart
-          if (leader && !(dbg & 1)) {
-            const uint32_t ah = sbase + s0 * kTSlotBytes, al = ah + 16384;
-#pragma unroll
-            for (int kk = 0; kk < 8; ++kk) {
-              const uint32_t oa = kk * 2048;  // 16 tile rows = two 8-row groups
-              const uint32_t bh = b2 + (0 * 2 + (kk >> 2)) * N2 * 128 + (kk & 3) * 32;
-              const uint32_t bl = b2 + (1 * 2 + (kk >> 2)) * N2 * 128 + (kk & 3) * 32;
-              const uint32_t acc = (t > 0 || kk > 0) ? 1u : 0u;
-              // the small correction products in their own accumulator (the
-              // tensor core's accumulation truncates: the hi*hi sum then sees
-              // a third of the additions)
-              mma_ss(tYc + j * N2, desc(al + oa, kTSlotBytes), desc(bh, 16), id2, acc);
-              mma_ss(tYc + j * N2, desc(ah + oa, kTSlotBytes), desc(bl, 16), id2, 1u);
-              mma_ss(tY + j * N2, desc(ah + oa, kTSlotBytes), desc(bh, 16), id2, acc);
-            }
-          }
-          if (leader) {
-            tcommit(&s_empty[s0]);
-            tcommit(&s_empty[s0 + 1]);
-          }
-          __syncwarp();
+        const uint32_t zb = (ntile + t) & 1u;
+        {
+          TC_T0();
+          bwait(&s_zdone[zb], (ntile + t) / 2 + 1);
+          TC_ACC(1);
         }
-        if (leader) tcommit(&s_b2free);
+        tfence_after();
+        const int r = qd * 32 + lane, rt = t * kTR + r;
+        float z[HP];
+#pragma unroll
+        for (int h0 = 0; h0 < HP; h0 += 8)
+          tld8(tmem + (static_cast<uint32_t>(qd * 32) << 16) + zb * HP + h0, z + h0);
+        tld_wait();
+        tfence_before();
+        __syncwarp();
+        if (lane == 0) barrive(&s_zfree[zb]);
+        const bool lv = rt < nr;
+        float* zo = zout + (int64_t)(r0 + rt) * H;
+#pragma unroll
+        for (int h = 0; h < HP; ++h)
+          if (h < H) {
+            const float v = lv ? z[h] * p2(-(s_k[lv ? rt : 0] + s_vexp[h])) : 0.f;
+            s_z[r * H1 + h] = v;
+            if (lv) zo[h] = v;
+          }
+        s_z[r * H1 + H] = lv ? 1.f : 0.f;
+        __syncwarp();
+        // E over this warp's 32 rows: A(g, t) = zhat[row t][8 mi + g],
+        // B(t, g) = q zhat[row t][8 ni + g] (k = 4 rows per DMMA)
+        const int g = lane >> 2, tq = lane & 3;
+        for (int k0 = 0; k0 < 32; k0 += 4) {
+          const int rr = qd * 32 + k0 + tq, rtt = t * kTR + rr;
+          const double q = s_q[rtt];
+          double za[3], zq[3];
+#pragma unroll
+          for (int m = 0; m < 3; ++m) {
+            const int col = 8 * m + g;
+            za[m] = col < H1 ? static_cast<double>(s_z[rr * H1 + col]) : 0.0;
+            zq[m] = q * za[m];
+          }
+          dmma_f64(ec[0], za[0], zq[0]);
+          dmma_f64(ec[1], za[0], zq[1]);
+          dmma_f64(ec[2], za[0], zq[2]);
+          dmma_f64(ec[3], za[1], zq[1]);
+          dmma_f64(ec[4], za[1], zq[2]);
+          dmma_f64(ec[5], za[2], zq[2]);
+        }
         __syncwarp();
       }
-      if (leader) tcommit(&s_ydone);
-      __syncwarp();
-      ++ny;
+      // E out: the 4 warps' partials in order, both triangles
+#pragma unroll
+      for (int i = 0; i < 6; ++i) {
+        s_epart[qd][(i * 2 + 0) * 32 + lane] = ec[i][0];
+        s_epart[qd][(i * 2 + 1) * 32 + lane] = ec[i][1];
+      }
+      asm volatile("bar.sync 3, 128;" ::: "memory");
+      if (qd == 0) {
+        double* pe = direct ? a.E + (int64_t)c * H1 * H1 : part + (int64_t)item * part_stride + (int64_t)nh1 * D + D;
+        const int g = lane >> 2, tq = lane & 3;
+        const int tmi[6] = {0, 0, 0, 1, 1, 2}, tni[6] = {0, 1, 2, 1, 2, 2};
+#pragma unroll
+        for (int i = 0; i < 6; ++i)
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const double v = ((s_epart[0][(i * 2 + u) * 32 + lane] + s_epart[1][(i * 2 + u) * 32 + lane]) +
+                              s_epart[2][(i * 2 + u) * 32 + lane]) + s_epart[3][(i * 2 + u) * 32 + lane];
+            const int ei = 8 * tmi[i] + g, ej = 8 * tni[i] + 2 * tq + u;
+            if (ei < H1 && ej < H1 && ei <= ej) {
+              pe[ej * H1 + ei] = v;
+              pe[ei * H1 + ej] = v;
+            }
+          }
+      }
+    } else {
+      // ---- MMA issuer (warp 12, lane 0)
+      const bool leader = lane == 0;
+      const uint32_t id1 = idesc(HP, false);
+      const uint32_t vb = sbase + L.off_V;
+      uint32_t g = gp;
+      for (int t = 0; t < T; ++t) {
+        const uint32_t tt = ntile + t, zb = tt & 1u;
+        if (tt >= 2) bwait(&s_zfree[zb], tt / 2);  // the epilogue is done with this Z buffer
+        tfence_after();
+        for (int p = 0; p < L.npair; ++p, ++g) {
+          const int slot = static_cast<int>(g % kTPairs);
+          {
+            TC_T0();
+            bwait(&s_full[slot], g / kTPairs + 1);
+            TC_ACC(2);
+          }
+          tfence_after();
+          if (leader && !(dbg & 1)) {
+#pragma unroll
+            for (int hf = 0; hf < 2; ++hf) {
+              const int k = 2 * p + hf;
+              if (k >= L.nch) break;
+              const uint32_t ah = sbase + slot * kTPairBytes + hf * kTUnit, al = ah + 2 * kTUnit;
+              const uint32_t bh = vb + (k * 2) * HP * 128, bl = bh + HP * 128;
+#pragma unroll
+              for (int kk = 0; kk < 4; ++kk) {
+                const uint32_t o = kk * 32;
+                const uint32_t acc = (k > 0 || kk > 0) ? 1u : 0u;
+                const uint32_t dz = tmem + zb * HP;
+                mma_ss(dz, desc(al + o, 16), desc(bh + o, 16), idesc_m(HP), acc);
+                mma_ss(dz, desc(ah + o, 16), desc(bl + o, 16), idesc_m(HP), 1u);
+                mma_ss(dz, desc(ah + o, 16), desc(bh + o, 16), idesc_m(HP), 1u);
+              }
+            }
+            tcommit(&s_empty[slot]);
+          }
+          __syncwarp();
+        }
+        if (leader) tcommit(&s_zdone[zb]);
+        __syncwarp();
+        (void)id1;
+      }
     }
+    gp += static_cast<uint32_t>(T * L.npair);
+    ntile += static_cast<uint32_t>(T);
   }
   tfence_before();
   __syncthreads();
   tfence_after();
-  if (warp == 8) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(L.tmem_cols));
+  if (warp == kTMma) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(32));
+  if ((dbg & 4) && blockIdx.x == 0 && (tid == 0 || tid == kTEpi0 * 32 || tid == kTMma * 32))
+    printf("stats_z %d: total %lld fill %lld zdone %lld full %lld\n", warp, clock64() - tstart, prof[0], prof[1],
+           prof[2]);
+}
+
+// ---------------------------------------------------------------- kernel Y
+// GEMM ii per tile: Y_v [D x N2] += [v]^T (MN-major A: a pair slot = 128
+// dimensions) . [q zhat 2^(e_h - k_n)] (K-major B2, double-buffered, built by
+// warps 8-11 from kernel Z's zhat while the previous tile multiplies); the
+// fill warps also accumulate sq_v = sum q v^2 (fp32 per chunk, fp64 per warp
+// and dimension).
+template <int N2>
+__global__ void __launch_bounds__(kTThreads, 1)
+    k_stats_y(StatsArgs a, const float* __restrict__ xmax, const float* __restrict__ mumax,
+              const float* __restrict__ vl1_g, const int* __restrict__ itemoff, int nh1, double* part,
+              int64_t part_stride, const float* __restrict__ zin, int dbg) {
+  extern __shared__ __align__(1024) unsigned char sm[];
+  __shared__ uint64_t s_full[kTPairs], s_empty[kTPairs], s_b2ready[2], s_b2free[2], s_ydone;
+  __shared__ uint32_t s_tmem;
+  __shared__ int s_item;
+  __shared__ float s_bmax[kTMma];
+  __shared__ int s_colexp[32];
+  long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  const long long tstart = clock64();
+  const Dims dm = a.dm;
+  const int D = dm.D, H = dm.H, H1 = H + 1;
+  const TcLayout L = tc_layout(D, H);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t sbase = su32(sm);
+  int* s_row = reinterpret_cast<int*>(sm + L.off_row_y);
+  double* s_q = reinterpret_cast<double*>(sm + L.off_q_y);
+  int* s_k = reinterpret_cast<int*>(sm + L.off_k_y);
+  float* s_sqw = reinterpret_cast<float*>(sm + L.off_sqw);
+  if (tid == 0) {
+    for (int i = 0; i < kTPairs; ++i) {
+      binit(&s_full[i], 2 * kTFill);
+      binit(&s_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      binit(&s_b2ready[i], 4);
+      binit(&s_b2free[i], 1);
+    }
+    binit(&s_ydone, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == kTMma) {  // Y_v: hi*hi at 0, corrections at 256 (npair x N2 <= 224 columns each)
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&s_tmem)), "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tfence_before();
+  __syncthreads();
+  tfence_after();
+  const uint32_t tmem = s_tmem;
+  const uint32_t tY = tmem, tYc = tmem + 256;
+  const int total = __ldg(itemoff + dm.C);
+  uint32_t gp = 0, ntile = 0, ny = 0;
+  for (;;) {
+    __syncthreads();
+    if (tid == 0) s_item = a.qctr ? atomicAdd(a.qctr + 1, 1) : -1;
+    __syncthreads();
+    const int item = s_item;
+    if (item < 0 || item >= total) break;
+    const int c = find_item_t(itemoff, dm.C, item);
+    const int r0 = a.off[c] + (item - itemoff[c]) * kTItemRows;
+    const int nr = min(a.off[c + 1], r0 + kTItemRows) - r0;
+    const int T = (nr + kTR - 1) / kTR;
+    const bool direct = itemoff[c + 1] - itemoff[c] == 1;
+    if (warp < kTMma) {
+      item_rows(a, xmax, __ldg(mumax + c), r0, nr, s_row, s_q, s_k, s_bmax);
+      for (int i = tid; i < kTFill * kTMaxChunks * 64; i += kTMma * 32) s_sqw[i] = 0.f;
+      producers_all_sync();
+      if (tid < N2) {  // B2's column scales from the bounds: |zhat_h| <= |V_h|_1 max_n bound_n
+        float mm = 0.f;
+        for (int w = 0; w < kTMma; ++w) mm = fmaxf(mm, s_bmax[w]);
+        const float bnd = tid < H ? 1.01f * __ldg(vl1_g + (int64_t)c * 16 + tid) * mm * mm * p2(-13)
+                                  : (tid == H ? 1.01f * mm * p2(-13) : 0.f);
+        s_colexp[tid] = sexp(bnd);
+      }
+      producers_all_sync();
+    }
+    if (warp < kTFill) {
+      TC_T0();
+      fill_item<true>(a, L, c, nr, T, sbase, s_row, s_q, s_k, s_full, s_empty, gp, s_sqw, dbg, [](int) {});
+      TC_ACC(0);
+    } else if (warp < kTMma) {
+      // ---- B2 builders (warps 8-11): thread = tile row
+      const int r = (warp - kTEpi0) * 32 + lane;
+      for (int t = 0; t < T; ++t) {
+        const uint32_t tt = ntile + t, bb = tt & 1u;
+        if (tt >= 2) {
+          TC_T0();
+          bwait(&s_b2free[bb], tt / 2);
+          TC_ACC(1);
+        }
+        const int rt = t * kTR + r;
+        const bool lv = rt < nr;
+        const float* zi = zin + (int64_t)(r0 + (lv ? rt : 0)) * H;
+        const float qs = lv ? static_cast<float>(s_q[rt]) : 0.f;
+        const int kr = lv ? s_k[rt] : 0;
+        const uint32_t b2 = sbase + L.off_B2 + bb * (2 * 2 * N2 * 128);
+        const int kc = r >> 6, rl = r & 63;
+#pragma unroll 4
+        for (int h = 0; h < N2; ++h) {
+          float b = 0.f;
+          if (lv && h < H1) b = qs * (h < H ? __ldg(zi + h) : 1.f) * p2(s_colexp[h] - kr);
+          __half bh, bl;
+          split1(b, bh, bl);
+          const uint32_t o = (kc * N2 + h) * 128 + (((rl >> 3) ^ (h & 7)) << 4) + (rl & 7) * 2;
+          asm volatile("st.shared.b16 [%0], %1;" ::"r"(b2 + o), "h"(*reinterpret_cast<uint16_t*>(&bh)) : "memory");
+          asm volatile("st.shared.b16 [%0], %1;" ::"r"(b2 + 2 * N2 * 128 + o), "h"(*reinterpret_cast<uint16_t*>(&bl))
+                       : "memory");
+        }
+        fence_async();
+        __syncwarp();
+        if (lane == 0) barrive(&s_b2ready[bb]);
+      }
+    } else {
+      // ---- MMA issuer
+      const bool leader = lane == 0;
+      const uint32_t id2 = idesc(N2, true);
+      uint32_t g = gp;
+      for (int t = 0; t < T; ++t) {
+        const uint32_t tt = ntile + t, bb = tt & 1u;
+        bwait(&s_b2ready[bb], tt / 2 + 1);
+        tfence_after();
+        const uint32_t b2 = sbase + L.off_B2 + bb * (2 * 2 * N2 * 128);
+        for (int p = 0; p < L.npair; ++p, ++g) {
+          const int slot = static_cast<int>(g % kTPairs);
+          {
+            TC_T0();
+            bwait(&s_full[slot], g / kTPairs + 1);
+            TC_ACC(2);
+          }
+          tfence_after();
+          if (leader && !(dbg & 1)) {
+            const uint32_t ah = sbase + slot * kTPairBytes, al = ah + 2 * kTUnit;
+#pragma unroll
+            for (int kk = 0; kk < kTR / 16; ++kk) {
+              const uint32_t oa = kk * 2048;  // 16 tile rows = two 8-row groups
+              const uint32_t bh = b2 + (kk >> 2) * N2 * 128 + (kk & 3) * 32, bl = bh + 2 * N2 * 128;
+              const uint32_t acc = (t > 0 || kk > 0) ? 1u : 0u;
+              // the small correction products in their own accumulator (the
+              // tensor core's accumulation truncates)
+              mma_ss(tYc + p * N2, desc(al + oa, kTUnit), desc(bh, 16), id2, acc);
+              mma_ss(tYc + p * N2, desc(ah + oa, kTUnit), desc(bl, 16), id2, 1u);
+              mma_ss(tY + p * N2, desc(ah + oa, kTUnit), desc(bh, 16), id2, acc);
+            }
+            tcommit(&s_empty[slot]);
+          }
+          __syncwarp();
+        }
+        if (leader) tcommit(&s_b2free[bb]);
+        __syncwarp();
+      }
+      if (leader) tcommit(&s_ydone);
+      __syncwarp();
+    }
+    // ---- item end: Y_v (warps 0-3: TMEM lanes = a pair's 128 dimensions) and sq_v
+    ++ny;
+    if (warp < kTMma) {
+      bwait(&s_ydone, ny);
+      tfence_after();
+      if (warp < 4) {
+        double* pp = direct ? nullptr : part + (int64_t)item * part_stride;
+        for (int j = 0; j < L.npair; ++j) {
+          const int d = j * 128 + warp * 32 + lane;
+#pragma unroll
+          for (int h0 = 0; h0 < N2; h0 += 8) {
+            if (h0 >= H1) break;
+            float y[8], yc[8];
+            tld8(tY + (static_cast<uint32_t>(warp * 32) << 16) + j * N2 + h0, y);
+            tld8(tYc + (static_cast<uint32_t>(warp * 32) << 16) + j * N2 + h0, yc);
+            tld_wait();
+            if (d < D) {
+#pragma unroll
+              for (int u = 0; u < 8; ++u) {
+                const int h = h0 + u;
+                if (h >= H1) break;
+                const double v = static_cast<double>(y[u] + yc[u]) * static_cast<double>(p2(-s_colexp[h]));
+                if (direct) a.Y[((int64_t)c * H1 + h) * D + d] = v;
+                else pp[(int64_t)h * D + d] = v;
+              }
+            }
+          }
+        }
+      }
+      producers_all_sync();
+      for (int d = tid; d < D; d += kTMma * 32) {
+        double v = 0.0;
+        for (int w = 0; w < kTFill; ++w) v += static_cast<double>(s_sqw[(int64_t)w * kTMaxChunks * 64 + d]);
+        if (direct) a.sq[(int64_t)c * D + d] = v;
+        else part[(int64_t)item * part_stride + (int64_t)nh1 * D + d] = v;
+      }
+      tfence_before();
+    }
+    gp += static_cast<uint32_t>(T * L.npair);
+    ntile += static_cast<uint32_t>(T);
+  }
+  tfence_before();
+  __syncthreads();
+  tfence_after();
+  if (warp == kTMma) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  if ((dbg & 4) && blockIdx.x == 0 && (tid == 0 || tid == kTEpi0 * 32 || tid == kTMma * 32))
+    printf("stats_y %d: total %lld fill %lld b2free %lld full %lld\n", warp, clock64() - tstart, prof[0], prof[1],
+           prof[2]);
 }
 
 // GEMM i's B for component c, built once per precompute: V_c^T rows h
@@ -662,27 +797,32 @@ cudaError_t launch_stats_vimg(const Dims& dm, const float* V32, void* img, int* 
 }
 
 bool stats_tc_ok(const Dims& dm) {
+  const TcLayout L = tc_layout(dm.D, dm.H);
   return dm.D % 4 == 0 && dm.D <= kTMaxChunks * 64 && dm.H >= 1 && dm.H <= 16 &&
-         tc_layout(dm.D, dm.H).total <= 227 * 1024;
+         L.total_z <= 227 * 1024 - 4096 && L.total_y <= 227 * 1024 - 4096;  // (+ static)
 }
 int stats_tc_rows() { return kTItemRows; }
 
+// two passes over the K-pairs (vmfa_stats_tc.cu header): k_stats_z (zhat to
+// zbuf, E), then k_stats_y (Y_v, sq_v); qctr[0], qctr[1] their work queues
 cudaError_t launch_stats_tc(const StatsArgs& a, const float* xmax, const float* mumax, const int* itemoff, int nh1,
                             double* part, int64_t part_stride, cudaStream_t s) {
-  if (!a.vimg || !a.vexp || !a.vl1) return cudaErrorInvalidValue;
+  if (!a.vimg || !a.vexp || !a.vl1 || !a.zbuf || !a.qctr) return cudaErrorInvalidValue;
   const TcLayout L = tc_layout(a.dm.D, a.dm.H);
-  const size_t smem = L.total;
+  static const int dbg = [] {
+    const char* v = std::getenv("VMFA_STATS_TC_DBG");  // diagnostics: 1 skip MMAs, 2 skip row loads, 4 cycles
+    return v ? std::atoi(v) : 0;
+  }();
+  if (cudaError_t e = cudaMemsetAsync(a.qctr, 0, 2 * sizeof(int), s); e != cudaSuccess) return e;
+  cudaFuncSetAttribute(k_stats_z<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(L.total_z));
+  k_stats_z<16><<<sm_count(), kTThreads, L.total_z, s>>>(a, xmax, mumax, static_cast<const unsigned char*>(a.vimg),
+                                                          a.vexp, itemoff, nh1, part, part_stride, a.zbuf, dbg);
   auto go = [&](auto kern) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    static const int dbg = [] {
-      const char* v = std::getenv("VMFA_STATS_TC_DBG");  // diagnostics: 1 skip MMAs, 2 skip row loads
-      return v ? std::atoi(v) : 0;
-    }();
-    kern<<<sm_count(), kTThreads, smem, s>>>(a, xmax, mumax, static_cast<const unsigned char*>(a.vimg), a.vexp,
-                                             a.vl1, itemoff, nh1, part, part_stride, dbg);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(L.total_y));
+    kern<<<sm_count(), kTThreads, L.total_y, s>>>(a, xmax, mumax, a.vl1, itemoff, nh1, part, part_stride, a.zbuf, dbg);
   };
-  if (L.HP == 16 && L.N2 == 16) go(k_stats_tc<16, 16>);
-  else if (L.HP == 16 && L.N2 == 32) go(k_stats_tc<16, 32>);
+  if (L.N2 == 16) go(k_stats_y<16>);
+  else if (L.N2 == 32) go(k_stats_y<32>);
   else return cudaErrorInvalidValue;
   return cudaGetLastError();
 }

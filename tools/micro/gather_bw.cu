@@ -5,6 +5,7 @@
 //   mode 2: cp.async.bulk per row by one thread per warp, ring of U rows
 // Reports aggregate GB/s of gathered bytes.
 #include <cstdio>
+#include <cstdlib>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -14,7 +15,7 @@ __device__ __forceinline__ uint64_t hash(uint64_t x) {
   return x;
 }
 
-template <int MODE, int U>
+template <int MODE, int U, int HH = 2>
 __global__ void k(const float4* X, int64_t nrows, int rowb, int rows_per_warp, float* sink) {
   extern __shared__ __align__(128) unsigned char sm[];
   __shared__ uint64_t bar[32][U];
@@ -25,12 +26,12 @@ __global__ void k(const float4* X, int64_t nrows, int rowb, int rows_per_warp, f
   float acc = 0.f;
   if (MODE == 0) {
     for (int r0 = 0; r0 < rows_per_warp; r0 += U) {
-      float4 v[U][2];
+      float4 v[U][HH];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int64_t row = hash(gw * 1000003 + r0 + u) % nrows;
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
+        for (int h = 0; h < HH; ++h) {
           const int o = lane + 32 * h;
           v[u][h] = o < f4 ? __ldg(X + row * f4 + o) : make_float4(0, 0, 0, 0);
         }
@@ -38,7 +39,7 @@ __global__ void k(const float4* X, int64_t nrows, int rowb, int rows_per_warp, f
 #pragma unroll
       for (int u = 0; u < U; ++u)
 #pragma unroll
-        for (int h = 0; h < 2; ++h) acc += v[u][h].x + v[u][h].y + v[u][h].z + v[u][h].w;
+        for (int h = 0; h < HH; ++h) acc += v[u][h].x + v[u][h].y + v[u][h].z + v[u][h].w;
     }
   } else if (MODE == 1) {
     const uint32_t base = smem_u32(sm) + warp * U * rowb;
@@ -130,9 +131,35 @@ __global__ void k(const float4* X, int64_t nrows, int rowb, int rows_per_warp, f
   if (acc == 1234.5f) sink[0] = acc;
 }
 
-int main() {
-  const int64_t nrows = 200000;
-  const int rowb = 1024;
+int main(int argc, char** argv) {
+  const int64_t nrows = argc > 1 ? atoll(argv[1]) : 200000;
+  const int rowb = argc > 2 ? atoi(argv[2]) : 1024;
+  if (argc > 1) {  // large-table mode: LDG gathers of long rows only
+    float4* X;
+    cudaMalloc(&X, nrows * rowb);
+    cudaMemset(X, 0, nrows * rowb);
+    float* sink;
+    cudaMalloc(&sink, 4);
+    for (int rep = 0; rep < 2; ++rep)
+    for (int threads : {256, 512}) {
+      auto kern = rowb <= 512 ? k<0, 24, 1> : k<0, 4, 7>;
+      const int rpw = 512;
+      kern<<<148, threads>>>(X, nrows, rowb, 16, sink);
+      cudaEvent_t e0, e1;
+      cudaEventCreate(&e0);
+      cudaEventCreate(&e1);
+      cudaEventRecord(e0);
+      kern<<<148, threads>>>(X, nrows, rowb, rpw, sink);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      printf("table %.2f GB rows %d B threads %d: %7.1f GB/s %s\n", nrows * (double)rowb / 1e9, rowb, threads,
+             148.0 * (threads / 32) * rpw * rowb / ms / 1e6, cudaGetErrorString(cudaGetLastError()));
+    }
+    // contiguous rows (same kernel, row = sequential): stream reference
+    return 0;
+  }
   float4* X;
   cudaMalloc(&X, nrows * rowb);
   cudaMemset(X, 0, nrows * rowb);

@@ -10,9 +10,11 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
   d |= (uint64_t)1 << 16; d |= (uint64_t)(1024 >> 4) << 32; d |= (uint64_t)1 << 46; d |= (uint64_t)2 << 61;
   return d;
 }
+__device__ int g_amn = 0;  // 1: A MN-major (bit 15), LBO 16 KB between 64-element atoms
 __device__ __forceinline__ uint32_t idesc(int N, int kind_bf16) {
   const uint32_t fmt = kind_bf16 ? 1u : 2u;
-  return (1u << 4) | (fmt << 7) | (fmt << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+  return (1u << 4) | (fmt << 7) | (fmt << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24) |
+         (g_amn ? (1u << 15) : 0u);
 }
 template <int TS, int BF16>
 __global__ void k(int N, int iters, unsigned long long* out) {
@@ -34,7 +36,9 @@ __global__ void k(int N, int iters, unsigned long long* out) {
   const uint32_t tmem = s_tmem;
   if (threadIdx.x == 0) {
     const uint32_t id = idesc(N, BF16);
-    const uint64_t a = sdesc(base), b = sdesc(base + 32 * 1024);
+    uint64_t a = sdesc(base);
+    if (g_amn) a = (a & ~(0x3FFFull << 16)) | ((uint64_t)((16384 >> 4) & 0x3FFF) << 16);
+    const uint64_t b = sdesc(base + 32 * 1024);
     unsigned long long t0 = clock64();
     for (int i = 0; i < iters; ++i) {
       if (TS) {
@@ -57,8 +61,9 @@ __global__ void k(int N, int iters, unsigned long long* out) {
   __syncthreads();
   if (threadIdx.x < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" :: "r"(tmem));
 }
-int main() {
+int main(int argc, char** argv) {
   unsigned long long* d; cudaMalloc(&d, 8);
+  if (argc > 1) { int one = 1; cudaMemcpyToSymbol(g_amn, &one, sizeof one); printf("A MN-major\n"); }
   const int Ns[] = {16, 32, 64, 96, 128, 192, 256};
   for (int ts = 0; ts < 2; ++ts) for (int bf = 0; bf < 2; ++bf) for (int N : Ns) {
     auto kern = ts ? (bf ? k<1,1> : k<1,0>) : (bf ? k<0,1> : k<0,0>);
