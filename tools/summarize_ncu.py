@@ -9,8 +9,8 @@ Writes
   profiles/<round>/launch_shares.txt       per-kernel totals and shares of the list
   profiles/<round>/ncu_full_summary.csv    selected --set full metrics per launch
   profiles/<round>/bench.json              the bench line of the same code
-  profiles/scorer_traffic.json             DRAM bytes of one scoring launch pair
-                                           (anchor + extra), read by bench.py
+  profiles/<round>/scorer_traffic_configN.json  DRAM bytes of one scoring launch
+                                           pair (anchor + extra), read by bench.py
                                            for roofline.traffic
 """
 from __future__ import annotations
@@ -88,6 +88,8 @@ def main():
     ap.add_argument("--launches")
     ap.add_argument("--full")
     ap.add_argument("--bench")
+    ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--full2", help="a second --set full report (other kernels), appended to the summary")
     a = ap.parse_args()
     d = os.path.join(ROOT, "profiles", a.round)
     os.makedirs(d, exist_ok=True)
@@ -99,6 +101,8 @@ def main():
         json.dump(json.loads(line), open(os.path.join(d, "bench.json"), "w"), indent=1)
     if a.full:
         rows = full_summary(a.full)
+        if a.full2:
+            rows += full_summary(a.full2)[2:]
         with open(os.path.join(d, "ncu_full_summary.csv"), "w", newline="") as f:
             csv.writer(f).writerows(rows)
         # scoring launch pair = the anchor launch (the one writing the lj table,
@@ -108,18 +112,18 @@ def main():
         if len(sc) >= 2:
             tcol, rcol, wcol = (h.index(m) for m in ("gpu__time_duration.sum", "dram__bytes_read.sum",
                                                      "dram__bytes_write.sum"))
-            mb = lambda r: (float(r[rcol]) + float(r[wcol]))  # noqa: E731
+            units = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+            rs, ws = units[rows[1][rcol]], units[rows[1][wcol]]  # (read and write may differ in unit)
+            mb = lambda r: float(r[rcol]) * rs + float(r[wcol]) * ws  # noqa: E731
             sc.sort(key=lambda r: float(r[tcol]))
             anchor, extra = sc[-1], sc[0]
-            unit = rows[1][rcol]
-            scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[unit]
             traffic = {"kernel": "k_score_ws (anchor + extra launch of one E-step)",
-                       "bytes_per_launch_pair": (mb(anchor) + mb(extra)) * scale,
-                       "anchor_bytes": mb(anchor) * scale, "extra_bytes": mb(extra) * scale,
+                       "bytes_per_launch_pair": mb(anchor) + mb(extra),
+                       "anchor_bytes": mb(anchor), "extra_bytes": mb(extra),
+                       "anchor_ms": float(anchor[tcol]), "extra_ms": float(extra[tcol]),
                        "source": f"profiles/{a.round}/ncu_full_summary.csv "
                                  "(dram__bytes_read.sum + dram__bytes_write.sum, ncu --set full)"}
-            json.dump(traffic, open(os.path.join(ROOT, "profiles", "scorer_traffic.json"), "w"),
-                      indent=1)
+            json.dump(traffic, open(os.path.join(d, f"scorer_traffic_config{a.config}.json"), "w"), indent=1)
 
 
 if __name__ == "__main__":
