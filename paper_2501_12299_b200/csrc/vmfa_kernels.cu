@@ -541,6 +541,17 @@ __device__ __forceinline__ double from_fixed(long long hi, long long lo) {
 constexpr int kGupdBatch = 4;  // points in flight per warp in k_gupdate
 constexpr int kGupdProbes = 32;  // probe limit of a dense-rows item's hash
 __device__ __forceinline__ unsigned hash_key(int k) { return static_cast<unsigned>(k) * 2654435761u; }
+// Exact 64-bit integer add into shared memory from two native 32-bit atomics
+// (a 64-bit shared atomicAdd compiles to a CAS spin loop on sm_100): the low
+// word's add returns its old value, so its wrap-around is detected exactly
+// and carried into the high word. The pair is read only after a barrier.
+__device__ __forceinline__ void smem_add_u64(unsigned long long* addr, unsigned long long v) {
+  unsigned* w = reinterpret_cast<unsigned*>(addr);
+  const unsigned lo = static_cast<unsigned>(v), hi = static_cast<unsigned>(v >> 32);
+  const unsigned old = atomicAdd(w, lo);
+  const unsigned up = hi + (old + lo < old ? 1u : 0u);
+  if (up) atomicAdd(w + 1, up);
+}
 
 struct KeyMin {
   double v;
@@ -582,9 +593,13 @@ __global__ void __launch_bounds__(kGupdThreads) k_gupdate(GupdArgs a, int capmax
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nw = kGupdThreads / 32;
   const int64_t CC = (int64_t)dm.C * dm.C;
-  long long* g_cnt = a.gt_cnt + (int64_t)blockIdx.x * dm.C;
-  long long* g_hi = a.gt_hi + (int64_t)blockIdx.x * dm.C;
-  long long* g_lo = a.gt_lo + (int64_t)blockIdx.x * dm.C;
+  // capmax < 0: the dense table (one (cnt, hi, lo) entry per component,
+  // indexed by c~, no probing) lives in shared memory (C <= kGupdDenseMax);
+  // otherwise the per-CTA global tables back the hash
+  const bool sdense = capmax < 0;
+  long long* g_cnt = sdense ? reinterpret_cast<long long*>(smem_raw) : a.gt_cnt + (int64_t)blockIdx.x * dm.C;
+  long long* g_hi = sdense ? g_cnt + dm.C : a.gt_hi + (int64_t)blockIdx.x * dm.C;
+  long long* g_lo = sdense ? g_hi + dm.C : a.gt_lo + (int64_t)blockIdx.x * dm.C;
   const int total = a.itemoff[dm.C];
   for (int item = blockIdx.x; item < total; item += gridDim.x) {
     const int c = find_item(a.itemoff, dm.C, item);
@@ -596,7 +611,9 @@ __global__ void __launch_bounds__(kGupdThreads) k_gupdate(GupdArgs a, int capmax
     const long long bound = llmin((long long)dm.C - 1, (long long)npts * (dm.stride - 1));
     int cap = 32;
     bool use_smem;
-    if (to_rows && (a.xc || a.list)) {  // small table sized for the typical key count; overflow adds into row c of xc (or the list)
+    if (sdense) {
+      use_smem = false;
+    } else if (to_rows && (a.xc || a.list)) {  // small table sized for the typical key count; overflow adds into row c of xc (or the list)
       while (cap < 2 * bound && cap < min(capmax, kGupdRowsCap)) cap <<= 1;
       use_smem = true;
     } else {
@@ -696,13 +713,19 @@ __global__ void __launch_bounds__(kGupdThreads) k_gupdate(GupdArgs a, int capmax
               atomicAdd(reinterpret_cast<unsigned long long*>(a.xc + 2 * CC + at), static_cast<unsigned long long>(lo));
             } else {
               atomicAdd(t_cnt + h, 1);
-              atomicAdd(reinterpret_cast<unsigned long long*>(t_hi + h), static_cast<unsigned long long>(hi));
-              atomicAdd(reinterpret_cast<unsigned long long*>(t_lo + h), static_cast<unsigned long long>(lo));
+              smem_add_u64(reinterpret_cast<unsigned long long*>(t_hi + h), static_cast<unsigned long long>(hi));
+              smem_add_u64(reinterpret_cast<unsigned long long*>(t_lo + h), static_cast<unsigned long long>(lo));
             }
-          } else {
-            atomicAdd(reinterpret_cast<unsigned long long*>(g_cnt + ct), 1ULL);
-            atomicAdd(reinterpret_cast<unsigned long long*>(g_hi + ct), static_cast<unsigned long long>(hi));
-            atomicAdd(reinterpret_cast<unsigned long long*>(g_lo + ct), static_cast<unsigned long long>(lo));
+          } else if (sdense) {  // (shared-memory atomics: the pointers below are known to be shared)
+            unsigned long long* d = reinterpret_cast<unsigned long long*>(smem_raw);
+            atomicAdd(reinterpret_cast<unsigned*>(d + ct), 1u);  // (count < 2^32: the high word stays 0)
+            smem_add_u64(d + dm.C + ct, static_cast<unsigned long long>(hi));
+            smem_add_u64(d + 2 * dm.C + ct, static_cast<unsigned long long>(lo));
+          } else {  // (the per-CTA global tables)
+            const int64_t gb = (int64_t)blockIdx.x * dm.C + ct;
+            atomicAdd(reinterpret_cast<unsigned long long*>(a.gt_cnt + gb), 1ULL);
+            atomicAdd(reinterpret_cast<unsigned long long*>(a.gt_hi + gb), static_cast<unsigned long long>(hi));
+            atomicAdd(reinterpret_cast<unsigned long long*>(a.gt_lo + gb), static_cast<unsigned long long>(lo));
           }
           }
         }
@@ -3126,7 +3149,13 @@ int gupd_capmax(const Dims& dm, int pts_per_item) {
 cudaError_t launch_gupdate(const GupdArgs& a, int grid, cudaStream_t s) {
   int capmax = gupd_capmax(a.dm, a.pts_per_item);
   if (a.force_rows) capmax = std::min(capmax, kGupdRowsCap);
-  const size_t smem = static_cast<size_t>(capmax) * (2 * sizeof(long long) + 2 * sizeof(int));
+  size_t smem = static_cast<size_t>(capmax) * (2 * sizeof(long long) + 2 * sizeof(int));
+  // small C: a dense (cnt, hi, lo) row per CTA in shared memory -- no hash
+  // probing, and 24 C bytes instead of 24 cap (config 3: 96 KB, two CTAs per SM)
+  if (a.dm.C <= kGupdDenseMax && !a.dump) {
+    capmax = -1;
+    smem = static_cast<size_t>(a.dm.C) * 3 * sizeof(long long);
+  }
   cudaFuncSetAttribute(k_gupdate, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   k_gupdate<<<grid, kGupdThreads, smem, s>>>(a, capmax);
   return cudaGetLastError();
