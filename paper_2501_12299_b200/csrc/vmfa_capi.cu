@@ -101,6 +101,7 @@ struct vmfa_ctx {
   int* svexp = nullptr;
   float* svl1 = nullptr;
   float* szbuf = nullptr;  // its zhat per K-pair (N C' x H)
+  uint16_t* limg = nullptr;  // image-free anchor stages: per (anchor, group, chunk) lin / psi rows (fp16)
   unsigned long long* nfix = nullptr;         // scores re-evaluated in fp64 (vmfa_fixup.cu), accumulated
   long long* fix_list = nullptr;              // flagged scores of one scoring launch
   unsigned long long* fix_cnt = nullptr;      // [count, overflow]
@@ -348,7 +349,7 @@ cudaError_t run_score(vmfa_ctx* x, int mode, const ScoreArgs& a) {
       return e;
     return launch_score_ws(mode, a,
                            WsOperands{x->xmax, x->mumax, x->mu32, x->brec, x->srec, x->bimg, x->bscl, x->simg, x->sscl,
-                                      x->fix_list, x->fix_cnt, x->fix_cap},
+                                      x->fix_list, x->fix_cnt, x->fix_cap, x->limg},
                            x->jobs, x->stream);
   }
   if (x->scorer == 1) return launch_score_tc(mode, a, x->WT, x->ipsi32, x->mu32, x->stream);
@@ -424,7 +425,7 @@ int run_precompute(vmfa_ctx* x, int* failed, bool sync = true) {
   a.logdet = x->logdet;
   a.logpi = x->logpi;
   a.kconst = x->kconst;
-  a.P = x->P;
+  a.P = x->scorer == 0 ? x->P : nullptr;  // (the FFMA scorer's packed rows)
   a.V32 = x->V32;
   a.mu32 = x->mu32;
   a.WT = x->WT;
@@ -470,7 +471,8 @@ int score_anchors(vmfa_ctx* x) {
   TRY(ensure_kinv_current(x));
   if (x->scorer == 2) {
     const int tok = x->begin(kFamOther, dm.C);
-    CU(launch_ws_images(dm, 0, x->WT, x->mu32, x->ipsi32, x->g, x->gcnt, x->bimg, x->bscl, s, x->sscl, x->brec));
+    CU(launch_ws_images(dm, 0, x->WT, x->mu32, x->ipsi32, x->g, x->gcnt, x->bimg, x->bscl, s, x->sscl, x->brec,
+                        x->limg));
     CU(launch_ws_records(dm, 0, x->WT, x->mu32, x->ipsi32, x->kconst, x->g, x->gcnt, x->bscl, x->brec, s, 1));
     x->end(tok);
   }
@@ -1077,6 +1079,11 @@ int vmfa_ctx_create(vmfa_ctx** out, int device, int C, int D, int H, int Cp, int
     x->fix_cap = std::max<long long>(1 << 20, std::min<long long>(static_cast<long long>(N) * dm.SL, 1LL << 26));
     A(x->jobs, static_cast<size_t>(x->fix_cap) / 128 + Cs + 2);
     A(x->bimg, ws_image_halves(dm, 0));
+    // image-free anchor stages, opt-in (VMFA_IMAGE_FREE=1): the loader then
+    // assembles every stage from 3 + 2 G bulk copies, which measured slower at
+    // config 3 (anchor pass 7.84 -> 9.66 ms) than one copy of the prebuilt image
+    if (ws_image_free_ok(dm) && std::getenv("VMFA_IMAGE_FREE") && std::getenv("VMFA_IMAGE_FREE")[0] == '1')
+      A(x->limg, ws_small_image_halves(dm));
     A(x->simg, ws_image_halves(dm, 1));
     A(x->bscl, ws_scale_floats(dm, 0));
     A(x->brec, ws_record_floats(dm, 0));

@@ -2627,7 +2627,7 @@ __global__ void __launch_bounds__(128) k_precompute(PrecompArgs a) {
             for (int i = 0; i < 4; ++i) {
               const int h = h0 + i;
               if (h >= H) continue;
-              a.P[((int64_t)c * D + d) * HP + h] = static_cast<float>(w[i][j]);
+              if (a.P) a.P[((int64_t)c * D + d) * HP + h] = static_cast<float>(w[i][j]);
               a.WT[((int64_t)c * a.Hp + h) * D + d] = static_cast<float>(w[i][j]);
               if (a.W64) a.W64[((int64_t)c * H + h) * D + d] = w[i][j];
               a.V32[((int64_t)c * D + d) * H + h] = static_cast<float>(v[i][j]);
@@ -2639,14 +2639,16 @@ __global__ void __launch_bounds__(128) k_precompute(PrecompArgs a) {
           const int d = d0 + dd;
           if (d >= D) continue;
           const double ip = 1.0 / psi[d];
-          float* row = a.P + ((int64_t)c * D + d) * HP;
-          for (int h = H; h < Hc; ++h) row[h] = 0.f;
+          if (a.P) {
+            float* row = a.P + ((int64_t)c * D + d) * HP;
+            for (int h = H; h < Hc; ++h) row[h] = 0.f;
+            row[Hc] = static_cast<float>(a.mu[(int64_t)c * D + d]);
+            row[Hc + 1] = static_cast<float>(ip);
+            row[Hc + 2] = 0.f;
+            row[Hc + 3] = 0.f;
+          }
           for (int h = H; h < a.Hp; ++h) a.WT[((int64_t)c * a.Hp + h) * D + d] = 0.f;
           a.ipsi32[(int64_t)c * D + d] = static_cast<float>(ip);
-          row[Hc] = static_cast<float>(a.mu[(int64_t)c * D + d]);
-          row[Hc + 1] = static_cast<float>(ip);
-          row[Hc + 2] = 0.f;
-          row[Hc + 3] = 0.f;
           a.mu32[(int64_t)c * D + d] = static_cast<float>(a.mu[(int64_t)c * D + d]);
         }
       }
@@ -2686,24 +2688,27 @@ __global__ void __launch_bounds__(128) k_precompute_rows(PrecompArgs a) {
         u[i] = t * s_rinv[i];
       }
     }
-    float* row = a.P + ((int64_t)c * D + d) * HP;
 #pragma unroll
     for (int h = 0; h < HM; ++h)
       if (h < H) {
-        const float f = static_cast<float>(u[h]);
-        row[h] = f;
-        a.WT[((int64_t)c * a.Hp + h) * D + d] = f;
+        a.WT[((int64_t)c * a.Hp + h) * D + d] = static_cast<float>(u[h]);
         if (a.W64) a.W64[((int64_t)c * H + h) * D + d] = u[h];
       }
-    for (int h = H; h < Hc; ++h) row[h] = 0.f;
     for (int h = H; h < a.Hp; ++h) a.WT[((int64_t)c * a.Hp + h) * D + d] = 0.f;
     const double mud = a.mu[(int64_t)c * D + d];
     a.ipsi32[(int64_t)c * D + d] = static_cast<float>(ip);
-    row[Hc] = static_cast<float>(mud);
-    row[Hc + 1] = static_cast<float>(ip);
-    row[Hc + 2] = 0.f;
-    row[Hc + 3] = 0.f;
     a.mu32[(int64_t)c * D + d] = static_cast<float>(mud);
+    if (a.P) {  // the FFMA scorer's packed rows (only that scorer reads them)
+      float* row = a.P + ((int64_t)c * D + d) * HP;
+#pragma unroll
+      for (int h = 0; h < HM; ++h)
+        if (h < H) row[h] = static_cast<float>(u[h]);
+      for (int h = H; h < Hc; ++h) row[h] = 0.f;
+      row[Hc] = static_cast<float>(mud);
+      row[Hc + 1] = static_cast<float>(ip);
+      row[Hc + 2] = 0.f;
+      row[Hc + 3] = 0.f;
+    }
 #pragma unroll
     for (int i = HM - 1; i >= 0; --i) {  // backward: v = R^-T w => V column d
       if (i < H) {
@@ -2714,9 +2719,18 @@ __global__ void __launch_bounds__(128) k_precompute_rows(PrecompArgs a) {
         u[i] = t * s_rinv[i];
       }
     }
+    float* vrow = a.V32 + ((int64_t)c * D + d) * H;
+    if ((H & 3) == 0) {  // 16-byte stores
 #pragma unroll
-    for (int h = 0; h < HM; ++h)
-      if (h < H) a.V32[((int64_t)c * D + d) * H + h] = static_cast<float>(u[h]);
+      for (int h = 0; h < HM; h += 4)
+        if (h < H)
+          *reinterpret_cast<float4*>(vrow + h) = make_float4(static_cast<float>(u[h]), static_cast<float>(u[h + 1]),
+                                                             static_cast<float>(u[h + 2]), static_cast<float>(u[h + 3]));
+    } else {
+#pragma unroll
+      for (int h = 0; h < HM; ++h)
+        if (h < H) vrow[h] = static_cast<float>(u[h]);
+    }
   }
 }
 

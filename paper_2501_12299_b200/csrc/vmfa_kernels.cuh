@@ -292,6 +292,7 @@ struct WsOperands {
   long long* fix_list = nullptr;           // flagged scores: output indices (vmfa_fixup.cu)
   unsigned long long* fix_cnt = nullptr;   // [0] count, [1] overflow
   long long fix_cap = 0;
+  const void* limg = nullptr;  // image-free anchor stages: lin / psi images (bimg unused)
 };
 // fp64 re-evaluation of the scores the tensor-core scorer flagged (vmfa_fixup.cu)
 struct FixArgs {
@@ -375,7 +376,9 @@ int64_t ws_image_halves(const Dims& dm, int single);
 int64_t ws_scale_floats(const Dims& dm, int single);
 cudaError_t launch_ws_images(const Dims& dm, int single, const float* WT, const float* mu32, const float* ipsi32,
                              const int* g, const int* gcnt, void* img, float* bscl, cudaStream_t s,
-                             const float* sscl = nullptr, float* rec = nullptr);
+                             const float* sscl = nullptr, float* rec = nullptr, void* limg = nullptr);
+int64_t ws_small_image_halves(const Dims& dm);
+bool ws_image_free_ok(const Dims& dm);
 // per-row max |value| of an N x D fp32 matrix (A-row scale bounds)
 cudaError_t launch_rowmax(int64_t N, int D, const float* X, float* xmax, cudaStream_t s);
 

@@ -78,6 +78,12 @@ __host__ __device__ constexpr int qg_max(int Hp) { return (256 - 2 * kNL) / Hp <
 struct WsArgs {
   Dims dm;
   int mode;
+  // image-free anchor stages (Hp % 8 == 0): per (anchor, group, chunk) a
+  // small image [lin hi | lin lo | psi hi | psi lo] (16 lines each) and the
+  // W rows of every component copied from its one-component image
+  const __half* limg;
+  const __half* simg1;
+  int N1max1;
   int Hp;            // W rows per component (>= 8)
   int qg;            // components per job (group)
   int N1max;         // 16 + round16(qg * Hp)
@@ -549,14 +555,35 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_ws(WsArgs a, const __grid
         }
         const int ng = a.mode == kModeAnchor ? a.ngroups : 1;
         const __half* src0 = a.img + ((int64_t)c * ng + grp) * nchunk * (a.stage_bytes / 2);
+        const bool ifree = a.mode == kModeAnchor && a.limg != nullptr;
+        const int nq = min(a.qg, w.J.w - w.g0);
+        const uint32_t wb = HP * 128;                 // one plane of a component's W rows
+        const uint32_t s1 = 2 * 128 * (a.N1max1 + kNL);  // one-component stage bytes
         for (int ch = 0; ch < nchunk; ++ch, ++bc) {
           const int s = static_cast<int>(bc % NB);
           const uint32_t use = bc / NB;
           if (use >= 1) mbar_wait(&s_bempty[s], (use - 1) & 1u);
           trace(tp, static_cast<int>(bc), 5);
-          mbar_arrive_expect_tx(&s_bfull[s], a.stage_bytes);
-          bulk_copy(sbase + s * a.stage_bytes, src0 + (int64_t)ch * (a.stage_bytes / 2), a.stage_bytes,
-                    &s_bfull[s]);
+          const uint32_t dst = sbase + s * a.stage_bytes;
+          if (!ifree) {
+            mbar_arrive_expect_tx(&s_bfull[s], a.stage_bytes);
+            bulk_copy(dst, src0 + (int64_t)ch * (a.stage_bytes / 2), a.stage_bytes, &s_bfull[s]);
+          } else {
+            // stage = [B1 hi: lin 16 | W of q_0..q_nq-1 | B1 lo: same | B2 hi | B2 lo]
+            const __half* li = a.limg + (((int64_t)c * ng + grp) * nchunk + ch) * (4 * kNL * 64);
+            const uint32_t lo1 = a.N1max * 128;  // B1 lo plane offset (bytes)
+            mbar_arrive_expect_tx(&s_bfull[s], 4u * kNL * 128u + 2u * wb * static_cast<uint32_t>(nq));
+            bulk_copy(dst, li, kNL * 128, &s_bfull[s]);                          // lin hi
+            bulk_copy(dst + lo1, li + kNL * 64, kNL * 128, &s_bfull[s]);         // lin lo
+            bulk_copy(dst + 2 * lo1, li + 2 * kNL * 64, 2 * kNL * 128, &s_bfull[s]);  // psi hi | psi lo
+            for (int qi = 0; qi < nq; ++qi) {
+              const int q = __ldg(a.g + (int64_t)c * dm.G + w.g0 + qi);
+              const __half* sq = a.simg1 + ((int64_t)q * nchunk + ch) * (s1 / 2);
+              const uint32_t o = (kNL + qi * HP) * 128;
+              bulk_copy(dst + o, sq + kNL * 64, wb, &s_bfull[s]);                              // W hi
+              bulk_copy(dst + lo1 + o, sq + (a.N1max1 + kNL) * 64, wb, &s_bfull[s]);           // W lo
+            }
+          }
           trace(tp, static_cast<int>(bc), 6);
         }
       }
@@ -845,7 +872,7 @@ __global__ void __launch_bounds__(256) k_build_records(Dims dm, int Hp, int qg, 
 __global__ void __launch_bounds__(256) k_build_images(Dims dm, int Hp, int qg, int ngroups, int N1max, int single,
                                                       const float* WT, const float* mu32, const float* ipsi32,
                                                       const int* g, const int* gcnt, __half* img, float* bscl,
-                                                      const float* sscl, int N1max1, float* rec) {
+                                                      const float* sscl, int N1max1, float* rec, __half* limg) {
   const int lane = threadIdx.x & 31;
   const int nchunk = (dm.D + kKC - 1) / kKC;
   const int ng = single ? 1 : ngroups;
@@ -931,9 +958,21 @@ __global__ void __launch_bounds__(256) k_build_images(Dims dm, int Hp, int qg, i
     if (lane == 0) bscl[((int64_t)a * ng + grp) * nrow + row] = exp2i(-k);
     // matrix offsets (halves) within a stage: B1 hi 0, B1 lo N1max*64, B2 hi 2*N1max*64, B2 lo +16*64
     const int rr = row < N1max ? row : row - N1max;
-    const int64_t off_hi = row < N1max ? 0 : 2 * (int64_t)N1max * 64;
-    const int64_t off_lo = row < N1max ? (int64_t)N1max * 64 : 2 * (int64_t)N1max * 64 + kNL * 64;
+    int64_t off_hi = row < N1max ? 0 : 2 * (int64_t)N1max * 64;
+    int64_t off_lo = row < N1max ? (int64_t)N1max * 64 : 2 * (int64_t)N1max * 64 + kNL * 64;
     __half* base = img + ((int64_t)a * ng + grp) * nchunk * stage_h;
+    int64_t sth = stage_h;
+    // limg != null (image-free anchor stages): only the lin and psi rows are
+    // written, into the small image [lin hi | lin lo | psi hi | psi lo] (16
+    // lines each, the same line positions and swizzle as in the stage); the W
+    // rows come from the one-component images at scoring time
+    const bool wimg = limg == nullptr || (row < N1max ? row < kNL : true);
+    if (limg != nullptr) {
+      base = limg + ((int64_t)a * ng + grp) * nchunk * (4 * kNL * 64);
+      sth = 4 * kNL * 64;
+      off_hi = row < N1max ? 0 : 2 * kNL * 64;
+      off_lo = off_hi + kNL * 64;
+    }
     // rec != null (anchor images): the record sums ride along -- a W row h of
     // q gives b_h = sum_d W_q[h][d] (mu_q - mu_a)[d], the psi row of q gives
     // m = sum_d psi_q^-1 (mu_q - mu_a)^2 (fp32 differences as the scorer's
@@ -954,11 +993,12 @@ __global__ void __launch_bounds__(256) k_build_images(Dims dm, int Hp, int qg, i
           }
         }
       }
+      if (!wimg) continue;
       uint32_t hw[4], lw[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i) split2(v[2 * i] * sc, v[2 * i + 1] * sc, hw[i], lw[i]);
       const int pos = rr * 64 + (((j ^ (rr & 7)) & 7) << 3);  // 128B swizzle: 16-byte unit j of row rr
-      __half* st = base + ch * stage_h;
+      __half* st = base + ch * sth;
       *reinterpret_cast<uint4*>(st + off_hi + pos) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
       *reinterpret_cast<uint4*>(st + off_lo + pos) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
     }
@@ -1021,6 +1061,13 @@ int64_t ws_image_halves(const Dims& dm, int single) {
   const int ng = single ? 1 : ws_groups(dm);
   return (int64_t)dm.C * ng * nchunk * 2 * 64 * (ws_n1max(dm, single) + kNL);
 }
+// image-free anchor stages: the per-(anchor, group, chunk) lin / psi image
+// (halves), and whether the W rows can be copied from the one-component
+// images with their swizzle phase intact (Hp a multiple of 8)
+int64_t ws_small_image_halves(const Dims& dm) {
+  return (int64_t)dm.C * ws_groups(dm) * ((dm.D + kKC - 1) / kKC) * 4 * kNL * 64;
+}
+bool ws_image_free_ok(const Dims& dm) { return ws_hp(dm.H) % 8 == 0; }
 int64_t ws_scale_floats(const Dims& dm, int single) {
   const int ng = single ? 1 : ws_groups(dm);
   return (int64_t)dm.C * ng * (ws_n1max(dm, single) + kNL);
@@ -1031,11 +1078,12 @@ int64_t ws_record_floats(const Dims& dm, int single) {
 
 cudaError_t launch_ws_images(const Dims& dm, int single, const float* WT, const float* mu32, const float* ipsi32,
                              const int* g, const int* gcnt, void* img, float* bscl, cudaStream_t s,
-                             const float* sscl, float* rec) {
+                             const float* sscl, float* rec, void* limg) {
   k_build_images<<<sm_count() * 8, 256, 0, s>>>(dm, ws_hp(dm.H), ws_qg(dm, single), ws_groups(dm),
                                                 ws_n1max(dm, single), single, WT, mu32, ipsi32, g, gcnt,
                                                 static_cast<__half*>(img), bscl, single ? nullptr : sscl,
-                                                ws_n1max(dm, 1), single ? nullptr : rec);
+                                                ws_n1max(dm, 1), single ? nullptr : rec,
+                                                single ? nullptr : static_cast<__half*>(limg));
   return cudaGetLastError();
 }
 
@@ -1193,6 +1241,9 @@ cudaError_t launch_score_ws(int mode, const ScoreArgs& s, const WsOperands& op, 
   a.mu32 = op.mu32;
   a.rec = single ? op.srec : op.brec;
   a.img = static_cast<const __half*>(single ? op.simg : op.bimg);
+  a.limg = single ? nullptr : static_cast<const __half*>(op.limg);
+  a.simg1 = static_cast<const __half*>(op.simg);
+  a.N1max1 = ws_n1max(s.dm, 1);
   a.ngroups = ws_groups(s.dm);
   a.jobs = jobs;
   a.itemoff = s.itemoff;

@@ -61,10 +61,14 @@ def test_precompute_caches_match_oracle(oracle, gpu):
     dict(N=2000, D=100, C=50, H=16, Cp=4, G=8),   # H=16 chunk
     dict(N=1500, D=64, C=60, H=12, Cp=3, G=18),   # two component groups per anchor job (G > 15)
 ])
-@pytest.mark.parametrize("scorer", ["ws", "tc", "ffma"])
+@pytest.mark.parametrize("scorer", ["ws", "ws-imagefree", "tc", "ffma"])
 def test_estep_teacher_forced(oracle, gpu, case, scorer, monkeypatch):
+    # ws-imagefree: the warp-specialised scorer assembling each anchor stage
+    # from the one-component images (VMFA_IMAGE_FREE=1, opt-in)
     O, V = oracle, gpu
-    monkeypatch.setenv("VMFA_SCORER", scorer)
+    monkeypatch.setenv("VMFA_SCORER", scorer.split("-")[0])
+    if scorer == "ws-imagefree":
+        monkeypatch.setenv("VMFA_IMAGE_FREE", "1")
     X, _ = gaussian_problem(case["N"], case["D"], max(case["C"] // 2, 2), min(case["H"], 4), seed=7)
     C, H, Cp, G = case["C"], case["H"], case["Cp"], case["G"]
     p, st, floor, sess = _setup(O, V, X, C, H, Cp, G)
