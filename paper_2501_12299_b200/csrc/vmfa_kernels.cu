@@ -1637,6 +1637,11 @@ __device__ __forceinline__ void mma3c(float (&acc)[4], const float (&ah)[4], con
 // to the row ring), fresh accumulators per k-step, and with H + 1 = 17 the
 // constant column of [zhat; 1] (Y_v[:, H] = sum q v) accumulated by FFMA next
 // to sq_v while the m16 tile holds the 16 latent columns.
+__device__ __forceinline__ void dmma_e(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
 template <int NTH, int NTW, bool BIG>
 __global__ void __launch_bounds__(kStatsThreads, BIG ? 1 : 2) k_stats_mma(StatsArgs a, const int* __restrict__ itemoff,
                                                                int rows_per_item, int nh1, double* part,
@@ -1667,6 +1672,7 @@ __global__ void __launch_bounds__(kStatsThreads, BIG ? 1 : 2) k_stats_mma(StatsA
   const bool cfma = H1 > 16;  // constant column by FFMA (BIG only)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int gid = lane >> 2, tig = lane & 3;
+  __shared__ double s_ecc[12][32];  // E tiles (warp 0's DMMA fragments, kept in shared memory between batches)
   // E: thread = (upper-triangle entry, row group)
   const int NE = H1 * (H1 + 1) / 2;
   const int EG = max(1, kStatsThreads / NE);
@@ -1738,7 +1744,10 @@ __global__ void __launch_bounds__(kStatsThreads, BIG ? 1 : 2) k_stats_mma(StatsA
     const double qdiv = qmax > 0.0 ? qmax : 1.0;
     const int nbat = (nr + BR - 1) / BR;
     for (int i = tid; i < nbat * BR; i += kStatsThreads) s_qall[i] = i < nr ? s_qall[i] / qdiv : 0.0;
-    if (ei >= 0) s_accE[tid] = 0.0;
+    if (BIG && warp == 0)
+#pragma unroll
+      for (int i = 0; i < 12; ++i) s_ecc[i][lane] = 0.0;
+    if (!BIG && ei >= 0) s_accE[tid] = 0.0;
     float acc[NTW][4];
     double sqd[NTW];  // sq_v: fp32 over a batch's rows per lane, then fp64
     double yhd[NTW];  // Y_v[:, H] when cfma
@@ -1846,10 +1855,39 @@ __global__ void __launch_bounds__(kStatsThreads, BIG ? 1 : 2) k_stats_mma(StatsA
         reinterpret_cast<float2*>(&s_Af[ks][ln][1])[up] = make_float2(qz0 - hi0, qz1 - hi1);
       }
       __syncthreads();
-      if (ei >= 0) {
+      if (!BIG && ei >= 0) {  // (16 columns or fewer: a thread per upper-triangle entry)
         double e = s_accE[tid];
         for (int r = eg; r < nb; r += EG) e = fma(s_q[r], s_zd[r * kSmZD + ei] * s_zd[r * kSmZD + ej], e);
         s_accE[tid] = e;
+      }
+      if (BIG && warp == 0) {
+        double ecc[6][2];
+#pragma unroll
+        for (int i = 0; i < 6; ++i) ecc[i][0] = s_ecc[2 * i][lane], ecc[i][1] = s_ecc[2 * i + 1][lane];
+        // E += [zhat; 1]^T diag(q) [zhat; 1] over the batch rows by fp64 DMMA
+        // m8n8k4 (k = 4 rows): A(g, t) = zhat[row t][8 mi + g], B(t, g) =
+        // q_row zhat[row t][8 ni + g]; the 6 upper 8x8 tiles of the 24 x 24
+        // padding (H1 <= 17), accumulated by warp 0 over the item
+#pragma unroll
+        for (int k0 = 0; k0 < BR; k0 += 4) {
+          const int r = k0 + tig;
+          const double q = r < nb ? s_q[r] : 0.0;
+          double za[3], zq[3];
+#pragma unroll
+          for (int m = 0; m < 3; ++m) {
+            const int col = 8 * m + gid;
+            za[m] = (col < H1 && r < nb) ? s_zd[r * kSmZD + col] : 0.0;
+            zq[m] = q * za[m];
+          }
+          dmma_e(ecc[0], za[0], zq[0]);
+          dmma_e(ecc[1], za[0], zq[1]);
+          dmma_e(ecc[2], za[0], zq[2]);
+          dmma_e(ecc[3], za[1], zq[1]);
+          dmma_e(ecc[4], za[1], zq[2]);
+          dmma_e(ecc[5], za[2], zq[2]);
+        }
+#pragma unroll
+        for (int i = 0; i < 6; ++i) s_ecc[2 * i][lane] = ecc[i][0], s_ecc[2 * i + 1][lane] = ecc[i][1];
       }
       // (ii) Y_v^T += (Q zhat)^T v over the batch's 4 k-steps (rows past nb:
       // q = 0 and A = 0, stale finite v), chained per batch, then one FADD
@@ -1910,11 +1948,24 @@ __global__ void __launch_bounds__(kStatsThreads, BIG ? 1 : 2) k_stats_mma(StatsA
     double* pp = direct ? nullptr : part + (int64_t)item * part_stride;
     double* pe = direct ? a.E + (int64_t)c * H1 * H1 : pp + (int64_t)nh1 * D + D;
     __syncthreads();
-    if (ei >= 0 && eg == 0) {
+    if (!BIG && ei >= 0 && eg == 0) {
       double e = 0.0;
       for (int g = 0; g < EG; ++g) e += s_accE[tid + g * NE];
       pe[ej * H1 + ei] = e * qmax;
       pe[ei * H1 + ej] = e * qmax;
+    }
+    if (BIG && warp == 0) {
+      const int tmi[6] = {0, 0, 0, 1, 1, 2}, tni[6] = {0, 1, 2, 1, 2, 2};
+#pragma unroll
+      for (int i = 0; i < 6; ++i)
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int e0 = 8 * tmi[i] + gid, e1 = 8 * tni[i] + 2 * tig + u;
+          if (e0 < H1 && e1 < H1 && e0 <= e1) {
+            pe[e1 * H1 + e0] = s_ecc[2 * i + u][lane] * qmax;
+            pe[e0 * H1 + e1] = s_ecc[2 * i + u][lane] * qmax;
+          }
+        }
     }
 #pragma unroll
     for (int i = 0; i < NTW; ++i) {
