@@ -667,7 +667,8 @@ int estep_local(vmfa_ctx* x, uint64_t seed, uint64_t it, int mode, bool exchange
     a.itemoff = x->part_items;
     a.pts_per_item = x->gupd_pts;
     a.exchange = exchange ? 1 : 0;
-    a.force_rows = ((x->xc && dm.C - 1 > kGupdCap / 2) || x->sparse) ? 1 : 0;
+    // (a dense shared-memory table holds every key for C <= kGupdDenseMax)
+    a.force_rows = ((x->xc && dm.C - 1 > kGupdCap / 2 && dm.C > kGupdDenseMax) || x->sparse) ? 1 : 0;
     a.xc = x->xc;
     if (x->sparse) {
       a.list = 1;
@@ -1162,7 +1163,7 @@ int vmfa_ctx_create(vmfa_ctx** out, int device, int C, int D, int H, int Cp, int
     const int64_t bal = std::max<int64_t>(128, static_cast<int64_t>(N) / (4 * sm_count()));
     // large C (with the dense rows): every item adds into the rows through a
     // small hash (k_gupdate force_rows); items of up to 512 points
-    const int64_t capb = (C - 1 <= kGupdCap / 2) ? (int64_t{1} << 30) : 512;
+    const int64_t capb = (C - 1 <= kGupdCap / 2 || C <= kGupdDenseMax) ? (int64_t{1} << 30) : 512;
     x->gupd_pts = static_cast<int>(std::min(bal, capb));
   }
   // dense C x C rows (count, fixed-point hi, lo) for split components and the

@@ -596,10 +596,12 @@ __global__ void __launch_bounds__(kGupdThreads) k_gupdate(GupdArgs a, int capmax
   // capmax < 0: the dense table (one (cnt, hi, lo) entry per component,
   // indexed by c~, no probing) lives in shared memory (C <= kGupdDenseMax);
   // otherwise the per-CTA global tables back the hash
+  // (shared layout: hi [C] u64 | lo [C] u64 | cnt [C] u32 -- 20 bytes per component)
   const bool sdense = capmax < 0;
-  long long* g_cnt = sdense ? reinterpret_cast<long long*>(smem_raw) : a.gt_cnt + (int64_t)blockIdx.x * dm.C;
-  long long* g_hi = sdense ? g_cnt + dm.C : a.gt_hi + (int64_t)blockIdx.x * dm.C;
+  long long* g_cnt = a.gt_cnt + (int64_t)blockIdx.x * dm.C;
+  long long* g_hi = sdense ? reinterpret_cast<long long*>(smem_raw) : a.gt_hi + (int64_t)blockIdx.x * dm.C;
   long long* g_lo = sdense ? g_hi + dm.C : a.gt_lo + (int64_t)blockIdx.x * dm.C;
+  unsigned* d_cnt = reinterpret_cast<unsigned*>(smem_raw + 16 * static_cast<size_t>(dm.C));
   const int total = a.itemoff[dm.C];
   for (int item = blockIdx.x; item < total; item += gridDim.x) {
     const int c = find_item(a.itemoff, dm.C, item);
@@ -630,7 +632,8 @@ __global__ void __launch_bounds__(kGupdThreads) k_gupdate(GupdArgs a, int capmax
         }
       } else {
         for (int i = tid; i < dm.C; i += kGupdThreads) {
-          g_cnt[i] = 0;
+          if (sdense) d_cnt[i] = 0u;
+          else g_cnt[i] = 0;
           g_hi[i] = 0;
           g_lo[i] = 0;
         }
@@ -718,9 +721,9 @@ __global__ void __launch_bounds__(kGupdThreads) k_gupdate(GupdArgs a, int capmax
             }
           } else if (sdense) {  // (shared-memory atomics: the pointers below are known to be shared)
             unsigned long long* d = reinterpret_cast<unsigned long long*>(smem_raw);
-            atomicAdd(reinterpret_cast<unsigned*>(d + ct), 1u);  // (count < 2^32: the high word stays 0)
-            smem_add_u64(d + dm.C + ct, static_cast<unsigned long long>(hi));
-            smem_add_u64(d + 2 * dm.C + ct, static_cast<unsigned long long>(lo));
+            atomicAdd(reinterpret_cast<unsigned*>(smem_raw + 16 * static_cast<size_t>(dm.C)) + ct, 1u);
+            smem_add_u64(d + ct, static_cast<unsigned long long>(hi));
+            smem_add_u64(d + dm.C + ct, static_cast<unsigned long long>(lo));
           } else {  // (the per-CTA global tables)
             const int64_t gb = (int64_t)blockIdx.x * dm.C + ct;
             atomicAdd(reinterpret_cast<unsigned long long*>(a.gt_cnt + gb), 1ULL);
@@ -741,7 +744,7 @@ __global__ void __launch_bounds__(kGupdThreads) k_gupdate(GupdArgs a, int capmax
         lo = t_lo[i];
       } else {
         ct = i;
-        cnt = g_cnt[i];
+        cnt = sdense ? static_cast<long long>(d_cnt[i]) : g_cnt[i];
         hi = g_hi[i];
         lo = g_lo[i];
       }
@@ -890,17 +893,22 @@ __global__ void __launch_bounds__(kGupdThreads) k_gselect_dense(Dims dm, long lo
     if (tid == 0) s_nsel = 0;
     __syncthreads();
     long long* rc = xc + (int64_t)c * dm.C;
-    for (int r = 0; r < dm.G - 1; ++r) {
-      KeyMin best{INFINITY, 0x7fffffff};
+    // G-1 rounds of a block argmin over the threads' own minima (entry ct
+    // belongs to thread ct mod kGupdThreads); a winner's count is zeroed in the
+    // row (the row is cleared below anyway) and only its owner rescans
+    KeyMin mine{INFINITY, 0x7fffffff};
+    auto own_min = [&]() {
+      mine = KeyMin{INFINITY, 0x7fffffff};
       for (int ct = tid; ct < dm.C; ct += kGupdThreads) {
         const long long cnt = rc[ct];
         if (cnt <= 0) continue;
-        bool taken = false;
-        for (int q = 0; q < s_nsel; ++q) taken |= (s_sel[q] == ct);
-        if (taken) continue;
         const KeyMin k{from_fixed(rc[CC + ct], rc[2 * CC + ct]) / static_cast<double>(cnt), ct};
-        if (kless(k, best)) best = k;
+        if (kless(k, mine)) mine = k;
       }
+    };
+    own_min();
+    for (int r = 0; r < dm.G - 1; ++r) {
+      KeyMin best = mine;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
         KeyMin oth{__shfl_xor_sync(kFull, best.v, o), __shfl_xor_sync(kFull, best.c, o)};
@@ -916,6 +924,11 @@ __global__ void __launch_bounds__(kGupdThreads) k_gselect_dense(Dims dm, long lo
       }
       __syncthreads();
       if (s_nsel <= r) break;
+      const int win = s_sel[r];
+      if (tid == win % kGupdThreads) {
+        rc[win] = 0;
+        own_min();
+      }
     }
     if (tid == 0) {
       int out[64];
@@ -3219,7 +3232,7 @@ cudaError_t launch_gupdate(const GupdArgs& a, int grid, cudaStream_t s) {
   // probing, and 24 C bytes instead of 24 cap (config 3: 96 KB, two CTAs per SM)
   if (a.dm.C <= kGupdDenseMax && !a.dump) {
     capmax = -1;
-    smem = static_cast<size_t>(a.dm.C) * 3 * sizeof(long long);
+    smem = static_cast<size_t>(a.dm.C) * (2 * sizeof(long long) + sizeof(unsigned));
   }
   cudaFuncSetAttribute(k_gupdate, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   k_gupdate<<<grid, kGupdThreads, smem, s>>>(a, capmax);

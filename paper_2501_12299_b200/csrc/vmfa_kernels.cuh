@@ -23,7 +23,7 @@ constexpr int kXsStride = kScoreRows + 2;  // transposed x tile stride (floats)
 constexpr int kStatsThreads = 256;
 constexpr int kGupdCap = 8192;      // smem hash capacity of the block-3 accumulator (24 B per entry)
 constexpr int kGupdThreads = 512;
-constexpr int kGupdDenseMax = 4096;  // C up to which the g-update table is a dense shared-memory row
+constexpr int kGupdDenseMax = 11000;  // C up to which the g-update table is a dense shared-memory row (20 B each)
 constexpr int kGupdRowsCap = 2048;  // hash of an item that adds into the dense rows (overflow goes to xc)
 
 // Packed fp32 scoring parameters of one component (precompute output):

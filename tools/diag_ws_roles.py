@@ -1,5 +1,6 @@
-"""Per-role cycle breakdown of the warp-specialised scorer on BASELINE config 2
-(diagnostics; uses vmfa_diag_scorer_cycles)."""
+"""Per-role cycle breakdown of the warp-specialised scorer on a BASELINE config
+(argv[1], default 2; argv[2] rows, default the config's N) (diagnostics; uses
+vmfa_diag_scorer_cycles)."""
 import ctypes as C
 import os
 import sys
@@ -10,8 +11,10 @@ sys.path.insert(0, os.path.join(os.path.dirname(__file__), ".."))
 from paper_2501_12299_b200 import vmfa as V  # noqa: E402
 from paper_2501_12299_b200.abi import lib  # noqa: E402
 
-X = V.gen_synthetic(V.synth_spec(2))
-m = V.CONFIGS[2]["model"]
+CFG = int(sys.argv[1]) if len(sys.argv) > 1 else 2
+ROWS = int(sys.argv[2]) if len(sys.argv) > 2 else 0
+X = V.gen_synthetic(V.synth_spec(CFG, N=ROWS) if ROWS else V.synth_spec(CFG))
+m = V.CONFIGS[CFG]["model"]
 p, st, floor, _ = V.initialize(X, m["C"], m["H"], m["Cprime"], m["G"], seed=0)
 s = V.Session(m["C"], X.shape[1], m["H"], m["Cprime"], m["G"], X)
 s.set_floor(floor)
