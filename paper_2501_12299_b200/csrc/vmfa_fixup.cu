@@ -488,7 +488,7 @@ cudaError_t launch_fix_f64(const Dims& dm, const FixArgs& f, int mode, const int
     FixParams p{dm.D, dm.H, f.X, f.mu, f.psi, f.lam, f.R, f.kconst, false};
     const size_t smem = fix_dmma_smem(dm.D, dm.H);
     auto go = [&](auto kern) {
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+      ensure_dyn_smem(reinterpret_cast<const void*>(kern), smem);
       kern<<<sm_count() * 2, kFixThreads, smem, s>>>(p, f.W64, dm, mode, f.qoff, f.iof, f.sorted, f.nfix, out);
     };
     switch (dm.H / 8) {
@@ -502,7 +502,7 @@ cudaError_t launch_fix_f64(const Dims& dm, const FixArgs& f, int mode, const int
   const size_t smem = fix_smem(dm.D, dm.H, &sm);
   FixParams p{dm.D, dm.H, f.X, f.mu, f.psi, f.lam, f.R, f.kconst, sm};
   if (smem > 48 * 1024)
-    cudaFuncSetAttribute(k_fix_grouped, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    ensure_dyn_smem(reinterpret_cast<const void*>(k_fix_grouped), smem);
   k_fix_grouped<<<sm_count() * 2, kFixThreads, smem, s>>>(p, dm, mode, f.qoff, f.iof, f.sorted, f.nfix, out);
   return cudaGetLastError();
 }
@@ -512,7 +512,7 @@ cudaError_t launch_fix_scan_anchor(const Dims& dm, const FixArgs& f, const int* 
   bool sm = false;
   const size_t smem = fix_smem(dm.D, dm.H, &sm);
   FixParams p{dm.D, dm.H, f.X, f.mu, f.psi, f.lam, f.R, f.kconst, sm};
-  if (smem > 48 * 1024) cudaFuncSetAttribute(k_fix_anchor, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (smem > 48 * 1024) ensure_dyn_smem(reinterpret_cast<const void*>(k_fix_anchor), smem);
   k_fix_anchor<<<sm_count() * 4, kFixThreads, smem, s>>>(p, dm, g, gcnt, kinv_off, kinv_ent, f.ovf, LJ);
   return cudaGetLastError();
 }
@@ -522,7 +522,7 @@ cudaError_t launch_fix_scan_single(const Dims& dm, const FixArgs& f, const int* 
   bool sm = false;
   const size_t smem = fix_smem(dm.D, dm.H, &sm);
   FixParams p{dm.D, dm.H, f.X, f.mu, f.psi, f.lam, f.R, f.kconst, sm};
-  if (smem > 48 * 1024) cudaFuncSetAttribute(k_fix_single, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (smem > 48 * 1024) ensure_dyn_smem(reinterpret_cast<const void*>(k_fix_single), smem);
   k_fix_single<<<sm_count() * 4, kFixThreads, smem, s>>>(p, dm.C, off, ent, extra_stride, extra_col, f.ovf, out);
   return cudaGetLastError();
 }

@@ -10,6 +10,9 @@
 // Duplicates across anchors are scored but dropped by k_select, which also
 // reproduces the reference's insertion order, tie rules and counters exactly.
 #include <algorithm>
+#include <mutex>
+#include <utility>
+#include <vector>
 #include <cfloat>
 #include <cmath>
 #include <cstdint>
@@ -3127,6 +3130,23 @@ int grid_for(int64_t n, int threads, int cap) {
 
 }  // namespace
 
+cudaError_t ensure_dyn_smem(const void* kern, size_t bytes) {
+  static std::mutex mu;
+  static std::vector<std::pair<const void*, size_t>> done;
+  std::lock_guard<std::mutex> lock(mu);
+  for (auto& e : done)
+    if (e.first == kern) {
+      if (e.second >= bytes) return cudaSuccess;
+      const cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 static_cast<int>(bytes));
+      if (r == cudaSuccess) e.second = bytes;
+      return r;
+    }
+  const cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
+  if (r == cudaSuccess) done.emplace_back(kern, bytes);
+  return r;
+}
+
 int sm_count() {
   static int cached = 0;
   if (cached == 0) {
@@ -3180,7 +3200,7 @@ template <int MODE>
 static cudaError_t launch_score_mode(const ScoreArgs& a, int grid, cudaStream_t s) {
   const size_t smem = static_cast<size_t>(a.dm.D) * kXsStride * sizeof(float);
   auto go = [&](auto kern) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    ensure_dyn_smem(reinterpret_cast<const void*>(kern), smem);
     kern<<<grid, kScoreThreads, smem, s>>>(a);
   };
   if (a.L.hc == 4) go(k_score<MODE, 4>);
@@ -3201,7 +3221,7 @@ cudaError_t launch_select(const SelectArgs& a, cudaStream_t s) {
   const size_t smem = static_cast<size_t>((a.dm.C + 31) / 32) * 8 * sizeof(unsigned) + 64 * (sizeof(float) + sizeof(int));
   if (smem > 200 * 1024) return cudaErrorInvalidValue;
   auto go = [&](auto kern) {
-    if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (smem > 48 * 1024) ensure_dyn_smem(reinterpret_cast<const void*>(kern), smem);
     kern<<<grid, 256, smem, s>>>(a);
   };
   switch (ns) {
@@ -3234,7 +3254,7 @@ cudaError_t launch_gupdate(const GupdArgs& a, int grid, cudaStream_t s) {
     capmax = -1;
     smem = static_cast<size_t>(a.dm.C) * (2 * sizeof(long long) + sizeof(unsigned));
   }
-  cudaFuncSetAttribute(k_gupdate, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  ensure_dyn_smem(reinterpret_cast<const void*>(k_gupdate), smem);
   k_gupdate<<<grid, kGupdThreads, smem, s>>>(a, capmax);
   return cudaGetLastError();
 }
@@ -3286,7 +3306,7 @@ static void stats_pass(const StatsArgs& a, const int* itemoff, int rpi, int grid
       }
   const size_t smem = std::max(static_cast<size_t>(nbuf) * per_buf, red) + fixed;
   auto go = [&](auto kern) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    ensure_dyn_smem(reinterpret_cast<const void*>(kern), smem);
     kern<<<grid, kStatsThreads, smem, s>>>(a, itemoff, rpi, col0, part, ps, nbuf);
   };
   if (GD <= kStatsThreads) go(k_stats<NH1, 1>);
@@ -3355,7 +3375,7 @@ cudaError_t launch_stats(const StatsArgs& a, const int* itemoff, int rows_per_it
     const int per_sm = (!big && nbuf <= 2) ? 2 : 1;  // 2 x (66.5 + 17 KB dynamic + 30 KB static) fits at D = 256
     const size_t smem = nbuf * per_buf + fixed;
     auto go = [&](auto kern) {
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+      ensure_dyn_smem(reinterpret_cast<const void*>(kern), smem);
       kern<<<sm_count() * per_sm, kStatsThreads, smem, s>>>(a, itemoff, rows_per_item, nh1, part, ps, nbuf);
     };
     if (big) {
@@ -3395,7 +3415,7 @@ cudaError_t launch_stats(const StatsArgs& a, const int* itemoff, int rows_per_it
   }
   if (H1 > nh1) {
     const size_t smem = 2 * static_cast<size_t>(kStatsBatch) * kEZS * sizeof(double);
-    cudaFuncSetAttribute(k_stats_E, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    ensure_dyn_smem(reinterpret_cast<const void*>(k_stats_E), smem);
     k_stats_E<<<grid, kStatsThreads, smem, s>>>(a, itemoff, rows_per_item, part, ps);
     k_stats_reduce<<<sm_count() * 8, 256, 0, s>>>(a.dm, itemoff, part, ps, 1, 0, nh1, 1, a.Nc, a.E, a.Y, a.sq);
     cudaError_t e = cudaGetLastError();
@@ -3422,7 +3442,7 @@ cudaError_t launch_update(const UpdateArgs& a, cudaStream_t s) {
   const int H1 = a.dm.H + 1;
   const size_t smem = (2 * static_cast<size_t>(H1) * H1 + static_cast<size_t>(H1) * 128) * sizeof(double);
   auto go = [&](auto kern) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    ensure_dyn_smem(reinterpret_cast<const void*>(kern), smem);
     kern<<<min(a.dm.C, sm_count() * 8), 128, smem, s>>>(a);
   };
   if (H1 <= 5) go(k_update<5>);
@@ -3445,7 +3465,7 @@ cudaError_t launch_precompute(const PrecompArgs& a, cudaStream_t s) {
                       sizeof(double);
   const dim3 rgrid((a.dm.D + 127) / 128, a.dm.C);
   auto go = [&](auto kern, auto rows) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    ensure_dyn_smem(reinterpret_cast<const void*>(kern), smem);
     kern<<<min(a.dm.C, sm_count() * 8), 128, smem, s>>>(a);
     if (rows) rows<<<rgrid, 128, 0, s>>>(a);
   };

@@ -269,6 +269,10 @@ cudaError_t launch_validate_K(const int* K, int64_t N, int Cp, int C, long long*
 cudaError_t launch_logpi(const double* pi, int C, double* logpi, cudaStream_t s);
 
 int sm_count();
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per kernel and size:
+// the call costs host time on every launch and opened gaps between queued
+// kernels in the plain-launch (profiling) path
+cudaError_t ensure_dyn_smem(const void* kern, size_t bytes);
 // tensor-core scorer (vmfa_score_tc.cu)
 bool score_tc_supported(const Dims& dm);
 cudaError_t launch_score_tc(int mode, const ScoreArgs& s, const float* WT, const float* ipsi32,

@@ -534,7 +534,7 @@ cudaError_t launch_score_tc(int mode, const ScoreArgs& s, const float* WT, const
   a.out = s.out;
   const int grid = sm_count();
   auto go = [&](auto kern) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn));
+    ensure_dyn_smem(reinterpret_cast<const void*>(kern), dyn);
     kern<<<grid, kTcThreads, dyn, st>>>(a);
   };
   switch (a.Hp) {

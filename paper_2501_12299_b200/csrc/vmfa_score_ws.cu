@@ -1259,7 +1259,7 @@ cudaError_t launch_score_ws(int mode, const ScoreArgs& s, const WsOperands& op, 
   a.dbg = g_ws_prof ? g_ws_dbg : 0;
   if (build_jobs) k_build_jobs<<<(s.dm.C + 255) / 256, 256, 0, st>>>(s.dm.C, mode, s.off, s.itemoff, s.gcnt, jobs);
   auto go = [&](auto kern) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn));
+    ensure_dyn_smem(reinterpret_cast<const void*>(kern), dyn);
     kern<<<sm_count(), kThreads, dyn, st>>>(a, xmap);
   };
   const bool prof = g_ws_prof != nullptr;

@@ -814,11 +814,11 @@ cudaError_t launch_stats_tc(const StatsArgs& a, const float* xmax, const float* 
     return v ? std::atoi(v) : 0;
   }();
   if (cudaError_t e = cudaMemsetAsync(a.qctr, 0, 2 * sizeof(int), s); e != cudaSuccess) return e;
-  cudaFuncSetAttribute(k_stats_z<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(L.total_z));
+  ensure_dyn_smem(reinterpret_cast<const void*>(k_stats_z<16>), L.total_z);
   k_stats_z<16><<<sm_count(), kTThreads, L.total_z, s>>>(a, xmax, mumax, static_cast<const unsigned char*>(a.vimg),
                                                           a.vexp, itemoff, nh1, part, part_stride, a.zbuf, dbg);
   auto go = [&](auto kern) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(L.total_y));
+    ensure_dyn_smem(reinterpret_cast<const void*>(kern), L.total_y);
     kern<<<sm_count(), kTThreads, L.total_y, s>>>(a, xmax, mumax, a.vl1, itemoff, nh1, part, part_stride, a.zbuf, dbg);
   };
   if (L.N2 == 16) go(k_stats_y<16>);
