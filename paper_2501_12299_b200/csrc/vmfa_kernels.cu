@@ -2153,6 +2153,12 @@ __device__ __forceinline__ void chol_solve_thread_t(const double* R, double* b, 
     }
 }
 
+__device__ __forceinline__ void dmma_f64_pre(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
 __device__ __forceinline__ void set_status(unsigned long long* st, int c, int code) {
   atomicMin(st, (static_cast<unsigned long long>(c) << 8) | static_cast<unsigned long long>(code));
 }
@@ -2721,6 +2727,110 @@ __global__ void __launch_bounds__(128) k_precompute(PrecompArgs a) {
       }
     }
     __syncthreads();
+  }
+}
+
+// k_precompute for H <= 16 with a WARP per component (no block barriers, 8
+// components in flight per CTA): M = Lambda^T Psi^-1 Lambda by fp64 DMMA
+// m8n8k4 (the upper 8x8 tiles, k = 4 dimensions; A(g, t) = Lambda[8 mi + g][d],
+// B(t, g) = Lambda[8 ni + g][d] / psi_d), symmetrised from the upper
+// triangle, + I; Cholesky by the warp (+1e-10 retry -> CholeskyFailure),
+// Sigma_z by lanes 0..H-1, log|Sigma| by a warp reduction (model.cpp:43-73).
+// The per-dimension scoring rows follow in k_precompute_rows.
+constexpr int kPreWarps = 8;
+__global__ void __launch_bounds__(kPreWarps * 32) k_precompute_w(PrecompArgs a) {
+  __shared__ double s_L[kPreWarps][16 * 16], s_R[kPreWarps][16 * 16];
+  __shared__ int s_ok[kPreWarps];
+  const Dims dm = a.dm;
+  const int H = dm.H, D = dm.D;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  double* sL = s_L[warp];
+  double* sR = s_R[warp];
+  const int nt = (H + 7) / 8;  // 8 x 8 tiles per side (1 or 2)
+  for (int c = blockIdx.x * kPreWarps + warp; c < dm.C; c += gridDim.x * kPreWarps) {
+    const double* lam = a.lam + (int64_t)c * D * H;
+    const double* psi = a.psi + (int64_t)c * D;
+    double acc[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};  // tiles (0,0), (0,1), (1,1)
+    double lsum = 0.0;  // sum log psi over this lane's dimensions
+    for (int d0 = 0; d0 < D; d0 += 4) {
+      const int d = d0 + t;
+      const bool dv = d < D;
+      const double ip = dv ? 1.0 / psi[d] : 0.0;
+      if (dv && g == 0) lsum += log(psi[d]);
+      double av[2], bv[2];
+#pragma unroll
+      for (int m = 0; m < 2; ++m) {
+        const int h = 8 * m + g;
+        av[m] = (m < nt && h < H && dv) ? lam[(int64_t)h * D + d] : 0.0;
+        bv[m] = av[m] * ip;
+      }
+      dmma_f64_pre(acc[0], av[0], bv[0]);
+      if (nt > 1) {
+        dmma_f64_pre(acc[1], av[0], bv[1]);
+        dmma_f64_pre(acc[2], av[1], bv[1]);
+      }
+    }
+    // M tiles -> sL (upper, then mirrored), + I
+    {
+      const int tmi[3] = {0, 0, 1}, tni[3] = {0, 1, 1};
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        if (i > 0 && nt < 2) break;
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int r = 8 * tmi[i] + g, cc = 8 * tni[i] + 2 * t + u;
+          if (r < H && cc < H && r <= cc) {
+            sL[r * H + cc] = acc[i][u];
+            sL[cc * H + r] = acc[i][u];
+          }
+        }
+      }
+    }
+    __syncwarp();
+    for (int p = lane; p < H * H; p += 32) {
+      const int i = p % H, j = p / H;
+      const double v = sL[p] + (i == j ? 1.0 : 0.0);
+      sL[p] = v;
+      a.Lmat[(int64_t)c * H * H + p] = v;
+    }
+    __syncwarp();
+    warp_cholesky(sL, sR, H, &s_ok[warp]);
+    __syncwarp();
+    if (!s_ok[warp]) {  // model.cpp:55-63
+      if (lane < H) sL[lane * H + lane] += 1e-10;
+      __syncwarp();
+      warp_cholesky(sL, sR, H, &s_ok[warp]);
+      __syncwarp();
+      if (!s_ok[warp]) {
+        if (lane == 0) set_status(a.status, c, 2 /* CholeskyFailure */);
+        continue;
+      }
+      for (int p = lane; p < H * H; p += 32) a.Lmat[(int64_t)c * H * H + p] = sL[p];
+    }
+    for (int p = lane; p < H * H; p += 32) a.R[(int64_t)c * H * H + p] = sR[p];
+    if (lane < H) {  // Sigma_z = L^-1 (model.cpp:65), column `lane`
+      double b[16];
+#pragma unroll
+      for (int h = 0; h < 16; ++h) b[h] = h == lane ? 1.0 : 0.0;
+      chol_solve_thread_t<16>(sR, b, H);
+#pragma unroll
+      for (int h = 0; h < 16; ++h)
+        if (h < H) a.Sz[(int64_t)c * H * H + lane * H + h] = b[h];
+    }
+    // log|Sigma| (model.cpp:67-70): fixed-order warp reduction of sum log psi
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) lsum += __shfl_xor_sync(kFull, lsum, o);
+    if (lane == 0) {
+      double ld = 0.0;
+      for (int h = 0; h < H; ++h) ld += log(sR[h * H + h]);
+      const double logdet = 2.0 * ld + lsum;
+      const double pp = a.pi[c];
+      const double lp = pp > 0.0 ? log(pp) : -INFINITY;  // model.cpp:71
+      a.logdet[c] = logdet;
+      a.logpi[c] = lp;
+      a.kconst[c] = lp - 0.5 * (D * kLog2Pi + logdet);
+    }
+    __syncwarp();
   }
 }
 
@@ -3471,7 +3581,10 @@ cudaError_t launch_precompute(const PrecompArgs& a, cudaStream_t s) {
   };
   using RowsK = void (*)(PrecompArgs);
   if (H <= kPreFastH) go(k_precompute<kPreFastH>, static_cast<RowsK>(k_precompute_rows<kPreFastH>));
-  else if (H <= 16) go(k_precompute<16>, static_cast<RowsK>(k_precompute_rows<16>));
+  else if (H <= 16) {
+    k_precompute_w<<<(a.dm.C + kPreWarps - 1) / kPreWarps, kPreWarps * 32, 0, s>>>(a);
+    k_precompute_rows<16><<<rgrid, 128, 0, s>>>(a);
+  }
   else if (H <= 32) go(k_precompute<32>, static_cast<RowsK>(k_precompute_rows<32>));
   else go(k_precompute<0>, static_cast<RowsK>(nullptr));
   return cudaGetLastError();
