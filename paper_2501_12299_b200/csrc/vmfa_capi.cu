@@ -102,6 +102,7 @@ struct vmfa_ctx {
   float* svl1 = nullptr;
   float* szbuf = nullptr;  // its zhat per K-pair (N C' x H)
   uint16_t* limg = nullptr;  // image-free anchor stages: per (anchor, group, chunk) lin / psi rows (fp16)
+  bool ifree_only = false;    // the full anchor images do not fit: image-free stages everywhere
   unsigned long long* nfix = nullptr;         // scores re-evaluated in fp64 (vmfa_fixup.cu), accumulated
   long long* fix_list = nullptr;              // flagged scores of one scoring launch
   unsigned long long* fix_cnt = nullptr;      // [count, overflow]
@@ -334,6 +335,7 @@ int csr_by_key(vmfa_ctx* x, const unsigned* keys, int64_t n, int* off, int* ent,
 
 int score_grid() { return sm_count() * 8; }
 constexpr size_t kImageBudget = size_t(16) << 30;  // scorer B stage images (bytes)
+constexpr size_t kImageFreeBudget = size_t(64) << 30;  // image-free stages: small + one-component images
 
 // the compute stream waits for a pending asynchronous row upload (first X consumer)
 cudaError_t wait_x(vmfa_ctx* x) {
@@ -927,7 +929,7 @@ int dense_prepare(vmfa_ctx* x) {
   CU(launch_dense_groups(dm.C, dm.G, x->dense_g, x->dense_gcnt, s));
   if (x->scorer == 2) {
     CU(launch_ws_images(dm, 0, x->WT, x->mu32, x->ipsi32, x->dense_g, x->dense_gcnt, x->bimg, x->bscl, s,
-                        x->sscl));
+                        x->sscl, nullptr, x->ifree_only ? x->limg : nullptr));
     CU(launch_ws_records(dm, 0, x->WT, x->mu32, x->ipsi32, x->kconst, x->dense_g, x->dense_gcnt, x->bscl, x->brec,
                          s));
   }
@@ -959,7 +961,8 @@ int dense_chunk(vmfa_ctx* x, int64_t r0, int Rc) {
     a.out = x->dense_LJ;
     CU(wait_x(x));
     if (ws) {
-      const WsOperands op{x->xmax + r0, x->mumax, x->mu32, x->brec, x->srec, x->bimg, x->bscl, x->simg, x->sscl};
+      WsOperands op{x->xmax + r0, x->mumax, x->mu32, x->brec, x->srec, x->bimg, x->bscl, x->simg, x->sscl};
+      if (x->ifree_only) op.limg = x->limg;
       CU(launch_score_ws(kModeAnchor, a, op, x->dense_jobs, s, false));
     } else {  // single-role scorers (shapes the warp-specialised one does not take): CSR items
       CU(launch_dense_csr(C, G, Rc, x->score_rows, x->dense_off, x->dense_items, s));
@@ -1022,8 +1025,18 @@ int vmfa_ctx_create(vmfa_ctx** out, int device, int C, int D, int H, int Cp, int
     // the warp-specialised scorer streams prebuilt B stage images: fall back
     // to the single-role tensor scorer when they exceed the memory budget
     if (x->scorer == 2 &&
-        static_cast<size_t>(ws_image_halves(x->dm, 0) + ws_image_halves(x->dm, 1)) * 2 > kImageBudget)
-      x->scorer = 1;
+        static_cast<size_t>(ws_image_halves(x->dm, 0) + ws_image_halves(x->dm, 1)) * 2 > kImageBudget) {
+      // ... unless the image-free anchor stages fit (small per-anchor lin / psi
+      // images + the one-component images; config 5: ~50 GB instead of ~200)
+      const size_t free_bytes =
+          static_cast<size_t>(ws_small_image_halves(x->dm) + ws_image_halves(x->dm, 1)) * 2;
+      if (ws_image_free_ok(x->dm) && free_bytes <= kImageFreeBudget) x->ifree_only = true;
+      else x->scorer = 1;
+    }
+    // VMFA_IMAGE_FREE=2: the image-free route as if the full images did not fit (tests)
+    if (x->scorer == 2 && ws_image_free_ok(x->dm) && std::getenv("VMFA_IMAGE_FREE") &&
+        std::getenv("VMFA_IMAGE_FREE")[0] == '2')
+      x->ifree_only = true;
     if (x->scorer == 1 && !score_tc_supported(x->dm)) x->scorer = 0;
     if (x->scorer == 0 && static_cast<size_t>(D) * kXsStride * sizeof(float) > 200 * 1024) {
       const size_t dmax = 200 * 1024 / (kXsStride * sizeof(float));
@@ -1079,11 +1092,14 @@ int vmfa_ctx_create(vmfa_ctx** out, int device, int C, int D, int H, int Cp, int
     // config 2 flags ~1e6 scores per pass
     x->fix_cap = std::max<long long>(1 << 20, std::min<long long>(static_cast<long long>(N) * dm.SL, 1LL << 26));
     A(x->jobs, static_cast<size_t>(x->fix_cap) / 128 + Cs + 2);
-    A(x->bimg, ws_image_halves(dm, 0));
-    // image-free anchor stages, opt-in (VMFA_IMAGE_FREE=1): the loader then
-    // assembles every stage from 3 + 2 G bulk copies, which measured slower at
-    // config 3 (anchor pass 7.84 -> 9.66 ms) than one copy of the prebuilt image
-    if (ws_image_free_ok(dm) && std::getenv("VMFA_IMAGE_FREE") && std::getenv("VMFA_IMAGE_FREE")[0] == '1')
+    // image-free anchor stages: required when the full anchor images exceed
+    // the budget (ifree_only: no bimg at all), else opt-in (VMFA_IMAGE_FREE=1);
+    // the loader then assembles every stage from 3 + 2 G bulk copies, which
+    // measured slower at config 3 (anchor pass 7.84 -> 9.66 ms) than one copy
+    // of the prebuilt image
+    if (!x->ifree_only) A(x->bimg, ws_image_halves(dm, 0));
+    if (x->ifree_only ||
+        (ws_image_free_ok(dm) && std::getenv("VMFA_IMAGE_FREE") && std::getenv("VMFA_IMAGE_FREE")[0] == '1'))
       A(x->limg, ws_small_image_halves(dm));
     A(x->simg, ws_image_halves(dm, 1));
     A(x->bscl, ws_scale_floats(dm, 0));

@@ -501,8 +501,7 @@ cudaError_t launch_fix_f64(const Dims& dm, const FixArgs& f, int mode, const int
   }
   const size_t smem = fix_smem(dm.D, dm.H, &sm);
   FixParams p{dm.D, dm.H, f.X, f.mu, f.psi, f.lam, f.R, f.kconst, sm};
-  if (smem > 48 * 1024)
-    ensure_dyn_smem(reinterpret_cast<const void*>(k_fix_grouped), smem);
+  ensure_dyn_smem(reinterpret_cast<const void*>(k_fix_grouped), smem);
   k_fix_grouped<<<sm_count() * 2, kFixThreads, smem, s>>>(p, dm, mode, f.qoff, f.iof, f.sorted, f.nfix, out);
   return cudaGetLastError();
 }
@@ -512,7 +511,7 @@ cudaError_t launch_fix_scan_anchor(const Dims& dm, const FixArgs& f, const int* 
   bool sm = false;
   const size_t smem = fix_smem(dm.D, dm.H, &sm);
   FixParams p{dm.D, dm.H, f.X, f.mu, f.psi, f.lam, f.R, f.kconst, sm};
-  if (smem > 48 * 1024) ensure_dyn_smem(reinterpret_cast<const void*>(k_fix_anchor), smem);
+  ensure_dyn_smem(reinterpret_cast<const void*>(k_fix_anchor), smem);
   k_fix_anchor<<<sm_count() * 4, kFixThreads, smem, s>>>(p, dm, g, gcnt, kinv_off, kinv_ent, f.ovf, LJ);
   return cudaGetLastError();
 }
@@ -522,7 +521,7 @@ cudaError_t launch_fix_scan_single(const Dims& dm, const FixArgs& f, const int* 
   bool sm = false;
   const size_t smem = fix_smem(dm.D, dm.H, &sm);
   FixParams p{dm.D, dm.H, f.X, f.mu, f.psi, f.lam, f.R, f.kconst, sm};
-  if (smem > 48 * 1024) ensure_dyn_smem(reinterpret_cast<const void*>(k_fix_single), smem);
+  ensure_dyn_smem(reinterpret_cast<const void*>(k_fix_single), smem);
   k_fix_single<<<sm_count() * 4, kFixThreads, smem, s>>>(p, dm.C, off, ent, extra_stride, extra_col, f.ovf, out);
   return cudaGetLastError();
 }

@@ -3331,7 +3331,7 @@ cudaError_t launch_select(const SelectArgs& a, cudaStream_t s) {
   const size_t smem = static_cast<size_t>((a.dm.C + 31) / 32) * 8 * sizeof(unsigned) + 64 * (sizeof(float) + sizeof(int));
   if (smem > 200 * 1024) return cudaErrorInvalidValue;
   auto go = [&](auto kern) {
-    if (smem > 48 * 1024) ensure_dyn_smem(reinterpret_cast<const void*>(kern), smem);
+    ensure_dyn_smem(reinterpret_cast<const void*>(kern), smem);
     kern<<<grid, 256, smem, s>>>(a);
   };
   switch (ns) {

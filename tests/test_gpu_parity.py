@@ -61,14 +61,17 @@ def test_precompute_caches_match_oracle(oracle, gpu):
     dict(N=2000, D=100, C=50, H=16, Cp=4, G=8),   # H=16 chunk
     dict(N=1500, D=64, C=60, H=12, Cp=3, G=18),   # two component groups per anchor job (G > 15)
 ])
-@pytest.mark.parametrize("scorer", ["ws", "ws-imagefree", "tc", "ffma"])
+@pytest.mark.parametrize("scorer", ["ws", "ws-imagefree", "ws-imagefree-only", "tc", "ffma"])
 def test_estep_teacher_forced(oracle, gpu, case, scorer, monkeypatch):
     # ws-imagefree: the warp-specialised scorer assembling each anchor stage
-    # from the one-component images (VMFA_IMAGE_FREE=1, opt-in)
+    # from the one-component images (VMFA_IMAGE_FREE=1, opt-in); -only: the
+    # route without any full anchor images (VMFA_IMAGE_FREE=2, config 5)
     O, V = oracle, gpu
     monkeypatch.setenv("VMFA_SCORER", scorer.split("-")[0])
     if scorer == "ws-imagefree":
         monkeypatch.setenv("VMFA_IMAGE_FREE", "1")
+    if scorer == "ws-imagefree-only":
+        monkeypatch.setenv("VMFA_IMAGE_FREE", "2")
     X, _ = gaussian_problem(case["N"], case["D"], max(case["C"] // 2, 2), min(case["H"], 4), seed=7)
     C, H, Cp, G = case["C"], case["H"], case["Cp"], case["G"]
     p, st, floor, sess = _setup(O, V, X, C, H, Cp, G)
@@ -466,11 +469,16 @@ def test_lookahead_free_energy_is_exact(oracle, gpu, scorer, monkeypatch):
 @pytest.mark.parametrize("case", [dict(N=3000, D=64, C=57, H=4, G=5, frozen=()),
                                   dict(N=2500, D=100, C=40, H=8, G=10, frozen=(3, 17)),
                                   dict(N=700, D=30, C=23, H=3, G=23, frozen=(0,))])
-def test_exact_log_likelihood_matches_oracle(oracle, gpu, case):
+@pytest.mark.parametrize("imagefree", ["0", "2"])
+def test_exact_log_likelihood_matches_oracle(oracle, gpu, case, imagefree, monkeypatch):
     # exact_log_likelihood (model.cpp:139-148): all-pairs N x C log-joints and
     # the per-row LSE; C not a multiple of G (short last block), D % 4 != 0 and
     # frozen components (pi = 0 -> l = -inf) included; calling it leaves the
-    # lookahead state of the training loop intact
+    # lookahead state of the training loop intact. imagefree "2": the route
+    # taken when the full anchor images exceed the budget (config 5), where
+    # every anchor stage -- the dense pass's too -- is assembled by the loader
+    if imagefree != "0":
+        monkeypatch.setenv("VMFA_IMAGE_FREE", imagefree)
     O, V = oracle, gpu
     X, _ = gaussian_problem(case["N"], case["D"], max(4, case["C"] // 2), 3, seed=5)
     C, H, G = case["C"], case["H"], case["G"]
