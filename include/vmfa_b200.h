@@ -104,6 +104,14 @@ int vmfa_upload_data(vmfa_ctx* ctx, const float* X, int64_t row_begin, int64_t r
  * valid and unchanged until the next call that synchronises the context
  * (iterate, any download, ...). Page-locked X gives a truly asynchronous copy. */
 int vmfa_upload_data_async(vmfa_ctx* ctx, const float* X, int64_t row_begin, int64_t rows);
+/* Pipelined uploads (a second device row buffer): vmfa_stage_data_async
+ * copies rows into the staging buffer on the copy stream, after the work
+ * already enqueued that may still read it; vmfa_swap_data makes the staged
+ * rows current (later work waits for their copy) and the previous rows the
+ * staging buffer. A training / serving loop stages the next batch while the
+ * current one is processed. X stays valid until the next synchronising call. */
+int vmfa_stage_data_async(vmfa_ctx* ctx, const float* X, int64_t row_begin, int64_t rows);
+int vmfa_swap_data(vmfa_ctx* ctx);
 /* Lookahead (default on, env VMFA_LOOKAHEAD=0 turns it off): the truncated
  * free energy after the M-step is read from the next E-step's anchor pass,
  * which that E-step then skips. Off: F gets its own one-component pass (same

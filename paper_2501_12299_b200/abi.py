@@ -61,6 +61,8 @@ _SIGS = {
     "vmfa_ctx_device_bytes": (_I, [_P, C.POINTER(C.c_size_t)]),
     "vmfa_upload_data": (_I, [_P, _P, _I64, _I64]),
     "vmfa_upload_data_async": (_I, [_P, _P, _I64, _I64]),
+    "vmfa_stage_data_async": (_I, [_P, _P, _I64, _I64]),
+    "vmfa_swap_data": (_I, [_P]),
     "vmfa_set_lookahead": (_I, [_P, _I]),
     "vmfa_save_dataset": (_I, [C.c_char_p, _P, _I64, _I]),
     "vmfa_dataset_info": (_I, [C.c_char_p, _P, _P]),

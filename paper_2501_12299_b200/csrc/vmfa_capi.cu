@@ -191,6 +191,12 @@ struct vmfa_ctx {
   // vmfa_upload_data_async: rows copied on a second stream; X consumers wait on x_ready
   cudaStream_t cstream = nullptr;
   cudaEvent_t x_ready = nullptr, x_free = nullptr;
+  // vmfa_stage_data_async / vmfa_swap_data: a second row buffer filled on
+  // cstream while the current one is in use (pipelined uploads)
+  float* Xs = nullptr;
+  float* xmax_s = nullptr;
+  cudaEvent_t xs_ready = nullptr;
+  bool xs_pending = false;
   bool x_pending = false;
   bool have_estep = false;
   // CUDA graphs of vmfa_iterate (default; VMFA_GRAPH=0 disables): one per host-side pre-state
@@ -201,13 +207,14 @@ struct vmfa_ctx {
   struct HostState {
     int *g, *gcnt, *g_new, *gcnt_new;
     double *pi, *pi2, *mu, *mu2, *lam, *lam2, *psi, *psi2;
+    float *X, *xmax;  // (the staged-row double buffer swaps them)
     bool prescored, kinv, have_estep;
     int mode;
     bool lookahead;
     bool operator==(const HostState& o) const {
       return g == o.g && gcnt == o.gcnt && g_new == o.g_new && gcnt_new == o.gcnt_new && pi == o.pi &&
              pi2 == o.pi2 && mu == o.mu && mu2 == o.mu2 && lam == o.lam && lam2 == o.lam2 && psi == o.psi &&
-             psi2 == o.psi2 && prescored == o.prescored && kinv == o.kinv && have_estep == o.have_estep &&
+             psi2 == o.psi2 && X == o.X && xmax == o.xmax && prescored == o.prescored && kinv == o.kinv && have_estep == o.have_estep &&
              mode == o.mode && lookahead == o.lookahead;
     }
   };
@@ -1293,6 +1300,46 @@ int vmfa_upload_data_async(vmfa_ctx* x, const float* X, int64_t row_begin, int64
   return VMFA_OK;
 }
 
+int vmfa_stage_data_async(vmfa_ctx* x, const float* X, int64_t row_begin, int64_t rows) {
+  TRY(check_ctx(x));
+  if (!X || row_begin < 0 || rows < 0 || row_begin + rows > x->dm.N)
+    return fail(VMFA_ERR_INVALID_ARGUMENT, "vmfa_stage_data_async: row range outside the shard");
+  if (!x->cstream) {
+    CU(cudaStreamCreateWithFlags(&x->cstream, cudaStreamNonBlocking));
+    CU(cudaEventCreateWithFlags(&x->x_ready, cudaEventDisableTiming));
+    CU(cudaEventCreateWithFlags(&x->x_free, cudaEventDisableTiming));
+  }
+  if (!x->Xs) {
+    const size_t N = static_cast<size_t>(x->dm.N), D = static_cast<size_t>(x->dm.D);
+    int r = x->alloc(x->Xs, N * D);
+    if (r == VMFA_OK && x->xmax) r = x->alloc(x->xmax_s, N);
+    if (r != VMFA_OK) return r;
+    CU(cudaEventCreateWithFlags(&x->xs_ready, cudaEventDisableTiming));
+  }
+  // after everything already enqueued (which may still read the staging
+  // buffer: it was the current one before the last swap)
+  CU(cudaEventRecord(x->x_free, x->stream));
+  CU(cudaStreamWaitEvent(x->cstream, x->x_free, 0));
+  CU(cudaMemcpyAsync(x->Xs + row_begin * x->dm.D, X, sizeof(float) * rows * x->dm.D, cudaMemcpyHostToDevice,
+                     x->cstream));
+  if (x->xmax_s) CU(launch_rowmax(rows, x->dm.D, x->Xs + row_begin * x->dm.D, x->xmax_s + row_begin, x->cstream));
+  CU(cudaEventRecord(x->xs_ready, x->cstream));
+  x->xs_pending = true;
+  return VMFA_OK;
+}
+
+int vmfa_swap_data(vmfa_ctx* x) {
+  TRY(check_ctx(x));
+  if (!x->Xs || !x->xs_pending) return fail(VMFA_ERR_INVALID_ARGUMENT, "vmfa_swap_data: nothing staged");
+  CU(wait_x(x));
+  CU(cudaStreamWaitEvent(x->stream, x->xs_ready, 0));  // later work reads the staged rows
+  std::swap(x->X, x->Xs);
+  std::swap(x->xmax, x->xmax_s);
+  x->xs_pending = false;
+  x->prescored = false;
+  return VMFA_OK;
+}
+
 int vmfa_set_lookahead(vmfa_ctx* x, int enable) {
   TRY(check_ctx(x));
   x->lookahead = enable != 0;
@@ -1744,6 +1791,7 @@ vmfa_ctx::HostState host_state(const vmfa_ctx* x, int mode) {
   h.g = x->g, h.gcnt = x->gcnt, h.g_new = x->g_new, h.gcnt_new = x->gcnt_new;
   h.pi = x->pi, h.pi2 = x->pi2, h.mu = x->mu, h.mu2 = x->mu2;
   h.lam = x->lam, h.lam2 = x->lam2, h.psi = x->psi, h.psi2 = x->psi2;
+  h.X = x->X, h.xmax = x->xmax;
   h.prescored = x->prescored, h.kinv = x->kinv_for_current_K, h.have_estep = x->have_estep;
   h.mode = mode;
   h.lookahead = x->lookahead;

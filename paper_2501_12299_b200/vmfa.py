@@ -136,6 +136,18 @@ class Session:
         else:
             check(lib().vmfa_upload_data(self._h, ptr(X), row_begin, X.shape[0]))
 
+    def stage_data(self, X: np.ndarray, row_begin: int = 0):
+        """vmfa_stage_data_async: rows into the second device buffer on the copy
+        stream (the next batch, while the current one is processed); X must
+        stay unchanged until the next synchronising call."""
+        X = _c(X, np.float32)
+        check(lib().vmfa_stage_data_async(self._h, ptr(X), row_begin, X.shape[0]))
+        self._staged_x = X
+
+    def swap_data(self):
+        """vmfa_swap_data: the staged rows become current."""
+        check(lib().vmfa_swap_data(self._h))
+
     def set_lookahead(self, enable: bool):
         """vmfa_set_lookahead: truncated F from the next E-step's anchor pass
         (default) or from its own one-component pass (same value)."""

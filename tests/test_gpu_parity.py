@@ -621,6 +621,39 @@ def test_async_upload_matches_sync(oracle, gpu):
     assert np.array_equal(Ka, Kb) and np.array_equal(mua, mub)
 
 
+def test_staged_rows_match_sync_upload(oracle, gpu):
+    # vmfa_stage_data_async / vmfa_swap_data (the pipelined row uploads of the
+    # e2e loop): rows staged while an iteration runs and swapped in before the
+    # next one give the same iterations as synchronous uploads, across several
+    # swaps (both device buffers in turn, one cached graph per buffer)
+    O, V = oracle, gpu
+    X, _ = gaussian_problem(5000, 64, 20, 3, seed=8)
+    Xs = [X, (X + np.float32(0.25)).astype(np.float32), (X - np.float32(0.5)).astype(np.float32)]
+    C, H, Cp, G = 30, 4, 3, 5
+    out = []
+    for staged in (False, True):
+        p, st, floor, sess = _setup(O, V, X, C, H, Cp, G)
+        sess.variational_e_step(0, 0)
+        sess.set_lookahead(False)
+        pinned = [np.ascontiguousarray(x) for x in Xs]
+        rs = []
+        if staged:
+            sess.stage_data(pinned[1])
+        for it in range(1, 6):
+            nxt = pinned[(it + 1) % 3]
+            if staged:
+                sess.swap_data()      # this iteration's rows: pinned[it % 3]
+                sess.stage_data(nxt)  # the next iteration's, copied while this one runs
+            else:
+                sess.upload_data(pinned[it % 3])
+            rs.append(sess.iterate(0, it)["F"])
+        out.append((rs, sess.download_state().K, sess.download_params().mu))
+        sess.close()
+    (ra, Ka, mua), (rb, Kb, mub) = out
+    assert ra == rb
+    assert np.array_equal(Ka, Kb) and np.array_equal(mua, mub)
+
+
 def test_upload_state_validates_K_on_device(gpu):
     # VarState::validate (estep.cpp:15-68): K rows sorted, distinct, in range
     V = gpu
