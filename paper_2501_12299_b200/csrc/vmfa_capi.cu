@@ -446,7 +446,8 @@ int run_precompute(vmfa_ctx* x, int* failed, bool sync = true) {
   CU(launch_precompute(a, s));
   if (x->scorer == 2) {
     CU(launch_ws_images(x->dm, 1, x->WT, x->mu32, x->ipsi32, x->g, x->gcnt, x->simg, x->sscl, s));
-    CU(launch_ws_records(x->dm, 1, x->WT, x->mu32, x->ipsi32, x->kconst, x->g, x->gcnt, x->sscl, x->srec, s));
+    CU(launch_ws_records(x->dm, 1, x->WT, x->mu32, x->ipsi32, x->kconst, x->g, x->gcnt, x->sscl, x->srec, s, 0,
+                         x->logpi, x->logdet));
     CU(launch_rowmax(x->dm.C, x->dm.D, x->mu32, x->mumax, s));
   }
   if (x->svimg) CU(launch_stats_vimg(x->dm, x->V32, x->svimg, x->svexp, x->svl1, s));
@@ -482,7 +483,8 @@ int score_anchors(vmfa_ctx* x) {
     const int tok = x->begin(kFamOther, dm.C);
     CU(launch_ws_images(dm, 0, x->WT, x->mu32, x->ipsi32, x->g, x->gcnt, x->bimg, x->bscl, s, x->sscl, x->brec,
                         x->limg));
-    CU(launch_ws_records(dm, 0, x->WT, x->mu32, x->ipsi32, x->kconst, x->g, x->gcnt, x->bscl, x->brec, s, 1));
+    CU(launch_ws_records(dm, 0, x->WT, x->mu32, x->ipsi32, x->kconst, x->g, x->gcnt, x->bscl, x->brec, s, 1,
+                         x->logpi, x->logdet));
     x->end(tok);
   }
   ScoreArgs a = score_args(x);
@@ -938,7 +940,7 @@ int dense_prepare(vmfa_ctx* x) {
     CU(launch_ws_images(dm, 0, x->WT, x->mu32, x->ipsi32, x->dense_g, x->dense_gcnt, x->bimg, x->bscl, s,
                         x->sscl, nullptr, x->ifree_only ? x->limg : nullptr));
     CU(launch_ws_records(dm, 0, x->WT, x->mu32, x->ipsi32, x->kconst, x->dense_g, x->dense_gcnt, x->bscl, x->brec,
-                         s));
+                         s, 0, x->logpi, x->logdet));
   }
   return VMFA_OK;
 }

@@ -374,7 +374,8 @@ cudaError_t launch_lse_dense(const float* LJ, int64_t R, int SL, int C, double* 
 int64_t ws_record_floats(const Dims& dm, int single);
 cudaError_t launch_ws_records(const Dims& dm, int single, const float* WT, const float* mu32, const float* ipsi32,
                               const double* kconst, const int* g, const int* gcnt, const float* scl, float* rec,
-                              cudaStream_t s, int fused = 0);
+                              cudaStream_t s, int fused = 0, const double* logpi = nullptr,
+                              const double* logdet = nullptr);
 // B stage images (single != 0: one component per job), sizes in halves / floats
 int64_t ws_image_halves(const Dims& dm, int single);
 int64_t ws_scale_floats(const Dims& dm, int single);

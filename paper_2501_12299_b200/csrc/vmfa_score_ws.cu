@@ -716,8 +716,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_ws(WsArgs a, const __grid
         float lj = static_cast<float>(kc - 0.5 * Q);
         // the test's scale (_helpers.lj_term_scale) is >= max(0.92 D, |kconst| - |log pi|, |Q| / 2)
         const float B = fabsf(d2q) + fabsf(linq) + fabsf(rc[2]) + 2.f * ey + yy;
-        const float M = fmaxf(fmaxf(0.9f * static_cast<float>(dm.D), fabsf(static_cast<float>(kc)) - 20.f),
-                              0.5f * fabsf(static_cast<float>(Q)));
+        // M: a lower bound of that term scale; rc[6] + |Q| / 2 is the scale itself
+        const float M = fmaxf(fmaxf(fmaxf(0.9f * static_cast<float>(dm.D), fabsf(static_cast<float>(kc)) - 20.f),
+                                    0.5f * fabsf(static_cast<float>(Q))),
+                              rc[6] + 0.5f * fabsf(static_cast<float>(Q)));
         const bool flag = B > kCancel * M;
         unsigned bits = __float_as_uint(lj);
         if (isfinite(lj)) bits = flag ? (bits | 1u) : (bits & ~1u);
@@ -799,7 +801,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_ws(WsArgs a, const __grid
 __global__ void __launch_bounds__(256) k_build_records(Dims dm, int Hp, int qg, int ngroups, int N1max, int single,
                                                        const float* WT, const float* mu32, const float* ipsi32,
                                                        const double* kconst, const int* g, const int* gcnt,
-                                                       const float* scl, float* rec, int fused) {
+                                                       const float* scl, float* rec, int fused,
+                                                       const double* logpi, const double* logdet) {
   const int lane = threadIdx.x & 31;
   const int R = rec_stride(Hp);
   const int nslot = single ? 1 : dm.G;
@@ -856,7 +859,12 @@ __global__ void __launch_bounds__(256) k_build_records(Dims dm, int Hp, int qg, 
       out[3] = sr[qi];
       out[4] = sr[N1max + qi];
       out[5] = isfinite(kc) ? static_cast<float>(kc - static_cast<double>(hi)) : 0.f;
-      out[6] = 0.f;
+      // [6] the magnitude of the log-joint's constant terms, |log pi| + (D
+      // log 2pi + |log|Sigma||) / 2: with |Q| / 2 it is the scale the
+      // parity tests measure log-joint errors against (flag criterion)
+      out[6] = (logpi && logdet && isfinite(logpi[q]))
+                   ? static_cast<float>(fabs(logpi[q]) + 0.5 * (dm.D * 1.8378770664093453 + fabs(logdet[q])))
+                   : 0.f;
       out[7] = 0.f;
     }
   }
@@ -1089,10 +1097,10 @@ cudaError_t launch_ws_images(const Dims& dm, int single, const float* WT, const 
 
 cudaError_t launch_ws_records(const Dims& dm, int single, const float* WT, const float* mu32, const float* ipsi32,
                               const double* kconst, const int* g, const int* gcnt, const float* scl, float* rec,
-                              cudaStream_t s, int fused) {
+                              cudaStream_t s, int fused, const double* logpi, const double* logdet) {
   k_build_records<<<sm_count() * 8, 256, 0, s>>>(dm, ws_hp(dm.H), ws_qg(dm, single), ws_groups(dm),
                                                  ws_n1max(dm, single), single, WT, mu32, ipsi32, kconst, g, gcnt,
-                                                 scl, rec, single ? 0 : fused);
+                                                 scl, rec, single ? 0 : fused, logpi, logdet);
   return cudaGetLastError();
 }
 
