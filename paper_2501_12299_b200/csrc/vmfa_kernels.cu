@@ -307,6 +307,15 @@ __global__ void __launch_bounds__(256) k_select(SelectArgs a) {
   // per warp: own log-joint of each anchor j (its self slot) and its rank, <= 8 anchors
   float* qual = reinterpret_cast<float*>(s_seen + W * (blockDim.x >> 5)) + (threadIdx.x >> 5) * 8;
   int* qrank = reinterpret_cast<int*>(s_seen + W * (blockDim.x >> 5)) + 64 + (threadIdx.x >> 5) * 8;
+  // per warp: hash of the row's scored components -> best (rank, slot)
+  constexpr int kHB = NS <= 1 ? 6 : NS <= 2 ? 7 : NS <= 4 ? 8 : 9;
+  constexpr unsigned kHS = 1u << kHB;
+  int* hkey = reinterpret_cast<int*>(s_seen + W * (blockDim.x >> 5)) + 128 + (threadIdx.x >> 5) * (2 * kHS);
+  unsigned* hval = reinterpret_cast<unsigned*>(hkey) + kHS;
+  if constexpr (NS > 2) {  // (the table exists only where it is used)
+    for (int i = lane; i < static_cast<int>(kHS); i += 32) hkey[i] = -1, hval[i] = 0u;
+    __syncwarp();
+  }
   const int64_t warp0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int CpG = dm.Cp * dm.G;
@@ -344,6 +353,7 @@ __global__ void __launch_bounds__(256) k_select(SelectArgs a) {
         __syncwarp();
       }
     }
+    __syncwarp();  // the last round's bitmap reads precede the clearing
 #pragma unroll
     for (int k = 0; k + 1 < NS; ++k)
       if (uniq[k]) atomicAnd(&seen[comp[k] >> 5], ~(1u << (comp[k] & 31)));
@@ -394,33 +404,70 @@ __global__ void __launch_bounds__(256) k_select(SelectArgs a) {
         qrank[lane] = r;
       }
       __syncwarp();
-      unsigned pk[NS];
-      int br[NS], bs[NS];
+      int bs[NS];
+      if constexpr (NS <= 2) {
+        // NS <= 2 (at most 64 slots): only duplicate slots can beat a first
+        // occurrence, so they alone are visited (warp-uniform loop over their
+        // ballot), ranks packed with the component in one 32-bit shuffle
+        unsigned pk[NS];
+        int br[NS];
 #pragma unroll
-      for (int k = 0; k < NS; ++k) {
-        const int s = k * 32 + lane;
-        int rk = pri[k] == INFINITY ? 15 : 0;
-        if (s < CpG && comp[k] >= 0 && pri[k] != INFINITY)
-          rk = qrank[__float2int_rz((static_cast<float>(s) + 0.5f) * invG)];
-        pk[k] = comp[k] >= 0 ? (static_cast<unsigned>(comp[k]) << 4) | static_cast<unsigned>(rk) : 0xffffffffu;
-        br[k] = rk;
-        bs[k] = s;
-      }
-#pragma unroll
-      for (int k2 = 0; k2 < NS; ++k2) {
-        unsigned dm2 = __ballot_sync(kFull, comp[k2] >= 0 && !uniq[k2]);
-        while (dm2) {
-          const int t = __ffs(dm2) - 1;
-          dm2 &= dm2 - 1;
-          const unsigned o = __shfl_sync(kFull, pk[k2], t);
-          const int orank = static_cast<int>(o & 15u);
-#pragma unroll
-          for (int k = 0; k < NS; ++k)
-            if (uniq[k] && static_cast<int>(o >> 4) == comp[k] && orank > br[k]) {
-              br[k] = orank;
-              bs[k] = k2 * 32 + t;
-            }
+        for (int k = 0; k < NS; ++k) {
+          const int s = k * 32 + lane;
+          int rk = pri[k] == INFINITY ? 15 : 0;
+          if (s < CpG && comp[k] >= 0 && pri[k] != INFINITY)
+            rk = qrank[__float2int_rz((static_cast<float>(s) + 0.5f) * invG)];
+          pk[k] = comp[k] >= 0 ? (static_cast<unsigned>(comp[k]) << 4) | static_cast<unsigned>(rk) : 0xffffffffu;
+          br[k] = rk;
+          bs[k] = s;
         }
+#pragma unroll
+        for (int k2 = 0; k2 < NS; ++k2) {
+          unsigned dm2 = __ballot_sync(kFull, comp[k2] >= 0 && !uniq[k2]);
+          while (dm2) {
+            const int t = __ffs(dm2) - 1;
+            dm2 &= dm2 - 1;
+            const unsigned o = __shfl_sync(kFull, pk[k2], t);
+            const int orank = static_cast<int>(o & 15u);
+#pragma unroll
+            for (int k = 0; k < NS; ++k)
+              if (uniq[k] && static_cast<int>(o >> 4) == comp[k] && orank > br[k]) {
+                br[k] = orank;
+                bs[k] = k2 * 32 + t;
+              }
+          }
+        }
+      } else {
+        // every scored slot posts (rank, slot) under its component in a small
+        // per-warp hash (linear probing, <= 50 % load): the maximum of
+        // rank << 8 | (255 - slot) is the best slot, the smallest one on a tie
+        int pos[NS];
+#pragma unroll
+        for (int k = 0; k < NS; ++k) {
+          const int s = k * 32 + lane;
+          bs[k] = s;
+          pos[k] = -1;
+          // (a duplicate extra slot is unscored and never wins)
+          if (comp[k] < 0 || (s >= CpG && !uniq[k])) continue;
+          int rk = pri[k] == INFINITY ? 15 : 0;
+          if (s < CpG && pri[k] != INFINITY) rk = qrank[__float2int_rz((static_cast<float>(s) + 0.5f) * invG)];
+          unsigned h = (static_cast<unsigned>(comp[k]) * 2654435761u) >> (32 - kHB);
+          for (;;) {
+            const int old = atomicCAS(&hkey[h], -1, comp[k]);
+            if (old == -1 || old == comp[k]) break;
+            h = (h + 1u) & (kHS - 1);
+          }
+          pos[k] = static_cast<int>(h);
+          atomicMax(&hval[h], (static_cast<unsigned>(rk) << 8) | static_cast<unsigned>(255 - s));
+        }
+        __syncwarp();
+#pragma unroll
+        for (int k = 0; k < NS; ++k)
+          if (uniq[k]) bs[k] = 255 - static_cast<int>(hval[pos[k]] & 255u);
+        __syncwarp();
+#pragma unroll
+        for (int k = 0; k < NS; ++k)
+          if (pos[k] >= 0) hkey[pos[k]] = -1, hval[pos[k]] = 0u;
       }
       float ljw[NS];
 #pragma unroll
@@ -3328,7 +3375,9 @@ cudaError_t launch_select(const SelectArgs& a, cudaStream_t s) {
   const int ns = (a.dm.SL + 31) / 32;
   const int grid = grid_for(a.dm.N * 32, 256, sm_count() * 16);
   // 8 warps' bitmaps + their anchor log-joints and ranks
-  const size_t smem = static_cast<size_t>((a.dm.C + 31) / 32) * 8 * sizeof(unsigned) + 64 * (sizeof(float) + sizeof(int));
+  const size_t hs = ns <= 2 ? 0 : ns <= 4 ? 256 : 512;  // k_select's per-warp hash (key + value), NS > 2 only
+  const size_t smem = static_cast<size_t>((a.dm.C + 31) / 32) * 8 * sizeof(unsigned) +
+                      64 * (sizeof(float) + sizeof(int)) + 8 * hs * 8;
   if (smem > 200 * 1024) return cudaErrorInvalidValue;
   auto go = [&](auto kern) {
     ensure_dyn_smem(reinterpret_cast<const void*>(kern), smem);

@@ -1,0 +1,8 @@
+# statistics kernel check: parity tests + config bench phase split
+mkdir -p gpurun_out/ab
+timeout 900 python -m pytest tests -m gpu -x -q -k "mstep or stats or suffstats" 2>&1 | tail -3
+for c in ${CONFIGS:-3}; do
+timeout 600 python bench.py --config $c --steps 5 --warmup 3 --no-cpu-baseline --no-e2e --no-exact-ll > gpurun_out/ab/c$c.json 2> gpurun_out/ab/c$c.err
+python -c "
+import json; d=json.load(open('gpurun_out/ab/c$c.json')); print('config $c ms', round(d['ms_per_step'],3), {k: round(v,3) for k,v in d['phase_ms'].items()})" 2>&1 | tail -1
+done
