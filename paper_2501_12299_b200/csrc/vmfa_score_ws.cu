@@ -992,11 +992,21 @@ __global__ void __launch_bounds__(256) k_build_images(Dims dm, int Hp, int qg, i
       float v[8];
       load8(ch * kKC + 8 * j, v);
       if (sums) {
+        const int d0 = ch * kKC + 8 * j;
+        float dq[8];
+        if (vec && d0 + 8 <= dm.D) {  // (two 16-byte loads per mean instead of 8 scalar ones)
+          const float4 q0 = *reinterpret_cast<const float4*>(mq + d0), q1 = *reinterpret_cast<const float4*>(mq + d0 + 4);
+          const float4 a0 = *reinterpret_cast<const float4*>(ma + d0), a1 = *reinterpret_cast<const float4*>(ma + d0 + 4);
+          dq[0] = q0.x - a0.x, dq[1] = q0.y - a0.y, dq[2] = q0.z - a0.z, dq[3] = q0.w - a0.w;
+          dq[4] = q1.x - a1.x, dq[5] = q1.y - a1.y, dq[6] = q1.z - a1.z, dq[7] = q1.w - a1.w;
+        } else {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) dq[i] = d0 + i < dm.D ? mq[d0 + i] - ma[d0 + i] : 0.f;
+        }
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-          const int d = ch * kKC + 8 * j + i;
-          if (d < dm.D) {
-            const double dl = static_cast<double>(mq[d] - ma[d]);
+          if (d0 + i < dm.D) {
+            const double dl = static_cast<double>(dq[i]);
             acc += kind == 2 ? static_cast<double>(v[i]) * dl : static_cast<double>(v[i]) * dl * dl;
           }
         }
