@@ -204,6 +204,14 @@ struct vmfa_ctx {
   unsigned long long* sit = nullptr;  // (seed, E-step index) read by k_extra
   bool capturing = false;
   bool graph_off = false;
+  // vmfa_iterate runs block 3 (g update) on a side stream next to the
+  // statistics / update / precompute: forked after the label partition,
+  // joined before the anchor images (the first reader of the new g)
+  cudaStream_t gstream = nullptr;
+  cudaEvent_t g_fork = nullptr, g_join = nullptr;
+  double* logpi_g = nullptr;  // log pi of the E-step's parameters (precompute rewrites logpi)
+  GupdArgs g_args{};
+  bool g_deferred = false, g_join_pending = false;
   struct HostState {
     int *g, *gcnt, *g_new, *gcnt_new;
     double *pi, *pi2, *mu, *mu2, *lam, *lam2, *psi, *psi2;
@@ -600,7 +608,7 @@ int cooc_count(vmfa_ctx* x, int64_t* n) {
 }
 
 // E-step blocks 1, 2, 4 and the local part of block 3.
-int estep_local(vmfa_ctx* x, uint64_t seed, uint64_t it, int mode, bool exchange) {
+int estep_local(vmfa_ctx* x, uint64_t seed, uint64_t it, int mode, bool exchange, bool defer_g = false) {
   const Dims& dm = x->dm;
   cudaStream_t s = x->stream;
   CU(cudaMemsetAsync(x->st_select, 0, sizeof(int), s));
@@ -658,7 +666,7 @@ int estep_local(vmfa_ctx* x, uint64_t seed, uint64_t it, int mode, bool exchange
   TRY(csr_by_key(x, reinterpret_cast<const unsigned*>(x->labels), dm.N, x->part_off, x->part_ent, nullptr, 1));
   CU(launch_items_scan(x->part_off, dm.C, x->gupd_pts, 1, x->part_items, s));
   // block 3 (local accumulation; selection unless exchanging)
-  CU(launch_logpi(x->pi, dm.C, x->logpi, s));
+  CU(launch_logpi(x->pi, dm.C, x->logpi_g, s));
   {
     GupdArgs a{};
     a.dm = dm;
@@ -669,7 +677,7 @@ int estep_local(vmfa_ctx* x, uint64_t seed, uint64_t it, int mode, bool exchange
     a.ret_idx = x->ret_idx;
     a.ret_lj = x->ret_lj;
     a.lablj = x->lablj;
-    a.logpi = x->logpi;
+    a.logpi = x->logpi_g;
     a.g_new = x->g_new;
     a.gcnt_new = x->gcnt_new;
     a.gt_cnt = x->gt_cnt;
@@ -705,9 +713,12 @@ int estep_local(vmfa_ctx* x, uint64_t seed, uint64_t it, int mode, bool exchange
       a.dump_n = x->dump_n;
       a.dump_cap = x->dump_cap;
     }
-    const int tok = x->begin(kFamGupdate, dm.N);
-    CU(launch_gupdate(a, x->gupd_grid, s));
-    if (!exchange && x->xc)
+    // (vmfa_iterate: launched by launch_deferred_gupdate on the side stream)
+    x->g_deferred = defer_g && !exchange && !x->sparse && !x->dump && !x->profile;
+    if (x->g_deferred) x->g_args = a;
+    const int tok = x->g_deferred ? -1 : x->begin(kFamGupdate, dm.N);
+    if (!x->g_deferred) CU(launch_gupdate(a, x->gupd_grid, s));
+    if (!x->g_deferred && !exchange && x->xc)
       CU(launch_gselect_dense(dm, x->xc, x->part_items, a.force_rows, x->g_new, x->gcnt_new, s));
     if (x->sparse) {
       // the rank-local list reduced by key (sent as it is in exchange mode);
@@ -717,7 +728,7 @@ int estep_local(vmfa_ctx* x, uint64_t seed, uint64_t it, int mode, bool exchange
       TRY(cooc_reduce(x, n));
       if (!exchange) CU(launch_cooc_select(cooc_args(x), 0, dm.C, 0, x->g_new, x->gcnt_new, s));
     }
-    x->end(tok);
+    if (!x->g_deferred) x->end(tok);
   }
   // scalars: F_estep = sum lse, joints = sum ret_cnt
   CU(launch_sum_f64(x->lse, dm.N, x->partials, x->scal + 0, s));
@@ -743,6 +754,30 @@ int estep_finish(vmfa_ctx* x, bool exchange, bool sync = true) {
   CU(cudaMemcpyAsync(&flag, x->st_select, sizeof(int), cudaMemcpyDeviceToHost, s));
   CU(cudaStreamSynchronize(s));
   if (flag) return fail(VMFA_ERR_INSUFFICIENT_CANDIDATES, "search space smaller than C'");
+  return VMFA_OK;
+}
+
+// Block 3 of a deferred E-step (estep_local with defer_g) on the side stream:
+// it depends on the selection and the label partition only, so it runs next
+// to the K inversion, the statistics, update_params and precompute;
+// join_gupdate orders it before the first
+// reader of the new g (the anchor images of the next scoring pass).
+int launch_deferred_gupdate(vmfa_ctx* x) {
+  if (!x->g_deferred) return VMFA_OK;
+  x->g_deferred = false;
+  const GupdArgs& a = x->g_args;
+  CU(cudaEventRecord(x->g_fork, x->stream));
+  CU(cudaStreamWaitEvent(x->gstream, x->g_fork, 0));
+  CU(launch_gupdate(a, x->gupd_grid, x->gstream));
+  if (x->xc) CU(launch_gselect_dense(x->dm, x->xc, x->part_items, a.force_rows, a.g_new, a.gcnt_new, x->gstream));
+  CU(cudaEventRecord(x->g_join, x->gstream));
+  x->g_join_pending = true;
+  return VMFA_OK;
+}
+int join_gupdate(vmfa_ctx* x) {
+  if (!x->g_join_pending) return VMFA_OK;
+  x->g_join_pending = false;
+  CU(cudaStreamWaitEvent(x->stream, x->g_join, 0));
   return VMFA_OK;
 }
 
@@ -1064,6 +1099,12 @@ int vmfa_ctx_create(vmfa_ctx** out, int device, int C, int D, int H, int Cp, int
     }
     x->own_stream = true;
   }
+  if (cudaStreamCreateWithFlags(&x->gstream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&x->g_fork, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&x->g_join, cudaEventDisableTiming) != cudaSuccess) {
+    vmfa_ctx_destroy(x);
+    return fail(VMFA_ERR_CUDA, "side stream creation failed");
+  }
   const size_t N = static_cast<size_t>(n_local), Cs = static_cast<size_t>(C);
   const size_t H1 = static_cast<size_t>(H) + 1;
   int r = VMFA_OK;
@@ -1089,6 +1130,7 @@ int vmfa_ctx_create(vmfa_ctx** out, int device, int C, int D, int H, int Cp, int
   A(x->Sz, Cs * H * H);
   A(x->logdet, Cs);
   A(x->logpi, Cs);
+  A(x->logpi_g, Cs);
   A(x->kconst, Cs);
   A(x->P, Cs * D * x->L.HP);
   A(x->V32, Cs * D * H);
@@ -1256,6 +1298,12 @@ int vmfa_ctx_destroy(vmfa_ctx* x) {
     cudaEventDestroy(x->x_ready);
     cudaEventDestroy(x->x_free);
   }
+  if (x->gstream) {
+    cudaStreamSynchronize(x->gstream);
+    cudaStreamDestroy(x->gstream);
+  }
+  if (x->g_fork) cudaEventDestroy(x->g_fork);
+  if (x->g_join) cudaEventDestroy(x->g_join);
   for (void* p : x->allocs) cudaFree(p);
   if (x->hstat) cudaFreeHost(x->hstat);
   for (auto& e : x->pending) {
@@ -1820,12 +1868,18 @@ bool graphs_enabled(const vmfa_ctx* x) {
 // of selection, update and precompute land in the pinned readback.
 int iterate_enqueue(vmfa_ctx* x, uint64_t seed, uint64_t iteration, int mode, int* failed) {
   cudaStream_t s = x->stream;
-  TRY(estep_local(x, seed, iteration, mode, false));
+  static const bool side = [] {  // VMFA_GSTREAM=0: block 3 in line on the main stream
+    const char* v = std::getenv("VMFA_GSTREAM");
+    return !(v && v[0] == '0');
+  }();
+  TRY(estep_local(x, seed, iteration, mode, false, side));
   TRY(estep_finish(x, false, false));
+  TRY(launch_deferred_gupdate(x));
   TRY(stats_local(x));
   TRY(launch_update_params(x));
   swap_params(x);
   TRY(run_precompute(x, failed, false));
+  TRY(join_gupdate(x));
   TRY(free_energy_local(x, x->lookahead));
   CU(launch_count_empty(x->pi, x->dm.C, x->n_empty, s));
   IterStatus* h = x->hstat;
