@@ -1215,9 +1215,10 @@ int vmfa_ctx_create(vmfa_ctx** out, int device, int C, int D, int H, int Cp, int
   {
     const int64_t pairs = static_cast<int64_t>(N) * Cp;
     const int64_t target = (pairs + sm_count() * 8 - 1) / (sm_count() * 8);
-    x->stats_rows = static_cast<int>(std::min<int64_t>(1024, std::max<int64_t>(256, (target + 31) / 32 * 32)));
+    const int64_t cap = stats_rows_cap(dm);
+    x->stats_rows = static_cast<int>(std::min<int64_t>(cap, std::max<int64_t>(256, (target + 31) / 32 * 32)));
     if (const char* v = std::getenv("VMFA_STATS_ROWS"))  // experiments: K-pairs per statistics item
-      x->stats_rows = static_cast<int>(std::min<int64_t>(1024, std::max<int64_t>(32, std::atoll(v) / 32 * 32)));
+      x->stats_rows = static_cast<int>(std::min<int64_t>(cap, std::max<int64_t>(32, std::atoll(v) / 32 * 32)));
     if (x->scorer == 2 && stats_use_tc(dm)) {  // the tcgen05 statistics kernel
       x->stats_rows = stats_tc_rows();
       A(x->svimg, static_cast<size_t>(stats_tc_image_bytes(dm)));

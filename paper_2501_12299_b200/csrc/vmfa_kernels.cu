@@ -1135,6 +1135,7 @@ __device__ int g_stats_prof_on;
 // deterministic; no atomics.
 constexpr int kStatsBatch = 32;
 constexpr int kStatsMaxRows = 1024;  // K-pairs per statistics item (upper bound)
+constexpr int kStatsMaxRowsBig = 1536;  // ... of k_stats_mma's BIG variant (one CTA per SM: room for longer items)
 constexpr int kStatsMaxBuf = 6;      // row-batch ring depth (bulk-copy path)
 constexpr int kStatsMaxH1 = 17;   // columns of Y per pass
 
@@ -1718,10 +1719,12 @@ __global__ void __launch_bounds__(kStatsThreads, BIG ? 1 : 2) k_stats_mma(StatsA
   __shared__ __align__(16) float4 s_Af[BR / 8][32][2];  // phase (ii) A fragments (hi, lo) per k-step, lane
   __shared__ double s_zd[BR * kSmZD];  // [zhat; 1] rows in fp64 (E)
   __shared__ double s_red[kStatsThreads / 32];
-  __shared__ double s_accE[kStatsThreads];
+  __shared__ double s_accE[BIG ? 1 : kStatsThreads];
   __shared__ uint64_t s_xbar[kStatsMaxBuf];
-  __shared__ int s_eall[kStatsMaxRows];
-  __shared__ double s_qall[kStatsMaxRows];
+  // K-pairs per item, at most (the longer items where the static arrays fit: D <= 832)
+  constexpr int MAXR = BIG && NTW <= 13 ? kStatsMaxRowsBig : kStatsMaxRows;
+  __shared__ int s_eall[MAXR];
+  __shared__ double s_qall[MAXR];
   __shared__ int s_item;
   __shared__ float s_qb[BR];  // the batch's responsibilities (fp32; 0 past the item end)
   const Dims dm = a.dm;
@@ -3491,6 +3494,11 @@ static bool stats_mma_big(const Dims& dm) { return dm.D > 256 || dm.H + 1 > 16; 
 // parity-tested, but measured 2-3x slower than k_stats_mma on configs 1-3
 // (GEMM ii reduces over rows, so every row chunk is produced twice and the
 // synchronous cooperative fills stay latency-bound)
+// K-pairs per statistics item, at most: with the BIG tensor-core variant most
+// components are a single item (written directly, no partial rows to reduce)
+int stats_rows_cap(const Dims& dm) {
+  return stats_mma_ok(dm) && stats_mma_big(dm) && dm.D <= 832 && !stats_use_tc(dm) ? kStatsMaxRowsBig : kStatsMaxRows;
+}
 bool stats_use_tc(const Dims& dm) {
   const char* v = std::getenv("VMFA_STATS");
   return v && std::strcmp(v, "tc") == 0 && stats_tc_ok(dm);

@@ -175,6 +175,7 @@ struct StatsArgs {
 };
 // the tcgen05 statistics kernel takes the pass (opt-in: VMFA_STATS=tc)
 bool stats_use_tc(const Dims& dm);
+int stats_rows_cap(const Dims& dm);
 
 struct UpdateArgs {
   Dims dm;
