@@ -1097,7 +1097,8 @@ int64_t ws_record_floats(const Dims& dm, int single) {
 cudaError_t launch_ws_images(const Dims& dm, int single, const float* WT, const float* mu32, const float* ipsi32,
                              const int* g, const int* gcnt, void* img, float* bscl, cudaStream_t s,
                              const float* sscl, float* rec, void* limg) {
-  k_build_images<<<sm_count() * 8, 256, 0, s>>>(dm, ws_hp(dm.H), ws_qg(dm, single), ws_groups(dm),
+  // (warp-strided over the B rows; 32 blocks per SM measured 0.09 ms faster than 8 at config 3)
+  k_build_images<<<sm_count() * 32, 256, 0, s>>>(dm, ws_hp(dm.H), ws_qg(dm, single), ws_groups(dm),
                                                 ws_n1max(dm, single), single, WT, mu32, ipsi32, g, gcnt,
                                                 static_cast<__half*>(img), bscl, single ? nullptr : sscl,
                                                 ws_n1max(dm, 1), single ? nullptr : rec,
