@@ -2802,6 +2802,7 @@ __global__ void __launch_bounds__(kPreWarps * 32) k_precompute_w(PrecompArgs a) 
     const double* psi = a.psi + (int64_t)c * D;
     double acc[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};  // tiles (0,0), (0,1), (1,1)
     double lsum = 0.0;  // sum log psi over this lane's dimensions
+#pragma unroll 4
     for (int d0 = 0; d0 < D; d0 += 4) {
       const int d = d0 + t;
       const bool dv = d < D;
