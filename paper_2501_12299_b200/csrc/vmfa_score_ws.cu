@@ -675,11 +675,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_ws(WsArgs a, const __grid
       const int N1 = kNL + ((nq * HP + 15) / 16) * 16;
       const uint32_t trow = tmem + b * a.TB + (static_cast<uint32_t>(quad * 32) << 16);
       float lin[16], d2[16];
-      tmem_ld_nowait<16>(trow, lin);
-      tmem_ld_nowait<16>(trow + N1, d2);
-      tmem_wait_ld();
-      pin_regs<16>(lin);
-      pin_regs<16>(d2);
+      if constexpr (HP > 16) {  // (HP <= 16: loaded after the W columns, see below)
+        tmem_ld_nowait<16>(trow, lin);
+        tmem_ld_nowait<16>(trow + N1, d2);
+        tmem_wait_ld();
+        pin_regs<16>(lin);
+        pin_regs<16>(d2);
+      }
       int64_t obase = 0;
       if (e >= 0) {
         if (a.mode == kModeAnchor) {
@@ -735,7 +737,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_ws(WsArgs a, const __grid
         }
       };
       if constexpr (HP <= 16) {
-        for (int q0 = 0; q0 < nq; q0 += kEpiBatch) {
+        // The accumulator is held only while its columns are read: |y|^2 and
+        // the error sum of every component first (two registers each), then
+        // the lin / psi columns; the buffer is released before the fp64
+        // assembly, flags and stores (with one accumulator buffer -- 192
+        // columns at config 3 -- the next job's MMAs wait for this release)
+        constexpr int QMAX = qg_max(HP);
+        float yyv[QMAX], eyv[QMAX];
+#pragma unroll
+        for (int q0 = 0; q0 < QMAX; q0 += kEpiBatch) {
+          if (q0 >= nq) break;
           const int nb = min(kEpiBatch, nq - q0);
           float y[kEpiBatch][HP];
 #pragma unroll
@@ -745,19 +756,37 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_ws(WsArgs a, const __grid
           pin_regs<kEpiBatch * HP>(&y[0][0]);
 #pragma unroll
           for (int qi = 0; qi < kEpiBatch; ++qi) {
-            if (qi >= nb) break;
-            const float* rc = srec + (q0 + qi) * R;
+            if (q0 + qi >= QMAX) break;
             float yy = 0.f, ey = 0.f;
+            if (qi < nb) {
+              const float* rc = srec + (q0 + qi) * R;
 #pragma unroll
-            for (int h = 0; h < HP; ++h) {
-              const float ys = y[qi][h] * (invA * rc[8 + HP + h]);
-              const float t = ys - rc[8 + h];
-              yy = fmaf(t, t, yy);
-              ey = fmaf(fabsf(t), fabsf(ys) + fabsf(rc[8 + h]), ey);
+              for (int h = 0; h < HP; ++h) {
+                const float ys = y[qi][h] * (invA * rc[8 + HP + h]);
+                const float t = ys - rc[8 + h];
+                yy = fmaf(t, t, yy);
+                ey = fmaf(fabsf(t), fabsf(ys) + fabsf(rc[8 + h]), ey);
+              }
             }
-            finish(q0 + qi, yy, ey);
+            yyv[q0 + qi] = yy;
+            eyv[q0 + qi] = ey;
           }
         }
+        tmem_ld_nowait<16>(trow, lin);
+        tmem_ld_nowait<16>(trow + N1, d2);
+        tmem_wait_ld();
+        pin_regs<16>(lin);
+        pin_regs<16>(d2);
+        fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&s_tempty[b]);
+        if (PROF) pf.lap(kEWork);
+#pragma unroll
+        for (int qi = 0; qi < QMAX; ++qi) {
+          if (qi >= nq) break;
+          finish(qi, yyv[qi], eyv[qi]);
+        }
+        continue;
       } else {  // wide factors: 16 columns at a time
         for (int qi = 0; qi < nq; ++qi) {
           const float* rc = srec + qi * R;

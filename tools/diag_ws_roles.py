@@ -49,6 +49,11 @@ lib().vmfa_diag_scorer_cycles(1 | (DBG << 1), big.ctypes.data_as(C.c_void_p), bi
 kt2 = s.kernel_times()
 print("WS_DBG", DBG, {k: round(v["ms"], 3) for k, v in kt2.items() if v["ms"] > 0})
 lib().vmfa_diag_scorer_cycles(0, None, 0)
+print("role counters of this E-step (anchor + extra launches):")
+tp2 = float(big[0:4].sum() + big[9:11].sum())
+for i, nme in enumerate(names):
+    den = tp2 if (i < 4 or i >= 9) else float(big[4:7].sum() if i < 7 else big[7:9].sum())
+    print(f"  {nme:14s} {int(big[i]):>16d}  share-in-role {big[i] / den:6.3f}")
 tr = big[16:].reshape(-1, 8).astype(np.int64)
 n = int((tr[:, 3] > 0).sum())
 t0 = tr[0, 0] if tr[0, 0] > 0 else tr[0, 1]
