@@ -675,7 +675,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_ws(WsArgs a, const __grid
       const int N1 = kNL + ((nq * HP + 15) / 16) * 16;
       const uint32_t trow = tmem + b * a.TB + (static_cast<uint32_t>(quad * 32) << 16);
       float lin[16], d2[16];
-      if constexpr (HP > 16) {  // (HP <= 16: loaded after the W columns, see below)
+      if constexpr (HP != 16) {  // (HP == 16: loaded after the W columns, see below)
         tmem_ld_nowait<16>(trow, lin);
         tmem_ld_nowait<16>(trow + N1, d2);
         tmem_wait_ld();
@@ -736,7 +736,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_ws(WsArgs a, const __grid
           }
         }
       };
-      if constexpr (HP <= 16) {
+      if constexpr (HP == 16) {
         // The accumulator is held only while its columns are read: |y|^2 and
         // the error sum of every component first (two registers each), then
         // the lin / psi columns; the buffer is released before the fp64
@@ -787,6 +787,30 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_ws(WsArgs a, const __grid
           finish(qi, yyv[qi], eyv[qi]);
         }
         continue;
+      } else if constexpr (HP < 16) {  // two accumulator buffers fit: the epilogue overlaps the next job as it is
+        for (int q0 = 0; q0 < nq; q0 += kEpiBatch) {
+          const int nb = min(kEpiBatch, nq - q0);
+          float y[kEpiBatch][HP];
+#pragma unroll
+          for (int qi = 0; qi < kEpiBatch; ++qi)
+            if (qi < nb) tmem_ld_nowait<HP>(trow + kNL + (q0 + qi) * HP, y[qi]);
+          tmem_wait_ld();
+          pin_regs<kEpiBatch * HP>(&y[0][0]);
+#pragma unroll
+          for (int qi = 0; qi < kEpiBatch; ++qi) {
+            if (qi >= nb) break;
+            const float* rc = srec + (q0 + qi) * R;
+            float yy = 0.f, ey = 0.f;
+#pragma unroll
+            for (int h = 0; h < HP; ++h) {
+              const float ys = y[qi][h] * (invA * rc[8 + HP + h]);
+              const float t = ys - rc[8 + h];
+              yy = fmaf(t, t, yy);
+              ey = fmaf(fabsf(t), fabsf(ys) + fabsf(rc[8 + h]), ey);
+            }
+            finish(q0 + qi, yy, ey);
+          }
+        }
       } else {  // wide factors: 16 columns at a time
         for (int qi = 0; qi < nq; ++qi) {
           const float* rc = srec + qi * R;
