@@ -410,9 +410,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_ws(WsArgs a, const __grid
     // issue unit `unit` (slot p = chunks [p*CPS, (p+1)*CPS) of row n) of this
     // quadrant (slice-0 warps only): one bulk copy per row covers CPS chunks
     // (the SM accepts a bulk copy only every ~26 cycles, tools/micro/bulk_issue.cu)
-    auto issue_x = [&](int n, int p, uint32_t unit) {
-      const int sl = static_cast<int>(unit % XS);
-      const uint32_t use = unit / XS;
+    // (slot index and use count are carried incrementally: the runtime
+    // divisions by XS / CPS per chunk were ~10 % of the kernel's stall samples)
+    auto issue_x = [&](int n, int p, int sl, uint32_t use) {
       if (use >= 1) mbar_wait(&s_xempty[sl][quad], (use - 1) & 1u);
       const int d0 = p * CPS * kKC;
       const bool valid = n >= 0 && d0 < dm.D && !(PROF && (a.dbg & 1));
@@ -447,7 +447,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_ws(WsArgs a, const __grid
     uint32_t su = 0;  // flat X-ring slot counter
     int xs = 0;
     if (w.valid(total) && ah == 0)
-      for (int k = 0; k < ahead; ++k) issue_x(n_cur, k, static_cast<uint32_t>(k));
+      for (int k = 0; k < ahead; ++k) issue_x(n_cur, k, k, 0u);
+    uint32_t sdiv = 0;  // su / XS (xs = su % XS)
     int jb = 0;
     while (w.valid(total)) {
       const int mslot = jb & 1;
@@ -455,15 +456,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_ws(WsArgs a, const __grid
       mbar_wait(&s_mufull[mslot], (jb >> 1) & 1);
       const float* mu_s = s_mu[mslot] + s_muoff[mslot];
       for (int ch = 0; ch < nchunk; ++ch, ++sc) {
-        const int within = ch % CPS;
+        const int within = CPS == 1 ? 0 : (ch & (CPS - 1));  // CPS is 1 or 2
         if (within == 0) {
           if (ah == 0) {  // prefetch slot su + ahead (this job or the next)
-            const int p2 = ch / CPS + ahead;
-            if (p2 < nslot) issue_x(n_cur, p2, su + ahead);
-            else issue_x(wn.valid(total) ? n_nxt : -1, p2 - nslot, su + ahead);
+            const int p2 = (CPS == 1 ? ch : ch >> 1) + ahead;
+            int sl = xs + ahead;
+            uint32_t use = sdiv;
+            if (sl >= XS) sl -= XS, use += 1u;
+            if (p2 < nslot) issue_x(n_cur, p2, sl, use);
+            else issue_x(wn.valid(total) ? n_nxt : -1, p2 - nslot, sl, use);
           }
-          xs = static_cast<int>(su % XS);
-          mbar_wait(&s_xfull[xs][quad], (su / XS) & 1u);
+          mbar_wait(&s_xfull[xs][quad], sdiv & 1u);
         }
         if (PROF) pf.lap(kPBuild);  // (waiting for the row pieces)
         const int s = static_cast<int>(sc & 1u);
@@ -496,6 +499,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_ws(WsArgs a, const __grid
           __syncwarp();
           if (lane == 0) mbar_arrive(&s_xempty[xs][quad]);
           ++su;
+          if (++xs == XS) xs = 0, ++sdiv;
         }
         if (PROF) pf.lap(kPSplit);
         if (use >= 1) mbar_wait(&s_aempty[s], (use - 1) & 1u);
