@@ -595,6 +595,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_ws(WsArgs a, const __grid
   } else if (warp == kMmaWarp) {
     // ============================================================ MMA issuer
     uint32_t sc = 0, bc = 0;
+    int sb = 0;        // bc % NB and the parity of bc / NB, carried incrementally
+    uint32_t bph = 0;
     int jb = 0;
     Prof pf{};
     if (PROF) pf.start();
@@ -607,12 +609,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_ws(WsArgs a, const __grid
       if (use_b >= 1) mbar_wait(&s_tempty[b], (use_b - 1) & 1);
       fence_after();
       if (PROF) pf.lap(kMWaitTE);
-      for (int ch = 0; ch < nchunk; ++ch, ++sc, ++bc) {
+      for (int ch = 0; ch < nchunk; ++ch, ++sc, ++bc, sb = sb + 1 == NB ? (bph ^= 1u, 0) : sb + 1) {
         const int s = static_cast<int>(sc & 1u);
-        const int sb = static_cast<int>(bc % NB);
         mbar_wait(&s_afull[s], (sc >> 1) & 1u);
         if (lane == 0) trace(tp, static_cast<int>(sc), 4);
-        mbar_wait(&s_bfull[sb], (bc / NB) & 1u);
+        mbar_wait(&s_bfull[sb], bph);
         fence_after();
         if (PROF) pf.lap(kMWaitFull);
         if (lane == 0) trace(tp, static_cast<int>(sc), 2);
