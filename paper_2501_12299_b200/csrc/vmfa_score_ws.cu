@@ -543,7 +543,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_ws(WsArgs a, const __grid
   } else if (warp == kLoadWarp) {
     // ============================================================ loader
     if (lane == 0) {
-      uint32_t bc = 0;
+      uint32_t bc = 0, luse = 0;
+      int ls = 0;
       int jb = 0;
       for (Walk w = walk_begin(a.jobs, total); w.valid(total); w.advance(a.jobs, a.qg, total), ++jb) {
         const int c = w.J.x;
@@ -563,9 +564,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_ws(WsArgs a, const __grid
         const int nq = min(a.qg, w.J.w - w.g0);
         const uint32_t wb = HP * 128;                 // one plane of a component's W rows
         const uint32_t s1 = 2 * 128 * (a.N1max1 + kNL);  // one-component stage bytes
-        for (int ch = 0; ch < nchunk; ++ch, ++bc) {
-          const int s = static_cast<int>(bc % NB);
-          const uint32_t use = bc / NB;
+        for (int ch = 0; ch < nchunk; ++ch, ++bc, ls = ls + 1 == NB ? (++luse, 0) : ls + 1) {
+          const int s = ls;  // bc % NB, and luse = bc / NB, carried incrementally
+          const uint32_t use = luse;
           if (use >= 1) mbar_wait(&s_bempty[s], (use - 1) & 1u);
           trace(tp, static_cast<int>(bc), 5);
           const uint32_t dst = sbase + s * a.stage_bytes;
