@@ -948,11 +948,23 @@ __global__ void __launch_bounds__(256) k_build_images(Dims dm, int Hp, int qg, i
   const int64_t stage_h = 2 * 64 * (int64_t)nrow;  // halves per stage
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const bool vec = (dm.D & 3) == 0;
+  const bool small = (int64_t)dm.C * ng * nrow < (int64_t{1} << 31);
   for (int64_t wi = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; wi < (int64_t)dm.C * ng * nrow;
        wi += nw) {
-    const int row = static_cast<int>(wi % nrow);
-    const int grp = static_cast<int>((wi / nrow) % ng);
-    const int a = static_cast<int>(wi / ((int64_t)nrow * ng));
+    // (row, group, anchor) of this warp's B row: 32-bit divisions when the row
+    // count allows (three 64-bit divisions per row were a third of the kernel's
+    // instructions)
+    int row, grp, a;
+    if (small) {
+      const unsigned w32 = static_cast<unsigned>(wi), ag = w32 / static_cast<unsigned>(nrow);
+      row = static_cast<int>(w32 - ag * static_cast<unsigned>(nrow));
+      a = static_cast<int>(ag / static_cast<unsigned>(ng));
+      grp = static_cast<int>(ag - static_cast<unsigned>(a) * static_cast<unsigned>(ng));
+    } else {
+      row = static_cast<int>(wi % nrow);
+      grp = static_cast<int>((wi / nrow) % ng);
+      a = static_cast<int>(wi / ((int64_t)nrow * ng));
+    }
     const int slot0 = grp * qg;
     const int nq = single ? 1 : min(qg, gcnt[a] - slot0);
     // source of this row: kind 0 zero, 1 lin (q), 2 W (q, h), 3 psi (q)
