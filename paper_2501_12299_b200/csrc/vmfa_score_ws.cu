@@ -34,6 +34,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstdlib>
+#include <type_traits>
 
 #include <cuda.h>  // CUtensorMap (the encoder is fetched through cudaGetDriverEntryPoint)
 #include <cuda_fp16.h>
@@ -474,27 +475,34 @@ __global__ void __launch_bounds__(kThreads, 1) k_score_ws(WsArgs a, const __grid
         const int d0 = ch * kKC + kElem * ah;
         const uint32_t xrow = xbase + xs * SLOT + ar * (XR * 4) + (within * kKC + kElem * ah) * 4;
         uint32_t vh[kElem / 2], vl[kElem / 2], qh[kElem / 2], ql[kElem / 2];
+        // (a live row's slice inside D -- nearly every call -- skips the per-element bounds selects)
+        auto build = [&](auto fullc) {
+          constexpr bool kFullSlice = decltype(fullc)::value;
 #pragma unroll
-        for (int jj = 0; jj < kXSeg; ++jj) {
-          const int d = d0 + 4 * jj;
-          float xv[4];
-          asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-                       : "=f"(xv[0]), "=f"(xv[1]), "=f"(xv[2]), "=f"(xv[3])
-                       : "r"(xrow + jj * 16)
-                       : "memory");
-          const float4 m4 = *reinterpret_cast<const float4*>(mu_s + d);  // (D % 4 == 0: aligned window)
-          const float mv[4] = {m4.x, m4.y, m4.z, m4.w};
-          float v[4], q[4];
+          for (int jj = 0; jj < kXSeg; ++jj) {
+            const int d = d0 + 4 * jj;
+            float xv[4];
+            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                         : "=f"(xv[0]), "=f"(xv[1]), "=f"(xv[2]), "=f"(xv[3])
+                         : "r"(xrow + jj * 16)
+                         : "memory");
+            const float4 m4 = *reinterpret_cast<const float4*>(mu_s + d);  // (D % 4 == 0: aligned window)
+            const float mv[4] = {m4.x, m4.y, m4.z, m4.w};
+            float v[4], q[4];
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            v[k] = (d + k < dm.D && n_cur >= 0) ? (xv[k] - mv[k]) * sA : 0.f;
-            q[k] = (v[k] * v[k]) * exp2i(-kTargetExp);
+            for (int k = 0; k < 4; ++k) {
+              if constexpr (kFullSlice) v[k] = (xv[k] - mv[k]) * sA;
+              else v[k] = (d + k < dm.D && n_cur >= 0) ? (xv[k] - mv[k]) * sA : 0.f;
+              q[k] = (v[k] * v[k]) * exp2i(-kTargetExp);
+            }
+            split2(v[0], v[1], vh[2 * jj], vl[2 * jj]);
+            split2(v[2], v[3], vh[2 * jj + 1], vl[2 * jj + 1]);
+            split2(q[0], q[1], qh[2 * jj], ql[2 * jj]);
+            split2(q[2], q[3], qh[2 * jj + 1], ql[2 * jj + 1]);
           }
-          split2(v[0], v[1], vh[2 * jj], vl[2 * jj]);
-          split2(v[2], v[3], vh[2 * jj + 1], vl[2 * jj + 1]);
-          split2(q[0], q[1], qh[2 * jj], ql[2 * jj]);
-          split2(q[2], q[3], qh[2 * jj + 1], ql[2 * jj + 1]);
-        }
+        };
+        if (n_cur >= 0 && d0 + kElem <= dm.D) build(std::true_type{});
+        else build(std::false_type{});
         if (within == CPS - 1 || ch == nchunk - 1) {  // this warp is done with the row slot
           __syncwarp();
           if (lane == 0) mbar_arrive(&s_xempty[xs][quad]);
